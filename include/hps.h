@@ -1,0 +1,129 @@
+/* hps.h — C-ABI of libhps.so: the B200-native HPS direct solver with
+ * impedance-to-impedance (ItI) operators for the variable-coefficient
+ * Helmholtz impedance problem (arXiv:1812.07167).
+ *
+ *   -Laplace(u) - kappa^2 c(x) u = s(x)  in the rectangle Omega
+ *   du/dnu + i eta u             = t(x)  on its boundary            (eq. 1)
+ *
+ * hps_build is the precomputation stage (Algorithm 1): the
+ * batched leaf build and the level-by-level merge tree
+ * (PAPER.md:472-625).  hps_solve is the solve stage (Algorithm 2,
+ * PAPER.md:670-710): upward body-load sweep, downward impedance sweep.
+ * Every step runs in this library's own sm_100a CUDA kernels (no cuBLAS /
+ * cuSOLVER), in complex128.
+ *
+ * Conventions:
+ *  - Leaf discretisation: p x p Chebyshev-Lobatto tensor grid, corners dropped
+ *    (PAPER.md:300-325).  q = p - 2 boundary nodes per leaf edge.
+ *  - Node (ix, iy) of a leaf's tensor grid has index iy*p + ix (x fastest),
+ *    x_k = x0 + (1 - cos(k pi/(p-1))) h/2.
+ *  - Boundary order of every box: [S, E, N, W], each edge by increasing
+ *    coordinate (PAPER.md:321 fixes [s, e, n, w]; within-edge order is ours).
+ *  - Leaf natural order: leaf (ix, iy) has index iy*nx + ix.
+ *  - Complex numbers are interleaved (re, im) doubles (== cuDoubleComplex ==
+ *    std::complex<double> == numpy complex128).
+ *  - Matrices returned by the export calls are row-major.
+ *
+ * Ownership: the handle owns all device memory for the stored operators.
+ * Input pointers are borrowed for the duration of the call; they may be host
+ * or device (CUDA-visible) memory — the library asks the driver which.
+ * Output buffers are caller-allocated, host or device.
+ *
+ * Errors: every int-returning call returns 0 or a negative HPS_E* code; the
+ * message of the last failure on the calling thread is hps_last_error().  No
+ * C++ exception crosses the ABI.  On a build error *out is set to NULL; on a
+ * solve error the contents of u are unspecified and the handle stays valid.
+ * Calls on one handle must not overlap (one call at a time per handle).
+ */
+#ifndef HPS_H_
+#define HPS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_OK 0
+#define HPS_EINVAL (-1)    /* invalid argument (message says which) */
+#define HPS_ESINGULAR (-2) /* zero pivot while inverting B (leaf) or W (merge); message names the level */
+#define HPS_ENOMEM (-3)    /* device allocation failed */
+#define HPS_ECUDA (-4)     /* CUDA runtime / launch error */
+#define HPS_ENOTKEPT (-5)  /* export of an operator the handle did not keep */
+
+typedef struct {
+  double x0, x1, y0, y1; /* the rectangle Omega, x1 > x0, y1 > y0 */
+  int32_t nx, ny;        /* leaves per side, powers of two (1 allowed) */
+} hps_grid;
+
+typedef struct {
+  double re, im;
+} hps_c128;
+
+typedef struct hps_handle hps_handle;
+
+typedef struct {
+  int32_t keep_root_R;  /* 1: form the root ItI operator R^1 (Algorithm 1, tau = 1).  Algorithm 2
+                           never uses it; 0 skips the two root GEMMs (default 1). */
+  int32_t keep_all_R;   /* 1: keep every box's R for hps_export_R (debug / parity; default 0) */
+  int32_t device;       /* CUDA device ordinal (default: current device) */
+  int32_t leaf_chunk;   /* leaves factored per batch (0 = automatic) */
+} hps_opts;
+
+/* Precomputation stage (Algorithm 1).
+ *  g         : domain and leaf grid (nx, ny powers of two; leaves must be congruent rectangles).
+ *  p         : Chebyshev points per leaf side, p >= 4.
+ *  q         : boundary nodes per leaf edge; must equal p - 2 (corner-free scheme).
+ *  kappa     : wavenumber, kappa >= 0 (PAPER.md:227 has kappa > 0; 0 is allowed).
+ *  eta       : impedance parameter, Re(eta) != 0.
+ *  c_samples : c(x) at every leaf's p*p tensor nodes, [nx*ny leaves, natural order][p*p]; corner
+ *              values are ignored.  Host or device memory; complex (the PDE allows complex c).
+ *  opt       : NULL for defaults.
+ *  out       : receives the handle (NULL on error). */
+int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_c128* c_samples,
+              const hps_opts* opt, hps_handle** out);
+
+/* Solve stage (Algorithm 2) for nrhs right-hand sides.
+ *  s : body load at interior nodes, [nrhs][nx*ny leaves][q*q] (x fastest); NULL means s = 0 and
+ *      the upward pass is skipped.
+ *  t : incoming impedance data on the root boundary, [nrhs][2(nx+ny)q] in [S,E,N,W] order.
+ *  u : output, [nrhs][nx*ny leaves][p*p-4]; each leaf in [I_b (S,E,N,W); I_i] order
+ *      (PAPER.md:321-325).  Nodes on a shared edge appear once per leaf.
+ *  Host or device pointers. */
+int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps_c128* u);
+
+/* ItI operator of a box (heap numbering: root 1, children 2*tau (alpha: west / south) and
+ * 2*tau + 1 (beta: east / north)).  out: n_b(box)^2, row-major, canonical
+ * order.  The root is available when keep_root_R = 1; other boxes need keep_all_R = 1. */
+int hps_export_R(const hps_handle* h, int64_t box, hps_c128* out);
+
+/* Leaf operators Psi ((p^2-4) x (4p-8)) and Y ((p^2-4) x (p-2)^2), row-major, of the leaf with
+ * natural index `leaf`.  Either output may be NULL. */
+int hps_export_leaf(const hps_handle* h, int64_t leaf, hps_c128* psi, hps_c128* y);
+
+/* Sizes: n_b of a box (heap id), number of boxes, leaf depth. Returns -1 on a bad id. */
+int64_t hps_box_nb(const hps_handle* h, int64_t box);
+int64_t hps_num_boxes(const hps_handle* h);
+
+/* Tensor-node coordinates of every leaf, [nx*ny][p*p] (x fastest), and the root boundary
+ * nodes with their outward unit normals, [2(nx+ny)(p-2)] in [S,E,N,W] order.  Host pointers.
+ * Pure geometry (no device work); lets callers sample c, s, t. */
+int hps_leaf_nodes(const hps_grid* g, int p, double* x, double* y);
+int hps_root_boundary_nodes(const hps_grid* g, int p, double* x, double* y, double* nx, double* ny);
+
+/* Device time (ms, CUDA events on the library stream) of the last build / solve, split by phase:
+ * which = 0 build total, 1 leaf factor, 2 merges, 3 solve total, 4 upward, 5 downward. */
+double hps_last_time_ms(const hps_handle* h, int which);
+
+/* Statistics of the last build/solve for the roofline report: number of kernel launches and
+ * algorithmic FLOPs (8 real flops per complex multiply-add). which: 0 build, 1 solve. */
+int64_t hps_last_launches(const hps_handle* h, int which);
+double hps_last_flops(const hps_handle* h, int which);
+
+void hps_free(hps_handle* h);
+const char* hps_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HPS_H_ */

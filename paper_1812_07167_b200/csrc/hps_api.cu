@@ -1,0 +1,939 @@
+// hps_api.cu — the C-ABI (include/hps.h): tree planner, operator store and the level-by-level
+// orchestration of the precomputation (Algorithm 1) and solve (Algorithm 2,
+// PAPER.md:670-710) stages.  All arithmetic runs in this library's kernels (leaf.cu, zgj.cu,
+// zgemm.cu); the host code below only plans index maps and sequences launches.
+//
+// Tree (reading Q6): heap numbering, root 1, children 2 tau (alpha: west or
+// south) and 2 tau + 1 (beta: east or north); a box of a x b leaves splits vertically when
+// a >= b, else horizontally.  All boxes of one depth are congruent, so one set of index maps
+// per merge level serves every merge of that level (batched launches).
+// Boundary order of every box: [S, E, N, W], each edge by increasing coordinate (reading Q5).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "hps.h"
+#include "hps_internal.cuh"
+#include "hps_kernels.cuh"
+
+thread_local int64_t* g_launch_counter = nullptr;
+static thread_local std::string g_err_msg;
+void hps_set_error(const std::string& m) { g_err_msg = m; }
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Device buffer (RAII)
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  void alloc(size_t n) {
+    release();
+    if (n == 0) return;
+    cudaError_t e = cudaMalloc(&p, n);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      throw HpsError{HPS_ENOMEM, "cudaMalloc of " + std::to_string(n) + " bytes failed: " + cudaGetErrorString(e)};
+    }
+    bytes = n;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+inline zt Z(double re, double im) { return make_double2(re, im); }
+
+struct Depth {
+  int a, b;  // box size in leaves
+  int nb;    // boundary nodes 2 (a + b) q
+};
+
+struct MergeLevel {
+  int d;  // depth of the parent boxes
+  int nparent, a, b, vertical, nbc, n1, n2, n3, ntau;
+  DevBuf maps;
+  int *I1a, *I2b, *I3a, *I3b, *pp, *cmapA, *cmapB;
+  DevBuf ops;
+  zt *PhiA, *PhiB, *Winv, *R33a, *R33b, *R13a, *R23b;
+};
+
+bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// Chebyshev-Lobatto nodes on [-1, 1], ascending, and the spectral differentiation matrix
+// (Trefethen's closed form; reading Q4).
+void cheb(int p, std::vector<double>& x, std::vector<double>& D) {
+  const int N = p - 1;
+  x.assign(p, 0.0);
+  for (int k = 0; k < p; ++k) x[k] = -std::cos(M_PI * k / N);
+  x[0] = -1.0;
+  x[N] = 1.0;
+  if (N % 2 == 0) x[N / 2] = 0.0;
+  D.assign((size_t)p * p, 0.0);
+  for (int i = 0; i < p; ++i) {
+    double s = 0.0;
+    const double ci = (i == 0 || i == N) ? 2.0 : 1.0;
+    for (int j = 0; j < p; ++j) {
+      if (i == j) continue;
+      const double cj = (j == 0 || j == N) ? 2.0 : 1.0;
+      const double v = (ci / cj) * (((i + j) & 1) ? -1.0 : 1.0) / (x[i] - x[j]);
+      D[(size_t)i * p + j] = v;
+      s += v;
+    }
+    D[(size_t)i * p + i] = -s;
+  }
+}
+
+template <class T>
+void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+  b.alloc(sizeof(T) * std::max<size_t>(v.size(), 1));
+  if (!v.empty()) HPS_CUDA_CHECK(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+struct hps_handle {
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  hps_grid g{};
+  int p = 0, q = 0, nbl = 0, ni = 0, nt = 0;
+  double kappa = 0;
+  zt eta{};
+  int L = 0, nleaf = 0;
+  bool keep_root_R = true, keep_all_R = false;
+  std::vector<Depth> depth;
+  std::vector<int> leaf_nat_h, nat_to_heap_h;
+  DevBuf leaf_nat, nat_to_heap, zero_idx;
+  DevBuf store;  // [nleaf heap][nt][nt] = [Psi | Y] per leaf (row-major)
+  std::vector<MergeLevel> lev;  // lev[d] merges children at depth d+1 into depth d
+  std::vector<DevBuf> R;        // R[d]: [2^d][nb(d)][nb(d)] (only the kept ones)
+  DevBuf info;
+  double times[6] = {0, 0, 0, 0, 0, 0};
+  int64_t launches[2] = {0, 0};
+  double flops[2] = {0, 0};
+  cudaEvent_t ev[6] = {};
+  ~hps_handle() {
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Planner: depths, leaf permutation, per-level merge maps
+// ---------------------------------------------------------------------------
+void plan_tree(hps_handle& H) {
+  const int q = H.q;
+  H.depth.clear();
+  int a = H.g.nx, b = H.g.ny;
+  H.depth.push_back({a, b, 2 * (a + b) * q});
+  while (!(a == 1 && b == 1)) {
+    if (a >= b) a /= 2;
+    else b /= 2;
+    H.depth.push_back({a, b, 2 * (a + b) * q});
+  }
+  H.L = (int)H.depth.size() - 1;
+  H.nleaf = H.g.nx * H.g.ny;
+  // leaf heap index -> natural index
+  std::vector<int> ox(1, 0), oy(1, 0);
+  for (int d = 0; d < H.L; ++d) {
+    const Depth& P = H.depth[d];
+    const Depth& Cd = H.depth[d + 1];
+    const bool vertical = P.a >= P.b;
+    std::vector<int> nx2(2 * ox.size()), ny2(2 * oy.size());
+    for (size_t i = 0; i < ox.size(); ++i) {
+      nx2[2 * i] = ox[i];
+      ny2[2 * i] = oy[i];
+      nx2[2 * i + 1] = ox[i] + (vertical ? Cd.a : 0);
+      ny2[2 * i + 1] = oy[i] + (vertical ? 0 : Cd.b);
+    }
+    ox.swap(nx2);
+    oy.swap(ny2);
+  }
+  H.leaf_nat_h.resize(H.nleaf);
+  H.nat_to_heap_h.resize(H.nleaf);
+  for (int l = 0; l < H.nleaf; ++l) {
+    H.leaf_nat_h[l] = oy[l] * H.g.nx + ox[l];
+    H.nat_to_heap_h[H.leaf_nat_h[l]] = l;
+  }
+}
+
+void plan_level(hps_handle& H, int d, MergeLevel& M) {
+  const int q = H.q;
+  const Depth& P = H.depth[d];
+  const Depth& C = H.depth[d + 1];
+  M.d = d;
+  M.nparent = 1 << d;
+  M.a = C.a;
+  M.b = C.b;
+  M.vertical = P.a >= P.b;
+  M.nbc = C.nb;
+  const int a = C.a, b = C.b, aq = a * q, bq = b * q, nbc = C.nb;
+  M.n3 = M.vertical ? bq : aq;
+  M.n1 = M.n2 = nbc - M.n3;
+  M.ntau = 2 * M.n1;
+  std::vector<int> I1a, I2b, I3a, I3b, pp;
+  if (M.vertical) {  // alpha west | beta east; I3 = alpha.E = beta.W
+    for (int k = 0; k < bq; ++k) I3a.push_back(aq + k);
+    for (int k = 0; k < bq; ++k) I3b.push_back(2 * aq + bq + k);
+    for (int j = 0; j < aq; ++j) I1a.push_back(j);                    // alpha S
+    for (int j = aq + bq; j < nbc; ++j) I1a.push_back(j);             // alpha N, W
+    for (int j = 0; j < 2 * aq + bq; ++j) I2b.push_back(j);           // beta S, E, N
+    // parent [S: aS bS | E: bE | N: aN bN | W: aW]
+    for (int j = 0; j < aq; ++j) pp.push_back(j);                      // aS
+    for (int j = 0; j < aq; ++j) pp.push_back(2 * aq + bq + j);        // aN
+    for (int j = 0; j < bq; ++j) pp.push_back(4 * aq + bq + j);        // aW
+    for (int j = 0; j < aq; ++j) pp.push_back(aq + j);                 // bS
+    for (int j = 0; j < bq; ++j) pp.push_back(2 * aq + j);             // bE
+    for (int j = 0; j < aq; ++j) pp.push_back(3 * aq + bq + j);        // bN
+  } else {  // alpha south / beta north; I3 = alpha.N = beta.S
+    for (int k = 0; k < aq; ++k) I3a.push_back(aq + bq + k);
+    for (int k = 0; k < aq; ++k) I3b.push_back(k);
+    for (int j = 0; j < aq + bq; ++j) I1a.push_back(j);               // alpha S, E
+    for (int j = 2 * aq + bq; j < nbc; ++j) I1a.push_back(j);         // alpha W
+    for (int j = aq; j < nbc; ++j) I2b.push_back(j);                   // beta E, N, W
+    // parent [S: aS | E: aE bE | N: bN | W: aW bW]
+    for (int j = 0; j < aq; ++j) pp.push_back(j);                      // aS
+    for (int j = 0; j < bq; ++j) pp.push_back(aq + j);                 // aE
+    for (int j = 0; j < bq; ++j) pp.push_back(2 * aq + 2 * bq + j);    // aW
+    for (int j = 0; j < bq; ++j) pp.push_back(aq + bq + j);            // bE
+    for (int j = 0; j < aq; ++j) pp.push_back(aq + 2 * bq + j);        // bN
+    for (int j = 0; j < bq; ++j) pp.push_back(2 * aq + 3 * bq + j);    // bW
+  }
+  std::vector<int> all;
+  auto put = [&](std::vector<int>& v) {
+    size_t o = all.size();
+    all.insert(all.end(), v.begin(), v.end());
+    return o;
+  };
+  std::vector<int> cmA(M.ntau, -1), cmB(M.ntau, -1);
+  for (int j = 0; j < M.n1; ++j) cmA[j] = I1a[j];
+  for (int j = 0; j < M.n2; ++j) cmB[M.n1 + j] = I2b[j];
+  size_t o1 = put(I1a), o2 = put(I2b), o3 = put(I3a), o4 = put(I3b), o5 = put(pp), o6 = put(cmA), o7 = put(cmB);
+  upload(M.maps, all, H.st);
+  int* base = M.maps.as<int>();
+  M.I1a = base + o1;
+  M.I2b = base + o2;
+  M.I3a = base + o3;
+  M.I3b = base + o4;
+  M.pp = base + o5;
+  M.cmapA = base + o6;
+  M.cmapB = base + o7;
+  // stored operators: Phi^a, Phi^b, W^{-1}, R33a, R33b, R13a, R23b
+  const size_t n3 = M.n3, nt = M.ntau, n1 = M.n1, n2 = M.n2, np = M.nparent;
+  const size_t per = 2 * n3 * nt + 3 * n3 * n3 + n1 * n3 + n2 * n3;
+  M.ops.alloc(sizeof(zt) * per * np);
+  zt* o = M.ops.as<zt>();
+  M.PhiA = o;
+  o += np * n3 * nt;
+  M.PhiB = o;
+  o += np * n3 * nt;
+  M.Winv = o;
+  o += np * n3 * n3;
+  M.R33a = o;
+  o += np * n3 * n3;
+  M.R33b = o;
+  o += np * n3 * n3;
+  M.R13a = o;
+  o += np * n1 * n3;
+  M.R23b = o;
+}
+
+ZOp op(const zt* p, int64_t rs, int64_t bs, const int* rmap = nullptr, const int* cmap = nullptr) {
+  ZOp o;
+  o.ptr = p;
+  o.rs = rs;
+  o.cs = 1;
+  o.bs = bs;
+  o.rmap = rmap;
+  o.cmap = cmap;
+  return o;
+}
+ZOut out(zt* p, int64_t rs, int64_t bs, const int* rmap = nullptr, const int* cmap = nullptr) {
+  ZOut o;
+  o.ptr = p;
+  o.rs = rs;
+  o.cs = 1;
+  o.bs = bs;
+  o.rmap = rmap;
+  o.cmap = cmap;
+  return o;
+}
+
+void check_info(hps_handle& H, const char* what) {
+  int info = 0;
+  HPS_CUDA_CHECK(cudaMemcpyAsync(&info, H.info.p, sizeof(int), cudaMemcpyDeviceToHost, H.st));
+  HPS_CUDA_CHECK(cudaStreamSynchronize(H.st));
+  if (info) throw HpsError{HPS_ESINGULAR, std::string("zero pivot while inverting ") + what + " (batch entry " +
+                                              std::to_string(info - 1) + ")"};
+}
+
+// ---------------------------------------------------------------------------
+// Precomputation: leaves then merges bottom-up (Algorithm 1)
+// ---------------------------------------------------------------------------
+void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
+  const int p = H.p, nt = H.nt, nb = H.nbl, nleaf = H.nleaf;
+  std::vector<double> x, D;
+  cheb(p, x, D);
+  const double hx = (H.g.x1 - H.g.x0) / H.g.nx, hy = (H.g.y1 - H.g.y0) / H.g.ny;
+  std::vector<double> dm((size_t)4 * p * p, 0.0);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) {
+      dm[(size_t)i * p + j] = D[(size_t)i * p + j] * (2.0 / hx);
+      dm[(size_t)p * p + i * p + j] = D[(size_t)i * p + j] * (2.0 / hy);
+    }
+  for (int i = 0; i < p; ++i)  // second derivatives D^2 = D D (SPEC reading)
+    for (int j = 0; j < p; ++j) {
+      double sx = 0, sy = 0;
+      for (int k = 0; k < p; ++k) {
+        sx += dm[(size_t)i * p + k] * dm[(size_t)k * p + j];
+        sy += dm[(size_t)p * p + i * p + k] * dm[(size_t)p * p + k * p + j];
+      }
+      dm[(size_t)2 * p * p + i * p + j] = sx;
+      dm[(size_t)3 * p * p + i * p + j] = sy;
+    }
+  // I^tau positions: [S, E, N, W] (increasing coordinate) then interior (x fastest)
+  std::vector<int> pos((size_t)p * p, -1), node;
+  for (int ix = 1; ix <= p - 2; ++ix) node.push_back(ix);                 // S
+  for (int iy = 1; iy <= p - 2; ++iy) node.push_back(iy * p + p - 1);     // E
+  for (int ix = 1; ix <= p - 2; ++ix) node.push_back((p - 1) * p + ix);   // N
+  for (int iy = 1; iy <= p - 2; ++iy) node.push_back(iy * p);             // W
+  for (int iy = 1; iy <= p - 2; ++iy)
+    for (int ix = 1; ix <= p - 2; ++ix) node.push_back(iy * p + ix);
+  for (int r = 0; r < nt; ++r) pos[node[r]] = r;
+  DevBuf ddm, dpos, dnode;
+  upload(ddm, dm, H.st);
+  upload(dpos, pos, H.st);
+  upload(dnode, node, H.st);
+
+  const size_t mat = (size_t)nt * nt;
+  H.store.alloc(sizeof(zt) * mat * nleaf);
+  int chunk = chunk_opt > 0 ? chunk_opt : (int)std::max<size_t>(1, ((size_t)1 << 30) / (mat * sizeof(zt)));
+  chunk = std::min(chunk, nleaf);
+  DevBuf work, ws;
+  work.alloc(sizeof(zt) * mat * chunk);
+  ws.alloc(std::max<size_t>(zgj_workspace_bytes(nt, chunk), 16));
+  for (int l0 = 0; l0 < nleaf; l0 += chunk) {
+    const int nc = std::min(chunk, nleaf - l0);
+    launch_leaf_assemble(work.as<zt>(), (int64_t)mat, l0, nc, H.leaf_nat.as<int>(), c_dev, p, ddm.as<double>(),
+                         dpos.as<int>(), dnode.as<int>(), H.kappa * H.kappa, H.eta, H.st);
+    zgj_invert(work.as<zt>(), nt, (int64_t)mat, H.store.as<zt>() + (size_t)l0 * mat, nt, (int64_t)mat, nt, nc, ws.p,
+               H.info.as<int>(), H.st, nullptr);
+  }
+  H.flops[0] += 8.0 * (double)nt * nt * nt * nleaf;
+  // leaf R (PAPER.md:398-402 via R = I - 2 i eta Psi_b)
+  H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
+  launch_leaf_R(H.store.as<zt>(), (int64_t)mat, H.R[H.L].as<zt>(), nleaf, nt, nb, H.eta, H.st);
+  // keep the workspaces alive until the stream drains (they are freed on scope exit)
+  HPS_CUDA_CHECK(cudaStreamSynchronize(H.st));
+}
+
+void build_merge(hps_handle& H, int d) {
+  MergeLevel& M = H.lev[d];
+  const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau, nbc = M.nbc;
+  const int64_t cs2 = (int64_t)nbc * nbc;
+  const zt* Ra = H.R[d + 1].as<zt>();
+  const zt* Rb = Ra + cs2;
+  const int64_t cbs = 2 * cs2;
+  cudaStream_t st = H.st;
+  const int64_t s33 = (int64_t)n3 * n3;
+  // (a) retained child blocks
+  {
+    ZCopy c;
+    c.batch = np;
+    c.M = n3;
+    c.N = n3;
+    c.A = op(Ra, nbc, cbs, M.I3a, M.I3a);
+    c.C = out(M.R33a, n3, s33);
+    zcopy(c, st);
+    c.A = op(Rb, nbc, cbs, M.I3b, M.I3b);
+    c.C = out(M.R33b, n3, s33);
+    zcopy(c, st);
+    c.M = n1;
+    c.A = op(Ra, nbc, cbs, M.I1a, M.I3a);
+    c.C = out(M.R13a, n3, (int64_t)n1 * n3);
+    zcopy(c, st);
+    c.M = n2;
+    c.A = op(Rb, nbc, cbs, M.I2b, M.I3b);
+    c.C = out(M.R23b, n3, (int64_t)n2 * n3);
+    zcopy(c, st);
+  }
+  // (b) W = I - R33b R33a  (Algorithm 1 line 7)
+  DevBuf Wk, X, ws;
+  Wk.alloc(sizeof(zt) * s33 * np);
+  {
+    ZGemm g;
+    g.M = g.N = g.K = n3;
+    g.batch = np;
+    g.A = op(M.R33b, n3, s33);
+    g.B = op(M.R33a, n3, s33);
+    g.C = out(Wk.as<zt>(), n3, s33);
+    g.alpha = Z(-1, 0);
+    g.diag = Z(1, 0);
+    zgemm(g, st);
+  }
+  // (c) W^{-1}
+  ws.alloc(std::max<size_t>(zgj_workspace_bytes(n3, np), 16));
+  zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>(), st, nullptr);
+  // (d) X = [R33b R31a | -R32b] ; Phi^a = W^{-1} X  (line 8)
+  const int64_t sx = (int64_t)n3 * nt;
+  X.alloc(sizeof(zt) * sx * np);
+  {
+    ZGemm g;
+    g.M = n3;
+    g.N = n1;
+    g.K = n3;
+    g.batch = np;
+    g.A = op(M.R33b, n3, s33);
+    g.B = op(Ra, nbc, cbs, M.I3a, M.I1a);
+    g.C = out(X.as<zt>(), nt, sx);
+    zgemm(g, st);
+    ZCopy c;
+    c.batch = np;
+    c.M = n3;
+    c.N = n2;
+    c.A = op(Rb, nbc, cbs, M.I3b, M.I2b);
+    c.C = out(X.as<zt>() + n1, nt, sx);
+    c.alpha = Z(-1, 0);
+    zcopy(c, st);
+    g.N = nt;
+    g.A = op(M.Winv, n3, s33);
+    g.B = op(X.as<zt>(), nt, sx);
+    g.C = out(M.PhiA, nt, sx);
+    zgemm(g, st);
+  }
+  // (e) Phi^b = -[R31a | 0] - R33a Phi^a  (line 10, equivalent form)
+  {
+    ZGemm g;
+    g.M = n3;
+    g.N = nt;
+    g.K = n3;
+    g.batch = np;
+    g.A = op(M.R33a, n3, s33);
+    g.B = op(M.PhiA, nt, sx);
+    g.Cin = op(Ra, nbc, cbs, M.I3a, M.cmapA);
+    g.C = out(M.PhiB, nt, sx);
+    g.alpha = Z(-1, 0);
+    g.beta = Z(-1, 0);
+    zgemm(g, st);
+  }
+  double fl = 8.0 * np * ((double)n3 * n3 * n3 * 2 + (double)n3 * n3 * n1 + 2.0 * n3 * n3 * nt);
+  // (f) R^tau = diag(R11a, R22b) + [R13a Phi^a ; R23b Phi^b], scattered to canonical order (line 12)
+  const bool need_R = (d > 0) || H.keep_root_R || H.keep_all_R;
+  if (need_R) {
+    H.R[d].alloc(sizeof(zt) * (size_t)nt * nt * np);
+    const int64_t ps = (int64_t)nt * nt;
+    ZGemm g;
+    g.M = n1;
+    g.N = nt;
+    g.K = n3;
+    g.batch = np;
+    g.A = op(M.R13a, n3, (int64_t)n1 * n3);
+    g.B = op(M.PhiA, nt, sx);
+    g.Cin = op(Ra, nbc, cbs, M.I1a, M.cmapA);
+    g.beta = Z(1, 0);
+    g.C = out(H.R[d].as<zt>(), nt, ps, M.pp, M.pp);
+    zgemm(g, st);
+    g.M = n2;
+    g.A = op(M.R23b, n3, (int64_t)n2 * n3);
+    g.B = op(M.PhiB, nt, sx);
+    g.Cin = op(Rb, nbc, cbs, M.I2b, M.cmapB);
+    g.C = out(H.R[d].as<zt>(), nt, ps, M.pp + n1, M.pp);
+    zgemm(g, st);
+    fl += 8.0 * np * (double)nt * nt * n3;
+  }
+  H.flops[0] += fl;
+  HPS_CUDA_CHECK(cudaStreamSynchronize(st));  // temporaries die at scope exit
+  if (!H.keep_all_R) H.R[d + 1].release();    // Algorithm 1 line 14
+}
+
+// ---------------------------------------------------------------------------
+// Solve (Algorithm 2).  Internal vectors: [box][n][nrhs] (RHS innermost).
+// ---------------------------------------------------------------------------
+void solve_impl(hps_handle& H, int nrhs, const zt* s_dev, const zt* t_dev, zt* u_dev) {
+  cudaStream_t st = H.st;
+  const int nleaf = H.nleaf, nt = H.nt, nb = H.nbl, ni = H.ni, L = H.L;
+  const int64_t R = nrhs;
+  std::vector<DevBuf> h(L + 1), t(L + 1), TTa(L), TTb(L);
+  DevBuf sint, ut, uint_;
+  const bool has_s = s_dev != nullptr;
+  double fl = 0;
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev[0], st));
+  // ---- upward pass (lines 1-9) ----
+  if (has_s) {
+    sint.alloc(sizeof(zt) * (size_t)nleaf * ni * R);
+    launch_rhs_in(s_dev, sint.as<zt>(), H.leaf_nat.as<int>(), nleaf, ni, nrhs, st);
+    ut.alloc(sizeof(zt) * (size_t)nleaf * nt * R);
+    {  // u~ = Y s
+      ZGemm g;
+      g.M = nt;
+      g.N = nrhs;
+      g.K = ni;
+      g.batch = nleaf;
+      g.A = op(H.store.as<zt>() + nb, nt, (int64_t)nt * nt);
+      g.B = op(sint.as<zt>(), R, (int64_t)ni * R);
+      g.C = out(ut.as<zt>(), R, (int64_t)nt * R);
+      zgemm(g, st);
+      fl += 8.0 * nleaf * (double)nt * ni * R;
+    }
+    h[L].alloc(sizeof(zt) * (size_t)nleaf * nb * R);
+    {  // h = Gamma s = -2 i eta u~(I_b)
+      ZCopy c;
+      c.batch = nleaf;
+      c.M = nb;
+      c.N = nrhs;
+      c.A = op(ut.as<zt>(), R, (int64_t)nt * R);
+      c.C = out(h[L].as<zt>(), R, (int64_t)nb * R);
+      c.alpha = Z(2.0 * H.eta.y, -2.0 * H.eta.x);
+      zcopy(c, st);
+    }
+    for (int d = L - 1; d >= 0; --d) {
+      MergeLevel& M = H.lev[d];
+      const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, ntau = M.ntau, nbc = M.nbc;
+      const int64_t s33 = (int64_t)n3 * n3, cb = 2 * (int64_t)nbc * R;
+      const zt* ha = h[d + 1].as<zt>();
+      const zt* hb = ha + (int64_t)nbc * R;
+      DevBuf tmp;
+      tmp.alloc(sizeof(zt) * (size_t)np * n3 * R);
+      TTa[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
+      TTb[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
+      ZGemm g;
+      g.batch = np;
+      g.N = nrhs;
+      // tmp = R33b h3a - h3b ; t~a = W^{-1} tmp ; t~b = -h3a - R33a t~a   (Upsilon actions)
+      g.M = n3;
+      g.K = n3;
+      g.A = op(M.R33b, n3, s33);
+      g.B = op(ha, R, cb, M.I3a);
+      g.Cin = op(hb, R, cb, M.I3b);
+      g.beta = Z(-1, 0);
+      g.C = out(tmp.as<zt>(), R, (int64_t)n3 * R);
+      zgemm(g, st);
+      g.A = op(M.Winv, n3, s33);
+      g.B = op(tmp.as<zt>(), R, (int64_t)n3 * R);
+      g.Cin = ZOp();
+      g.beta = Z(0, 0);
+      g.C = out(TTa[d].as<zt>(), R, (int64_t)n3 * R);
+      zgemm(g, st);
+      g.A = op(M.R33a, n3, s33);
+      g.B = op(TTa[d].as<zt>(), R, (int64_t)n3 * R);
+      g.Cin = op(ha, R, cb, M.I3a);
+      g.alpha = Z(-1, 0);
+      g.beta = Z(-1, 0);
+      g.C = out(TTb[d].as<zt>(), R, (int64_t)n3 * R);
+      zgemm(g, st);
+      fl += 8.0 * np * 3.0 * n3 * n3 * R;
+      if (d > 0) {  // h^tau = [h1a; h2b] + [R13a t~a; R23b t~b]  (eq. flux_part), canonical order
+        h[d].alloc(sizeof(zt) * (size_t)np * ntau * R);
+        g.alpha = Z(1, 0);
+        g.beta = Z(1, 0);
+        g.M = n1;
+        g.A = op(M.R13a, n3, (int64_t)n1 * n3);
+        g.B = op(TTa[d].as<zt>(), R, (int64_t)n3 * R);
+        g.Cin = op(ha, R, cb, M.I1a);
+        g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp);
+        zgemm(g, st);
+        g.M = n2;
+        g.A = op(M.R23b, n3, (int64_t)n2 * n3);
+        g.B = op(TTb[d].as<zt>(), R, (int64_t)n3 * R);
+        g.Cin = op(hb, R, cb, M.I2b);
+        g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp + n1);
+        zgemm(g, st);
+        fl += 8.0 * np * (double)(n1 + n2) * n3 * R;
+      }
+      HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+      h[d + 1].release();
+    }
+  }
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev[1], st));
+  // ---- downward pass (lines 10-18) ----
+  t[0].alloc(sizeof(zt) * (size_t)H.depth[0].nb * R);
+  launch_rhs_in(t_dev, t[0].as<zt>(), H.zero_idx.as<int>(), 1, H.depth[0].nb, nrhs, st);
+  for (int d = 0; d < L; ++d) {
+    MergeLevel& M = H.lev[d];
+    const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, ntau = M.ntau, nbc = M.nbc;
+    t[d + 1].alloc(sizeof(zt) * (size_t)2 * np * nbc * R);
+    zt* ta = t[d + 1].as<zt>();
+    zt* tb = ta + (int64_t)nbc * R;
+    const int64_t cb = 2 * (int64_t)nbc * R, pb = (int64_t)ntau * R;
+    ZGemm g;
+    g.batch = np;
+    g.M = n3;
+    g.N = nrhs;
+    g.K = ntau;
+    g.A = op(M.PhiA, ntau, (int64_t)n3 * ntau);
+    g.B = op(t[d].as<zt>(), R, pb, M.pp);
+    if (has_s) {
+      g.Cin = op(TTa[d].as<zt>(), R, (int64_t)n3 * R);
+      g.beta = Z(1, 0);
+    }
+    g.C = out(ta, R, cb, M.I3a);
+    zgemm(g, st);  // t3a = Phi^a t + t~a
+    g.A = op(M.PhiB, ntau, (int64_t)n3 * ntau);
+    if (has_s) g.Cin = op(TTb[d].as<zt>(), R, (int64_t)n3 * R);
+    g.C = out(tb, R, cb, M.I3b);
+    zgemm(g, st);  // t3b = Phi^b t + t~b
+    fl += 8.0 * np * 2.0 * n3 * ntau * R;
+    ZCopy c;
+    c.batch = np;
+    c.N = nrhs;
+    c.M = n1;
+    c.A = op(t[d].as<zt>(), R, pb, M.pp);
+    c.C = out(ta, R, cb, M.I1a);
+    zcopy(c, st);
+    c.M = n2;
+    c.A = op(t[d].as<zt>(), R, pb, M.pp + n1);
+    c.C = out(tb, R, cb, M.I2b);
+    zcopy(c, st);
+    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    t[d].release();
+    if (has_s) {
+      TTa[d].release();
+      TTb[d].release();
+    }
+  }
+  uint_.alloc(sizeof(zt) * (size_t)nleaf * nt * R);
+  {  // u = Psi t + u~  (line 13)
+    ZGemm g;
+    g.M = nt;
+    g.N = nrhs;
+    g.K = nb;
+    g.batch = nleaf;
+    g.A = op(H.store.as<zt>(), nt, (int64_t)nt * nt);
+    g.B = op(t[L].as<zt>(), R, (int64_t)nb * R);
+    if (has_s) {
+      g.Cin = op(ut.as<zt>(), R, (int64_t)nt * R);
+      g.beta = Z(1, 0);
+    }
+    g.C = out(uint_.as<zt>(), R, (int64_t)nt * R);
+    zgemm(g, st);
+    fl += 8.0 * nleaf * (double)nt * nb * R;
+  }
+  launch_rhs_out(uint_.as<zt>(), u_dev, H.nat_to_heap.as<int>(), nleaf, nt, nrhs, st);
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev[2], st));
+  HPS_CUDA_CHECK(cudaEventSynchronize(H.ev[2]));
+  float a = 0, b = 0;
+  cudaEventElapsedTime(&a, H.ev[0], H.ev[1]);
+  cudaEventElapsedTime(&b, H.ev[1], H.ev[2]);
+  H.times[3] = a + b;
+  H.times[4] = a;
+  H.times[5] = b;
+  H.flops[1] = fl;
+}
+
+int fail(const HpsError& e) {
+  hps_set_error(e.msg);
+  return e.code;
+}
+
+struct LaunchScope {
+  int64_t* prev;
+  explicit LaunchScope(int64_t* c) : prev(g_launch_counter) {
+    *c = 0;
+    g_launch_counter = c;
+  }
+  ~LaunchScope() { g_launch_counter = prev; }
+};
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* hps_last_error(void) { return g_err_msg.c_str(); }
+
+int hps_leaf_nodes(const hps_grid* g, int p, double* x, double* y) {
+  if (!g || p < 2 || g->nx < 1 || g->ny < 1 || !x || !y) {
+    hps_set_error("hps_leaf_nodes: invalid argument");
+    return HPS_EINVAL;
+  }
+  std::vector<double> xi, D;
+  cheb(p, xi, D);
+  const double hx = (g->x1 - g->x0) / g->nx, hy = (g->y1 - g->y0) / g->ny;
+  for (int ly = 0; ly < g->ny; ++ly)
+    for (int lx = 0; lx < g->nx; ++lx) {
+      const size_t base = ((size_t)ly * g->nx + lx) * p * p;
+      for (int iy = 0; iy < p; ++iy)
+        for (int ix = 0; ix < p; ++ix) {
+          x[base + iy * p + ix] = g->x0 + lx * hx + (1.0 + xi[ix]) * 0.5 * hx;
+          y[base + iy * p + ix] = g->y0 + ly * hy + (1.0 + xi[iy]) * 0.5 * hy;
+        }
+    }
+  return HPS_OK;
+}
+
+int hps_root_boundary_nodes(const hps_grid* g, int p, double* x, double* y, double* nx, double* ny) {
+  if (!g || p < 4 || g->nx < 1 || g->ny < 1 || !x || !y || !nx || !ny) {
+    hps_set_error("hps_root_boundary_nodes: invalid argument");
+    return HPS_EINVAL;
+  }
+  std::vector<double> xi, D;
+  cheb(p, xi, D);
+  const double hx = (g->x1 - g->x0) / g->nx, hy = (g->y1 - g->y0) / g->ny;
+  size_t o = 0;
+  auto push = [&](double px, double py, double vx, double vy) {
+    x[o] = px;
+    y[o] = py;
+    nx[o] = vx;
+    ny[o] = vy;
+    ++o;
+  };
+  for (int l = 0; l < g->nx; ++l)
+    for (int k = 1; k <= p - 2; ++k) push(g->x0 + l * hx + (1 + xi[k]) * 0.5 * hx, g->y0, 0, -1);  // S
+  for (int l = 0; l < g->ny; ++l)
+    for (int k = 1; k <= p - 2; ++k) push(g->x1, g->y0 + l * hy + (1 + xi[k]) * 0.5 * hy, 1, 0);   // E
+  for (int l = 0; l < g->nx; ++l)
+    for (int k = 1; k <= p - 2; ++k) push(g->x0 + l * hx + (1 + xi[k]) * 0.5 * hx, g->y1, 0, 1);   // N
+  for (int l = 0; l < g->ny; ++l)
+    for (int k = 1; k <= p - 2; ++k) push(g->x0, g->y0 + l * hy + (1 + xi[k]) * 0.5 * hy, -1, 0);  // W
+  return HPS_OK;
+}
+
+int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_c128* c_samples,
+              const hps_opts* opt, hps_handle** outp) {
+  if (outp) *outp = nullptr;
+  if (!g || !outp || !c_samples) {
+    hps_set_error("hps_build: NULL argument");
+    return HPS_EINVAL;
+  }
+  if (p < 4) {
+    hps_set_error("hps_build: p must be >= 4");
+    return HPS_EINVAL;
+  }
+  if (q != p - 2) {
+    hps_set_error("hps_build: q must equal p - 2 (corner-free Chebyshev boundary nodes)");
+    return HPS_EINVAL;
+  }
+  if (!is_pow2(g->nx) || !is_pow2(g->ny)) {
+    hps_set_error("hps_build: nx and ny must be powers of two");
+    return HPS_EINVAL;
+  }
+  if (!(g->x1 > g->x0) || !(g->y1 > g->y0) || !std::isfinite(g->x0) || !std::isfinite(g->x1) ||
+      !std::isfinite(g->y0) || !std::isfinite(g->y1)) {
+    hps_set_error("hps_build: need finite x1 > x0 and y1 > y0");
+    return HPS_EINVAL;
+  }
+  if (!(kappa >= 0) || !std::isfinite(kappa)) {
+    hps_set_error("hps_build: kappa must be finite and >= 0");
+    return HPS_EINVAL;
+  }
+  if (eta.re == 0.0 || !std::isfinite(eta.re) || !std::isfinite(eta.im)) {
+    hps_set_error("hps_build: Re(eta) must be nonzero and eta finite");
+    return HPS_EINVAL;
+  }
+  std::unique_ptr<hps_handle> H(new hps_handle());
+  try {
+    if (opt && opt->device >= 0) HPS_CUDA_CHECK(cudaSetDevice(opt->device));
+    HPS_CUDA_CHECK(cudaGetDevice(&H->dev));
+    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H->st, cudaStreamNonBlocking));
+    for (auto& e : H->ev) HPS_CUDA_CHECK(cudaEventCreate(&e));
+    H->g = *g;
+    H->p = p;
+    H->q = q;
+    H->nbl = 4 * q;
+    H->ni = q * q;
+    H->nt = p * p - 4;
+    H->kappa = kappa;
+    H->eta = make_double2(eta.re, eta.im);
+    H->keep_root_R = opt ? opt->keep_root_R != 0 : true;
+    H->keep_all_R = opt ? opt->keep_all_R != 0 : false;
+    LaunchScope ls(&H->launches[0]);
+    H->flops[0] = 0;
+    plan_tree(*H);
+    upload(H->leaf_nat, H->leaf_nat_h, H->st);
+    upload(H->nat_to_heap, H->nat_to_heap_h, H->st);
+    upload(H->zero_idx, std::vector<int>{0}, H->st);
+    H->info.alloc(sizeof(int));
+    HPS_CUDA_CHECK(cudaMemsetAsync(H->info.p, 0, sizeof(int), H->st));
+    H->R.resize(H->L + 1);
+    H->lev.resize(H->L);
+    for (int d = 0; d < H->L; ++d) plan_level(*H, d, H->lev[d]);
+    // c samples: host or device
+    const size_t cbytes = sizeof(zt) * (size_t)H->nleaf * p * p;
+    DevBuf cbuf;
+    const zt* c_dev = reinterpret_cast<const zt*>(c_samples);
+    if (!is_device_ptr(c_samples)) {
+      cbuf.alloc(cbytes);
+      HPS_CUDA_CHECK(cudaMemcpyAsync(cbuf.p, c_samples, cbytes, cudaMemcpyHostToDevice, H->st));
+      c_dev = cbuf.as<zt>();
+    }
+    HPS_CUDA_CHECK(cudaEventRecord(H->ev[0], H->st));
+    build_leaves(*H, c_dev, opt ? opt->leaf_chunk : 0);
+    HPS_CUDA_CHECK(cudaEventRecord(H->ev[1], H->st));
+    check_info(*H, "a leaf matrix B");
+    for (int d = H->L - 1; d >= 0; --d) {
+      build_merge(*H, d);
+      check_info(*H, ("W at merge depth " + std::to_string(d)).c_str());
+    }
+    HPS_CUDA_CHECK(cudaEventRecord(H->ev[2], H->st));
+    HPS_CUDA_CHECK(cudaEventSynchronize(H->ev[2]));
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, H->ev[0], H->ev[1]);
+    cudaEventElapsedTime(&b, H->ev[1], H->ev[2]);
+    H->times[0] = a + b;
+    H->times[1] = a;
+    H->times[2] = b;
+  } catch (const HpsError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(HpsError{HPS_ECUDA, e.what()});
+  }
+  *outp = H.release();
+  return HPS_OK;
+}
+
+int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps_c128* u) {
+  if (!h || nrhs < 0 || !t || !u) {
+    hps_set_error("hps_solve: invalid argument");
+    return HPS_EINVAL;
+  }
+  if (nrhs == 0) return HPS_OK;
+  try {
+    HPS_CUDA_CHECK(cudaSetDevice(h->dev));
+    LaunchScope ls(&h->launches[1]);
+    const size_t sb = sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni;
+    const size_t tb = sizeof(zt) * (size_t)nrhs * h->depth[0].nb;
+    const size_t ub = sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt;
+    DevBuf sd, td, ud;
+    const zt* s_dev = reinterpret_cast<const zt*>(s);
+    const zt* t_dev = reinterpret_cast<const zt*>(t);
+    zt* u_dev = reinterpret_cast<zt*>(u);
+    if (s && !is_device_ptr(s)) {
+      sd.alloc(sb);
+      HPS_CUDA_CHECK(cudaMemcpyAsync(sd.p, s, sb, cudaMemcpyHostToDevice, h->st));
+      s_dev = sd.as<zt>();
+    }
+    if (!is_device_ptr(t)) {
+      td.alloc(tb);
+      HPS_CUDA_CHECK(cudaMemcpyAsync(td.p, t, tb, cudaMemcpyHostToDevice, h->st));
+      t_dev = td.as<zt>();
+    }
+    const bool u_host = !is_device_ptr(u);
+    if (u_host) {
+      ud.alloc(ub);
+      u_dev = ud.as<zt>();
+    }
+    solve_impl(*h, nrhs, s_dev, t_dev, u_dev);
+    if (u_host) HPS_CUDA_CHECK(cudaMemcpyAsync(u, u_dev, ub, cudaMemcpyDeviceToHost, h->st));
+    HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
+  } catch (const HpsError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(HpsError{HPS_ECUDA, e.what()});
+  }
+  return HPS_OK;
+}
+
+int64_t hps_box_nb(const hps_handle* h, int64_t box) {
+  if (!h || box < 1) return -1;
+  int d = 0;
+  while (((int64_t)1 << (d + 1)) <= box) ++d;
+  if (d > h->L) return -1;
+  return h->depth[d].nb;
+}
+
+int64_t hps_num_boxes(const hps_handle* h) { return h ? ((int64_t)2 << h->L) - 1 : -1; }
+
+int hps_export_R(const hps_handle* h, int64_t box, hps_c128* outR) {
+  if (!h || !outR || box < 1) {
+    hps_set_error("hps_export_R: invalid argument");
+    return HPS_EINVAL;
+  }
+  int d = 0;
+  while (((int64_t)1 << (d + 1)) <= box) ++d;
+  if (d > h->L) {
+    hps_set_error("hps_export_R: box id out of range");
+    return HPS_EINVAL;
+  }
+  if (!h->R[d].p) {
+    hps_set_error("hps_export_R: R of this box was not kept (set keep_all_R / keep_root_R)");
+    return HPS_ENOTKEPT;
+  }
+  try {
+    const size_t n = h->depth[d].nb;
+    const int64_t idx = box - ((int64_t)1 << d);
+    HPS_CUDA_CHECK(cudaMemcpy(outR, h->R[d].as<zt>() + idx * n * n, sizeof(zt) * n * n, cudaMemcpyDefault));
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+  return HPS_OK;
+}
+
+int hps_export_leaf(const hps_handle* h, int64_t leaf, hps_c128* psi, hps_c128* y) {
+  if (!h || leaf < 0 || leaf >= h->nleaf) {
+    hps_set_error("hps_export_leaf: invalid argument");
+    return HPS_EINVAL;
+  }
+  try {
+    const int nt = h->nt, nb = h->nbl, ni = h->ni;
+    const zt* base = h->store.as<zt>() + (size_t)h->nat_to_heap_h[leaf] * nt * nt;
+    if (psi)
+      HPS_CUDA_CHECK(cudaMemcpy2D(psi, sizeof(zt) * nb, base, sizeof(zt) * nt, sizeof(zt) * nb, nt, cudaMemcpyDefault));
+    if (y)
+      HPS_CUDA_CHECK(
+          cudaMemcpy2D(y, sizeof(zt) * ni, base + nb, sizeof(zt) * nt, sizeof(zt) * ni, nt, cudaMemcpyDefault));
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+  return HPS_OK;
+}
+
+double hps_last_time_ms(const hps_handle* h, int which) {
+  if (!h || which < 0 || which > 5) return -1;
+  return h->times[which];
+}
+
+int64_t hps_last_launches(const hps_handle* h, int which) {
+  if (!h || which < 0 || which > 1) return -1;
+  return h->launches[which];
+}
+
+double hps_last_flops(const hps_handle* h, int which) {
+  if (!h || which < 0 || which > 1) return -1;
+  return h->flops[which];
+}
+
+void hps_free(hps_handle* h) { delete h; }
+
+}  // extern "C"

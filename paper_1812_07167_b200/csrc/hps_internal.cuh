@@ -1,0 +1,91 @@
+// hps_internal.cuh — shared declarations of libhps.so (product path; no oracle code).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+typedef double2 zt;  // complex128, interleaved (re, im)
+
+// ---------------------------------------------------------------------------
+// Errors
+// ---------------------------------------------------------------------------
+struct HpsError {
+  int code;
+  std::string msg;
+};
+void hps_set_error(const std::string& msg);
+
+#define HPS_CUDA_CHECK(x)                                                                     \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess)                                                                    \
+      throw HpsError{-4, std::string("CUDA error ") + cudaGetErrorString(e_) + " at " +      \
+                             __FILE__ + ":" + std::to_string(__LINE__)};                       \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Batched complex GEMM on FP64 tensor cores (DMMA m8n8k4), zgemm.cu
+//   C[b](i, j) = alpha * sum_k A[b](i, k) B[b](k, j) + beta * Cin[b](i, j) + (i == j) * diag
+// Operand element (i, k) of batch b lives at ptr + b*bs + R(i)*rs + Cc(k)*cs where R / Cc are
+// the optional int maps (identity when NULL).  A negative map entry means "zero" for loads and
+// "skip" for stores.  Complex products are four real DMMAs (re/im sub-GEMMs).
+// ---------------------------------------------------------------------------
+// Without a column map, column j may skip a window: j -> j + (j >= cskip_at ? cskip_len : 0)
+// (used by the blocked Gauss-Jordan update, which touches every column but the panel).
+struct ZOp {
+  const zt* ptr = nullptr;
+  int64_t rs = 0, cs = 1, bs = 0;
+  const int* rmap = nullptr;
+  const int* cmap = nullptr;
+  int cskip_at = 0x7fffffff, cskip_len = 0;
+};
+
+struct ZOut {
+  zt* ptr = nullptr;
+  int64_t rs = 0, cs = 1, bs = 0;
+  const int* rmap = nullptr;
+  const int* cmap = nullptr;
+  int cskip_at = 0x7fffffff, cskip_len = 0;
+};
+
+__device__ __forceinline__ int zcol(const int* cmap, int j, int skip_at, int skip_len) {
+  return cmap ? cmap[j] : j + (j >= skip_at ? skip_len : 0);
+}
+
+struct ZGemm {
+  int M = 0, N = 0, K = 0, batch = 1;
+  ZOp A, B, Cin;  // Cin.ptr == nullptr => beta term omitted
+  ZOut C;
+  zt alpha = {1.0, 0.0};
+  zt beta = {0.0, 0.0};
+  zt diag = {0.0, 0.0};
+};
+
+void zgemm(const ZGemm& g, cudaStream_t st);
+
+// Batched 2-D gather/scale copy: C[b](i, j) = alpha * A[b](i, j) (+ beta * Cin), maps as above.
+struct ZCopy {
+  int M = 0, N = 0, batch = 1;
+  ZOp A;
+  ZOut C;
+  zt alpha = {1.0, 0.0};
+};
+void zcopy(const ZCopy& c, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Batched explicit inverse by Gauss-Jordan with partial pivoting, zgj.cu
+//   A: batch of n x n row-major matrices (lda, stride bs) — destroyed.
+//   out: batch of n x n row-major (ldo, stride obs) receives A^{-1}.
+//   ws: workspace from zgj_workspace_bytes.  info: device int, set to 1 + batch index of the
+//   first matrix with an exactly zero pivot (0 = success).
+// ---------------------------------------------------------------------------
+size_t zgj_workspace_bytes(int n, int batch);
+void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
+                void* ws, int* info, cudaStream_t st, int64_t* launches);
+
+// Launch counter used for the gpu_launches report.
+extern thread_local int64_t* g_launch_counter;
+inline void count_launch(int k = 1) {
+  if (g_launch_counter) *g_launch_counter += k;
+}

@@ -1,0 +1,10 @@
+// hps_kernels.cuh — launchers of the leaf / layout kernels (leaf.cu).
+#pragma once
+#include "hps_internal.cuh"
+
+void launch_leaf_assemble(zt* B, int64_t bstride, int leaf0, int nchunk, const int* leaf_nat, const zt* c, int p,
+                          const double* dmat, const int* pos, const int* node, double kappa2, zt eta,
+                          cudaStream_t st);
+void launch_leaf_R(const zt* store, int64_t sstride, zt* R, int nleaf, int nt, int nb, zt eta, cudaStream_t st);
+void launch_rhs_in(const zt* src, zt* dst, const int* leaf_nat, int nleaf, int n, int nrhs, cudaStream_t st);
+void launch_rhs_out(const zt* src, zt* dst, const int* nat_to_heap, int nleaf, int n, int nrhs, cudaStream_t st);

@@ -1,0 +1,140 @@
+// leaf.cu — batched leaf assembly and small layout kernels.
+//
+// B = [F ; Ahat(I_i, I^tau)]  (eq. 7; reading Q2), n^tau x n^tau row-major, columns in
+// I^tau = [I_b (S, E, N, W); I_i] order.  F = N + i eta I(I_b, I^tau) with N the outward
+// normal derivative (reading Q1: S -d/dy, E +d/dx, N +d/dy, W -d/dx).
+// Ahat = -Dx^2 - Dy^2 - diag(kappa^2 c) on the p x p tensor grid.
+// One CTA per leaf; one thread per row (each row has at most 2p nonzeros).
+#include "hps_internal.cuh"
+#include "hps_kernels.cuh"
+
+namespace {
+
+__global__ void leaf_assemble_kernel(zt* __restrict__ B, int64_t bstride, int leaf0, int nleaf_chunk,
+                                     const int* __restrict__ leaf_nat, const zt* __restrict__ c, int p,
+                                     const double* __restrict__ dmat,  // [4][p][p]: Dx, Dy, Dxx, Dyy
+                                     const int* __restrict__ pos,      // [p*p] -> I^tau position or -1
+                                     const int* __restrict__ node,     // [n^tau] -> tensor node
+                                     double kappa2, zt eta) {
+  const int lc = blockIdx.x;
+  if (lc >= nleaf_chunk) return;
+  const int q = p - 2, nb = 4 * q, nt = p * p - 4;
+  zt* Bl = B + (int64_t)lc * bstride;
+  const zt* cl = c + (int64_t)leaf_nat[leaf0 + lc] * p * p;
+  const int64_t n2 = (int64_t)nt * nt;
+  for (int64_t e = threadIdx.x; e < n2; e += blockDim.x) Bl[e] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const double* Dx = dmat;
+  const double* Dy = dmat + p * p;
+  const double* Dxx = dmat + 2 * p * p;
+  const double* Dyy = dmat + 3 * p * p;
+  for (int rho = threadIdx.x; rho < nt; rho += blockDim.x) {
+    const int tn = node[rho];
+    const int ix = tn % p, iy = tn / p;
+    zt* row = Bl + (int64_t)rho * nt;
+    if (rho < nb) {
+      const int edge = rho / q;  // 0 S, 1 E, 2 N, 3 W
+      for (int k = 0; k < p; ++k) {
+        if (edge == 0 || edge == 2) {  // -+ d/dy along the column (ix, k)
+          const int col = pos[k * p + ix];
+          const double v = (edge == 0 ? -1.0 : 1.0) * Dy[iy * p + k];
+          if (col >= 0) row[col].x += v;
+        } else {                       // +- d/dx along the row (k, iy)
+          const int col = pos[iy * p + k];
+          const double v = (edge == 1 ? 1.0 : -1.0) * Dx[ix * p + k];
+          if (col >= 0) row[col].x += v;
+        }
+      }
+      // + i eta on the diagonal
+      row[rho].x += -eta.y;
+      row[rho].y += eta.x;
+    } else {
+      for (int k = 0; k < p; ++k) {
+        row[pos[iy * p + k]].x -= Dxx[ix * p + k];
+        row[pos[k * p + ix]].x -= Dyy[iy * p + k];
+      }
+      const zt cv = cl[tn];
+      row[rho].x -= kappa2 * cv.x;
+      row[rho].y -= kappa2 * cv.y;
+    }
+  }
+}
+
+// R = I - 2 i eta Psi(I_b, :)  (from G = F - 2 i eta I(I_b, .) and F Psi = I)
+__global__ void leaf_R_kernel(const zt* __restrict__ store, int64_t sstride, zt* __restrict__ R, int nleaf, int nt,
+                              int nb, zt m2ieta) {
+  const int64_t total = (int64_t)nleaf * nb * nb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % nb);
+    const int64_t t = e / nb;
+    const int i = (int)(t % nb);
+    const int l = (int)(t / nb);
+    const zt psi = store[(int64_t)l * sstride + (int64_t)i * nt + j];
+    zt v = make_double2(m2ieta.x * psi.x - m2ieta.y * psi.y, m2ieta.x * psi.y + m2ieta.y * psi.x);
+    if (i == j) v.x += 1.0;
+    R[e] = v;
+  }
+}
+
+// ABI [nrhs][nleaf natural][n] -> internal [nleaf heap][n][nrhs]
+__global__ void rhs_in_kernel(const zt* __restrict__ src, zt* __restrict__ dst, const int* __restrict__ leaf_nat,
+                              int nleaf, int n, int nrhs) {
+  const int64_t total = (int64_t)nleaf * n * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e % nrhs);
+    const int64_t t = e / nrhs;
+    const int i = (int)(t % n);
+    const int l = (int)(t / n);
+    dst[e] = src[((int64_t)r * nleaf + leaf_nat[l]) * n + i];
+  }
+}
+
+// internal [nleaf heap][n][nrhs] -> ABI [nrhs][nleaf natural][n]
+__global__ void rhs_out_nat_kernel(const zt* __restrict__ src, zt* __restrict__ dst, const int* __restrict__ nat_to_heap,
+                                   int nleaf, int n, int nrhs) {
+  const int64_t total = (int64_t)nleaf * n * nrhs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n);
+    const int64_t t = e / n;
+    const int ln = (int)(t % nleaf);
+    const int r = (int)(t / nleaf);
+    dst[e] = src[((int64_t)nat_to_heap[ln] * n + i) * nrhs + r];
+  }
+}
+
+inline int grid_for(int64_t total) {
+  int64_t b = (total + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+}  // namespace
+
+void launch_leaf_assemble(zt* B, int64_t bstride, int leaf0, int nchunk, const int* leaf_nat, const zt* c, int p,
+                          const double* dmat, const int* pos, const int* node, double kappa2, zt eta,
+                          cudaStream_t st) {
+  leaf_assemble_kernel<<<nchunk, 256, 0, st>>>(B, bstride, leaf0, nchunk, leaf_nat, c, p, dmat, pos, node, kappa2,
+                                                eta);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_leaf_R(const zt* store, int64_t sstride, zt* R, int nleaf, int nt, int nb, zt eta, cudaStream_t st) {
+  const zt m2ieta = make_double2(2.0 * eta.y, -2.0 * eta.x);  // -2 i eta
+  leaf_R_kernel<<<grid_for((int64_t)nleaf * nb * nb), 256, 0, st>>>(store, sstride, R, nleaf, nt, nb, m2ieta);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_rhs_in(const zt* src, zt* dst, const int* leaf_nat, int nleaf, int n, int nrhs, cudaStream_t st) {
+  rhs_in_kernel<<<grid_for((int64_t)nleaf * n * nrhs), 256, 0, st>>>(src, dst, leaf_nat, nleaf, n, nrhs);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_rhs_out(const zt* src, zt* dst, const int* nat_to_heap, int nleaf, int n, int nrhs, cudaStream_t st) {
+  rhs_out_nat_kernel<<<grid_for((int64_t)nleaf * n * nrhs), 256, 0, st>>>(src, dst, nat_to_heap, nleaf, n, nrhs);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}

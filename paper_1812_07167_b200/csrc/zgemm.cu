@@ -1,0 +1,247 @@
+// zgemm.cu — batched complex128 GEMM on the FP64 tensor cores of sm_100a.
+//
+// Every dense product of the HPS merge (Algorithm 1 lines 7-13), of the
+// blocked Gauss-Jordan update (zgj.cu) and of the solve sweeps (Algorithm 2) is one call of
+// this kernel.  sm_100a has no tcgen05 / TMEM path for f64 (ptxas rejects .kind::f64), so the
+// FP64 tensor path is warp-level mma.sync m8n8k4 (SASS DMMA.8x8x4).  A complex product is four
+// real DMMAs: Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br (no 3M trick: it costs accuracy).
+// Operands are staged global -> shared with cp.async (16 B = one complex element, zero-fill
+// for ragged edges and for "zero" map entries), double-buffered.  Shared-memory strides are
+// chosen so that the 8x4 / 4x8 DMMA fragments load as conflict-free 16-byte LDS.
+#include "hps_internal.cuh"
+
+namespace {
+
+constexpr int BK = 16;  // K depth of one pipeline stage (complex elements)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ zt zmul(zt a, zt b) { return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+
+template <int BM, int BN, int WM, int WN>
+struct Cfg {
+  static constexpr int NWM = BM / WM, NWN = BN / WN, NT = NWM * NWN * 32;
+  static constexpr int TM = WM / 8, TN = WN / 8;
+  static constexpr int AS = BK + 4;  // A tile row stride (complex)
+  static constexpr int BS = BN + 2;  // B tile row stride (complex)
+  static constexpr int ITA = BM * BK / NT, ITB = BK * BN / NT;
+  static constexpr size_t SMEM = sizeof(zt) * 2 * (BM * AS + BK * BS);
+  static_assert(NT % BK == 0 && ITA >= 1 && ITB >= 1 && (BM * BK) % NT == 0 && (BK * BN) % NT == 0, "cfg");
+  static_assert(NT % BN == 0 || BN % NT == 0, "cfg");
+};
+
+template <int BM, int BN, int WM, int WN>
+__global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZGemm g) {
+  using C = Cfg<BM, BN, WM, WN>;
+  constexpr int NT = C::NT, TM = C::TM, TN = C::TN, AS = C::AS, BS = C::BS, ITA = C::ITA, ITB = C::ITB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zt* As = reinterpret_cast<zt*>(smem_raw);  // [2][BM][AS]
+  zt* Bs = As + 2 * BM * AS;                 // [2][BK][BS]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / C::NWN, wn = warp % C::NWN;
+  const int tilesN = (g.N + BN - 1) / BN;
+  const int m0 = (blockIdx.x / tilesN) * BM, n0 = (blockIdx.x % tilesN) * BN;
+
+  // Fixed per-thread load coordinates: A column (k) and B column (n) are fixed across the
+  // unrolled iterations; A rows / B rows step by NT/BK and NT/BN.
+  const int a_c = tid % BK, a_r0 = tid / BK;
+  const int b_c = tid % BN, b_r0 = tid / BN;
+  constexpr int A_RSTEP = NT / BK;
+  constexpr int B_RSTEP = (NT >= BN) ? NT / BN : 1;
+
+  for (int b = blockIdx.y; b < g.batch; b += gridDim.y) {
+    const zt* Ab = g.A.ptr + (int64_t)b * g.A.bs;
+    const zt* Bb = g.B.ptr + (int64_t)b * g.B.bs;
+    // A row offsets (fixed over k)
+    int64_t a_roff[ITA];
+    bool a_rok[ITA];
+#pragma unroll
+    for (int it = 0; it < ITA; ++it) {
+      const int gi = m0 + a_r0 + it * A_RSTEP;
+      int ri = gi < g.M ? (g.A.rmap ? g.A.rmap[gi] : gi) : -1;
+      a_rok[it] = ri >= 0;
+      a_roff[it] = (int64_t)(ri < 0 ? 0 : ri) * g.A.rs;
+    }
+    // B column offset (fixed over k)
+    int64_t b_coff;
+    bool b_cok;
+    {
+      const int gj = n0 + b_c;
+      int cj = gj < g.N ? zcol(g.B.cmap, gj, g.B.cskip_at, g.B.cskip_len) : -1;
+      b_cok = cj >= 0;
+      b_coff = (int64_t)(cj < 0 ? 0 : cj) * g.B.cs;
+    }
+
+    auto load_stage = [&](int stage, int k0) {
+      {
+        const int gk = k0 + a_c;
+        int ck = gk < g.K ? zcol(g.A.cmap, gk, g.A.cskip_at, g.A.cskip_len) : -1;
+        const int64_t coff = (int64_t)(ck < 0 ? 0 : ck) * g.A.cs;
+#pragma unroll
+        for (int it = 0; it < ITA; ++it) {
+          const bool ok = a_rok[it] && ck >= 0;
+          cp_async16(&As[(stage * BM + a_r0 + it * A_RSTEP) * AS + a_c], ok ? Ab + a_roff[it] + coff : g.A.ptr, ok);
+        }
+      }
+#pragma unroll
+      for (int it = 0; it < ITB; ++it) {
+        const int r = b_r0 + it * B_RSTEP;
+        const int gk = k0 + r;
+        int rk = gk < g.K ? (g.B.rmap ? g.B.rmap[gk] : gk) : -1;
+        const bool ok = b_cok && rk >= 0;
+        cp_async16(&Bs[(stage * BK + r) * BS + b_c], ok ? Bb + (int64_t)rk * g.B.rs + b_coff : g.B.ptr, ok);
+      }
+      cp_async_commit();
+    };
+
+    double accr[TM][TN][2], acci[TM][TN][2];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
+
+    const int nk = (g.K + BK - 1) / BK;
+    if (nk > 0) load_stage(0, 0);
+    for (int kt = 0; kt < nk; ++kt) {
+      if (kt + 1 < nk) {
+        load_stage((kt + 1) & 1, (kt + 1) * BK);
+        cp_async_wait1();
+      } else {
+        cp_async_wait0();
+      }
+      __syncthreads();
+      const zt* Ast = As + (kt & 1) * BM * AS + (wm * C::TM * 8) * AS;
+      const zt* Bst = Bs + (kt & 1) * BK * BS + wn * C::TN * 8;
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        zt af[TM], bf[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) af[i] = Ast[(i * 8 + (lane >> 2)) * AS + kk * 4 + (lane & 3)];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) bf[j] = Bst[(kk * 4 + (lane & 3)) * BS + j * 8 + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const double nai = -af[i].y;
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            dmma(accr[i][j][0], accr[i][j][1], af[i].x, bf[j].x);
+            dmma(accr[i][j][0], accr[i][j][1], nai, bf[j].y);
+            dmma(acci[i][j][0], acci[i][j][1], af[i].x, bf[j].y);
+            dmma(acci[i][j][0], acci[i][j][1], af[i].y, bf[j].x);
+          }
+        }
+      }
+      __syncthreads();
+    }
+
+    // Epilogue: C = alpha * acc + beta * Cin + diag * [i == j]
+    const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + (int64_t)b * g.Cin.bs : nullptr;
+    zt* Cb = g.C.ptr + (int64_t)b * g.C.bs;
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
+      if (gi >= g.M) continue;
+      const int ro = g.C.rmap ? g.C.rmap[gi] : gi;
+      const int ri = Cinb ? (g.Cin.rmap ? g.Cin.rmap[gi] : gi) : -1;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gj = n0 + wn * C::TN * 8 + j * 8 + (lane & 3) * 2 + h;
+          if (gj >= g.N) continue;
+          zt v = zmul(g.alpha, make_double2(accr[i][j][h], acci[i][j][h]));
+          if (Cinb && ri >= 0) {
+            const int cj = zcol(g.Cin.cmap, gj, g.Cin.cskip_at, g.Cin.cskip_len);
+            if (cj >= 0) {
+              const zt cv = Cinb[(int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs];
+              const zt bv = zmul(g.beta, cv);
+              v.x += bv.x;
+              v.y += bv.y;
+            }
+          }
+          if (gi == gj) {
+            v.x += g.diag.x;
+            v.y += g.diag.y;
+          }
+          const int co = zcol(g.C.cmap, gj, g.C.cskip_at, g.C.cskip_len);
+          if (ro >= 0 && co >= 0) Cb[(int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
+        }
+      }
+    }
+  }
+}
+
+template <int BM, int BN, int WM, int WN>
+void launch(const ZGemm& g, cudaStream_t st) {
+  using C = Cfg<BM, BN, WM, WN>;
+  static bool attr_set = false;
+  auto kern = zgemm_kernel<BM, BN, WM, WN>;
+  if (!attr_set) {
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
+  dim3 grid(tiles, g.batch < 65535 ? g.batch : 65535);
+  kern<<<grid, C::NT, C::SMEM, st>>>(g);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+__global__ void zcopy_kernel(const ZCopy c) {
+  const int64_t total = (int64_t)c.batch * c.M * c.N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e % c.N);
+    const int64_t t = e / c.N;
+    const int i = (int)(t % c.M);
+    const int b = (int)(t / c.M);
+    const int ro = c.C.rmap ? c.C.rmap[i] : i;
+    const int co = zcol(c.C.cmap, j, c.C.cskip_at, c.C.cskip_len);
+    if (ro < 0 || co < 0) continue;
+    const int ri = c.A.rmap ? c.A.rmap[i] : i;
+    const int ci = zcol(c.A.cmap, j, c.A.cskip_at, c.A.cskip_len);
+    zt v = make_double2(0.0, 0.0);
+    if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[(int64_t)b * c.A.bs + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
+    c.C.ptr[(int64_t)b * c.C.bs + (int64_t)ro * c.C.rs + (int64_t)co * c.C.cs] = v;
+  }
+}
+
+}  // namespace
+
+void zgemm(const ZGemm& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return;
+  const int64_t t64 = (int64_t)((g.M + 63) / 64) * ((g.N + 63) / 64) * g.batch;
+  if (g.N <= 8)
+    launch<64, 8, 16, 8>(g, st);
+  else if (g.M <= 16 && g.N <= 16)
+    launch<16, 16, 8, 8>(g, st);
+  else if (g.M <= 32 || g.N <= 32 || t64 < 296)
+    launch<32, 32, 16, 16>(g, st);
+  else
+    launch<64, 64, 32, 32>(g, st);
+}
+
+void zcopy(const ZCopy& c, cudaStream_t st) {
+  const int64_t total = (int64_t)c.batch * c.M * c.N;
+  if (total <= 0) return;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  zcopy_kernel<<<blocks, 256, 0, st>>>(c);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}

@@ -1,0 +1,182 @@
+"""Thin Python binding of libhps.so (include/hps.h) — argument marshalling only.
+
+Every step of the build and solve runs in the library's sm_100a kernels.  Arrays may be
+numpy (host) or torch CUDA tensors (device); the library detects which.  There is no CPU
+fallback: if libhps.so is missing or no CUDA device is present, calls raise.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhps.so")
+_lib = None
+
+HPS_ERRORS = {-1: "EINVAL", -2: "ESINGULAR", -3: "ENOMEM", -4: "ECUDA", -5: "ENOTKEPT"}
+
+
+class HpsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{HPS_ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class hps_grid(C.Structure):
+    _fields_ = [("x0", C.c_double), ("x1", C.c_double), ("y0", C.c_double), ("y1", C.c_double),
+                ("nx", C.c_int32), ("ny", C.c_int32)]
+
+
+class hps_c128(C.Structure):
+    _fields_ = [("re", C.c_double), ("im", C.c_double)]
+
+
+class hps_opts(C.Structure):
+    _fields_ = [("keep_root_R", C.c_int32), ("keep_all_R", C.c_int32), ("device", C.c_int32),
+                ("leaf_chunk", C.c_int32)]
+
+
+SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
+           "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
+           "hps_last_flops", "hps_free", "hps_last_error"]
+
+
+def lib():
+    """Load libhps.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        vp, dp, i32, i64 = C.c_void_p, C.c_void_p, C.c_int, C.c_int64
+        L.hps_build.argtypes = [C.POINTER(hps_grid), i32, i32, C.c_double, hps_c128, dp, C.POINTER(hps_opts),
+                                C.POINTER(vp)]
+        L.hps_solve.argtypes = [vp, i32, dp, dp, dp]
+        L.hps_export_R.argtypes = [vp, i64, dp]
+        L.hps_export_leaf.argtypes = [vp, i64, dp, dp]
+        L.hps_box_nb.argtypes = [vp, i64]
+        L.hps_box_nb.restype = i64
+        L.hps_num_boxes.argtypes = [vp]
+        L.hps_num_boxes.restype = i64
+        L.hps_leaf_nodes.argtypes = [C.POINTER(hps_grid), i32, dp, dp]
+        L.hps_root_boundary_nodes.argtypes = [C.POINTER(hps_grid), i32, dp, dp, dp, dp]
+        L.hps_last_time_ms.argtypes = [vp, i32]
+        L.hps_last_time_ms.restype = C.c_double
+        L.hps_last_launches.argtypes = [vp, i32]
+        L.hps_last_launches.restype = i64
+        L.hps_last_flops.argtypes = [vp, i32]
+        L.hps_last_flops.restype = C.c_double
+        L.hps_free.argtypes = [vp]
+        L.hps_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise HpsError(rc, lib().hps_last_error().decode())
+
+
+def _ptr(a, nelem, what):
+    """Device pointer of a torch tensor or host pointer of a numpy array (complex128)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):   # torch tensor
+        import torch
+        if a.dtype != torch.complex128 or not a.is_contiguous():
+            raise TypeError(f"{what}: need a contiguous complex128 tensor")
+        if a.numel() != nelem:
+            raise ValueError(f"{what}: expected {nelem} elements, got {a.numel()}")
+        return a.data_ptr()
+    if not isinstance(a, np.ndarray) or a.dtype != np.complex128 or not a.flags.c_contiguous:
+        raise TypeError(f"{what}: need a C-contiguous numpy complex128 array")
+    if a.size != nelem:
+        raise ValueError(f"{what}: expected {nelem} elements, got {a.size}")
+    return a.ctypes.data
+
+
+def grid(x0, x1, y0, y1, nx, ny):
+    return hps_grid(x0, x1, y0, y1, nx, ny)
+
+
+def leaf_nodes(g, p):
+    n = g.nx * g.ny * p * p
+    X = np.zeros((g.nx * g.ny, p * p))
+    Y = np.zeros_like(X)
+    del n
+    _check(lib().hps_leaf_nodes(C.byref(g), p, X.ctypes.data, Y.ctypes.data))
+    return X, Y
+
+
+def root_boundary_nodes(g, p):
+    n = 2 * (g.nx + g.ny) * (p - 2)
+    X, Y, NX, NY = (np.zeros(n) for _ in range(4))
+    _check(lib().hps_root_boundary_nodes(C.byref(g), p, X.ctypes.data, Y.ctypes.data, NX.ctypes.data,
+                                         NY.ctypes.data))
+    return X, Y, NX, NY
+
+
+class Solver:
+    """hps_build on construction; solve() is hps_solve."""
+
+    def __init__(self, g, p, kappa, eta, c, keep_root_R=True, keep_all_R=False, device=-1, leaf_chunk=0):
+        self.g, self.p = g, p
+        self.nleaf = g.nx * g.ny
+        self.q, self.nt, self.ni = p - 2, p * p - 4, (p - 2) ** 2
+        self.nb_root = 2 * (g.nx + g.ny) * (p - 2)
+        opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk))
+        eta = complex(eta)
+        h = C.c_void_p()
+        cp = _ptr(c, self.nleaf * p * p, "c_samples")
+        self._c = c   # keep alive during the call
+        _check(lib().hps_build(C.byref(g), p, p - 2, float(kappa), hps_c128(eta.real, eta.imag), cp,
+                               C.byref(opts), C.byref(h)))
+        self.h = h
+
+    def solve(self, s, t, u=None):
+        """s: [nrhs][nleaf][q*q] or None, t: [nrhs][nb_root]; returns u [nrhs][nleaf][p*p-4]."""
+        nrhs = int(t.shape[0])
+        if u is None:
+            if hasattr(t, "data_ptr"):
+                import torch
+                u = torch.empty((nrhs, self.nleaf, self.nt), dtype=torch.complex128, device=t.device)
+            else:
+                u = np.zeros((nrhs, self.nleaf, self.nt), complex)
+        _check(lib().hps_solve(self.h, nrhs, _ptr(s, nrhs * self.nleaf * self.ni, "s"),
+                               _ptr(t, nrhs * self.nb_root, "t"), _ptr(u, nrhs * self.nleaf * self.nt, "u")))
+        return u
+
+    def nb(self, box):
+        return lib().hps_box_nb(self.h, box)
+
+    def R(self, box=1):
+        n = self.nb(box)
+        out = np.zeros((n, n), complex)
+        _check(lib().hps_export_R(self.h, box, out.ctypes.data))
+        return out
+
+    def leaf_ops(self, leaf):
+        Psi = np.zeros((self.nt, 4 * self.q), complex)
+        Y = np.zeros((self.nt, self.ni), complex)
+        _check(lib().hps_export_leaf(self.h, leaf, Psi.ctypes.data, Y.ctypes.data))
+        return Psi, Y
+
+    def time_ms(self, which):
+        return lib().hps_last_time_ms(self.h, which)
+
+    def launches(self, which):
+        return lib().hps_last_launches(self.h, which)
+
+    def flops(self, which):
+        return lib().hps_last_flops(self.h, which)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hps_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,63 @@
+"""Host-side checks of the C-ABI (no GPU): the library loads, exports every symbol the
+header declares, validates arguments, and its host geometry matches the oracle's."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import __graft_entry__
+from paper_1812_07167_b200 import hps
+
+HDR = os.path.join(os.path.dirname(os.path.dirname(__file__)), "include", "hps.h")
+
+
+@pytest.fixture(scope="module")
+def L():
+    __graft_entry__.build()
+    return hps.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    decl = set(re.findall(r"\b(hps_[a-z_A-Z0-9]+)\s*\(", open(HDR).read()))
+    assert decl, "no declarations parsed"
+    for name in decl:
+        assert hasattr(L, name), name
+    assert set(hps.SYMBOLS) == decl
+
+
+@pytest.mark.parametrize("nx,ny,p", [(1, 1, 4), (2, 4, 8), (4, 4, 16)])
+def test_geometry_matches_oracle(L, orc, nx, ny, p):
+    g = hps.grid(0.1, 0.9, -0.3, 0.5, nx, ny)
+    X, Y = hps.leaf_nodes(g, p)
+    Xo, Yo = orc.leaf_nodes(0.1, 0.9, -0.3, 0.5, nx, ny, p)
+    assert np.max(np.abs(X - Xo)) < 1e-15 and np.max(np.abs(Y - Yo)) < 1e-15
+    b = hps.root_boundary_nodes(g, p)
+    bo = orc.root_boundary(0.1, 0.9, -0.3, 0.5, nx, ny, p)
+    for u, v in zip(b, bo):
+        assert np.max(np.abs(u - v)) < 1e-15
+
+
+def _build_rc(L, **kw):
+    args = dict(g=hps.grid(0, 1, 0, 1, 2, 2), p=8, q=6, kappa=1.0, eta=hps.hps_c128(1.0, 0.0))
+    args.update(kw)
+    c = np.ones(4 * 64, complex)
+    h = C.c_void_p()
+    rc = L.hps_build(C.byref(args["g"]), args["p"], args["q"], args["kappa"], args["eta"], c.ctypes.data, None,
+                     C.byref(h))
+    return rc, h
+
+
+def test_argument_validation(L):
+    # all rejected before any device work
+    assert _build_rc(L, q=5)[0] == -1
+    assert _build_rc(L, p=3, q=1)[0] == -1
+    assert _build_rc(L, g=hps.grid(0, 1, 0, 1, 3, 2))[0] == -1
+    assert _build_rc(L, g=hps.grid(1, 0, 0, 1, 2, 2))[0] == -1
+    assert _build_rc(L, kappa=-1.0)[0] == -1
+    assert _build_rc(L, eta=hps.hps_c128(0.0, 1.0))[0] == -1
+    rc, h = _build_rc(L, q=5)
+    assert not h.value
+    assert b"q must equal" in L.hps_last_error()
+    L.hps_free(None)   # no-op

@@ -1,0 +1,87 @@
+"""CUDA path (through the C-ABI) vs the CPU oracle, element by element, on seeded inputs.
+
+Tolerance: 1e-9 relative max-norm on R and u (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1812_07167_b200 import hps, inputs
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+def rel(a, b):
+    return np.max(np.abs(a - b)) / np.max(np.abs(b))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import torch
+    assert torch.cuda.is_available()
+    import __graft_entry__
+    __graft_entry__.build()
+
+
+def problem(nx, ny, p, kappa, eta, x1=1.0, y1=1.0, nrhs=2, seed=0):
+    g = hps.grid(0.0, x1, 0.0, y1, nx, ny)
+    X, Y = hps.leaf_nodes(g, p)
+    c = (1 + 0.3 * np.exp(-((X - 0.4 * x1) ** 2 + (Y - 0.6 * y1) ** 2) / 0.05)).astype(complex)
+    rng = np.random.default_rng(seed)
+    ni, nbr = (p - 2) ** 2, 2 * (nx + ny) * (p - 2)
+    s = rng.standard_normal((nrhs, nx * ny, ni)) + 1j * rng.standard_normal((nrhs, nx * ny, ni))
+    t = rng.standard_normal((nrhs, nbr)) + 1j * rng.standard_normal((nrhs, nbr))
+    return g, c, s, t
+
+
+@pytest.mark.parametrize("p", [4, 8, 10, 16])
+def test_leaf_parity(p):
+    g, c, s, t = problem(2, 1, p, 7.0, 7.0 + 1j)
+    S = hps.Solver(g, p, 7.0, 7.0 + 1j, c, keep_all_R=True)
+    for leaf in range(2):
+        Psi, Y = S.leaf_ops(leaf)
+        lo = oracle.leaf(p, 0.5, 1.0, 7.0, 7.0 + 1j, c[leaf])
+        assert rel(Psi, lo["Psi"]) < TOL
+        assert rel(Y, lo["Y"]) < TOL
+
+
+@pytest.mark.parametrize("nx,ny,p", [(1, 1, 8), (2, 1, 8), (1, 2, 6), (4, 4, 8), (8, 4, 6), (4, 8, 10)])
+def test_every_R_and_u(nx, ny, p):
+    kappa, eta = 9.0, 9.0 - 2j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx)
+    S = hps.Solver(g, p, kappa, eta, c, keep_all_R=True)
+    O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c, keep_all_R=True)
+    for box in range(1, 2 * nx * ny):
+        assert rel(S.R(box), O.R(box)) < TOL, box
+    u = S.solve(s, t)
+    uo = O.solve(s, t)
+    assert rel(u, uo) < TOL
+    # s = None path (homogeneous: downward sweep only)
+    u0 = S.solve(None, t)
+    assert rel(u0, O.solve(np.zeros_like(s), t)) < TOL
+
+
+def test_config1_plane_wave():
+    cfg = inputs.CONFIGS[1]
+    g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
+    X, Y = hps.leaf_nodes(g, cfg.p)
+    c, s, t = inputs.make_inputs(cfg, X, Y, *hps.root_boundary_nodes(g, cfg.p))
+    S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
+    u = S.solve(s, t)
+    O = oracle.Oracle(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p, cfg.kappa, cfg.eta, c)
+    assert rel(u, O.solve(s, t)) < TOL
+    assert rel(S.R(1), O.R(1)) < TOL
+    # and the physics: plane wave to the C1 discretisation error (SURVEY: 2.8e-5 at p = 8)
+    Xi, Yi = inputs.interior_of(cfg.p, X), inputs.interior_of(cfg.p, Y)
+    exact_i = inputs.plane_wave(cfg.kappa, cfg.theta, Xi, Yi)
+    assert np.max(np.abs(u[0][:, 4 * (cfg.p - 2):] - exact_i)) < 1e-4
+
+
+def test_torch_device_buffers():
+    import torch
+    g, c, s, t = problem(4, 2, 8, 5.0, 5.0)
+    d = lambda a: torch.from_numpy(a).cuda()
+    S = hps.Solver(g, 8, 5.0, 5.0, d(c))
+    u = S.solve(d(s), d(t)).cpu().numpy()
+    O = oracle.Oracle(0, 1, 0, 1, 4, 2, 8, 5.0, 5.0, c)
+    assert rel(u, O.solve(s, t)) < TOL
