@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark: one step = the whole HPS hot path on one batch of synthetic input —
+precomputation (batched leaf build + merge tree, Algorithm 1) followed by the solve sweeps
+(Algorithm 2) — through the C-ABI of libhps.so.
+
+Default workload: BASELINE.json configs[1] (C2: unit square, 32x32 leaves, p = 16,
+kappa = eta = 40 pi, 1 RHS).  `--config 3` runs C3 (128x128 leaves, 64 RHS).
+
+Metric (BASELINE.json): "HPS precompute sec & DOF/s; solve ms per RHS; FP64-TC % of peak;
+HBM GB/s".  `value` is DOF/s of one full step (DOF = unique discretisation nodes, reading
+Q16; step time = device time of build + solve on the library stream), summed over ranks;
+the extra keys carry the build seconds, build DOF/s and solve ms per RHS.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl hps|reference]
+Under torchrun (N > 1) every rank builds and solves its own replica of the workload
+(weak scaling, no data-path collective).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1812_07167_b200 import inputs  # noqa: E402
+
+METRIC = "HPS precompute sec & DOF/s; solve ms per RHS; FP64-TC % of peak; HBM GB/s"
+
+
+def load_json(path, default=None):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return default
+
+
+def fp64_peak():
+    """Measured FP64 tensor (DMMA m8n8k4) peak of this pool's B200 (tools/fp64_peaks.cu)."""
+    pk = load_json(os.path.join(ROOT, "bench", "peaks_fp64.json"), {})
+    return pk.get("dmma_m8n8k4_tflops", 37.16), "bench/peaks_fp64.json (tools/fp64_peaks.cu, DMMA.8x8x4 loop)"
+
+
+def hbm_peak():
+    mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {})
+    if "hbm_gbs" in mp:
+        return mp["hbm_gbs"], "MEASURED_PEAKS.json hbm_gbs"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except Exception:
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def setup(cfg, hps):
+    g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
+    X, Y = hps.leaf_nodes(g, cfg.p)
+    c, s, t = inputs.make_inputs(cfg, X, Y, *hps.root_boundary_nodes(g, cfg.p))
+    return g, np.ascontiguousarray(c), np.ascontiguousarray(s), np.ascontiguousarray(t)
+
+
+def flush_l2(torch, buf):
+    buf.add_(1.0)   # 256 MiB write > 126 MB L2
+
+
+def run_hps(args, rank, world, dist):
+    import torch
+    from paper_1812_07167_b200 import hps
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    cfg = inputs.CONFIGS[args.config]
+    nrhs = args.nrhs or cfg.nrhs
+    g, c, s, t = setup(cfg, hps)
+    s, t = s[:nrhs], t[:nrhs]
+    dev = f"cuda:{local}"
+    c_d = torch.from_numpy(c).to(dev)
+    s_d = torch.from_numpy(np.ascontiguousarray(s)).to(dev)
+    t_d = torch.from_numpy(np.ascontiguousarray(t)).to(dev)
+    u_d = torch.empty((nrhs, cfg.nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128, device=dev)
+    l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+
+    def step(profile=False):
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=True, device=local, profile=profile)
+        S.solve(s_d, t_d, u_d)
+        rec = dict(build_ms=S.time_ms(0), leaf_ms=S.time_ms(1), merge_ms=S.time_ms(2), solve_ms=S.time_ms(3),
+                   up_ms=S.time_ms(4), down_ms=S.time_ms(5), launches=S.launches(0) + S.launches(1),
+                   build_flops=S.flops(0), solve_flops=S.flops(1), kstats=S.kernel_stats())
+        S.close()
+        return rec
+
+    for _ in range(args.warmup):
+        flush_l2(torch, l2buf)
+        step()
+    torch.cuda.synchronize()
+    recs = []
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush_l2(torch, l2buf)
+            torch.cuda.synchronize()
+            recs.append(step(profile=True))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        wall = time.perf_counter() - w0
+    clocks = clk.summary()
+    step_ms = statistics.mean(r["build_ms"] + r["solve_ms"] for r in recs)
+    build_ms = statistics.mean(r["build_ms"] for r in recs)
+    solve_ms = statistics.mean(r["solve_ms"] for r in recs)
+    if world > 1:
+        tt = torch.tensor([step_ms, build_ms, solve_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms, build_ms, solve_ms = tt.tolist()
+
+    # ---- end-to-end through the public API with pinned HOST buffers ----
+    c_h = torch.from_numpy(c).pin_memory()
+    s_h = torch.from_numpy(np.ascontiguousarray(s)).pin_memory()
+    t_h = torch.from_numpy(np.ascontiguousarray(t)).pin_memory()
+    u_h = torch.empty((nrhs, cfg.nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128).pin_memory()
+    e2e = []
+    for k in range(args.warmup + args.steps):
+        flush_l2(torch, l2buf)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = time.perf_counter()
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_h, keep_root_R=True, device=local)
+        S.solve(s_h, t_h, u_h)
+        _ = complex(u_h[0, 0, 0])        # result read on the host
+        e1 = time.perf_counter()
+        S.close()
+        if k >= args.warmup:
+            e2e.append(e1 - e0)
+    e2e_s = statistics.mean(e2e)
+    if world > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = tt.item()
+
+    if rank != 0:
+        return None
+    dof = cfg.n_unique
+    value = world * dof / (step_ms / 1e3)
+    # ---- roofline of the dominant kernel class (device time from CUDA events) ----
+    agg = {}
+    for r in recs:
+        for k, v in r["kstats"].items():
+            a = agg.setdefault(k, dict(launches=0, ms=0.0, flops=0.0, bytes=0.0))
+            for f in a:
+                a[f] += v[f]
+    dom = max(agg, key=lambda k: agg[k]["ms"])
+    A = agg[dom]
+    traffic_tab = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json"), {})
+    traffic = traffic_tab.get(f"C{args.config}", {}).get(dom)
+    if A["flops"] > 0:
+        peak, src = fp64_peak()
+        achieved = A["flops"] / (A["ms"] / 1e3) / 1e12
+        roof = dict(bound="tensor", achieved=round(achieved, 3), peak=peak, unit="TFLOP/s",
+                    frac=round(achieved / peak, 4), traffic=traffic, kernel=dom, peak_source=src,
+                    launches=A["launches"] // len(recs), avg_launch_us=round(1e3 * A["ms"] / A["launches"], 2),
+                    share_of_step=round(A["ms"] / len(recs) / step_ms, 3))
+    else:
+        peak, src = hbm_peak()
+        achieved = A["bytes"] / (A["ms"] / 1e3) / 1e9
+        roof = dict(bound="hbm", achieved=round(achieved, 1), peak=peak, unit="GB/s",
+                    frac=round(achieved / peak, 4), traffic=traffic, kernel=dom, peak_source=src,
+                    launches=A["launches"] // len(recs), share_of_step=round(A["ms"] / len(recs) / step_ms, 3))
+    per_class = {k: dict(launches=v["launches"] // len(recs), ms=round(v["ms"] / len(recs), 3),
+                         tflops=round(v["flops"] / max(v["ms"], 1e-9) / 1e9, 3) if v["flops"] else None,
+                         gbs=round(v["bytes"] / max(v["ms"], 1e-9) / 1e6, 1))
+                 for k, v in agg.items()}
+    out = {
+        "metric": METRIC, "value": round(value, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
+                   "dof": dof, "kappa": round(cfg.kappa, 4), "keep_root_R": True,
+                   "l2": "256 MiB buffer written between steps; stored operators > L2",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "build_s": round(build_ms / 1e3, 6), "build_dof_per_s": round(world * dof / (build_ms / 1e3), 1),
+        "solve_ms_per_rhs": round(solve_ms / nrhs, 4),
+        "build_tflops": round(statistics.mean(r["build_flops"] for r in recs) / (build_ms / 1e3) / 1e12, 3),
+        "phase_ms": {k: round(statistics.mean(r[k] for r in recs), 3)
+                     for k in ["leaf_ms", "merge_ms", "up_ms", "down_ms"]},
+        "kernel_classes": per_class,
+        "roofline": roof,
+        "clocks": clocks,
+        "wall_s_timed_region": round(wall, 3),
+        "gpu_launches": int(sum(r["launches"] for r in recs)),
+        "e2e": {"value": round(world * dof / e2e_s, 1), "unit": "DOF/s",
+                "h2d_bytes_per_step": int(c.nbytes + s.nbytes + t.nbytes),
+                "d2h_bytes_per_step": int(nrhs * cfg.nleaf * (cfg.p * cfg.p - 4) * 16), "s_per_step": round(e2e_s, 4)},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, c, s, t, args)
+    return out
+
+
+def oracle_run(cfg, c, s, t):
+    """The oracle as it stands (Algorithm 1 + 2 on host cores, OpenMP over boxes)."""
+    import oracle
+    t0 = time.perf_counter()
+    O = oracle.Oracle(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p, cfg.kappa, cfg.eta, c)
+    t1 = time.perf_counter()
+    O.solve(s, t)
+    t2 = time.perf_counter()
+    O.close()
+    return t1 - t0, t2 - t1
+
+
+def cpu_cores():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def cpu_baseline(cfg, c, s, t, args):
+    nrhs = s.shape[0]
+    if cfg.nleaf <= 32 * 32:
+        tb, ts = oracle_run(cfg, c, s, t)
+        return {"value": round(cfg.n_unique / (tb + ts), 1), "unit": "DOF/s", "cores": cpu_cores(), "kind": "oracle",
+                "sample": f"full workload ({cfg.nx}x{cfg.ny} leaves, {nrhs} RHS): oracle build {tb:.2f} s + solve "
+                          f"{ts:.2f} s on {cpu_cores()} threads",
+                "build_s": round(tb, 3), "solve_ms_per_rhs": round(1e3 * ts / nrhs, 3)}
+    # larger configs: a 32x32-leaf corner of the same problem, extrapolated by the method's flop count
+    sub = inputs.Config(**{**cfg.__dict__, "nx": 32, "ny": 32, "x1": cfg.x0 + (cfg.x1 - cfg.x0) * 32 / cfg.nx,
+                           "y1": cfg.y0 + (cfg.y1 - cfg.y0) * 32 / cfg.ny, "nrhs": 1})
+    from paper_1812_07167_b200 import hps
+    g, cs, ss, ts_ = setup(sub, hps)
+    tb, tsv = oracle_run(sub, cs, ss[:1], ts_[:1])
+    f_full, f_sub = flop_model(cfg), flop_model(sub)
+    est = tb * f_full / f_sub + tsv * nrhs * (cfg.nleaf / sub.nleaf)
+    return {"value": round(cfg.n_unique / est, 1), "unit": "DOF/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"32x32-leaf corner, 1 RHS, build {tb:.2f} s + solve {tsv:.2f} s; extrapolated by the "
+                      f"method's flop count to {cfg.nx}x{cfg.ny} leaves, {nrhs} RHS"}
+
+
+def flop_model(cfg):
+    """Algorithmic build flops (leaf 8 nt^3 + merges incl. root R), as counted by libhps."""
+    q, p = cfg.p - 2, cfg.p
+    nt = p * p - 4
+    fl = 8.0 * nt ** 3 * cfg.nleaf
+    a, b = cfg.nx, cfg.ny
+    dims = [(a, b)]
+    while (a, b) != (1, 1):
+        if a >= b:
+            a //= 2
+        else:
+            b //= 2
+        dims.append((a, b))
+    for d in range(len(dims) - 1):
+        pa, pb = dims[d]
+        ca, cb = dims[d + 1]
+        n3 = (cb if pa >= pb else ca) * q
+        nbc = 2 * (ca + cb) * q
+        n1 = nbc - n3
+        ntau = 2 * n1
+        fl += 8.0 * 2 ** d * (2 * n3 ** 3 + n3 * n3 * n1 + 2 * n3 * n3 * ntau + ntau * ntau * n3)
+    return fl
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return None
+    import oracle
+    oracle.build()
+    from paper_1812_07167_b200 import hps
+    cfg = inputs.CONFIGS[args.config]
+    nrhs = args.nrhs or cfg.nrhs
+    # geometry from the oracle itself (no CUDA needed on this arm)
+    X, Y = oracle.leaf_nodes(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p)
+    Xb = oracle.root_boundary(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p)
+    c, s, t = inputs.make_inputs(cfg, X, Y, *Xb, nrhs=nrhs)
+    del hps
+    small = inputs.CONFIGS[1]
+    Xs, Ys = oracle.leaf_nodes(small.x0, small.x1, small.y0, small.y1, small.nx, small.ny, small.p)
+    cs, ss, tss = inputs.make_inputs(small, Xs, Ys, *oracle.root_boundary(small.x0, small.x1, small.y0, small.y1,
+                                                                          small.nx, small.ny, small.p))
+    for _ in range(args.warmup):      # warm-up on the small case (bounded run time)
+        oracle_run(small, cs, ss, tss)
+    times = []
+    sample = "full workload"
+    for _ in range(args.steps):
+        if cfg.nleaf <= 32 * 32:
+            tb, ts = oracle_run(cfg, c, s, t)
+            times.append(tb + ts)
+        else:
+            cb = cpu_baseline(cfg, c, s, t, args)
+            times.append(cfg.n_unique / cb["value"])
+            sample = cb["sample"]
+    step_s = statistics.mean(times)
+    val = cfg.n_unique / step_s
+    return {"metric": METRIC, "value": round(val, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * step_s, 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
+                       "dof": cfg.n_unique},
+            "cpu_baseline": {"value": round(val, 1), "unit": "DOF/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": round(val, 1), "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--nrhs", type=int, default=0)
+    ap.add_argument("--impl", default="hps", choices=["hps", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+            dist.init_process_group("nccl")
+        out = run_hps(args, rank, world, dist)
+        if dist is not None:
+            dist.destroy_process_group()
+    if out is not None and rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

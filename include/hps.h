@@ -68,6 +68,10 @@ typedef struct {
   int32_t keep_all_R;   /* 1: keep every box's R for hps_export_R (debug / parity; default 0) */
   int32_t device;       /* CUDA device ordinal (default: current device) */
   int32_t leaf_chunk;   /* leaves factored per batch (0 = automatic) */
+  int32_t profile;      /* 1: time every kernel with CUDA events on the library stream (see
+                           hps_kernel_stats); 0: counters only (default) */
+  int32_t leaf_mode;    /* 0 (default): B^{-1} through the interior Schur complement;
+                           1: Gauss-Jordan on the full n^tau x n^tau matrix B */
 } hps_opts;
 
 /* Precomputation stage (Algorithm 1).
@@ -119,6 +123,15 @@ double hps_last_time_ms(const hps_handle* h, int which);
  * algorithmic FLOPs (8 real flops per complex multiply-add). which: 0 build, 1 solve. */
 int64_t hps_last_launches(const hps_handle* h, int which);
 double hps_last_flops(const hps_handle* h, int which);
+
+/* Per-kernel-class statistics accumulated since the handle was built (or hps_reset_stats):
+ * class 0 ZGEMM (DMMA), 1 Gauss-Jordan panel, 2 Gauss-Jordan small (in shared memory),
+ * 3 Gauss-Jordan swaps/permutation, 4 leaf assembly, 5 gathers / layout.  ms is the sum of
+ * CUDA-event durations around each launch (only while profiling is on); flops and bytes are
+ * ALGORITHMIC (8 flops per complex multiply-add; operand bytes read + written once). */
+int hps_set_profiling(hps_handle* h, int on);
+int hps_kernel_stats(const hps_handle* h, int cls, int64_t* launches, double* ms, double* flops, double* bytes);
+int hps_reset_stats(hps_handle* h);
 
 void hps_free(hps_handle* h);
 const char* hps_last_error(void);

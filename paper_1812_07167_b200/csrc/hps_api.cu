@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -25,38 +26,92 @@ thread_local int64_t* g_launch_counter = nullptr;
 static thread_local std::string g_err_msg;
 void hps_set_error(const std::string& m) { g_err_msg = m; }
 
+// ---------------------------------------------------------------------------
+// Per-kernel-class statistics (see hps_internal.cuh)
+// ---------------------------------------------------------------------------
+thread_local std::vector<cudaEvent_t> g_ev_pool;  // reused across handles (one device per process)
+
+struct Prof {
+  bool timing = false;
+  KStats stats;
+  std::vector<cudaEvent_t>& pool = g_ev_pool;
+  size_t used = 0;
+  struct Rec {
+    int cls;
+    size_t e0, e1;
+  };
+  std::vector<Rec> recs;
+  std::vector<std::pair<int, size_t>> open;
+  cudaEvent_t ev() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      HPS_CUDA_CHECK(cudaEventCreate(&e));
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void finalize() {  // caller has synchronised the stream
+    for (const Rec& r : recs) {
+      float ms = 0;
+      if (cudaEventElapsedTime(&ms, pool[r.e0], pool[r.e1]) == cudaSuccess) stats.ms[r.cls] += ms;
+    }
+    recs.clear();
+    used = 0;
+  }
+};
+thread_local Prof* g_prof = nullptr;
+
+void prof_begin(int cls, double flops, double bytes, cudaStream_t st) {
+  Prof* P = g_prof;
+  if (!P) return;
+  P->stats.launches[cls] += 1;
+  P->stats.flops[cls] += flops;
+  P->stats.bytes[cls] += bytes;
+  if (P->timing) {
+    const size_t i = P->used;
+    HPS_CUDA_CHECK(cudaEventRecord(P->ev(), st));
+    P->open.push_back({cls, i});
+  }
+}
+
+void prof_end(cudaStream_t st) {
+  Prof* P = g_prof;
+  if (!P || !P->timing || P->open.empty()) return;
+  const size_t i = P->used;
+  cudaEventRecord(P->ev(), st);
+  P->recs.push_back({P->open.back().first, P->open.back().second, i});
+  P->open.pop_back();
+}
+
 namespace {
 
 // ---------------------------------------------------------------------------
 // Device buffer (RAII)
 // ---------------------------------------------------------------------------
+// Device memory comes from the stream-ordered pool of the device (cudaMallocAsync on the
+// library stream, retained across handles: release threshold = max), so temporaries of one
+// level are freed without synchronising and re-used by the next build without a driver call.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t st = nullptr;
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
-  DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) {
-      release();
-      p = o.p;
-      bytes = o.bytes;
-      o.p = nullptr;
-      o.bytes = 0;
-    }
-    return *this;
-  }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; o.bytes = 0; }
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, st);
     p = nullptr;
     bytes = 0;
   }
   void alloc(size_t n) {
     release();
     if (n == 0) return;
-    cudaError_t e = cudaMalloc(&p, n);
+    st = g_alloc_stream;
+    cudaError_t e = cudaMallocAsync(&p, n, st);
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
@@ -116,6 +171,16 @@ void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
   if (!v.empty()) HPS_CUDA_CHECK(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
 }
 
+void retain_pool(int dev) {
+  static thread_local int done = -1;
+  if (done == dev) return;
+  cudaMemPool_t pool;
+  HPS_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t thr = ~0ull;
+  HPS_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done = dev;
+}
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes a;
@@ -138,6 +203,7 @@ struct hps_handle {
   zt eta{};
   int L = 0, nleaf = 0;
   bool keep_root_R = true, keep_all_R = false;
+  int leaf_mode = 0;  // 0: Schur complement on the interior (default), 1: invert the full B
   std::vector<Depth> depth;
   std::vector<int> leaf_nat_h, nat_to_heap_h;
   DevBuf leaf_nat, nat_to_heap, zero_idx;
@@ -149,7 +215,20 @@ struct hps_handle {
   int64_t launches[2] = {0, 0};
   double flops[2] = {0, 0};
   cudaEvent_t ev[6] = {};
+  Prof prof;
   ~hps_handle() {
+    // return every buffer to the pool on our stream, then retire the stream
+    leaf_nat.release();
+    nat_to_heap.release();
+    zero_idx.release();
+    store.release();
+    for (auto& m : lev) {
+      m.maps.release();
+      m.ops.release();
+    }
+    for (auto& r : R) r.release();
+    info.release();
+    if (st) cudaStreamSynchronize(st);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (st) cudaStreamDestroy(st);
@@ -299,12 +378,64 @@ ZOut out(zt* p, int64_t rs, int64_t bs, const int* rmap = nullptr, const int* cm
   return o;
 }
 
-void check_info(hps_handle& H, const char* what) {
-  int info = 0;
-  HPS_CUDA_CHECK(cudaMemcpyAsync(&info, H.info.p, sizeof(int), cudaMemcpyDeviceToHost, H.st));
+// info[0]: leaves, info[1 + d]: merges at depth d (1 + batch entry of the first zero pivot)
+void check_info(hps_handle& H) {
+  std::vector<int> info(H.L + 1, 0);
+  HPS_CUDA_CHECK(cudaMemcpyAsync(info.data(), H.info.p, sizeof(int) * info.size(), cudaMemcpyDeviceToHost, H.st));
   HPS_CUDA_CHECK(cudaStreamSynchronize(H.st));
-  if (info) throw HpsError{HPS_ESINGULAR, std::string("zero pivot while inverting ") + what + " (batch entry " +
-                                              std::to_string(info - 1) + ")"};
+  if (info[0])
+    throw HpsError{HPS_ESINGULAR, "zero pivot while inverting the leaf matrix of heap leaf " + std::to_string(info[0] - 1)};
+  for (int d = 0; d < H.L; ++d)
+    if (info[1 + d])
+      throw HpsError{HPS_ESINGULAR, "zero pivot while inverting W of merge " + std::to_string(info[1 + d] - 1) +
+                                        " at depth " + std::to_string(d)};
+}
+
+// Line operators of the Schur-complement leaf (leaf.cu): for the x-lines (W, E closure) and
+// y-lines (S, N closure), G = inverse of the 2x2 impedance closure, F_I its interior coupling,
+// Ub = [D2(i,0) D2(i,p-1)] G, V = G F_I, L = -D2_II + Ub F_I.  Layout matches leaf.cu.
+std::vector<zt> schur_consts(int p, double hx, double hy, zt eta_z, const std::vector<double>& dm) {
+  typedef std::complex<double> C;
+  const int q = p - 2;
+  const C ieta = C(0, 1) * C(eta_z.x, eta_z.y);
+  std::vector<C> L[2], Ub[2], V[2], Gi[2];
+  for (int ax = 0; ax < 2; ++ax) {
+    const double* D1 = dm.data() + (size_t)ax * p * p;        // Dx or Dy (scaled)
+    const double* D2 = dm.data() + (size_t)(2 + ax) * p * p;  // Dxx or Dyy
+    // closure rows: [first node (W or S): -D(0,:) + i eta e_0 ; last node (E or N): +D(p-1,:) + i eta e_{p-1}]
+    C g00 = -D1[0] + ieta, g01 = -D1[p - 1], g10 = D1[(size_t)(p - 1) * p], g11 = D1[(size_t)(p - 1) * p + p - 1] + ieta;
+    const C det = g00 * g11 - g01 * g10;
+    Gi[ax] = {g11 / det, -g01 / det, -g10 / det, g00 / det};
+    std::vector<C> FI(2 * q);
+    for (int j = 0; j < q; ++j) {
+      FI[j] = -D1[j + 1];
+      FI[q + j] = D1[(size_t)(p - 1) * p + j + 1];
+    }
+    Ub[ax].assign(2 * q, 0.0);
+    for (int i = 0; i < q; ++i)
+      for (int sd = 0; sd < 2; ++sd)
+        Ub[ax][i * 2 + sd] = D2[(size_t)(i + 1) * p] * Gi[ax][0 * 2 + sd] + D2[(size_t)(i + 1) * p + p - 1] * Gi[ax][1 * 2 + sd];
+    V[ax].assign(2 * q, 0.0);
+    for (int sd = 0; sd < 2; ++sd)
+      for (int j = 0; j < q; ++j) V[ax][sd * q + j] = Gi[ax][sd * 2 + 0] * FI[j] + Gi[ax][sd * 2 + 1] * FI[q + j];
+    L[ax].assign((size_t)q * q, 0.0);
+    for (int i = 0; i < q; ++i)
+      for (int j = 0; j < q; ++j)
+        L[ax][(size_t)i * q + j] = -D2[(size_t)(i + 1) * p + j + 1] + Ub[ax][i * 2 + 0] * FI[j] + Ub[ax][i * 2 + 1] * FI[q + j];
+  }
+  std::vector<zt> out;
+  auto put = [&](const std::vector<C>& v) {
+    for (const C& z : v) out.push_back(make_double2(z.real(), z.imag()));
+  };
+  put(L[0]);
+  put(L[1]);
+  put(Ub[0]);
+  put(Ub[1]);
+  put(V[0]);
+  put(V[1]);
+  put(Gi[0]);
+  put(Gi[1]);
+  return out;
 }
 
 // ---------------------------------------------------------------------------
@@ -347,24 +478,39 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
 
   const size_t mat = (size_t)nt * nt;
   H.store.alloc(sizeof(zt) * mat * nleaf);
-  int chunk = chunk_opt > 0 ? chunk_opt : (int)std::max<size_t>(1, ((size_t)1 << 30) / (mat * sizeof(zt)));
+  const bool schur = H.leaf_mode == 0;
+  const int ninv = schur ? H.ni : nt;  // matrix inverted per leaf
+  const size_t wmat = (size_t)ninv * ninv;
+  int chunk = chunk_opt > 0 ? chunk_opt : (int)std::max<size_t>(1, ((size_t)1 << 30) / (wmat * sizeof(zt)));
   chunk = std::min(chunk, nleaf);
-  DevBuf work, ws;
-  work.alloc(sizeof(zt) * mat * chunk);
-  ws.alloc(std::max<size_t>(zgj_workspace_bytes(nt, chunk), 16));
+  DevBuf work, ws, dK;
+  work.alloc(sizeof(zt) * wmat * chunk);
+  ws.alloc(std::max<size_t>(zgj_workspace_bytes(ninv, chunk), 16));
+  if (schur) upload(dK, schur_consts(p, hx, hy, H.eta, dm), H.st);
   for (int l0 = 0; l0 < nleaf; l0 += chunk) {
     const int nc = std::min(chunk, nleaf - l0);
-    launch_leaf_assemble(work.as<zt>(), (int64_t)mat, l0, nc, H.leaf_nat.as<int>(), c_dev, p, ddm.as<double>(),
-                         dpos.as<int>(), dnode.as<int>(), H.kappa * H.kappa, H.eta, H.st);
-    zgj_invert(work.as<zt>(), nt, (int64_t)mat, H.store.as<zt>() + (size_t)l0 * mat, nt, (int64_t)mat, nt, nc, ws.p,
-               H.info.as<int>(), H.st, nullptr);
+    if (schur) {
+      launch_leaf_schur_assemble(work.as<zt>(), (int64_t)wmat, l0, nc, H.leaf_nat.as<int>(), c_dev, p, dK.as<zt>(),
+                                 H.kappa * H.kappa, H.st);
+      zgj_invert(work.as<zt>(), ninv, (int64_t)wmat, H.store.as<zt>() + (size_t)l0 * mat + (size_t)nb * nt + nb, nt,
+                 (int64_t)mat, ninv, nc, ws.p, H.info.as<int>(), H.st, nullptr);
+      launch_leaf_schur_finish(H.store.as<zt>(), (int64_t)mat, l0, nc, p, dK.as<zt>(), H.st);
+    } else {
+      launch_leaf_assemble(work.as<zt>(), (int64_t)mat, l0, nc, H.leaf_nat.as<int>(), c_dev, p, ddm.as<double>(),
+                           dpos.as<int>(), dnode.as<int>(), H.kappa * H.kappa, H.eta, H.st);
+      zgj_invert(work.as<zt>(), nt, (int64_t)mat, H.store.as<zt>() + (size_t)l0 * mat, nt, (int64_t)mat, nt, nc,
+                 ws.p, H.info.as<int>(), H.st, nullptr);
+    }
   }
-  H.flops[0] += 8.0 * (double)nt * nt * nt * nleaf;
+  if (schur) {
+    const double q = p - 2, ni = H.ni;
+    H.flops[0] += nleaf * (8.0 * ni * ni * ni + 8.0 * q * (2.0 * ni * nb + (double)nb * nb));
+  } else {
+    H.flops[0] += 8.0 * (double)nt * nt * nt * nleaf;
+  }
   // leaf R (PAPER.md:398-402 via R = I - 2 i eta Psi_b)
   H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
   launch_leaf_R(H.store.as<zt>(), (int64_t)mat, H.R[H.L].as<zt>(), nleaf, nt, nb, H.eta, H.st);
-  // keep the workspaces alive until the stream drains (they are freed on scope exit)
-  HPS_CUDA_CHECK(cudaStreamSynchronize(H.st));
 }
 
 void build_merge(hps_handle& H, int d) {
@@ -413,7 +559,7 @@ void build_merge(hps_handle& H, int d) {
   }
   // (c) W^{-1}
   ws.alloc(std::max<size_t>(zgj_workspace_bytes(n3, np), 16));
-  zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>(), st, nullptr);
+  zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>() + 1 + d, st, nullptr);
   // (d) X = [R33b R31a | -R32b] ; Phi^a = W^{-1} X  (line 8)
   const int64_t sx = (int64_t)n3 * nt;
   X.alloc(sizeof(zt) * sx * np);
@@ -482,8 +628,7 @@ void build_merge(hps_handle& H, int d) {
     fl += 8.0 * np * (double)nt * nt * n3;
   }
   H.flops[0] += fl;
-  HPS_CUDA_CHECK(cudaStreamSynchronize(st));  // temporaries die at scope exit
-  if (!H.keep_all_R) H.R[d + 1].release();    // Algorithm 1 line 14
+  if (!H.keep_all_R) H.R[d + 1].release();    // Algorithm 1 line 14 (stream-ordered free)
 }
 
 // ---------------------------------------------------------------------------
@@ -580,7 +725,6 @@ void solve_impl(hps_handle& H, int nrhs, const zt* s_dev, const zt* t_dev, zt* u
         zgemm(g, st);
         fl += 8.0 * np * (double)(n1 + n2) * n3 * R;
       }
-      HPS_CUDA_CHECK(cudaStreamSynchronize(st));
       h[d + 1].release();
     }
   }
@@ -624,7 +768,6 @@ void solve_impl(hps_handle& H, int nrhs, const zt* s_dev, const zt* t_dev, zt* u
     c.A = op(t[d].as<zt>(), R, pb, M.pp + n1);
     c.C = out(tb, R, cb, M.I2b);
     zcopy(c, st);
-    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
     t[d].release();
     if (has_s) {
       TTa[d].release();
@@ -667,11 +810,21 @@ int fail(const HpsError& e) {
 
 struct LaunchScope {
   int64_t* prev;
-  explicit LaunchScope(int64_t* c) : prev(g_launch_counter) {
+  Prof* prev_prof;
+  Prof* mine;
+  LaunchScope(int64_t* c, Prof* p) : prev(g_launch_counter), prev_prof(g_prof), mine(p) {
     *c = 0;
     g_launch_counter = c;
+    g_prof = p;
   }
-  ~LaunchScope() { g_launch_counter = prev; }
+  ~LaunchScope() {
+    if (mine && mine->timing) {
+      cudaDeviceSynchronize();
+      mine->finalize();
+    }
+    g_launch_counter = prev;
+    g_prof = prev_prof;
+  }
 };
 
 }  // namespace
@@ -767,6 +920,8 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     if (opt && opt->device >= 0) HPS_CUDA_CHECK(cudaSetDevice(opt->device));
     HPS_CUDA_CHECK(cudaGetDevice(&H->dev));
     HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H->st, cudaStreamNonBlocking));
+    retain_pool(H->dev);
+    g_alloc_stream = H->st;
     for (auto& e : H->ev) HPS_CUDA_CHECK(cudaEventCreate(&e));
     H->g = *g;
     H->p = p;
@@ -778,14 +933,16 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     H->eta = make_double2(eta.re, eta.im);
     H->keep_root_R = opt ? opt->keep_root_R != 0 : true;
     H->keep_all_R = opt ? opt->keep_all_R != 0 : false;
-    LaunchScope ls(&H->launches[0]);
+    H->leaf_mode = opt ? opt->leaf_mode : 0;
+    H->prof.timing = opt ? opt->profile != 0 : false;
+    LaunchScope ls(&H->launches[0], &H->prof);
     H->flops[0] = 0;
     plan_tree(*H);
     upload(H->leaf_nat, H->leaf_nat_h, H->st);
     upload(H->nat_to_heap, H->nat_to_heap_h, H->st);
     upload(H->zero_idx, std::vector<int>{0}, H->st);
-    H->info.alloc(sizeof(int));
-    HPS_CUDA_CHECK(cudaMemsetAsync(H->info.p, 0, sizeof(int), H->st));
+    H->info.alloc(sizeof(int) * (H->L + 1));
+    HPS_CUDA_CHECK(cudaMemsetAsync(H->info.p, 0, sizeof(int) * (H->L + 1), H->st));
     H->R.resize(H->L + 1);
     H->lev.resize(H->L);
     for (int d = 0; d < H->L; ++d) plan_level(*H, d, H->lev[d]);
@@ -801,13 +958,10 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     HPS_CUDA_CHECK(cudaEventRecord(H->ev[0], H->st));
     build_leaves(*H, c_dev, opt ? opt->leaf_chunk : 0);
     HPS_CUDA_CHECK(cudaEventRecord(H->ev[1], H->st));
-    check_info(*H, "a leaf matrix B");
-    for (int d = H->L - 1; d >= 0; --d) {
-      build_merge(*H, d);
-      check_info(*H, ("W at merge depth " + std::to_string(d)).c_str());
-    }
+    for (int d = H->L - 1; d >= 0; --d) build_merge(*H, d);
     HPS_CUDA_CHECK(cudaEventRecord(H->ev[2], H->st));
     HPS_CUDA_CHECK(cudaEventSynchronize(H->ev[2]));
+    check_info(*H);
     float a = 0, b = 0;
     cudaEventElapsedTime(&a, H->ev[0], H->ev[1]);
     cudaEventElapsedTime(&b, H->ev[1], H->ev[2]);
@@ -831,7 +985,8 @@ int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps
   if (nrhs == 0) return HPS_OK;
   try {
     HPS_CUDA_CHECK(cudaSetDevice(h->dev));
-    LaunchScope ls(&h->launches[1]);
+    g_alloc_stream = h->st;
+    LaunchScope ls(&h->launches[1], &h->prof);
     const size_t sb = sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni;
     const size_t tb = sizeof(zt) * (size_t)nrhs * h->depth[0].nb;
     const size_t ub = sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt;
@@ -932,6 +1087,27 @@ int64_t hps_last_launches(const hps_handle* h, int which) {
 double hps_last_flops(const hps_handle* h, int which) {
   if (!h || which < 0 || which > 1) return -1;
   return h->flops[which];
+}
+
+int hps_set_profiling(hps_handle* h, int on) {
+  if (!h) return HPS_EINVAL;
+  h->prof.timing = on != 0;
+  return HPS_OK;
+}
+
+int hps_kernel_stats(const hps_handle* h, int cls, int64_t* launches, double* ms, double* flops, double* bytes) {
+  if (!h || cls < 0 || cls >= K_NCLASS) return HPS_EINVAL;
+  if (launches) *launches = h->prof.stats.launches[cls];
+  if (ms) *ms = h->prof.stats.ms[cls];
+  if (flops) *flops = h->prof.stats.flops[cls];
+  if (bytes) *bytes = h->prof.stats.bytes[cls];
+  return HPS_OK;
+}
+
+int hps_reset_stats(hps_handle* h) {
+  if (!h) return HPS_EINVAL;
+  h->prof.stats = KStats();
+  return HPS_OK;
 }
 
 void hps_free(hps_handle* h) { delete h; }

@@ -89,3 +89,27 @@ extern thread_local int64_t* g_launch_counter;
 inline void count_launch(int k = 1) {
   if (g_launch_counter) *g_launch_counter += k;
 }
+
+// ---------------------------------------------------------------------------
+// Per-kernel-class accounting (hps_kernel_stats): launches, algorithmic FLOPs / bytes, and —
+// when profiling is on — device time from CUDA events recorded on the launching stream.
+// ---------------------------------------------------------------------------
+enum KClass { K_ZGEMM = 0, K_GJ_PANEL, K_GJ_SMALL, K_GJ_AUX, K_LEAF_ASM, K_LAYOUT, K_NCLASS };
+
+struct KStats {
+  int64_t launches[K_NCLASS] = {};
+  double flops[K_NCLASS] = {};
+  double bytes[K_NCLASS] = {};
+  double ms[K_NCLASS] = {};
+};
+
+struct Prof;
+extern thread_local Prof* g_prof;
+void prof_begin(int cls, double flops, double bytes, cudaStream_t st);
+void prof_end(cudaStream_t st);
+
+struct ProfScope {
+  cudaStream_t st;
+  ProfScope(int cls, double flops, double bytes, cudaStream_t s) : st(s) { prof_begin(cls, flops, bytes, s); }
+  ~ProfScope() { prof_end(st); }
+};

@@ -102,6 +102,112 @@ __global__ void rhs_out_nat_kernel(const zt* __restrict__ src, zt* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Schur-complement leaf: the boundary block F_b of B couples
+// each boundary node only with the opposite node of the same grid line (S_ix <-> N_ix,
+// W_iy <-> E_iy), so F_b^{-1} = G is a set of 2x2 blocks and eliminating u_b first leaves the
+// interior operator  S = A_ii - A_ib G F_i = Lx (+) Ly - kappa^2 diag(c)  (line operators Lx,
+// Ly shared by every leaf).  Then  Y_i = S^{-1}, Psi_i = S^{-1} Ub, Y_b = -V S^{-1},
+// Psi_b = G - V Psi_i  with Ub = -A_ib G and V = G F_i (both one-line sparse).
+// consts layout (complex): Lx[q*q] Ly[q*q] Ubx[q][2] Uby[q][2] Vx[2][q] Vy[2][q] Gx[2][2] Gy[2][2]
+// ---------------------------------------------------------------------------
+__global__ void leaf_schur_assemble_kernel(zt* __restrict__ S, int64_t sstride, int leaf0, int nchunk,
+                                           const int* __restrict__ leaf_nat, const zt* __restrict__ c, int p,
+                                           const zt* __restrict__ K, double kappa2) {
+  const int lc = blockIdx.x;
+  if (lc >= nchunk) return;
+  const int q = p - 2, ni = q * q;
+  const zt* Lx = K;
+  const zt* Ly = K + q * q;
+  const zt* cl = c + (int64_t)leaf_nat[leaf0 + lc] * p * p;
+  zt* Sl = S + (int64_t)lc * sstride;
+  for (int e = threadIdx.x; e < ni * ni; e += blockDim.x) {
+    const int r = e / ni, cc = e % ni;
+    const int ix = r % q, iy = r / q, jx = cc % q, jy = cc / q;
+    zt v = make_double2(0.0, 0.0);
+    if (iy == jy) {
+      v.x += Lx[ix * q + jx].x;
+      v.y += Lx[ix * q + jx].y;
+    }
+    if (ix == jx) {
+      v.x += Ly[iy * q + jy].x;
+      v.y += Ly[iy * q + jy].y;
+    }
+    if (r == cc) {
+      const zt cv = cl[(iy + 1) * p + ix + 1];
+      v.x -= kappa2 * cv.x;
+      v.y -= kappa2 * cv.y;
+    }
+    Sl[e] = v;
+  }
+}
+
+__device__ __forceinline__ void zfma(zt& acc, zt a, zt b) {
+  acc.x += a.x * b.x - a.y * b.y;
+  acc.y += a.x * b.y + a.y * b.x;
+}
+
+// store[l] = [Psi | Y] (nt x nt, row-major); on entry its (I_i, I_i) block holds S^{-1}.
+__global__ void leaf_schur_finish_kernel(zt* __restrict__ store, int64_t sstride, int leaf0, int nchunk, int p,
+                                         const zt* __restrict__ K) {
+  const int lc = blockIdx.x;
+  if (lc >= nchunk) return;
+  const int q = p - 2, ni = q * q, nb = 4 * q, nt = nb + ni;
+  const zt* Ubx = K + 2 * q * q;
+  const zt* Uby = Ubx + 2 * q;
+  const zt* Vx = Uby + 2 * q;
+  const zt* Vy = Vx + 2 * q;
+  const zt* Gx = Vy + 2 * q;
+  const zt* Gy = Gx + 4;
+  zt* base = store + (int64_t)(leaf0 + lc) * sstride;
+  const zt* Si = base + (int64_t)nb * nt + nb;  // S^{-1}, ld nt
+  // Psi_i = S^{-1} Ub
+  for (int e = threadIdx.x; e < ni * nb; e += blockDim.x) {
+    const int r = e / nb, b = e % nb, edge = b / q, k = b % q;
+    zt acc = make_double2(0.0, 0.0);
+    if (edge == 0 || edge == 2) {  // S_k / N_k: y-line ix = k
+      const int side = edge == 0 ? 0 : 1;
+      for (int t = 0; t < q; ++t) zfma(acc, Si[(int64_t)r * nt + t * q + k], Uby[t * 2 + side]);
+    } else {                       // E_k / W_k: x-line iy = k
+      const int side = edge == 3 ? 0 : 1;
+      for (int t = 0; t < q; ++t) zfma(acc, Si[(int64_t)r * nt + k * q + t], Ubx[t * 2 + side]);
+    }
+    base[(int64_t)(nb + r) * nt + b] = acc;
+  }
+  // Y_b = -V S^{-1}
+  for (int e = threadIdx.x; e < nb * ni; e += blockDim.x) {
+    const int b = e / ni, cc = e % ni, edge = b / q, k = b % q;
+    zt acc = make_double2(0.0, 0.0);
+    if (edge == 0 || edge == 2) {
+      const int side = edge == 0 ? 0 : 1;
+      for (int t = 0; t < q; ++t) zfma(acc, Vy[side * q + t], Si[(int64_t)(t * q + k) * nt + cc]);
+    } else {
+      const int side = edge == 3 ? 0 : 1;
+      for (int t = 0; t < q; ++t) zfma(acc, Vx[side * q + t], Si[(int64_t)(k * q + t) * nt + cc]);
+    }
+    base[(int64_t)b * nt + nb + cc] = make_double2(-acc.x, -acc.y);
+  }
+  __syncthreads();
+  // Psi_b = G - V Psi_i
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int b = e / nb, b2 = e % nb, edge = b / q, k = b % q;
+    const zt* Pi = base + (int64_t)nb * nt;  // Psi_i rows
+    zt acc = make_double2(0.0, 0.0);
+    zt gv = make_double2(0.0, 0.0);
+    const int e2 = b2 / q, k2 = b2 % q;
+    if (edge == 0 || edge == 2) {
+      const int side = edge == 0 ? 0 : 1;
+      for (int t = 0; t < q; ++t) zfma(acc, Vy[side * q + t], Pi[(int64_t)(t * q + k) * nt + b2]);
+      if (k2 == k && (e2 == 0 || e2 == 2)) gv = Gy[side * 2 + (e2 == 0 ? 0 : 1)];
+    } else {
+      const int side = edge == 3 ? 0 : 1;
+      for (int t = 0; t < q; ++t) zfma(acc, Vx[side * q + t], Pi[(int64_t)(k * q + t) * nt + b2]);
+      if (k2 == k && (e2 == 1 || e2 == 3)) gv = Gx[side * 2 + (e2 == 3 ? 0 : 1)];
+    }
+    base[(int64_t)b * nt + b2] = make_double2(gv.x - acc.x, gv.y - acc.y);
+  }
+}
+
 inline int grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
@@ -114,6 +220,8 @@ inline int grid_for(int64_t total) {
 void launch_leaf_assemble(zt* B, int64_t bstride, int leaf0, int nchunk, const int* leaf_nat, const zt* c, int p,
                           const double* dmat, const int* pos, const int* node, double kappa2, zt eta,
                           cudaStream_t st) {
+  const double nt = p * p - 4;
+  ProfScope ps(K_LEAF_ASM, 0.0, 16.0 * nt * nt * nchunk, st);
   leaf_assemble_kernel<<<nchunk, 256, 0, st>>>(B, bstride, leaf0, nchunk, leaf_nat, c, p, dmat, pos, node, kappa2,
                                                 eta);
   HPS_CUDA_CHECK(cudaGetLastError());
@@ -122,19 +230,41 @@ void launch_leaf_assemble(zt* B, int64_t bstride, int leaf0, int nchunk, const i
 
 void launch_leaf_R(const zt* store, int64_t sstride, zt* R, int nleaf, int nt, int nb, zt eta, cudaStream_t st) {
   const zt m2ieta = make_double2(2.0 * eta.y, -2.0 * eta.x);  // -2 i eta
+  ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nleaf * nb * nb, st);
   leaf_R_kernel<<<grid_for((int64_t)nleaf * nb * nb), 256, 0, st>>>(store, sstride, R, nleaf, nt, nb, m2ieta);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
 
 void launch_rhs_in(const zt* src, zt* dst, const int* leaf_nat, int nleaf, int n, int nrhs, cudaStream_t st) {
+  ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nleaf * n * nrhs, st);
   rhs_in_kernel<<<grid_for((int64_t)nleaf * n * nrhs), 256, 0, st>>>(src, dst, leaf_nat, nleaf, n, nrhs);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
 
 void launch_rhs_out(const zt* src, zt* dst, const int* nat_to_heap, int nleaf, int n, int nrhs, cudaStream_t st) {
+  ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nleaf * n * nrhs, st);
   rhs_out_nat_kernel<<<grid_for((int64_t)nleaf * n * nrhs), 256, 0, st>>>(src, dst, nat_to_heap, nleaf, n, nrhs);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_leaf_schur_assemble(zt* S, int64_t sstride, int leaf0, int nchunk, const int* leaf_nat, const zt* c, int p,
+                                const zt* consts, double kappa2, cudaStream_t st) {
+  const double ni = (p - 2) * (p - 2);
+  ProfScope ps(K_LEAF_ASM, 0.0, 16.0 * ni * ni * nchunk, st);
+  leaf_schur_assemble_kernel<<<nchunk, 256, 0, st>>>(S, sstride, leaf0, nchunk, leaf_nat, c, p, consts, kappa2);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_leaf_schur_finish(zt* store, int64_t sstride, int leaf0, int nchunk, int p, const zt* consts,
+                              cudaStream_t st) {
+  const double q = p - 2, ni = q * q, nb = 4 * q;
+  ProfScope ps(K_LEAF_ASM, 8.0 * nchunk * q * (2.0 * ni * nb + nb * nb),
+               16.0 * nchunk * (2.0 * ni * ni + 2.0 * ni * nb + nb * nb + ni * nb), st);
+  leaf_schur_finish_kernel<<<nchunk, 256, 0, st>>>(store, sstride, leaf0, nchunk, p, consts);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

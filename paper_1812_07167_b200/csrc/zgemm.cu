@@ -225,6 +225,9 @@ __global__ void zcopy_kernel(const ZCopy c) {
 
 void zgemm(const ZGemm& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return;
+  const double mn = (double)g.M * g.N, bt = (double)g.batch;
+  ProfScope ps(K_ZGEMM, 8.0 * mn * g.K * bt,
+               16.0 * bt * ((double)g.M * g.K + (double)g.K * g.N + mn * (g.Cin.ptr ? 2.0 : 1.0)), st);
   const int64_t t64 = (int64_t)((g.M + 63) / 64) * ((g.N + 63) / 64) * g.batch;
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
@@ -239,6 +242,7 @@ void zgemm(const ZGemm& g, cudaStream_t st) {
 void zcopy(const ZCopy& c, cudaStream_t st) {
   const int64_t total = (int64_t)c.batch * c.M * c.N;
   if (total <= 0) return;
+  ProfScope ps(K_LAYOUT, 0.0, 32.0 * total, st);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 32) blocks = 148 * 32;
   zcopy_kernel<<<blocks, 256, 0, st>>>(c);

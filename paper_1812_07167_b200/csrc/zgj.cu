@@ -345,6 +345,7 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
                                                 sizeof(int) * kSmallMax + 16)));
       attr = true;
     }
+    ProfScope ps(K_GJ_SMALL, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
       zgj_small_kernel<<<nbatch, kThreads, smem, st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
@@ -369,6 +370,7 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
   for (int k0 = 0; k0 < n; k0 += pp.nb) {
     const int wdt = std::min(pp.nb, n - k0);
     {
+      ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)wdt * wdt * batch, 32.0 * n * (double)wdt * batch, st);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(batch * pp.cs);
       cfg.blockDim = dim3(kThreads);
@@ -386,10 +388,13 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
     }
     const int nc = n - wdt;
     if (nc > 0) {
-      dim3 g((nc + 255) / 256, batch);
-      zgj_swapz_kernel<<<g, 256, 0, st>>>(A, lda, bs, n, k0, wdt, piv, Z);
-      HPS_CUDA_CHECK(cudaGetLastError());
-      count_launch();
+      {
+        dim3 g((nc + 255) / 256, batch);
+        ProfScope ps(K_GJ_AUX, 0.0, 16.0 * 4.0 * wdt * (double)nc * batch, st);
+        zgj_swapz_kernel<<<g, 256, 0, st>>>(A, lda, bs, n, k0, wdt, piv, Z);
+        HPS_CUDA_CHECK(cudaGetLastError());
+        count_launch();
+      }
       ZGemm gm;
       gm.M = n;
       gm.N = nc;
@@ -415,10 +420,14 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
       zgemm(gm, st);
     }
   }
-  zgj_pi_kernel<<<(batch + 127) / 128, 128, 0, st>>>(piv, pi, n, batch);
-  HPS_CUDA_CHECK(cudaGetLastError());
-  count_launch();
+  {
+    ProfScope ps(K_GJ_AUX, 0.0, 8.0 * n * (double)batch, st);
+    zgj_pi_kernel<<<(batch + 127) / 128, 128, 0, st>>>(piv, pi, n, batch);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+  }
   const int64_t total = (int64_t)batch * n * n;
+  ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)total, st);
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
   zgj_colperm_kernel<<<blocks, 256, 0, st>>>(A, lda, bs, out, ldo, obs, pi, n, batch);
   HPS_CUDA_CHECK(cudaGetLastError());

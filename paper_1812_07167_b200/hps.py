@@ -33,12 +33,15 @@ class hps_c128(C.Structure):
 
 class hps_opts(C.Structure):
     _fields_ = [("keep_root_R", C.c_int32), ("keep_all_R", C.c_int32), ("device", C.c_int32),
-                ("leaf_chunk", C.c_int32)]
+                ("leaf_chunk", C.c_int32), ("profile", C.c_int32), ("leaf_mode", C.c_int32)]
 
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
-           "hps_last_flops", "hps_free", "hps_last_error"]
+           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_free",
+           "hps_last_error"]
+
+KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout"]
 
 
 def lib():
@@ -66,6 +69,10 @@ def lib():
         L.hps_last_launches.restype = i64
         L.hps_last_flops.argtypes = [vp, i32]
         L.hps_last_flops.restype = C.c_double
+        L.hps_set_profiling.argtypes = [vp, i32]
+        L.hps_kernel_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]
+        L.hps_reset_stats.argtypes = [vp]
         L.hps_free.argtypes = [vp]
         L.hps_last_error.restype = C.c_char_p
         _lib = L
@@ -119,12 +126,13 @@ def root_boundary_nodes(g, p):
 class Solver:
     """hps_build on construction; solve() is hps_solve."""
 
-    def __init__(self, g, p, kappa, eta, c, keep_root_R=True, keep_all_R=False, device=-1, leaf_chunk=0):
+    def __init__(self, g, p, kappa, eta, c, keep_root_R=True, keep_all_R=False, device=-1, leaf_chunk=0,
+                 profile=False, leaf_mode=0):
         self.g, self.p = g, p
         self.nleaf = g.nx * g.ny
         self.q, self.nt, self.ni = p - 2, p * p - 4, (p - 2) ** 2
         self.nb_root = 2 * (g.nx + g.ny) * (p - 2)
-        opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk))
+        opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk), int(profile), int(leaf_mode))
         eta = complex(eta)
         h = C.c_void_p()
         cp = _ptr(c, self.nleaf * p * p, "c_samples")
@@ -169,6 +177,21 @@ class Solver:
 
     def flops(self, which):
         return lib().hps_last_flops(self.h, which)
+
+    def set_profiling(self, on):
+        _check(lib().hps_set_profiling(self.h, int(on)))
+
+    def reset_stats(self):
+        _check(lib().hps_reset_stats(self.h))
+
+    def kernel_stats(self):
+        """{class name: dict(launches, ms, flops, bytes)} accumulated since build / reset."""
+        out = {}
+        for k, name in enumerate(KCLASSES):
+            n, ms, fl, by = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+            _check(lib().hps_kernel_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by)))
+            out[name] = dict(launches=n.value, ms=ms.value, flops=fl.value, bytes=by.value)
+        return out
 
     def close(self):
         if getattr(self, "h", None):

@@ -34,10 +34,11 @@ def problem(nx, ny, p, kappa, eta, x1=1.0, y1=1.0, nrhs=2, seed=0):
     return g, c, s, t
 
 
-@pytest.mark.parametrize("p", [4, 8, 10, 16])
-def test_leaf_parity(p):
+@pytest.mark.parametrize("leaf_mode", [0, 1])
+@pytest.mark.parametrize("p", [4, 8, 10, 16, 20])
+def test_leaf_parity(p, leaf_mode):
     g, c, s, t = problem(2, 1, p, 7.0, 7.0 + 1j)
-    S = hps.Solver(g, p, 7.0, 7.0 + 1j, c, keep_all_R=True)
+    S = hps.Solver(g, p, 7.0, 7.0 + 1j, c, keep_all_R=True, leaf_mode=leaf_mode)
     for leaf in range(2):
         Psi, Y = S.leaf_ops(leaf)
         lo = oracle.leaf(p, 0.5, 1.0, 7.0, 7.0 + 1j, c[leaf])
