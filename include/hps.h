@@ -133,6 +133,12 @@ int hps_set_profiling(hps_handle* h, int on);
 int hps_kernel_stats(const hps_handle* h, int cls, int64_t* launches, double* ms, double* flops, double* bytes);
 int hps_reset_stats(hps_handle* h);
 
+/* Batched explicit inverse (the library's Gauss-Jordan kernels with partial pivoting, the same
+ * code path that inverts the leaf matrices and W).  A: batch x n x n row-major, out: same
+ * shape; host or device pointers; A is not modified.  Returns HPS_ESINGULAR on an exactly
+ * zero pivot.  Exposed for kernel-level tests. */
+int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* out);
+
 void hps_free(hps_handle* h);
 const char* hps_last_error(void);
 

@@ -1110,6 +1110,47 @@ int hps_reset_stats(hps_handle* h) {
   return HPS_OK;
 }
 
+int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* outp) {
+  if (n <= 0 || batch <= 0 || !A || !outp) {
+    hps_set_error("hps_zinv_batched: invalid argument");
+    return HPS_EINVAL;
+  }
+  try {
+    cudaStream_t st;
+    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int dev;
+    HPS_CUDA_CHECK(cudaGetDevice(&dev));
+    retain_pool(dev);
+    g_alloc_stream = st;
+    const size_t bytes = sizeof(zt) * (size_t)n * n * batch;
+    int rc = HPS_OK;
+    {
+      DevBuf a, o, ws, info;
+      a.alloc(bytes);
+      o.alloc(bytes);
+      ws.alloc(std::max<size_t>(zgj_workspace_bytes(n, batch), 16));
+      info.alloc(sizeof(int));
+      HPS_CUDA_CHECK(cudaMemcpyAsync(a.p, A, bytes, cudaMemcpyDefault, st));
+      HPS_CUDA_CHECK(cudaMemsetAsync(info.p, 0, sizeof(int), st));
+      zgj_invert(a.as<zt>(), n, (int64_t)n * n, o.as<zt>(), n, (int64_t)n * n, n, batch, ws.p, info.as<int>(), st,
+                 nullptr);
+      int h_info = 0;
+      HPS_CUDA_CHECK(cudaMemcpyAsync(outp, o.p, bytes, cudaMemcpyDefault, st));
+      HPS_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+      if (h_info) {
+        hps_set_error("hps_zinv_batched: zero pivot in batch entry " + std::to_string(h_info - 1));
+        rc = HPS_ESINGULAR;
+      }
+    }
+    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    return rc;
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+}
+
 void hps_free(hps_handle* h) { delete h; }
 
 }  // extern "C"

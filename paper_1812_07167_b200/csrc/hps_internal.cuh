@@ -33,12 +33,14 @@ void hps_set_error(const std::string& msg);
 // ---------------------------------------------------------------------------
 // Without a column map, column j may skip a window: j -> j + (j >= cskip_at ? cskip_len : 0)
 // (used by the blocked Gauss-Jordan update, which touches every column but the panel).
+// rmap_bs: batch stride of the row map (0 = one map shared by the whole batch).
 struct ZOp {
   const zt* ptr = nullptr;
   int64_t rs = 0, cs = 1, bs = 0;
   const int* rmap = nullptr;
   const int* cmap = nullptr;
   int cskip_at = 0x7fffffff, cskip_len = 0;
+  int64_t rmap_bs = 0;
 };
 
 struct ZOut {
@@ -47,6 +49,7 @@ struct ZOut {
   const int* rmap = nullptr;
   const int* cmap = nullptr;
   int cskip_at = 0x7fffffff, cskip_len = 0;
+  int64_t rmap_bs = 0;
 };
 
 __device__ __forceinline__ int zcol(const int* cmap, int j, int skip_at, int skip_len) {

@@ -8,6 +8,9 @@
 // Operands are staged global -> shared with cp.async (16 B = one complex element, zero-fill
 // for ragged edges and for "zero" map entries), double-buffered.  Shared-memory strides are
 // chosen so that the 8x4 / 4x8 DMMA fragments load as conflict-free 16-byte LDS.
+#include <cstdio>
+#include <cstdlib>
+
 #include "hps_internal.cuh"
 
 namespace {
@@ -26,7 +29,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -68,13 +71,17 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
   for (int b = blockIdx.y; b < g.batch; b += gridDim.y) {
     const zt* Ab = g.A.ptr + (int64_t)b * g.A.bs;
     const zt* Bb = g.B.ptr + (int64_t)b * g.B.bs;
+    const int* Arm = g.A.rmap ? g.A.rmap + (int64_t)b * g.A.rmap_bs : nullptr;
+    const int* Brm = g.B.rmap ? g.B.rmap + (int64_t)b * g.B.rmap_bs : nullptr;
+    const int* Crm = g.C.rmap ? g.C.rmap + (int64_t)b * g.C.rmap_bs : nullptr;
+    const int* Irm = g.Cin.rmap ? g.Cin.rmap + (int64_t)b * g.Cin.rmap_bs : nullptr;
     // A row offsets (fixed over k)
     int64_t a_roff[ITA];
     bool a_rok[ITA];
 #pragma unroll
     for (int it = 0; it < ITA; ++it) {
       const int gi = m0 + a_r0 + it * A_RSTEP;
-      int ri = gi < g.M ? (g.A.rmap ? g.A.rmap[gi] : gi) : -1;
+      int ri = gi < g.M ? (Arm ? Arm[gi] : gi) : -1;
       a_rok[it] = ri >= 0;
       a_roff[it] = (int64_t)(ri < 0 ? 0 : ri) * g.A.rs;
     }
@@ -103,21 +110,44 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
       for (int it = 0; it < ITB; ++it) {
         const int r = b_r0 + it * B_RSTEP;
         const int gk = k0 + r;
-        int rk = gk < g.K ? (g.B.rmap ? g.B.rmap[gk] : gk) : -1;
+        int rk = gk < g.K ? (Brm ? Brm[gk] : gk) : -1;
         const bool ok = b_cok && rk >= 0;
         cp_async16(&Bs[(stage * BK + r) * BS + b_c], ok ? Bb + (int64_t)rk * g.B.rs + b_coff : g.B.ptr, ok);
       }
       cp_async_commit();
     };
 
-    double accr[TM][TN][2], acci[TM][TN][2];
-#pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
-
     const int nk = (g.K + BK - 1) / BK;
     if (nk > 0) load_stage(0, 0);
+
+    // Accumulators start at (beta / alpha) Cin, so the Cin loads overlap the first stage.
+    double accr[TM][TN][2], acci[TM][TN][2];
+    const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + (int64_t)b * g.Cin.bs : nullptr;
+    zt ba = make_double2(0.0, 0.0);
+    if (Cinb) {
+      const double d = g.alpha.x * g.alpha.x + g.alpha.y * g.alpha.y;
+      const zt ia = make_double2(g.alpha.x / d, -g.alpha.y / d);
+      ba = zmul(g.beta, ia);
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
+      const int ri = (Cinb && gi < g.M) ? (Irm ? Irm[gi] : gi) : -1;
+#pragma unroll
+      for (int j = 0; j < TN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gj = n0 + wn * C::TN * 8 + j * 8 + (lane & 3) * 2 + h;
+          zt v = make_double2(0.0, 0.0);
+          if (ri >= 0 && gj < g.N) {
+            const int cj = zcol(g.Cin.cmap, gj, g.Cin.cskip_at, g.Cin.cskip_len);
+            if (cj >= 0) v = zmul(ba, Cinb[(int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
+          }
+          accr[i][j][h] = v.x;
+          acci[i][j][h] = v.y;
+        }
+    }
+
     for (int kt = 0; kt < nk; ++kt) {
       if (kt + 1 < nk) {
         load_stage((kt + 1) & 1, (kt + 1) * BK);
@@ -135,30 +165,36 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
         for (int i = 0; i < TM; ++i) af[i] = Ast[(i * 8 + (lane >> 2)) * AS + kk * 4 + (lane & 3)];
 #pragma unroll
         for (int j = 0; j < TN; ++j) bf[j] = Bst[(kk * 4 + (lane & 3)) * BS + j * 8 + (lane >> 2)];
+        // four real sub-products, ordered so that consecutive DMMAs on one accumulator are
+        // 2*TM*TN instructions apart (no back-to-back accumulator dependency)
 #pragma unroll
-        for (int i = 0; i < TM; ++i) {
-          const double nai = -af[i].y;
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
-          for (int j = 0; j < TN; ++j) {
-            dmma(accr[i][j][0], accr[i][j][1], af[i].x, bf[j].x);
-            dmma(accr[i][j][0], accr[i][j][1], nai, bf[j].y);
-            dmma(acci[i][j][0], acci[i][j][1], af[i].x, bf[j].y);
-            dmma(acci[i][j][0], acci[i][j][1], af[i].y, bf[j].x);
-          }
-        }
+          for (int j = 0; j < TN; ++j) dmma(accr[i][j][0], accr[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma(acci[i][j][0], acci[i][j][1], af[i].x, bf[j].y);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma(accr[i][j][0], accr[i][j][1], -af[i].y, bf[j].y);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) dmma(acci[i][j][0], acci[i][j][1], af[i].y, bf[j].x);
       }
       __syncthreads();
     }
 
-    // Epilogue: C = alpha * acc + beta * Cin + diag * [i == j]
-    const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + (int64_t)b * g.Cin.bs : nullptr;
+    // Epilogue: C = alpha * acc + diag * [i == j]
     zt* Cb = g.C.ptr + (int64_t)b * g.C.bs;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
       if (gi >= g.M) continue;
-      const int ro = g.C.rmap ? g.C.rmap[gi] : gi;
-      const int ri = Cinb ? (g.Cin.rmap ? g.Cin.rmap[gi] : gi) : -1;
+      const int ro = Crm ? Crm[gi] : gi;
+      if (ro < 0) continue;
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
 #pragma unroll
@@ -166,21 +202,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
           const int gj = n0 + wn * C::TN * 8 + j * 8 + (lane & 3) * 2 + h;
           if (gj >= g.N) continue;
           zt v = zmul(g.alpha, make_double2(accr[i][j][h], acci[i][j][h]));
-          if (Cinb && ri >= 0) {
-            const int cj = zcol(g.Cin.cmap, gj, g.Cin.cskip_at, g.Cin.cskip_len);
-            if (cj >= 0) {
-              const zt cv = Cinb[(int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs];
-              const zt bv = zmul(g.beta, cv);
-              v.x += bv.x;
-              v.y += bv.y;
-            }
-          }
           if (gi == gj) {
             v.x += g.diag.x;
             v.y += g.diag.y;
           }
           const int co = zcol(g.C.cmap, gj, g.C.cskip_at, g.C.cskip_len);
-          if (ro >= 0 && co >= 0) Cb[(int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
+          if (co >= 0) Cb[(int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
         }
       }
     }
@@ -210,10 +237,10 @@ __global__ void zcopy_kernel(const ZCopy c) {
     const int64_t t = e / c.N;
     const int i = (int)(t % c.M);
     const int b = (int)(t / c.M);
-    const int ro = c.C.rmap ? c.C.rmap[i] : i;
+    const int ro = c.C.rmap ? c.C.rmap[(int64_t)b * c.C.rmap_bs + i] : i;
     const int co = zcol(c.C.cmap, j, c.C.cskip_at, c.C.cskip_len);
     if (ro < 0 || co < 0) continue;
-    const int ri = c.A.rmap ? c.A.rmap[i] : i;
+    const int ri = c.A.rmap ? c.A.rmap[(int64_t)b * c.A.rmap_bs + i] : i;
     const int ci = zcol(c.A.cmap, j, c.A.cskip_at, c.A.cskip_len);
     zt v = make_double2(0.0, 0.0);
     if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[(int64_t)b * c.A.bs + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
@@ -223,7 +250,38 @@ __global__ void zcopy_kernel(const ZCopy c) {
 
 }  // namespace
 
+// HPS_TRACE=1: time every ZGEMM with events (synchronous) and print its shape to stderr.
+static bool trace_on() {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("HPS_TRACE");
+    t = (e && *e == '1') ? 1 : 0;
+  }
+  return t == 1;
+}
+
+void zgemm_impl(const ZGemm& g, cudaStream_t st);
+
 void zgemm(const ZGemm& g, cudaStream_t st) {
+  if (!trace_on()) return zgemm_impl(g, st);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, st);
+  zgemm_impl(g, st);
+  cudaEventRecord(b, st);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const double fl = 8.0 * g.M * (double)g.N * g.K * g.batch;
+  fprintf(stderr, "[zgemm] M=%d N=%d K=%d batch=%d cin=%d maps=%d%d%d%d  %.3f ms  %.2f TF\n", g.M, g.N, g.K, g.batch,
+          g.Cin.ptr != nullptr, g.A.rmap != nullptr, g.B.rmap != nullptr, g.B.cmap != nullptr, g.C.rmap != nullptr,
+          ms, fl / ms / 1e9);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
+void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return;
   const double mn = (double)g.M * g.N, bt = (double)g.batch;
   ProfScope ps(K_ZGEMM, 8.0 * mn * g.K * bt,

@@ -38,7 +38,7 @@ class hps_opts(C.Structure):
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
-           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_free",
+           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_free",
            "hps_last_error"]
 
 KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout"]
@@ -73,6 +73,7 @@ def lib():
         L.hps_kernel_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
         L.hps_reset_stats.argtypes = [vp]
+        L.hps_zinv_batched.argtypes = [i32, i32, dp, dp]
         L.hps_free.argtypes = [vp]
         L.hps_last_error.restype = C.c_char_p
         _lib = L
@@ -121,6 +122,14 @@ def root_boundary_nodes(g, p):
     _check(lib().hps_root_boundary_nodes(C.byref(g), p, X.ctypes.data, Y.ctypes.data, NX.ctypes.data,
                                          NY.ctypes.data))
     return X, Y, NX, NY
+
+
+def zinv_batched(A):
+    """Batched inverse through the library's Gauss-Jordan kernels (A: [batch, n, n] complex128)."""
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    out = np.zeros_like(A)
+    _check(lib().hps_zinv_batched(A.shape[-1], A.shape[0], A.ctypes.data, out.ctypes.data))
+    return out
 
 
 class Solver:

@@ -86,3 +86,26 @@ def test_torch_device_buffers():
     u = S.solve(d(s), d(t)).cpu().numpy()
     O = oracle.Oracle(0, 1, 0, 1, 4, 2, 8, 5.0, 5.0, c)
     assert rel(u, O.solve(s, t)) < TOL
+
+
+@pytest.mark.parametrize("n,batch", [(14, 300), (20, 2), (33, 3), (60, 400), (100, 5), (196, 7), (252, 2),
+                                     (257, 1), (300, 2), (448, 1), (700, 1), (1100, 1), (4200, 1)])
+def test_batched_inverse(n, batch):
+    """The Gauss-Jordan kernels (small, register panel, cluster panel) vs the oracle's LU."""
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
+    A[:, 0, 0] = 0.0    # forces a pivot exchange on the first step
+    X = hps.zinv_batched(A)
+    if n <= 1500:
+        for b in range(min(batch, 2)):
+            ref = oracle.invert(A[b])
+            assert rel(X[b], ref) < 1e-10 * max(1, n / 100)
+    # residual, a property that holds at any size
+    assert np.max(np.abs(A[-1] @ X[-1] - np.eye(n))) < 1e-9 * max(1, n / 500)
+
+
+def test_batched_inverse_singular():
+    A = np.zeros((2, 40, 40), complex)
+    A[0] = np.eye(40)
+    with pytest.raises(hps.HpsError):
+        hps.zinv_batched(A)
