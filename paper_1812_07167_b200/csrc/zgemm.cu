@@ -120,15 +120,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
     const int nk = (g.K + BK - 1) / BK;
     if (nk > 0) load_stage(0, 0);
 
-    // Accumulators start at (beta / alpha) Cin, so the Cin loads overlap the first stage.
+    // Accumulators start at (beta / alpha) Cin, so the Cin loads overlap the first stage.  When
+    // beta == alpha (every use but one) the raw values are loaded with no arithmetic, so all
+    // loads are in flight together and the first DMMA is the first consumer.
     double accr[TM][TN][2], acci[TM][TN][2];
     const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + (int64_t)b * g.Cin.bs : nullptr;
-    zt ba = make_double2(0.0, 0.0);
-    if (Cinb) {
-      const double d = g.alpha.x * g.alpha.x + g.alpha.y * g.alpha.y;
-      const zt ia = make_double2(g.alpha.x / d, -g.alpha.y / d);
-      ba = zmul(g.beta, ia);
-    }
+    const bool raw = g.beta.x == g.alpha.x && g.beta.y == g.alpha.y;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
@@ -141,11 +138,25 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
           zt v = make_double2(0.0, 0.0);
           if (ri >= 0 && gj < g.N) {
             const int cj = zcol(g.Cin.cmap, gj, g.Cin.cskip_at, g.Cin.cskip_len);
-            if (cj >= 0) v = zmul(ba, Cinb[(int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
+            if (cj >= 0) v = Cinb[(int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs];
           }
           accr[i][j][h] = v.x;
           acci[i][j][h] = v.y;
         }
+    }
+    if (Cinb && !raw) {
+      const double d = g.alpha.x * g.alpha.x + g.alpha.y * g.alpha.y;
+      const zt ba = zmul(g.beta, make_double2(g.alpha.x / d, -g.alpha.y / d));
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const zt v = zmul(ba, make_double2(accr[i][j][h], acci[i][j][h]));
+            accr[i][j][h] = v.x;
+            acci[i][j][h] = v.y;
+          }
     }
 
     for (int kt = 0; kt < nk; ++kt) {

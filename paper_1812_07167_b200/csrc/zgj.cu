@@ -168,22 +168,8 @@ __device__ __forceinline__ void write_maps(const PanelArgs& a, int b, int i, int
 
 // Register rows are kept ROTATED: after each Gauss-Jordan step the row shifts left by one, so
 // the active column kk always sits in register slot 0 (no dynamic register indexing) and after
-// w steps slot p holds panel column (p + w) mod NB.  The broadcast update row `uprow` equals the
-// scaled pivot row except uprow[0] = 1/pivot + 1, which makes the rank-1 step uniform:
-// row <- row - f * uprow  gives row[kk] = f - f (1/pivot + 1) = -f/pivot as Gauss-Jordan needs.
-template <int NB>
-__device__ __forceinline__ void row_axpy(zt (&row)[NB], zt fs, const zt* up) {
-  const double nfx = -fs.x, nfy = -fs.y;
-#pragma unroll
-  for (int j = 0; j < NB; ++j) {
-    const zt pj = up[j];
-    row[j].x = fma(nfx, pj.x, row[j].x);
-    row[j].x = fma(fs.y, pj.y, row[j].x);
-    row[j].y = fma(nfx, pj.y, row[j].y);
-    row[j].y = fma(nfy, pj.x, row[j].y);
-  }
-}
-
+// w steps slot p holds panel column (p + w) mod NB.  The pivot row is broadcast RAW; every
+// thread derives 1/pivot itself, so no thread serialises the scaling.
 template <int NB>
 __device__ __forceinline__ void row_rotate(zt (&row)[NB]) {
   const zt t = row[0];
@@ -192,17 +178,35 @@ __device__ __forceinline__ void row_rotate(zt (&row)[NB]) {
   row[NB - 1] = t;
 }
 
+// 1 / z for the pivot: conj(z) / |z|^2 with an IEEE round-to-nearest reciprocal.
+__device__ __forceinline__ zt zinv_fast(zt a) {
+  const double rd = __drcp_rn(a.x * a.x + a.y * a.y);
+  return make_double2(a.x * rd, -a.y * rd);
+}
+
+// Gauss-Jordan step on one register row given the RAW pivot row `pr` (slot 0 = pivot value):
+// row <- row - g * pr with g = row[0] / pivot, then slot 0 <- -g.
 template <int NB>
-__device__ __forceinline__ void publish_pivot(const zt (&row)[NB], zt* prow, zt* uprow) {
-  const zt inv = zinv(row[0]);
-  prow[0] = inv;
-  uprow[0] = make_double2(inv.x + 1.0, inv.y);
+__device__ __forceinline__ void row_step(zt (&row)[NB], const zt* pr, zt inv) {
+  const zt g = zmul(row[0], inv);
+  const double ngx = -g.x, ngy = -g.y;
 #pragma unroll
   for (int j = 1; j < NB; ++j) {
-    const zt v = zmul(row[j], inv);
-    prow[j] = v;
-    uprow[j] = v;
+    const zt pj = pr[j];
+    row[j].x = fma(ngx, pj.x, row[j].x);
+    row[j].x = fma(g.y, pj.y, row[j].x);
+    row[j].y = fma(ngx, pj.y, row[j].y);
+    row[j].y = fma(ngy, pj.x, row[j].y);
   }
+  row[0] = make_double2(ngx, ngy);
+}
+
+// Pivot row itself: row <- pr / pivot with slot 0 <- 1 / pivot.
+template <int NB>
+__device__ __forceinline__ void row_pivot(zt (&row)[NB], const zt* pr, zt inv) {
+#pragma unroll
+  for (int j = 1; j < NB; ++j) row[j] = zmul(pr[j], inv);
+  row[0] = inv;
 }
 
 template <int NB>
@@ -222,7 +226,7 @@ __device__ __forceinline__ void store_rotated(const zt (&row)[NB], zt* dst, int 
 // ---------------------------------------------------------------------------
 template <int NB>
 __global__ void __launch_bounds__(256) zgj_panel_reg_kernel(const PanelArgs a) {
-  __shared__ zt prow[NB], uprow[NB], tmp[NB];
+  __shared__ zt prow[NB], tmp[NB];
   __shared__ double rv[8];
   __shared__ int ri[8];
   __shared__ int s_orig_r, s_orig_k;
@@ -259,8 +263,9 @@ __global__ void __launch_bounds__(256) zgj_panel_reg_kernel(const PanelArgs a) {
       singular = true;
       if (r == 0x7fffffff) r = k;
     }
-    if (i == r) {
-      publish_pivot<NB>(row, prow, uprow);
+    if (i == r) {  // publish the raw pivot row
+#pragma unroll
+      for (int j = 0; j < NB; ++j) prow[j] = row[j];
       s_orig_r = orig;
     }
     if (i == k && r != k) {
@@ -269,9 +274,9 @@ __global__ void __launch_bounds__(256) zgj_panel_reg_kernel(const PanelArgs a) {
       s_orig_k = orig;
     }
     __syncthreads();
+    const zt inv = zinv_fast(prow[0]);
     if (i == k) {
-#pragma unroll
-      for (int j = 0; j < NB; ++j) row[j] = prow[j];
+      row_pivot<NB>(row, prow, inv);
       orig = s_orig_r;
     } else {
       if (i == r) {  // receives the displaced row k
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(256) zgj_panel_reg_kernel(const PanelArgs a) {
         for (int j = 0; j < NB; ++j) row[j] = tmp[j];
         orig = s_orig_k;
       }
-      row_axpy<NB>(row, row[0], uprow);
+      row_step<NB>(row, prow, inv);
     }
     row_rotate<NB>(row);
     if (tid == 0) piv[k] = r;
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(256) zgj_panel_creg_kernel(const PanelArgs a) 
   const int CS = (int)cluster.num_blocks();
   const int c = (int)cluster.block_rank();
   const int b = blockIdx.x / CS, n = a.n, k0 = a.k0, w = a.w;
-  __shared__ zt prow[NB], uprow[NB], tmp[NB], lprow[NB], luprow[NB];
+  __shared__ zt prow[NB], tmp[NB], lprow[NB];
   __shared__ double rv[8];
   __shared__ int ri[8];
   __shared__ Slot slot;
@@ -360,8 +365,9 @@ __global__ void __launch_bounds__(256) zgj_panel_creg_kernel(const PanelArgs a) 
     }
     __syncthreads();
     const int r = s_r;
-    if (i == r) {
-      publish_pivot<NB>(row, prow, uprow);
+    if (i == r) {  // publish the raw pivot row
+#pragma unroll
+      for (int j = 0; j < NB; ++j) prow[j] = row[j];
       orig_r_pub = orig;
     }
     if (i == k && r != k) {
@@ -370,15 +376,12 @@ __global__ void __launch_bounds__(256) zgj_panel_creg_kernel(const PanelArgs a) 
       orig_k_pub = orig;
     }
     cluster.sync();  // (2) pivot row published
-    if (tid < NB) {
-      lprow[tid] = cluster.map_shared_rank(prow, r / 256)[tid];
-      luprow[tid] = cluster.map_shared_rank(uprow, r / 256)[tid];
-    }
+    if (tid < NB) lprow[tid] = cluster.map_shared_rank(prow, r / 256)[tid];
     __syncthreads();
+    const zt inv = zinv_fast(lprow[0]);
     if (i == k) {
       orig = *cluster.map_shared_rank(&orig_r_pub, r / 256);
-#pragma unroll
-      for (int j = 0; j < NB; ++j) row[j] = lprow[j];
+      row_pivot<NB>(row, lprow, inv);
     } else if (i < n) {
       if (i == r) {
         const zt* rt = cluster.map_shared_rank(tmp, k / 256);
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(256) zgj_panel_creg_kernel(const PanelArgs a) 
         for (int j = 0; j < NB; ++j) row[j] = rt[j];
         orig = *cluster.map_shared_rank(&orig_k_pub, k / 256);
       }
-      row_axpy<NB>(row, row[0], luprow);
+      row_step<NB>(row, lprow, inv);
     }
     row_rotate<NB>(row);
     if (c == 0 && tid == 0) piv[k] = r;
