@@ -12,8 +12,10 @@ Q16; step time = device time of build + solve on the library stream), summed ove
 the extra keys carry the build seconds, build DOF/s and solve ms per RHS.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl hps|reference]
-Under torchrun (N > 1) every rank builds and solves its own replica of the workload
-(weak scaling, no data-path collective).
+Under torchrun (N > 1) the workload is SHARDED by subtree (paper_1812_07167_b200.dist): each
+rank builds and solves its 1/N of the leaves and its subtree with no communication, the
+subtree-root operators / outgoing data are all-gathered over NCCL and the top log2(N) levels
+are merged on every rank (strong scaling of the same workload).
 """
 import argparse
 import json
@@ -255,6 +257,70 @@ def run_hps(args, rank, world, dist):
     return out
 
 
+def run_sharded(args, rank, world, dist_mod):
+    """N > 1: subtree-sharded build + solve over NCCL (strong scaling of one workload)."""
+    import torch
+    from paper_1812_07167_b200 import dist as hdist
+    from paper_1812_07167_b200 import hps
+    import __graft_entry__
+    if rank == 0:
+        __graft_entry__.build()
+    dist_mod.barrier()
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    cfg = inputs.CONFIGS[args.config]
+    nrhs = args.nrhs or cfg.nrhs
+    g, c, s, t = setup(cfg, hps)
+    s, t = s[:nrhs], t[:nrhs]
+    sub, i0, j0 = hdist.local_block(g, world, rank)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    c_l, s_l, t_d = d(hdist.slice_leaves(c, g, sub, i0, j0)), d(hdist.slice_leaves(s, g, sub, i0, j0)), d(t)
+    comm = hdist.TorchComm()
+    be = hdist.CudaBackend(device=local)
+    l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+    launches = 0
+
+    def step():
+        nonlocal launches
+        D = hdist.DistributedHPS(comm, be, g, cfg.p, cfg.kappa, cfg.eta, c_l)
+        D.solve(s_l, t_d)
+        torch.cuda.synchronize()
+        launches += D.sub.launches(0) + D.sub.launches(1) + hps.lib().hps_last_launches(D.top.h, 0) + \
+            hps.lib().hps_last_launches(D.top.h, 1)
+        D.close()
+
+    for _ in range(args.warmup):
+        flush_l2(torch, l2buf)
+        step()
+    launches = 0
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush_l2(torch, l2buf)
+            torch.cuda.synchronize()
+            dist_mod.barrier()
+            t0 = time.perf_counter()
+            step()
+            dist_mod.barrier()
+            times.append(time.perf_counter() - t0)
+    tt = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    dist_mod.all_reduce(tt, op=dist_mod.ReduceOp.MAX)
+    step_s = tt.item()
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": round(cfg.n_unique / step_s, 1), "unit": "DOF/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * step_s, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
+                       "dof": cfg.n_unique, "parallelism": f"subtree shards x{world}, top {int(np.log2(world))} "
+                                                            f"levels replicated after an NCCL all-gather",
+                       "l2": "256 MiB buffer written between steps"},
+            "clocks": clk.summary(), "gpu_launches": int(launches),
+            "timing": "host wall clock between barriers + device synchronize, max over ranks"}
+
+
 def oracle_run(cfg, c, s, t):
     """The oracle as it stands (Algorithm 1 + 2 on host cores, OpenMP over boxes)."""
     import oracle
@@ -379,7 +445,9 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
             dist.init_process_group("nccl")
-        out = run_hps(args, rank, world, dist)
+            out = run_sharded(args, rank, world, dist)
+        else:
+            out = run_hps(args, rank, world, dist)
         if dist is not None:
             dist.destroy_process_group()
     if out is not None and rank == 0:

@@ -96,6 +96,40 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
  *  Host or device pointers. */
 int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps_c128* u);
 
+/* ---- Subtree sharding (multi-GPU) ---------------------------------------
+ * The tree's top `depth` levels are split off: rank r builds the subtree of the depth-`depth`
+ * box with heap index r (hps_subtree_grid gives its rectangle) with hps_build, the subtree-root
+ * ItI operators of all ranks are gathered, and hps_build_top merges them (Algorithm 1 for the
+ * boxes above `depth`).  The solve splits the same way: hps_solve_up on every subtree, gather
+ * of the subtree-root outgoing data h, hps_solve_top (upward merges above `depth`, then the
+ * downward pass from the root data t to the depth-`depth` boxes), hps_solve_down on every
+ * subtree.  Layouts: R_sub [2^depth][nb][nb] row-major (heap order), h_sub / t_sub
+ * [2^depth][nrhs][nb] with nb = n_b of a depth-`depth` box. */
+
+/* Rectangle and leaf offset (ix0, iy0 in leaves) of the depth-`depth` box with heap index
+ * `index` (0 .. 2^depth - 1) of grid g.  Host-only geometry. */
+int hps_subtree_grid(const hps_grid* g, int depth, int64_t index, hps_grid* sub, int32_t* leaf_i0,
+                     int32_t* leaf_j0);
+
+/* Merge tree above `depth` from the given subtree-root ItI operators (Algorithm 1
+ * for the boxes tau < 2^depth).  The handle's R of box 1 is exported by hps_export_R when
+ * keep_root_R = 1. */
+int hps_build_top(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, int depth, const hps_c128* R_sub,
+                  const hps_opts* opt, hps_handle** out);
+
+/* Upward pass of a (sub)tree handle: body load s as for hps_solve (NULL = 0); writes the root's
+ * outgoing particular impedance data h_root [nrhs][n_b(root)] (eq. flux_part) and keeps the
+ * leaf particular solutions and interface corrections for the matching hps_solve_down. */
+int hps_solve_up(hps_handle* h, int nrhs, const hps_c128* s, hps_c128* h_root);
+
+/* Downward pass of a (sub)tree handle from the root incoming data t [nrhs][n_b(root)]; u as in
+ * hps_solve.  Uses the state of the preceding hps_solve_up with the same nrhs (else s = 0). */
+int hps_solve_down(hps_handle* h, int nrhs, const hps_c128* t, hps_c128* u);
+
+/* Top handle: upward merges from h_sub (NULL = 0), downward pass from the root data t_root
+ * [nrhs][n_b(1)] to the depth boxes' incoming data t_sub. */
+int hps_solve_top(hps_handle* h, int nrhs, const hps_c128* h_sub, const hps_c128* t_root, hps_c128* t_sub);
+
 /* ItI operator of a box (heap numbering: root 1, children 2*tau (alpha: west / south) and
  * 2*tau + 1 (beta: east / north)).  out: n_b(box)^2, row-major, canonical
  * order.  The root is available when keep_root_R = 1; other boxes need keep_all_R = 1. */

@@ -585,6 +585,19 @@ int oracle_merge(int p, int cnx, int cny, int vertical, const cplx* Ra, const cp
   return 0;
 }
 
+// Leaf-index rectangle [i0, i1) x [j0, j1) and split orientation of box `box` (heap id).
+int oracle_box_rect(int nx, int ny, int64_t box, int* i0, int* i1, int* j0, int* j1, int* vertical) {
+  Tree T = make_tree(nx, ny);
+  if (box < 1 || box >= (int64_t)T.box.size()) return -1;
+  const Box& b = T.box[box];
+  *i0 = b.i0;
+  *i1 = b.i1;
+  *j0 = b.j0;
+  *j1 = b.j1;
+  *vertical = b.leaf ? -1 : b.vertical;
+  return 0;
+}
+
 // Tree facts for tests: number of boxes, leaf depth, per-box n_b.
 int oracle_tree_info(int nx, int ny, int p, int64_t* nboxes, int* depth) {
   Tree T = make_tree(nx, ny);

@@ -11,7 +11,7 @@ _SRC = os.path.join(_HERE, "hps_oracle.cpp")
 _lib = None
 
 __all__ = [
-    "build", "lib", "cheb", "leaf_nodes", "root_boundary", "leaf", "leaf_disc", "merge", "tree_info",
+    "build", "lib", "cheb", "leaf_nodes", "root_boundary", "leaf", "leaf_disc", "merge", "box_rect", "tree_info",
     "Oracle", "global_dense", "invert", "matmul",
 ]
 
@@ -37,6 +37,7 @@ def lib():
         L.oracle_leaf.argtypes = [i32, d, d, d, d, d, dp, dp, dp, dp, dp, dp]
         L.oracle_leaf_disc.argtypes = [i32, d, d, d, d, d, dp, dp, dp, dp, dp]
         L.oracle_merge.argtypes = [i32, i32, i32, i32, dp, dp, dp, dp, dp, dp, dp, dp, dp]
+        L.oracle_box_rect.argtypes = [i32, i32, i64] + [C.POINTER(C.c_int)] * 5
         L.oracle_tree_info.argtypes = [i32, i32, i32, C.POINTER(i64), C.POINTER(i32)]
         L.oracle_build.argtypes = [d, d, d, d, i32, i32, i32, d, d, d, dp, i32]
         L.oracle_build.restype = vp
@@ -136,6 +137,13 @@ def merge(p, cnx, cny, vertical, Ra, Rb):
                               _p(out["PhiB"]), _p(out["Winv"]), _p(out["UpsA"]), _p(out["UpsB"]),
                               _p(out["GammaT"])), "oracle_merge")
     return out
+
+
+def box_rect(nx, ny, box):
+    """(i0, i1, j0, j1, vertical) of a heap box (vertical = -1 for a leaf)."""
+    v = [C.c_int() for _ in range(5)]
+    _check(lib().oracle_box_rect(nx, ny, box, *[C.byref(x) for x in v]), "oracle_box_rect")
+    return tuple(x.value for x in v)
 
 
 def tree_info(nx, ny, p=4):

@@ -194,6 +194,21 @@ bool is_device_ptr(const void* p) {
 
 }  // namespace
 
+struct SolveState {
+  int nrhs = 0;
+  bool has_s = false;
+  DevBuf ut;                     // leaf particular solutions [nleaf][nt][R]
+  std::vector<DevBuf> TTa, TTb;  // interface corrections t~ per merge level [np][n3][R]
+  double flops_up = 0, flops_down = 0;
+  void reset(int L) {
+    ut.release();
+    TTa.clear();
+    TTb.clear();
+    TTa.resize(L);
+    TTb.resize(L);
+  }
+};
+
 struct hps_handle {
   int dev = 0;
   cudaStream_t st = nullptr;
@@ -202,11 +217,15 @@ struct hps_handle {
   double kappa = 0;
   zt eta{};
   int L = 0, nleaf = 0;
+  int Lb = 0;               // depth of the bottom operators: L (leaves) or the top depth
+  bool has_leaves = true;   // false for a top handle (hps_build_top)
+  SolveState ss;
+  DevBuf ident;             // identity index map 0 .. 2^Lb - 1
   bool keep_root_R = true, keep_all_R = false;
   int leaf_mode = 0;  // 0: Schur complement on the interior (default), 1: invert the full B
   std::vector<Depth> depth;
   std::vector<int> leaf_nat_h, nat_to_heap_h;
-  DevBuf leaf_nat, nat_to_heap, zero_idx;
+  DevBuf leaf_nat, nat_to_heap;
   DevBuf store;  // [nleaf heap][nt][nt] = [Psi | Y] per leaf (row-major)
   std::vector<MergeLevel> lev;  // lev[d] merges children at depth d+1 into depth d
   std::vector<DevBuf> R;        // R[d]: [2^d][nb(d)][nb(d)] (only the kept ones)
@@ -218,9 +237,10 @@ struct hps_handle {
   Prof prof;
   ~hps_handle() {
     // return every buffer to the pool on our stream, then retire the stream
+    ss.reset(0);
+    ident.release();
     leaf_nat.release();
     nat_to_heap.release();
-    zero_idx.release();
     store.release();
     for (auto& m : lev) {
       m.maps.release();
@@ -634,105 +654,134 @@ void build_merge(hps_handle& H, int d) {
 // ---------------------------------------------------------------------------
 // Solve (Algorithm 2).  Internal vectors: [box][n][nrhs] (RHS innermost).
 // ---------------------------------------------------------------------------
-void solve_impl(hps_handle& H, int nrhs, const zt* s_dev, const zt* t_dev, zt* u_dev) {
+// Upward pass (Algorithm 2 lines 1-9).  Bottom data: leaf s (ABI [R][nleaf][ni], natural
+// order) for a leaf handle, or the outgoing particular data of the depth-Lb boxes
+// (ABI [2^Lb][R][nb(Lb)]) for a top handle; NULL = zero body load.  Keeps u~, t~ in H.ss.
+// h_root (ABI [R][nb(0)], device) receives the root's outgoing particular data if non-NULL.
+void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
   cudaStream_t st = H.st;
-  const int nleaf = H.nleaf, nt = H.nt, nb = H.nbl, ni = H.ni, L = H.L;
+  const int Lb = H.Lb, nt = H.nt, nb = H.nbl, ni = H.ni;
   const int64_t R = nrhs;
-  std::vector<DevBuf> h(L + 1), t(L + 1), TTa(L), TTb(L);
-  DevBuf sint, ut, uint_;
-  const bool has_s = s_dev != nullptr;
+  SolveState& S = H.ss;
+  S.reset(Lb);
+  S.nrhs = nrhs;
+  S.has_s = bottom != nullptr;
+  if (!S.has_s) {
+    if (h_root) HPS_CUDA_CHECK(cudaMemsetAsync(h_root, 0, sizeof(zt) * (size_t)H.depth[0].nb * R, st));
+    return;
+  }
   double fl = 0;
-  HPS_CUDA_CHECK(cudaEventRecord(H.ev[0], st));
-  // ---- upward pass (lines 1-9) ----
-  if (has_s) {
-    sint.alloc(sizeof(zt) * (size_t)nleaf * ni * R);
-    launch_rhs_in(s_dev, sint.as<zt>(), H.leaf_nat.as<int>(), nleaf, ni, nrhs, st);
-    ut.alloc(sizeof(zt) * (size_t)nleaf * nt * R);
+  std::vector<DevBuf> h(Lb + 1);
+  const int nbot = 1 << Lb;
+  const int nbb = H.depth[Lb].nb;
+  h[Lb].alloc(sizeof(zt) * (size_t)nbot * nbb * R);
+  if (H.has_leaves) {
+    DevBuf sint;
+    sint.alloc(sizeof(zt) * (size_t)nbot * ni * R);
+    launch_rhs_in(bottom, sint.as<zt>(), H.leaf_nat.as<int>(), nbot, ni, nrhs, (int64_t)nbot * ni, ni, st);
+    S.ut.alloc(sizeof(zt) * (size_t)nbot * nt * R);
     {  // u~ = Y s
       ZGemm g;
       g.M = nt;
       g.N = nrhs;
       g.K = ni;
-      g.batch = nleaf;
+      g.batch = nbot;
       g.A = op(H.store.as<zt>() + nb, nt, (int64_t)nt * nt);
       g.B = op(sint.as<zt>(), R, (int64_t)ni * R);
-      g.C = out(ut.as<zt>(), R, (int64_t)nt * R);
+      g.C = out(S.ut.as<zt>(), R, (int64_t)nt * R);
       zgemm(g, st);
-      fl += 8.0 * nleaf * (double)nt * ni * R;
+      fl += 8.0 * nbot * (double)nt * ni * R;
     }
-    h[L].alloc(sizeof(zt) * (size_t)nleaf * nb * R);
     {  // h = Gamma s = -2 i eta u~(I_b)
       ZCopy c;
-      c.batch = nleaf;
+      c.batch = nbot;
       c.M = nb;
       c.N = nrhs;
-      c.A = op(ut.as<zt>(), R, (int64_t)nt * R);
-      c.C = out(h[L].as<zt>(), R, (int64_t)nb * R);
+      c.A = op(S.ut.as<zt>(), R, (int64_t)nt * R);
+      c.C = out(h[Lb].as<zt>(), R, (int64_t)nb * R);
       c.alpha = Z(2.0 * H.eta.y, -2.0 * H.eta.x);
       zcopy(c, st);
     }
-    for (int d = L - 1; d >= 0; --d) {
-      MergeLevel& M = H.lev[d];
-      const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, ntau = M.ntau, nbc = M.nbc;
-      const int64_t s33 = (int64_t)n3 * n3, cb = 2 * (int64_t)nbc * R;
-      const zt* ha = h[d + 1].as<zt>();
-      const zt* hb = ha + (int64_t)nbc * R;
-      DevBuf tmp;
-      tmp.alloc(sizeof(zt) * (size_t)np * n3 * R);
-      TTa[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
-      TTb[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
-      ZGemm g;
-      g.batch = np;
-      g.N = nrhs;
-      // tmp = R33b h3a - h3b ; t~a = W^{-1} tmp ; t~b = -h3a - R33a t~a   (Upsilon actions)
-      g.M = n3;
-      g.K = n3;
-      g.A = op(M.R33b, n3, s33);
-      g.B = op(ha, R, cb, M.I3a);
-      g.Cin = op(hb, R, cb, M.I3b);
-      g.beta = Z(-1, 0);
-      g.C = out(tmp.as<zt>(), R, (int64_t)n3 * R);
-      zgemm(g, st);
-      g.A = op(M.Winv, n3, s33);
-      g.B = op(tmp.as<zt>(), R, (int64_t)n3 * R);
-      g.Cin = ZOp();
-      g.beta = Z(0, 0);
-      g.C = out(TTa[d].as<zt>(), R, (int64_t)n3 * R);
-      zgemm(g, st);
-      g.A = op(M.R33a, n3, s33);
-      g.B = op(TTa[d].as<zt>(), R, (int64_t)n3 * R);
-      g.Cin = op(ha, R, cb, M.I3a);
-      g.alpha = Z(-1, 0);
-      g.beta = Z(-1, 0);
-      g.C = out(TTb[d].as<zt>(), R, (int64_t)n3 * R);
-      zgemm(g, st);
-      fl += 8.0 * np * 3.0 * n3 * n3 * R;
-      if (d > 0) {  // h^tau = [h1a; h2b] + [R13a t~a; R23b t~b]  (eq. flux_part), canonical order
-        h[d].alloc(sizeof(zt) * (size_t)np * ntau * R);
-        g.alpha = Z(1, 0);
-        g.beta = Z(1, 0);
-        g.M = n1;
-        g.A = op(M.R13a, n3, (int64_t)n1 * n3);
-        g.B = op(TTa[d].as<zt>(), R, (int64_t)n3 * R);
-        g.Cin = op(ha, R, cb, M.I1a);
-        g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp);
-        zgemm(g, st);
-        g.M = n2;
-        g.A = op(M.R23b, n3, (int64_t)n2 * n3);
-        g.B = op(TTb[d].as<zt>(), R, (int64_t)n3 * R);
-        g.Cin = op(hb, R, cb, M.I2b);
-        g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp + n1);
-        zgemm(g, st);
-        fl += 8.0 * np * (double)(n1 + n2) * n3 * R;
-      }
-      h[d + 1].release();
-    }
+  } else {  // given [box][R][nbb]
+    launch_rhs_in(bottom, h[Lb].as<zt>(), H.ident.as<int>(), nbot, nbb, nrhs, nbb, R * nbb, st);
   }
-  HPS_CUDA_CHECK(cudaEventRecord(H.ev[1], st));
-  // ---- downward pass (lines 10-18) ----
+  for (int d = Lb - 1; d >= 0; --d) {
+    MergeLevel& M = H.lev[d];
+    const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, ntau = M.ntau, nbc = M.nbc;
+    const int64_t s33 = (int64_t)n3 * n3, cb = 2 * (int64_t)nbc * R;
+    const zt* ha = h[d + 1].as<zt>();
+    const zt* hb = ha + (int64_t)nbc * R;
+    DevBuf tmp;
+    tmp.alloc(sizeof(zt) * (size_t)np * n3 * R);
+    S.TTa[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
+    S.TTb[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
+    ZGemm g;
+    g.batch = np;
+    g.N = nrhs;
+    // tmp = R33b h3a - h3b ; t~a = W^{-1} tmp ; t~b = -h3a - R33a t~a   (Upsilon actions)
+    g.M = n3;
+    g.K = n3;
+    g.A = op(M.R33b, n3, s33);
+    g.B = op(ha, R, cb, M.I3a);
+    g.Cin = op(hb, R, cb, M.I3b);
+    g.beta = Z(-1, 0);
+    g.C = out(tmp.as<zt>(), R, (int64_t)n3 * R);
+    zgemm(g, st);
+    g.A = op(M.Winv, n3, s33);
+    g.B = op(tmp.as<zt>(), R, (int64_t)n3 * R);
+    g.Cin = ZOp();
+    g.beta = Z(0, 0);
+    g.C = out(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
+    zgemm(g, st);
+    g.A = op(M.R33a, n3, s33);
+    g.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
+    g.Cin = op(ha, R, cb, M.I3a);
+    g.alpha = Z(-1, 0);
+    g.beta = Z(-1, 0);
+    g.C = out(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
+    zgemm(g, st);
+    fl += 8.0 * np * 3.0 * n3 * n3 * R;
+    if (d > 0 || h_root) {  // h^tau = [h1a; h2b] + [R13a t~a; R23b t~b]  (eq. flux_part), canonical order
+      h[d].alloc(sizeof(zt) * (size_t)np * ntau * R);
+      g.alpha = Z(1, 0);
+      g.beta = Z(1, 0);
+      g.M = n1;
+      g.A = op(M.R13a, n3, (int64_t)n1 * n3);
+      g.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
+      g.Cin = op(ha, R, cb, M.I1a);
+      g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp);
+      zgemm(g, st);
+      g.M = n2;
+      g.A = op(M.R23b, n3, (int64_t)n2 * n3);
+      g.B = op(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
+      g.Cin = op(hb, R, cb, M.I2b);
+      g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp + n1);
+      zgemm(g, st);
+      fl += 8.0 * np * (double)(n1 + n2) * n3 * R;
+    }
+    h[d + 1].release();
+  }
+  if (h_root) {
+    const int nb0 = H.depth[0].nb;
+    launch_rhs_out(h[0].as<zt>(), h_root, H.ident.as<int>(), 1, nb0, nrhs, (int64_t)nb0, nb0, st);
+  }
+  S.flops_up = fl;
+}
+
+// Downward pass (lines 10-18).  t_root: ABI [R][nb(0)].  Leaf handle: u out (ABI
+// [R][nleaf][nt], natural order).  Top handle: t of the depth-Lb boxes (ABI [2^Lb][R][nb(Lb)]).
+void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
+  cudaStream_t st = H.st;
+  const int Lb = H.Lb, nt = H.nt, nb = H.nbl;
+  const int64_t R = nrhs;
+  SolveState& S = H.ss;
+  const bool has_s = S.has_s && S.nrhs == nrhs;
+  double fl = 0;
+  std::vector<DevBuf> t(Lb + 1);
   t[0].alloc(sizeof(zt) * (size_t)H.depth[0].nb * R);
-  launch_rhs_in(t_dev, t[0].as<zt>(), H.zero_idx.as<int>(), 1, H.depth[0].nb, nrhs, st);
-  for (int d = 0; d < L; ++d) {
+  launch_rhs_in(t_root, t[0].as<zt>(), H.ident.as<int>(), 1, H.depth[0].nb, nrhs, (int64_t)H.depth[0].nb,
+                H.depth[0].nb, st);
+  for (int d = 0; d < Lb; ++d) {
     MergeLevel& M = H.lev[d];
     const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, ntau = M.ntau, nbc = M.nbc;
     t[d + 1].alloc(sizeof(zt) * (size_t)2 * np * nbc * R);
@@ -747,13 +796,13 @@ void solve_impl(hps_handle& H, int nrhs, const zt* s_dev, const zt* t_dev, zt* u
     g.A = op(M.PhiA, ntau, (int64_t)n3 * ntau);
     g.B = op(t[d].as<zt>(), R, pb, M.pp);
     if (has_s) {
-      g.Cin = op(TTa[d].as<zt>(), R, (int64_t)n3 * R);
+      g.Cin = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
       g.beta = Z(1, 0);
     }
     g.C = out(ta, R, cb, M.I3a);
     zgemm(g, st);  // t3a = Phi^a t + t~a
     g.A = op(M.PhiB, ntau, (int64_t)n3 * ntau);
-    if (has_s) g.Cin = op(TTb[d].as<zt>(), R, (int64_t)n3 * R);
+    if (has_s) g.Cin = op(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
     g.C = out(tb, R, cb, M.I3b);
     zgemm(g, st);  // t3b = Phi^b t + t~b
     fl += 8.0 * np * 2.0 * n3 * ntau * R;
@@ -769,38 +818,32 @@ void solve_impl(hps_handle& H, int nrhs, const zt* s_dev, const zt* t_dev, zt* u
     c.C = out(tb, R, cb, M.I2b);
     zcopy(c, st);
     t[d].release();
-    if (has_s) {
-      TTa[d].release();
-      TTb[d].release();
-    }
   }
-  uint_.alloc(sizeof(zt) * (size_t)nleaf * nt * R);
-  {  // u = Psi t + u~  (line 13)
-    ZGemm g;
+  const int nbot = 1 << Lb;
+  if (H.has_leaves) {
+    DevBuf uint_;
+    uint_.alloc(sizeof(zt) * (size_t)nbot * nt * R);
+    ZGemm g;  // u = Psi t + u~  (line 13)
     g.M = nt;
     g.N = nrhs;
     g.K = nb;
-    g.batch = nleaf;
+    g.batch = nbot;
     g.A = op(H.store.as<zt>(), nt, (int64_t)nt * nt);
-    g.B = op(t[L].as<zt>(), R, (int64_t)nb * R);
+    g.B = op(t[Lb].as<zt>(), R, (int64_t)nb * R);
     if (has_s) {
-      g.Cin = op(ut.as<zt>(), R, (int64_t)nt * R);
+      g.Cin = op(S.ut.as<zt>(), R, (int64_t)nt * R);
       g.beta = Z(1, 0);
     }
     g.C = out(uint_.as<zt>(), R, (int64_t)nt * R);
     zgemm(g, st);
-    fl += 8.0 * nleaf * (double)nt * nb * R;
+    fl += 8.0 * nbot * (double)nt * nb * R;
+    launch_rhs_out(uint_.as<zt>(), outp, H.nat_to_heap.as<int>(), nbot, nt, nrhs, (int64_t)nbot * nt, nt, st);
+  } else {
+    const int nbb = H.depth[Lb].nb;
+    launch_rhs_out(t[Lb].as<zt>(), outp, H.ident.as<int>(), nbot, nbb, nrhs, nbb, R * nbb, st);
   }
-  launch_rhs_out(uint_.as<zt>(), u_dev, H.nat_to_heap.as<int>(), nleaf, nt, nrhs, st);
-  HPS_CUDA_CHECK(cudaEventRecord(H.ev[2], st));
-  HPS_CUDA_CHECK(cudaEventSynchronize(H.ev[2]));
-  float a = 0, b = 0;
-  cudaEventElapsedTime(&a, H.ev[0], H.ev[1]);
-  cudaEventElapsedTime(&b, H.ev[1], H.ev[2]);
-  H.times[3] = a + b;
-  H.times[4] = a;
-  H.times[5] = b;
-  H.flops[1] = fl;
+  S.flops_down = fl;
+  S.reset(Lb);
 }
 
 int fail(const HpsError& e) {
@@ -883,91 +926,187 @@ int hps_root_boundary_nodes(const hps_grid* g, int p, double* x, double* y, doub
   return HPS_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+int validate_problem(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const char* who) {
+  auto bad = [&](const std::string& m) {
+    hps_set_error(std::string(who) + ": " + m);
+    return HPS_EINVAL;
+  };
+  if (!g) return bad("NULL grid");
+  if (p < 4) return bad("p must be >= 4");
+  if (q != p - 2) return bad("q must equal p - 2 (corner-free Chebyshev boundary nodes)");
+  if (!is_pow2(g->nx) || !is_pow2(g->ny)) return bad("nx and ny must be powers of two");
+  if (!(g->x1 > g->x0) || !(g->y1 > g->y0) || !std::isfinite(g->x0) || !std::isfinite(g->x1) ||
+      !std::isfinite(g->y0) || !std::isfinite(g->y1))
+    return bad("need finite x1 > x0 and y1 > y0");
+  if (!(kappa >= 0) || !std::isfinite(kappa)) return bad("kappa must be finite and >= 0");
+  if (eta.re == 0.0 || !std::isfinite(eta.re) || !std::isfinite(eta.im)) return bad("Re(eta) must be nonzero and eta finite");
+  return HPS_OK;
+}
+
+// Common handle set-up: stream, plan, maps, per-level operator stores.
+void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_opts* opt) {
+  if (opt && opt->device >= 0) HPS_CUDA_CHECK(cudaSetDevice(opt->device));
+  HPS_CUDA_CHECK(cudaGetDevice(&H.dev));
+  HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
+  retain_pool(H.dev);
+  g_alloc_stream = H.st;
+  for (auto& e : H.ev) HPS_CUDA_CHECK(cudaEventCreate(&e));
+  H.g = *g;
+  H.p = p;
+  H.q = q;
+  H.nbl = 4 * q;
+  H.ni = q * q;
+  H.nt = p * p - 4;
+  H.kappa = kappa;
+  H.eta = make_double2(eta.re, eta.im);
+  H.keep_root_R = opt ? opt->keep_root_R != 0 : true;
+  H.keep_all_R = opt ? opt->keep_all_R != 0 : false;
+  H.leaf_mode = opt ? opt->leaf_mode : 0;
+  H.prof.timing = opt ? opt->profile != 0 : false;
+}
+
+void plan_all(hps_handle& H, int Lb) {
+  plan_tree(H);
+  H.Lb = Lb;
+  upload(H.leaf_nat, H.leaf_nat_h, H.st);
+  upload(H.nat_to_heap, H.nat_to_heap_h, H.st);
+  std::vector<int> id(std::max(1, 1 << Lb));
+  for (size_t i = 0; i < id.size(); ++i) id[i] = (int)i;
+  upload(H.ident, id, H.st);
+  H.info.alloc(sizeof(int) * (H.L + 1));
+  HPS_CUDA_CHECK(cudaMemsetAsync(H.info.p, 0, sizeof(int) * (H.L + 1), H.st));
+  H.R.resize(H.L + 1);
+  H.lev.resize(Lb);
+  for (int d = 0; d < Lb; ++d) plan_level(H, d, H.lev[d]);
+  H.ss.reset(Lb);
+}
+
+void finish_build_timing(hps_handle& H) {
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev[2], H.st));
+  HPS_CUDA_CHECK(cudaEventSynchronize(H.ev[2]));
+  check_info(H);
+  float a = 0, b = 0;
+  cudaEventElapsedTime(&a, H.ev[0], H.ev[1]);
+  cudaEventElapsedTime(&b, H.ev[1], H.ev[2]);
+  H.times[0] = a + b;
+  H.times[1] = a;
+  H.times[2] = b;
+}
+
+// Borrow a caller buffer as device memory: device pointers are used as is, host pointers are
+// staged through `tmp` (stream-ordered).
+const zt* dev_in(const void* p, size_t bytes, DevBuf& tmp, cudaStream_t st) {
+  if (!p) return nullptr;
+  if (is_device_ptr(p)) return reinterpret_cast<const zt*>(p);
+  tmp.alloc(bytes);
+  HPS_CUDA_CHECK(cudaMemcpyAsync(tmp.p, p, bytes, cudaMemcpyHostToDevice, st));
+  return tmp.as<zt>();
+}
+
+struct DevOut {
+  void* user;
+  size_t bytes;
+  DevBuf tmp;
+  zt* dev;
+  DevOut(void* u, size_t b, cudaStream_t) : user(u), bytes(b), dev(nullptr) {
+    if (is_device_ptr(u)) {
+      dev = reinterpret_cast<zt*>(u);
+    } else {
+      tmp.alloc(b);
+      dev = tmp.as<zt>();
+    }
+  }
+  void finish(cudaStream_t st) {
+    if (dev != user) HPS_CUDA_CHECK(cudaMemcpyAsync(user, dev, bytes, cudaMemcpyDeviceToHost, st));
+  }
+};
+
+void record_solve_times(hps_handle& H, bool up, bool down) {
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev[5], H.st));
+  HPS_CUDA_CHECK(cudaEventSynchronize(H.ev[5]));
+  float a = 0, b = 0;
+  if (up && down) {
+    cudaEventElapsedTime(&a, H.ev[3], H.ev[4]);
+    cudaEventElapsedTime(&b, H.ev[4], H.ev[5]);
+  } else if (up) {
+    cudaEventElapsedTime(&a, H.ev[3], H.ev[5]);
+  } else {
+    cudaEventElapsedTime(&b, H.ev[3], H.ev[5]);
+  }
+  H.times[3] = a + b;
+  H.times[4] = a;
+  H.times[5] = b;
+  H.flops[1] = (up ? H.ss.flops_up : 0) + (down ? H.ss.flops_down : 0);
+}
+
+}  // namespace
+
+extern "C" {
+
 int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_c128* c_samples,
               const hps_opts* opt, hps_handle** outp) {
   if (outp) *outp = nullptr;
-  if (!g || !outp || !c_samples) {
+  if (!outp || !c_samples) {
     hps_set_error("hps_build: NULL argument");
     return HPS_EINVAL;
   }
-  if (p < 4) {
-    hps_set_error("hps_build: p must be >= 4");
-    return HPS_EINVAL;
-  }
-  if (q != p - 2) {
-    hps_set_error("hps_build: q must equal p - 2 (corner-free Chebyshev boundary nodes)");
-    return HPS_EINVAL;
-  }
-  if (!is_pow2(g->nx) || !is_pow2(g->ny)) {
-    hps_set_error("hps_build: nx and ny must be powers of two");
-    return HPS_EINVAL;
-  }
-  if (!(g->x1 > g->x0) || !(g->y1 > g->y0) || !std::isfinite(g->x0) || !std::isfinite(g->x1) ||
-      !std::isfinite(g->y0) || !std::isfinite(g->y1)) {
-    hps_set_error("hps_build: need finite x1 > x0 and y1 > y0");
-    return HPS_EINVAL;
-  }
-  if (!(kappa >= 0) || !std::isfinite(kappa)) {
-    hps_set_error("hps_build: kappa must be finite and >= 0");
-    return HPS_EINVAL;
-  }
-  if (eta.re == 0.0 || !std::isfinite(eta.re) || !std::isfinite(eta.im)) {
-    hps_set_error("hps_build: Re(eta) must be nonzero and eta finite");
-    return HPS_EINVAL;
-  }
+  if (int rc = validate_problem(g, p, q, kappa, eta, "hps_build")) return rc;
   std::unique_ptr<hps_handle> H(new hps_handle());
   try {
-    if (opt && opt->device >= 0) HPS_CUDA_CHECK(cudaSetDevice(opt->device));
-    HPS_CUDA_CHECK(cudaGetDevice(&H->dev));
-    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H->st, cudaStreamNonBlocking));
-    retain_pool(H->dev);
-    g_alloc_stream = H->st;
-    for (auto& e : H->ev) HPS_CUDA_CHECK(cudaEventCreate(&e));
-    H->g = *g;
-    H->p = p;
-    H->q = q;
-    H->nbl = 4 * q;
-    H->ni = q * q;
-    H->nt = p * p - 4;
-    H->kappa = kappa;
-    H->eta = make_double2(eta.re, eta.im);
-    H->keep_root_R = opt ? opt->keep_root_R != 0 : true;
-    H->keep_all_R = opt ? opt->keep_all_R != 0 : false;
-    H->leaf_mode = opt ? opt->leaf_mode : 0;
-    H->prof.timing = opt ? opt->profile != 0 : false;
+    init_handle(*H, g, p, q, kappa, eta, opt);
     LaunchScope ls(&H->launches[0], &H->prof);
     H->flops[0] = 0;
     plan_tree(*H);
-    upload(H->leaf_nat, H->leaf_nat_h, H->st);
-    upload(H->nat_to_heap, H->nat_to_heap_h, H->st);
-    upload(H->zero_idx, std::vector<int>{0}, H->st);
-    H->info.alloc(sizeof(int) * (H->L + 1));
-    HPS_CUDA_CHECK(cudaMemsetAsync(H->info.p, 0, sizeof(int) * (H->L + 1), H->st));
-    H->R.resize(H->L + 1);
-    H->lev.resize(H->L);
-    for (int d = 0; d < H->L; ++d) plan_level(*H, d, H->lev[d]);
-    // c samples: host or device
-    const size_t cbytes = sizeof(zt) * (size_t)H->nleaf * p * p;
+    plan_all(*H, H->L);  // (plan_tree runs again inside; cheap)
+    H->has_leaves = true;
     DevBuf cbuf;
-    const zt* c_dev = reinterpret_cast<const zt*>(c_samples);
-    if (!is_device_ptr(c_samples)) {
-      cbuf.alloc(cbytes);
-      HPS_CUDA_CHECK(cudaMemcpyAsync(cbuf.p, c_samples, cbytes, cudaMemcpyHostToDevice, H->st));
-      c_dev = cbuf.as<zt>();
-    }
+    const zt* c_dev = dev_in(c_samples, sizeof(zt) * (size_t)H->nleaf * p * p, cbuf, H->st);
     HPS_CUDA_CHECK(cudaEventRecord(H->ev[0], H->st));
     build_leaves(*H, c_dev, opt ? opt->leaf_chunk : 0);
     HPS_CUDA_CHECK(cudaEventRecord(H->ev[1], H->st));
     for (int d = H->L - 1; d >= 0; --d) build_merge(*H, d);
-    HPS_CUDA_CHECK(cudaEventRecord(H->ev[2], H->st));
-    HPS_CUDA_CHECK(cudaEventSynchronize(H->ev[2]));
-    check_info(*H);
-    float a = 0, b = 0;
-    cudaEventElapsedTime(&a, H->ev[0], H->ev[1]);
-    cudaEventElapsedTime(&b, H->ev[1], H->ev[2]);
-    H->times[0] = a + b;
-    H->times[1] = a;
-    H->times[2] = b;
+    finish_build_timing(*H);
+  } catch (const HpsError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(HpsError{HPS_ECUDA, e.what()});
+  }
+  *outp = H.release();
+  return HPS_OK;
+}
+
+int hps_build_top(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, int depth, const hps_c128* R_sub,
+                  const hps_opts* opt, hps_handle** outp) {
+  if (outp) *outp = nullptr;
+  if (!outp || !R_sub) {
+    hps_set_error("hps_build_top: NULL argument");
+    return HPS_EINVAL;
+  }
+  if (int rc = validate_problem(g, p, q, kappa, eta, "hps_build_top")) return rc;
+  std::unique_ptr<hps_handle> H(new hps_handle());
+  try {
+    init_handle(*H, g, p, q, kappa, eta, opt);
+    LaunchScope ls(&H->launches[0], &H->prof);
+    H->flops[0] = 0;
+    plan_tree(*H);
+    if (depth < 0 || depth > H->L) {
+      hps_set_error("hps_build_top: depth must be in [0, leaf depth]");
+      return HPS_EINVAL;
+    }
+    plan_all(*H, depth);
+    H->has_leaves = false;
+    const size_t nbb = H->depth[depth].nb;
+    const size_t bytes = sizeof(zt) * nbb * nbb * ((size_t)1 << depth);
+    H->R[depth].alloc(bytes);
+    HPS_CUDA_CHECK(cudaMemcpyAsync(H->R[depth].p, R_sub, bytes, cudaMemcpyDefault, H->st));
+    HPS_CUDA_CHECK(cudaEventRecord(H->ev[0], H->st));
+    HPS_CUDA_CHECK(cudaEventRecord(H->ev[1], H->st));
+    for (int d = depth - 1; d >= 0; --d) build_merge(*H, d);
+    finish_build_timing(*H);
   } catch (const HpsError& e) {
     return fail(e);
   } catch (const std::exception& e) {
@@ -978,8 +1117,8 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
 }
 
 int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps_c128* u) {
-  if (!h || nrhs < 0 || !t || !u) {
-    hps_set_error("hps_solve: invalid argument");
+  if (!h || nrhs < 0 || !t || !u || !h->has_leaves) {
+    hps_set_error("hps_solve: invalid argument (needs a leaf handle, t and u)");
     return HPS_EINVAL;
   }
   if (nrhs == 0) return HPS_OK;
@@ -987,36 +1126,133 @@ int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps
     HPS_CUDA_CHECK(cudaSetDevice(h->dev));
     g_alloc_stream = h->st;
     LaunchScope ls(&h->launches[1], &h->prof);
-    const size_t sb = sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni;
-    const size_t tb = sizeof(zt) * (size_t)nrhs * h->depth[0].nb;
-    const size_t ub = sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt;
-    DevBuf sd, td, ud;
-    const zt* s_dev = reinterpret_cast<const zt*>(s);
-    const zt* t_dev = reinterpret_cast<const zt*>(t);
-    zt* u_dev = reinterpret_cast<zt*>(u);
-    if (s && !is_device_ptr(s)) {
-      sd.alloc(sb);
-      HPS_CUDA_CHECK(cudaMemcpyAsync(sd.p, s, sb, cudaMemcpyHostToDevice, h->st));
-      s_dev = sd.as<zt>();
-    }
-    if (!is_device_ptr(t)) {
-      td.alloc(tb);
-      HPS_CUDA_CHECK(cudaMemcpyAsync(td.p, t, tb, cudaMemcpyHostToDevice, h->st));
-      t_dev = td.as<zt>();
-    }
-    const bool u_host = !is_device_ptr(u);
-    if (u_host) {
-      ud.alloc(ub);
-      u_dev = ud.as<zt>();
-    }
-    solve_impl(*h, nrhs, s_dev, t_dev, u_dev);
-    if (u_host) HPS_CUDA_CHECK(cudaMemcpyAsync(u, u_dev, ub, cudaMemcpyDeviceToHost, h->st));
+    DevBuf sd, td;
+    const zt* s_dev = dev_in(s, sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni, sd, h->st);
+    const zt* t_dev = dev_in(t, sizeof(zt) * (size_t)nrhs * h->depth[0].nb, td, h->st);
+    DevOut uo(u, sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt, h->st);
+    HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
+    solve_up_impl(*h, nrhs, s_dev, nullptr);
+    HPS_CUDA_CHECK(cudaEventRecord(h->ev[4], h->st));
+    solve_down_impl(*h, nrhs, t_dev, uo.dev);
+    record_solve_times(*h, true, true);
+    uo.finish(h->st);
     HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
   } catch (const HpsError& e) {
     return fail(e);
   } catch (const std::exception& e) {
     return fail(HpsError{HPS_ECUDA, e.what()});
   }
+  return HPS_OK;
+}
+
+int hps_solve_up(hps_handle* h, int nrhs, const hps_c128* s, hps_c128* h_root) {
+  if (!h || nrhs <= 0 || !h_root || !h->has_leaves) {
+    hps_set_error("hps_solve_up: invalid argument");
+    return HPS_EINVAL;
+  }
+  try {
+    HPS_CUDA_CHECK(cudaSetDevice(h->dev));
+    g_alloc_stream = h->st;
+    LaunchScope ls(&h->launches[1], &h->prof);
+    DevBuf sd;
+    const zt* s_dev = dev_in(s, sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni, sd, h->st);
+    DevOut ho(h_root, sizeof(zt) * (size_t)nrhs * h->depth[0].nb, h->st);
+    HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
+    solve_up_impl(*h, nrhs, s_dev, ho.dev);
+    record_solve_times(*h, true, false);
+    ho.finish(h->st);
+    HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
+  } catch (const HpsError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(HpsError{HPS_ECUDA, e.what()});
+  }
+  return HPS_OK;
+}
+
+int hps_solve_down(hps_handle* h, int nrhs, const hps_c128* t, hps_c128* u) {
+  if (!h || nrhs <= 0 || !t || !u || !h->has_leaves) {
+    hps_set_error("hps_solve_down: invalid argument");
+    return HPS_EINVAL;
+  }
+  try {
+    HPS_CUDA_CHECK(cudaSetDevice(h->dev));
+    g_alloc_stream = h->st;
+    LaunchScope ls(&h->launches[1], &h->prof);
+    DevBuf td;
+    const zt* t_dev = dev_in(t, sizeof(zt) * (size_t)nrhs * h->depth[0].nb, td, h->st);
+    DevOut uo(u, sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt, h->st);
+    HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
+    solve_down_impl(*h, nrhs, t_dev, uo.dev);
+    record_solve_times(*h, false, true);
+    uo.finish(h->st);
+    HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
+  } catch (const HpsError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(HpsError{HPS_ECUDA, e.what()});
+  }
+  return HPS_OK;
+}
+
+int hps_solve_top(hps_handle* h, int nrhs, const hps_c128* h_sub, const hps_c128* t_root, hps_c128* t_sub) {
+  if (!h || nrhs <= 0 || !t_root || !t_sub || h->has_leaves) {
+    hps_set_error("hps_solve_top: invalid argument (needs a top handle)");
+    return HPS_EINVAL;
+  }
+  try {
+    HPS_CUDA_CHECK(cudaSetDevice(h->dev));
+    g_alloc_stream = h->st;
+    LaunchScope ls(&h->launches[1], &h->prof);
+    const size_t nbot = (size_t)1 << h->Lb, nbb = h->depth[h->Lb].nb;
+    DevBuf hd, td;
+    const zt* h_dev = dev_in(h_sub, sizeof(zt) * nbot * nrhs * nbb, hd, h->st);
+    const zt* t_dev = dev_in(t_root, sizeof(zt) * (size_t)nrhs * h->depth[0].nb, td, h->st);
+    DevOut to(t_sub, sizeof(zt) * nbot * nrhs * nbb, h->st);
+    HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
+    solve_up_impl(*h, nrhs, h_dev, nullptr);
+    HPS_CUDA_CHECK(cudaEventRecord(h->ev[4], h->st));
+    solve_down_impl(*h, nrhs, t_dev, to.dev);
+    record_solve_times(*h, true, true);
+    to.finish(h->st);
+    HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
+  } catch (const HpsError& e) {
+    return fail(e);
+  } catch (const std::exception& e) {
+    return fail(HpsError{HPS_ECUDA, e.what()});
+  }
+  return HPS_OK;
+}
+
+int hps_subtree_grid(const hps_grid* g, int depth, int64_t index, hps_grid* sub, int32_t* leaf_i0, int32_t* leaf_j0) {
+  if (!g || !sub || depth < 0 || index < 0 || index >= ((int64_t)1 << depth) || !is_pow2(g->nx) || !is_pow2(g->ny)) {
+    hps_set_error("hps_subtree_grid: invalid argument");
+    return HPS_EINVAL;
+  }
+  int a = g->nx, b = g->ny, i0 = 0, j0 = 0;
+  for (int d = 0; d < depth; ++d) {
+    if (a == 1 && b == 1) {
+      hps_set_error("hps_subtree_grid: depth exceeds the leaf depth");
+      return HPS_EINVAL;
+    }
+    const bool vertical = a >= b;
+    if (vertical) a /= 2;
+    else b /= 2;
+    const int bit = (int)((index >> (depth - 1 - d)) & 1);  // heap path: 0 = alpha, 1 = beta
+    if (bit) {
+      if (vertical) i0 += a;
+      else j0 += b;
+    }
+  }
+  const double hx = (g->x1 - g->x0) / g->nx, hy = (g->y1 - g->y0) / g->ny;
+  sub->x0 = g->x0 + i0 * hx;
+  sub->x1 = g->x0 + (i0 + a) * hx;
+  sub->y0 = g->y0 + j0 * hy;
+  sub->y1 = g->y0 + (j0 + b) * hy;
+  sub->nx = a;
+  sub->ny = b;
+  if (leaf_i0) *leaf_i0 = i0;
+  if (leaf_j0) *leaf_j0 = j0;
   return HPS_OK;
 }
 
@@ -1056,7 +1292,7 @@ int hps_export_R(const hps_handle* h, int64_t box, hps_c128* outR) {
 }
 
 int hps_export_leaf(const hps_handle* h, int64_t leaf, hps_c128* psi, hps_c128* y) {
-  if (!h || leaf < 0 || leaf >= h->nleaf) {
+  if (!h || !h->has_leaves || leaf < 0 || leaf >= h->nleaf) {
     hps_set_error("hps_export_leaf: invalid argument");
     return HPS_EINVAL;
   }

@@ -6,8 +6,10 @@ void launch_leaf_assemble(zt* B, int64_t bstride, int leaf0, int nchunk, const i
                           const double* dmat, const int* pos, const int* node, double kappa2, zt eta,
                           cudaStream_t st);
 void launch_leaf_R(const zt* store, int64_t sstride, zt* R, int nleaf, int nt, int nb, zt eta, cudaStream_t st);
-void launch_rhs_in(const zt* src, zt* dst, const int* leaf_nat, int nleaf, int n, int nrhs, cudaStream_t st);
-void launch_rhs_out(const zt* src, zt* dst, const int* nat_to_heap, int nleaf, int n, int nrhs, cudaStream_t st);
+void launch_rhs_in(const zt* src, zt* dst, const int* map, int nbox, int n, int nrhs, int64_t sr, int64_t sb,
+                   cudaStream_t st);
+void launch_rhs_out(const zt* src, zt* dst, const int* map, int nbox, int n, int nrhs, int64_t sr, int64_t sb,
+                    cudaStream_t st);
 void launch_leaf_schur_assemble(zt* S, int64_t sstride, int leaf0, int nchunk, const int* leaf_nat, const zt* c, int p,
                                 const zt* consts, double kappa2, cudaStream_t st);
 void launch_leaf_schur_finish(zt* store, int64_t sstride, int leaf0, int nchunk, int p, const zt* consts,

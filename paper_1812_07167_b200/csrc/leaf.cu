@@ -76,29 +76,29 @@ __global__ void leaf_R_kernel(const zt* __restrict__ store, int64_t sstride, zt*
   }
 }
 
-// ABI [nrhs][nleaf natural][n] -> internal [nleaf heap][n][nrhs]
-__global__ void rhs_in_kernel(const zt* __restrict__ src, zt* __restrict__ dst, const int* __restrict__ leaf_nat,
-                              int nleaf, int n, int nrhs) {
-  const int64_t total = (int64_t)nleaf * n * nrhs;
+// external [r * sr + map[l] * sb + i] -> internal [l][n][nrhs]   (ABI: sr = nleaf n, sb = n)
+__global__ void rhs_in_kernel(const zt* __restrict__ src, zt* __restrict__ dst, const int* __restrict__ map,
+                              int nbox, int n, int nrhs, int64_t sr, int64_t sb) {
+  const int64_t total = (int64_t)nbox * n * nrhs;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(e % nrhs);
     const int64_t t = e / nrhs;
     const int i = (int)(t % n);
     const int l = (int)(t / n);
-    dst[e] = src[((int64_t)r * nleaf + leaf_nat[l]) * n + i];
+    dst[e] = src[(int64_t)r * sr + (int64_t)map[l] * sb + i];
   }
 }
 
-// internal [nleaf heap][n][nrhs] -> ABI [nrhs][nleaf natural][n]
-__global__ void rhs_out_nat_kernel(const zt* __restrict__ src, zt* __restrict__ dst, const int* __restrict__ nat_to_heap,
-                                   int nleaf, int n, int nrhs) {
-  const int64_t total = (int64_t)nleaf * n * nrhs;
+// internal [map[ln]][n][nrhs] -> external [r * sr + ln * sb + i]
+__global__ void rhs_out_kernel(const zt* __restrict__ src, zt* __restrict__ dst, const int* __restrict__ map,
+                               int nbox, int n, int nrhs, int64_t sr, int64_t sb) {
+  const int64_t total = (int64_t)nbox * n * nrhs;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % n);
     const int64_t t = e / n;
-    const int ln = (int)(t % nleaf);
-    const int r = (int)(t / nleaf);
-    dst[e] = src[((int64_t)nat_to_heap[ln] * n + i) * nrhs + r];
+    const int ln = (int)(t % nbox);
+    const int r = (int)(t / nbox);
+    dst[(int64_t)r * sr + (int64_t)ln * sb + i] = src[((int64_t)map[ln] * n + i) * nrhs + r];
   }
 }
 
@@ -236,16 +236,18 @@ void launch_leaf_R(const zt* store, int64_t sstride, zt* R, int nleaf, int nt, i
   count_launch();
 }
 
-void launch_rhs_in(const zt* src, zt* dst, const int* leaf_nat, int nleaf, int n, int nrhs, cudaStream_t st) {
-  ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nleaf * n * nrhs, st);
-  rhs_in_kernel<<<grid_for((int64_t)nleaf * n * nrhs), 256, 0, st>>>(src, dst, leaf_nat, nleaf, n, nrhs);
+void launch_rhs_in(const zt* src, zt* dst, const int* map, int nbox, int n, int nrhs, int64_t sr, int64_t sb,
+                   cudaStream_t st) {
+  ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nbox * n * nrhs, st);
+  rhs_in_kernel<<<grid_for((int64_t)nbox * n * nrhs), 256, 0, st>>>(src, dst, map, nbox, n, nrhs, sr, sb);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
 
-void launch_rhs_out(const zt* src, zt* dst, const int* nat_to_heap, int nleaf, int n, int nrhs, cudaStream_t st) {
-  ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nleaf * n * nrhs, st);
-  rhs_out_nat_kernel<<<grid_for((int64_t)nleaf * n * nrhs), 256, 0, st>>>(src, dst, nat_to_heap, nleaf, n, nrhs);
+void launch_rhs_out(const zt* src, zt* dst, const int* map, int nbox, int n, int nrhs, int64_t sr, int64_t sb,
+                    cudaStream_t st) {
+  ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nbox * n * nrhs, st);
+  rhs_out_kernel<<<grid_for((int64_t)nbox * n * nrhs), 256, 0, st>>>(src, dst, map, nbox, n, nrhs, sr, sb);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

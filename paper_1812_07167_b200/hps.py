@@ -38,7 +38,8 @@ class hps_opts(C.Structure):
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
-           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_free",
+           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
+           "hps_solve_down", "hps_solve_top", "hps_free",
            "hps_last_error"]
 
 KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout"]
@@ -74,6 +75,13 @@ def lib():
                                        C.POINTER(C.c_double)]
         L.hps_reset_stats.argtypes = [vp]
         L.hps_zinv_batched.argtypes = [i32, i32, dp, dp]
+        L.hps_subtree_grid.argtypes = [C.POINTER(hps_grid), i32, i64, C.POINTER(hps_grid), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32)]
+        L.hps_build_top.argtypes = [C.POINTER(hps_grid), i32, i32, C.c_double, hps_c128, i32, dp,
+                                    C.POINTER(hps_opts), C.POINTER(vp)]
+        L.hps_solve_up.argtypes = [vp, i32, dp, dp]
+        L.hps_solve_down.argtypes = [vp, i32, dp, dp]
+        L.hps_solve_top.argtypes = [vp, i32, dp, dp, dp]
         L.hps_free.argtypes = [vp]
         L.hps_last_error.restype = C.c_char_p
         _lib = L
@@ -124,6 +132,25 @@ def root_boundary_nodes(g, p):
     return X, Y, NX, NY
 
 
+def subtree_grid(g, depth, index):
+    """(sub-grid, leaf i0, leaf j0) of the depth-`depth` box with heap index `index`."""
+    sub = hps_grid()
+    i0, j0 = C.c_int32(), C.c_int32()
+    _check(lib().hps_subtree_grid(C.byref(g), depth, index, C.byref(sub), C.byref(i0), C.byref(j0)))
+    return sub, i0.value, j0.value
+
+
+def nb_of(g, p):
+    return 2 * (g.nx + g.ny) * (p - 2)
+
+
+def _empty_like_ref(ref, shape):
+    if hasattr(ref, "data_ptr"):
+        import torch
+        return torch.empty(shape, dtype=torch.complex128, device=ref.device)
+    return np.zeros(shape, complex)
+
+
 def zinv_batched(A):
     """Batched inverse through the library's Gauss-Jordan kernels (A: [batch, n, n] complex128)."""
     A = np.ascontiguousarray(A, dtype=np.complex128)
@@ -161,6 +188,22 @@ class Solver:
                 u = np.zeros((nrhs, self.nleaf, self.nt), complex)
         _check(lib().hps_solve(self.h, nrhs, _ptr(s, nrhs * self.nleaf * self.ni, "s"),
                                _ptr(t, nrhs * self.nb_root, "t"), _ptr(u, nrhs * self.nleaf * self.nt, "u")))
+        return u
+
+    def solve_up(self, s, nrhs, h_root=None):
+        """Upward pass only; returns the root's outgoing particular data [nrhs][nb_root]."""
+        if h_root is None:
+            h_root = _empty_like_ref(s if s is not None else np.zeros(1, complex), (nrhs, self.nb_root))
+        _check(lib().hps_solve_up(self.h, nrhs, _ptr(s, nrhs * self.nleaf * self.ni, "s"),
+                                  _ptr(h_root, nrhs * self.nb_root, "h_root")))
+        return h_root
+
+    def solve_down(self, t, u=None):
+        nrhs = int(t.shape[0])
+        if u is None:
+            u = _empty_like_ref(t, (nrhs, self.nleaf, self.nt))
+        _check(lib().hps_solve_down(self.h, nrhs, _ptr(t, nrhs * self.nb_root, "t"),
+                                    _ptr(u, nrhs * self.nleaf * self.nt, "u")))
         return u
 
     def nb(self, box):
@@ -201,6 +244,53 @@ class Solver:
             _check(lib().hps_kernel_stats(self.h, k, C.byref(n), C.byref(ms), C.byref(fl), C.byref(by)))
             out[name] = dict(launches=n.value, ms=ms.value, flops=fl.value, bytes=by.value)
         return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hps_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TopSolver:
+    """hps_build_top: the merge tree above `depth` from the gathered subtree-root operators."""
+
+    def __init__(self, g, p, kappa, eta, depth, R_sub, keep_root_R=True, device=-1, profile=False):
+        self.g, self.p, self.depth = g, p, depth
+        sub, _, _ = subtree_grid(g, depth, 0)
+        self.nb_sub = nb_of(sub, p)
+        self.nb_root = nb_of(g, p)
+        self.nsub = 1 << depth
+        opts = hps_opts(int(keep_root_R), 0, int(device), 0, int(profile), 0)
+        eta = complex(eta)
+        h = C.c_void_p()
+        _check(lib().hps_build_top(C.byref(g), p, p - 2, float(kappa), hps_c128(eta.real, eta.imag), depth,
+                                   _ptr(R_sub, self.nsub * self.nb_sub ** 2, "R_sub"), C.byref(opts), C.byref(h)))
+        self.h = h
+
+    def solve(self, h_sub, t_root, t_sub=None):
+        """h_sub [2^depth][nrhs][nb_sub] (or None), t_root [nrhs][nb_root] -> t_sub [2^depth][nrhs][nb_sub]."""
+        nrhs = int(t_root.shape[0])
+        if t_sub is None:
+            t_sub = _empty_like_ref(t_root, (self.nsub, nrhs, self.nb_sub))
+        _check(lib().hps_solve_top(self.h, nrhs, _ptr(h_sub, self.nsub * nrhs * self.nb_sub, "h_sub"),
+                                   _ptr(t_root, nrhs * self.nb_root, "t_root"),
+                                   _ptr(t_sub, self.nsub * nrhs * self.nb_sub, "t_sub")))
+        return t_sub
+
+    def R(self, box=1):
+        n = lib().hps_box_nb(self.h, box)
+        out = np.zeros((n, n), complex)
+        _check(lib().hps_export_R(self.h, box, out.ctypes.data))
+        return out
+
+    def time_ms(self, which):
+        return lib().hps_last_time_ms(self.h, which)
 
     def close(self):
         if getattr(self, "h", None):

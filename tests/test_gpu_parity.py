@@ -109,3 +109,35 @@ def test_batched_inverse_singular():
     A[0] = np.eye(40)
     with pytest.raises(hps.HpsError):
         hps.zinv_batched(A)
+
+
+@pytest.mark.parametrize("world,nx,ny,p", [(2, 4, 4, 8), (4, 8, 4, 6), (8, 8, 8, 6), (4, 32, 32, 16)])
+def test_virtual_ranks_match_single_gpu(world, nx, ny, p):
+    """Subtree sharding (dist.DistributedHPS) with `world` virtual ranks on one GPU equals the
+    single-handle build/solve: root R and every rank's u (SURVEY §8(e) parity)."""
+    import torch
+    from paper_1812_07167_b200 import dist
+    kappa, eta = 11.0, 11.0 + 2j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx, nrhs=3)
+    S = hps.Solver(g, p, kappa, eta, c)
+    u_ref = S.solve(s, t)
+    R_ref = S.R(1)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+    def rank_fn(comm):
+        sub, i0, j0 = dist.local_block(g, comm.world, comm.rank)
+        D = dist.DistributedHPS(comm, dist.CudaBackend(), g, p, kappa, eta,
+                                d(dist.slice_leaves(c, g, sub, i0, j0)))
+        u = D.solve(d(dist.slice_leaves(s, g, sub, i0, j0)), d(t)).cpu().numpy()
+        R = D.root_R()
+        D.close()
+        return u, R, (sub, i0, j0)
+
+    res = dist.run_threads(world, rank_fn)
+    for u, R, (sub, i0, j0) in res:
+        assert rel(R, R_ref) < 1e-11
+        assert rel(u, dist.slice_leaves(u_ref, g, sub, i0, j0)) < 1e-11
+    # and against the oracle for the smallest case
+    if nx * ny <= 16:
+        O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c)
+        assert rel(u_ref, O.solve(s, t)) < TOL
