@@ -173,6 +173,14 @@ int hps_reset_stats(hps_handle* h);
  * zero pivot.  Exposed for kernel-level tests. */
 int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* out);
 
+/* Batched complex GEMM through the library's DMMA kernel: C = alpha A B + beta Cin for
+ * contiguous row-major A [batch][M][K], B [batch][K][N], Cin / C [batch][M][N] (Cin may be
+ * NULL).  cfg selects a tile configuration (-1 = the library's choice); the call runs `reps`
+ * times after one warm-up and returns the mean device time in *ms.  Exposed for kernel tests
+ * and tuning. */
+int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A, const hps_c128* B,
+                      const hps_c128* Cin, hps_c128* C, hps_c128 alpha, hps_c128 beta, int reps, double* ms);
+
 void hps_free(hps_handle* h);
 const char* hps_last_error(void);
 

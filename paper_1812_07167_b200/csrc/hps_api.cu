@@ -1387,6 +1387,65 @@ int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* outp) {
   }
 }
 
+int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A, const hps_c128* B,
+                      const hps_c128* Cin, hps_c128* C, hps_c128 alpha, hps_c128 beta, int reps, double* ms) {
+  if (M <= 0 || N <= 0 || K < 0 || batch <= 0 || !A || !B || !C || reps < 1) {
+    hps_set_error("hps_zgemm_batched: invalid argument");
+    return HPS_EINVAL;
+  }
+  try {
+    cudaStream_t st;
+    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int dev;
+    HPS_CUDA_CHECK(cudaGetDevice(&dev));
+    retain_pool(dev);
+    g_alloc_stream = st;
+    {
+      const size_t ab = sizeof(zt) * (size_t)M * K * batch, bb = sizeof(zt) * (size_t)K * N * batch,
+                   cb = sizeof(zt) * (size_t)M * N * batch;
+      DevBuf ta, tb, tc;
+      const zt* a = dev_in(A, ab, ta, st);
+      const zt* b = dev_in(B, bb, tb, st);
+      const zt* ci = dev_in(Cin, cb, tc, st);
+      DevOut co(C, cb, st);
+      ZGemm g;
+      g.M = M;
+      g.N = N;
+      g.K = K;
+      g.batch = batch;
+      g.A = op(a, K, (int64_t)M * K);
+      g.B = op(b, N, (int64_t)K * N);
+      if (ci) g.Cin = op(ci, N, (int64_t)M * N);
+      g.C = out(co.dev, N, (int64_t)M * N);
+      g.alpha = make_double2(alpha.re, alpha.im);
+      g.beta = make_double2(beta.re, beta.im);
+      extern thread_local int g_zgemm_force;
+      g_zgemm_force = cfg;
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      zgemm(g, st);  // warm-up
+      cudaEventRecord(e0, st);
+      for (int r = 0; r < reps; ++r) zgemm(g, st);
+      cudaEventRecord(e1, st);
+      g_zgemm_force = -1;
+      HPS_CUDA_CHECK(cudaEventSynchronize(e1));
+      float t = 0;
+      cudaEventElapsedTime(&t, e0, e1);
+      if (ms) *ms = t / reps;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      co.finish(st);
+      HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+  return HPS_OK;
+}
+
 void hps_free(hps_handle* h) { delete h; }
 
 }  // extern "C"

@@ -292,20 +292,40 @@ void zgemm(const ZGemm& g, cudaStream_t st) {
   cudaEventDestroy(b);
 }
 
+thread_local int g_zgemm_force = -1;  // tile configuration override (tests / tuning)
+
+bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
+  switch (cfg) {
+    case 0: launch<64, 8, 16, 8>(g, st); return true;
+    case 1: launch<16, 16, 8, 8>(g, st); return true;
+    case 2: launch<32, 32, 16, 16>(g, st); return true;
+    case 3: launch<64, 64, 32, 32>(g, st); return true;
+    case 4: launch<64, 64, 32, 16>(g, st); return true;
+    case 5: launch<64, 32, 32, 16>(g, st); return true;
+    case 6: launch<32, 64, 16, 32>(g, st); return true;
+    case 7: launch<128, 64, 32, 32>(g, st); return true;
+    case 8: launch<64, 64, 16, 32>(g, st); return true;
+    default: return false;
+  }
+}
+
 void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return;
   const double mn = (double)g.M * g.N, bt = (double)g.batch;
   ProfScope ps(K_ZGEMM, 8.0 * mn * g.K * bt,
                16.0 * bt * ((double)g.M * g.K + (double)g.K * g.N + mn * (g.Cin.ptr ? 2.0 : 1.0)), st);
-  const int64_t t64 = (int64_t)((g.M + 63) / 64) * ((g.N + 63) / 64) * g.batch;
+  if (g_zgemm_force >= 0 && launch_cfg(g_zgemm_force, g, st)) return;
+  // Tile choice from the sweep in profiles/r01_gemm_tune.txt: 32x32 tiles (5 CTAs / SM) win
+  // for the short-K and Cin-heavy shapes of the merges and the Gauss-Jordan updates; 64x32 tiles
+  // win once K is long enough to amortise the tile loads.
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
-  else if (g.M <= 16 && g.N <= 16)
+  else if (g.M <= 16)
     launch<16, 16, 8, 8>(g, st);
-  else if (g.M <= 32 || g.N <= 32 || t64 < 296)
-    launch<32, 32, 16, 16>(g, st);
+  else if (g.K >= 512)
+    launch<64, 32, 32, 16>(g, st);
   else
-    launch<64, 64, 32, 32>(g, st);
+    launch<32, 32, 16, 16>(g, st);
 }
 
 void zcopy(const ZCopy& c, cudaStream_t st) {

@@ -39,7 +39,7 @@ class hps_opts(C.Structure):
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
            "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
-           "hps_solve_down", "hps_solve_top", "hps_free",
+           "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free",
            "hps_last_error"]
 
 KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout"]
@@ -75,6 +75,8 @@ def lib():
                                        C.POINTER(C.c_double)]
         L.hps_reset_stats.argtypes = [vp]
         L.hps_zinv_batched.argtypes = [i32, i32, dp, dp]
+        L.hps_zgemm_batched.argtypes = [i32, i32, i32, i32, i32, dp, dp, dp, dp, hps_c128, hps_c128, i32,
+                                        C.POINTER(C.c_double)]
         L.hps_subtree_grid.argtypes = [C.POINTER(hps_grid), i32, i64, C.POINTER(hps_grid), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32)]
         L.hps_build_top.argtypes = [C.POINTER(hps_grid), i32, i32, C.c_double, hps_c128, i32, dp,
@@ -149,6 +151,20 @@ def _empty_like_ref(ref, shape):
         import torch
         return torch.empty(shape, dtype=torch.complex128, device=ref.device)
     return np.zeros(shape, complex)
+
+
+def zgemm_batched(A, B, Cin=None, alpha=1.0, beta=0.0, cfg=-1, reps=1):
+    """C = alpha A B + beta Cin through the library's DMMA kernel; returns (C, ms per call).
+    A [batch, M, K], B [batch, K, N] (numpy complex128 or torch CUDA tensors)."""
+    batch, M, K = A.shape
+    N = B.shape[2]
+    out = _empty_like_ref(A, (batch, M, N))
+    ms = C.c_double()
+    a, b = complex(alpha), complex(beta)
+    _check(lib().hps_zgemm_batched(cfg, M, N, K, batch, _ptr(A, batch * M * K, "A"), _ptr(B, batch * K * N, "B"),
+                                   _ptr(Cin, batch * M * N, "Cin"), _ptr(out, batch * M * N, "C"),
+                                   hps_c128(a.real, a.imag), hps_c128(b.real, b.imag), reps, C.byref(ms)))
+    return out, ms.value
 
 
 def zinv_batched(A):

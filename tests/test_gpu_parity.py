@@ -141,3 +141,18 @@ def test_virtual_ranks_match_single_gpu(world, nx, ny, p):
     if nx * ny <= 16:
         O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c)
         assert rel(u_ref, O.solve(s, t)) < TOL
+
+
+@pytest.mark.parametrize("cfg", list(range(9)))
+@pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1)])
+def test_zgemm_configs(cfg, M, N, K, batch):
+    """Every DMMA tile configuration vs the oracle's triple-loop product (ragged edges, beta)."""
+    rng = np.random.default_rng(M * 1000 + N + K)
+    A = rng.standard_normal((batch, M, K)) + 1j * rng.standard_normal((batch, M, K))
+    B = rng.standard_normal((batch, K, N)) + 1j * rng.standard_normal((batch, K, N))
+    Cin = rng.standard_normal((batch, M, N)) + 1j * rng.standard_normal((batch, M, N))
+    for alpha, beta in [(1.0, 1.0), (-1.0, 0.5 - 2j)]:
+        C, _ = hps.zgemm_batched(A, B, Cin, alpha, beta, cfg=cfg)
+        for b in range(batch):
+            ref = alpha * oracle.matmul(A[b], B[b]) + beta * Cin[b]
+            assert rel(C[b], ref) < 1e-13
