@@ -219,16 +219,28 @@ __device__ __forceinline__ void store_rotated(const zt (&row)[NB], zt* dst, int 
   }
 }
 
+// Pivot key: the high 32 bits of |z|^2 (sign 0, exponent, 20 mantissa bits: monotone in |z|^2),
+// low 9 bits replaced by (511 - local row) so one unsigned max picks the largest magnitude and,
+// among magnitudes equal to ~1e-4 relative, the lowest row (threshold partial pivoting; a
+// pivot within that tolerance of the column maximum keeps the growth bound of partial pivoting).
+__device__ __forceinline__ unsigned pivot_key(zt f, int local, bool valid) {
+  if (!valid) return 0u;
+  const double m = f.x * f.x + f.y * f.y;
+  const unsigned hi = (unsigned)(__double_as_longlong(m) >> 32);
+  return (hi & ~511u) | (unsigned)(511 - local);
+}
+
 // ---------------------------------------------------------------------------
-// Register-resident panel, n <= 256: thread t owns panel row t in registers; the rank-1
-// update is register-local; per step two barriers and one shared broadcast of the scaled pivot
-// row (plus the displaced row k).
+// Register-resident panel, n <= THREADS (256 or 512): thread t owns panel row t in registers;
+// the rank-1 update is register-local; per step two barriers, one warp max-reduction
+// (REDUX) of packed pivot keys and one shared broadcast of the raw pivot row (plus the
+// displaced row k).
 // ---------------------------------------------------------------------------
-template <int NB>
-__global__ void __launch_bounds__(256) zgj_panel_reg_kernel(const PanelArgs a) {
+template <int NB, int THREADS>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS) zgj_panel_reg_kernel(const PanelArgs a) {
+  constexpr int NW = THREADS / 32;
   __shared__ zt prow[NB], tmp[NB];
-  __shared__ double rv[8];
-  __shared__ int ri[8];
+  __shared__ unsigned wkey[NW];
   __shared__ int s_orig_r, s_orig_k;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x, n = a.n, k0 = a.k0, w = a.w;
@@ -243,25 +255,16 @@ __global__ void __launch_bounds__(256) zgj_panel_reg_kernel(const PanelArgs a) {
   bool singular = false;
   for (int kk = 0; kk < w; ++kk) {
     const int k = k0 + kk;
-    double bv = -1.0;
-    int bi = 0x7fffffff;
-    if (i < n && i >= k) {
-      bv = zabs2(row[0]);
-      bi = i;
-    }
-    warp_amax(bv, bi);
-    if (lane == 0) {
-      rv[warp] = bv;
-      ri[warp] = bi;
-    }
+    const unsigned key = __reduce_max_sync(0xffffffffu, pivot_key(row[0], i, i < n && i >= k));
+    if (lane == 0) wkey[warp] = key;
     __syncthreads();
-    double gv = rv[0];
-    int r = ri[0];
+    unsigned best = wkey[0];
 #pragma unroll
-    for (int w2 = 1; w2 < 8; ++w2) amax_merge(gv, r, rv[w2], ri[w2]);
-    if (gv <= 0.0) {
+    for (int w2 = 1; w2 < NW; ++w2) best = max(best, wkey[w2]);
+    int r = 511 - (int)(best & 511u);
+    if ((best & ~511u) == 0u) {  // exactly zero column below the diagonal
       singular = true;
-      if (r == 0x7fffffff) r = k;
+      r = k;
     }
     if (i == r) {  // publish the raw pivot row
 #pragma unroll
@@ -312,8 +315,7 @@ __global__ void __launch_bounds__(256) zgj_panel_creg_kernel(const PanelArgs a) 
   const int c = (int)cluster.block_rank();
   const int b = blockIdx.x / CS, n = a.n, k0 = a.k0, w = a.w;
   __shared__ zt prow[NB], tmp[NB], lprow[NB];
-  __shared__ double rv[8];
-  __shared__ int ri[8];
+  __shared__ unsigned wkey[8];
   __shared__ Slot slot;
   __shared__ int s_r, orig_r_pub, orig_k_pub;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -328,37 +330,33 @@ __global__ void __launch_bounds__(256) zgj_panel_creg_kernel(const PanelArgs a) 
   bool singular = false;
   for (int kk = 0; kk < w; ++kk) {
     const int k = k0 + kk;
-    double bv = -1.0;
-    int bi = 0x7fffffff;
-    if (i < n && i >= k) {
-      bv = zabs2(row[0]);
-      bi = i;
-    }
-    warp_amax(bv, bi);
-    if (lane == 0) {
-      rv[warp] = bv;
-      ri[warp] = bi;
-    }
+    const unsigned key = __reduce_max_sync(0xffffffffu, pivot_key(row[0], tid, i < n && i >= k));
+    if (lane == 0) wkey[warp] = key;
     __syncthreads();
     if (tid == 0) {
-      for (int w2 = 1; w2 < 8; ++w2) amax_merge(bv, bi, rv[w2], ri[w2]);
-      slot.v = bv;
-      slot.i = bi;
+      unsigned best = wkey[0];
+      for (int w2 = 1; w2 < 8; ++w2) best = max(best, wkey[w2]);
+      slot.v = 0.0;
+      slot.i = (int)best;  // packed key of this CTA's best row
     }
     cluster.sync();  // (1) candidates visible
     if (warp == 0) {
-      double gv = -1.0;
-      int gi = 0x7fffffff;
-      if (lane < CS) {
-        const Slot* rs = cluster.map_shared_rank(&slot, lane);
-        gv = rs->v;
-        gi = rs->i;
+      // cluster-wide: larger key wins; equal keys -> lower CTA rank (lower row)
+      const unsigned ck = lane < CS ? (unsigned)cluster.map_shared_rank(&slot, lane)->i : 0u;
+      const unsigned long long k64 = ((unsigned long long)ck << 32) | (unsigned)(31 - lane);
+      unsigned long long bestk = k64;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long o64 = __shfl_xor_sync(0xffffffffu, bestk, o);
+        bestk = o64 > bestk ? o64 : bestk;
       }
-      warp_amax(gv, gi);
       if (lane == 0) {
-        if (gv <= 0.0) {
+        const unsigned kb = (unsigned)(bestk >> 32);
+        const int crank = 31 - (int)(bestk & 31u);
+        int gi = crank * 256 + (511 - (int)(kb & 511u));
+        if ((kb & ~511u) == 0u) {
           singular = true;
-          if (gi == 0x7fffffff) gi = k;
+          gi = k;
         }
         s_r = gi;
       }
@@ -553,9 +551,10 @@ int pow2_ceil(int v) {
 
 PanelPlan panel_plan(int n) {
   if (n <= 4096) {
-    const int npan = (n + 31) / 32;
+    const int wmax = (n > 256 && n <= 512) ? 16 : 32;  // 512-thread panels hold 16 columns per thread
+    const int npan = (n + wmax - 1) / wmax;
     const int nb = (n + npan - 1) / npan;  // equal panels, no narrow tail
-    if (n <= 256) return PanelPlan{0, nb, 1, n, 0};
+    if (n <= 512) return PanelPlan{0, nb, 1, n, 0};
     return PanelPlan{1, nb, pow2_ceil((n + 255) / 256), 256, 0};
   }
   const size_t budget = 150 * 1024;
@@ -634,7 +633,12 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)w * w * batch, 32.0 * n * (double)w * batch, st);
       if (pp.mode == 0) {
-        zgj_panel_reg_kernel<32><<<batch, 256, 0, st>>>(pa);
+        if (n <= 256 && pp.nb <= 28)
+          zgj_panel_reg_kernel<28, 256><<<batch, 256, 0, st>>>(pa);
+        else if (n <= 256)
+          zgj_panel_reg_kernel<32, 256><<<batch, 256, 0, st>>>(pa);
+        else
+          zgj_panel_reg_kernel<16, 512><<<batch, 512, 0, st>>>(pa);
         HPS_CUDA_CHECK(cudaGetLastError());
       } else if (pp.mode == 1) {
         void* args[] = {&pa};
