@@ -509,6 +509,146 @@ __global__ void __launch_bounds__(kThreads) zgj_panel_smem_kernel(const PanelArg
   cluster.sync();
 }
 
+// ---------------------------------------------------------------------------
+// Fused whole-matrix Gauss-Jordan, n <= THREADS: one CTA per matrix, in place.  Thread i owns
+// row i.  For each panel of w <= NB columns: the panel is factored with its rows in registers
+// (as zgj_panel_reg), written back, then the CTA streams the other columns in chunks of CH:
+// every thread loads its SOURCE row's chunk (row permutation of the panel's swaps), panel rows
+// park theirs in shared memory (Z) and restart from zero, and each thread accumulates
+// sum_kk T(i,kk) Z(kk,:) with DFMA (B200: FP64 SIMT peak ~= DMMA peak).  No ping-pong buffer,
+// no launches between panels, the matrix stays in the SM's L1/L2.  The column swaps are
+// undone while writing the result to `out`.
+// ---------------------------------------------------------------------------
+template <int NB, int THREADS, int CH>
+__global__ void __launch_bounds__(THREADS, 1) zgj_fused_kernel(zt* __restrict__ A, int64_t lda,
+                                                                           int64_t bs, zt* __restrict__ out,
+                                                                           int64_t ldo, int64_t obs, int n,
+                                                                           int* __restrict__ info) {
+  constexpr int NW = THREADS / 32;
+  __shared__ zt prow[NB], tmp[NB];
+  __shared__ zt Zs[NB][CH];
+  __shared__ unsigned wkey[NW];
+  __shared__ int s_orig_r, s_orig_k;
+  __shared__ int piv_s[THREADS], pi_s[THREADS];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
+  zt* Ab = A + (int64_t)b * bs;
+  const int i = tid;
+  const bool live = i < n;
+  bool singular = false;
+  for (int k0 = 0; k0 < n; k0 += NB) {
+    const int w = min(NB, n - k0);
+    zt row[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) row[j] = (live && j < w) ? Ab[(int64_t)i * lda + k0 + j] : make_double2(0.0, 0.0);
+    int orig = i;
+    for (int kk = 0; kk < w; ++kk) {
+      const int k = k0 + kk;
+      const unsigned key = __reduce_max_sync(0xffffffffu, pivot_key(row[0], i, live && i >= k));
+      if (lane == 0) wkey[warp] = key;
+      __syncthreads();
+      unsigned best = wkey[0];
+#pragma unroll
+      for (int w2 = 1; w2 < NW; ++w2) best = max(best, wkey[w2]);
+      int r = 511 - (int)(best & 511u);
+      if ((best & ~511u) == 0u) {
+        singular = true;
+        r = k;
+      }
+      if (i == r) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) prow[j] = row[j];
+        s_orig_r = orig;
+      }
+      if (i == k && r != k) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) tmp[j] = row[j];
+        s_orig_k = orig;
+      }
+      __syncthreads();
+      const zt inv = zinv_fast(prow[0]);
+      if (i == k) {
+        row_pivot<NB>(row, prow, inv);
+        orig = s_orig_r;
+      } else {
+        if (i == r) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) row[j] = tmp[j];
+          orig = s_orig_k;
+        }
+        row_step<NB>(row, prow, inv);
+      }
+      row_rotate<NB>(row);
+      if (tid == 0) piv_s[k] = r;
+    }
+    for (int e = w; e < NB; ++e) row_rotate<NB>(row);  // slot j = panel column j again
+    if (live)
+#pragma unroll
+      for (int j = 0; j < NB; ++j)
+        if (j < w) Ab[(int64_t)i * lda + k0 + j] = row[j];
+    __syncthreads();  // trailing reads below see every row's previous-panel update
+    // trailing columns J = [0, k0) U [k0 + w, n) in chunks of CH (indices into J)
+    const int nc = n - w;
+    const bool prow_i = i >= k0 && i < k0 + w;
+    for (int c0 = 0; c0 < nc; c0 += CH) {
+      zt acc[CH];
+#pragma unroll
+      for (int jj = 0; jj < CH; ++jj) {
+        const int cj = c0 + jj;
+        const int col = cj < k0 ? cj : cj + w;
+        acc[jj] = (live && cj < nc) ? Ab[(int64_t)orig * lda + col] : make_double2(0.0, 0.0);
+      }
+      __syncthreads();  // previous chunk finished reading Zs
+      if (prow_i) {
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          Zs[i - k0][jj] = acc[jj];
+          acc[jj] = make_double2(0.0, 0.0);
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < NB; ++kk) {
+        if (kk < w) {
+          const zt t = row[kk];
+#pragma unroll
+          for (int jj = 0; jj < CH; ++jj) {
+            const zt z = Zs[kk][jj];
+            acc[jj].x = fma(t.x, z.x, acc[jj].x);
+            acc[jj].x = fma(-t.y, z.y, acc[jj].x);
+            acc[jj].y = fma(t.x, z.y, acc[jj].y);
+            acc[jj].y = fma(t.y, z.x, acc[jj].y);
+          }
+        }
+      }
+      if (live)
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          const int cj = c0 + jj;
+          if (cj < nc) Ab[(int64_t)i * lda + (cj < k0 ? cj : cj + w)] = acc[jj];
+        }
+    }
+    __syncthreads();
+  }
+  // undo the column swaps: out(i, j) = A(i, pi(j)),  pi = S_{n-1} o ... o S_0
+  if (tid == 0) {
+    for (int j = 0; j < n; ++j) pi_s[j] = j;
+    for (int k = n - 1; k >= 0; --k) {
+      const int r = piv_s[k];
+      const int t = pi_s[k];
+      pi_s[k] = pi_s[r];
+      pi_s[r] = t;
+    }
+  }
+  __syncthreads();
+  if (live) {
+    zt* ob = out + (int64_t)b * obs + (int64_t)i * ldo;
+    const zt* ar = Ab + (int64_t)i * lda;
+    for (int j = 0; j < n; ++j) ob[j] = ar[pi_s[j]];
+  }
+  if (singular && tid == 0) atomicCAS(info, 0, b + 1);
+}
+
 // pi = S_{n-1} o ... o S_0 (one thread per matrix)
 __global__ void zgj_pi_kernel(const int* piv_all, int* pi_all, int n, int batch) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -568,7 +708,8 @@ PanelPlan panel_plan(int n) {
   return PanelPlan{2, 16, 16, rp, sizeof(zt) * ((size_t)rp * 16 + 32) + 64 + sizeof(int) * rp};
 }
 
-bool use_small(int n, int batch) { return n <= kSmallMax && (n <= 32 || batch >= 2 * 148); }
+bool use_small(int n, int batch) { return n <= 32; }
+bool use_fused(int n, int batch) { return n > 32 && n <= 256 && (batch >= 16 || n <= 128); }
 
 void launch_cluster(const void* kern, int grid, int cs, size_t smem, cudaStream_t st, void** args) {
   cudaLaunchConfig_t cfg = {};
@@ -603,6 +744,17 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
       const int nbatch = std::min(65535, batch - b0);
       zgj_small_kernel<<<nbatch, kThreads, smem, st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
                                                        obs, n, info);
+      HPS_CUDA_CHECK(cudaGetLastError());
+      count_launch();
+    }
+    return;
+  }
+  if (use_fused(n, batch)) {
+    ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
+    for (int b0 = 0; b0 < batch; b0 += 65535) {
+      const int nbatch = std::min(65535, batch - b0);
+      zgj_fused_kernel<28, 256, 8><<<nbatch, 256, 0, st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs,
+                                                            ldo, obs, n, info);
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
     }
@@ -702,7 +854,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
 }  // namespace
 
 size_t zgj_workspace_bytes(int n, int batch) {
-  if (use_small(n, batch)) return 16;
+  if (use_small(n, batch) || use_fused(n, batch)) return 16;
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256;
 }
