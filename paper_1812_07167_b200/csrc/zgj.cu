@@ -194,8 +194,12 @@ __device__ __forceinline__ void row_step(zt (&row)[NB], const zt* pr, zt inv) {
   for (int j = 1; j < NB; ++j) {
     const zt pj = pr[j];
     row[j].x = fma(ngx, pj.x, row[j].x);
-    row[j].x = fma(g.y, pj.y, row[j].x);
     row[j].y = fma(ngx, pj.y, row[j].y);
+  }
+#pragma unroll
+  for (int j = 1; j < NB; ++j) {
+    const zt pj = pr[j];
+    row[j].x = fma(g.y, pj.y, row[j].x);
     row[j].y = fma(ngy, pj.x, row[j].y);
   }
   row[0] = make_double2(ngx, ngy);
@@ -509,27 +513,41 @@ __global__ void __launch_bounds__(kThreads) zgj_panel_smem_kernel(const PanelArg
   cluster.sync();
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
 // ---------------------------------------------------------------------------
-// Fused whole-matrix Gauss-Jordan, n <= THREADS: one CTA per matrix, in place.  Thread i owns
-// row i.  For each panel of w <= NB columns: the panel is factored with its rows in registers
-// (as zgj_panel_reg), written back, then the CTA streams the other columns in chunks of CH:
-// every thread loads its SOURCE row's chunk (row permutation of the panel's swaps), panel rows
-// park theirs in shared memory (Z) and restart from zero, and each thread accumulates
-// sum_kk T(i,kk) Z(kk,:) with DFMA (B200: FP64 SIMT peak ~= DMMA peak).  No ping-pong buffer,
-// no launches between panels, the matrix stays in the SM's L1/L2.  The column swaps are
-// undone while writing the result to `out`.
+// Fused whole-matrix Gauss-Jordan, n <= 256: one CTA (8 warps) per matrix, in place.
+// For each panel of w <= NB = 28 columns:
+//  * panel phase: thread i owns row i of the panel in registers (as zgj_panel_reg: packed-key
+//    REDUX pivot search, raw pivot-row broadcast, rotated rows); the transform T (n x w) is
+//    parked in shared memory and written back to the panel columns;
+//  * update phase (FP64 tensor cores): the other columns, in chunks of CH = 32, are gathered
+//    through the panel's row permutation straight into DMMA accumulator fragments (warp w owns
+//    rows 32w .. 32w+31), panel rows park theirs in shared memory (Z) and restart from zero,
+//    and  C += T Z  runs as m8n8k4 DMMAs (complex = 4 real products) with T and Z fragments
+//    from shared memory; the chunk is stored back in place.
+// No ping-pong buffer and no launch per panel.  The column swaps are undone while writing the
+// result to `out`.  Dynamic shared memory: T [n][28] (stride 28 = 4 mod 8 complex: conflict-free
+// A fragments) + Z [28][34].
 // ---------------------------------------------------------------------------
-template <int NB, int THREADS, int CH>
-__global__ void __launch_bounds__(THREADS, 1) zgj_fused_kernel(zt* __restrict__ A, int64_t lda,
-                                                                           int64_t bs, zt* __restrict__ out,
-                                                                           int64_t ldo, int64_t obs, int n,
-                                                                           int* __restrict__ info) {
-  constexpr int NW = THREADS / 32;
+constexpr int FU_NB = 28;
+
+template <int CH, int MINB>
+__global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
+                                                           zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
+                                                           int* __restrict__ info) {
+  constexpr int NB = FU_NB, ZS = CH + 2, NW = 8, TN = CH / 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [n][NB]
+  zt* Zs = Ts + n * NB;                       // [NB][ZS]
   __shared__ zt prow[NB], tmp[NB];
-  __shared__ zt Zs[NB][CH];
   __shared__ unsigned wkey[NW];
   __shared__ int s_orig_r, s_orig_k;
-  __shared__ int piv_s[THREADS], pi_s[THREADS];
+  __shared__ int piv_s[256], pi_s[256], orig_s[256];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = blockIdx.x;
   zt* Ab = A + (int64_t)b * bs;
@@ -538,97 +556,136 @@ __global__ void __launch_bounds__(THREADS, 1) zgj_fused_kernel(zt* __restrict__ 
   bool singular = false;
   for (int k0 = 0; k0 < n; k0 += NB) {
     const int w = min(NB, n - k0);
-    zt row[NB];
+    {  // ---- panel phase ----
+      int orig = i;
+      zt row[NB];
 #pragma unroll
-    for (int j = 0; j < NB; ++j) row[j] = (live && j < w) ? Ab[(int64_t)i * lda + k0 + j] : make_double2(0.0, 0.0);
-    int orig = i;
-    for (int kk = 0; kk < w; ++kk) {
-      const int k = k0 + kk;
-      const unsigned key = __reduce_max_sync(0xffffffffu, pivot_key(row[0], i, live && i >= k));
-      if (lane == 0) wkey[warp] = key;
-      __syncthreads();
-      unsigned best = wkey[0];
+      for (int j = 0; j < NB; ++j) row[j] = (live && j < w) ? Ab[(int64_t)i * lda + k0 + j] : make_double2(0.0, 0.0);
+      for (int kk = 0; kk < w; ++kk) {
+        const int k = k0 + kk;
+        const unsigned key = __reduce_max_sync(0xffffffffu, pivot_key(row[0], i, live && i >= k));
+        if (lane == 0) wkey[warp] = key;
+        __syncthreads();
+        unsigned best = wkey[0];
 #pragma unroll
-      for (int w2 = 1; w2 < NW; ++w2) best = max(best, wkey[w2]);
-      int r = 511 - (int)(best & 511u);
-      if ((best & ~511u) == 0u) {
-        singular = true;
-        r = k;
-      }
-      if (i == r) {
-#pragma unroll
-        for (int j = 0; j < NB; ++j) prow[j] = row[j];
-        s_orig_r = orig;
-      }
-      if (i == k && r != k) {
-#pragma unroll
-        for (int j = 0; j < NB; ++j) tmp[j] = row[j];
-        s_orig_k = orig;
-      }
-      __syncthreads();
-      const zt inv = zinv_fast(prow[0]);
-      if (i == k) {
-        row_pivot<NB>(row, prow, inv);
-        orig = s_orig_r;
-      } else {
+        for (int w2 = 1; w2 < NW; ++w2) best = max(best, wkey[w2]);
+        int r = 511 - (int)(best & 511u);
+        if ((best & ~511u) == 0u) {
+          singular = true;
+          r = k;
+        }
         if (i == r) {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) row[j] = tmp[j];
-          orig = s_orig_k;
+          for (int j = 0; j < NB; ++j) prow[j] = row[j];
+          s_orig_r = orig;
         }
-        row_step<NB>(row, prow, inv);
-      }
-      row_rotate<NB>(row);
-      if (tid == 0) piv_s[k] = r;
-    }
-    for (int e = w; e < NB; ++e) row_rotate<NB>(row);  // slot j = panel column j again
-    if (live)
+        if (i == k && r != k) {
 #pragma unroll
-      for (int j = 0; j < NB; ++j)
-        if (j < w) Ab[(int64_t)i * lda + k0 + j] = row[j];
-    __syncthreads();  // trailing reads below see every row's previous-panel update
-    // trailing columns J = [0, k0) U [k0 + w, n) in chunks of CH (indices into J)
-    const int nc = n - w;
-    const bool prow_i = i >= k0 && i < k0 + w;
-    for (int c0 = 0; c0 < nc; c0 += CH) {
-      zt acc[CH];
-#pragma unroll
-      for (int jj = 0; jj < CH; ++jj) {
-        const int cj = c0 + jj;
-        const int col = cj < k0 ? cj : cj + w;
-        acc[jj] = (live && cj < nc) ? Ab[(int64_t)orig * lda + col] : make_double2(0.0, 0.0);
-      }
-      __syncthreads();  // previous chunk finished reading Zs
-      if (prow_i) {
-#pragma unroll
-        for (int jj = 0; jj < CH; ++jj) {
-          Zs[i - k0][jj] = acc[jj];
-          acc[jj] = make_double2(0.0, 0.0);
+          for (int j = 0; j < NB; ++j) tmp[j] = row[j];
+          s_orig_k = orig;
         }
-      }
-      __syncthreads();
+        __syncthreads();
+        const zt inv = zinv_fast(prow[0]);
+        if (i == k) {
+          row_pivot<NB>(row, prow, inv);
+          orig = s_orig_r;
+        } else {
+          if (i == r) {
 #pragma unroll
-      for (int kk = 0; kk < NB; ++kk) {
-        if (kk < w) {
-          const zt t = row[kk];
-#pragma unroll
-          for (int jj = 0; jj < CH; ++jj) {
-            const zt z = Zs[kk][jj];
-            acc[jj].x = fma(t.x, z.x, acc[jj].x);
-            acc[jj].x = fma(-t.y, z.y, acc[jj].x);
-            acc[jj].y = fma(t.x, z.y, acc[jj].y);
-            acc[jj].y = fma(t.y, z.x, acc[jj].y);
+            for (int j = 0; j < NB; ++j) row[j] = tmp[j];
+            orig = s_orig_k;
           }
+          row_step<NB>(row, prow, inv);
+        }
+        row_rotate<NB>(row);
+        if (tid == 0) piv_s[k] = r;
+      }
+      // after w rotations register slot p holds panel column (p + w) mod NB
+      if (live) {
+#pragma unroll
+        for (int p = 0; p < NB; ++p) {
+          int j = p + w;
+          if (j >= NB) j -= NB;
+          Ts[i * NB + j] = (j < w) ? row[p] : make_double2(0.0, 0.0);
+          if (j < w) Ab[(int64_t)i * lda + k0 + j] = row[p];
         }
       }
-      if (live)
-#pragma unroll
-        for (int jj = 0; jj < CH; ++jj) {
-          const int cj = c0 + jj;
-          if (cj < nc) Ab[(int64_t)i * lda + (cj < k0 ? cj : cj + w)] = acc[jj];
-        }
+      orig_s[i] = live ? orig : 0;
     }
     __syncthreads();
+    // ---- update phase: other columns J = [0, k0) U [k0 + w, n), chunks of CH ----
+    const int nc = n - w;
+    const int rbase = warp * 32;
+    for (int c0 = 0; c0 < nc; c0 += CH) {
+      double accr[4][TN][2], acci[4][TN][2];
+      // gather the permuted chunk into the accumulator fragments; panel rows go to Z
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        const int rr = rbase + mi * 8 + (lane >> 2);
+        const bool rlive = rr < n;
+        const zt* src = Ab + (int64_t)(rlive ? orig_s[rr] : 0) * lda;
+        const bool is_p = rr >= k0 && rr < k0 + w;
+#pragma unroll
+        for (int ni = 0; ni < TN; ++ni)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cl = ni * 8 + (lane & 3) * 2 + h;
+            const int cj = c0 + cl;
+            zt v = make_double2(0.0, 0.0);
+            if (rlive && cj < nc) v = src[cj < k0 ? cj : cj + w];
+            if (is_p) {
+              Zs[(rr - k0) * ZS + cl] = v;
+              v = make_double2(0.0, 0.0);
+            }
+            accr[mi][ni][h] = v.x;
+            acci[mi][ni][h] = v.y;
+          }
+      }
+      __syncthreads();  // Z complete; every gather of this chunk done before any store below
+      if (rbase < n) {
+#pragma unroll
+        for (int k4 = 0; k4 < NB / 4; ++k4) {
+          zt af[4], bf[TN];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi) {
+            const int rr = min(rbase + mi * 8 + (lane >> 2), n - 1);
+            af[mi] = Ts[rr * NB + k4 * 4 + (lane & 3)];
+          }
+#pragma unroll
+          for (int ni = 0; ni < TN; ++ni) bf[ni] = Zs[(k4 * 4 + (lane & 3)) * ZS + ni * 8 + (lane >> 2)];
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < TN; ++ni) dmma884(accr[mi][ni][0], accr[mi][ni][1], af[mi].x, bf[ni].x);
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < TN; ++ni) dmma884(acci[mi][ni][0], acci[mi][ni][1], af[mi].x, bf[ni].y);
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < TN; ++ni) dmma884(accr[mi][ni][0], accr[mi][ni][1], -af[mi].y, bf[ni].y);
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < TN; ++ni) dmma884(acci[mi][ni][0], acci[mi][ni][1], af[mi].y, bf[ni].x);
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int rr = rbase + mi * 8 + (lane >> 2);
+          if (rr >= n) continue;
+          zt* dst = Ab + (int64_t)rr * lda;
+#pragma unroll
+          for (int ni = 0; ni < TN; ++ni)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int cj = c0 + ni * 8 + (lane & 3) * 2 + h;
+              if (cj < nc) dst[cj < k0 ? cj : cj + w] = make_double2(accr[mi][ni][h], acci[mi][ni][h]);
+            }
+        }
+      }
+      __syncthreads();  // Z reusable; this chunk's stores visible to the next panel
+    }
   }
   // undo the column swaps: out(i, j) = A(i, pi(j)),  pi = S_{n-1} o ... o S_0
   if (tid == 0) {
@@ -641,10 +698,10 @@ __global__ void __launch_bounds__(THREADS, 1) zgj_fused_kernel(zt* __restrict__ 
     }
   }
   __syncthreads();
-  if (live) {
-    zt* ob = out + (int64_t)b * obs + (int64_t)i * ldo;
-    const zt* ar = Ab + (int64_t)i * lda;
-    for (int j = 0; j < n; ++j) ob[j] = ar[pi_s[j]];
+  zt* ob = out + (int64_t)b * obs;
+  for (int e = tid; e < n * n; e += 256) {
+    const int r = e / n, j = e % n;
+    ob[(int64_t)r * ldo + j] = Ab[(int64_t)r * lda + pi_s[j]];
   }
   if (singular && tid == 0) atomicCAS(info, 0, b + 1);
 }
@@ -753,8 +810,21 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
-      zgj_fused_kernel<28, 256, 8><<<nbatch, 256, 0, st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs,
-                                                            ldo, obs, n, info);
+      static int fcfg = -1;
+      if (fcfg < 0) {
+        const char* e = getenv("HPS_FUSED_CFG");
+        fcfg = (e && *e == '1') ? 1 : 0;
+        HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_fused_kernel<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(sizeof(zt) * (256 * FU_NB + FU_NB * 18))));
+        HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_fused_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(sizeof(zt) * (256 * FU_NB + FU_NB * 34))));
+      }
+      if (fcfg == 0)
+        zgj_fused_kernel<16, 2><<<nbatch, 256, sizeof(zt) * ((size_t)n * FU_NB + FU_NB * 18), st>>>(
+            A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo, obs, n, info);
+      else
+        zgj_fused_kernel<32, 1><<<nbatch, 256, sizeof(zt) * ((size_t)n * FU_NB + FU_NB * 34), st>>>(
+            A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo, obs, n, info);
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
     }

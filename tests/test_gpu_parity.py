@@ -62,6 +62,17 @@ def test_every_R_and_u(nx, ny, p):
     assert rel(u0, O.solve(np.zeros_like(s), t)) < TOL
 
 
+def test_leaf_parity_batched_p16():
+    """16 leaves at p = 16: the batched (fused) interior inversion path, several leaves vs oracle."""
+    g, c, s, t = problem(4, 4, 16, 30.0, 30.0 + 3j)
+    S = hps.Solver(g, 16, 30.0, 30.0 + 3j, c)
+    for leaf in [0, 5, 15]:
+        Psi, Y = S.leaf_ops(leaf)
+        lo = oracle.leaf(16, 0.25, 0.25, 30.0, 30.0 + 3j, c[leaf])
+        assert rel(Psi, lo["Psi"]) < TOL
+        assert rel(Y, lo["Y"]) < TOL
+
+
 def test_config1_plane_wave():
     cfg = inputs.CONFIGS[1]
     g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
@@ -88,7 +99,8 @@ def test_torch_device_buffers():
     assert rel(u, O.solve(s, t)) < TOL
 
 
-@pytest.mark.parametrize("n,batch", [(14, 300), (20, 2), (33, 3), (60, 400), (100, 5), (196, 7), (252, 2),
+@pytest.mark.parametrize("n,batch", [(14, 300), (20, 2), (33, 3), (60, 400), (100, 5), (196, 7), (196, 40), (252, 2),
+                                     (252, 17), (230, 16), (57, 20),
                                      (257, 1), (300, 2), (448, 1), (700, 1), (1100, 1), (4200, 1)])
 def test_batched_inverse(n, batch):
     """The Gauss-Jordan kernels (small, register panel, cluster panel) vs the oracle's LU."""
