@@ -148,11 +148,17 @@ __device__ __forceinline__ void zfma(zt& acc, zt a, zt b) {
 }
 
 // store[l] = [Psi | Y] (nt x nt, row-major); on entry its (I_i, I_i) block holds S^{-1}.
-__global__ void leaf_schur_finish_kernel(zt* __restrict__ store, int64_t sstride, int leaf0, int nchunk, int p,
-                                         const zt* __restrict__ K) {
+// Psi_i: each warp stages one row of S^{-1} in shared memory (one coalesced read) and its lanes
+// form the 4q outputs of that row.  Y_b and Psi_b: the two boundary nodes of a grid line read
+// the same rows, so each thread forms both (S_k with N_k, W_k with E_k): S^{-1} is read twice.
+// Dynamic shared memory: 8 warps x n_i complex.
+__global__ void __launch_bounds__(256) leaf_schur_finish_kernel(zt* __restrict__ store, int64_t sstride, int leaf0,
+                                                                int nchunk, int p, const zt* __restrict__ K) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lc = blockIdx.x;
   if (lc >= nchunk) return;
   const int q = p - 2, ni = q * q, nb = 4 * q, nt = nb + ni;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const zt* Ubx = K + 2 * q * q;
   const zt* Uby = Ubx + 2 * q;
   const zt* Vx = Uby + 2 * q;
@@ -161,50 +167,80 @@ __global__ void leaf_schur_finish_kernel(zt* __restrict__ store, int64_t sstride
   const zt* Gy = Gx + 4;
   zt* base = store + (int64_t)(leaf0 + lc) * sstride;
   const zt* Si = base + (int64_t)nb * nt + nb;  // S^{-1}, ld nt
+  zt* rowbuf = reinterpret_cast<zt*>(smem_raw) + warp * ni;
   // Psi_i = S^{-1} Ub
-  for (int e = threadIdx.x; e < ni * nb; e += blockDim.x) {
-    const int r = e / nb, b = e % nb, edge = b / q, k = b % q;
-    zt acc = make_double2(0.0, 0.0);
-    if (edge == 0 || edge == 2) {  // S_k / N_k: y-line ix = k
-      const int side = edge == 0 ? 0 : 1;
-      for (int t = 0; t < q; ++t) zfma(acc, Si[(int64_t)r * nt + t * q + k], Uby[t * 2 + side]);
-    } else {                       // E_k / W_k: x-line iy = k
-      const int side = edge == 3 ? 0 : 1;
-      for (int t = 0; t < q; ++t) zfma(acc, Si[(int64_t)r * nt + k * q + t], Ubx[t * 2 + side]);
+  for (int r = warp; r < ni; r += 8) {
+    for (int c = lane; c < ni; c += 32) rowbuf[c] = Si[(int64_t)r * nt + c];
+    __syncwarp();
+    for (int b = lane; b < nb; b += 32) {
+      const int edge = b / q, k = b % q;
+      zt acc = make_double2(0.0, 0.0);
+      if (edge == 0 || edge == 2) {  // S_k / N_k: y-line ix = k
+        const int side = edge == 0 ? 0 : 1;
+        for (int t = 0; t < q; ++t) zfma(acc, rowbuf[t * q + k], Uby[t * 2 + side]);
+      } else {                       // E_k / W_k: x-line iy = k
+        const int side = edge == 3 ? 0 : 1;
+        for (int t = 0; t < q; ++t) zfma(acc, rowbuf[k * q + t], Ubx[t * 2 + side]);
+      }
+      base[(int64_t)(nb + r) * nt + b] = acc;
     }
-    base[(int64_t)(nb + r) * nt + b] = acc;
+    __syncwarp();
   }
-  // Y_b = -V S^{-1}
-  for (int e = threadIdx.x; e < nb * ni; e += blockDim.x) {
-    const int b = e / ni, cc = e % ni, edge = b / q, k = b % q;
-    zt acc = make_double2(0.0, 0.0);
-    if (edge == 0 || edge == 2) {
-      const int side = edge == 0 ? 0 : 1;
-      for (int t = 0; t < q; ++t) zfma(acc, Vy[side * q + t], Si[(int64_t)(t * q + k) * nt + cc]);
-    } else {
-      const int side = edge == 3 ? 0 : 1;
-      for (int t = 0; t < q; ++t) zfma(acc, Vx[side * q + t], Si[(int64_t)(k * q + t) * nt + cc]);
+  // Y_b = -V S^{-1}: thread (line type, k, cc) forms both nodes of the line
+  for (int e = threadIdx.x; e < 2 * q * ni; e += blockDim.x) {
+    const int ltype = e / (q * ni), rem = e % (q * ni), k = rem / ni, cc = rem % ni;
+    zt a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    if (ltype == 0) {  // y-line ix = k: S_k (side 0), N_k (side 1)
+      for (int t = 0; t < q; ++t) {
+        const zt v = Si[(int64_t)(t * q + k) * nt + cc];
+        zfma(a0, Vy[t], v);
+        zfma(a1, Vy[q + t], v);
+      }
+      base[(int64_t)k * nt + nb + cc] = make_double2(-a0.x, -a0.y);
+      base[(int64_t)(2 * q + k) * nt + nb + cc] = make_double2(-a1.x, -a1.y);
+    } else {           // x-line iy = k: W_k (side 0), E_k (side 1)
+      for (int t = 0; t < q; ++t) {
+        const zt v = Si[(int64_t)(k * q + t) * nt + cc];
+        zfma(a0, Vx[t], v);
+        zfma(a1, Vx[q + t], v);
+      }
+      base[(int64_t)(3 * q + k) * nt + nb + cc] = make_double2(-a0.x, -a0.y);
+      base[(int64_t)(q + k) * nt + nb + cc] = make_double2(-a1.x, -a1.y);
     }
-    base[(int64_t)b * nt + nb + cc] = make_double2(-acc.x, -acc.y);
   }
   __syncthreads();
   // Psi_b = G - V Psi_i
-  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
-    const int b = e / nb, b2 = e % nb, edge = b / q, k = b % q;
-    const zt* Pi = base + (int64_t)nb * nt;  // Psi_i rows
-    zt acc = make_double2(0.0, 0.0);
-    zt gv = make_double2(0.0, 0.0);
+  const zt* Pi = base + (int64_t)nb * nt;  // Psi_i rows
+  for (int e = threadIdx.x; e < 2 * q * nb; e += blockDim.x) {
+    const int ltype = e / (q * nb), rem = e % (q * nb), k = rem / nb, b2 = rem % nb;
     const int e2 = b2 / q, k2 = b2 % q;
-    if (edge == 0 || edge == 2) {
-      const int side = edge == 0 ? 0 : 1;
-      for (int t = 0; t < q; ++t) zfma(acc, Vy[side * q + t], Pi[(int64_t)(t * q + k) * nt + b2]);
-      if (k2 == k && (e2 == 0 || e2 == 2)) gv = Gy[side * 2 + (e2 == 0 ? 0 : 1)];
+    zt a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+    if (ltype == 0) {
+      for (int t = 0; t < q; ++t) {
+        const zt v = Pi[(int64_t)(t * q + k) * nt + b2];
+        zfma(a0, Vy[t], v);
+        zfma(a1, Vy[q + t], v);
+      }
+      if (k2 == k && (e2 == 0 || e2 == 2)) {
+        g0 = Gy[0 * 2 + (e2 == 0 ? 0 : 1)];
+        g1 = Gy[1 * 2 + (e2 == 0 ? 0 : 1)];
+      }
+      base[(int64_t)k * nt + b2] = make_double2(g0.x - a0.x, g0.y - a0.y);
+      base[(int64_t)(2 * q + k) * nt + b2] = make_double2(g1.x - a1.x, g1.y - a1.y);
     } else {
-      const int side = edge == 3 ? 0 : 1;
-      for (int t = 0; t < q; ++t) zfma(acc, Vx[side * q + t], Pi[(int64_t)(k * q + t) * nt + b2]);
-      if (k2 == k && (e2 == 1 || e2 == 3)) gv = Gx[side * 2 + (e2 == 3 ? 0 : 1)];
+      for (int t = 0; t < q; ++t) {
+        const zt v = Pi[(int64_t)(k * q + t) * nt + b2];
+        zfma(a0, Vx[t], v);
+        zfma(a1, Vx[q + t], v);
+      }
+      if (k2 == k && (e2 == 1 || e2 == 3)) {
+        g0 = Gx[0 * 2 + (e2 == 3 ? 0 : 1)];
+        g1 = Gx[1 * 2 + (e2 == 3 ? 0 : 1)];
+      }
+      base[(int64_t)(3 * q + k) * nt + b2] = make_double2(g0.x - a0.x, g0.y - a0.y);
+      base[(int64_t)(q + k) * nt + b2] = make_double2(g1.x - a1.x, g1.y - a1.y);
     }
-    base[(int64_t)b * nt + b2] = make_double2(gv.x - acc.x, gv.y - acc.y);
   }
 }
 
@@ -266,7 +302,10 @@ void launch_leaf_schur_finish(zt* store, int64_t sstride, int leaf0, int nchunk,
   const double q = p - 2, ni = q * q, nb = 4 * q;
   ProfScope ps(K_LEAF_ASM, 8.0 * nchunk * q * (2.0 * ni * nb + nb * nb),
                16.0 * nchunk * (2.0 * ni * ni + 2.0 * ni * nb + nb * nb + ni * nb), st);
-  leaf_schur_finish_kernel<<<nchunk, 256, 0, st>>>(store, sstride, leaf0, nchunk, p, consts);
+  const size_t smem = sizeof(zt) * 8 * (size_t)(p - 2) * (p - 2);
+  if (smem > 48 * 1024)
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(leaf_schur_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  leaf_schur_finish_kernel<<<nchunk, 256, smem, st>>>(store, sstride, leaf0, nchunk, p, consts);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
