@@ -68,8 +68,8 @@ typedef struct {
   int32_t keep_all_R;   /* 1: keep every box's R for hps_export_R (debug / parity; default 0) */
   int32_t device;       /* CUDA device ordinal (default: current device) */
   int32_t leaf_chunk;   /* leaves factored per batch (0 = automatic) */
-  int32_t profile;      /* 1: time every kernel with CUDA events on the library stream (see
-                           hps_kernel_stats); 0: counters only (default) */
+  int32_t profile;      /* bit mask of kernel classes (see hps_kernel_stats) to time with CUDA
+                           events on the library stream; -1 = all; 0: counters only (default) */
   int32_t leaf_mode;    /* 0 (default): B^{-1} through the interior Schur complement;
                            1: Gauss-Jordan on the full n^tau x n^tau matrix B */
 } hps_opts;
@@ -164,7 +164,7 @@ double hps_last_flops(const hps_handle* h, int which);
  * Gauss-Jordan (one CTA per matrix).  ms is the sum of
  * CUDA-event durations around each launch (only while profiling is on); flops and bytes are
  * ALGORITHMIC (8 flops per complex multiply-add; operand bytes read + written once). */
-int hps_set_profiling(hps_handle* h, int on);
+int hps_set_profiling(hps_handle* h, int mask);
 int hps_kernel_stats(const hps_handle* h, int cls, int64_t* launches, double* ms, double* flops, double* bytes);
 int hps_reset_stats(hps_handle* h);
 

@@ -32,7 +32,7 @@ void hps_set_error(const std::string& m) { g_err_msg = m; }
 thread_local std::vector<cudaEvent_t> g_ev_pool;  // reused across handles (one device per process)
 
 struct Prof {
-  bool timing = false;
+  unsigned timing = 0;  // bit mask of kernel classes timed with events
   KStats stats;
   std::vector<cudaEvent_t>& pool = g_ev_pool;
   size_t used = 0;
@@ -67,20 +67,24 @@ void prof_begin(int cls, double flops, double bytes, cudaStream_t st) {
   P->stats.launches[cls] += 1;
   P->stats.flops[cls] += flops;
   P->stats.bytes[cls] += bytes;
-  if (P->timing) {
+  if (P->timing & (1u << cls)) {
     const size_t i = P->used;
     HPS_CUDA_CHECK(cudaEventRecord(P->ev(), st));
     P->open.push_back({cls, i});
+  } else if (P->timing) {
+    P->open.push_back({-1, 0});  // placeholder keeps begin/end pairs matched
   }
 }
 
 void prof_end(cudaStream_t st) {
   Prof* P = g_prof;
   if (!P || !P->timing || P->open.empty()) return;
+  const auto top = P->open.back();
+  P->open.pop_back();
+  if (top.first < 0) return;
   const size_t i = P->used;
   cudaEventRecord(P->ev(), st);
-  P->recs.push_back({P->open.back().first, P->open.back().second, i});
-  P->open.pop_back();
+  P->recs.push_back({top.first, top.second, i});
 }
 
 namespace {
@@ -966,7 +970,7 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   H.keep_root_R = opt ? opt->keep_root_R != 0 : true;
   H.keep_all_R = opt ? opt->keep_all_R != 0 : false;
   H.leaf_mode = opt ? opt->leaf_mode : 0;
-  H.prof.timing = opt ? opt->profile != 0 : false;
+  H.prof.timing = opt ? (unsigned)opt->profile : 0u;
 }
 
 void plan_all(hps_handle& H, int Lb) {
@@ -1325,9 +1329,9 @@ double hps_last_flops(const hps_handle* h, int which) {
   return h->flops[which];
 }
 
-int hps_set_profiling(hps_handle* h, int on) {
+int hps_set_profiling(hps_handle* h, int mask) {
   if (!h) return HPS_EINVAL;
-  h->prof.timing = on != 0;
+  h->prof.timing = (unsigned)mask;
   return HPS_OK;
 }
 

@@ -184,7 +184,8 @@ class Solver:
         self.nleaf = g.nx * g.ny
         self.q, self.nt, self.ni = p - 2, p * p - 4, (p - 2) ** 2
         self.nb_root = 2 * (g.nx + g.ny) * (p - 2)
-        opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk), int(profile), int(leaf_mode))
+        mask = -1 if profile is True else int(profile)
+        opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk), mask, int(leaf_mode))
         eta = complex(eta)
         h = C.c_void_p()
         cp = _ptr(c, self.nleaf * p * p, "c_samples")
@@ -246,8 +247,8 @@ class Solver:
     def flops(self, which):
         return lib().hps_last_flops(self.h, which)
 
-    def set_profiling(self, on):
-        _check(lib().hps_set_profiling(self.h, int(on)))
+    def set_profiling(self, mask):
+        _check(lib().hps_set_profiling(self.h, -1 if mask is True else int(mask)))
 
     def reset_stats(self):
         _check(lib().hps_reset_stats(self.h))
@@ -282,7 +283,7 @@ class TopSolver:
         self.nb_sub = nb_of(sub, p)
         self.nb_root = nb_of(g, p)
         self.nsub = 1 << depth
-        opts = hps_opts(int(keep_root_R), 0, int(device), 0, int(profile), 0)
+        opts = hps_opts(int(keep_root_R), 0, int(device), 0, -1 if profile is True else int(profile), 0)
         eta = complex(eta)
         h = C.c_void_p()
         _check(lib().hps_build_top(C.byref(g), p, p - 2, float(kappa), hps_c128(eta.real, eta.imag), depth,
