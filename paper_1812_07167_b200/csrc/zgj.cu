@@ -523,27 +523,31 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // Fused whole-matrix Gauss-Jordan, n <= 256: one CTA (8 warps) per matrix, in place.
 // For each panel of w <= NB = 28 columns:
 //  * panel phase: thread i owns row i of the panel in registers (as zgj_panel_reg: packed-key
-//    REDUX pivot search, raw pivot-row broadcast, rotated rows); the transform T (n x w) is
-//    parked in shared memory and written back to the panel columns;
-//  * update phase (FP64 tensor cores): the other columns, in chunks of CH = 32, are gathered
-//    through the panel's row permutation straight into DMMA accumulator fragments (warp w owns
-//    rows 32w .. 32w+31), panel rows park theirs in shared memory (Z) and restart from zero,
-//    and  C += T Z  runs as m8n8k4 DMMAs (complex = 4 real products) with T and Z fragments
-//    from shared memory; the chunk is stored back in place.
+//    REDUX pivot search, raw pivot-row broadcast, rotated rows); the transform T is written
+//    back to the panel columns and each warp then holds its 32 rows of T as DMMA A fragments
+//    in registers for the whole update phase;
+//  * update phase (FP64 tensor cores): the other columns, in chunks of CH, are gathered
+//    through the panel's row permutation by cp.async into a double-buffered shared stage
+//    (chunk c+1 is in flight while chunk c is computed); panel rows of the stage are the
+//    B operand Z, the other rows seed the accumulators, C += T Z runs as m8n8k4 DMMAs
+//    (complex = 4 real products) and the chunk is stored back in place.
 // No ping-pong buffer and no launch per panel.  The column swaps are undone while writing the
-// result to `out`.  Dynamic shared memory: T [n][28] (stride 28 = 4 mod 8 complex: conflict-free
-// A fragments) + Z [28][34].
+// result to `out`.  Dynamic shared memory: stage [2][n][CH + 2] complex.
 // ---------------------------------------------------------------------------
 constexpr int FU_NB = 28;
 
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem));
+}
+
 template <int CH, int MINB>
 __global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
-                                                           zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
-                                                           int* __restrict__ info) {
-  constexpr int NB = FU_NB, ZS = CH + 2, NW = 8, TN = CH / 8;
+                                                              zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
+                                                              int* __restrict__ info) {
+  constexpr int NB = FU_NB, SS = CH + 2, NW = 8, TN = CH / 8, K4 = NB / 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [n][NB]
-  zt* Zs = Ts + n * NB;                       // [NB][ZS]
+  zt* stage = reinterpret_cast<zt*>(smem_raw);  // [2][n][SS]
   __shared__ zt prow[NB], tmp[NB];
   __shared__ unsigned wkey[NW];
   __shared__ int s_orig_r, s_orig_k;
@@ -553,6 +557,7 @@ __global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A
   zt* Ab = A + (int64_t)b * bs;
   const int i = tid;
   const bool live = i < n;
+  const int sbuf = n * SS;
   bool singular = false;
   for (int k0 = 0; k0 < n; k0 += NB) {
     const int w = min(NB, n - k0);
@@ -606,69 +611,84 @@ __global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A
         for (int p = 0; p < NB; ++p) {
           int j = p + w;
           if (j >= NB) j -= NB;
-          Ts[i * NB + j] = (j < w) ? row[p] : make_double2(0.0, 0.0);
           if (j < w) Ab[(int64_t)i * lda + k0 + j] = row[p];
         }
       }
       orig_s[i] = live ? orig : 0;
     }
-    __syncthreads();
-    // ---- update phase: other columns J = [0, k0) U [k0 + w, n), chunks of CH ----
+    __syncthreads();  // T and the previous panel's update visible to every thread
     const int nc = n - w;
+    if (nc <= 0) continue;
+    // A fragments of T for this warp's rows (register resident for the whole update phase)
     const int rbase = warp * 32;
-    for (int c0 = 0; c0 < nc; c0 += CH) {
-      double accr[4][TN][2], acci[4][TN][2];
-      // gather the permuted chunk into the accumulator fragments; panel rows go to Z
+    zt af[4][K4];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
-        const int rr = rbase + mi * 8 + (lane >> 2);
-        const bool rlive = rr < n;
-        const zt* src = Ab + (int64_t)(rlive ? orig_s[rr] : 0) * lda;
-        const bool is_p = rr >= k0 && rr < k0 + w;
+    for (int mi = 0; mi < 4; ++mi) {
+      const int rr = min(rbase + mi * 8 + (lane >> 2), n - 1);
 #pragma unroll
-        for (int ni = 0; ni < TN; ++ni)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cl = ni * 8 + (lane & 3) * 2 + h;
-            const int cj = c0 + cl;
-            zt v = make_double2(0.0, 0.0);
-            if (rlive && cj < nc) v = src[cj < k0 ? cj : cj + w];
-            if (is_p) {
-              Zs[(rr - k0) * ZS + cl] = v;
-              v = make_double2(0.0, 0.0);
-            }
-            accr[mi][ni][h] = v.x;
-            acci[mi][ni][h] = v.y;
-          }
+      for (int k4 = 0; k4 < K4; ++k4) {
+        const int kc = k4 * 4 + (lane & 3);
+        af[mi][k4] = kc < w ? Ab[(int64_t)rr * lda + k0 + kc] : make_double2(0.0, 0.0);
       }
-      __syncthreads();  // Z complete; every gather of this chunk done before any store below
+    }
+    // chunk gather: thread t copies row t's CH elements of the permuted matrix into the stage
+    auto gather = [&](int c0, int buf) {
+      if (live) {
+        const zt* src = Ab + (int64_t)orig_s[i] * lda;
+        zt* dst = stage + buf * sbuf + i * SS;
+#pragma unroll
+        for (int jj = 0; jj < CH; ++jj) {
+          const int cj = min(c0 + jj, nc - 1);  // clamp: tail columns are never stored
+          cpa16(dst + jj, src + (cj < k0 ? cj : cj + w));
+        }
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    gather(0, 0);
+    int buf = 0;
+    for (int c0 = 0; c0 < nc; c0 += CH, buf ^= 1) {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      __syncthreads();  // chunk c staged by every thread; chunk c-1 fully consumed
+      if (c0 + CH < nc) gather(c0 + CH, buf ^ 1);
+      const zt* sg = stage + buf * sbuf;
       if (rbase < n) {
+        double accr[4][TN][2], acci[4][TN][2];
 #pragma unroll
-        for (int k4 = 0; k4 < NB / 4; ++k4) {
-          zt af[4], bf[TN];
+        for (int mi = 0; mi < 4; ++mi) {
+          const int rr = rbase + mi * 8 + (lane >> 2);
+          const bool seed = rr < n && !(rr >= k0 && rr < k0 + w);
 #pragma unroll
-          for (int mi = 0; mi < 4; ++mi) {
-            const int rr = min(rbase + mi * 8 + (lane >> 2), n - 1);
-            af[mi] = Ts[rr * NB + k4 * 4 + (lane & 3)];
-          }
+          for (int ni = 0; ni < TN; ++ni)
 #pragma unroll
-          for (int ni = 0; ni < TN; ++ni) bf[ni] = Zs[(k4 * 4 + (lane & 3)) * ZS + ni * 8 + (lane >> 2)];
+            for (int h = 0; h < 2; ++h) {
+              const zt v = seed ? sg[rr * SS + ni * 8 + (lane & 3) * 2 + h] : make_double2(0.0, 0.0);
+              accr[mi][ni][h] = v.x;
+              acci[mi][ni][h] = v.y;
+            }
+        }
+#pragma unroll
+        for (int k4 = 0; k4 < K4; ++k4) {
+          zt bf[TN];
+          const int kr = k4 * 4 + (lane & 3);
+#pragma unroll
+          for (int ni = 0; ni < TN; ++ni)
+            bf[ni] = kr < w ? sg[(k0 + kr) * SS + ni * 8 + (lane >> 2)] : make_double2(0.0, 0.0);
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < TN; ++ni) dmma884(accr[mi][ni][0], accr[mi][ni][1], af[mi].x, bf[ni].x);
+            for (int ni = 0; ni < TN; ++ni) dmma884(accr[mi][ni][0], accr[mi][ni][1], af[mi][k4].x, bf[ni].x);
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < TN; ++ni) dmma884(acci[mi][ni][0], acci[mi][ni][1], af[mi].x, bf[ni].y);
+            for (int ni = 0; ni < TN; ++ni) dmma884(acci[mi][ni][0], acci[mi][ni][1], af[mi][k4].x, bf[ni].y);
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < TN; ++ni) dmma884(accr[mi][ni][0], accr[mi][ni][1], -af[mi].y, bf[ni].y);
+            for (int ni = 0; ni < TN; ++ni) dmma884(accr[mi][ni][0], accr[mi][ni][1], -af[mi][k4].y, bf[ni].y);
 #pragma unroll
           for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-            for (int ni = 0; ni < TN; ++ni) dmma884(acci[mi][ni][0], acci[mi][ni][1], af[mi].y, bf[ni].x);
+            for (int ni = 0; ni < TN; ++ni) dmma884(acci[mi][ni][0], acci[mi][ni][1], af[mi][k4].y, bf[ni].x);
         }
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
@@ -684,8 +704,8 @@ __global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A
             }
         }
       }
-      __syncthreads();  // Z reusable; this chunk's stores visible to the next panel
     }
+    __syncthreads();  // last chunk stored before the next panel reads
   }
   // undo the column swaps: out(i, j) = A(i, pi(j)),  pi = S_{n-1} o ... o S_0
   if (tid == 0) {
@@ -810,20 +830,21 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
-      static int fcfg = -1;
-      if (fcfg < 0) {
-        const char* e = getenv("HPS_FUSED_CFG");
-        fcfg = (e && *e == '1') ? 1 : 0;
-        HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_fused_kernel<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)(sizeof(zt) * (256 * FU_NB + FU_NB * 18))));
-        HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_fused_kernel<32, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)(sizeof(zt) * (256 * FU_NB + FU_NB * 34))));
+      static bool fattr = false;
+      if (!fattr) {
+        HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_fused_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(sizeof(zt) * 2 * 256 * 10)));
+        HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_fused_kernel<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(sizeof(zt) * 2 * 256 * 18)));
+        fattr = true;
       }
-      if (fcfg == 0)
-        zgj_fused_kernel<16, 2><<<nbatch, 256, sizeof(zt) * ((size_t)n * FU_NB + FU_NB * 18), st>>>(
+      // large batches: two CTAs per SM overlap one matrix's pivot steps with the other's update;
+      // small batches: one CTA per SM with wider chunks has the shorter critical path
+      if (batch >= 148)
+        zgj_fused_kernel<8, 2><<<nbatch, 256, sizeof(zt) * 2 * (size_t)n * 10, st>>>(
             A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo, obs, n, info);
       else
-        zgj_fused_kernel<32, 1><<<nbatch, 256, sizeof(zt) * ((size_t)n * FU_NB + FU_NB * 34), st>>>(
+        zgj_fused_kernel<16, 1><<<nbatch, 256, sizeof(zt) * 2 * (size_t)n * 18, st>>>(
             A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo, obs, n, info);
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
