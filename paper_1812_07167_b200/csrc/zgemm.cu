@@ -241,6 +241,84 @@ void launch(const ZGemm& g, cudaStream_t st) {
   count_launch();
 }
 
+// Skinny products (N <= 4, the solve sweeps at few right-hand sides): one warp per output
+// row, lanes stride over K with coalesced 16-byte loads of the A row, warp-shuffle reduction.
+// Bandwidth-bound (A is read once); parallel over M x batch warps, so the long-K / single-merge
+// matvecs at the top of the tree do not serialise on a handful of CTAs.
+template <int NMAX>
+__global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= g.M) return;
+  for (int b = blockIdx.y; b < g.batch; b += gridDim.y) {
+    const int* Arm = g.A.rmap ? g.A.rmap + (int64_t)b * g.A.rmap_bs : nullptr;
+    const int* Brm = g.B.rmap ? g.B.rmap + (int64_t)b * g.B.rmap_bs : nullptr;
+    const int* Crm = g.C.rmap ? g.C.rmap + (int64_t)b * g.C.rmap_bs : nullptr;
+    const int* Irm = g.Cin.rmap ? g.Cin.rmap + (int64_t)b * g.Cin.rmap_bs : nullptr;
+    const int ra = Arm ? Arm[row] : row;
+    double accr[NMAX], acci[NMAX];
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r) accr[r] = acci[r] = 0.0;
+    if (ra >= 0) {
+      const zt* Ab = g.A.ptr + (int64_t)b * g.A.bs + (int64_t)ra * g.A.rs;
+      const zt* Bb = g.B.ptr + (int64_t)b * g.B.bs;
+      int64_t bco[NMAX];
+      bool bok[NMAX];
+#pragma unroll
+      for (int r = 0; r < NMAX; ++r) {
+        const int cj = r < g.N ? zcol(g.B.cmap, r, g.B.cskip_at, g.B.cskip_len) : -1;
+        bok[r] = cj >= 0;
+        bco[r] = (int64_t)(cj < 0 ? 0 : cj) * g.B.cs;
+      }
+      for (int k = lane; k < g.K; k += 32) {
+        const int ck = zcol(g.A.cmap, k, g.A.cskip_at, g.A.cskip_len);
+        const int rk = Brm ? Brm[k] : k;
+        if (ck < 0 || rk < 0) continue;
+        const zt a = Ab[(int64_t)ck * g.A.cs];
+        const zt* Brow = Bb + (int64_t)rk * g.B.rs;
+#pragma unroll
+        for (int r = 0; r < NMAX; ++r) {
+          if (!bok[r]) continue;
+          const zt v = Brow[bco[r]];
+          accr[r] = fma(a.x, v.x, accr[r]);
+          accr[r] = fma(-a.y, v.y, accr[r]);
+          acci[r] = fma(a.x, v.y, acci[r]);
+          acci[r] = fma(a.y, v.x, acci[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        accr[r] += __shfl_xor_sync(0xffffffffu, accr[r], o);
+        acci[r] += __shfl_xor_sync(0xffffffffu, acci[r], o);
+      }
+    const int ro = Crm ? Crm[row] : row;
+    if (ro < 0) continue;
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r) {
+      if (lane != r || r >= g.N) continue;
+      zt v = zmul(g.alpha, make_double2(accr[r], acci[r]));
+      if (g.Cin.ptr) {
+        const int ri = Irm ? Irm[row] : row;
+        const int cj = zcol(g.Cin.cmap, r, g.Cin.cskip_at, g.Cin.cskip_len);
+        if (ri >= 0 && cj >= 0) {
+          const zt cv = zmul(g.beta, g.Cin.ptr[(int64_t)b * g.Cin.bs + (int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
+          v.x += cv.x;
+          v.y += cv.y;
+        }
+      }
+      if (row == r) {
+        v.x += g.diag.x;
+        v.y += g.diag.y;
+      }
+      const int co = zcol(g.C.cmap, r, g.C.cskip_at, g.C.cskip_len);
+      if (co >= 0) g.C.ptr[(int64_t)b * g.C.bs + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
+    }
+  }
+}
+
 __global__ void zcopy_kernel(const ZCopy c) {
   const int64_t total = (int64_t)c.batch * c.M * c.N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -305,6 +383,15 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
     case 6: launch<32, 64, 16, 32>(g, st); return true;
     case 7: launch<128, 64, 32, 32>(g, st); return true;
     case 8: launch<64, 64, 16, 32>(g, st); return true;
+    case 9: {
+      dim3 grid((g.M + 7) / 8, g.batch < 65535 ? g.batch : 65535);
+      if (g.N == 1) zgemv_kernel<1><<<grid, 256, 0, st>>>(g);
+      else if (g.N <= 4) zgemv_kernel<4><<<grid, 256, 0, st>>>(g);
+      else return false;
+      HPS_CUDA_CHECK(cudaGetLastError());
+      count_launch();
+      return true;
+    }
     default: return false;
   }
 }
@@ -315,6 +402,16 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   ProfScope ps(K_ZGEMM, 8.0 * mn * g.K * bt,
                16.0 * bt * ((double)g.M * g.K + (double)g.K * g.N + mn * (g.Cin.ptr ? 2.0 : 1.0)), st);
   if (g_zgemm_force >= 0 && launch_cfg(g_zgemm_force, g, st)) return;
+  if (g.N <= 4 && g_zgemm_force != -2) {
+    dim3 grid((g.M + 7) / 8, g.batch < 65535 ? g.batch : 65535);
+    if (g.N == 1)
+      zgemv_kernel<1><<<grid, 256, 0, st>>>(g);
+    else
+      zgemv_kernel<4><<<grid, 256, 0, st>>>(g);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
   // Tile choice from the sweep in profiles/r01_gemm_tune.txt: 32x32 tiles (5 CTAs / SM) win
   // for the short-K and Cin-heavy shapes of the merges and the Gauss-Jordan updates; 64x32 tiles
   // win once K is long enough to amortise the tile loads.

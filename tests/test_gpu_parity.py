@@ -155,14 +155,17 @@ def test_virtual_ranks_match_single_gpu(world, nx, ny, p):
         assert rel(u_ref, O.solve(s, t)) < TOL
 
 
-@pytest.mark.parametrize("cfg", list(range(9)))
-@pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1)])
+@pytest.mark.parametrize("cfg", list(range(10)))
+@pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1),
+                                         (70, 1, 300, 2), (33, 3, 45, 3)])
 def test_zgemm_configs(cfg, M, N, K, batch):
     """Every DMMA tile configuration vs the oracle's triple-loop product (ragged edges, beta)."""
     rng = np.random.default_rng(M * 1000 + N + K)
     A = rng.standard_normal((batch, M, K)) + 1j * rng.standard_normal((batch, M, K))
     B = rng.standard_normal((batch, K, N)) + 1j * rng.standard_normal((batch, K, N))
     Cin = rng.standard_normal((batch, M, N)) + 1j * rng.standard_normal((batch, M, N))
+    if cfg == 9 and N > 4:
+        pytest.skip("GEMV path is for N <= 4")
     for alpha, beta in [(1.0, 1.0), (-1.0, 0.5 - 2j)]:
         C, _ = hps.zgemm_batched(A, B, Cin, alpha, beta, cfg=cfg)
         for b in range(batch):
