@@ -171,3 +171,74 @@ def test_zgemm_configs(cfg, M, N, K, batch):
         for b in range(batch):
             ref = alpha * oracle.matmul(A[b], B[b]) + beta * Cin[b]
             assert rel(C[b], ref) < 1e-13
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configurations at full size, in the bench's launch configuration
+# ---------------------------------------------------------------------------
+def _bench_inputs(cfgno, nrhs=None):
+    import bench
+    cfg = inputs.CONFIGS[cfgno]
+    g, c, s, t = bench.setup(cfg, hps)
+    if nrhs is not None:
+        s, t = s[:nrhs], t[:nrhs]
+    return cfg, g, c, s, t
+
+
+def test_config2_full_vs_oracle():
+    """C2 (the bench workload), whole problem: root R and u vs the oracle's Algorithm 1 + 2."""
+    cfg, g, c, s, t = _bench_inputs(2)
+    S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
+    u = S.solve(s, t)
+    O = oracle.Oracle(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p, cfg.kappa, cfg.eta, c)
+    assert rel(S.R(1), O.R(1)) < TOL
+    assert rel(u, O.solve(s, t)) < TOL
+
+
+def test_config3_sampled_leaves_and_merges():
+    """C3 (128x128 leaves, 10 ppw): sampled leaves vs oracle.leaf, and level-local merges — the
+    GPU children's R fed to oracle.merge must give the GPU parent R — at every level whose merge
+    the oracle finishes in seconds (child n_b <= 1344)."""
+    cfg, g, c, s, t = _bench_inputs(3, nrhs=1)
+    S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c, keep_all_R=True)
+    h = 1.0 / 128
+    rng = np.random.default_rng(3)
+    for leaf in rng.choice(cfg.nleaf, 3, replace=False):
+        Psi, Y = S.leaf_ops(int(leaf))
+        lo = oracle.leaf(cfg.p, h, h, cfg.kappa, cfg.eta, c[leaf])
+        assert rel(Psi, lo["Psi"]) < TOL and rel(Y, lo["Y"]) < TOL
+    L = 14
+    for d in range(L - 1, -1, -1):
+        box = (1 << d) + int(rng.integers(0, 1 << d))
+        ci0, ci1, cj0, cj1, _ = oracle.box_rect(cfg.nx, cfg.ny, 2 * box)
+        vertical = oracle.box_rect(cfg.nx, cfg.ny, box)[4]
+        if 2 * ((ci1 - ci0) + (cj1 - cj0)) * (cfg.p - 2) > 1344:
+            break
+        ref = oracle.merge(cfg.p, ci1 - ci0, cj1 - cj0, vertical, S.R(2 * box), S.R(2 * box + 1))["Rtau"]
+        assert rel(S.R(box), ref) < TOL, (d, box)
+
+
+def test_config3_polynomial_exact():
+    """At C3 scale no oracle run is needed for u: a global polynomial of degree p-1 per variable
+    is reproduced exactly by the discretisation, so the CUDA path's u must match
+    it to rounding (bound derived from cond ~ 1e6 x eps x levels)."""
+    import numpy.polynomial.chebyshev as npc
+    cfg = inputs.CONFIGS[3]
+    p = cfg.p
+    g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
+    X, Y = hps.leaf_nodes(g, p)
+    Xb, Yb, NX, NY = hps.root_boundary_nodes(g, p)
+    rng = np.random.default_rng(9)
+    a = (rng.standard_normal((p, p)) + 1j * rng.standard_normal((p, p))) / np.outer(np.arange(1, p + 1), np.arange(1, p + 1))
+    val = lambda x, y, dx=0, dy=0: npc.chebval2d(2 * x - 1, 2 * y - 1,
+                                                 (npc.chebder(npc.chebder(a, dx, axis=0) * 2 ** dx, dy, axis=1) * 2 ** dy)
+                                                 if (dx or dy) else a)
+    c = inputs.c_at(cfg, X, Y)
+    Xi, Yi, ci = inputs.interior_of(p, X), inputs.interior_of(p, Y), inputs.interior_of(p, c)
+    s = (-(val(Xi, Yi, 2, 0) + val(Xi, Yi, 0, 2)) - cfg.kappa ** 2 * ci * val(Xi, Yi))[None]
+    t = (NX * val(Xb, Yb, 1, 0) + NY * val(Xb, Yb, 0, 1) + 1j * cfg.eta * val(Xb, Yb))[None]
+    S = hps.Solver(g, p, cfg.kappa, cfg.eta, c, keep_root_R=False)
+    u = S.solve(np.ascontiguousarray(s), np.ascontiguousarray(t))[0]
+    ex_i = val(Xi, Yi)
+    scale = np.max(np.abs(ex_i))
+    assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / scale < 1e-7
