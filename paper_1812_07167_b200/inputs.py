@@ -197,3 +197,28 @@ def make_inputs(cfg, X, Y, Xb, Yb, NXb, NYb, nrhs=None):
     s = s_interior(cfg, interior_of(cfg.p, X), interior_of(cfg.p, Y), nrhs)
     t = t_boundary(cfg, Xb, Yb, NXb, NYb, nrhs)
     return c, s, t
+
+
+# ---------------------------------------------------------------------------
+# The paper's own experiment (Sec. 4): unit square, kappa = 16,
+# c = exp(-8[(x-.5)^2 + (y-.5)^2]) (reading Q17), exact u = exp(i 2 pi kappa x) exp(i 2 pi kappa y),
+# s = -Lap u - kappa^2 c u = (8 pi^2 kappa^2 - kappa^2 c) u, t = du/dnu + i eta u, eta = kappa.
+# ---------------------------------------------------------------------------
+PAPER_KAPPA = 16.0
+
+
+def paper_c(X, Y):
+    return np.exp(-8.0 * ((X - 0.5) ** 2 + (Y - 0.5) ** 2)).astype(complex)
+
+
+def paper_u(X, Y, kappa=PAPER_KAPPA):
+    return np.exp(2j * math.pi * kappa * X) * np.exp(2j * math.pi * kappa * Y)
+
+
+def paper_s(X, Y, kappa=PAPER_KAPPA):
+    return (8.0 * math.pi ** 2 * kappa ** 2 - kappa ** 2 * paper_c(X, Y)) * paper_u(X, Y, kappa)
+
+
+def paper_t(X, Y, NX, NY, kappa=PAPER_KAPPA, eta=PAPER_KAPPA):
+    du = 2j * math.pi * kappa * paper_u(X, Y, kappa)   # d/dx u = d/dy u
+    return NX * du + NY * du + 1j * eta * paper_u(X, Y, kappa)

@@ -242,3 +242,29 @@ def test_config3_polynomial_exact():
     ex_i = val(Xi, Yi)
     scale = np.max(np.abs(ex_i))
     assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / scale < 1e-7
+
+
+def test_paper_experiment_convergence():
+    """The paper's Sec. 4.1 experiment (NEXT-1): e_inf decays with N for each n_c, spectrally
+    faster for larger n_c; at n_c = 16 it reaches the roundoff plateau."""
+    from paper_1812_07167_b200 import experiments
+    tab = experiments.convergence_table(ps=(6, 9, 16), sides=(8, 16, 32))
+    for p, rows in tab.items():
+        errs = [e for _, e in rows]
+        assert errs[-1] < errs[0] / 10, (p, errs)
+    assert tab[16][-1][1] < 1e-8, tab[16]
+    assert tab[16][1][1] < tab[9][1][1] < tab[6][1][1]
+
+
+def test_paper_experiment_matches_oracle_small():
+    """Same manufactured problem through the oracle on a 4x4-leaf grid: GPU u == oracle u."""
+    p, m, kappa = 9, 4, inputs.PAPER_KAPPA
+    g = hps.grid(0.0, 1.0, 0.0, 1.0, m, m)
+    X, Y = hps.leaf_nodes(g, p)
+    Xb, Yb, NX, NY = hps.root_boundary_nodes(g, p)
+    c = inputs.paper_c(X, Y)
+    s = inputs.paper_s(inputs.interior_of(p, X), inputs.interior_of(p, Y))[None]
+    t = inputs.paper_t(Xb, Yb, NX, NY)[None]
+    S = hps.Solver(g, p, kappa, kappa, c)
+    O = oracle.Oracle(0, 1, 0, 1, m, m, p, kappa, kappa, c)
+    assert rel(S.solve(s, t), O.solve(s, t)) < TOL
