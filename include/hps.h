@@ -174,6 +174,17 @@ int hps_reset_stats(hps_handle* h);
  * zero pivot.  Exposed for kernel-level tests. */
 int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* out);
 
+/* As hps_zinv_batched, but runs the inversion `reps` times (each on a fresh device copy of A)
+ * and returns the mean device time of the inversion alone (CUDA events) in *ms.  `mode`
+ * selects the kernel family (0 = library choice, 1 = whole-matrix fused, 2 = blocked
+ * panel + GEMM, 3 = warp-specialised look-ahead, n <= 240) for kernel comparisons.  Exposed for kernel tests and tuning. */
+int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* out, int reps, double* ms);
+
+/* Debug: arm (on = 1) / disarm the clock64 timeline of CTA 0 of the warp-specialised
+ * Gauss-Jordan kernel and copy the last one (160 values: [panel][10]) to host `out` (may be
+ * NULL).  Used by tools/gj_tune.py only. */
+int hps_debug_ws_trace(int on, int64_t* out);
+
 /* Batched complex GEMM through the library's DMMA kernel: C = alpha A B + beta Cin for
  * contiguous row-major A [batch][M][K], B [batch][K][N], Cin / C [batch][M][N] (Cin may be
  * NULL).  cfg selects a tile configuration (-1 = the library's choice); the call runs `reps`

@@ -1391,6 +1391,76 @@ int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* outp) {
   }
 }
 
+int hps_debug_ws_trace(int on, int64_t* out) {
+  try {
+    zgj_ws_trace(on, reinterpret_cast<long long*>(out));
+    return HPS_OK;
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+}
+
+int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* outp, int reps, double* ms) {
+  if (n <= 0 || batch <= 0 || !A || !outp || reps < 1 || mode < 0 || mode > 3) {
+    hps_set_error("hps_zinv_timed: invalid argument");
+    return HPS_EINVAL;
+  }
+  try {
+    cudaStream_t st;
+    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int dev;
+    HPS_CUDA_CHECK(cudaGetDevice(&dev));
+    retain_pool(dev);
+    g_alloc_stream = st;
+    const size_t bytes = sizeof(zt) * (size_t)n * n * batch;
+    int rc = HPS_OK;
+    {
+      DevBuf src, a, o, ws, info;
+      src.alloc(bytes);
+      a.alloc(bytes);
+      o.alloc(bytes);
+      extern int g_gj_mode_force;
+      g_gj_mode_force = mode;
+      ws.alloc(std::max<size_t>(zgj_workspace_bytes(n, batch), 16));
+      info.alloc(sizeof(int));
+      HPS_CUDA_CHECK(cudaMemcpyAsync(src.p, A, bytes, cudaMemcpyDefault, st));
+      HPS_CUDA_CHECK(cudaMemsetAsync(info.p, 0, sizeof(int), st));
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      double tot = 0;
+      for (int r = 0; r <= reps; ++r) {  // r == 0: warm-up
+        HPS_CUDA_CHECK(cudaMemcpyAsync(a.p, src.p, bytes, cudaMemcpyDeviceToDevice, st));
+        cudaEventRecord(e0, st);
+        zgj_invert(a.as<zt>(), n, (int64_t)n * n, o.as<zt>(), n, (int64_t)n * n, n, batch, ws.p, info.as<int>(), st,
+                   nullptr);
+        cudaEventRecord(e1, st);
+        HPS_CUDA_CHECK(cudaEventSynchronize(e1));
+        float t = 0;
+        cudaEventElapsedTime(&t, e0, e1);
+        if (r > 0) tot += t;
+      }
+      g_gj_mode_force = 0;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+      if (ms) *ms = tot / reps;
+      int h_info = 0;
+      HPS_CUDA_CHECK(cudaMemcpyAsync(outp, o.p, bytes, cudaMemcpyDefault, st));
+      HPS_CUDA_CHECK(cudaMemcpyAsync(&h_info, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+      if (h_info) {
+        hps_set_error("hps_zinv_timed: zero pivot in batch entry " + std::to_string(h_info - 1));
+        rc = HPS_ESINGULAR;
+      }
+    }
+    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    cudaStreamDestroy(st);
+    return rc;
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+}
+
 int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A, const hps_c128* B,
                       const hps_c128* Cin, hps_c128* C, hps_c128 alpha, hps_c128 beta, int reps, double* ms) {
   if (M <= 0 || N <= 0 || K < 0 || batch <= 0 || !A || !B || !C || reps < 1) {

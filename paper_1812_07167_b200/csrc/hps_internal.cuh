@@ -87,6 +87,9 @@ size_t zgj_workspace_bytes(int n, int batch);
 void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
                 void* ws, int* info, cudaStream_t st, int64_t* launches);
 
+// Debug timeline of the warp-specialised Gauss-Jordan kernel (hps_debug_ws_trace).
+void zgj_ws_trace(int on, long long* out);
+
 // Launch counter used for the gpu_launches report.
 extern thread_local int64_t* g_launch_counter;
 inline void count_launch(int k = 1) {

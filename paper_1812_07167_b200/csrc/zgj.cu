@@ -25,6 +25,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "hps_internal.cuh"
 
@@ -198,15 +199,12 @@ template <int NB>
 __device__ __forceinline__ void row_step(zt (&row)[NB], const zt* pr, zt inv) {
   const zt g = zmul(row[0], inv);
   const double ngx = -g.x, ngy = -g.y;
+  // one shared-memory read of each pivot-row element (broadcast LDS costs 4 B/lane/cycle)
 #pragma unroll
   for (int j = 1; j < NB; ++j) {
     const zt pj = pr[j];
     row[j].x = fma(ngx, pj.x, row[j].x);
     row[j].y = fma(ngx, pj.y, row[j].y);
-  }
-#pragma unroll
-  for (int j = 1; j < NB; ++j) {
-    const zt pj = pr[j];
     row[j].x = fma(g.y, pj.y, row[j].x);
     row[j].y = fma(ngy, pj.x, row[j].y);
   }
@@ -734,6 +732,338 @@ __global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A
   if (singular && tid == 0) atomicCAS(info, 0, b + 1);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised Gauss-Jordan with look-ahead, n <= WS_NMAX: one CTA of 16 warps per matrix.
+// Implicit partial pivoting: rows never move.  The pivot of global step k is row plist[k]
+// (pstep[row] = k); at the end the in-place matrix M satisfies A^{-1}(k, j) = M(plist[k],
+// pstep[j]) (the row and column permutations of the row pivoting; checked against the textbook
+// blocked GJ in tests/test_gpu_parity.py::test_zinv_*).
+//  * panel warps 0-7 (thread i owns row i): factor panel p+1 (w <= 28 columns, pivot search
+//    over the rows not yet pivoted, ONE barrier per step: every warp publishes its best
+//    candidate row, all threads pick the winner), then write T (the factored panel columns)
+//    to shared memory and back in place;
+//  * update warps 8-15 (FP64 tensor cores): for panel p, stage Z = the old pivot rows of p
+//    (all other columns) in shared memory by cp.async, then C(i, J) = [i not a pivot of p]
+//    C(i, J) + T(i, :) Z(:, J) for every other column J as m8n8k4 DMMAs (complex = 4 real
+//    products), accumulators seeded straight from global memory.  The columns of panel p+1
+//    are updated first and released to the panel warps (named barrier), so the panel
+//    factorisation of p+1 overlaps the rest of the update of p.
+// The matrix stays in L2 (one CTA per SM: 148 x 614 KB at n = 196), every pass reads and
+// writes it once; T and Z live in shared memory.
+// ---------------------------------------------------------------------------
+constexpr int WS_NB = 28, WS_NMAX = 240;
+// optional timeline of CTA 0 (clock64 per milestone, hps_debug_ws_trace): [panel][10]
+__device__ long long g_ws_trace[16 * 16];
+__device__ int g_ws_trace_on;
+#define WS_MARK(p, slot)                                                              \
+  do {                                                                                \
+    if (trace && (p) < 16) g_ws_trace[(p) * 16 + (slot)] = clock64();                 \
+  } while (0)
+enum { BAR_PANEL = 1, BAR_UPD = 2, BAR_READY = 3, BAR_TFREE = 4, BAR_TREADY = 5 };
+
+__device__ __forceinline__ void bar_sync_n(int id, int cnt) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void bar_arrive_n(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;\n" ::: "memory"); }
+__device__ __forceinline__ void cpa16_zfill(void* smem, const void* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(valid ? 16 : 0));
+}
+
+struct WsPanels {
+  int npan, base, rem;
+  __device__ __forceinline__ int k0(int p) const { return p * base + min(p, rem); }
+  __device__ __forceinline__ int w(int p) const { return p < npan ? base + (p < rem ? 1 : 0) : 0; }
+};
+
+__host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16, == 2 (mod 8)
+  const int npan = (n + WS_NB - 1) / WS_NB;
+  const int need = n - n / npan + 16;
+  return ((need - 2 + 7) / 8) * 8 + 2;
+}
+__host__ __device__ inline size_t ws_smem(int n) {
+  return sizeof(zt) * ((size_t)((n + 7) & ~7) * WS_NB + (size_t)WS_NB * ws_zs(n));
+}
+
+__global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
+                                                        zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
+                                                        int* __restrict__ info) {
+  constexpr int NB = WS_NB;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int mtr = (n + 7) & ~7, zs = ws_zs(n);
+  zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [mtr][NB]  T of the current panel
+  zt* Zs = Ts + (size_t)mtr * NB;            // [NB][zs]   old pivot rows, virtual column order
+  __shared__ zt prow4[2][NB];
+  __shared__ __align__(16) unsigned wkey4[2][8];
+  __shared__ int pstep[256], plist[256];
+  const int tid = threadIdx.x, lane = tid & 31;
+  zt* M = A + (int64_t)blockIdx.x * bs;
+  WsPanels P;
+  P.npan = (n + NB - 1) / NB;
+  P.base = n / P.npan;
+  P.rem = n % P.npan;
+  if (tid < 256) pstep[tid] = 1 << 30;
+  const bool trace = g_ws_trace_on && blockIdx.x == 0 && (tid == 0 || tid == 256);
+  __syncthreads();
+
+  // roles: panel warps 8-15 (latency-critical; the SMSP arbiter favours high warp ids),
+  // update warps 0-7
+  if (tid >= 256) {
+    // ================= panel warps =================
+    // Thread = 4 rows x 7 columns of the panel (rows wp*32 + q*8 + rg, q = 0..3; columns
+    // cg*7 + c): per step each warp reads only 7 + 1 pivot-row elements from shared memory
+    // (a 128-bit LDS costs 4 crossbar cycles even as a broadcast, so one-row-per-thread
+    // panels are bound by the pivot-row broadcast), the multipliers of its rows travel by
+    // shuffle from the lane holding the active column.  Two barriers per step: pivot keys,
+    // then the winning row (published raw by its 4 lanes).
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
+    const int pt = tid - 256, wp = pt >> 5, cg = lane & 3, rg = lane >> 2;
+    int rq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rq[q] = wp * 32 + q * 8 + rg;
+    bool piv[4] = {false, false, false, false};
+    bool singular = false;
+    const bool warp_live = wp * 32 < n;
+    long long tacc[5] = {0, 0, 0, 0, 0};
+    for (int p = 0; p < P.npan; ++p) {
+      const int k0 = P.k0(p), w = P.w(p);
+      if (p > 0) bar_sync_n(BAR_READY, 512);  // columns of p updated by pass p-1
+      WS_MARK(p, 0);
+      zt a[4][7];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int c = 0; c < 7; ++c) {
+          const int j = cg * 7 + c;
+          a[q][c] = (rq[q] < n && j < w) ? __ldcg(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
+        }
+      for (int cga = 0; cga * 7 < w; ++cga) {
+        const bool act = cg == cga;
+        const int src = (lane & ~3) | cga;
+#pragma unroll
+        for (int s = 0; s < 7; ++s) {
+          const int kk = cga * 7 + s;
+          if (kk < w) {
+            const int k = k0 + kk, par = k & 1;
+            long long c0 = trace ? clock64() : 0;
+            unsigned key = 0u;
+            if (act) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (!piv[q] && rq[q] < n) key = max(key, pivot_key(a[q][s], rq[q], true));
+            }
+            key = __reduce_max_sync(0xffffffffu, key);
+            if (lane == 0) wkey4[par][wp] = key;
+            long long c1 = trace ? clock64() : 0;
+            bar_sync_n(BAR_PANEL, 256);
+            long long c2 = trace ? clock64() : 0;
+            const uint4 k03 = *reinterpret_cast<const uint4*>(&wkey4[par][0]);
+            const uint4 k47 = *reinterpret_cast<const uint4*>(&wkey4[par][4]);
+            const unsigned best =
+                max(max(max(k03.x, k03.y), max(k03.z, k03.w)), max(max(k47.x, k47.y), max(k47.z, k47.w)));
+            if ((best & ~511u) == 0u) singular = true;
+            const int r = 511 - (int)(best & 511u);
+            if (wp == (r >> 5) && rg == (r & 7)) {  // the 4 lanes of row r publish it raw
+              const int qq = (r >> 3) & 3;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (q == qq) {
+#pragma unroll
+                  for (int c = 0; c < 7; ++c) prow4[par][cg * 7 + c] = a[q][c];
+                }
+              if (cg == 0) {
+                pstep[r] = k;
+                plist[k] = r;
+              }
+            }
+            long long c3 = trace ? clock64() : 0;
+            bar_sync_n(BAR_PANEL, 256);
+            long long c4 = trace ? clock64() : 0;
+            if (warp_live) {
+              const zt inv = zinv_fast(prow4[par][kk]);
+              zt g[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const zt v = a[q][s];
+                g[q] = zmul(make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)), inv);
+                if (rq[q] == r) {  // pivot row: a <- pr / pivot  (as 0 - (-inv) pr)
+                  piv[q] = true;
+                  g[q] = make_double2(-inv.x, -inv.y);
+#pragma unroll
+                  for (int c = 0; c < 7; ++c) a[q][c] = make_double2(0.0, 0.0);
+                }
+              }
+#pragma unroll
+              for (int c = 0; c < 7; ++c) {
+                const zt pc = prow4[par][cg * 7 + c];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  a[q][c].x = fma(-g[q].x, pc.x, a[q][c].x);
+                  a[q][c].y = fma(-g[q].x, pc.y, a[q][c].y);
+                  a[q][c].x = fma(g[q].y, pc.y, a[q][c].x);
+                  a[q][c].y = fma(-g[q].y, pc.x, a[q][c].y);
+                }
+              }
+              if (act) {  // active column: -g (= 1/pivot on the pivot row)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) a[q][s] = make_double2(-g[q].x, -g[q].y);
+              }
+            }
+            if (trace) {
+              // force completion of the update before reading the clock
+              double sink = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) sink += a[q][6].x;
+              long long c5 = clock64() + (sink == 12345.678 ? 1 : 0);
+              tacc[0] += c1 - c0;
+              tacc[1] += c2 - c1;
+              tacc[2] += c3 - c2;
+              tacc[3] += c4 - c3;
+              tacc[4] += c5 - c4;
+            }
+          }
+        }
+      }
+      WS_MARK(p, 1);
+      if (p > 0) bar_sync_n(BAR_TFREE, 512);  // update warps done with T / Z of p-1
+      WS_MARK(p, 2);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (rq[q] < mtr) {
+#pragma unroll
+          for (int c = 0; c < 7; ++c) {
+            const int j = cg * 7 + c;
+            Ts[rq[q] * NB + j] = j < w ? a[q][c] : make_double2(0.0, 0.0);
+            if (j < w && rq[q] < n) M[(int64_t)rq[q] * lda + k0 + j] = a[q][c];
+          }
+        }
+      fence_cta();
+      bar_arrive_n(BAR_TREADY, 512);
+      WS_MARK(p, 3);
+    }
+    if (singular && pt == 0) atomicCAS(info, 0, blockIdx.x + 1);
+    if (trace)
+      for (int e = 0; e < 5; ++e) g_ws_trace[15 * 16 + e] = tacc[e];
+  } else {
+    // ================= update warps =================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+    const int u = tid, uw = u >> 5;
+    const int MT = mtr >> 3;
+    for (int p = 0; p < P.npan; ++p) {
+      const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2;
+      const bool has_next = p + 1 < P.npan;
+      const int w1 = has_next ? P.w(p + 1) : 0;
+      const int nv = n - w;
+      // virtual column v -> actual: [0, w1) = panel p+1, then [0, k0) and [k0 + w + w1, n)
+      auto act = [&](int v) {
+        if (v < w1) return k0 + w + v;
+        v -= w1;
+        return v < k0 ? v : v + w + w1;
+      };
+      bar_sync_n(BAR_TREADY, 512);
+      WS_MARK(p, 4);
+      // stage Z (two cp.async groups: the columns of panel p+1, then the rest)
+      for (int part = 0; part < 2; ++part) {
+        const int v0 = part ? w1 : 0, nvp = part ? nv - w1 : w1;
+        for (int e = u; e < w4 * nvp; e += 256) {
+          const int m = e / nvp, v = v0 + e - m * nvp;
+          const bool ok = m < w;
+          const int srow = ok ? plist[k0 + m] : 0;
+          cpa16_zfill(Zs + m * zs + v, M + (int64_t)srow * lda + act(v), ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+      }
+      for (int part = 0; part < 2; ++part) {
+        const int v0 = part ? w1 : 0, v1 = part ? nv : w1;
+        if (part == 0) {
+          if (!has_next) continue;
+          asm volatile("cp.async.wait_group 1;\n" ::);
+        } else {
+          asm volatile("cp.async.wait_group 0;\n" ::);
+        }
+        bar_sync_n(BAR_UPD, 256);
+        WS_MARK(p, 5 + 2 * part);
+        const int NPR = (v1 - v0 + 15) >> 4, units = MT * NPR;
+        // unit (m-tile mt, 16 virtual columns from vb): seeds for unit un + 8 are prefetched
+        // into registers while unit un runs on the tensor cores
+        struct Unit {
+          int rr, col[2][2];
+          bool rok, cok[2][2];
+          zt seed[2][2];
+        };
+        auto load_unit = [&](int un, Unit& U) {
+          const int mt = un % MT, vb = v0 + (un / MT) * 16;
+          U.rr = mt * 8 + (lane >> 2);
+          U.rok = U.rr < n && (unsigned)(pstep[U.rr < n ? U.rr : 0] - k0) >= (unsigned)w;
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int v = vb + t * 8 + (lane & 3) * 2 + h;
+              U.cok[t][h] = v < v1;
+              U.col[t][h] = U.cok[t][h] ? act(v) : 0;
+              U.seed[t][h] = (U.rok && U.cok[t][h]) ? __ldcg(M + (int64_t)U.rr * lda + U.col[t][h])
+                                                    : make_double2(0.0, 0.0);
+            }
+        };
+        Unit cur, nxt;
+        if (uw < units) load_unit(uw, nxt);
+        for (int un = uw; un < units; un += 8) {
+          cur = nxt;
+          if (un + 8 < units) load_unit(un + 8, nxt);
+          const int mt = un % MT, vb = v0 + (un / MT) * 16;
+          double ar[2][2], ai[2][2];
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              ar[t][h] = cur.seed[t][h].x;
+              ai[t][h] = cur.seed[t][h].y;
+            }
+          const zt* Trow = Ts + (mt * 8 + (lane >> 2)) * NB + (lane & 3);
+          const zt* Zc = Zs + (lane & 3) * zs + vb + (lane >> 2);
+#pragma unroll 7
+          for (int k4 = 0; k4 < K4; ++k4) {
+            const zt a = Trow[k4 * 4];
+            const zt b0 = Zc[k4 * 4 * zs], b1 = Zc[k4 * 4 * zs + 8];
+            dmma884(ar[0][0], ar[0][1], a.x, b0.x);
+            dmma884(ar[1][0], ar[1][1], a.x, b1.x);
+            dmma884(ai[0][0], ai[0][1], a.x, b0.y);
+            dmma884(ai[1][0], ai[1][1], a.x, b1.y);
+            dmma884(ar[0][0], ar[0][1], -a.y, b0.y);
+            dmma884(ar[1][0], ar[1][1], -a.y, b1.y);
+            dmma884(ai[0][0], ai[0][1], a.y, b0.x);
+            dmma884(ai[1][0], ai[1][1], a.y, b1.x);
+          }
+          if (cur.rr < n) {
+#pragma unroll
+            for (int t = 0; t < 2; ++t)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+                if (cur.cok[t][h]) M[(int64_t)cur.rr * lda + cur.col[t][h]] = make_double2(ar[t][h], ai[t][h]);
+          }
+        }
+        WS_MARK(p, 6 + 2 * part);
+        if (part == 0) {
+          fence_cta();
+          bar_arrive_n(BAR_READY, 512);
+        }
+      }
+      if (has_next) bar_arrive_n(BAR_TFREE, 512);
+    }
+  }
+  __syncthreads();
+  // A^{-1}(k, j) = M(plist[k], pstep[j])
+  zt* ob = out + (int64_t)blockIdx.x * obs;
+  for (int e = tid; e < n * n; e += 512) {
+    const int k = e / n, j = e - k * n;
+    ob[(int64_t)k * ldo + j] = __ldcg(M + (int64_t)plist[k] * lda + pstep[j]);
+  }
+}
+
 // pi = S_{n-1} o ... o S_0 (one thread per matrix)
 __global__ void zgj_pi_kernel(const int* piv_all, int* pi_all, int n, int batch) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -795,6 +1125,28 @@ PanelPlan panel_plan(int n) {
 
 bool use_small(int n, int batch) { return n <= 32; }
 bool use_fused(int n, int batch) { return n > 32 && n <= 256 && (batch >= 16 || n <= 128); }
+// HPS_GJ=fused|blocked forces the older paths (kernel comparisons in tools/gj_tune.py)
+}  // namespace
+int g_gj_mode_force = 0;
+// debug: timeline of CTA 0 of the next zgj_ws launch (on = 1 arms it; out[160] clock64 values)
+void zgj_ws_trace(int on, long long* out) {
+  HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_ws_trace_on, &on, sizeof(int)));
+  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_ws_trace, sizeof(long long) * 256));
+}  // hps_zinv_timed: 1 = fused, 2 = blocked (0 = library choice / HPS_GJ)
+namespace {
+int gj_mode_env() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("HPS_GJ");
+    m = (e && !strcmp(e, "fused")) ? 1 : (e && !strcmp(e, "blocked")) ? 2 : 0;
+  }
+  return g_gj_mode_force ? g_gj_mode_force : m;
+}
+// measured (tools/gj_tune.py): the warp-specialised kernel wins for 100 <= n <= 200 at every batch size;
+// above that its panel phase (8 warps x 4 rows) outgrows the update
+bool use_ws(int n, int batch) {
+  return (gj_mode_env() == 0 && n >= 100 && n <= 200) || (gj_mode_env() == 3 && n > 32 && n <= WS_NMAX);
+}
 
 void launch_cluster(const void* kern, int grid, int cs, size_t smem, cudaStream_t st, void** args) {
   cudaLaunchConfig_t cfg = {};
@@ -834,7 +1186,24 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     }
     return;
   }
-  if (use_fused(n, batch)) {
+  if (use_ws(n, batch)) {
+    ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
+    static bool wattr = false;
+    if (!wattr) {
+      HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)ws_smem(WS_NMAX)));
+      wattr = true;
+    }
+    for (int b0 = 0; b0 < batch; b0 += 65535) {
+      const int nbatch = std::min(65535, batch - b0);
+      zgj_ws_kernel<<<nbatch, 512, ws_smem(n), st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
+                                                      obs, n, info);
+      HPS_CUDA_CHECK(cudaGetLastError());
+      count_launch();
+    }
+    return;
+  }
+  if (gj_mode_env() != 2 && use_fused(n, batch)) {
     ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
@@ -953,7 +1322,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
 }  // namespace
 
 size_t zgj_workspace_bytes(int n, int batch) {
-  if (use_small(n, batch) || use_fused(n, batch)) return 16;
+  if (use_small(n, batch) || use_ws(n, batch) || (gj_mode_env() != 2 && use_fused(n, batch))) return 16;
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256;
 }

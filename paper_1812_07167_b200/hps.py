@@ -38,7 +38,7 @@ class hps_opts(C.Structure):
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
-           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
+           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free",
            "hps_last_error"]
 
@@ -75,6 +75,8 @@ def lib():
                                        C.POINTER(C.c_double)]
         L.hps_reset_stats.argtypes = [vp]
         L.hps_zinv_batched.argtypes = [i32, i32, dp, dp]
+        L.hps_zinv_timed.argtypes = [i32, i32, i32, dp, dp, i32, C.POINTER(C.c_double)]
+        L.hps_debug_ws_trace.argtypes = [i32, dp]
         L.hps_zgemm_batched.argtypes = [i32, i32, i32, i32, i32, dp, dp, dp, dp, hps_c128, hps_c128, i32,
                                         C.POINTER(C.c_double)]
         L.hps_subtree_grid.argtypes = [C.POINTER(hps_grid), i32, i64, C.POINTER(hps_grid), C.POINTER(C.c_int32),
@@ -173,6 +175,17 @@ def zinv_batched(A):
     out = np.zeros_like(A)
     _check(lib().hps_zinv_batched(A.shape[-1], A.shape[0], A.ctypes.data, out.ctypes.data))
     return out
+
+
+def zinv_timed(A, mode=0, reps=3):
+    """Batched inverse of A [batch, n, n] (numpy or torch CUDA) with kernel family `mode`
+    (0 library choice, 1 fused, 2 blocked); returns (A^{-1}, mean ms per inversion)."""
+    batch, n, _ = A.shape
+    out = _empty_like_ref(A, (batch, n, n))
+    ms = C.c_double()
+    _check(lib().hps_zinv_timed(mode, n, batch, _ptr(A, batch * n * n, "A"), _ptr(out, batch * n * n, "out"), reps,
+                                C.byref(ms)))
+    return out, ms.value
 
 
 class Solver:
