@@ -785,7 +785,7 @@ __host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16
   return ((need - 2 + 7) / 8) * 8 + 2;
 }
 __host__ __device__ inline size_t ws_smem(int n) {
-  return sizeof(zt) * ((size_t)((n + 7) & ~7) * WS_NB + (size_t)WS_NB * ws_zs(n));
+  return sizeof(zt) * ((size_t)((n + 15) & ~15) * WS_NB + (size_t)WS_NB * ws_zs(n));
 }
 
 __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
@@ -793,12 +793,12 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
                                                         int* __restrict__ info) {
   constexpr int NB = WS_NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int mtr = (n + 7) & ~7, zs = ws_zs(n);
-  zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [mtr][NB]  T of the current panel
+  const int mtr = (n + 15) & ~15, zs = ws_zs(n);
+  zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [mtr][NB]  T of the current panel (16-row pairs)
   zt* Zs = Ts + (size_t)mtr * NB;            // [NB][zs]   old pivot rows, virtual column order
   __shared__ zt prow4[2][NB];
   __shared__ __align__(16) unsigned wkey4[2][8];
-  __shared__ int pstep[256], plist[256];
+  __shared__ int pstep[256], plist[256], colmap[WS_NMAX + 16];
   const int tid = threadIdx.x, lane = tid & 31;
   zt* M = A + (int64_t)blockIdx.x * bs;
   WsPanels P;
@@ -827,7 +827,6 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
     bool piv[4] = {false, false, false, false};
     bool singular = false;
     const bool warp_live = wp * 32 < n;
-    long long tacc[5] = {0, 0, 0, 0, 0};
     for (int p = 0; p < P.npan; ++p) {
       const int k0 = P.k0(p), w = P.w(p);
       if (p > 0) bar_sync_n(BAR_READY, 512);  // columns of p updated by pass p-1
@@ -848,7 +847,6 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
           const int kk = cga * 7 + s;
           if (kk < w) {
             const int k = k0 + kk, par = k & 1;
-            long long c0 = trace ? clock64() : 0;
             unsigned key = 0u;
             if (act) {
 #pragma unroll
@@ -857,9 +855,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
             }
             key = __reduce_max_sync(0xffffffffu, key);
             if (lane == 0) wkey4[par][wp] = key;
-            long long c1 = trace ? clock64() : 0;
             bar_sync_n(BAR_PANEL, 256);
-            long long c2 = trace ? clock64() : 0;
             const uint4 k03 = *reinterpret_cast<const uint4*>(&wkey4[par][0]);
             const uint4 k47 = *reinterpret_cast<const uint4*>(&wkey4[par][4]);
             const unsigned best =
@@ -879,22 +875,26 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
                 plist[k] = r;
               }
             }
-            long long c3 = trace ? clock64() : 0;
             bar_sync_n(BAR_PANEL, 256);
-            long long c4 = trace ? clock64() : 0;
             if (warp_live) {
               const zt inv = zinv_fast(prow4[par][kk]);
               zt g[4];
+              bool isp[4];
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
                 const zt v = a[q][s];
                 g[q] = zmul(make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)), inv);
-                if (rq[q] == r) {  // pivot row: a <- pr / pivot  (as 0 - (-inv) pr)
-                  piv[q] = true;
-                  g[q] = make_double2(-inv.x, -inv.y);
+                isp[q] = rq[q] == r;
+              }
+              if (wp == (r >> 5)) {  // warp-uniform: the warp holding the pivot row
 #pragma unroll
-                  for (int c = 0; c < 7; ++c) a[q][c] = make_double2(0.0, 0.0);
-                }
+                for (int q = 0; q < 4; ++q)
+                  if (isp[q]) {  // pivot row: a <- pr / pivot exactly (as 0 - (-inv) pr)
+                    piv[q] = true;
+                    g[q] = make_double2(-inv.x, -inv.y);
+#pragma unroll
+                    for (int c = 0; c < 7; ++c) a[q][c] = make_double2(0.0, 0.0);
+                  }
               }
 #pragma unroll
               for (int c = 0; c < 7; ++c) {
@@ -911,18 +911,6 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
 #pragma unroll
                 for (int q = 0; q < 4; ++q) a[q][s] = make_double2(-g[q].x, -g[q].y);
               }
-            }
-            if (trace) {
-              // force completion of the update before reading the clock
-              double sink = 0;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) sink += a[q][6].x;
-              long long c5 = clock64() + (sink == 12345.678 ? 1 : 0);
-              tacc[0] += c1 - c0;
-              tacc[1] += c2 - c1;
-              tacc[2] += c3 - c2;
-              tacc[3] += c4 - c3;
-              tacc[4] += c5 - c4;
             }
           }
         }
@@ -945,8 +933,6 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
       WS_MARK(p, 3);
     }
     if (singular && pt == 0) atomicCAS(info, 0, blockIdx.x + 1);
-    if (trace)
-      for (int e = 0; e < 5; ++e) g_ws_trace[15 * 16 + e] = tacc[e];
   } else {
     // ================= update warps =================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
@@ -965,6 +951,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
       };
       bar_sync_n(BAR_TREADY, 512);
       WS_MARK(p, 4);
+      for (int v = u; v < nv + 16; v += 256) colmap[v] = v < nv ? act(v) : -1;
       // stage Z (two cp.async groups: the columns of panel p+1, then the rest)
       for (int part = 0; part < 2; ++part) {
         const int v0 = part ? w1 : 0, nvp = part ? nv - w1 : w1;
@@ -986,35 +973,51 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
         }
         bar_sync_n(BAR_UPD, 256);
         WS_MARK(p, 5 + 2 * part);
-        const int NPR = (v1 - v0 + 15) >> 4, units = MT * NPR;
-        // unit (m-tile mt, 16 virtual columns from vb): seeds for unit un + 8 are prefetched
-        // into registers while unit un runs on the tensor cores
+        const int NPR = (v1 - v0 + 15) >> 4;
+        // unit = (m-tile mt, 16 virtual columns from v0 + 16 npr), dealt round-robin over the 8
+        // update warps; the seeds of the next unit are prefetched into registers while the
+        // current one runs on the tensor cores.  Column addresses come from colmap (no integer
+        // division or branches on the issue path).
         struct Unit {
           int rr, col[2][2];
-          bool rok, cok[2][2];
+          bool rok;
           zt seed[2][2];
         };
-        auto load_unit = [&](int un, Unit& U) {
-          const int mt = un % MT, vb = v0 + (un / MT) * 16;
+        auto load_unit = [&](int mt, int npr, Unit& U) {
           U.rr = mt * 8 + (lane >> 2);
-          U.rok = U.rr < n && (unsigned)(pstep[U.rr < n ? U.rr : 0] - k0) >= (unsigned)w;
+          const int rc = min(U.rr, n - 1);
+          U.rok = U.rr < n && (unsigned)(pstep[rc] - k0) >= (unsigned)w;
+          const int vb = v0 + npr * 16 + (lane & 3) * 2;
+          const zt* rowp = M + (int64_t)rc * lda;
 #pragma unroll
           for (int t = 0; t < 2; ++t)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const int v = vb + t * 8 + (lane & 3) * 2 + h;
-              U.cok[t][h] = v < v1;
-              U.col[t][h] = U.cok[t][h] ? act(v) : 0;
-              U.seed[t][h] = (U.rok && U.cok[t][h]) ? __ldcg(M + (int64_t)U.rr * lda + U.col[t][h])
-                                                    : make_double2(0.0, 0.0);
+              const int v = vb + t * 8 + h;
+              U.col[t][h] = v < v1 ? colmap[v] : -1;
+              const zt sv = __ldcg(rowp + max(U.col[t][h], 0));
+              U.seed[t][h] = (U.rok && U.col[t][h] >= 0) ? sv : make_double2(0.0, 0.0);
             }
         };
         Unit cur, nxt;
-        if (uw < units) load_unit(uw, nxt);
-        for (int un = uw; un < units; un += 8) {
+        int mt = uw, npr = 0;
+        while (mt >= MT) {
+          mt -= MT;
+          ++npr;
+        }
+        bool have = npr < NPR;
+        if (have) load_unit(mt, npr, nxt);
+        while (have) {
           cur = nxt;
-          if (un + 8 < units) load_unit(un + 8, nxt);
-          const int mt = un % MT, vb = v0 + (un / MT) * 16;
+          const int cmt = mt, cnpr = npr;
+          mt += 8;
+          while (mt >= MT) {
+            mt -= MT;
+            ++npr;
+          }
+          have = npr < NPR;
+          if (have) load_unit(mt, npr, nxt);
+          const int vb = v0 + cnpr * 16;
           double ar[2][2], ai[2][2];
 #pragma unroll
           for (int t = 0; t < 2; ++t)
@@ -1023,7 +1026,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
               ar[t][h] = cur.seed[t][h].x;
               ai[t][h] = cur.seed[t][h].y;
             }
-          const zt* Trow = Ts + (mt * 8 + (lane >> 2)) * NB + (lane & 3);
+          const zt* Trow = Ts + (cmt * 8 + (lane >> 2)) * NB + (lane & 3);
           const zt* Zc = Zs + (lane & 3) * zs + vb + (lane >> 2);
 #pragma unroll 7
           for (int k4 = 0; k4 < K4; ++k4) {
@@ -1039,11 +1042,12 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
             dmma884(ai[1][0], ai[1][1], a.y, b1.x);
           }
           if (cur.rr < n) {
+            zt* rowp = M + (int64_t)cur.rr * lda;
 #pragma unroll
             for (int t = 0; t < 2; ++t)
 #pragma unroll
               for (int h = 0; h < 2; ++h)
-                if (cur.cok[t][h]) M[(int64_t)cur.rr * lda + cur.col[t][h]] = make_double2(ar[t][h], ai[t][h]);
+                if (cur.col[t][h] >= 0) rowp[cur.col[t][h]] = make_double2(ar[t][h], ai[t][h]);
           }
         }
         WS_MARK(p, 6 + 2 * part);

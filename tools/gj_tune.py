@@ -39,9 +39,6 @@ if os.environ.get("WS_TRACE"):
     names = ["P:ready", "P:factored", "P:tfree", "P:tready", "U:tready", "U:z1", "U:ph1", "U:z2", "U:ph2", "-"]
     print("n", n, "batch", batch, "(kclk relative to pass 0 start)")
     print("  p " + " ".join(f"{x:>10s}" for x in names[:9]))
-    steps = n
-    print("panel step stages (clk/step, thread 0 of the panel warps): key+redux %.0f | bar1 %.0f | select+publish %.0f | bar2 %.0f | update %.0f"
-          % tuple(t[15, :5] / steps))
     for p in range(15):
         if t[p].any():
             print(f"{p:3d} " + " ".join(f"{(v - t0) / 1e3:10.1f}" if v else f"{'':>10s}" for v in t[p, :9]))
