@@ -70,8 +70,11 @@ typedef struct {
   int32_t leaf_chunk;   /* leaves factored per batch (0 = automatic) */
   int32_t profile;      /* bit mask of kernel classes (see hps_kernel_stats) to time with CUDA
                            events on the library stream; -1 = all; 0: counters only (default) */
-  int32_t leaf_mode;    /* 0 (default): B^{-1} through the interior Schur complement;
-                           1: Gauss-Jordan on the full n^tau x n^tau matrix B */
+  int32_t leaf_mode;    /* 0 (default): B^{-1} through the interior Schur complement,
+                           with [Psi | Y] and R formed in the epilogue of the inverse kernel;
+                           1: Gauss-Jordan on the full n^tau x n^tau matrix B;
+                           2: as 0 but with the separate finish kernel (comparison path).
+                           Other values: HPS_EINVAL */
 } hps_opts;
 
 /* Precomputation stage (Algorithm 1).

@@ -226,7 +226,8 @@ struct hps_handle {
   SolveState ss;
   DevBuf ident;             // identity index map 0 .. 2^Lb - 1
   bool keep_root_R = true, keep_all_R = false;
-  int leaf_mode = 0;  // 0: Schur complement on the interior (default), 1: invert the full B
+  int leaf_mode = 0;  // 0: Schur complement on the interior (default), 1: invert the full B, 2: Schur, unfused
+  bool leaf_fused = true;
   std::vector<Depth> depth;
   std::vector<int> leaf_nat_h, nat_to_heap_h;
   DevBuf leaf_nat, nat_to_heap;
@@ -502,7 +503,7 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
 
   const size_t mat = (size_t)nt * nt;
   H.store.alloc(sizeof(zt) * mat * nleaf);
-  const bool schur = H.leaf_mode == 0;
+  const bool schur = H.leaf_mode != 1;
   const int ninv = schur ? H.ni : nt;  // matrix inverted per leaf
   const size_t wmat = (size_t)ninv * ninv;
   int chunk = chunk_opt > 0 ? chunk_opt : (int)std::max<size_t>(1, ((size_t)1 << 30) / (wmat * sizeof(zt)));
@@ -511,11 +512,20 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   work.alloc(sizeof(zt) * wmat * chunk);
   ws.alloc(std::max<size_t>(zgj_workspace_bytes(ninv, chunk), 16));
   if (schur) upload(dK, schur_consts(p, hx, hy, H.eta, dm), H.st);
+  // leaf R (PAPER.md:398-402 via R = I - 2 i eta Psi_b): written by the fused leaf epilogue where
+  // it applies, else by leaf_R below
+  H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
+  bool fused_all = schur;
   for (int l0 = 0; l0 < nleaf; l0 += chunk) {
     const int nc = std::min(chunk, nleaf - l0);
     if (schur) {
       launch_leaf_schur_assemble(work.as<zt>(), (int64_t)wmat, l0, nc, H.leaf_nat.as<int>(), c_dev, p, dK.as<zt>(),
                                  H.kappa * H.kappa, H.st);
+      if (H.leaf_fused &&
+          zgj_invert_leaf_schur(work.as<zt>(), (int64_t)wmat, H.store.as<zt>() + (size_t)l0 * mat, (int64_t)mat, p, nc,
+                                dK.as<zt>(), H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, H.eta, H.info.as<int>(), H.st))
+        continue;
+      fused_all = false;
       zgj_invert(work.as<zt>(), ninv, (int64_t)wmat, H.store.as<zt>() + (size_t)l0 * mat + (size_t)nb * nt + nb, nt,
                  (int64_t)mat, ninv, nc, ws.p, H.info.as<int>(), H.st, nullptr);
       launch_leaf_schur_finish(H.store.as<zt>(), (int64_t)mat, l0, nc, p, dK.as<zt>(), H.st);
@@ -532,9 +542,7 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   } else {
     H.flops[0] += 8.0 * (double)nt * nt * nt * nleaf;
   }
-  // leaf R (PAPER.md:398-402 via R = I - 2 i eta Psi_b)
-  H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
-  launch_leaf_R(H.store.as<zt>(), (int64_t)mat, H.R[H.L].as<zt>(), nleaf, nt, nb, H.eta, H.st);
+  if (!fused_all) launch_leaf_R(H.store.as<zt>(), (int64_t)mat, H.R[H.L].as<zt>(), nleaf, nt, nb, H.eta, H.st);
 }
 
 void build_merge(hps_handle& H, int d) {
@@ -970,6 +978,7 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   H.keep_root_R = opt ? opt->keep_root_R != 0 : true;
   H.keep_all_R = opt ? opt->keep_all_R != 0 : false;
   H.leaf_mode = opt ? opt->leaf_mode : 0;
+  H.leaf_fused = H.leaf_mode == 0;
   H.prof.timing = opt ? (unsigned)opt->profile : 0u;
 }
 
@@ -1059,6 +1068,10 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     return HPS_EINVAL;
   }
   if (int rc = validate_problem(g, p, q, kappa, eta, "hps_build")) return rc;
+  if (opt && (opt->leaf_mode < 0 || opt->leaf_mode > 2)) {
+    hps_set_error("hps_build: leaf_mode must be 0, 1 or 2");
+    return HPS_EINVAL;
+  }
   std::unique_ptr<hps_handle> H(new hps_handle());
   try {
     init_handle(*H, g, p, q, kappa, eta, opt);

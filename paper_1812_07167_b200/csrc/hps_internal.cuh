@@ -87,6 +87,13 @@ size_t zgj_workspace_bytes(int n, int batch);
 void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
                 void* ws, int* info, cudaStream_t st, int64_t* launches);
 
+// Leaf S^{-1} by the warp-specialised Gauss-Jordan kernel with the fused Schur epilogue: writes
+// the whole leaf operator [Psi | Y] (n_t x n_t, stride mstride) and the leaf R (nb x nb, batch
+// stride nb*nb) for `batch` leaves; S (n_i x n_i, stride sstride) is destroyed.  K =
+// schur_consts.  Returns false without launching when the kernel does not apply.
+bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
+                           zt eta, int* info, cudaStream_t st);
+
 // Debug timeline of the warp-specialised Gauss-Jordan kernel (hps_debug_ws_trace).
 void zgj_ws_trace(int on, long long* out);
 

@@ -779,6 +779,18 @@ struct WsPanels {
   __device__ __forceinline__ int w(int p) const { return p < npan ? base + (p < rem ? 1 : 0) : 0; }
 };
 
+// Leaf epilogue (leaf_mode 0): instead of writing S^{-1} alone, the CTA that
+// inverted S forms the whole leaf operator [Psi | Y] = B^{-1} and the leaf R from it:
+//   Y_i = S^{-1},  Psi_i = S^{-1} U,  Y_b = -V S^{-1},  Psi_b = G - V Psi_i,  R = I - 2 i eta Psi_b
+// (U, V, G act along one grid line each; constants K from schur_consts).  S^{-1} is read once,
+// one x-line (q rows) at a time into shared memory; the y-line sums accumulate in shared memory.
+struct WsFinish {
+  const zt* K;   // schur_consts: Lx, Ly, Ubx, Uby, Vx, Vy, Gx, Gy
+  zt* R;         // leaf R of batch entry 0 (nb x nb, batch stride nb*nb)
+  zt m2ieta;     // -2 i eta
+  int p;         // 0 = plain inverse output
+};
+
 __host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16, == 2 (mod 8)
   const int npan = (n + WS_NB - 1) / WS_NB;
   const int need = n - n / npan + 16;
@@ -790,7 +802,7 @@ __host__ __device__ inline size_t ws_smem(int n) {
 
 __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
                                                         zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
-                                                        int* __restrict__ info) {
+                                                        int* __restrict__ info, const WsFinish fin) {
   constexpr int NB = WS_NB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mtr = (n + 15) & ~15, zs = ws_zs(n);
@@ -1060,12 +1072,131 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
     }
   }
   __syncthreads();
-  // A^{-1}(k, j) = M(plist[k], pstep[j])
   zt* ob = out + (int64_t)blockIdx.x * obs;
-  for (int e = tid; e < n * n; e += 512) {
-    const int k = e / n, j = e - k * n;
-    ob[(int64_t)k * ldo + j] = __ldcg(M + (int64_t)plist[k] * lda + pstep[j]);
+  if (fin.p == 0) {
+    // A^{-1}(k, j) = M(plist[k], pstep[j])
+    for (int e = tid; e < n * n; e += 512) {
+      const int k = e / n, j = e - k * n;
+      ob[(int64_t)k * ldo + j] = __ldcg(M + (int64_t)plist[k] * lda + pstep[j]);
+    }
+    return;
   }
+  // ---- fused leaf epilogue (n = n_i = q^2, ldo = n_t) ----
+  const int q = fin.p - 2, ni = n, nb = 4 * q, nt = (int)ldo;
+  const zt* Ubx = fin.K + 2 * q * q;
+  const zt* Uby = Ubx + 2 * q;
+  const zt* Vx = Uby + 2 * q;
+  const zt* Vy = Vx + 2 * q;
+  const zt* Gx = Vy + 2 * q;
+  const zt* Gy = Gx + 4;
+  zt* base = ob - ((int64_t)nb * nt + nb);  // leaf operator [Psi | Y], rows [I_b; I_i]
+  zt* Rl = fin.R + (int64_t)blockIdx.x * nb * nb;
+  zt* C = reinterpret_cast<zt*>(smem_raw);  // [q][ni]   S^{-1} rows of x-line k
+  zt* Pc = C + q * ni;                       // [q][nb]   Psi_i rows of x-line k
+  zt* accY = Pc + q * nb;                    // [2q][ni]  y-line sums for Y_b (S rows, then N rows)
+  zt* accP = accY + 2 * q * ni;              // [2q][nb]  y-line sums for Psi_b
+  const zt m2 = fin.m2ieta;
+  auto zmac = [](zt& acc, zt a, zt b) {
+    acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+    acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  };
+  auto put_psib = [&](int row, int b2, zt v) {  // Psi_b entry and the matching R entry
+    base[(int64_t)row * nt + b2] = v;
+    zt r = make_double2(m2.x * v.x - m2.y * v.y, m2.x * v.y + m2.y * v.x);
+    if (row == b2) r.x += 1.0;
+    Rl[row * nb + b2] = r;
+  };
+  for (int e = tid; e < 2 * q * ni; e += 512) accY[e] = make_double2(0.0, 0.0);
+  for (int e = tid; e < 2 * q * nb; e += 512) accP[e] = make_double2(0.0, 0.0);
+  for (int kx = 0; kx < q; ++kx) {  // x-line iy = kx: interior rows kx*q + t
+    __syncthreads();
+    for (int e = tid; e < q * ni; e += 512) {
+      const int t = e / ni, j = e - t * ni;
+      const zt v = __ldcg(M + (int64_t)plist[kx * q + t] * lda + pstep[j]);
+      C[e] = v;
+      base[(int64_t)(nb + kx * q + t) * nt + nb + j] = v;  // Y_i
+    }
+    __syncthreads();
+    // Psi_i rows of this line
+    for (int e = tid; e < q * nb; e += 512) {
+      const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
+      const zt* Cr = C + t * ni;
+      zt acc = make_double2(0.0, 0.0);
+      if (edge == 0 || edge == 2) {  // S / N: y-line ix = kk
+        const int side = edge == 0 ? 0 : 1;
+        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[t2 * q + kk], Uby[t2 * 2 + side]);
+      } else {  // E / W: x-line iy = kk
+        const int side = edge == 3 ? 0 : 1;
+        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[kk * q + t2], Ubx[t2 * 2 + side]);
+      }
+      Pc[e] = acc;
+      base[(int64_t)(nb + kx * q + t) * nt + b] = acc;
+    }
+    // Y_b: W_kx, E_kx complete on this line; S/N (y-lines) accumulate
+    for (int j = tid; j < ni; j += 512) {
+      zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+      for (int t = 0; t < q; ++t) {
+        const zt v = C[t * ni + j];
+        zmac(w0, Vx[t], v);
+        zmac(w1, Vx[q + t], v);
+      }
+      base[(int64_t)(3 * q + kx) * nt + nb + j] = make_double2(-w0.x, -w0.y);
+      base[(int64_t)(q + kx) * nt + nb + j] = make_double2(-w1.x, -w1.y);
+    }
+    for (int e = tid; e < q * ni; e += 512) {  // node (ix = kk, iy = kx) is position kx of y-line kk
+      const int kk = e / ni, j = e - kk * ni;
+      const zt v = C[kk * ni + j];
+      zmac(accY[kk * ni + j], Vy[kx], v);
+      zmac(accY[(q + kk) * ni + j], Vy[q + kx], v);
+    }
+    __syncthreads();  // Pc complete
+    for (int b2 = tid; b2 < nb; b2 += 512) {
+      zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+      for (int t = 0; t < q; ++t) {
+        const zt v = Pc[t * nb + b2];
+        zmac(w0, Vx[t], v);
+        zmac(w1, Vx[q + t], v);
+      }
+      const int e2 = b2 / q, k2 = b2 - e2 * q;
+      zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+      if (k2 == kx && (e2 == 1 || e2 == 3)) {
+        g0 = Gx[0 * 2 + (e2 == 3 ? 0 : 1)];
+        g1 = Gx[1 * 2 + (e2 == 3 ? 0 : 1)];
+      }
+      put_psib(3 * q + kx, b2, make_double2(g0.x - w0.x, g0.y - w0.y));
+      put_psib(q + kx, b2, make_double2(g1.x - w1.x, g1.y - w1.y));
+    }
+    for (int e = tid; e < q * nb; e += 512) {
+      const int kk = e / nb, b2 = e - kk * nb;
+      const zt v = Pc[kk * nb + b2];
+      zmac(accP[kk * nb + b2], Vy[kx], v);
+      zmac(accP[(q + kk) * nb + b2], Vy[q + kx], v);
+    }
+  }
+  __syncthreads();
+  // y-lines: S_kk (row kk) and N_kk (row 2q + kk)
+  for (int e = tid; e < q * ni; e += 512) {
+    const int kk = e / ni, j = e - kk * ni;
+    const zt a0 = accY[kk * ni + j], a1 = accY[(q + kk) * ni + j];
+    base[(int64_t)kk * nt + nb + j] = make_double2(-a0.x, -a0.y);
+    base[(int64_t)(2 * q + kk) * nt + nb + j] = make_double2(-a1.x, -a1.y);
+  }
+  for (int e = tid; e < q * nb; e += 512) {
+    const int kk = e / nb, b2 = e - kk * nb, e2 = b2 / q, k2 = b2 - e2 * q;
+    const zt a0 = accP[kk * nb + b2], a1 = accP[(q + kk) * nb + b2];
+    zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+    if (k2 == kk && (e2 == 0 || e2 == 2)) {
+      g0 = Gy[0 * 2 + (e2 == 0 ? 0 : 1)];
+      g1 = Gy[1 * 2 + (e2 == 0 ? 0 : 1)];
+    }
+    put_psib(kk, b2, make_double2(g0.x - a0.x, g0.y - a0.y));
+    put_psib(2 * q + kk, b2, make_double2(g1.x - a1.x, g1.y - a1.y));
+  }
+}
+
+size_t ws_finish_smem(int p) {
+  const size_t q = p - 2, ni = q * q, nb = 4 * q;
+  return sizeof(zt) * (q * ni + q * nb + 2 * q * ni + 2 * q * nb);
 }
 
 // pi = S_{n-1} o ... o S_0 (one thread per matrix)
@@ -1201,7 +1332,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
       zgj_ws_kernel<<<nbatch, 512, ws_smem(n), st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
-                                                      obs, n, info);
+                                                      obs, n, info, WsFinish{nullptr, nullptr, {0.0, 0.0}, 0});
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
     }
@@ -1324,6 +1455,34 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
 }
 
 }  // namespace
+
+// Leaf inverse with the fused Schur epilogue (see WsFinish).  Returns false (nothing launched)
+// when the warp-specialised kernel does not apply to n = (p-2)^2; the caller then runs the
+// plain inverse and leaf_schur_finish.
+bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
+                           zt eta, int* info, cudaStream_t st) {
+  const int q = p - 2, n = q * q, nb = 4 * q, nt = nb + n;
+  if (!use_ws(n, batch) || ws_finish_smem(p) > ws_smem(n)) return false;
+  static bool wattr = false;
+  if (!wattr) {
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)ws_smem(WS_NMAX)));
+    wattr = true;
+  }
+  const double ni = n;
+  ProfScope ps(K_GJ_FUSED, 8.0 * ni * ni * ni * batch + 8.0 * batch * q * (2.0 * ni * nb + (double)nb * nb),
+               16.0 * batch * (ni * ni + (double)nt * nt + nb * nb), st);
+  const zt m2ieta = make_double2(2.0 * eta.y, -2.0 * eta.x);
+  for (int b0 = 0; b0 < batch; b0 += 65535) {
+    const int nbatch = std::min(65535, batch - b0);
+    zgj_ws_kernel<<<nbatch, 512, ws_smem(n), st>>>(
+        S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
+        info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p});
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+  }
+  return true;
+}
 
 size_t zgj_workspace_bytes(int n, int batch) {
   if (use_small(n, batch) || use_ws(n, batch) || (gj_mode_env() != 2 && use_fused(n, batch))) return 16;

@@ -34,9 +34,11 @@ def problem(nx, ny, p, kappa, eta, x1=1.0, y1=1.0, nrhs=2, seed=0):
     return g, c, s, t
 
 
-@pytest.mark.parametrize("leaf_mode", [0, 1])
-@pytest.mark.parametrize("p", [4, 8, 10, 16, 20])
+@pytest.mark.parametrize("leaf_mode", [0, 1, 2])
+@pytest.mark.parametrize("p", [4, 8, 10, 12, 14, 16, 20])
 def test_leaf_parity(p, leaf_mode):
+    """Leaf operators Psi, Y and the leaf R on non-square leaves (h_x = 0.5, h_y = 1): p = 12, 14,
+    16 run the warp-specialised inverse (n_i = 100, 144, 196) with the fused epilogue in mode 0."""
     g, c, s, t = problem(2, 1, p, 7.0, 7.0 + 1j)
     S = hps.Solver(g, p, 7.0, 7.0 + 1j, c, keep_all_R=True, leaf_mode=leaf_mode)
     for leaf in range(2):
@@ -44,6 +46,7 @@ def test_leaf_parity(p, leaf_mode):
         lo = oracle.leaf(p, 0.5, 1.0, 7.0, 7.0 + 1j, c[leaf])
         assert rel(Psi, lo["Psi"]) < TOL
         assert rel(Y, lo["Y"]) < TOL
+        assert rel(S.R(2 + leaf), lo["R"]) < TOL
 
 
 @pytest.mark.parametrize("nx,ny,p", [(1, 1, 8), (2, 1, 8), (1, 2, 6), (4, 4, 8), (8, 4, 6), (4, 8, 10)])
