@@ -107,7 +107,7 @@ inline void count_launch(int k = 1) {
 // Per-kernel-class accounting (hps_kernel_stats): launches, algorithmic FLOPs / bytes, and —
 // when profiling is on — device time from CUDA events recorded on the launching stream.
 // ---------------------------------------------------------------------------
-enum KClass { K_ZGEMM = 0, K_GJ_PANEL, K_GJ_SMALL, K_GJ_AUX, K_LEAF_ASM, K_LAYOUT, K_GJ_FUSED, K_NCLASS };
+enum KClass { K_ZGEMM = 0, K_GJ_PANEL, K_GJ_SMALL, K_GJ_AUX, K_LEAF_ASM, K_LAYOUT, K_GJ_FUSED, K_LEAF_GJ, K_NCLASS };
 
 struct KStats {
   int64_t launches[K_NCLASS] = {};

@@ -1007,8 +1007,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
             for (int h = 0; h < 2; ++h) {
               const int v = vb + t * 8 + h;
               U.col[t][h] = v < v1 ? colmap[v] : -1;
-              const zt sv = __ldcg(rowp + max(U.col[t][h], 0));
-              U.seed[t][h] = (U.rok && U.col[t][h] >= 0) ? sv : make_double2(0.0, 0.0);
+              U.seed[t][h] = __ldcg(rowp + max(U.col[t][h], 0));  // masked at use: no wait here
             }
         };
         Unit cur, nxt;
@@ -1035,8 +1034,9 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
           for (int t = 0; t < 2; ++t)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              ar[t][h] = cur.seed[t][h].x;
-              ai[t][h] = cur.seed[t][h].y;
+              const bool ok = cur.rok && cur.col[t][h] >= 0;
+              ar[t][h] = ok ? cur.seed[t][h].x : 0.0;
+              ai[t][h] = ok ? cur.seed[t][h].y : 0.0;
             }
           const zt* Trow = Ts + (cmt * 8 + (lane >> 2)) * NB + (lane & 3);
           const zt* Zc = Zs + (lane & 3) * zs + vb + (lane >> 2);
@@ -1077,11 +1077,12 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
     // A^{-1}(k, j) = M(plist[k], pstep[j])
     for (int e = tid; e < n * n; e += 512) {
       const int k = e / n, j = e - k * n;
-      ob[(int64_t)k * ldo + j] = __ldcg(M + (int64_t)plist[k] * lda + pstep[j]);
+      __stcs(&ob[(int64_t)k * ldo + j], __ldcg(M + (int64_t)plist[k] * lda + pstep[j]));
     }
     return;
   }
-  // ---- fused leaf epilogue (n = n_i = q^2, ldo = n_t) ----
+  // ---- fused leaf epilogue (n = n_i = q^2, ldo = n_t); outputs are streamed past L2 (st.cs) so the
+  // in-place matrices of the other CTAs stay resident ----
   const int q = fin.p - 2, ni = n, nb = 4 * q, nt = (int)ldo;
   const zt* Ubx = fin.K + 2 * q * q;
   const zt* Uby = Ubx + 2 * q;
@@ -1101,10 +1102,10 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
     acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
   };
   auto put_psib = [&](int row, int b2, zt v) {  // Psi_b entry and the matching R entry
-    base[(int64_t)row * nt + b2] = v;
+    __stcs(&base[(int64_t)row * nt + b2], v);
     zt r = make_double2(m2.x * v.x - m2.y * v.y, m2.x * v.y + m2.y * v.x);
     if (row == b2) r.x += 1.0;
-    Rl[row * nb + b2] = r;
+    __stcs(&Rl[row * nb + b2], r);
   };
   for (int e = tid; e < 2 * q * ni; e += 512) accY[e] = make_double2(0.0, 0.0);
   for (int e = tid; e < 2 * q * nb; e += 512) accP[e] = make_double2(0.0, 0.0);
@@ -1114,7 +1115,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
       const int t = e / ni, j = e - t * ni;
       const zt v = __ldcg(M + (int64_t)plist[kx * q + t] * lda + pstep[j]);
       C[e] = v;
-      base[(int64_t)(nb + kx * q + t) * nt + nb + j] = v;  // Y_i
+      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + nb + j], v);  // Y_i
     }
     __syncthreads();
     // Psi_i rows of this line
@@ -1130,7 +1131,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
         for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[kk * q + t2], Ubx[t2 * 2 + side]);
       }
       Pc[e] = acc;
-      base[(int64_t)(nb + kx * q + t) * nt + b] = acc;
+      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + b], acc);
     }
     // Y_b: W_kx, E_kx complete on this line; S/N (y-lines) accumulate
     for (int j = tid; j < ni; j += 512) {
@@ -1140,8 +1141,8 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
         zmac(w0, Vx[t], v);
         zmac(w1, Vx[q + t], v);
       }
-      base[(int64_t)(3 * q + kx) * nt + nb + j] = make_double2(-w0.x, -w0.y);
-      base[(int64_t)(q + kx) * nt + nb + j] = make_double2(-w1.x, -w1.y);
+      __stcs(&base[(int64_t)(3 * q + kx) * nt + nb + j], make_double2(-w0.x, -w0.y));
+      __stcs(&base[(int64_t)(q + kx) * nt + nb + j], make_double2(-w1.x, -w1.y));
     }
     for (int e = tid; e < q * ni; e += 512) {  // node (ix = kk, iy = kx) is position kx of y-line kk
       const int kk = e / ni, j = e - kk * ni;
@@ -1178,8 +1179,8 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
   for (int e = tid; e < q * ni; e += 512) {
     const int kk = e / ni, j = e - kk * ni;
     const zt a0 = accY[kk * ni + j], a1 = accY[(q + kk) * ni + j];
-    base[(int64_t)kk * nt + nb + j] = make_double2(-a0.x, -a0.y);
-    base[(int64_t)(2 * q + kk) * nt + nb + j] = make_double2(-a1.x, -a1.y);
+    __stcs(&base[(int64_t)kk * nt + nb + j], make_double2(-a0.x, -a0.y));
+    __stcs(&base[(int64_t)(2 * q + kk) * nt + nb + j], make_double2(-a1.x, -a1.y));
   }
   for (int e = tid; e < q * nb; e += 512) {
     const int kk = e / nb, b2 = e - kk * nb, e2 = b2 / q, k2 = b2 - e2 * q;
@@ -1470,7 +1471,7 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
     wattr = true;
   }
   const double ni = n;
-  ProfScope ps(K_GJ_FUSED, 8.0 * ni * ni * ni * batch + 8.0 * batch * q * (2.0 * ni * nb + (double)nb * nb),
+  ProfScope ps(K_LEAF_GJ, 8.0 * ni * ni * ni * batch + 8.0 * batch * q * (2.0 * ni * nb + (double)nb * nb),
                16.0 * batch * (ni * ni + (double)nt * nt + nb * nb), st);
   const zt m2ieta = make_double2(2.0 * eta.y, -2.0 * eta.x);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
