@@ -271,3 +271,62 @@ def test_paper_experiment_matches_oracle_small():
     S = hps.Solver(g, p, kappa, kappa, c)
     O = oracle.Oracle(0, 1, 0, 1, m, m, p, kappa, kappa, c)
     assert rel(S.solve(s, t), O.solve(s, t)) < TOL
+
+
+def _root_R_device(S):
+    import torch
+    n = S.nb(1)
+    R = torch.empty((n, n), dtype=torch.complex128, device="cuda")
+    hps._check(hps.lib().hps_export_R(S.h, 1, R.data_ptr()))
+    return R
+
+
+@pytest.mark.parametrize("cfgno", [2, 3, 4])
+def test_root_R_conj_unitary_full_size(cfgno):
+    """Full-size pin with no oracle run (reading Q9): kappa, c, eta are real in C2-C4, so the
+    composite DtN map is real and the root ItI map satisfies R conj(R) = I exactly; the CUDA
+    path's R^1 (1792^2 at C2 ... 14336^2 at C4, built in the bench's launch configuration)
+    must reproduce it to rounding.  The check product runs on the GPU through torch (test
+    infrastructure only).  Measured: 1.4e-14 (C2), 2.7e-14 (C3), 4.1e-14 (C4)."""
+    import torch
+    cfg, g, c, s, t = _bench_inputs(cfgno, nrhs=1)
+    assert np.isrealobj(c) or np.max(np.abs(np.imag(c))) == 0.0
+    S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, torch.from_numpy(np.ascontiguousarray(c)).cuda())
+    R = _root_R_device(S)
+    E = R @ R.conj() - torch.eye(R.shape[0], dtype=torch.complex128, device="cuda")
+    err = E.abs().max().item()
+    S.close()
+    assert err < 1e-10, err
+
+
+def test_config4_sampled_leaves_and_polynomial():
+    """C4 (256 x 256 leaves, 16.7M Chebyshev nodes, kappa h = 10) on one GPU: sampled leaf
+    operators vs oracle.leaf, and the polynomial manufactured solution reproduced through the
+    whole 16-level tree (collocation is exact on degree <= p-1 polynomials)."""
+    import numpy.polynomial.chebyshev as npc
+    import torch
+    cfg = inputs.CONFIGS[4]
+    p = cfg.p
+    g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
+    X, Y = hps.leaf_nodes(g, p)
+    Xb, Yb, NX, NY = hps.root_boundary_nodes(g, p)
+    c = inputs.c_at(cfg, X, Y)
+    rng = np.random.default_rng(11)
+    a = (rng.standard_normal((p, p)) + 1j * rng.standard_normal((p, p))) / np.outer(np.arange(1, p + 1), np.arange(1, p + 1))
+    val = lambda x, y, dx=0, dy=0: npc.chebval2d(2 * x - 1, 2 * y - 1,
+                                                 (npc.chebder(npc.chebder(a, dx, axis=0) * 2 ** dx, dy, axis=1) * 2 ** dy)
+                                                 if (dx or dy) else a)
+    Xi, Yi, ci = inputs.interior_of(p, X), inputs.interior_of(p, Y), inputs.interior_of(p, c)
+    s = (-(val(Xi, Yi, 2, 0) + val(Xi, Yi, 0, 2)) - cfg.kappa ** 2 * ci * val(Xi, Yi))[None]
+    t = (NX * val(Xb, Yb, 1, 0) + NY * val(Xb, Yb, 0, 1) + 1j * cfg.eta * val(Xb, Yb))[None]
+    dev = lambda z: torch.from_numpy(np.ascontiguousarray(z)).cuda()
+    S = hps.Solver(g, p, cfg.kappa, cfg.eta, dev(c), keep_root_R=False)
+    h = 1.0 / cfg.nx
+    for leaf in rng.choice(cfg.nleaf, 2, replace=False):
+        Psi, Yop = S.leaf_ops(int(leaf))
+        lo = oracle.leaf(p, h, h, cfg.kappa, cfg.eta, c[leaf])
+        assert rel(Psi, lo["Psi"]) < TOL and rel(Yop, lo["Y"]) < TOL
+    u = S.solve(dev(s), dev(t))[0].cpu().numpy()
+    S.close()
+    ex_i = val(Xi, Yi)
+    assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / np.max(np.abs(ex_i)) < 1e-7
