@@ -1229,8 +1229,11 @@ __device__ __forceinline__ void p47_sync(bool clustered) {
   }
 }
 
+// CG = 7-column groups per row: 4 -> 28-column panels, 256 rows per CTA; 2 -> 14-column panels,
+// 512 rows per CTA (a single CTA up to n = 512).
+template <int CG>
 __global__ void __launch_bounds__(256, 1) zgj_panel47_kernel(const PanelArgs a) {
-  constexpr int NB = WS_NB;
+  constexpr int NB = 7 * CG, RPW = 128 / CG, RPC = 8 * RPW;
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
   const bool clustered = CS > 1;
@@ -1239,13 +1242,13 @@ __global__ void __launch_bounds__(256, 1) zgj_panel47_kernel(const PanelArgs a) 
   __shared__ zt wrow[2][8][NB];
   __shared__ __align__(16) unsigned wkey[2][8];
   __shared__ zt prw[8][NB];
-  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg_ = lane & 3, rg = lane >> 2;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg_ = lane % CG, rg = lane / CG;
   const zt* Xb = a.X + (int64_t)b * a.bsx;
   zt* Yb = a.Y + (int64_t)b * a.bsy;
   int* piv = a.piv + (int64_t)b * n;
   int rq[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) rq[q] = c * 256 + wp * 32 + q * 8 + rg;
+  for (int q = 0; q < 4; ++q) rq[q] = c * RPC + wp * RPW + q * (32 / CG) + rg;
   // rows pivoted in earlier panels (pflag) are never candidates again
   int* pflag = a.pflag + (int64_t)b * n;
   bool pv[4], pthis[4];
@@ -1262,11 +1265,11 @@ __global__ void __launch_bounds__(256, 1) zgj_panel47_kernel(const PanelArgs a) 
       const int j = cg_ * 7 + cc;
       av[q][cc] = (rq[q] < n && j < w) ? __ldcg(Xb + (int64_t)rq[q] * a.ldx + k0 + j) : make_double2(0.0, 0.0);
     }
-  const bool warp_live = c * 256 + wp * 32 < n;
+  const bool warp_live = c * RPC + wp * RPW < n;
   bool singular = false;
   for (int cga = 0; cga * 7 < w; ++cga) {
     const bool act = cg_ == cga;
-    const int src = (lane & ~3) | cga;
+    const int src = (lane - cg_) + cga;
 #pragma unroll
     for (int s = 0; s < 7; ++s) {
       const int kk = cga * 7 + s;
@@ -1280,9 +1283,9 @@ __global__ void __launch_bounds__(256, 1) zgj_panel47_kernel(const PanelArgs a) 
         }
         const unsigned wk = __reduce_max_sync(0xffffffffu, key);
         if (wk != 0u) {  // this warp's candidate row: its 4 lanes publish it raw
-          const int lr = 4095 - (int)(wk & 4095u) - c * 256 - wp * 32;  // local row in the warp
-          if (rg == (lr & 7)) {
-            const int qq = lr >> 3;
+          const int lr = 4095 - (int)(wk & 4095u) - c * RPC - wp * RPW;  // local row in the warp
+          if (rg == lr % (32 / CG)) {
+            const int qq = lr / (32 / CG);
 #pragma unroll
             for (int q = 0; q < 4; ++q)
               if (q == qq) {
@@ -1302,7 +1305,7 @@ __global__ void __launch_bounds__(256, 1) zgj_panel47_kernel(const PanelArgs a) 
         best = __reduce_max_sync(0xffffffffu, best);
         if ((best & ~4095u) == 0u) singular = true;
         const int r = 4095 - (int)(best & 4095u);
-        const int rc = r >> 8, rw = (r & 255) >> 5;
+        const int rc = r / RPC, rw = (r % RPC) / RPW;
         if (lane < NB) {
           const zt* sp = clustered ? cluster.map_shared_rank(&wrow[par][rw][0], rc) : &wrow[par][rw][0];
           prw[wp][lane] = sp[lane];
@@ -1495,8 +1498,11 @@ void launch_cluster(const void* kern, int grid, int cs, size_t smem, cudaStream_
 // (cluster of ceil(n / 256) CTAs) and one DMMA GEMM for the other columns; X/Y ping-pong.
 void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch, void* ws,
                     int* info, cudaStream_t st) {
-  const int npan = (n + WS_NB - 1) / WS_NB, base = n / npan, rem = n % npan;
-  const int CS = (n + 255) / 256;
+  // 28-column panels on ceil(n / 256) CTAs.  (14-column panels in one CTA for 256 < n <= 512,
+  // CG = 2, measured slower: the step cost is the same and there are twice as many panels.)
+  const int CG = 4, NBW = 7 * CG;
+  const int npan = (n + NBW - 1) / NBW, base = n / npan, rem = n % npan;
+  const int CS = (n + 1024 / CG - 1) / (1024 / CG);
   char* wsp = static_cast<char*>(ws);
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   zt* B2 = reinterpret_cast<zt*>(wsp);
@@ -1506,7 +1512,7 @@ void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_
   int* pflag = cinmap + (size_t)batch * n;
   static bool attr = false;
   if (!attr) {
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_panel47_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_panel47_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     attr = true;
   }
   HPS_CUDA_CHECK(cudaMemsetAsync(pflag, 0, sizeof(int) * (size_t)batch * n, st));
@@ -1520,7 +1526,10 @@ void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)w * w * batch, 32.0 * n * (double)w * batch, st);
       if (CS == 1) {
-        zgj_panel47_kernel<<<batch, 256, 0, st>>>(pa);
+        if (CG == 2)
+          zgj_panel47_kernel<2><<<batch, 256, 0, st>>>(pa);
+        else
+          zgj_panel47_kernel<4><<<batch, 256, 0, st>>>(pa);
         HPS_CUDA_CHECK(cudaGetLastError());
       } else {
         cudaLaunchConfig_t cfg = {};
@@ -1534,7 +1543,7 @@ void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel47_kernel, pa));
+        HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel47_kernel<4>, pa));
       }
       count_launch();
     }

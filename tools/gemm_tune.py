@@ -13,6 +13,8 @@ shapes = [  # (M, N, K, batch, has_cin) — from the C2/C3 traces
     (252, 1, 196, 1024, 0), (448, 1, 1792, 1, 1),
 ]
 cfgs = list(range(9))
+if len(sys.argv) > 1:
+    shapes = [tuple(int(v) for v in a.split('x')) for a in sys.argv[1:]]
 torch.manual_seed(0)
 for (M, N, K, batch, cin) in shapes:
     A = torch.randn(batch, M, K, dtype=torch.complex128, device="cuda")
