@@ -804,7 +804,7 @@ __host__ __device__ inline size_t ws_smem(int n) {
 __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
                                                         zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
                                                         int* __restrict__ info, const WsFinish fin) {
-  constexpr int NB = WS_NB;
+  constexpr int NB = WS_NB, CPT = WS_NB / 4;  // panel columns, columns per panel thread
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mtr = (n + 15) & ~15, zs = ws_zs(n);
   zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [mtr][NB]  T of the current panel (16-row pairs)
@@ -844,20 +844,20 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
       const int k0 = P.k0(p), w = P.w(p);
       if (p > 0) bar_sync_n(BAR_READY, 512);  // columns of p updated by pass p-1
       WS_MARK(p, 0);
-      zt a[4][7];
+      zt a[4][CPT];
 #pragma unroll
       for (int q = 0; q < 4; ++q)
 #pragma unroll
-        for (int c = 0; c < 7; ++c) {
-          const int j = cg * 7 + c;
+        for (int c = 0; c < CPT; ++c) {
+          const int j = cg * CPT + c;
           a[q][c] = (rq[q] < n && j < w) ? __ldcg(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
         }
-      for (int cga = 0; cga * 7 < w; ++cga) {
+      for (int cga = 0; cga * CPT < w; ++cga) {
         const bool act = cg == cga;
         const int src = (lane & ~3) | cga;
 #pragma unroll
-        for (int s = 0; s < 7; ++s) {
-          const int kk = cga * 7 + s;
+        for (int s = 0; s < CPT; ++s) {
+          const int kk = cga * CPT + s;
           if (kk < w) {
             const int k = k0 + kk, par = k & 1;
             unsigned key = 0u;
@@ -881,7 +881,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
               for (int q = 0; q < 4; ++q)
                 if (q == qq) {
 #pragma unroll
-                  for (int c = 0; c < 7; ++c) prow4[par][cg * 7 + c] = a[q][c];
+                  for (int c = 0; c < CPT; ++c) prow4[par][cg * CPT + c] = a[q][c];
                 }
               if (cg == 0) {
                 pstep[r] = k;
@@ -906,12 +906,12 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
                     piv[q] = true;
                     g[q] = make_double2(-inv.x, -inv.y);
 #pragma unroll
-                    for (int c = 0; c < 7; ++c) a[q][c] = make_double2(0.0, 0.0);
+                    for (int c = 0; c < CPT; ++c) a[q][c] = make_double2(0.0, 0.0);
                   }
               }
 #pragma unroll
-              for (int c = 0; c < 7; ++c) {
-                const zt pc = prow4[par][cg * 7 + c];
+              for (int c = 0; c < CPT; ++c) {
+                const zt pc = prow4[par][cg * CPT + c];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   a[q][c].x = fma(-g[q].x, pc.x, a[q][c].x);
@@ -935,8 +935,8 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
       for (int q = 0; q < 4; ++q)
         if (rq[q] < mtr) {
 #pragma unroll
-          for (int c = 0; c < 7; ++c) {
-            const int j = cg * 7 + c;
+          for (int c = 0; c < CPT; ++c) {
+            const int j = cg * CPT + c;
             Ts[rq[q] * NB + j] = j < w ? a[q][c] : make_double2(0.0, 0.0);
             if (j < w && rq[q] < n) M[(int64_t)rq[q] * lda + k0 + j] = a[q][c];
           }
