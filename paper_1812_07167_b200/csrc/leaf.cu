@@ -102,6 +102,60 @@ __global__ void rhs_out_kernel(const zt* __restrict__ src, zt* __restrict__ dst,
   }
 }
 
+// Tiled versions for nrhs >= 8: each 256-thread block moves 32 x 32 (node, rhs) tiles through
+// shared memory so both the node-contiguous ABI side and the rhs-contiguous internal side are
+// read and written in 512-byte rows (the element-wise kernels above read one of the two sides
+// with a stride of nrhs or of a whole RHS slice).
+__global__ void __launch_bounds__(256) rhs_in_tiled_kernel(const zt* __restrict__ src, zt* __restrict__ dst,
+                                                           const int* __restrict__ map, int nbox, int n, int nrhs,
+                                                           int64_t sr, int64_t sb) {
+  __shared__ zt tile[32][33];
+  const int ti = (n + 31) / 32, tr = (nrhs + 31) / 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int64_t blk = blockIdx.x; blk < (int64_t)nbox * ti * tr; blk += gridDim.x) {
+    const int l = (int)(blk / (ti * tr)), rem = (int)(blk % (ti * tr)), i0 = (rem / tr) * 32, r0 = (rem % tr) * 32;
+    const zt* sp = src + (int64_t)map[l] * sb;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // read: i contiguous
+      const int r = r0 + ty + 8 * k, i = i0 + tx;
+      if (r < nrhs && i < n) tile[ty + 8 * k][tx] = sp[(int64_t)r * sr + i];
+    }
+    __syncthreads();
+    zt* dp = dst + (int64_t)l * n * nrhs;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // write: r contiguous
+      const int i = i0 + ty + 8 * k, r = r0 + tx;
+      if (r < nrhs && i < n) dp[(int64_t)i * nrhs + r] = tile[tx][ty + 8 * k];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) rhs_out_tiled_kernel(const zt* __restrict__ src, zt* __restrict__ dst,
+                                                            const int* __restrict__ map, int nbox, int n, int nrhs,
+                                                            int64_t sr, int64_t sb) {
+  __shared__ zt tile[32][33];
+  const int ti = (n + 31) / 32, tr = (nrhs + 31) / 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int64_t blk = blockIdx.x; blk < (int64_t)nbox * ti * tr; blk += gridDim.x) {
+    const int ln = (int)(blk / (ti * tr)), rem = (int)(blk % (ti * tr)), i0 = (rem / tr) * 32, r0 = (rem % tr) * 32;
+    const zt* sp = src + (int64_t)map[ln] * n * nrhs;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // read: r contiguous
+      const int i = i0 + ty + 8 * k, r = r0 + tx;
+      if (r < nrhs && i < n) tile[ty + 8 * k][tx] = sp[(int64_t)i * nrhs + r];
+    }
+    __syncthreads();
+    zt* dp = dst + (int64_t)ln * sb;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {  // write: i contiguous
+      const int r = r0 + ty + 8 * k, i = i0 + tx;
+      if (r < nrhs && i < n) dp[(int64_t)r * sr + i] = tile[tx][ty + 8 * k];
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Schur-complement leaf: the boundary block F_b of B couples
 // each boundary node only with the opposite node of the same grid line (S_ix <-> N_ix,
@@ -275,7 +329,11 @@ void launch_leaf_R(const zt* store, int64_t sstride, zt* R, int nleaf, int nt, i
 void launch_rhs_in(const zt* src, zt* dst, const int* map, int nbox, int n, int nrhs, int64_t sr, int64_t sb,
                    cudaStream_t st) {
   ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nbox * n * nrhs, st);
-  rhs_in_kernel<<<grid_for((int64_t)nbox * n * nrhs), 256, 0, st>>>(src, dst, map, nbox, n, nrhs, sr, sb);
+  if (nrhs >= 8)
+    rhs_in_tiled_kernel<<<grid_for((int64_t)nbox * ((n + 31) / 32) * ((nrhs + 31) / 32) * 256), 256, 0, st>>>(
+        src, dst, map, nbox, n, nrhs, sr, sb);
+  else
+    rhs_in_kernel<<<grid_for((int64_t)nbox * n * nrhs), 256, 0, st>>>(src, dst, map, nbox, n, nrhs, sr, sb);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
@@ -283,7 +341,11 @@ void launch_rhs_in(const zt* src, zt* dst, const int* map, int nbox, int n, int 
 void launch_rhs_out(const zt* src, zt* dst, const int* map, int nbox, int n, int nrhs, int64_t sr, int64_t sb,
                     cudaStream_t st) {
   ProfScope ps(K_LAYOUT, 0.0, 32.0 * (double)nbox * n * nrhs, st);
-  rhs_out_kernel<<<grid_for((int64_t)nbox * n * nrhs), 256, 0, st>>>(src, dst, map, nbox, n, nrhs, sr, sb);
+  if (nrhs >= 8)
+    rhs_out_tiled_kernel<<<grid_for((int64_t)nbox * ((n + 31) / 32) * ((nrhs + 31) / 32) * 256), 256, 0, st>>>(
+        src, dst, map, nbox, n, nrhs, sr, sb);
+  else
+    rhs_out_kernel<<<grid_for((int64_t)nbox * n * nrhs), 256, 0, st>>>(src, dst, map, nbox, n, nrhs, sr, sb);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

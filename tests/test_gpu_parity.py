@@ -330,3 +330,14 @@ def test_config4_sampled_leaves_and_polynomial():
     S.close()
     ex_i = val(Xi, Yi)
     assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / np.max(np.abs(ex_i)) < 1e-7
+
+
+@pytest.mark.parametrize("nx,ny,p,nrhs", [(4, 4, 8, 37), (8, 4, 10, 64), (2, 2, 16, 9)])
+def test_many_rhs(nx, ny, p, nrhs):
+    """Batches of right-hand sides through the tiled layout kernels (nrhs >= 8, ragged tiles)
+    and the GEMM sweeps: u for every RHS vs the oracle's Algorithm 2."""
+    kappa, eta = 11.0, 11.0
+    g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx, nrhs=nrhs, seed=5)
+    S = hps.Solver(g, p, kappa, eta, c)
+    O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c)
+    assert rel(S.solve(s, t), O.solve(s, t)) < TOL
