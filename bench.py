@@ -136,6 +136,11 @@ def run_hps(args, rank, world, dist):
     t_d = torch.from_numpy(np.ascontiguousarray(t)).to(dev)
     u_d = torch.empty((nrhs, cfg.nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128, device=dev)
     l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+    plan = None
+    if not args.no_plan:
+        # representative-action planner: measured once per machine/process,
+        # outside the timed region, like the paper's representative times
+        plan = {lab: hps.REGIMES[reg] for lab, n, nb, reg, tab in hps.plan_problem(g, cfg.p)}
 
     def step(profile=0):
         S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=True, device=local, profile=profile)
@@ -250,6 +255,7 @@ def run_hps(args, rank, world, dist):
         "phase_ms": {k: round(statistics.mean(r[k] for r in recs), 3)
                      for k in ["leaf_ms", "merge_ms", "up_ms", "down_ms"]},
         "kernel_classes_probe_step": per_class,
+        "plan": plan,
         "roofline": roof,
         "clocks": clocks,
         "wall_s_timed_region": round(wall, 3),
@@ -439,6 +445,7 @@ def main():
     ap.add_argument("--nrhs", type=int, default=0)
     ap.add_argument("--impl", default="hps", choices=["hps", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-plan", action="store_true", help="skip the representative-action planner (default rules)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

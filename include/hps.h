@@ -184,6 +184,27 @@ int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* out);
  * panel + GEMM, 3 = warp-specialised look-ahead, n <= 240) for kernel comparisons.  Exposed for kernel tests and tuning. */
 int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* out, int reps, double* ms);
 
+/* Representative-action planner.
+ * hps_rep_actions: host-only.  For the tree of grid g at order p, writes the size n and the box
+ * count of every level's representative action (Table 1): entry 0 the leaf
+ * interior x interior inverse (n_i, #leaves), entries 1..L the interface inverse W of the merge
+ * levels bottom-up (n3, 2^d).  Returns the number of entries (L + 1) or HPS_EINVAL (also when
+ * maxlev is too small).
+ * hps_plan_inverse: measures on the current device the representative time r of every regime
+ * of the batched inverse for `nbox` n x n matrices and records, for later builds in this
+ * process, the regime minimising eps = ceil(nbox / theta_o) * r.  Regimes (array index):
+ * 1 shared-memory matrix per CTA, 2 one CTA per matrix with explicit swaps, 3 warp-specialised
+ * look-ahead CTA per matrix, 4 blocked with implicit-pivoting panels + DMMA GEMM, 5 blocked with
+ * explicit-swap panels + DMMA GEMM.  eps, rep_ms (ms), theta_o: caller arrays of length 6;
+ * infeasible regimes get -1.  Returns the chosen regime (> 0) or a negative error code.
+ * hps_plan_set / hps_plan_clear: set (regime 0 = remove) / forget plan entries.
+ * hps_plan_regime: the regime the library will use for (n, nbox). */
+int hps_rep_actions(const hps_grid* g, int p, int maxlev, int* n_out, int* nbox_out);
+int hps_plan_inverse(int n, int nbox, double* eps, double* rep_ms, int* theta_o);
+int hps_plan_set(int n, int nbox, int regime);
+int hps_plan_clear(void);
+int hps_plan_regime(int n, int nbox);
+
 /* Debug: arm (on = 1) / disarm the clock64 timeline of CTA 0 of the warp-specialised
  * Gauss-Jordan kernel and copy the last one (160 values: [panel][10]) to host `out` (may be
  * NULL).  Used by tools/gj_tune.py only. */

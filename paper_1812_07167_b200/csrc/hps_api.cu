@@ -1413,6 +1413,63 @@ int hps_debug_ws_trace(int on, int64_t* out) {
   }
 }
 
+int hps_rep_actions(const hps_grid* g, int p, int maxlev, int* n_out, int* nbox_out) {
+  if (!g || p < 4 || g->nx < 1 || g->ny < 1 || !is_pow2(g->nx) || !is_pow2(g->ny) || !n_out || !nbox_out) {
+    hps_set_error("hps_rep_actions: invalid argument");
+    return HPS_EINVAL;
+  }
+  const int q = p - 2;
+  std::vector<std::pair<int, int>> ab{{g->nx, g->ny}};
+  while (!(ab.back().first == 1 && ab.back().second == 1)) {
+    auto [a, b] = ab.back();
+    if (a >= b) a /= 2;
+    else b /= 2;
+    ab.push_back({a, b});
+  }
+  const int L = (int)ab.size() - 1;
+  if (maxlev < L + 1) {
+    hps_set_error("hps_rep_actions: maxlev < number of levels");
+    return HPS_EINVAL;
+  }
+  n_out[0] = q * q;  // leaf: interior x interior inverse (Table 1)
+  nbox_out[0] = g->nx * g->ny;
+  for (int k = 1; k <= L; ++k) {  // merge levels bottom-up: depth d = L - k, interface inverse
+    const int d = L - k;
+    const bool vertical = ab[d].first >= ab[d].second;
+    n_out[k] = (vertical ? ab[d + 1].second : ab[d + 1].first) * q;
+    nbox_out[k] = 1 << d;
+  }
+  return L + 1;
+}
+
+int hps_plan_inverse(int n, int nbox, double* eps, double* rep_ms, int* theta_o) {
+  if (n <= 0 || nbox <= 0 || !eps || !rep_ms || !theta_o) {
+    hps_set_error("hps_plan_inverse: invalid argument");
+    return HPS_EINVAL;
+  }
+  try {
+    return zgj_plan_inverse(n, nbox, eps, rep_ms, theta_o);
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+}
+
+int hps_plan_set(int n, int nbox, int regime) {
+  if (n <= 0 || nbox <= 0 || regime < 0 || regime > 5) {
+    hps_set_error("hps_plan_set: invalid argument");
+    return HPS_EINVAL;
+  }
+  zgj_plan_set(n, nbox, regime);
+  return HPS_OK;
+}
+
+int hps_plan_clear(void) {
+  zgj_plan_clear();
+  return HPS_OK;
+}
+
+int hps_plan_regime(int n, int nbox) { return n > 0 && nbox > 0 ? zgj_regime_of(n, nbox) : HPS_EINVAL; }
+
 int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* outp, int reps, double* ms) {
   if (n <= 0 || batch <= 0 || !A || !outp || reps < 1 || mode < 0 || mode > 3) {
     hps_set_error("hps_zinv_timed: invalid argument");

@@ -94,6 +94,14 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
 bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
                            zt eta, int* info, cudaStream_t st);
 
+// Representative-action planner for the batched inverse (zgj.cu): regimes 1 small (shared
+// memory), 2 fused (one CTA per matrix, explicit swaps), 3 warp-specialised, 4 blocked with
+// implicit-pivoting panels, 5 blocked with explicit-swap panels.
+int zgj_plan_inverse(int n, int nbox, double* eps, double* rt, int* theta);
+void zgj_plan_set(int n, int nbox, int regime);
+void zgj_plan_clear();
+int zgj_regime_of(int n, int nbox);
+
 // Debug timeline of the warp-specialised Gauss-Jordan kernel (hps_debug_ws_trace).
 void zgj_ws_trace(int on, long long* out);
 

@@ -26,6 +26,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "hps_internal.cuh"
 
@@ -1478,6 +1480,59 @@ bool use_ws(int n, int batch) {
   return (gj_mode_env() == 0 && n >= 100 && n <= 200) || (gj_mode_env() == 3 && n > 32 && n <= WS_NMAX);
 }
 
+// ---------------------------------------------------------------------------
+// Regimes of the batched inverse and the representative-action planner (PAPER.md:881-953,
+// SURVEY 8(f) NEXT-3).  The paper picks, per tree level, theta_o boxes in parallel x theta_i
+// threads of parallel linear algebra per box minimising eps = ceil(N_boxes / theta_o) r^{theta_i}
+// with r the measured "representative time" of the level's representative action (the interior
+// inverse on the leaf level, the interface inverse W^{-1} on the others).  On the GPU the
+// choice is between kernel regimes: one CTA per box (theta_i = 1 SM, theta_o = boxes resident
+// per wave) or a blocked path whose panels and GEMM updates spread each box over the GPU
+// (theta_o = all boxes of the level in one batched launch).  hps_plan_inverse measures r for
+// every feasible regime on one wave and records the argmin of eps; without a plan entry the
+// measured default rules below apply.
+// ---------------------------------------------------------------------------
+enum Regime { REG_NONE = 0, REG_SMALL, REG_FUSED, REG_WS, REG_P47, REG_BLOCKED, REG_COUNT };
+std::mutex g_plan_mu;
+std::map<std::pair<int, int>, int> g_plan;  // (n, batch) -> regime
+thread_local int g_regime_force = REG_NONE;
+
+bool regime_feasible(int r, int n) {
+  switch (r) {
+    case REG_SMALL: return n <= kSmallMax;
+    case REG_FUSED: return n <= 256;
+    case REG_WS: return n > 32 && n <= WS_NMAX;
+    case REG_P47: return n <= 4096;
+    case REG_BLOCKED: return true;
+    default: return false;
+  }
+}
+
+int default_regime(int n, int batch) {
+  const int m = gj_mode_env();
+  if (m == 2) return n <= 32 ? REG_SMALL : REG_BLOCKED;
+  if (m == 3 && regime_feasible(REG_WS, n)) return REG_WS;
+  if (m == 1 && n > 32 && n <= 256) return REG_FUSED;
+  if (n <= 32) return REG_SMALL;
+  if (n >= 100 && n <= 200) return REG_WS;
+  if (use_fused(n, batch)) return REG_FUSED;
+  // implicit-pivoting 28-column panels: measured (tools/gj_tune.py) 1.5x faster than the explicit
+  // panels in one CTA (n <= 256) and 1.1-1.15x at clusters of 3-8 CTAs; at 2 and > 8 CTAs
+  // the explicit-swap panels are as fast or faster
+  if (n <= 256 || (n > 640 && n <= 2048)) return REG_P47;
+  return REG_BLOCKED;
+}
+
+int choose_regime(int n, int batch) {
+  if (g_regime_force != REG_NONE && regime_feasible(g_regime_force, n)) return g_regime_force;
+  if (gj_mode_env() == 0) {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    auto it = g_plan.find({n, batch});
+    if (it != g_plan.end()) return it->second;
+  }
+  return default_regime(n, batch);
+}
+
 void launch_cluster(const void* kern, int grid, int cs, size_t smem, cudaStream_t st, void** args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1593,7 +1648,8 @@ void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_
 void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch, void* ws,
                      int* info, cudaStream_t st) {
   if (n <= 0 || batch <= 0) return;
-  if (use_small(n, batch)) {
+  const int reg = choose_regime(n, batch);
+  if (reg == REG_SMALL) {
     const size_t smem = sizeof(zt) * ((size_t)n * (n + 1) + 2 * n) + sizeof(int) * n + 16;
     static bool attr = false;
     if (!attr) {
@@ -1612,7 +1668,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     }
     return;
   }
-  if (use_ws(n, batch)) {
+  if (reg == REG_WS) {
     ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
     static bool wattr = false;
     if (!wattr) {
@@ -1629,7 +1685,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     }
     return;
   }
-  if (gj_mode_env() != 2 && use_fused(n, batch)) {
+  if (reg == REG_FUSED) {
     ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
@@ -1654,10 +1710,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     }
     return;
   }
-  // implicit-pivoting 28-column panels: measured (tools/gj_tune.py) 1.5x faster than the explicit
-  // panels in one CTA (n <= 256) and 1.1-1.15x at clusters of 3-8 CTAs; at 2 and > 8 CTAs
-  // the explicit-swap panels are as fast or faster
-  if (gj_mode_env() != 2 && (n <= 256 || (n > 640 && n <= 2048))) {
+  if (reg == REG_P47) {
     zgj_invert_p47(A, lda, bs, out, ldo, obs, n, batch, ws, info, st);
     return;
   }
@@ -1760,7 +1813,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
 bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
                            zt eta, int* info, cudaStream_t st) {
   const int q = p - 2, n = q * q, nb = 4 * q, nt = nb + n;
-  if (!use_ws(n, batch) || ws_finish_smem(p) > ws_smem(n)) return false;
+  if (choose_regime(n, batch) != REG_WS || ws_finish_smem(p) > ws_smem(n)) return false;
   static bool wattr = false;
   if (!wattr) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1782,8 +1835,136 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
   return true;
 }
 
+// ---- representative-action planner (see the Regime comment) ----
+namespace {
+__global__ void plan_fill_kernel(zt* A, int n, int64_t total) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h = (uint64_t)e * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 29;
+    const double u = (double)(h >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    const double v = (double)((h * 0x94D049BB133111EBull) >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    const int64_t ij = e % ((int64_t)n * n);
+    const bool diag = ij / n == ij % n;
+    A[e] = make_double2(u + (diag ? 2.0 : 0.0), v);
+  }
+}
+
+int zgj_theta_o(int r, int n, int nbox, int nsm) {
+  switch (r) {
+    case REG_SMALL: {
+      int occ = 1;
+      const size_t smem = sizeof(zt) * ((size_t)n * (n + 1) + 2 * n) + sizeof(int) * n + 16;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, zgj_small_kernel, kThreads, smem);
+      return std::max(1, occ) * nsm;
+    }
+    case REG_FUSED: return nbox >= nsm ? 2 * nsm : nsm;
+    case REG_WS: return nsm;
+    default: return nbox;  // blocked regimes: every box of the level in one batched launch
+  }
+}
+
+}  // namespace
+
+// Measures the representative time of every feasible regime for `nbox` n x n inverses and
+// records the argmin of eps = ceil(nbox / theta_o) * r (one-CTA-per-box regimes: r = one wave
+// of theta_o boxes; blocked regimes: r measured on min(nbox, #SM) boxes, scaled linearly).
+// eps/r/theta (length REG_COUNT, index = regime) get -1 for infeasible regimes.
+int zgj_plan_inverse(int n, int nbox, double* eps, double* rt, int* theta) {
+  int dev, nsm;
+  HPS_CUDA_CHECK(cudaGetDevice(&dev));
+  HPS_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  cudaStream_t st;
+  HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const int mmax = std::min(nbox, 2 * nsm);
+  const size_t mat = (size_t)n * n, bytes = sizeof(zt) * mat * mmax;
+  size_t wsb = 16;
+  for (int r = REG_SMALL; r < REG_COUNT; ++r) {
+    g_regime_force = r;
+    if (regime_feasible(r, n)) wsb = std::max(wsb, zgj_workspace_bytes(n, mmax));
+  }
+  g_regime_force = REG_NONE;
+  void *src = nullptr, *a = nullptr, *o = nullptr, *ws = nullptr, *info = nullptr;
+  HPS_CUDA_CHECK(cudaMalloc(&src, bytes));
+  HPS_CUDA_CHECK(cudaMalloc(&a, bytes));
+  HPS_CUDA_CHECK(cudaMalloc(&o, bytes));
+  HPS_CUDA_CHECK(cudaMalloc(&ws, wsb));
+  HPS_CUDA_CHECK(cudaMalloc(&info, sizeof(int)));
+  plan_fill_kernel<<<148 * 8, 256, 0, st>>>((zt*)src, n, (int64_t)mat * mmax);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int best = REG_NONE;
+  double beste = 0;
+  for (int r = REG_SMALL; r < REG_COUNT; ++r) {
+    eps[r] = rt[r] = -1.0;
+    theta[r] = -1;
+    if (!regime_feasible(r, n)) continue;
+    const int th = zgj_theta_o(r, n, nbox, nsm);
+    const int m = std::min(nbox, std::min(th, nsm * 2 >= th ? th : mmax));
+    const int mm = std::min(m, mmax);
+    g_regime_force = r;
+    double tbest = 1e30;
+    for (int rep = 0; rep < 3; ++rep) {
+      HPS_CUDA_CHECK(cudaMemcpyAsync(a, src, sizeof(zt) * mat * mm, cudaMemcpyDeviceToDevice, st));
+      HPS_CUDA_CHECK(cudaMemsetAsync(info, 0, sizeof(int), st));
+      cudaEventRecord(e0, st);
+      zgj_invert_impl((zt*)a, n, (int64_t)mat, (zt*)o, n, (int64_t)mat, n, mm, ws, (int*)info, st);
+      cudaEventRecord(e1, st);
+      HPS_CUDA_CHECK(cudaEventSynchronize(e1));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep > 0) tbest = std::min(tbest, (double)ms);
+    }
+    g_regime_force = REG_NONE;
+    double e;
+    if (th >= nbox && (r == REG_P47 || r == REG_BLOCKED))
+      e = tbest * (double)nbox / mm;  // batched over the level: linear in the boxes
+    else
+      e = tbest * (double)((nbox + th - 1) / th) * ((double)std::min(th, nbox) / mm);
+    rt[r] = tbest;
+    theta[r] = th;
+    eps[r] = e;
+    if (best == REG_NONE || e < beste) {
+      best = r;
+      beste = e;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(src);
+  cudaFree(a);
+  cudaFree(o);
+  cudaFree(ws);
+  cudaFree(info);
+  cudaStreamDestroy(st);
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_plan[{n, nbox}] = best;
+  }
+  return best;
+}
+
+void zgj_plan_set(int n, int nbox, int regime) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  if (regime <= REG_NONE || regime >= REG_COUNT)
+    g_plan.erase({n, nbox});
+  else
+    g_plan[{n, nbox}] = regime;
+}
+
+void zgj_plan_clear() {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_plan.clear();
+}
+
+int zgj_regime_of(int n, int nbox) { return choose_regime(n, nbox); }
+
 size_t zgj_workspace_bytes(int n, int batch) {
-  if (use_small(n, batch) || use_ws(n, batch) || (gj_mode_env() != 2 && use_fused(n, batch))) return 16;
+  const int reg = choose_regime(n, batch);
+  if (reg == REG_SMALL || reg == REG_WS || reg == REG_FUSED) return 16;
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256;
 }

@@ -38,7 +38,7 @@ class hps_opts(C.Structure):
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
-           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
+           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free",
            "hps_last_error"]
 
@@ -77,6 +77,10 @@ def lib():
         L.hps_zinv_batched.argtypes = [i32, i32, dp, dp]
         L.hps_zinv_timed.argtypes = [i32, i32, i32, dp, dp, i32, C.POINTER(C.c_double)]
         L.hps_debug_ws_trace.argtypes = [i32, dp]
+        L.hps_rep_actions.argtypes = [C.POINTER(hps_grid), i32, i32, dp, dp]
+        L.hps_plan_inverse.argtypes = [i32, i32, dp, dp, dp]
+        L.hps_plan_set.argtypes = [i32, i32, i32]
+        L.hps_plan_regime.argtypes = [i32, i32]
         L.hps_zgemm_batched.argtypes = [i32, i32, i32, i32, i32, dp, dp, dp, dp, hps_c128, hps_c128, i32,
                                         C.POINTER(C.c_double)]
         L.hps_subtree_grid.argtypes = [C.POINTER(hps_grid), i32, i64, C.POINTER(hps_grid), C.POINTER(C.c_int32),
@@ -175,6 +179,50 @@ def zinv_batched(A):
     out = np.zeros_like(A)
     _check(lib().hps_zinv_batched(A.shape[-1], A.shape[0], A.ctypes.data, out.ctypes.data))
     return out
+
+
+REGIMES = {1: "smem", 2: "fused", 3: "warp-specialised", 4: "blocked-implicit", 5: "blocked-explicit"}
+
+
+def rep_actions(g, p):
+    """[(n, nbox)] of every level's representative action: the leaf inverse, then the merge
+    levels' interface inverses bottom-up (Table 1)."""
+    n = np.zeros(64, np.int32)
+    nb = np.zeros(64, np.int32)
+    k = lib().hps_rep_actions(C.byref(g), p, 64, n.ctypes.data, nb.ctypes.data)
+    if k < 0:
+        _check(k)
+    return [(int(n[i]), int(nb[i])) for i in range(k)]
+
+
+def plan_inverse(n, nbox):
+    """Measure the regimes for nbox n x n inverses and record the argmin of
+    eps = ceil(nbox / theta_o) r; returns (regime, {regime: (eps_ms, r_ms, theta_o)})."""
+    eps = np.zeros(6)
+    r = np.zeros(6)
+    th = np.zeros(6, np.int32)
+    reg = lib().hps_plan_inverse(n, nbox, eps.ctypes.data, r.ctypes.data, th.ctypes.data)
+    if reg < 0:
+        _check(reg)
+    return reg, {k: (float(eps[k]), float(r[k]), int(th[k])) for k in range(1, 6) if eps[k] >= 0}
+
+
+def plan_problem(g, p):
+    """Plan every level of a problem (the paper's per-level theta choice); returns table rows
+    (level label, n, nbox, chosen regime, {regime: (eps, r, theta_o)})."""
+    rows = []
+    for i, (n, nb) in enumerate(rep_actions(g, p)):
+        reg, tab = plan_inverse(n, nb)
+        rows.append(("leaf" if i == 0 else f"merge {i}", n, nb, reg, tab))
+    return rows
+
+
+def plan_clear():
+    lib().hps_plan_clear()
+
+
+def plan_regime(n, nbox):
+    return lib().hps_plan_regime(n, nbox)
 
 
 def zinv_timed(A, mode=0, reps=3):

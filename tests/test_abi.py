@@ -61,3 +61,18 @@ def test_argument_validation(L):
     assert not h.value
     assert b"q must equal" in L.hps_last_error()
     L.hps_free(None)   # no-op
+
+
+def test_rep_actions_match_survey_table():
+    """Representative actions per level (Table 1): the leaf interior inverse and the
+    merge interface inverses; sizes and box counts as SURVEY 8(a)'s per-level table (C3, C5)."""
+    from paper_1812_07167_b200 import hps
+    g = hps.grid(0.0, 1.0, 0.0, 1.0, 128, 128)
+    ra = hps.rep_actions(g, 16)
+    assert ra[0] == (196, 16384)
+    assert [n for n, _ in ra[1:]] == [14, 28, 28, 56, 56, 112, 112, 224, 224, 448, 448, 896, 896, 1792]
+    assert [b for _, b in ra[1:]] == [2 ** d for d in range(13, -1, -1)]
+    g5 = hps.grid(0.0, 2.0, 0.0, 1.0, 1024, 512)
+    ra5 = hps.rep_actions(g5, 16)
+    assert len(ra5) == 20 and ra5[0] == (196, 524288)
+    assert [n for n, _ in ra5[-5:]] == [1792, 3584, 3584, 7168, 7168]   # levels 15-19

@@ -341,3 +341,32 @@ def test_many_rhs(nx, ny, p, nrhs):
     S = hps.Solver(g, p, kappa, eta, c)
     O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c)
     assert rel(S.solve(s, t), O.solve(s, t)) < TOL
+
+
+def test_planned_regimes_parity():
+    """Representative-action planner (NEXT-3): plan every level of an 8 x 8-leaf, p = 12 tree
+    (leaf n_i = 100, interface n3 = 10 ... 80), build with the plan, and with every feasible
+    regime forced on the top interface inverse: R and u match the oracle in each case."""
+    nx, ny, p, kappa, eta = 8, 8, 12, 12.0, 12.0 - 1j
+    g, c, s, t = problem(nx, ny, p, kappa, eta)
+    O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
+    Ro, uo = O.R(1), O.solve(s, t)
+    try:
+        rows = hps.plan_problem(g, p)
+        assert len(rows) == 7
+        for _, n, nb, reg, tab in rows:
+            assert reg in tab and all(tab[reg][0] <= e for e, _, _ in tab.values())
+            assert hps.plan_regime(n, nb) == reg
+        S = hps.Solver(g, p, kappa, eta, c)
+        assert rel(S.R(1), Ro) < TOL and rel(S.solve(s, t), uo) < TOL
+        S.close()
+        n_top, nb_top = hps.rep_actions(g, p)[-1]
+        for reg in range(1, 6):
+            if reg == 1 and n_top > 112:
+                continue
+            hps._check(hps.lib().hps_plan_set(n_top, nb_top, reg))
+            S = hps.Solver(g, p, kappa, eta, c)
+            assert rel(S.R(1), Ro) < TOL, reg
+            S.close()
+    finally:
+        hps.plan_clear()
