@@ -1455,7 +1455,7 @@ int hps_plan_inverse(int n, int nbox, double* eps, double* rep_ms, int* theta_o)
 }
 
 int hps_plan_set(int n, int nbox, int regime) {
-  if (n <= 0 || nbox <= 0 || regime < 0 || regime > 5) {
+  if (n <= 0 || nbox <= 0 || regime < 0 || regime > 6) {
     hps_set_error("hps_plan_set: invalid argument");
     return HPS_EINVAL;
   }
@@ -1471,7 +1471,7 @@ int hps_plan_clear(void) {
 int hps_plan_regime(int n, int nbox) { return n > 0 && nbox > 0 ? zgj_regime_of(n, nbox) : HPS_EINVAL; }
 
 int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* outp, int reps, double* ms) {
-  if (n <= 0 || batch <= 0 || !A || !outp || reps < 1 || mode < 0 || mode > 3) {
+  if (n <= 0 || batch <= 0 || !A || !outp || reps < 1 || mode < 0 || mode > 6) {
     hps_set_error("hps_zinv_timed: invalid argument");
     return HPS_EINVAL;
   }
@@ -1490,7 +1490,8 @@ int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* outp
       a.alloc(bytes);
       o.alloc(bytes);
       extern int g_gj_mode_force;
-      g_gj_mode_force = mode;
+      g_gj_mode_force = mode <= 3 ? mode : 0;
+      zgj_force_regime(mode >= 4 ? mode : 0);
       ws.alloc(std::max<size_t>(zgj_workspace_bytes(n, batch), 16));
       info.alloc(sizeof(int));
       HPS_CUDA_CHECK(cudaMemcpyAsync(src.p, A, bytes, cudaMemcpyDefault, st));
@@ -1511,6 +1512,7 @@ int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* outp
         if (r > 0) tot += t;
       }
       g_gj_mode_force = 0;
+      zgj_force_regime(0);
       cudaEventDestroy(e0);
       cudaEventDestroy(e1);
       if (ms) *ms = tot / reps;

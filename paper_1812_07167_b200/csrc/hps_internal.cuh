@@ -101,6 +101,7 @@ int zgj_plan_inverse(int n, int nbox, double* eps, double* rt, int* theta);
 void zgj_plan_set(int n, int nbox, int regime);
 void zgj_plan_clear();
 int zgj_regime_of(int n, int nbox);
+void zgj_force_regime(int r);  // this thread; 0 = none
 
 // Debug timeline of the warp-specialised Gauss-Jordan kernel (hps_debug_ws_trace).
 void zgj_ws_trace(int on, long long* out);

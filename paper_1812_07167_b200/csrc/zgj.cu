@@ -1375,6 +1375,183 @@ __global__ void __launch_bounds__(256, 1) zgj_panel47_kernel(const PanelArgs a) 
   if (clustered) cluster.sync();  // no CTA leaves while a peer may still read its shared memory
 }
 
+// ---------------------------------------------------------------------------
+// Recursive panel (blocked path, n <= REC_NMAX, one CTA): the 28-column panel lives in shared
+// memory and is factored in sub-panels of 4 columns.  The pivot steps (the sequential,
+// latency-bound part) touch only the 4 sub-panel columns of every row (held in registers,
+// 2 rows per thread); after each sub-panel one rank-4 DMMA update applies its transform to the
+// other panel columns: C(i, J) = [i not a sub-panel pivot] C(i, J) + T4(i, :) Z4(:, J), the same
+// block Gauss-Jordan algebra as the trailing update of the whole matrix.  Per step: one
+// REDUX + one barrier for the pivot (every warp publishes its candidate's 4 values), 32 DFMA
+// per thread.  Interface and implicit pivoting as zgj_panel47_kernel.
+// ---------------------------------------------------------------------------
+constexpr int REC_NMAX = 496, REC_PS = 28;  // rows; shared row stride (== 4 mod 8: conflict-free)
+
+__host__ __device__ inline size_t rec_smem(int n) { return sizeof(zt) * ((size_t)n * REC_PS + 4 * 32); }
+
+__global__ void __launch_bounds__(256, 1) zgj_panel_rec_kernel(const PanelArgs a) {
+  constexpr int PS = REC_PS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zt* Ps = reinterpret_cast<zt*>(smem_raw);  // [n][PS] the panel
+  zt* Z4 = Ps + (size_t)a.n * PS;            // [4][32] old pivot rows of the sub-panel, other columns
+  __shared__ zt cand[2][8][4];
+  __shared__ __align__(16) unsigned wkey[2][8];
+  __shared__ int sub_piv[4];
+  __shared__ signed char subpv[REC_NMAX];  // sub-panel index in which a row was pivot (-1: none)
+  const int b = blockIdx.x, n = a.n, k0 = a.k0, w = a.w;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const zt* Xb = a.X + (int64_t)b * a.bsx;
+  zt* Yb = a.Y + (int64_t)b * a.bsy;
+  int* piv = a.piv + (int64_t)b * n;
+  int* pflag = a.pflag + (int64_t)b * n;
+  for (int i = wp; i < n; i += 8) {  // warp per row, lane per column: no integer division
+    if (lane < w) Ps[i * PS + lane] = __ldcg(Xb + (int64_t)i * a.ldx + k0 + lane);
+  }
+  for (int i = tid; i < n; i += 256) subpv[i] = -1;
+  const int r0 = tid, r1 = tid + 256;
+  bool pv0 = r0 < n ? pflag[r0] != 0 : true, pv1 = r1 < n ? pflag[r1] != 0 : true;
+  bool pt0 = false, pt1 = false;  // pivots of this panel
+  bool singular = false;
+  __syncthreads();
+  for (int c0 = 0; c0 < w; c0 += 4) {
+    const int ws = min(4, w - c0);
+    zt s0[4], s1[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      s0[c] = (r0 < n && c < ws) ? Ps[r0 * PS + c0 + c] : make_double2(0.0, 0.0);
+      s1[c] = (r1 < n && c < ws) ? Ps[r1 * PS + c0 + c] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      if (kk < ws) {
+        const int k = k0 + c0 + kk, par = k & 1;
+        const unsigned key0 = (!pv0) ? pivot_key12(s0[kk], r0) : 0u;
+        const unsigned key1 = (!pv1) ? pivot_key12(s1[kk], r1) : 0u;
+        const unsigned mk = max(key0, key1);
+        const unsigned wk = __reduce_max_sync(0xffffffffu, mk);
+        if (wk != 0u && mk == wk) {  // this lane holds the warp's candidate row
+          const bool second = key1 == wk;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) cand[par][wp][c] = second ? s1[c] : s0[c];
+        }
+        if (lane == 0) wkey[par][wp] = wk;
+        __syncthreads();
+        const uint4 ka = *reinterpret_cast<const uint4*>(&wkey[par][0]);
+        const uint4 kb = *reinterpret_cast<const uint4*>(&wkey[par][4]);
+        unsigned best = ka.x;
+        int bw = 0;
+        const unsigned kv[8] = {ka.x, ka.y, ka.z, ka.w, kb.x, kb.y, kb.z, kb.w};
+#pragma unroll
+        for (int q = 1; q < 8; ++q)
+          if (kv[q] > best) {
+            best = kv[q];
+            bw = q;
+          }
+        if ((best & ~4095u) == 0u) singular = true;
+        const int r = 4095 - (int)(best & 4095u);
+        zt pr[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) pr[c] = cand[par][bw][c];
+        const zt inv = zinv_fast(pr[kk]);
+        if (tid == 0) {
+          piv[k] = r;
+          sub_piv[kk] = r;
+          subpv[r] = (signed char)(c0 >> 2);
+        }
+        // rank-1 update of the sub-panel columns (pivot row: a <- pr / pivot exactly)
+        auto upd = [&](zt(&sv)[4], int row, bool& pvf, bool& ptf) {
+          zt g = zmul(sv[kk], inv);
+          if (row == r) {
+            pvf = true;
+            ptf = true;
+            g = make_double2(-inv.x, -inv.y);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) sv[c] = make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            sv[c].x = fma(-g.x, pr[c].x, sv[c].x);
+            sv[c].y = fma(-g.x, pr[c].y, sv[c].y);
+            sv[c].x = fma(g.y, pr[c].y, sv[c].x);
+            sv[c].y = fma(-g.y, pr[c].x, sv[c].y);
+          }
+          sv[kk] = make_double2(-g.x, -g.y);
+        };
+        if (r0 < n) upd(s0, r0, pv0, pt0);
+        if (r1 < n) upd(s1, r1, pv1, pt1);
+      }
+    }
+    // the sub-panel's 4 pivot rows, old values in the other panel columns -> Z4 (before anyone
+    // writes them back), then the sub-panel columns (T4) back into the panel
+    __syncthreads();
+    const int nother = w - ws;
+    for (int e = tid; e < 4 * 32; e += 256) {
+      const int m = e >> 5, j = e & 31;
+      zt v = make_double2(0.0, 0.0);
+      if (m < ws && j < nother) {
+        const int col = j < c0 ? j : j + ws;
+        v = Ps[sub_piv[m] * PS + col];
+      }
+      Z4[e] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < ws) {
+        if (r0 < n) Ps[r0 * PS + c0 + c] = s0[c];
+        if (r1 < n) Ps[r1 * PS + c0 + c] = s1[c];
+      }
+    __syncthreads();
+    // rank-4 DMMA update of the other panel columns: m-tiles of 8 rows x n-tiles of 8 columns
+    if (nother > 0) {
+      const int MT = (n + 7) >> 3, NTt = (nother + 7) >> 3;
+      const int sidx = c0 >> 2;
+      for (int mt = wp; mt < MT; mt += 8) {  // a warp keeps its m-tile (A fragment, pivot flag)
+        const int row = mt * 8 + (lane >> 2), rowc = min(row, n - 1);
+        const zt av = ((lane & 3) < ws) ? Ps[rowc * PS + c0 + (lane & 3)] : make_double2(0.0, 0.0);
+        const bool sp = subpv[rowc] == sidx;  // row is a pivot of this sub-panel: seed 0
+        for (int nt = 0; nt < NTt; ++nt) {
+        const zt bv = Z4[(lane & 3) * 32 + nt * 8 + (lane >> 2)];
+        double cr[2], ci[2];
+        int col[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int j = nt * 8 + (lane & 3) * 2 + h;
+          col[h] = j < nother ? (j < c0 ? j : j + ws) : -1;
+          const zt sv = (row < n && col[h] >= 0 && !sp) ? Ps[row * PS + col[h]] : make_double2(0.0, 0.0);
+          cr[h] = sv.x;
+          ci[h] = sv.y;
+        }
+        dmma884(cr[0], cr[1], av.x, bv.x);
+        dmma884(ci[0], ci[1], av.x, bv.y);
+        dmma884(cr[0], cr[1], -av.y, bv.y);
+        dmma884(ci[0], ci[1], av.y, bv.x);
+        if (row < n) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (col[h] >= 0) Ps[row * PS + col[h]] = make_double2(cr[h], ci[h]);
+        }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // T into Y, GEMM maps, pivot flags
+  for (int i = wp; i < n; i += 8)
+    if (lane < w) Yb[(int64_t)i * a.ldy + k0 + lane] = Ps[i * PS + lane];
+  if (r0 < n) {
+    a.cinmap[(int64_t)b * n + r0] = pt0 ? -1 : r0;
+    if (pt0) pflag[r0] = 1;
+  }
+  if (r1 < n) {
+    a.cinmap[(int64_t)b * n + r1] = pt1 ? -1 : r1;
+    if (pt1) pflag[r1] = 1;
+  }
+  __syncthreads();
+  if (tid < w) a.rowsrc[(int64_t)b * n + k0 + tid] = piv[k0 + tid];
+  if (singular && tid == 0) atomicCAS(a.info, 0, b + 1);
+}
+
 // A^{-1}(k, j) = M(piv[k], pinv[j]): one CTA per matrix
 __global__ void zgj_implicit_out_kernel(const zt* __restrict__ M, int64_t ldm, int64_t bsm, zt* __restrict__ out,
                                         int64_t ldo, int64_t obs, const int* __restrict__ piv_all, int n) {
@@ -1492,7 +1669,7 @@ bool use_ws(int n, int batch) {
 // every feasible regime on one wave and records the argmin of eps; without a plan entry the
 // measured default rules below apply.
 // ---------------------------------------------------------------------------
-enum Regime { REG_NONE = 0, REG_SMALL, REG_FUSED, REG_WS, REG_P47, REG_BLOCKED, REG_COUNT };
+enum Regime { REG_NONE = 0, REG_SMALL, REG_FUSED, REG_WS, REG_P47, REG_BLOCKED, REG_REC, REG_COUNT };
 std::mutex g_plan_mu;
 std::map<std::pair<int, int>, int> g_plan;  // (n, batch) -> regime
 thread_local int g_regime_force = REG_NONE;
@@ -1504,6 +1681,7 @@ bool regime_feasible(int r, int n) {
     case REG_WS: return n > 32 && n <= WS_NMAX;
     case REG_P47: return n <= 4096;
     case REG_BLOCKED: return true;
+    case REG_REC: return n > 32 && n <= REC_NMAX;
     default: return false;
   }
 }
@@ -1552,7 +1730,7 @@ void launch_cluster(const void* kern, int grid, int cs, size_t smem, cudaStream_
 // Blocked Gauss-Jordan with implicit pivoting: per 28-column panel one zgj_panel47_kernel launch
 // (cluster of ceil(n / 256) CTAs) and one DMMA GEMM for the other columns; X/Y ping-pong.
 void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch, void* ws,
-                    int* info, cudaStream_t st) {
+                    int* info, cudaStream_t st, bool rec = false) {
   // 28-column panels on ceil(n / 256) CTAs.  (14-column panels in one CTA for 256 < n <= 512,
   // CG = 2, measured slower: the step cost is the same and there are twice as many panels.)
   const int CG = 4, NBW = 7 * CG;
@@ -1568,6 +1746,8 @@ void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_
   static bool attr = false;
   if (!attr) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_panel47_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_panel_rec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)rec_smem(REC_NMAX)));
     attr = true;
   }
   HPS_CUDA_CHECK(cudaMemsetAsync(pflag, 0, sizeof(int) * (size_t)batch * n, st));
@@ -1580,7 +1760,10 @@ void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_
                  info, pflag};
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)w * w * batch, 32.0 * n * (double)w * batch, st);
-      if (CS == 1) {
+      if (rec) {
+        zgj_panel_rec_kernel<<<batch, 256, rec_smem(n), st>>>(pa);
+        HPS_CUDA_CHECK(cudaGetLastError());
+      } else if (CS == 1) {
         if (CG == 2)
           zgj_panel47_kernel<2><<<batch, 256, 0, st>>>(pa);
         else
@@ -1710,8 +1893,8 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     }
     return;
   }
-  if (reg == REG_P47) {
-    zgj_invert_p47(A, lda, bs, out, ldo, obs, n, batch, ws, info, st);
+  if (reg == REG_P47 || reg == REG_REC) {
+    zgj_invert_p47(A, lda, bs, out, ldo, obs, n, batch, ws, info, st, reg == REG_REC);
     return;
   }
   const PanelPlan pp = panel_plan(n);
@@ -1961,6 +2144,7 @@ void zgj_plan_clear() {
 }
 
 int zgj_regime_of(int n, int nbox) { return choose_regime(n, nbox); }
+void zgj_force_regime(int r) { g_regime_force = r; }
 
 size_t zgj_workspace_bytes(int n, int batch) {
   const int reg = choose_regime(n, batch);

@@ -15,7 +15,7 @@ for n, batch in shapes:
     A = torch.randn(batch, n, n, dtype=torch.complex128, device="cuda", generator=g)
     fl = 8.0 * n ** 3 * batch
     row = []
-    for mode in (0, 1, 2, 3):
+    for mode in (0, 1, 2, 3, 4, 6):
         try:
             X, ms = hps.zinv_timed(A, mode=mode, reps=3)
             idx = [0, batch // 2, batch - 1]
