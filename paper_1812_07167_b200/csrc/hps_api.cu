@@ -519,12 +519,13 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   for (int l0 = 0; l0 < nleaf; l0 += chunk) {
     const int nc = std::min(chunk, nleaf - l0);
     if (schur) {
+      if (H.leaf_fused && zgj_leaf_fused_applies(p, nc) &&
+          zgj_invert_leaf_schur(work.as<zt>(), (int64_t)wmat, H.store.as<zt>() + (size_t)l0 * mat, (int64_t)mat, p, nc,
+                                dK.as<zt>(), H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, H.eta, H.info.as<int>(), H.st,
+                                c_dev, H.leaf_nat.as<int>(), l0, H.kappa * H.kappa))
+        continue;  // assembly, inverse, [Psi | Y] and R in one kernel
       launch_leaf_schur_assemble(work.as<zt>(), (int64_t)wmat, l0, nc, H.leaf_nat.as<int>(), c_dev, p, dK.as<zt>(),
                                  H.kappa * H.kappa, H.st);
-      if (H.leaf_fused &&
-          zgj_invert_leaf_schur(work.as<zt>(), (int64_t)wmat, H.store.as<zt>() + (size_t)l0 * mat, (int64_t)mat, p, nc,
-                                dK.as<zt>(), H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, H.eta, H.info.as<int>(), H.st))
-        continue;
       fused_all = false;
       zgj_invert(work.as<zt>(), ninv, (int64_t)wmat, H.store.as<zt>() + (size_t)l0 * mat + (size_t)nb * nt + nb, nt,
                  (int64_t)mat, ninv, nc, ws.p, H.info.as<int>(), H.st, nullptr);

@@ -91,8 +91,12 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
 // the whole leaf operator [Psi | Y] (n_t x n_t, stride mstride) and the leaf R (nb x nb, batch
 // stride nb*nb) for `batch` leaves; S (n_i x n_i, stride sstride) is destroyed.  K =
 // schur_consts.  Returns false without launching when the kernel does not apply.
+// With c != nullptr the kernel also assembles S itself (c samples in natural leaf order, leaf_nat
+// the heap -> natural map, leaf0 the heap index of batch entry 0); S is then only workspace.
+bool zgj_leaf_fused_applies(int p, int batch);
 bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
-                           zt eta, int* info, cudaStream_t st);
+                           zt eta, int* info, cudaStream_t st, const zt* c = nullptr, const int* leaf_nat = nullptr,
+                           int leaf0 = 0, double kappa2 = 0.0);
 
 // Representative-action planner for the batched inverse (zgj.cu): regimes 1 small (shared
 // memory), 2 fused (one CTA per matrix, explicit swaps), 3 warp-specialised, 4 blocked with

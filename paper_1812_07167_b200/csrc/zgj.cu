@@ -792,6 +792,12 @@ struct WsFinish {
   zt* R;         // leaf R of batch entry 0 (nb x nb, batch stride nb*nb)
   zt m2ieta;     // -2 i eta
   int p;         // 0 = plain inverse output
+  // fused assembly of S = Lx (+) Ly - kappa^2 diag(c) (leaf_schur_assemble, DESIGN 3.1) into the
+  // CTA's work matrix before the elimination (c == nullptr: S is given)
+  const zt* c;           // c samples, natural leaf order, p*p per leaf
+  const int* leaf_nat;   // heap leaf -> natural leaf
+  int leaf0;             // heap index of batch entry 0
+  double kappa2;
 };
 
 __host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16, == 2 (mod 8)
@@ -822,6 +828,31 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
   P.rem = n % P.npan;
   if (tid < 256) pstep[tid] = 1 << 30;
   const bool trace = g_ws_trace_on && blockIdx.x == 0 && (tid == 0 || tid == 256);
+  if (fin.c) {  // assemble S in place (row iy*q + ix, Lx along x-lines, Ly along y-lines)
+    const int q = fin.p - 2;
+    const zt* Lx = fin.K;
+    const zt* Ly = fin.K + q * q;
+    const zt* cl = fin.c + (int64_t)fin.leaf_nat[fin.leaf0 + blockIdx.x] * fin.p * fin.p;
+    for (int r = tid >> 5; r < n; r += 16) {
+      const int ix = r % q, iy = r / q;
+      for (int cc = tid & 31; cc < n; cc += 32) {
+        const int jx = cc % q, jy = cc / q;
+        zt v = make_double2(0.0, 0.0);
+        if (iy == jy) v = Lx[ix * q + jx];
+        if (ix == jx) {
+          v.x += Ly[iy * q + jy].x;
+          v.y += Ly[iy * q + jy].y;
+        }
+        if (r == cc) {
+          const zt cv = cl[(iy + 1) * fin.p + ix + 1];
+          v.x -= fin.kappa2 * cv.x;
+          v.y -= fin.kappa2 * cv.y;
+        }
+        M[(int64_t)r * lda + cc] = v;
+      }
+    }
+    fence_cta();
+  }
   __syncthreads();
 
   // roles: panel warps 8-15 (latency-critical; the SMSP arbiter favours high warp ids),
@@ -1862,7 +1893,8 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
       zgj_ws_kernel<<<nbatch, 512, ws_smem(n), st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
-                                                      obs, n, info, WsFinish{nullptr, nullptr, {0.0, 0.0}, 0});
+                                                      obs, n, info,
+                                                      WsFinish{nullptr, nullptr, {0.0, 0.0}, 0, nullptr, nullptr, 0, 0.0});
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
     }
@@ -1993,10 +2025,16 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
 // Leaf inverse with the fused Schur epilogue (see WsFinish).  Returns false (nothing launched)
 // when the warp-specialised kernel does not apply to n = (p-2)^2; the caller then runs the
 // plain inverse and leaf_schur_finish.
+bool zgj_leaf_fused_applies(int p, int batch) {
+  const int n = (p - 2) * (p - 2);
+  return choose_regime(n, batch) == REG_WS && ws_finish_smem(p) <= ws_smem(n);
+}
+
 bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
-                           zt eta, int* info, cudaStream_t st) {
+                           zt eta, int* info, cudaStream_t st, const zt* c, const int* leaf_nat, int leaf0,
+                           double kappa2) {
   const int q = p - 2, n = q * q, nb = 4 * q, nt = nb + n;
-  if (choose_regime(n, batch) != REG_WS || ws_finish_smem(p) > ws_smem(n)) return false;
+  if (!zgj_leaf_fused_applies(p, batch)) return false;
   static bool wattr = false;
   if (!wattr) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2011,7 +2049,7 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
     const int nbatch = std::min(65535, batch - b0);
     zgj_ws_kernel<<<nbatch, 512, ws_smem(n), st>>>(
         S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
-        info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p});
+        info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2});
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
   }
