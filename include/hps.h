@@ -181,7 +181,7 @@ int hps_zinv_batched(int n, int batch, const hps_c128* A, hps_c128* out);
 /* As hps_zinv_batched, but runs the inversion `reps` times (each on a fresh device copy of A)
  * and returns the mean device time of the inversion alone (CUDA events) in *ms.  `mode`
  * selects the kernel family (0 = library choice, 1 = whole-matrix fused, 2 = blocked
- * panel + GEMM, 3 = warp-specialised look-ahead, n <= 240; 4-6 = planner regimes 4-6, see
+ * panel + GEMM, 3 = warp-specialised look-ahead, n <= 240; 4-7 = planner regimes 4-7, see
  * hps_plan_inverse) for kernel comparisons.  Exposed for kernel tests and tuning. */
 int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* out, int reps, double* ms);
 
@@ -197,7 +197,8 @@ int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* out,
  * 1 shared-memory matrix per CTA, 2 one CTA per matrix with explicit swaps, 3 warp-specialised
  * look-ahead CTA per matrix, 4 blocked with implicit-pivoting panels + DMMA GEMM, 5 blocked with
  * explicit-swap panels + DMMA GEMM, 6 blocked with recursive 4-column sub-panels in shared memory
- * (n <= 496).  eps, rep_ms (ms), theta_o: caller arrays of length 7;
+ * (n <= 496), 7 sequential-phase CTA per matrix (n <= 240).  eps, rep_ms (ms), theta_o: caller
+ * arrays of length 8;
  * infeasible regimes get -1.  Returns the chosen regime (> 0) or a negative error code.
  * hps_plan_set / hps_plan_clear: set (regime 0 = remove) / forget plan entries.
  * hps_plan_regime: the regime the library will use for (n, nbox). */

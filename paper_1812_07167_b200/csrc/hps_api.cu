@@ -1456,7 +1456,7 @@ int hps_plan_inverse(int n, int nbox, double* eps, double* rep_ms, int* theta_o)
 }
 
 int hps_plan_set(int n, int nbox, int regime) {
-  if (n <= 0 || nbox <= 0 || regime < 0 || regime > 6) {
+  if (n <= 0 || nbox <= 0 || regime < 0 || regime > 7) {
     hps_set_error("hps_plan_set: invalid argument");
     return HPS_EINVAL;
   }
@@ -1472,7 +1472,7 @@ int hps_plan_clear(void) {
 int hps_plan_regime(int n, int nbox) { return n > 0 && nbox > 0 ? zgj_regime_of(n, nbox) : HPS_EINVAL; }
 
 int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* outp, int reps, double* ms) {
-  if (n <= 0 || batch <= 0 || !A || !outp || reps < 1 || mode < 0 || mode > 6) {
+  if (n <= 0 || batch <= 0 || !A || !outp || reps < 1 || mode < 0 || mode > 7) {
     hps_set_error("hps_zinv_timed: invalid argument");
     return HPS_EINVAL;
   }

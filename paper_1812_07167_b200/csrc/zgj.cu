@@ -809,6 +809,135 @@ __host__ __device__ inline size_t ws_smem(int n) {
   return sizeof(zt) * ((size_t)((n + 15) & ~15) * WS_NB + (size_t)WS_NB * ws_zs(n));
 }
 
+// Output of the in-place Gauss-Jordan result M (pivot lists plist / pstep in shared memory):
+// the plain inverse (fin.p == 0) or the fused leaf epilogue.  All 512 threads of the CTA.
+__device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda, zt* __restrict__ out, int64_t ldo,
+                                          int64_t obs, int n, const WsFinish& fin, const int* plist,
+                                          const int* pstep, unsigned char* smem_raw) {
+  const int tid = threadIdx.x;
+  zt* ob = out + (int64_t)blockIdx.x * obs;
+  if (fin.p == 0) {
+    // A^{-1}(k, j) = M(plist[k], pstep[j])
+    for (int e = tid; e < n * n; e += 512) {
+      const int k = e / n, j = e - k * n;
+      __stcs(&ob[(int64_t)k * ldo + j], __ldcg(M + (int64_t)plist[k] * lda + pstep[j]));
+    }
+    return;
+  }
+  // ---- fused leaf epilogue (n = n_i = q^2, ldo = n_t); outputs are streamed past L2 (st.cs) so the
+  // in-place matrices of the other CTAs stay resident ----
+  const int q = fin.p - 2, ni = n, nb = 4 * q, nt = (int)ldo;
+  const zt* Ubx = fin.K + 2 * q * q;
+  const zt* Uby = Ubx + 2 * q;
+  const zt* Vx = Uby + 2 * q;
+  const zt* Vy = Vx + 2 * q;
+  const zt* Gx = Vy + 2 * q;
+  const zt* Gy = Gx + 4;
+  zt* base = ob - ((int64_t)nb * nt + nb);  // leaf operator [Psi | Y], rows [I_b; I_i]
+  zt* Rl = fin.R + (int64_t)blockIdx.x * nb * nb;
+  zt* C = reinterpret_cast<zt*>(smem_raw);  // [q][ni]   S^{-1} rows of x-line k
+  zt* Pc = C + q * ni;                       // [q][nb]   Psi_i rows of x-line k
+  zt* accY = Pc + q * nb;                    // [2q][ni]  y-line sums for Y_b (S rows, then N rows)
+  zt* accP = accY + 2 * q * ni;              // [2q][nb]  y-line sums for Psi_b
+  const zt m2 = fin.m2ieta;
+  auto zmac = [](zt& acc, zt a, zt b) {
+    acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+    acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+  };
+  auto put_psib = [&](int row, int b2, zt v) {  // Psi_b entry and the matching R entry
+    __stcs(&base[(int64_t)row * nt + b2], v);
+    zt r = make_double2(m2.x * v.x - m2.y * v.y, m2.x * v.y + m2.y * v.x);
+    if (row == b2) r.x += 1.0;
+    __stcs(&Rl[row * nb + b2], r);
+  };
+  for (int e = tid; e < 2 * q * ni; e += 512) accY[e] = make_double2(0.0, 0.0);
+  for (int e = tid; e < 2 * q * nb; e += 512) accP[e] = make_double2(0.0, 0.0);
+  for (int kx = 0; kx < q; ++kx) {  // x-line iy = kx: interior rows kx*q + t
+    __syncthreads();
+    for (int e = tid; e < q * ni; e += 512) {
+      const int t = e / ni, j = e - t * ni;
+      const zt v = __ldcg(M + (int64_t)plist[kx * q + t] * lda + pstep[j]);
+      C[e] = v;
+      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + nb + j], v);  // Y_i
+    }
+    __syncthreads();
+    // Psi_i rows of this line
+    for (int e = tid; e < q * nb; e += 512) {
+      const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
+      const zt* Cr = C + t * ni;
+      zt acc = make_double2(0.0, 0.0);
+      if (edge == 0 || edge == 2) {  // S / N: y-line ix = kk
+        const int side = edge == 0 ? 0 : 1;
+        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[t2 * q + kk], Uby[t2 * 2 + side]);
+      } else {  // E / W: x-line iy = kk
+        const int side = edge == 3 ? 0 : 1;
+        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[kk * q + t2], Ubx[t2 * 2 + side]);
+      }
+      Pc[e] = acc;
+      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + b], acc);
+    }
+    // Y_b: W_kx, E_kx complete on this line; S/N (y-lines) accumulate
+    for (int j = tid; j < ni; j += 512) {
+      zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+      for (int t = 0; t < q; ++t) {
+        const zt v = C[t * ni + j];
+        zmac(w0, Vx[t], v);
+        zmac(w1, Vx[q + t], v);
+      }
+      __stcs(&base[(int64_t)(3 * q + kx) * nt + nb + j], make_double2(-w0.x, -w0.y));
+      __stcs(&base[(int64_t)(q + kx) * nt + nb + j], make_double2(-w1.x, -w1.y));
+    }
+    for (int e = tid; e < q * ni; e += 512) {  // node (ix = kk, iy = kx) is position kx of y-line kk
+      const int kk = e / ni, j = e - kk * ni;
+      const zt v = C[kk * ni + j];
+      zmac(accY[kk * ni + j], Vy[kx], v);
+      zmac(accY[(q + kk) * ni + j], Vy[q + kx], v);
+    }
+    __syncthreads();  // Pc complete
+    for (int b2 = tid; b2 < nb; b2 += 512) {
+      zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+      for (int t = 0; t < q; ++t) {
+        const zt v = Pc[t * nb + b2];
+        zmac(w0, Vx[t], v);
+        zmac(w1, Vx[q + t], v);
+      }
+      const int e2 = b2 / q, k2 = b2 - e2 * q;
+      zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+      if (k2 == kx && (e2 == 1 || e2 == 3)) {
+        g0 = Gx[0 * 2 + (e2 == 3 ? 0 : 1)];
+        g1 = Gx[1 * 2 + (e2 == 3 ? 0 : 1)];
+      }
+      put_psib(3 * q + kx, b2, make_double2(g0.x - w0.x, g0.y - w0.y));
+      put_psib(q + kx, b2, make_double2(g1.x - w1.x, g1.y - w1.y));
+    }
+    for (int e = tid; e < q * nb; e += 512) {
+      const int kk = e / nb, b2 = e - kk * nb;
+      const zt v = Pc[kk * nb + b2];
+      zmac(accP[kk * nb + b2], Vy[kx], v);
+      zmac(accP[(q + kk) * nb + b2], Vy[q + kx], v);
+    }
+  }
+  __syncthreads();
+  // y-lines: S_kk (row kk) and N_kk (row 2q + kk)
+  for (int e = tid; e < q * ni; e += 512) {
+    const int kk = e / ni, j = e - kk * ni;
+    const zt a0 = accY[kk * ni + j], a1 = accY[(q + kk) * ni + j];
+    __stcs(&base[(int64_t)kk * nt + nb + j], make_double2(-a0.x, -a0.y));
+    __stcs(&base[(int64_t)(2 * q + kk) * nt + nb + j], make_double2(-a1.x, -a1.y));
+  }
+  for (int e = tid; e < q * nb; e += 512) {
+    const int kk = e / nb, b2 = e - kk * nb, e2 = b2 / q, k2 = b2 - e2 * q;
+    const zt a0 = accP[kk * nb + b2], a1 = accP[(q + kk) * nb + b2];
+    zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
+    if (k2 == kk && (e2 == 0 || e2 == 2)) {
+      g0 = Gy[0 * 2 + (e2 == 0 ? 0 : 1)];
+      g1 = Gy[1 * 2 + (e2 == 0 ? 0 : 1)];
+    }
+    put_psib(kk, b2, make_double2(g0.x - a0.x, g0.y - a0.y));
+    put_psib(2 * q + kk, b2, make_double2(g1.x - a1.x, g1.y - a1.y));
+  }
+}
+
 __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
                                                         zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
                                                         int* __restrict__ info, const WsFinish fin) {
@@ -1106,127 +1235,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
     }
   }
   __syncthreads();
-  zt* ob = out + (int64_t)blockIdx.x * obs;
-  if (fin.p == 0) {
-    // A^{-1}(k, j) = M(plist[k], pstep[j])
-    for (int e = tid; e < n * n; e += 512) {
-      const int k = e / n, j = e - k * n;
-      __stcs(&ob[(int64_t)k * ldo + j], __ldcg(M + (int64_t)plist[k] * lda + pstep[j]));
-    }
-    return;
-  }
-  // ---- fused leaf epilogue (n = n_i = q^2, ldo = n_t); outputs are streamed past L2 (st.cs) so the
-  // in-place matrices of the other CTAs stay resident ----
-  const int q = fin.p - 2, ni = n, nb = 4 * q, nt = (int)ldo;
-  const zt* Ubx = fin.K + 2 * q * q;
-  const zt* Uby = Ubx + 2 * q;
-  const zt* Vx = Uby + 2 * q;
-  const zt* Vy = Vx + 2 * q;
-  const zt* Gx = Vy + 2 * q;
-  const zt* Gy = Gx + 4;
-  zt* base = ob - ((int64_t)nb * nt + nb);  // leaf operator [Psi | Y], rows [I_b; I_i]
-  zt* Rl = fin.R + (int64_t)blockIdx.x * nb * nb;
-  zt* C = reinterpret_cast<zt*>(smem_raw);  // [q][ni]   S^{-1} rows of x-line k
-  zt* Pc = C + q * ni;                       // [q][nb]   Psi_i rows of x-line k
-  zt* accY = Pc + q * nb;                    // [2q][ni]  y-line sums for Y_b (S rows, then N rows)
-  zt* accP = accY + 2 * q * ni;              // [2q][nb]  y-line sums for Psi_b
-  const zt m2 = fin.m2ieta;
-  auto zmac = [](zt& acc, zt a, zt b) {
-    acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
-    acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
-  };
-  auto put_psib = [&](int row, int b2, zt v) {  // Psi_b entry and the matching R entry
-    __stcs(&base[(int64_t)row * nt + b2], v);
-    zt r = make_double2(m2.x * v.x - m2.y * v.y, m2.x * v.y + m2.y * v.x);
-    if (row == b2) r.x += 1.0;
-    __stcs(&Rl[row * nb + b2], r);
-  };
-  for (int e = tid; e < 2 * q * ni; e += 512) accY[e] = make_double2(0.0, 0.0);
-  for (int e = tid; e < 2 * q * nb; e += 512) accP[e] = make_double2(0.0, 0.0);
-  for (int kx = 0; kx < q; ++kx) {  // x-line iy = kx: interior rows kx*q + t
-    __syncthreads();
-    for (int e = tid; e < q * ni; e += 512) {
-      const int t = e / ni, j = e - t * ni;
-      const zt v = __ldcg(M + (int64_t)plist[kx * q + t] * lda + pstep[j]);
-      C[e] = v;
-      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + nb + j], v);  // Y_i
-    }
-    __syncthreads();
-    // Psi_i rows of this line
-    for (int e = tid; e < q * nb; e += 512) {
-      const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
-      const zt* Cr = C + t * ni;
-      zt acc = make_double2(0.0, 0.0);
-      if (edge == 0 || edge == 2) {  // S / N: y-line ix = kk
-        const int side = edge == 0 ? 0 : 1;
-        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[t2 * q + kk], Uby[t2 * 2 + side]);
-      } else {  // E / W: x-line iy = kk
-        const int side = edge == 3 ? 0 : 1;
-        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[kk * q + t2], Ubx[t2 * 2 + side]);
-      }
-      Pc[e] = acc;
-      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + b], acc);
-    }
-    // Y_b: W_kx, E_kx complete on this line; S/N (y-lines) accumulate
-    for (int j = tid; j < ni; j += 512) {
-      zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
-      for (int t = 0; t < q; ++t) {
-        const zt v = C[t * ni + j];
-        zmac(w0, Vx[t], v);
-        zmac(w1, Vx[q + t], v);
-      }
-      __stcs(&base[(int64_t)(3 * q + kx) * nt + nb + j], make_double2(-w0.x, -w0.y));
-      __stcs(&base[(int64_t)(q + kx) * nt + nb + j], make_double2(-w1.x, -w1.y));
-    }
-    for (int e = tid; e < q * ni; e += 512) {  // node (ix = kk, iy = kx) is position kx of y-line kk
-      const int kk = e / ni, j = e - kk * ni;
-      const zt v = C[kk * ni + j];
-      zmac(accY[kk * ni + j], Vy[kx], v);
-      zmac(accY[(q + kk) * ni + j], Vy[q + kx], v);
-    }
-    __syncthreads();  // Pc complete
-    for (int b2 = tid; b2 < nb; b2 += 512) {
-      zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
-      for (int t = 0; t < q; ++t) {
-        const zt v = Pc[t * nb + b2];
-        zmac(w0, Vx[t], v);
-        zmac(w1, Vx[q + t], v);
-      }
-      const int e2 = b2 / q, k2 = b2 - e2 * q;
-      zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
-      if (k2 == kx && (e2 == 1 || e2 == 3)) {
-        g0 = Gx[0 * 2 + (e2 == 3 ? 0 : 1)];
-        g1 = Gx[1 * 2 + (e2 == 3 ? 0 : 1)];
-      }
-      put_psib(3 * q + kx, b2, make_double2(g0.x - w0.x, g0.y - w0.y));
-      put_psib(q + kx, b2, make_double2(g1.x - w1.x, g1.y - w1.y));
-    }
-    for (int e = tid; e < q * nb; e += 512) {
-      const int kk = e / nb, b2 = e - kk * nb;
-      const zt v = Pc[kk * nb + b2];
-      zmac(accP[kk * nb + b2], Vy[kx], v);
-      zmac(accP[(q + kk) * nb + b2], Vy[q + kx], v);
-    }
-  }
-  __syncthreads();
-  // y-lines: S_kk (row kk) and N_kk (row 2q + kk)
-  for (int e = tid; e < q * ni; e += 512) {
-    const int kk = e / ni, j = e - kk * ni;
-    const zt a0 = accY[kk * ni + j], a1 = accY[(q + kk) * ni + j];
-    __stcs(&base[(int64_t)kk * nt + nb + j], make_double2(-a0.x, -a0.y));
-    __stcs(&base[(int64_t)(2 * q + kk) * nt + nb + j], make_double2(-a1.x, -a1.y));
-  }
-  for (int e = tid; e < q * nb; e += 512) {
-    const int kk = e / nb, b2 = e - kk * nb, e2 = b2 / q, k2 = b2 - e2 * q;
-    const zt a0 = accP[kk * nb + b2], a1 = accP[(q + kk) * nb + b2];
-    zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
-    if (k2 == kk && (e2 == 0 || e2 == 2)) {
-      g0 = Gy[0 * 2 + (e2 == 0 ? 0 : 1)];
-      g1 = Gy[1 * 2 + (e2 == 0 ? 0 : 1)];
-    }
-    put_psib(kk, b2, make_double2(g0.x - a0.x, g0.y - a0.y));
-    put_psib(2 * q + kk, b2, make_double2(g1.x - a1.x, g1.y - a1.y));
-  }
+  ws_output(M, lda, out, ldo, obs, n, fin, plist, pstep, smem_raw);
 }
 
 size_t ws_finish_smem(int p) {
@@ -1604,6 +1613,258 @@ __global__ void zgj_implicit_out_kernel(const zt* __restrict__ M, int64_t ldm, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Sequential-phase variant of the warp-specialised kernel (regime 7): all 16 warps factor the
+// panel (2 rows x 7 columns per thread), then all 16 warps apply its update.  Measured on B200
+// (tools/panel47_bench.cu): DMMA and DFMA share the FP64 issue resources, and warps issuing
+// DMMA back to back starve another warp's DFMA almost completely, so overlapping the pivot
+// steps with the tensor-core update (zgj_ws_kernel) stretches the pivot steps 2-4x; here the
+// pivot steps run alone and the update runs at 4 warps per sub-partition.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
+                                                         zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
+                                                         int* __restrict__ info, const WsFinish fin) {
+  constexpr int NB = WS_NB, CPT = WS_NB / 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int mtr = (n + 15) & ~15, zs = ws_zs(n);
+  zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [mtr][NB]
+  zt* Zs = Ts + (size_t)mtr * NB;            // [NB][zs]
+  __shared__ zt prow4[2][NB];
+  __shared__ __align__(16) unsigned wkey[2][16];
+  __shared__ int pstep[256], plist[256], colmap[WS_NMAX + 16];
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  zt* M = A + (int64_t)blockIdx.x * bs;
+  WsPanels P;
+  P.npan = (n + NB - 1) / NB;
+  P.base = n / P.npan;
+  P.rem = n % P.npan;
+  if (tid < 256) pstep[tid] = 1 << 30;
+  if (fin.c) {  // assemble S in place (as zgj_ws_kernel)
+    const int q = fin.p - 2;
+    const zt* Lx = fin.K;
+    const zt* Ly = fin.K + q * q;
+    const zt* cl = fin.c + (int64_t)fin.leaf_nat[fin.leaf0 + blockIdx.x] * fin.p * fin.p;
+    for (int r = tid >> 5; r < n; r += 16) {
+      const int ix = r % q, iy = r / q;
+      for (int cc = lane; cc < n; cc += 32) {
+        const int jx = cc % q, jy = cc / q;
+        zt v = make_double2(0.0, 0.0);
+        if (iy == jy) v = Lx[ix * q + jx];
+        if (ix == jx) {
+          v.x += Ly[iy * q + jy].x;
+          v.y += Ly[iy * q + jy].y;
+        }
+        if (r == cc) {
+          const zt cv = cl[(iy + 1) * fin.p + ix + 1];
+          v.x -= fin.kappa2 * cv.x;
+          v.y -= fin.kappa2 * cv.y;
+        }
+        M[(int64_t)r * lda + cc] = v;
+      }
+    }
+  }
+  __syncthreads();
+  int rq[2];
+  rq[0] = wp * 16 + rg;
+  rq[1] = wp * 16 + 8 + rg;
+  bool piv[2] = {false, false}, singular = false;
+  const bool warp_live = wp * 16 < n;
+  const int MT = mtr >> 3;
+  const bool trace = g_ws_trace_on && blockIdx.x == 0 && tid == 0;
+  for (int p = 0; p < P.npan; ++p) {
+    const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
+    WS_MARK(p, 0);
+    // ---------------- panel: w pivot steps on the n x w panel ----------------
+    zt a[2][CPT];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int j = cg * CPT + c;
+        a[q][c] = (rq[q] < n && j < w) ? __ldcg(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
+      }
+    for (int cga = 0; cga * CPT < w; ++cga) {
+      const bool act = cg == cga;
+      const int src = (lane & ~3) | cga;
+#pragma unroll
+      for (int s = 0; s < CPT; ++s) {
+        const int kk = cga * CPT + s;
+        if (kk < w) {
+          const int k = k0 + kk, par = k & 1;
+          unsigned key = 0u;
+          if (act) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              if (!piv[q] && rq[q] < n) key = max(key, pivot_key(a[q][s], rq[q], true));
+          }
+          key = __reduce_max_sync(0xffffffffu, key);
+          if (lane == 0) wkey[par][wp] = key;
+          __syncthreads();
+          unsigned best = 0u;
+#pragma unroll
+          for (int g4 = 0; g4 < 4; ++g4) {
+            const uint4 kq = *reinterpret_cast<const uint4*>(&wkey[par][4 * g4]);
+            best = max(best, max(max(kq.x, kq.y), max(kq.z, kq.w)));
+          }
+          if ((best & ~511u) == 0u) singular = true;
+          const int r = 511 - (int)(best & 511u);
+          if (wp == (r >> 4) && rg == (r & 7)) {  // the 4 lanes of row r publish it raw
+            const int qq = (r >> 3) & 1;
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+              if (q == qq) {
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) prow4[par][cg * CPT + c] = a[q][c];
+              }
+            if (cg == 0) {
+              pstep[r] = k;
+              plist[k] = r;
+            }
+          }
+          __syncthreads();
+          if (warp_live) {
+            const zt inv = zinv_fast(prow4[par][kk]);
+            zt g[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const zt v = a[q][s];
+              g[q] = zmul(make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)), inv);
+            }
+            if (wp == (r >> 4)) {
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+                if (rq[q] == r) {  // pivot row: a <- pr / pivot exactly (as 0 - (-inv) pr)
+                  piv[q] = true;
+                  g[q] = make_double2(-inv.x, -inv.y);
+#pragma unroll
+                  for (int c = 0; c < CPT; ++c) a[q][c] = make_double2(0.0, 0.0);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              const zt pc = prow4[par][cg * CPT + c];
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                a[q][c].x = fma(-g[q].x, pc.x, a[q][c].x);
+                a[q][c].y = fma(-g[q].x, pc.y, a[q][c].y);
+                a[q][c].x = fma(g[q].y, pc.y, a[q][c].x);
+                a[q][c].y = fma(-g[q].y, pc.x, a[q][c].y);
+              }
+            }
+            if (act) {
+#pragma unroll
+              for (int q = 0; q < 2; ++q) a[q][s] = make_double2(-g[q].x, -g[q].y);
+            }
+          }
+        }
+      }
+    }
+    WS_MARK(p, 1);
+    // T -> shared (A operand) and back in place
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      if (rq[q] < mtr) {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const int j = cg * CPT + c;
+          Ts[rq[q] * NB + j] = j < w ? a[q][c] : make_double2(0.0, 0.0);
+          if (j < w && rq[q] < n) M[(int64_t)rq[q] * lda + k0 + j] = a[q][c];
+        }
+      }
+    if (p + 1 == P.npan && nv == 0) break;
+    // ---------------- update: C(i, J) = [i not a pivot of p] C(i, J) + T(i,:) Z(:, J) -------------
+    for (int v = tid; v < nv + 16; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
+    __syncthreads();  // T, pivots, colmap visible
+    for (int e = tid; e < w4 * nv; e += 512) {
+      const int m = e / nv, v = e - m * nv;
+      const bool ok = m < w;
+      const int srow = ok ? plist[k0 + m] : 0;
+      cpa16_zfill(Zs + m * zs + v, M + (int64_t)srow * lda + colmap[v], ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    WS_MARK(p, 2);
+    const int NPR = (nv + 15) >> 4;
+    struct Unit {
+      int rr, col[2][2];
+      bool rok;
+      zt seed[2][2];
+    };
+    auto load_unit = [&](int mt, int npr, Unit& U) {
+      U.rr = mt * 8 + (lane >> 2);
+      const int rc = min(U.rr, n - 1);
+      U.rok = U.rr < n && (unsigned)(pstep[rc] - k0) >= (unsigned)w;
+      const int vb = npr * 16 + (lane & 3) * 2;
+      const zt* rowp = M + (int64_t)rc * lda;
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int v = vb + t * 8 + h;
+          U.col[t][h] = v < nv ? colmap[v] : -1;
+          U.seed[t][h] = __ldcg(rowp + max(U.col[t][h], 0));
+        }
+    };
+    Unit cur, nxt;
+    int mt = wp, npr = 0;
+    while (mt >= MT) {
+      mt -= MT;
+      ++npr;
+    }
+    bool have = npr < NPR;
+    if (have) load_unit(mt, npr, nxt);
+    while (have) {
+      cur = nxt;
+      const int cmt = mt, cnpr = npr;
+      mt += 16;
+      while (mt >= MT) {
+        mt -= MT;
+        ++npr;
+      }
+      have = npr < NPR;
+      if (have) load_unit(mt, npr, nxt);
+      double ar[2][2], ai[2][2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const bool ok = cur.rok && cur.col[t][h] >= 0;
+          ar[t][h] = ok ? cur.seed[t][h].x : 0.0;
+          ai[t][h] = ok ? cur.seed[t][h].y : 0.0;
+        }
+      const zt* Trow = Ts + (cmt * 8 + (lane >> 2)) * NB + (lane & 3);
+      const zt* Zc = Zs + (lane & 3) * zs + cnpr * 16 + (lane >> 2);
+#pragma unroll 7
+      for (int k4 = 0; k4 < K4; ++k4) {
+        const zt av = Trow[k4 * 4];
+        const zt b0 = Zc[k4 * 4 * zs], b1 = Zc[k4 * 4 * zs + 8];
+        dmma884(ar[0][0], ar[0][1], av.x, b0.x);
+        dmma884(ar[1][0], ar[1][1], av.x, b1.x);
+        dmma884(ai[0][0], ai[0][1], av.x, b0.y);
+        dmma884(ai[1][0], ai[1][1], av.x, b1.y);
+        dmma884(ar[0][0], ar[0][1], -av.y, b0.y);
+        dmma884(ar[1][0], ar[1][1], -av.y, b1.y);
+        dmma884(ai[0][0], ai[0][1], av.y, b0.x);
+        dmma884(ai[1][0], ai[1][1], av.y, b1.x);
+      }
+      if (cur.rr < n) {
+        zt* rowp = M + (int64_t)cur.rr * lda;
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (cur.col[t][h] >= 0) rowp[cur.col[t][h]] = make_double2(ar[t][h], ai[t][h]);
+      }
+    }
+    __syncthreads();  // update stored before the next panel reads its columns
+    WS_MARK(p, 3);
+  }
+  if (singular && tid == 0) atomicCAS(info, 0, blockIdx.x + 1);
+  __syncthreads();
+  ws_output(M, lda, out, ldo, obs, n, fin, plist, pstep, smem_raw);
+}
+
 // pi = S_{n-1} o ... o S_0 (one thread per matrix)
 __global__ void zgj_pi_kernel(const int* piv_all, int* pi_all, int n, int batch) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1700,7 +1961,7 @@ bool use_ws(int n, int batch) {
 // every feasible regime on one wave and records the argmin of eps; without a plan entry the
 // measured default rules below apply.
 // ---------------------------------------------------------------------------
-enum Regime { REG_NONE = 0, REG_SMALL, REG_FUSED, REG_WS, REG_P47, REG_BLOCKED, REG_REC, REG_COUNT };
+enum Regime { REG_NONE = 0, REG_SMALL, REG_FUSED, REG_WS, REG_P47, REG_BLOCKED, REG_REC, REG_SEQ, REG_COUNT };
 std::mutex g_plan_mu;
 std::map<std::pair<int, int>, int> g_plan;  // (n, batch) -> regime
 thread_local int g_regime_force = REG_NONE;
@@ -1713,6 +1974,7 @@ bool regime_feasible(int r, int n) {
     case REG_P47: return n <= 4096;
     case REG_BLOCKED: return true;
     case REG_REC: return n > 32 && n <= REC_NMAX;
+    case REG_SEQ: return n > 32 && n <= WS_NMAX;
     default: return false;
   }
 }
@@ -1723,7 +1985,9 @@ int default_regime(int n, int batch) {
   if (m == 3 && regime_feasible(REG_WS, n)) return REG_WS;
   if (m == 1 && n > 32 && n <= 256) return REG_FUSED;
   if (n <= 32) return REG_SMALL;
-  if (n >= 100 && n <= 200) return REG_WS;
+  // sequential-phase one-CTA-per-matrix kernel: measured fastest for 48 <= n <= 200 (the leaf
+  // n_i = 196 and the mid-level interfaces) at every batch size
+  if (n >= 48 && n <= 200) return REG_SEQ;
   if (use_fused(n, batch)) return REG_FUSED;
   // implicit-pivoting 28-column panels: measured (tools/gj_tune.py) 1.5x faster than the explicit
   // panels in one CTA (n <= 256) and 1.1-1.15x at clusters of 3-8 CTAs; at 2 and > 8 CTAs
@@ -1882,17 +2146,20 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     }
     return;
   }
-  if (reg == REG_WS) {
+  if (reg == REG_WS || reg == REG_SEQ) {
     ProfScope ps(K_GJ_FUSED, 8.0 * n * n * (double)n * batch, 32.0 * n * (double)n * batch, st);
     static bool wattr = false;
     if (!wattr) {
       HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)ws_smem(WS_NMAX)));
+      HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)ws_smem(WS_NMAX)));
       wattr = true;
     }
+    auto kern = reg == REG_SEQ ? zgj_seq_kernel : zgj_ws_kernel;
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
-      zgj_ws_kernel<<<nbatch, 512, ws_smem(n), st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
+      kern<<<nbatch, 512, ws_smem(n), st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
                                                       obs, n, info,
                                                       WsFinish{nullptr, nullptr, {0.0, 0.0}, 0, nullptr, nullptr, 0, 0.0});
       HPS_CUDA_CHECK(cudaGetLastError());
@@ -2027,7 +2294,8 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
 // plain inverse and leaf_schur_finish.
 bool zgj_leaf_fused_applies(int p, int batch) {
   const int n = (p - 2) * (p - 2);
-  return choose_regime(n, batch) == REG_WS && ws_finish_smem(p) <= ws_smem(n);
+  const int r = choose_regime(n, batch);
+  return (r == REG_WS || r == REG_SEQ) && ws_finish_smem(p) <= ws_smem(n);
 }
 
 bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
@@ -2039,6 +2307,8 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
   if (!wattr) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)ws_smem(WS_NMAX)));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)ws_smem(WS_NMAX)));
     wattr = true;
   }
   const double ni = n;
@@ -2047,7 +2317,8 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
   const zt m2ieta = make_double2(2.0 * eta.y, -2.0 * eta.x);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nbatch = std::min(65535, batch - b0);
-    zgj_ws_kernel<<<nbatch, 512, ws_smem(n), st>>>(
+    auto kern = choose_regime(n, batch) == REG_SEQ ? zgj_seq_kernel : zgj_ws_kernel;
+    kern<<<nbatch, 512, ws_smem(n), st>>>(
         S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
         info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2});
     HPS_CUDA_CHECK(cudaGetLastError());
@@ -2081,7 +2352,8 @@ int zgj_theta_o(int r, int n, int nbox, int nsm) {
       return std::max(1, occ) * nsm;
     }
     case REG_FUSED: return nbox >= nsm ? 2 * nsm : nsm;
-    case REG_WS: return nsm;
+    case REG_WS:
+    case REG_SEQ: return nsm;
     default: return nbox;  // blocked regimes: every box of the level in one batched launch
   }
 }
@@ -2186,7 +2458,7 @@ void zgj_force_regime(int r) { g_regime_force = r; }
 
 size_t zgj_workspace_bytes(int n, int batch) {
   const int reg = choose_regime(n, batch);
-  if (reg == REG_SMALL || reg == REG_WS || reg == REG_FUSED) return 16;
+  if (reg == REG_SMALL || reg == REG_WS || reg == REG_SEQ || reg == REG_FUSED) return 16;
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256;
 }

@@ -182,7 +182,7 @@ def zinv_batched(A):
 
 
 REGIMES = {1: "smem", 2: "fused", 3: "warp-specialised", 4: "blocked-implicit", 5: "blocked-explicit",
-           6: "blocked-recursive"}
+           6: "blocked-recursive", 7: "sequential-phase"}
 
 
 def rep_actions(g, p):
@@ -199,13 +199,13 @@ def rep_actions(g, p):
 def plan_inverse(n, nbox):
     """Measure the regimes for nbox n x n inverses and record the argmin of
     eps = ceil(nbox / theta_o) r; returns (regime, {regime: (eps_ms, r_ms, theta_o)})."""
-    eps = np.zeros(7)
-    r = np.zeros(7)
-    th = np.zeros(7, np.int32)
+    eps = np.zeros(8)
+    r = np.zeros(8)
+    th = np.zeros(8, np.int32)
     reg = lib().hps_plan_inverse(n, nbox, eps.ctypes.data, r.ctypes.data, th.ctypes.data)
     if reg < 0:
         _check(reg)
-    return reg, {k: (float(eps[k]), float(r[k]), int(th[k])) for k in range(1, 7) if eps[k] >= 0}
+    return reg, {k: (float(eps[k]), float(r[k]), int(th[k])) for k in range(1, 8) if eps[k] >= 0}
 
 
 def plan_problem(g, p):

@@ -361,8 +361,8 @@ def test_planned_regimes_parity():
         assert rel(S.R(1), Ro) < TOL and rel(S.solve(s, t), uo) < TOL
         S.close()
         n_top, nb_top = hps.rep_actions(g, p)[-1]
-        for reg in range(1, 7):
-            if (reg == 1 and n_top > 112) or (reg == 3 and n_top > 240):
+        for reg in range(1, 8):
+            if (reg == 1 and n_top > 112) or (reg in (3, 7) and n_top > 240):
                 continue
             hps._check(hps.lib().hps_plan_set(n_top, nb_top, reg))
             S = hps.Solver(g, p, kappa, eta, c)

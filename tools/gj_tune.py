@@ -15,7 +15,7 @@ for n, batch in shapes:
     A = torch.randn(batch, n, n, dtype=torch.complex128, device="cuda", generator=g)
     fl = 8.0 * n ** 3 * batch
     row = []
-    for mode in (0, 1, 2, 3, 4, 6):
+    for mode in (0, 3, 4, 6, 7):
         try:
             X, ms = hps.zinv_timed(A, mode=mode, reps=3)
             idx = [0, batch // 2, batch - 1]
@@ -31,7 +31,7 @@ if os.environ.get("WS_TRACE"):
     n, batch = shapes[0]
     A = torch.randn(batch, n, n, dtype=torch.complex128, device="cuda", generator=g)
     hps.lib().hps_debug_ws_trace(1, None)
-    hps.zinv_timed(A, mode=3, reps=1)
+    hps.zinv_timed(A, mode=int(os.environ.get("WS_TRACE_MODE", "3")), reps=1)
     buf = np.zeros(256, dtype=np.int64)
     hps.lib().hps_debug_ws_trace(0, buf.ctypes.data)
     t = buf.reshape(16, 16)

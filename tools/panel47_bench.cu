@@ -22,11 +22,67 @@ __device__ __forceinline__ unsigned pivot_key(zt f, int local) {
 }
 __device__ __forceinline__ void bar_sync_n(int id, int cnt) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(cnt) : "memory"); }
 
-template <int MODE>  // 0 full; 1 no row update; 2 no publish (fixed pivot row)
-__global__ void __launch_bounds__(256, 1) kern(const zt* in, zt* outp, long long* cyc, int npanels, int n) {
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+__device__ volatile int g_stop;
+__device__ long long g_bg_iters;
+// background update warps (threads 256..511): 3 DMMA only, 4 DMMA + LDS.128 fragments (3 per 8
+// DMMA, as zgj_ws_kernel), 5 as 4 plus LDG/STG of the accumulators every 56 DMMAs
+template <int BG>
+__device__ void background(const zt* in, zt* outp, const zt* sm) {
+  const int lane = threadIdx.x & 31;
+  double c[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  zt a = make_double2(1e-3, 2e-3), b0 = a, b1 = a;
+  int it = 0;
+  for (; !g_stop; ++it) {
+#pragma unroll
+    for (int k4 = 0; k4 < 7; ++k4) {
+      if (BG >= 4) {
+        a = sm[(lane & 7) * 28 + k4 * 4 + (lane >> 3)];
+        b0 = sm[224 + (lane & 3) * 34 + (lane >> 2) + k4];
+        b1 = sm[224 + (lane & 3) * 34 + 8 + (lane >> 2) + k4];
+      }
+      dmma(c[0][0], c[0][1], a.x, b0.x); dmma(c[1][0], c[1][1], a.x, b1.x);
+      dmma(c[2][0], c[2][1], a.x, b0.y); dmma(c[3][0], c[3][1], a.x, b1.y);
+      dmma(c[0][0], c[0][1], -a.y, b0.y); dmma(c[1][0], c[1][1], -a.y, b1.y);
+      dmma(c[2][0], c[2][1], a.y, b0.x); dmma(c[3][0], c[3][1], a.y, b1.x);
+      if (BG == 6) __nanosleep(32);
+      if (BG == 7) __nanosleep(0);
+    }
+    if (BG >= 5) {
+      const int idx = (threadIdx.x * 4 + it * 1024) & 8191;
+      zt v = in[idx];
+      c[0][0] += v.x;
+      outp[256 * 64 + (idx & 4095)] = make_double2(c[0][0], c[1][1]);
+    }
+  }
+  outp[256 * 64 + 4096 + (threadIdx.x & 255)] = make_double2(c[0][0] + c[1][0] + c[2][0] + c[3][0], c[0][1]);
+  if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long*)&g_bg_iters, (unsigned long long)it);
+
+}
+
+template <int MODE>  // 0 full; 1 no row update; 2 no publish (fixed pivot row); 3-5 full + background warps
+__global__ void __launch_bounds__(512, 1) kern(const zt* in, zt* outp, long long* cyc, int npanels, int n) {
   __shared__ zt prow4[2][28];
   __shared__ __align__(16) unsigned wkey4[2][8];
-  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  __shared__ zt bgsm[224 + 4 * 34 + 64];
+  if (threadIdx.x < 256) {  // background = warps 0-7; panel = warps 8-15 (arbiter favours high ids)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+    if (MODE >= 3) {
+      for (int i = threadIdx.x; i < 224 + 4 * 34 + 64; i += 256) bgsm[i] = in[i];
+      asm volatile("bar.sync 2, 256;\n" ::: "memory");
+      if (MODE == 3) background<3>(in, outp, bgsm);
+      if (MODE == 4) background<4>(in, outp, bgsm);
+      if (MODE == 5) background<5>(in, outp, bgsm);
+      if (MODE == 6) background<6>(in, outp, bgsm);
+      if (MODE == 7) background<7>(in, outp, bgsm);
+    }
+    return;
+  }
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
+  const int tid = threadIdx.x - 256, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
   int rq[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) rq[q] = wp * 32 + q * 8 + rg;
@@ -39,7 +95,7 @@ __global__ void __launch_bounds__(256, 1) kern(const zt* in, zt* outp, long long
     for (int q = 0; q < 4; ++q)
 #pragma unroll
       for (int c = 0; c < 7; ++c) a[q][c] = in[((rq[q] * 28 + cg * 7 + c) * 7 + pn) & 8191];
-    __syncthreads();
+    bar_sync_n(1, 256);
     long long t0 = clock64();
     for (int cga = 0; cga < 4; ++cga) {
       const bool act = cg == cga;
@@ -127,7 +183,10 @@ __global__ void __launch_bounds__(256, 1) kern(const zt* in, zt* outp, long long
       for (int c = 0; c < 7; ++c) acc.x += a[q][c].x + a[q][c].y;
     outp[tid + pn * 256] = acc;
   }
-  if (tid == 0) cyc[0] = tot;
+  if (tid == 0) {
+    cyc[0] = tot;
+    g_stop = 1;
+  }
 }
 int main() {
   zt *in, *out;
@@ -143,18 +202,34 @@ int main() {
   }
   cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
   const int np = 16;
-  const char* nm[] = {"full", "no row update", "no pivot search/publish"};
-  for (int mode = 0; mode < 3; ++mode)
-    for (int n : {64, 128, 224, 256}) {
+  const char* nm[] = {"full", "no row update", "no pivot search/publish", "full + DMMA warps",
+                      "full + DMMA/LDS warps", "full + DMMA/LDS/LDG warps", "  ... + nanosleep(32) per 8 DMMA",
+                      "  ... + nanosleep(0) per 8 DMMA"};
+  cudaMalloc(&out, (256 * 64 + 8192) * sizeof(zt));
+  for (int mode = 0; mode < 8; ++mode)
+    for (int n : {128, 224}) {
       long long c = 0;
       for (int r = 0; r < 2; ++r) {
-        if (mode == 0) kern<0><<<1, 256>>>(in, out, cyc, np, n);
-        if (mode == 1) kern<1><<<1, 256>>>(in, out, cyc, np, n);
-        if (mode == 2) kern<2><<<1, 256>>>(in, out, cyc, np, n);
+        int zero = 0;
+        long long z64 = 0;
+        cudaMemcpyToSymbol(g_stop, &zero, sizeof(int));
+        cudaMemcpyToSymbol(g_bg_iters, &z64, 8);
+        if (mode == 0) kern<0><<<1, 512>>>(in, out, cyc, np, n);
+        if (mode == 1) kern<1><<<1, 512>>>(in, out, cyc, np, n);
+        if (mode == 2) kern<2><<<1, 512>>>(in, out, cyc, np, n);
+        if (mode == 3) kern<3><<<1, 512>>>(in, out, cyc, np, n);
+        if (mode == 4) kern<4><<<1, 512>>>(in, out, cyc, np, n);
+        if (mode == 5) kern<5><<<1, 512>>>(in, out, cyc, np, n);
+        if (mode == 6) kern<6><<<1, 512>>>(in, out, cyc, np, n);
+        if (mode == 7) kern<7><<<1, 512>>>(in, out, cyc, np, n);
         cudaDeviceSynchronize();
         cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
       }
-      printf("%-24s n=%3d: %7.1f clk/step (%s)\n", nm[mode], n, (double)c / (np * 28), cudaGetErrorString(cudaGetLastError()));
+      long long bi = 0;
+      cudaMemcpyFromSymbol(&bi, g_bg_iters, 8);
+      const double steps = np * 28.0;
+      printf("%-34s n=%3d: %9.1f clk/step; background DMMA per step per SM %.0f (%.0f%% of pipe)\n", nm[mode], n,
+             (double)c / steps, bi * 56.0 / 2 / steps, 100.0 * bi * 56.0 / 2 * 16.0 / 4 / c);
       fflush(stdout);
     }
   return 0;

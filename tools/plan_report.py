@@ -7,11 +7,11 @@ from paper_1812_07167_b200 import hps, inputs
 cfg = inputs.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
 print(f"{cfg.name}: representative action = leaf interior inverse, then merge interface inverses")
-print(f"{'level':>9s} {'n':>5s} {'N_boxes':>8s}  " + "  ".join(f"{hps.REGIMES[k]:>22s}" for k in range(1, 7)) + "   chosen")
-print(f"{'':>25s}" + "  ".join(f"{'eps ms (r ms, th_o)':>22s}" for _ in range(1, 7)))
+print(f"{'level':>9s} {'n':>5s} {'N_boxes':>8s}  " + "  ".join(f"{hps.REGIMES[k]:>22s}" for k in range(1, 8)) + "   chosen")
+print(f"{'':>25s}" + "  ".join(f"{'eps ms (r ms, th_o)':>22s}" for _ in range(1, 8)))
 for lab, n, nb, reg, tab in hps.plan_problem(g, cfg.p):
     cells = []
-    for k in range(1, 7):
+    for k in range(1, 8):
         if k in tab:
             e, r, th = tab[k]
             cells.append(f"{e:9.3f} ({r:6.3f},{th:5d})")
