@@ -245,17 +245,22 @@ void launch(const ZGemm& g, cudaStream_t st) {
 // row, lanes stride over K with coalesced 16-byte loads of the A row, warp-shuffle reduction.
 // Bandwidth-bound (A is read once); parallel over M x batch warps, so the long-K / single-merge
 // matvecs at the top of the tree do not serialise on a handful of CTAs.
-template <int NMAX>
+template <int NMAX, int KS>
 __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
-  const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= g.M) return;
+  // KS warps share one output row (K split KS ways, partial sums reduced through shared
+  // memory), so the long-K matvecs at the top of the tree (few rows) still fill the GPU; the
+  // K loop keeps 4 independent A/B loads in flight per lane.
+  constexpr int RPB = 8 / KS;
+  __shared__ double part[8][NMAX][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, kw = warp % KS;
+  const int row = blockIdx.x * RPB + warp / KS;
+  const bool live = row < g.M;
   for (int b = blockIdx.y; b < g.batch; b += gridDim.y) {
     const int* Arm = g.A.rmap ? g.A.rmap + (int64_t)b * g.A.rmap_bs : nullptr;
     const int* Brm = g.B.rmap ? g.B.rmap + (int64_t)b * g.B.rmap_bs : nullptr;
     const int* Crm = g.C.rmap ? g.C.rmap + (int64_t)b * g.C.rmap_bs : nullptr;
     const int* Irm = g.Cin.rmap ? g.Cin.rmap + (int64_t)b * g.Cin.rmap_bs : nullptr;
-    const int ra = Arm ? Arm[row] : row;
+    const int ra = live ? (Arm ? Arm[row] : row) : -1;
     double accr[NMAX], acci[NMAX];
 #pragma unroll
     for (int r = 0; r < NMAX; ++r) accr[r] = acci[r] = 0.0;
@@ -270,21 +275,29 @@ __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
         bok[r] = cj >= 0;
         bco[r] = (int64_t)(cj < 0 ? 0 : cj) * g.B.cs;
       }
-      for (int k = lane; k < g.K; k += 32) {
-        const int ck = zcol(g.A.cmap, k, g.A.cskip_at, g.A.cskip_len);
-        const int rk = Brm ? Brm[k] : k;
-        if (ck < 0 || rk < 0) continue;
-        const zt a = Ab[(int64_t)ck * g.A.cs];
-        const zt* Brow = Bb + (int64_t)rk * g.B.rs;
+      constexpr int U = 4;
+      for (int k0 = kw * 32 + lane; k0 < g.K; k0 += 32 * KS * U) {
+        zt av[U], bv[U][NMAX];
 #pragma unroll
-        for (int r = 0; r < NMAX; ++r) {
-          if (!bok[r]) continue;
-          const zt v = Brow[bco[r]];
-          accr[r] = fma(a.x, v.x, accr[r]);
-          accr[r] = fma(-a.y, v.y, accr[r]);
-          acci[r] = fma(a.x, v.y, acci[r]);
-          acci[r] = fma(a.y, v.x, acci[r]);
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + u * 32 * KS;
+          const int ck = k < g.K ? zcol(g.A.cmap, k, g.A.cskip_at, g.A.cskip_len) : -1;
+          const int rk = k < g.K ? (Brm ? Brm[k] : k) : -1;
+          const bool ok = ck >= 0 && rk >= 0;
+          av[u] = ok ? Ab[(int64_t)ck * g.A.cs] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int r = 0; r < NMAX; ++r)
+            bv[u][r] = (ok && bok[r]) ? Bb[(int64_t)rk * g.B.rs + bco[r]] : make_double2(0.0, 0.0);
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < NMAX; ++r) {
+            accr[r] = fma(av[u].x, bv[u][r].x, accr[r]);
+            accr[r] = fma(-av[u].y, bv[u][r].y, accr[r]);
+            acci[r] = fma(av[u].x, bv[u][r].y, acci[r]);
+            acci[r] = fma(av[u].y, bv[u][r].x, acci[r]);
+          }
       }
     }
 #pragma unroll
@@ -294,6 +307,27 @@ __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
         accr[r] += __shfl_xor_sync(0xffffffffu, accr[r], o);
         acci[r] += __shfl_xor_sync(0xffffffffu, acci[r], o);
       }
+    if (KS > 1) {
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < NMAX; ++r) {
+          part[warp][r][0] = accr[r];
+          part[warp][r][1] = acci[r];
+        }
+      }
+      __syncthreads();
+      if (kw == 0) {
+#pragma unroll
+        for (int r = 0; r < NMAX; ++r)
+#pragma unroll
+          for (int j = 1; j < KS; ++j) {
+            accr[r] += part[warp + j][r][0];
+            acci[r] += part[warp + j][r][1];
+          }
+      }
+      __syncthreads();
+    }
+    if (!live || kw != 0) continue;
     const int ro = Crm ? Crm[row] : row;
     if (ro < 0) continue;
 #pragma unroll
@@ -317,6 +351,24 @@ __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
       if (co >= 0) g.C.ptr[(int64_t)b * g.C.bs + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
     }
   }
+}
+
+// Skinny-product launcher: KS from the work size (enough warps to fill the GPU, K >= 64 per warp)
+template <int NMAX>
+void launch_gemv(const ZGemm& g, cudaStream_t st) {
+  const int64_t rows = (int64_t)g.M * g.batch;
+  int ks = 1;
+  while (ks < 8 && rows * ks < 148 * 48 && g.K / (2 * ks) >= 64) ks *= 2;
+  const int rpb = 8 / ks;
+  dim3 grid((g.M + rpb - 1) / rpb, g.batch < 65535 ? g.batch : 65535);
+  switch (ks) {
+    case 1: zgemv_kernel<NMAX, 1><<<grid, 256, 0, st>>>(g); break;
+    case 2: zgemv_kernel<NMAX, 2><<<grid, 256, 0, st>>>(g); break;
+    case 4: zgemv_kernel<NMAX, 4><<<grid, 256, 0, st>>>(g); break;
+    default: zgemv_kernel<NMAX, 8><<<grid, 256, 0, st>>>(g); break;
+  }
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 __global__ void zcopy_kernel(const ZCopy c) {
@@ -384,12 +436,9 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
     case 7: launch<128, 64, 32, 32>(g, st); return true;
     case 8: launch<64, 64, 16, 32>(g, st); return true;
     case 9: {
-      dim3 grid((g.M + 7) / 8, g.batch < 65535 ? g.batch : 65535);
-      if (g.N == 1) zgemv_kernel<1><<<grid, 256, 0, st>>>(g);
-      else if (g.N <= 4) zgemv_kernel<4><<<grid, 256, 0, st>>>(g);
+      if (g.N == 1) launch_gemv<1>(g, st);
+      else if (g.N <= 4) launch_gemv<4>(g, st);
       else return false;
-      HPS_CUDA_CHECK(cudaGetLastError());
-      count_launch();
       return true;
     }
     default: return false;
@@ -403,13 +452,10 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
                16.0 * bt * ((double)g.M * g.K + (double)g.K * g.N + mn * (g.Cin.ptr ? 2.0 : 1.0)), st);
   if (g_zgemm_force >= 0 && launch_cfg(g_zgemm_force, g, st)) return;
   if (g.N <= 4 && g_zgemm_force != -2) {
-    dim3 grid((g.M + 7) / 8, g.batch < 65535 ? g.batch : 65535);
     if (g.N == 1)
-      zgemv_kernel<1><<<grid, 256, 0, st>>>(g);
+      launch_gemv<1>(g, st);
     else
-      zgemv_kernel<4><<<grid, 256, 0, st>>>(g);
-    HPS_CUDA_CHECK(cudaGetLastError());
-    count_launch();
+      launch_gemv<4>(g, st);
     return;
   }
   // Tile choice from the sweep in profiles/r01_gemm_tune.txt: 32x32 tiles (5 CTAs / SM) win

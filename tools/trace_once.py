@@ -8,6 +8,11 @@ import bench
 cfg = inputs.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 g, c, s, t = bench.setup(cfg, hps)
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+if os.environ.get("HPS_PLAN", "1") == "1":
+    hps.plan_problem(g, cfg.p)   # as bench.py does
+S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, d(c))
+S.solve(d(s), d(t))
+S.close()
 S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, d(c))
 S.solve(d(s), d(t))
 torch.cuda.synchronize()
