@@ -827,18 +827,22 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
   // ---- fused leaf epilogue (n = n_i = q^2, ldo = n_t); outputs are streamed past L2 (st.cs) so the
   // in-place matrices of the other CTAs stay resident ----
   const int q = fin.p - 2, ni = n, nb = 4 * q, nt = (int)ldo;
-  const zt* Ubx = fin.K + 2 * q * q;
+  zt* base = ob - ((int64_t)nb * nt + nb);  // leaf operator [Psi | Y], rows [I_b; I_i]
+  zt* Rl = fin.R + (int64_t)blockIdx.x * nb * nb;
+  // two x-lines per chunk (7 synchronised rounds instead of 14 at q = 14); the y-line sums of
+  // Y_b live in registers (11 per thread), those of Psi_b in shared memory
+  constexpr int LPC = 2, AY = 11;  // lines per chunk; ceil(2 q n_i / 512) for n_i <= 200
+  zt* C = reinterpret_cast<zt*>(smem_raw);  // [LPC][q][ni]  S^{-1} rows of the chunk's x-lines
+  zt* Pc = C + LPC * q * ni;                 // [LPC][q][nb]  Psi_i rows of the chunk's x-lines
+  zt* accP = Pc + LPC * q * nb;              // [2q][nb]      y-line sums for Psi_b
+  zt* Kc = accP + 2 * q * nb;                // Ubx, Uby, Vx, Vy (2q each), Gx, Gy (4 each)
+  for (int e = tid; e < 8 * q + 8; e += 512) Kc[e] = fin.K[2 * q * q + e];  // out of the inner loops
+  const zt* Ubx = Kc;
   const zt* Uby = Ubx + 2 * q;
   const zt* Vx = Uby + 2 * q;
   const zt* Vy = Vx + 2 * q;
   const zt* Gx = Vy + 2 * q;
   const zt* Gy = Gx + 4;
-  zt* base = ob - ((int64_t)nb * nt + nb);  // leaf operator [Psi | Y], rows [I_b; I_i]
-  zt* Rl = fin.R + (int64_t)blockIdx.x * nb * nb;
-  zt* C = reinterpret_cast<zt*>(smem_raw);  // [q][ni]   S^{-1} rows of x-line k
-  zt* Pc = C + q * ni;                       // [q][nb]   Psi_i rows of x-line k
-  zt* accY = Pc + q * nb;                    // [2q][ni]  y-line sums for Y_b (S rows, then N rows)
-  zt* accP = accY + 2 * q * ni;              // [2q][nb]  y-line sums for Psi_b
   const zt m2 = fin.m2ieta;
   auto zmac = [](zt& acc, zt a, zt b) {
     acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
@@ -850,57 +854,109 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
     if (row == b2) r.x += 1.0;
     __stcs(&Rl[row * nb + b2], r);
   };
-  for (int e = tid; e < 2 * q * ni; e += 512) accY[e] = make_double2(0.0, 0.0);
+  zt accY[AY];  // entry e = tid + 512 i of the [2q][ni] y-line sums (S rows, then N rows)
+#pragma unroll
+  for (int i = 0; i < AY; ++i) accY[i] = make_double2(0.0, 0.0);
   for (int e = tid; e < 2 * q * nb; e += 512) accP[e] = make_double2(0.0, 0.0);
-  for (int kx = 0; kx < q; ++kx) {  // x-line iy = kx: interior rows kx*q + t
+  const bool etr = g_ws_trace_on == n && blockIdx.x == 0 && tid == 0;
+  long long et[6] = {0, 0, 0, 0, 0, 0}, em = clock64();
+  auto emark = [&](int i) {
+    if (etr) {
+      const long long c = clock64();
+      et[i] += c - em;
+      em = c;
+    }
+  };
+  for (int kx0 = 0; kx0 < q; kx0 += LPC) {  // x-lines iy = kx0 .. kx0 + LPC - 1
+    const int nl = min(LPC, q - kx0);
     __syncthreads();
-    for (int e = tid; e < q * ni; e += 512) {
-      const int t = e / ni, j = e - t * ni;
-      const zt v = __ldcg(M + (int64_t)plist[kx * q + t] * lda + pstep[j]);
+    emark(0);
+    for (int e = tid; e < nl * q * ni; e += 512) {
+      const int t = e / ni, j = e - t * ni;  // t = line-local row l*q + t'
+      const zt v = __ldcg(M + (int64_t)plist[kx0 * q + t] * lda + pstep[j]);
       C[e] = v;
-      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + nb + j], v);  // Y_i
+      __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + nb + j], v);  // Y_i
     }
     __syncthreads();
-    // Psi_i rows of this line
-    for (int e = tid; e < q * nb; e += 512) {
+    emark(1);
+    // Psi_i rows of these lines
+    for (int e = tid; e < nl * q * nb; e += 512) {
       const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
       const zt* Cr = C + t * ni;
-      zt acc = make_double2(0.0, 0.0);
-      if (edge == 0 || edge == 2) {  // S / N: y-line ix = kk
-        const int side = edge == 0 ? 0 : 1;
-        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[t2 * q + kk], Uby[t2 * 2 + side]);
-      } else {  // E / W: x-line iy = kk
-        const int side = edge == 3 ? 0 : 1;
-        for (int t2 = 0; t2 < q; ++t2) zmac(acc, Cr[kk * q + t2], Ubx[t2 * 2 + side]);
+      // two independent accumulation chains (even / odd terms): the dot products are latency-bound
+      zt acc = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+      const bool yl = edge == 0 || edge == 2;  // S / N: y-line ix = kk; E / W: x-line iy = kk
+      const int side = yl ? (edge == 0 ? 0 : 1) : (edge == 3 ? 0 : 1);
+      const zt* Ub = yl ? Uby : Ubx;
+      const int cs = yl ? q : 1, c0 = yl ? kk : kk * q;
+#pragma unroll 7
+      for (int t2 = 0; t2 + 1 < q; t2 += 2) {
+        zmac(acc, Cr[c0 + t2 * cs], Ub[t2 * 2 + side]);
+        zmac(acc1, Cr[c0 + (t2 + 1) * cs], Ub[t2 * 2 + 2 + side]);
       }
+      if (q & 1) zmac(acc, Cr[c0 + (q - 1) * cs], Ub[(q - 1) * 2 + side]);
+      acc.x += acc1.x;
+      acc.y += acc1.y;
       Pc[e] = acc;
-      __stcs(&base[(int64_t)(nb + kx * q + t) * nt + b], acc);
+      __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + b], acc);
     }
-    // Y_b: W_kx, E_kx complete on this line; S/N (y-lines) accumulate
-    for (int j = tid; j < ni; j += 512) {
+    emark(2);
+    // Y_b: W_kx, E_kx complete on each line; S/N (y-lines) accumulate in registers
+    for (int e = tid; e < nl * ni; e += 512) {
+      const int l = e / ni, j = e - l * ni, kx = kx0 + l;
       zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
-      for (int t = 0; t < q; ++t) {
-        const zt v = C[t * ni + j];
+      zt w2 = make_double2(0.0, 0.0), w3 = make_double2(0.0, 0.0);
+#pragma unroll 7
+      for (int t = 0; t + 1 < q; t += 2) {
+        const zt v = C[(l * q + t) * ni + j], v1 = C[(l * q + t + 1) * ni + j];
         zmac(w0, Vx[t], v);
         zmac(w1, Vx[q + t], v);
+        zmac(w2, Vx[t + 1], v1);
+        zmac(w3, Vx[q + t + 1], v1);
       }
+      if (q & 1) {
+        const zt v = C[(l * q + q - 1) * ni + j];
+        zmac(w0, Vx[q - 1], v);
+        zmac(w1, Vx[2 * q - 1], v);
+      }
+      w0.x += w2.x;
+      w0.y += w2.y;
+      w1.x += w3.x;
+      w1.y += w3.y;
       __stcs(&base[(int64_t)(3 * q + kx) * nt + nb + j], make_double2(-w0.x, -w0.y));
       __stcs(&base[(int64_t)(q + kx) * nt + nb + j], make_double2(-w1.x, -w1.y));
     }
-    for (int e = tid; e < q * ni; e += 512) {  // node (ix = kk, iy = kx) is position kx of y-line kk
-      const int kk = e / ni, j = e - kk * ni;
-      const zt v = C[kk * ni + j];
-      zmac(accY[kk * ni + j], Vy[kx], v);
-      zmac(accY[(q + kk) * ni + j], Vy[q + kx], v);
+#pragma unroll
+    for (int i = 0; i < AY; ++i) {  // node (ix = kk, iy = kx) is position kx of y-line kk
+      const int e = tid + 512 * i;
+      if (e < 2 * q * ni) {
+        const int half = e >= q * ni, r = e - half * q * ni, kk = r / ni, j = r - kk * ni;
+        for (int l = 0; l < nl; ++l) zmac(accY[i], Vy[half * q + kx0 + l], C[(l * q + kk) * ni + j]);
+      }
     }
     __syncthreads();  // Pc complete
-    for (int b2 = tid; b2 < nb; b2 += 512) {
+    emark(3);
+    for (int e = tid; e < nl * nb; e += 512) {
+      const int l = e / nb, b2 = e - l * nb, kx = kx0 + l;
       zt w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
-      for (int t = 0; t < q; ++t) {
-        const zt v = Pc[t * nb + b2];
+      zt w2 = make_double2(0.0, 0.0), w3 = make_double2(0.0, 0.0);
+#pragma unroll 7
+      for (int t = 0; t + 1 < q; t += 2) {
+        const zt v = Pc[(l * q + t) * nb + b2], v1 = Pc[(l * q + t + 1) * nb + b2];
         zmac(w0, Vx[t], v);
         zmac(w1, Vx[q + t], v);
+        zmac(w2, Vx[t + 1], v1);
+        zmac(w3, Vx[q + t + 1], v1);
       }
+      if (q & 1) {
+        const zt v = Pc[(l * q + q - 1) * nb + b2];
+        zmac(w0, Vx[q - 1], v);
+        zmac(w1, Vx[2 * q - 1], v);
+      }
+      w0.x += w2.x;
+      w0.y += w2.y;
+      w1.x += w3.x;
+      w1.y += w3.y;
       const int e2 = b2 / q, k2 = b2 - e2 * q;
       zt g0 = make_double2(0.0, 0.0), g1 = make_double2(0.0, 0.0);
       if (k2 == kx && (e2 == 1 || e2 == 3)) {
@@ -912,18 +968,25 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
     }
     for (int e = tid; e < q * nb; e += 512) {
       const int kk = e / nb, b2 = e - kk * nb;
-      const zt v = Pc[kk * nb + b2];
-      zmac(accP[kk * nb + b2], Vy[kx], v);
-      zmac(accP[(q + kk) * nb + b2], Vy[q + kx], v);
+      for (int l = 0; l < nl; ++l) {
+        const zt v = Pc[(l * q + kk) * nb + b2];
+        zmac(accP[kk * nb + b2], Vy[kx0 + l], v);
+        zmac(accP[(q + kk) * nb + b2], Vy[q + kx0 + l], v);
+      }
     }
   }
   __syncthreads();
+  emark(4);
+  if (etr)
+    for (int i = 0; i < 5; ++i) g_ws_trace[15 * 16 + 4 + i] = et[i];
   // y-lines: S_kk (row kk) and N_kk (row 2q + kk)
-  for (int e = tid; e < q * ni; e += 512) {
-    const int kk = e / ni, j = e - kk * ni;
-    const zt a0 = accY[kk * ni + j], a1 = accY[(q + kk) * ni + j];
-    __stcs(&base[(int64_t)kk * nt + nb + j], make_double2(-a0.x, -a0.y));
-    __stcs(&base[(int64_t)(2 * q + kk) * nt + nb + j], make_double2(-a1.x, -a1.y));
+#pragma unroll
+  for (int i = 0; i < AY; ++i) {
+    const int e = tid + 512 * i;
+    if (e < 2 * q * ni) {
+      const int half = e >= q * ni, r = e - half * q * ni, kk = r / ni, j = r - kk * ni;
+      __stcs(&base[(int64_t)(half * 2 * q + kk) * nt + nb + j], make_double2(-accY[i].x, -accY[i].y));
+    }
   }
   for (int e = tid; e < q * nb; e += 512) {
     const int kk = e / nb, b2 = e - kk * nb, e2 = b2 / q, k2 = b2 - e2 * q;
@@ -1240,7 +1303,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
 
 size_t ws_finish_smem(int p) {
   const size_t q = p - 2, ni = q * q, nb = 4 * q;
-  return sizeof(zt) * (q * ni + q * nb + 2 * q * ni + 2 * q * nb);
+  return sizeof(zt) * (2 * q * ni + 2 * q * nb + 2 * q * nb + 8 * q + 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -1670,7 +1733,8 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
   bool piv[2] = {false, false}, singular = false;
   const bool warp_live = wp * 16 < n;
   const int MT = mtr >> 3;
-  const bool trace = g_ws_trace_on && blockIdx.x == 0 && tid == 0;
+  // trace armed with 1 (every launch) or with the matrix size n to trace
+  const bool trace = (g_ws_trace_on == 1 || g_ws_trace_on == n) && blockIdx.x == 0 && tid == 0;
   for (int p = 0; p < P.npan; ++p) {
     const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
     WS_MARK(p, 0);
@@ -1862,7 +1926,9 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
   }
   if (singular && tid == 0) atomicCAS(info, 0, blockIdx.x + 1);
   __syncthreads();
+  WS_MARK(15, 0);
   ws_output(M, lda, out, ldo, obs, n, fin, plist, pstep, smem_raw);
+  WS_MARK(15, 1);
 }
 
 // pi = S_{n-1} o ... o S_0 (one thread per matrix)
