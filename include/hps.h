@@ -70,10 +70,17 @@ typedef struct {
   int32_t leaf_chunk;   /* leaves factored per batch (0 = automatic) */
   int32_t profile;      /* bit mask of kernel classes (see hps_kernel_stats) to time with CUDA
                            events on the library stream; -1 = all; 0: counters only (default) */
-  int32_t leaf_mode;    /* 0 (default): B^{-1} through the interior Schur complement,
-                           with [Psi | Y] and R formed in the epilogue of the inverse kernel;
+  int32_t leaf_mode;    /* 0 (default): automatic -- mode 3 where it applies (real c samples,
+                           p - 2 <= 14 and kappa^2 max Re c < 0.9 pi^2 (1/hx^2 + 1/hy^2), the
+                           lowest Dirichlet eigenvalue of a leaf), else B^{-1} through the
+                           interior Schur complement with [Psi | Y] and R formed
+                           in the epilogue of the inverse kernel;
                            1: Gauss-Jordan on the full n^tau x n^tau matrix B;
-                           2: as 0 but with the separate finish kernel (comparison path).
+                           2: complex interior Schur complement with the separate finish kernel;
+                           3: real elimination of the interior block: one REAL
+                           inverse of A_ii per leaf plus the complex n_b x n_b complement
+                           Sigma = F_b - F_i A_ii^{-1} A_ib (eq. 7 rows reordered); needs real
+                           c samples and p - 2 <= 14 (else HPS_EINVAL), no resonance check.
                            Other values: HPS_EINVAL */
 } hps_opts;
 
@@ -169,6 +176,10 @@ double hps_last_flops(const hps_handle* h, int which);
  * CUDA-event durations around each launch (only while profiling is on); flops and bytes are
  * ALGORITHMIC (8 flops per complex multiply-add; operand bytes read + written once). */
 int hps_set_profiling(hps_handle* h, int mask);
+
+/* The leaf path hps_build took (leaf_mode numbering: 0 complex Schur fused, 1 full B, 2 complex
+ * Schur unfused, 3 real interior elimination); -1 for a top handle; HPS_EINVAL for NULL. */
+int hps_leaf_path(const hps_handle* h);
 int hps_kernel_stats(const hps_handle* h, int cls, int64_t* launches, double* ms, double* flops, double* bytes);
 int hps_reset_stats(hps_handle* h);
 

@@ -226,8 +226,10 @@ struct hps_handle {
   SolveState ss;
   DevBuf ident;             // identity index map 0 .. 2^Lb - 1
   bool keep_root_R = true, keep_all_R = false;
-  int leaf_mode = 0;  // 0: Schur complement on the interior (default), 1: invert the full B, 2: Schur, unfused
+  int leaf_mode = 0;  // 0: auto (3 where it applies, else Schur fused), 1: invert the full B, 2: Schur, unfused,
+                      // 3: real interior elimination
   bool leaf_fused = true;
+  int leaf_path = -1;  // the path build_leaves took (leaf_mode values; 0 = complex Schur, fused)
   std::vector<Depth> depth;
   std::vector<int> leaf_nat_h, nat_to_heap_h;
   DevBuf leaf_nat, nat_to_heap;
@@ -503,6 +505,71 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
 
   const size_t mat = (size_t)nt * nt;
   H.store.alloc(sizeof(zt) * mat * nleaf);
+  // leaf R (PAPER.md:398-402 via R = I - 2 i eta Psi_b): written by the fused leaf epilogues where
+  // they apply, else by leaf_R below
+  H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
+  if (H.leaf_mode == 0 || H.leaf_mode == 3) {
+    // real interior elimination: kappa^2 c real; in auto mode also kappa^2 max c
+    // below 0.9 x the lowest Dirichlet eigenvalue pi^2 (1/hx^2 + 1/hy^2) of a leaf, so A_ii is
+    // positive definite up to a margin (no interior resonance)
+    bool ok = leaf_real_fits(p);
+    if (ok) {
+      double cmax, imax;
+      leaf_real_c_bounds(c_dev, (int64_t)nleaf * p * p, cmax, imax, H.st);
+      const double k2 = H.kappa * H.kappa, lam1 = M_PI * M_PI * (1.0 / (hx * hx) + 1.0 / (hy * hy));
+      ok = imax == 0.0 && (H.leaf_mode == 3 || k2 * cmax < 0.9 * lam1);
+    }
+    if (H.leaf_mode == 3 && !ok)
+      throw HpsError{HPS_EINVAL, "hps_build: leaf_mode 3 needs real c samples and p - 2 <= 14"};
+    if (ok) {
+      const int q = p - 2;
+      std::vector<double> K((size_t)2 * q * q), KR((size_t)8 * q);
+      const double* D1x = dm.data();
+      const double* D1y = dm.data() + (size_t)p * p;
+      const double* D2x = dm.data() + (size_t)2 * p * p;
+      const double* D2y = dm.data() + (size_t)3 * p * p;
+      for (int i = 0; i < q; ++i)
+        for (int j = 0; j < q; ++j) {
+          K[(size_t)i * q + j] = D2x[(size_t)(i + 1) * p + j + 1];
+          K[(size_t)q * q + i * q + j] = D2y[(size_t)(i + 1) * p + j + 1];
+        }
+      for (int i = 0; i < q; ++i) {
+        KR[i] = -D2x[(size_t)(i + 1) * p];                      // A_ib, x-lines: W
+        KR[q + i] = -D2x[(size_t)(i + 1) * p + p - 1];          //                E
+        KR[2 * q + i] = -D2y[(size_t)(i + 1) * p];              // y-lines: S
+        KR[3 * q + i] = -D2y[(size_t)(i + 1) * p + p - 1];      //          N
+        KR[4 * q + i] = -D1x[i + 1];                            // F_i, W row: -d/dx
+        KR[5 * q + i] = D1x[(size_t)(p - 1) * p + i + 1];       //      E row: +d/dx
+        KR[6 * q + i] = -D1y[i + 1];                            //      S row: -d/dy
+        KR[7 * q + i] = D1y[(size_t)(p - 1) * p + i + 1];       //      N row: +d/dy
+      }
+      zt fb[2][2][2];
+      const zt ieta = make_double2(-H.eta.y, H.eta.x);
+      for (int ax = 0; ax < 2; ++ax) {
+        const double* D1 = ax == 0 ? D1x : D1y;
+        fb[ax][0][0] = make_double2(-D1[0] + ieta.x, ieta.y);
+        fb[ax][0][1] = make_double2(-D1[p - 1], 0.0);
+        fb[ax][1][0] = make_double2(D1[(size_t)(p - 1) * p], 0.0);
+        fb[ax][1][1] = make_double2(D1[(size_t)(p - 1) * p + p - 1] + ieta.x, ieta.y);
+      }
+      DevBuf dKr, dKR, wk;
+      upload(dKr, K, H.st);
+      upload(dKR, KR, H.st);
+      const size_t per = leaf_real_scratch_bytes(p, 1);
+      const int chunk = std::min(nleaf, chunk_opt > 0 ? chunk_opt : (int)std::max<size_t>(1, ((size_t)2 << 30) / per));
+      wk.alloc(per * chunk);
+      for (int l0 = 0; l0 < nleaf; l0 += chunk) {
+        const int nc = std::min(chunk, nleaf - l0);
+        launch_leaf_real(p, l0, nc, H.leaf_nat.as<int>(), c_dev, H.kappa * H.kappa, dKr.as<double>(), dKR.as<double>(),
+                         fb, H.eta, H.store.as<zt>() + (size_t)l0 * mat, (int64_t)mat,
+                         H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, wk.p, H.info.as<int>(), H.st);
+      }
+      const double ni = H.ni;
+      H.flops[0] += nleaf * (2.0 * ni * ni * ni + 8.0 * (double)nb * nb * (ni + nb) + 4.0 * ni * ni * nb);
+      H.leaf_path = 3;
+      return;
+    }
+  }
   const bool schur = H.leaf_mode != 1;
   const int ninv = schur ? H.ni : nt;  // matrix inverted per leaf
   const size_t wmat = (size_t)ninv * ninv;
@@ -512,9 +579,6 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   work.alloc(sizeof(zt) * wmat * chunk);
   ws.alloc(std::max<size_t>(zgj_workspace_bytes(ninv, chunk), 16));
   if (schur) upload(dK, schur_consts(p, hx, hy, H.eta, dm), H.st);
-  // leaf R (PAPER.md:398-402 via R = I - 2 i eta Psi_b): written by the fused leaf epilogue where
-  // it applies, else by leaf_R below
-  H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
   bool fused_all = schur;
   for (int l0 = 0; l0 < nleaf; l0 += chunk) {
     const int nc = std::min(chunk, nleaf - l0);
@@ -544,6 +608,7 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
     H.flops[0] += 8.0 * (double)nt * nt * nt * nleaf;
   }
   if (!fused_all) launch_leaf_R(H.store.as<zt>(), (int64_t)mat, H.R[H.L].as<zt>(), nleaf, nt, nb, H.eta, H.st);
+  H.leaf_path = schur ? (fused_all ? 0 : 2) : 1;
 }
 
 void build_merge(hps_handle& H, int d) {
@@ -1069,8 +1134,8 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     return HPS_EINVAL;
   }
   if (int rc = validate_problem(g, p, q, kappa, eta, "hps_build")) return rc;
-  if (opt && (opt->leaf_mode < 0 || opt->leaf_mode > 2)) {
-    hps_set_error("hps_build: leaf_mode must be 0, 1 or 2");
+  if (opt && (opt->leaf_mode < 0 || opt->leaf_mode > 3)) {
+    hps_set_error("hps_build: leaf_mode must be 0, 1, 2 or 3");
     return HPS_EINVAL;
   }
   std::unique_ptr<hps_handle> H(new hps_handle());
@@ -1341,6 +1406,11 @@ int64_t hps_last_launches(const hps_handle* h, int which) {
 double hps_last_flops(const hps_handle* h, int which) {
   if (!h || which < 0 || which > 1) return -1;
   return h->flops[which];
+}
+
+int hps_leaf_path(const hps_handle* h) {
+  if (!h) return HPS_EINVAL;
+  return h->leaf_path;
 }
 
 int hps_set_profiling(hps_handle* h, int mask) {

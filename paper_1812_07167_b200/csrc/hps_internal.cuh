@@ -94,6 +94,17 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
 // With c != nullptr the kernel also assembles S itself (c samples in natural leaf order, leaf_nat
 // the heap -> natural map, leaf0 the heap index of batch entry 0); S is then only workspace.
 bool zgj_leaf_fused_applies(int p, int batch);
+
+// Leaf operators by real elimination of the interior block (leaf_real.cu): for
+// kappa^2 c real, A_ii is real and B^{-1} follows from A_ii^{-1} and the complex n_b x n_b
+// Schur complement Sigma = F_b - F_i A_ii^{-1} A_ib.  K = [D2x | D2y] interior blocks (q x q
+// each), KR = A_ib / F_i line coefficients, fb = F_b line closures (layouts in leaf_real.cu).
+bool leaf_real_fits(int p);
+size_t leaf_real_scratch_bytes(int p, int batch);
+void leaf_real_c_bounds(const zt* c, int64_t n, double& cmax, double& imax, cudaStream_t st);
+void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt* c, double kappa2, const double* K,
+                      const double* KR, const zt (&fb)[2][2][2], zt eta, zt* store, int64_t mstride, zt* R,
+                      void* work, int* info, cudaStream_t st);
 bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
                            zt eta, int* info, cudaStream_t st, const zt* c = nullptr, const int* leaf_nat = nullptr,
                            int leaf0 = 0, double kappa2 = 0.0);

@@ -1,0 +1,782 @@
+// leaf_real.cu — leaf operators by real-arithmetic elimination of the interior block
+// (DESIGN.md 3.8).
+//
+// With u = [u_b; u_i] the leaf matrix is B = [F_b F_i; A_ib A_ii] (eq. 7 of PAPER.md:372-431,
+// rows: impedance rows F = N + i eta I on the boundary, interior collocation rows of
+// A^ = -D_xx - D_yy - kappa^2 diag(c)).  When kappa^2 c is real, A_ii, A_ib and F_i are real and
+// only F_b (the 2x2 line closures, holding i eta) is complex.  Eliminating u_i first:
+//   Sigma = F_b - F_i A_ii^{-1} A_ib                                  (n_b x n_b, complex)
+//   B^{-1} = [ Sigma^{-1}          , -Sigma^{-1} Q              ]     P = A_ii^{-1} A_ib (real)
+//            [ -P Sigma^{-1}       , A_ii^{-1} + P Sigma^{-1} Q ]     Q = F_i A_ii^{-1} (real)
+// so Psi = B^{-1}[:, I_b], Y = B^{-1}[:, I_i] and R = I - 2 i eta Psi_b follow from ONE real
+// n_i x n_i inverse (a quarter of the complex work) and products with n_b = 56 inner dimension.
+// A_ib and F_i couple a boundary node only with the q interior nodes of its grid line, so P, Q
+// and F_i P are 14-term line sums.
+// The elimination order needs A_ii well conditioned: it is used only when
+// kappa^2 max(c) < 0.9 x the lowest Dirichlet eigenvalue pi^2 (1/hx^2 + 1/hy^2) of the leaf, so
+// A_ii has no resonance (the caller checks; otherwise the complex Schur path of zgj.cu runs).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "hps_internal.cuh"
+
+namespace {
+
+constexpr int RL_NB = 28;  // panel width of the real Gauss-Jordan
+
+// phase timeline of CTA 0 (clock64), printed by launch_leaf_real when HPS_LR_TRACE=1 (debug)
+__device__ long long g_lr_trace[64];
+#define LR_MARK(i)                                                   \
+  do {                                                               \
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_lr_trace[i] = clock64(); \
+  } while (0)
+
+__device__ __forceinline__ void dmma884r(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ unsigned rkey(double v, int row) {
+  const double m = v * v;
+  const unsigned hi = (unsigned)(__double_as_longlong(m) >> 32);
+  return (hi & ~511u) | (unsigned)(511 - row);
+}
+
+__device__ __forceinline__ double rinv(double a) {  // 1/a: MUFU estimate + two Newton steps
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
+
+__device__ __forceinline__ void bsync(int id, int cnt) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(cnt) : "memory"); }
+
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
+}
+
+struct RPanels {
+  int npan, base, rem;
+  __device__ __forceinline__ int k0(int p) const { return p * base + min(p, rem); }
+  __device__ __forceinline__ int w(int p) const { return base + (p < rem ? 1 : 0); }
+};
+
+__host__ __device__ inline int rl_zs(int n) {  // Z row stride (doubles): >= n - wmin + 32, == 4 (mod 32)
+  const int npan = (n + RL_NB - 1) / RL_NB;
+  const int need = n - n / npan + 32;
+  return ((need - 4 + 31) / 32) * 32 + 4;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel A: assemble A_ii of leaf (leaf0 + blockIdx.x) and invert it in place by Gauss-Jordan
+// with partial (implicit) pivoting, the structure of zgj_seq_kernel in real arithmetic: all 16
+// warps run the pivot steps (2 rows x 7 columns per thread), then all 16 run the DMMA update
+// C(i, J) = [i not a pivot] C(i, J) + T(i, :) Z(:, J).  Leaves M with A_ii^{-1}(k, j) =
+// M(plist[k], pstep[j]) and writes plist, pstep to perm.
+// K = [D2x(1..q, 1..q) | D2y(1..q, 1..q)] (interior second-derivative blocks, scaled).
+// ---------------------------------------------------------------------------
+template <int RPT>
+__global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ Wk, int* __restrict__ perm,
+                                                          int leaf0, const int* __restrict__ leaf_nat,
+                                                          const zt* __restrict__ c, int p,
+                                                          const double* __restrict__ K, double kappa2,
+                                                          int* __restrict__ info) {
+  // panel: NPW = 32 / RPT warps, RPT rows x CPT columns per thread (the other warps wait at the
+  // block barrier that ends the panel: fewer warps per step means fewer redundant instructions
+  // per pivot step, which is issue-bound)
+  constexpr int NB = RL_NB, CPT = NB / 4, NPW = 32 / RPT, RPW = 8 * RPT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int q = p - 2, n = q * q, mtr = (n + 15) & ~15, zs = rl_zs(n);
+  double* Ts = reinterpret_cast<double*>(smem_raw);  // [mtr][NB]
+  double* Zs = Ts + (size_t)mtr * NB;                 // [NB][zs]
+  __shared__ double prow[2][NB];
+  __shared__ __align__(16) unsigned wkey[2][16];
+  __shared__ int pstep[256], plist[256], colmap[256 + 32];
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  double* M = Wk + (size_t)blockIdx.x * n * n;
+  {  // assemble A_ii (row iy*q + ix)
+    const double* D2x = K;
+    const double* D2y = K + q * q;
+    const zt* cl = c + (int64_t)leaf_nat[leaf0 + blockIdx.x] * p * p;
+    for (int r = wp; r < n; r += 16) {
+      const int ix = r % q, iy = r / q;
+      for (int cc = lane; cc < n; cc += 32) {
+        const int jx = cc % q, jy = cc / q;
+        double v = 0.0;
+        if (iy == jy) v -= D2x[ix * q + jx];
+        if (ix == jx) v -= D2y[iy * q + jy];
+        if (r == cc) v -= kappa2 * cl[(iy + 1) * p + ix + 1].x;
+        M[(int64_t)r * n + cc] = v;
+      }
+    }
+  }
+  if (tid < 256) pstep[tid] = 1 << 30;
+  if (tid < 32) wkey[0][tid] = 0u;
+  __syncthreads();
+  RPanels P;
+  P.npan = (n + NB - 1) / NB;
+  P.base = n / P.npan;
+  P.rem = n % P.npan;
+  int rq[RPT];
+  bool piv[RPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    rq[t] = wp * RPW + t * 8 + rg;
+    piv[t] = false;
+  }
+  bool singular = false;
+  const bool panel_warp = wp < NPW, warp_live = panel_warp && wp * RPW < n;
+  const int MT = mtr >> 3;
+  for (int pn = 0; pn < P.npan; ++pn) {
+    const int k0 = P.k0(pn), w = P.w(pn), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
+    LR_MARK(4 * pn);
+    if (panel_warp) {
+      double a[RPT][CPT];
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+          const int j = cg * CPT + cc;
+          a[t][cc] = (rq[t] < n && j < w) ? __ldcg(M + (int64_t)rq[t] * n + k0 + j) : 0.0;
+        }
+      for (int cga = 0; cga * CPT < w; ++cga) {
+        const bool act = cg == cga;
+        const int src = (lane & ~3) | cga;
+#pragma unroll
+        for (int s = 0; s < CPT; ++s) {
+          const int kk = cga * CPT + s;
+          if (kk < w) {
+            const int k = k0 + kk, par = k & 1;
+            unsigned key = 0u;
+            if (act) {
+#pragma unroll
+              for (int t = 0; t < RPT; ++t)
+                if (!piv[t] && rq[t] < n) key = max(key, rkey(a[t][s], rq[t]));
+            }
+            key = __reduce_max_sync(0xffffffffu, key);
+            if (lane == 0) wkey[par][wp] = key;
+            if (NPW == 16) __syncthreads(); else bsync(1, NPW * 32);
+            unsigned best = 0u;
+#pragma unroll
+            for (int g4 = 0; g4 < NPW / 4; ++g4) {
+              const uint4 kq = *reinterpret_cast<const uint4*>(&wkey[par][4 * g4]);
+              best = max(best, max(max(kq.x, kq.y), max(kq.z, kq.w)));
+            }
+            if ((best & ~511u) == 0u) singular = true;
+            const int r = 511 - (int)(best & 511u);
+            if (wp == r / RPW && rg == (r & 7)) {
+              const int tt = (r / 8) % RPT;
+#pragma unroll
+              for (int t = 0; t < RPT; ++t)
+                if (t == tt) {
+#pragma unroll
+                  for (int cc = 0; cc < CPT; ++cc) prow[par][cg * CPT + cc] = a[t][cc];
+                }
+              if (cg == 0) {
+                pstep[r] = k;
+                plist[k] = r;
+              }
+            }
+            if (NPW == 16) __syncthreads(); else bsync(1, NPW * 32);
+            if (warp_live) {
+              const double inv = rinv(prow[par][kk]);
+              double g[RPT];
+#pragma unroll
+              for (int t = 0; t < RPT; ++t) g[t] = __shfl_sync(0xffffffffu, a[t][s], src) * inv;
+              if (wp == r / RPW) {
+#pragma unroll
+                for (int t = 0; t < RPT; ++t)
+                  if (rq[t] == r) {  // pivot row: a <- pr / pivot exactly (as 0 - (-inv) pr)
+                    piv[t] = true;
+                    g[t] = -inv;
+#pragma unroll
+                    for (int cc = 0; cc < CPT; ++cc) a[t][cc] = 0.0;
+                  }
+              }
+#pragma unroll
+              for (int cc = 0; cc < CPT; ++cc) {
+                const double pc = prow[par][cg * CPT + cc];
+#pragma unroll
+                for (int t = 0; t < RPT; ++t) a[t][cc] = fma(-g[t], pc, a[t][cc]);
+              }
+              if (act) {
+#pragma unroll
+                for (int t = 0; t < RPT; ++t) a[t][s] = -g[t];
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RPT; ++t)
+        if (rq[t] < mtr) {
+#pragma unroll
+          for (int cc = 0; cc < CPT; ++cc) {
+            const int j = cg * CPT + cc;
+            Ts[rq[t] * NB + j] = j < w ? a[t][cc] : 0.0;
+            if (j < w && rq[t] < n) M[(int64_t)rq[t] * n + k0 + j] = a[t][cc];
+          }
+        }
+    }
+    if (nv == 0) break;
+    LR_MARK(4 * pn + 1);
+    // ---- update: all other columns, units of 8 rows x 32 columns ----
+    for (int v = tid; v < nv + 32; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
+    __syncthreads();
+    for (int e = tid; e < w4 * nv; e += 512) {
+      const int m = e / nv, v = e - m * nv;
+      if (m < w)
+        cpa8(Zs + m * zs + v, M + (int64_t)plist[k0 + m] * n + colmap[v]);
+      else
+        Zs[m * zs + v] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    LR_MARK(4 * pn + 2);
+    const int NP = (nv + 31) >> 5, NU = MT * NP;
+    // units of 8 rows x 32 columns, the next unit's seeds loaded before this unit's products
+    struct Unit {
+      int rr, col[4][2];
+      double seed[4][2];
+    };
+    auto load_unit = [&](int un, Unit& U) {
+      const int mt = un % MT, vb = (un / MT) * 32;
+      U.rr = mt * 8 + (lane >> 2);
+      const int rc = min(U.rr, n - 1);
+      const bool rok = U.rr < n && (unsigned)(pstep[rc] - k0) >= (unsigned)w;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int v = vb + t * 8 + (lane & 3) * 2 + h;
+          U.col[t][h] = v < nv ? colmap[v] : -1;
+          U.seed[t][h] = (rok && U.col[t][h] >= 0) ? __ldcg(M + (int64_t)rc * n + U.col[t][h]) : 0.0;
+        }
+    };
+    Unit cur, nxt;
+    int un = wp;
+    if (un < NU) load_unit(un, nxt);
+    while (un < NU) {
+      cur = nxt;
+      const int cun = un;
+      un += 16;
+      if (un < NU) load_unit(un, nxt);
+      const int mt = cun % MT, vb = (cun / MT) * 32;
+      double acc[4][2];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        acc[t][0] = cur.seed[t][0];
+        acc[t][1] = cur.seed[t][1];
+      }
+      const double* Trow = Ts + (mt * 8 + (lane >> 2)) * NB + (lane & 3);
+      const double* Zc = Zs + (lane & 3) * zs + vb + (lane >> 2);
+#pragma unroll 7
+      for (int k4 = 0; k4 < K4; ++k4) {
+        const double av = Trow[k4 * 4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma884r(acc[t][0], acc[t][1], av, Zc[k4 * 4 * zs + t * 8]);
+      }
+      if (cur.rr < n) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (cur.col[t][h] >= 0) M[(int64_t)cur.rr * n + cur.col[t][h]] = acc[t][h];
+      }
+    }
+    __syncthreads();
+    LR_MARK(4 * pn + 3);
+  }
+  if (singular && tid == 0) atomicCAS(info, 0, leaf0 + blockIdx.x + 1);
+  __syncthreads();
+  // A_ii^{-1}(k, j) = M(plist[k], pstep[j]): the permutations go out with M
+  int* pb = perm + (size_t)blockIdx.x * 2 * n;
+  for (int e = tid; e < n; e += 512) {
+    pb[e] = plist[e];
+    pb[n + e] = pstep[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Kernel B: leaf operators from A_ii^{-1} (see the header).  KR layout (doubles):
+//   ax[2][q]  A_ib coefficients of the x-lines: [0] W (-D2x(i+1, 0)), [1] E (-D2x(i+1, p-1))
+//   ay[2][q]  y-lines: [0] S, [1] N
+//   fx[2][q]  F_i coefficients: [0] W (-D1x(0, i+1)), [1] E (+D1x(p-1, i+1))
+//   fy[2][q]  [0] S, [1] N
+// fb: complex 2x2 closure per axis: [axis (0 x: W/E, 1 y: S/N)][row (first W/S)][col].
+// Boundary index: S_k = k, E_k = q + k, N_k = 2q + k, W_k = 3q + k.  Interior r = iy*q + ix.
+// The three dense products (Psi_i = -P Sigma^{-1}, W = Sigma^{-1} Q, Y_i = A_ii^{-1} + P W) run
+// on the FP64 tensor cores (DMMA m8n8k4) with complex operands stored re/im interleaved, so a
+// real x complex product is one real GEMM with twice the columns.
+// ---------------------------------------------------------------------------
+struct RLeafArgs {
+  const double* M;     // [leaf][n_i][n_i] dgj_leaf_kernel output: A_ii^{-1}(k, j) = M(plist[k], pstep[j])
+  const int* perm;     // [leaf][2][n_i] plist, pstep
+  double* Qg;          // [leaf][n_b][n_i] scratch
+  zt* store;           // leaf operators, entry 0 of the chunk, stride mstride
+  int64_t mstride;
+  zt* R;               // leaf R, entry 0 of the chunk, stride nb*nb
+  const double* KR;
+  zt fb[2][2][2];      // F_b closures
+  zt m2ieta;           // -2 i eta
+  int p, leaf0;
+};
+
+__device__ __forceinline__ void zfma_c(zt& acc, zt a, zt b) {  // acc += a * b
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+}
+
+// smallest L >= x with L = 4 or 12 (mod 16): rows of a DMMA operand (k = lane & 3, n = lane >> 2)
+// then fall in distinct bank pairs for each half warp
+__host__ __device__ inline int rl_ld(int x) {
+  while ((x & 15) != 4 && (x & 15) != 12) ++x;
+  return x;
+}
+
+struct RLeafSmem {  // offsets in doubles
+  int PS, SL, QL, WL, JB, mtr, ps, sg, qb, wb, ph1, total;
+  __host__ __device__ RLeafSmem(int p) {
+    const int q = p - 2, ni = q * q, nb = 4 * q;
+    JB = 28;
+    mtr = (ni + 7) & ~7;
+    PS = rl_ld(nb);
+    SL = rl_ld(2 * nb);
+    QL = rl_ld(JB);
+    WL = rl_ld(2 * JB);
+    ps = 0;
+    sg = ps + mtr * PS;
+    sg = (sg + 1) & ~1;
+    qb = sg + nb * SL;
+    wb = qb + nb * QL + 8;
+    wb = (wb + 1) & ~1;
+    ph1 = sg;  // phase 1 buffers (Cr[2], Qacc) alias Sigma / Q / W, which are written after it
+    const int t1 = wb + nb * WL + 32, t2 = ph1 + 4 * q * ni;
+    total = t1 > t2 ? t1 : t2;
+  }
+};
+
+// C = A B on DMMA.  Units of 8 rows x 32 columns over the 16 warps.  arow(r) -> pointer to A(r, 0)
+// (element k at arow(r)[k * astep]); B row-major with stride ldb.  pre(r, c, a0, a1) loads addends
+// for the accumulator pair (columns c, c + 1) before the product (their latency hides behind
+// it); store(r, c, a0, a1) consumes A B + addends (r < MT*8, c < N).
+template <typename ARow, typename Pre, typename Store>
+__device__ __forceinline__ void blk_mma(int MT, int N, int K4, ARow arow, int astep, const double* B, int ldb,
+                                        Pre pre, Store store) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int NU = (N + 31) >> 5;
+  for (int u = wp; u < MT * NU; u += 16) {
+    const int mt = u % MT, n0 = (u / MT) * 32;
+    const int r = mt * 8 + (lane >> 2);
+    const int ntile = min(4, (N - n0 + 7) >> 3);
+    double acc[4][2], ad[4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int c = n0 + t * 8 + (lane & 3) * 2;
+      if (c < N)
+        pre(r, c, ad[t][0], ad[t][1]);
+      else
+        ad[t][0] = ad[t][1] = 0.0;
+      acc[t][0] = acc[t][1] = 0.0;
+    }
+    const double* ap = arow(mt * 8 + (lane >> 2)) + (lane & 3) * astep;
+    const double* bp = B + (lane & 3) * ldb + n0 + (lane >> 2);
+    if (ntile == 4) {
+#pragma unroll 2
+      for (int k4 = 0; k4 < K4; ++k4) {
+        const double av = ap[k4 * 4 * astep];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) dmma884r(acc[t][0], acc[t][1], av, bp[k4 * 4 * ldb + t * 8]);
+      }
+    } else {
+      for (int k4 = 0; k4 < K4; ++k4) {
+        const double av = ap[k4 * 4 * astep];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (t < ntile) dmma884r(acc[t][0], acc[t][1], av, bp[k4 * 4 * ldb + t * 8]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int c = n0 + t * 8 + (lane & 3) * 2;
+      if (t < ntile && c < N) store(r, c, acc[t][0] + ad[t][0], acc[t][1] + ad[t][1]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A, int* __restrict__ info) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int p = A.p, q = p - 2, ni = q * q, nb = 4 * q, nt = nb + ni;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  const RLeafSmem L(p);
+  double* sm = reinterpret_cast<double*>(smem_raw);
+  double* Ps = sm + L.ps;  // [mtr][PS]  P = A_ii^{-1} A_ib
+  double* Sg = sm + L.sg;  // [nb][SL]   Sigma, then Sigma^{-1}, complex interleaved
+  double* Qb = sm + L.qb;  // [nb][QL]   column chunk of Q
+  double* Wb = sm + L.wb;  // [nb][WL]   W chunk, complex interleaved
+  zt* Sz = reinterpret_cast<zt*>(Sg);
+  const int SZ = L.SL / 2;
+  __shared__ int plist[256], pstep[256];
+  const double* Mg = A.M + (size_t)blockIdx.x * ni * ni;
+  double* Qg = A.Qg + (size_t)blockIdx.x * nb * ni;
+  zt* base = A.store + (int64_t)blockIdx.x * A.mstride;
+  zt* Rl = A.R + (int64_t)blockIdx.x * nb * nb;
+  const double* ax = A.KR;
+  const double* ay = ax + 2 * q;
+  const double* fx = ay + 2 * q;
+  const double* fy = fx + 2 * q;
+  for (int e = tid; e < ni; e += 512) {
+    plist[e] = A.perm[(size_t)blockIdx.x * 2 * ni + e];
+    pstep[e] = A.perm[(size_t)blockIdx.x * 2 * ni + ni + e];
+  }
+  LR_MARK(40);
+  // ---- phase 1: P = A_ii^{-1} A_ib and Q = F_i A_ii^{-1}, one x-line (q rows of A_ii^{-1}) at a
+  // time; row r of A_ii^{-1} is row plist[r] of M with columns permuted by pstep (cp.async
+  // gather, double-buffered)
+  double* Cr = sm + L.ph1;         // [2][q][ni]  rows of x-line k
+  double* Qacc = Cr + 2 * q * ni;  // [2q][ni]    S rows then N rows of Q
+  for (int e = tid; e < 2 * q * ni; e += 512) Qacc[e] = 0.0;
+  for (int e = tid; e < (L.mtr - ni) * L.PS; e += 512) Ps[ni * L.PS + e] = 0.0;
+  __syncthreads();  // plist / pstep
+  auto fetch = [&](int k, double* dst) {
+    for (int e = tid; e < q * ni; e += 512) {
+      const int t = e / ni, j = e - t * ni;
+      cpa8(dst + e, Mg + (size_t)plist[k * q + t] * ni + pstep[j]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  fetch(0, Cr);
+  for (int k = 0; k < q; ++k) {
+    double* Ck = Cr + (k & 1) * q * ni;
+    if (k + 1 < q) {
+      fetch(k + 1, Cr + ((k + 1) & 1) * q * ni);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    for (int e = tid; e < q * nb; e += 512) {
+      const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
+      const double* row = Ck + t * ni;
+      double s0 = 0.0, s1 = 0.0;
+      int off, st;
+      const double* co;
+      if (edge == 0 || edge == 2) {  // S / N: y-line ix = kk, nodes iy*q + kk
+        co = ay + (edge == 0 ? 0 : q);
+        off = kk;
+        st = q;
+      } else {  // E / W: x-line iy = kk, nodes kk*q + ix
+        co = ax + (edge == 3 ? 0 : q);
+        off = kk * q;
+        st = 1;
+      }
+      for (int i = 0; i + 1 < q; i += 2) {
+        s0 = fma(row[off + i * st], co[i], s0);
+        s1 = fma(row[off + (i + 1) * st], co[i + 1], s1);
+      }
+      if (q & 1) s0 = fma(row[off + (q - 1) * st], co[q - 1], s0);
+      Ps[(k * q + t) * L.PS + b] = s0 + s1;
+    }
+    // Q rows W_k, E_k complete (x-line k); S/N rows accumulate (row k*q + ix is point k of y-line ix)
+    for (int j = tid; j < ni; j += 512) {
+      double w0 = 0.0, w1 = 0.0;
+      for (int i = 0; i < q; ++i) {
+        const double v = Ck[i * ni + j];
+        w0 = fma(fx[i], v, w0);
+        w1 = fma(fx[q + i], v, w1);
+      }
+      Qg[(size_t)(3 * q + k) * ni + j] = w0;
+      Qg[(size_t)(q + k) * ni + j] = w1;
+    }
+    const double fs = fy[k], fn = fy[q + k];
+    for (int e = tid; e < q * ni; e += 512) {
+      const double v = Ck[e];
+      Qacc[e] = fma(fs, v, Qacc[e]);
+      Qacc[q * ni + e] = fma(fn, v, Qacc[q * ni + e]);
+    }
+    __syncthreads();  // Ck consumed before it is refilled
+  }
+  for (int e = tid; e < q * ni; e += 512) {
+    Qg[(size_t)e] = Qacc[e];                            // S_kk: row kk = e / ni
+    Qg[(size_t)2 * q * ni + e] = Qacc[q * ni + e];      // N_kk
+  }
+  __syncthreads();  // Qg visible to the block; Cr / Qacc dead
+  LR_MARK(41);
+  // ---- phase 2: Sigma = F_b - F_i P (complex n_b x n_b), then Sigma^{-1} in place ----
+  for (int e = tid; e < nb * nb; e += 512) {
+    const int b = e / nb, b2 = e - b * nb, edge = b / q, kk = b - edge * q;
+    double s = 0.0;
+    if (edge == 0 || edge == 2) {  // S / N rows: F_i on y-line kk (nodes iy*q + kk)
+      const double* co = fy + (edge == 0 ? 0 : q);
+      for (int i = 0; i < q; ++i) s = fma(co[i], Ps[(i * q + kk) * L.PS + b2], s);
+    } else {  // E / W rows: x-line kk (nodes kk*q + ix)
+      const double* co = fx + (edge == 3 ? 0 : q);
+      for (int i = 0; i < q; ++i) s = fma(co[i], Ps[(kk * q + i) * L.PS + b2], s);
+    }
+    zt v = make_double2(-s, 0.0);
+    const int e2 = b2 / q, k2 = b2 - e2 * q;
+    const int axis = (edge == 0 || edge == 2) ? 1 : 0, axis2 = (e2 == 0 || e2 == 2) ? 1 : 0;
+    if (k2 == kk && axis == axis2) {  // F_b: the 2x2 closure of the line (S_k, N_k) or (W_k, E_k)
+      const int ri = (edge == 0 || edge == 3) ? 0 : 1, ci = (e2 == 0 || e2 == 3) ? 0 : 1;
+      v.x += A.fb[axis][ri][ci].x;
+      v.y += A.fb[axis][ri][ci].y;
+    }
+    Sz[b * SZ + b2] = v;
+  }
+  // Gauss-Jordan with implicit partial pivoting (n_b <= 64): thread (i0 = tid / 64 + 8 m, j = tid % 64)
+  __shared__ int slist[64], sstep[64];
+  __shared__ zt prow_s[2][64], pcol_s[2][64];
+  if (tid < 64) sstep[tid] = 1 << 30;
+  const int jj = tid & 63, i0 = tid >> 6, MR = (nb + 7) >> 3;
+  __syncthreads();
+  LR_MARK(42);
+  for (int k = 0; k < nb; ++k) {
+    const int par = k & 1;
+    if (wp == 0) {  // pivot search over the rows not yet pivots; copy pivot row and column k
+      unsigned key = 0u;
+      for (int i = lane; i < nb; i += 32)
+        if (sstep[i] > k) {
+          const zt z = Sz[i * SZ + k];
+          const double m = fma(z.x, z.x, z.y * z.y);
+          key = max(key, ((unsigned)(__double_as_longlong(m) >> 32) & ~63u) | (unsigned)(63 - i));
+        }
+      key = __reduce_max_sync(0xffffffffu, key);
+      const int r = 63 - (int)(key & 63u);
+      if (lane == 0) {
+        slist[k] = r;
+        sstep[r] = k;
+        if ((key & ~63u) == 0u) atomicCAS(info, 0, A.leaf0 + blockIdx.x + 1);
+      }
+      for (int j = lane; j < nb; j += 32) {
+        prow_s[par][j] = Sz[r * SZ + j];
+        pcol_s[par][j] = Sz[j * SZ + k];
+      }
+    }
+    __syncthreads();
+    if (jj < nb) {
+      const int r = slist[k];
+      const zt pv = prow_s[par][k];
+      double d = fma(pv.x, pv.x, pv.y * pv.y), rd = rinv(d);
+      const zt inv = make_double2(pv.x * rd, -pv.y * rd);
+      const zt pr = prow_s[par][jj];
+      const zt prn = make_double2(pr.x * inv.x - pr.y * inv.y, pr.x * inv.y + pr.y * inv.x);  // pr / pivot
+      for (int m = 0; m < MR; ++m) {
+        const int i = i0 + 8 * m;
+        if (i < nb) {
+          zt v;
+          if (i == r) {
+            v = jj == k ? inv : prn;
+          } else {
+            const zt pc = pcol_s[par][i];
+            if (jj == k) {  // -S(i, k) / pivot
+              v = make_double2(-(pc.x * inv.x - pc.y * inv.y), -(pc.x * inv.y + pc.y * inv.x));
+            } else {
+              v = Sz[i * SZ + jj];
+              zfma_c(v, make_double2(-pc.x, -pc.y), prn);
+            }
+          }
+          Sz[i * SZ + jj] = v;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  LR_MARK(43);
+  {  // Sigma^{-1}(k, j) = S(slist[k], sstep[j]): gather to registers, then store in natural order
+    zt g[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int i = i0 + 8 * m;
+      if (m < MR && i < nb && jj < nb) g[m] = Sz[slist[i] * SZ + sstep[jj]];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int i = i0 + 8 * m;
+      if (m < MR && i < nb && jj < nb) Sz[i * SZ + jj] = g[m];
+    }
+    __syncthreads();
+  }
+  LR_MARK(44);
+  // ---- phase 3: Psi_b = Sigma^{-1} and R = I - 2 i eta Psi_b; Psi_i = -P Sigma^{-1} ----
+  for (int e = tid; e < nb * nb; e += 512) {
+    const int b = e / nb, b2 = e - b * nb;
+    const zt v = Sz[b * SZ + b2];
+    __stcs(&base[(int64_t)b * nt + b2], v);
+    zt rv = make_double2(A.m2ieta.x * v.x - A.m2ieta.y * v.y, A.m2ieta.x * v.y + A.m2ieta.y * v.x);
+    if (b == b2) rv.x += 1.0;
+    __stcs(&Rl[e], rv);
+  }
+  const int MTi = L.mtr >> 3, K4 = nb >> 2;
+  auto nopre = [](int, int, double& a0, double& a1) { a0 = a1 = 0.0; };
+  blk_mma(
+      MTi, 2 * nb, K4, [&](int r) { return Ps + r * L.PS; }, 1, Sg, L.SL, nopre,
+      [&](int r, int c, double a0, double a1) {
+        if (r < ni) __stcs(&base[(int64_t)(nb + r) * nt + (c >> 1)], make_double2(-a0, -a1));
+      });
+  LR_MARK(45);
+  // ---- phase 4: W = Sigma^{-1} Q by column chunks; Y_b = -W, Y_i = A_ii^{-1} + P W ----
+  const int JB = L.JB;
+  for (int j0 = 0; j0 < ni; j0 += JB) {
+    const int jw = min(JB, ni - j0);
+    __syncthreads();  // previous chunk's Qb / Wb consumed
+    for (int e = tid; e < nb * JB; e += 512) {
+      const int b = e / JB, j = e - b * JB;
+      Qb[b * L.QL + j] = j < jw ? __ldcg(Qg + (size_t)b * ni + j0 + j) : 0.0;
+    }
+    __syncthreads();
+    // rows 0..nb-1: Re Sigma^{-1} Q, rows nb..2nb-1: Im (A(row, k) = Sg[(row mod nb) SL + 2k + part])
+    blk_mma(
+        (2 * nb) >> 3, JB, K4,
+        [&](int r) { return r < nb ? Sg + r * L.SL : Sg + (r - nb) * L.SL + 1; }, 2, Qb, L.QL, nopre,
+        [&](int r, int c, double a0, double a1) {
+          const int b = r < nb ? r : r - nb, part = r < nb ? 0 : 1;
+          Wb[b * L.WL + 2 * c + part] = a0;
+          Wb[b * L.WL + 2 * c + 2 + part] = a1;
+        });
+    __syncthreads();
+    for (int e = tid; e < nb * jw; e += 512) {
+      const int b = e / jw, j = e - b * jw;
+      __stcs(&base[(int64_t)b * nt + nb + j0 + j], make_double2(-Wb[b * L.WL + 2 * j], -Wb[b * L.WL + 2 * j + 1]));
+    }
+    blk_mma(
+        MTi, 2 * jw, K4, [&](int r) { return Ps + r * L.PS; }, 1, Wb, L.WL,
+        [&](int r, int c, double& a0, double& a1) {
+          a0 = r < ni ? __ldcg(Mg + (size_t)plist[r] * ni + pstep[j0 + (c >> 1)]) : 0.0;
+          a1 = 0.0;
+        },
+        [&](int r, int c, double a0, double a1) {
+          if (r < ni) __stcs(&base[(int64_t)(nb + r) * nt + nb + j0 + (c >> 1)], make_double2(a0, a1));
+        });
+  }  LR_MARK(46);
+}
+
+// per-block max of Re c and of |Im c| over n samples
+__global__ void c_bounds_kernel(const zt* __restrict__ c, int64_t n, double* __restrict__ out) {
+  double mr = -1e300, mi = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const zt v = c[e];
+    mr = fmax(mr, v.x);
+    mi = fmax(mi, fabs(v.y));
+  }
+  for (int o = 16; o; o >>= 1) {
+    mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    mi = fmax(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+  }
+  __shared__ double sr[8], si[8];
+  if ((threadIdx.x & 31) == 0) {
+    sr[threadIdx.x >> 5] = mr;
+    si[threadIdx.x >> 5] = mi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      mr = fmax(mr, sr[w]);
+      mi = fmax(mi, si[w]);
+    }
+    out[2 * blockIdx.x] = mr;
+    out[2 * blockIdx.x + 1] = mi;
+  }
+}
+
+}  // namespace
+
+// max Re c and max |Im c| over n device samples (synchronises the stream)
+void leaf_real_c_bounds(const zt* c, int64_t n, double& cmax, double& imax, cudaStream_t st) {
+  constexpr int NBLK = 148;
+  double* d = nullptr;
+  HPS_CUDA_CHECK(cudaMallocAsync(&d, sizeof(double) * 2 * NBLK, st));
+  c_bounds_kernel<<<NBLK, 256, 0, st>>>(c, n, d);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+  double h[2 * NBLK];
+  HPS_CUDA_CHECK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+  HPS_CUDA_CHECK(cudaFreeAsync(d, st));
+  HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+  cmax = -1e300;
+  imax = 0.0;
+  for (int b = 0; b < NBLK; ++b) {
+    cmax = std::max(cmax, h[2 * b]);
+    imax = std::max(imax, h[2 * b + 1]);
+  }
+}
+
+size_t leaf_real_scratch_bytes(int p, int batch) {
+  const size_t q = p - 2, ni = q * q, nb = 4 * q;
+  return sizeof(double) * batch * (ni * ni + nb * ni) + sizeof(int) * batch * 2 * ni;
+}
+
+bool leaf_real_fits(int p) {
+  if (p < 4 || 4 * (p - 2) > 64 || (p - 2) * (p - 2) > 256) return false;
+  const int q = p - 2, ni = q * q;
+  const size_t smemA = sizeof(double) * ((size_t)((ni + 15) & ~15) * RL_NB + (size_t)RL_NB * rl_zs(ni));
+  const size_t smemB = sizeof(double) * (size_t)RLeafSmem(p).total;
+  return smemA <= 200 * 1024 && smemB <= 200 * 1024;
+}
+
+// Leaf operators of `batch` leaves (heap leaf0 ...) by the real interior elimination.  work:
+// leaf_real_scratch_bytes(p, batch).  K: D2x, D2y interior blocks; KR, fb: line coefficients and
+// closures (see the kernels).
+void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt* c, double kappa2, const double* K,
+                      const double* KR, const zt (&fb)[2][2][2], zt eta, zt* store, int64_t mstride, zt* R,
+                      void* work, int* info, cudaStream_t st) {
+  const int q = p - 2, ni = q * q, nb = 4 * q;
+  double* Wk = reinterpret_cast<double*>(work);
+  double* Qg = Wk + (size_t)batch * ni * ni;
+  int* perm = reinterpret_cast<int*>(Qg + (size_t)batch * ni * nb);
+  const size_t smemA = sizeof(double) * ((size_t)((ni + 15) & ~15) * RL_NB + (size_t)RL_NB * rl_zs(ni));
+  const size_t smemB = sizeof(double) * (size_t)RLeafSmem(p).total;
+  static bool attr = false;
+  if (!attr) {
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(leaf_real_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  const double nid = ni, nbd = nb;
+  ProfScope ps(K_LEAF_GJ, batch * (2.0 * nid * nid * nid + 8.0 * nbd * nbd * (nid + nbd) + 4.0 * nid * nid * nbd),
+               8.0 * batch * nid * nid + 16.0 * batch * ((nbd + nid) * (nbd + nid) + nbd * nbd), st);
+  for (int b0 = 0; b0 < batch; b0 += 65535) {
+    const int nbatch = std::min(65535, batch - b0);
+    static const int rpt = getenv("HPS_DGJ_RPT") ? atoi(getenv("HPS_DGJ_RPT")) : 4;
+    auto kern = rpt == 2 ? dgj_leaf_kernel<2> : dgj_leaf_kernel<4>;
+    kern<<<nbatch, 512, smemA, st>>>(Wk + (size_t)b0 * ni * ni, perm + (size_t)b0 * 2 * ni, leaf0 + b0,
+                                                leaf_nat, c, p, K, kappa2, info);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    RLeafArgs a;
+    a.M = Wk + (size_t)b0 * ni * ni;
+    a.perm = perm + (size_t)b0 * 2 * ni;
+    a.Qg = Qg + (size_t)b0 * ni * nb;
+    a.store = store + (int64_t)b0 * mstride;
+    a.mstride = mstride;
+    a.R = R + (int64_t)b0 * nb * nb;
+    a.KR = KR;
+    for (int x = 0; x < 2; ++x)
+      for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) a.fb[x][i][j] = fb[x][i][j];
+    a.m2ieta = make_double2(2.0 * eta.y, -2.0 * eta.x);
+    a.p = p;
+    a.leaf0 = leaf0 + b0;
+    leaf_real_ops_kernel<<<nbatch, 512, smemB, st>>>(a, info);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+  }
+  static const bool trace = getenv("HPS_LR_TRACE") && *getenv("HPS_LR_TRACE") == '1';
+  if (trace) {
+    long long t[64];
+    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    HPS_CUDA_CHECK(cudaMemcpyFromSymbol(t, g_lr_trace, sizeof(t)));
+    fprintf(stderr, "[leaf_real] dgj CTA0 (kclk from start): ");
+    for (int i = 0; i < 28; ++i) fprintf(stderr, "%s%.1f", i % 4 ? " " : " | ", (t[i] - t[0]) / 1e3);
+    fprintf(stderr, "\n[leaf_real] ops CTA0 phases (kclk): p1 %.1f  sigma %.1f  gj %.1f  perm %.1f  psi %.1f  p4 %.1f\n",
+            (t[41] - t[40]) / 1e3, (t[42] - t[41]) / 1e3, (t[43] - t[42]) / 1e3, (t[44] - t[43]) / 1e3,
+            (t[45] - t[44]) / 1e3, (t[46] - t[45]) / 1e3);
+  }
+}

@@ -38,7 +38,7 @@ class hps_opts(C.Structure):
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
-           "hps_last_flops", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
+           "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free",
            "hps_last_error"]
 
@@ -71,6 +71,7 @@ def lib():
         L.hps_last_flops.argtypes = [vp, i32]
         L.hps_last_flops.restype = C.c_double
         L.hps_set_profiling.argtypes = [vp, i32]
+        L.hps_leaf_path.argtypes = [vp]
         L.hps_kernel_stats.argtypes = [vp, i32, C.POINTER(i64), C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
         L.hps_reset_stats.argtypes = [vp]
@@ -308,6 +309,11 @@ class Solver:
 
     def flops(self, which):
         return lib().hps_last_flops(self.h, which)
+
+    def leaf_path(self):
+        """Leaf path the build took: 0 complex Schur (fused), 1 full B, 2 complex Schur (unfused),
+        3 real interior elimination (hps.h leaf_mode)."""
+        return lib().hps_leaf_path(self.h)
 
     def set_profiling(self, mask):
         _check(lib().hps_set_profiling(self.h, -1 if mask is True else int(mask)))

@@ -49,6 +49,49 @@ def test_leaf_parity(p, leaf_mode):
         assert rel(S.R(2 + leaf), lo["R"]) < TOL
 
 
+@pytest.mark.parametrize("p", [4, 6, 8, 10, 12, 13, 14, 16])
+def test_leaf_parity_real_elimination(p):
+    """leaf_mode 3 (real A_ii^{-1} + complex n_b x n_b complement) on non-square
+    leaves (h_x = 0.5, h_y = 1): Psi, Y and the leaf R vs the oracle's full-B inverse.  kappa = 4
+    keeps kappa^2 c (<= 20.8) below the lowest Dirichlet eigenvalue of the leaf (49.3)."""
+    g, c, s, t = problem(2, 1, p, 4.0, 4.0 + 1j)
+    S = hps.Solver(g, p, 4.0, 4.0 + 1j, c, keep_all_R=True, leaf_mode=3)
+    assert S.leaf_path() == 3
+    for leaf in range(2):
+        Psi, Y = S.leaf_ops(leaf)
+        lo = oracle.leaf(p, 0.5, 1.0, 4.0, 4.0 + 1j, c[leaf])
+        assert rel(Psi, lo["Psi"]) < TOL
+        assert rel(Y, lo["Y"]) < TOL
+        assert rel(S.R(2 + leaf), lo["R"]) < TOL
+
+
+def test_leaf_path_selection():
+    """Auto mode takes the real elimination only for real c below the first interior resonance;
+    leaf_mode 3 refuses complex c."""
+    g, c, s, t = problem(2, 1, 8, 4.0, 4.0 + 1j)
+    assert hps.Solver(g, 8, 4.0, 4.0 + 1j, c).leaf_path() == 3
+    # complex Schur path (2: unfused at n_i = 36, below the fused kernels' range)
+    assert hps.Solver(g, 8, 7.0, 7.0 + 1j, c).leaf_path() == 2   # 7^2 * 1.3 > 0.9 * 49.3
+    cc = c + 1e-3j
+    assert hps.Solver(g, 8, 4.0, 4.0 + 1j, cc).leaf_path() == 2
+    g16, c16, _, _ = problem(2, 1, 16, 7.0, 7.0 + 1j)
+    assert hps.Solver(g16, 16, 7.0, 7.0 + 1j, c16).leaf_path() == 0
+    with pytest.raises(Exception):
+        hps.Solver(g, 8, 4.0, 4.0 + 1j, cc, leaf_mode=3)
+
+
+def test_leaf_real_batched_p16_many_leaves():
+    """64 leaves at p = 16 on the real path (several CTAs per SM wave), sampled leaves vs oracle."""
+    g, c, s, t = problem(8, 8, 16, 25.0, 25.0 + 3j)
+    S = hps.Solver(g, 16, 25.0, 25.0 + 3j, c)
+    assert S.leaf_path() == 3
+    for leaf in [0, 17, 63]:
+        Psi, Y = S.leaf_ops(leaf)
+        lo = oracle.leaf(16, 0.125, 0.125, 25.0, 25.0 + 3j, c[leaf])
+        assert rel(Psi, lo["Psi"]) < TOL
+        assert rel(Y, lo["Y"]) < TOL
+
+
 @pytest.mark.parametrize("nx,ny,p", [(1, 1, 8), (2, 1, 8), (1, 2, 6), (4, 4, 8), (8, 4, 6), (4, 8, 10)])
 def test_every_R_and_u(nx, ny, p):
     kappa, eta = 9.0, 9.0 - 2j

@@ -15,7 +15,7 @@ for n, batch in shapes:
     A = torch.randn(batch, n, n, dtype=torch.complex128, device="cuda", generator=g)
     fl = 8.0 * n ** 3 * batch
     row = []
-    for mode in (0, 3, 4, 6, 7):
+    for mode in [int(m) for m in os.environ.get("GJ_MODES", "0,3,4,6,7").split(",")]:
         try:
             X, ms = hps.zinv_timed(A, mode=mode, reps=3)
             idx = [0, batch // 2, batch - 1]
