@@ -171,8 +171,9 @@ double hps_last_flops(const hps_handle* h, int which);
 /* Per-kernel-class statistics accumulated since the handle was built (or hps_reset_stats):
  * class 0 ZGEMM (DMMA), 1 Gauss-Jordan panel, 2 Gauss-Jordan small (in shared memory),
  * 3 Gauss-Jordan swaps/permutation, 4 leaf assembly, 5 gathers / layout, 6 fused whole-matrix
- * Gauss-Jordan (one CTA per matrix), 7 leaf inverse with the fused leaf epilogue (one
- * warp-specialised CTA per leaf: S^{-1}, [Psi | Y], R).  ms is the sum of
+ * Gauss-Jordan (one CTA per matrix), 7 leaf operators (one CTA per leaf: the complex Schur
+ * inverse with the fused epilogue, or the real interior elimination), 8 ZGEMV (products with
+ * N <= 4 right-hand sides: HBM-bound, flops and bytes as for class 0).  ms is the sum of
  * CUDA-event durations around each launch (only while profiling is on); flops and bytes are
  * ALGORITHMIC (8 flops per complex multiply-add; operand bytes read + written once). */
 int hps_set_profiling(hps_handle* h, int mask);

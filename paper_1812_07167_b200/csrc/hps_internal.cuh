@@ -95,7 +95,7 @@ void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t ob
 // the heap -> natural map, leaf0 the heap index of batch entry 0); S is then only workspace.
 bool zgj_leaf_fused_applies(int p, int batch);
 
-// Leaf operators by real elimination of the interior block (leaf_real.cu, DESIGN.md 3.8): for
+// Leaf operators by real elimination of the interior block (leaf_real.cu, DESIGN.md 3.1b): for
 // kappa^2 c real, A_ii is real and B^{-1} follows from A_ii^{-1} and the complex n_b x n_b
 // Schur complement Sigma = F_b - F_i A_ii^{-1} A_ib.  K = [D2x | D2y] interior blocks (q x q
 // each), KR = A_ib / F_i line coefficients, fb = F_b line closures (layouts in leaf_real.cu).
@@ -131,7 +131,7 @@ inline void count_launch(int k = 1) {
 // Per-kernel-class accounting (hps_kernel_stats): launches, algorithmic FLOPs / bytes, and —
 // when profiling is on — device time from CUDA events recorded on the launching stream.
 // ---------------------------------------------------------------------------
-enum KClass { K_ZGEMM = 0, K_GJ_PANEL, K_GJ_SMALL, K_GJ_AUX, K_LEAF_ASM, K_LAYOUT, K_GJ_FUSED, K_LEAF_GJ, K_NCLASS };
+enum KClass { K_ZGEMM = 0, K_GJ_PANEL, K_GJ_SMALL, K_GJ_AUX, K_LEAF_ASM, K_LAYOUT, K_GJ_FUSED, K_LEAF_GJ, K_ZGEMV, K_NCLASS };
 
 struct KStats {
   int64_t launches[K_NCLASS] = {};

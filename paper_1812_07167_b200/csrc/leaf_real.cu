@@ -1,5 +1,5 @@
 // leaf_real.cu — leaf operators by real-arithmetic elimination of the interior block
-// (DESIGN.md 3.8).
+// (DESIGN.md 3.1b).
 //
 // With u = [u_b; u_i] the leaf matrix is B = [F_b F_i; A_ib A_ii] (eq. 7 of PAPER.md:372-431,
 // rows: impedance rows F = N + i eta I on the boundary, interior collocation rows of
@@ -744,8 +744,8 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
                8.0 * batch * nid * nid + 16.0 * batch * ((nbd + nid) * (nbd + nid) + nbd * nbd), st);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nbatch = std::min(65535, batch - b0);
-    static const int rpt = getenv("HPS_DGJ_RPT") ? atoi(getenv("HPS_DGJ_RPT")) : 4;
-    auto kern = rpt == 2 ? dgj_leaf_kernel<2> : dgj_leaf_kernel<4>;
+    static const int rpt = getenv("HPS_DGJ_RPT") ? atoi(getenv("HPS_DGJ_RPT")) : 2;
+    auto kern = rpt == 4 ? dgj_leaf_kernel<4> : dgj_leaf_kernel<2>;
     kern<<<nbatch, 512, smemA, st>>>(Wk + (size_t)b0 * ni * ni, perm + (size_t)b0 * 2 * ni, leaf0 + b0,
                                                 leaf_nat, c, p, K, kappa2, info);
     HPS_CUDA_CHECK(cudaGetLastError());

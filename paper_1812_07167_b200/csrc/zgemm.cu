@@ -448,7 +448,9 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
 void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return;
   const double mn = (double)g.M * g.N, bt = (double)g.batch;
-  ProfScope ps(K_ZGEMM, 8.0 * mn * g.K * bt,
+  // N <= 4 runs the GEMV kernel: bound by HBM (the A operand is read once), its own class
+  const bool gemv = (g_zgemm_force < 0 && g.N <= 4) || g_zgemm_force == 9;
+  ProfScope ps(gemv ? K_ZGEMV : K_ZGEMM, 8.0 * mn * g.K * bt,
                16.0 * bt * ((double)g.M * g.K + (double)g.K * g.N + mn * (g.Cin.ptr ? 2.0 : 1.0)), st);
   if (g_zgemm_force >= 0 && launch_cfg(g_zgemm_force, g, st)) return;
   if (g.N <= 4 && g_zgemm_force != -2) {

@@ -42,7 +42,7 @@ SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free",
            "hps_last_error"]
 
-KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout", "zgj_fused", "leaf_gj"]
+KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout", "zgj_fused", "leaf_gj", "zgemv"]
 
 
 def lib():
