@@ -529,64 +529,123 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
     }
     Sz[b * SZ + b2] = v;
   }
-  // Gauss-Jordan with implicit partial pivoting (n_b <= 64): thread (i0 = tid / 64 + 8 m, j = tid % 64)
+  // Gauss-Jordan with implicit partial pivoting (n_b <= 64), Sigma held in registers: warp w owns
+  // rows 4w .. 4w+3, lane l columns 2l, 2l+1.  Per step: the pivot row goes through shared memory
+  // (written by its warp), the pivot column by shuffles inside each warp, and the owners of column
+  // k + 1 leave the pivot keys of the next step (shared-memory traffic per step: one row).
   __shared__ int slist[64], sstep[64];
-  __shared__ zt prow_s[2][64], pcol_s[2][64];
+  __shared__ __align__(16) unsigned wkey2[2][16];
+  __shared__ __align__(16) zt prow2[64];
+  const int NWG = (nb + 3) >> 2;  // warps in the elimination
+  const bool gw = wp < NWG;
+  zt a[4][2];
+  bool pivd[4];
+  __syncthreads();  // Sigma assembled
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    pivd[t] = false;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 4 * wp + t, c = 2 * lane + h;
+      a[t][h] = (gw && i < nb && c < nb) ? Sz[i * SZ + c] : make_double2(0.0, 0.0);
+    }
+  }
+  auto zkey = [](zt v, int i) {
+    return ((unsigned)(__double_as_longlong(fma(v.x, v.x, v.y * v.y)) >> 32) & ~63u) | (unsigned)(63 - i);
+  };
+  if (tid < 32) wkey2[0][tid & 15] = 0u;
   if (tid < 64) sstep[tid] = 1 << 30;
-  const int jj = tid & 63, i0 = tid >> 6, MR = (nb + 7) >> 3;
   __syncthreads();
+  if (gw && lane == 0) {  // keys of column 0
+    unsigned key = 0u;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (4 * wp + t < nb) key = max(key, zkey(a[t][0], 4 * wp + t));
+    wkey2[0][wp] = key;
+  }
   LR_MARK(42);
   for (int k = 0; k < nb; ++k) {
-    const int par = k & 1;
-    if (wp == 0) {  // pivot search over the rows not yet pivots; copy pivot row and column k
-      unsigned key = 0u;
-      for (int i = lane; i < nb; i += 32)
-        if (sstep[i] > k) {
-          const zt z = Sz[i * SZ + k];
-          const double m = fma(z.x, z.x, z.y * z.y);
-          key = max(key, ((unsigned)(__double_as_longlong(m) >> 32) & ~63u) | (unsigned)(63 - i));
-        }
-      key = __reduce_max_sync(0xffffffffu, key);
-      const int r = 63 - (int)(key & 63u);
-      if (lane == 0) {
-        slist[k] = r;
-        sstep[r] = k;
-        if ((key & ~63u) == 0u) atomicCAS(info, 0, A.leaf0 + blockIdx.x + 1);
-      }
-      for (int j = lane; j < nb; j += 32) {
-        prow_s[par][j] = Sz[r * SZ + j];
-        pcol_s[par][j] = Sz[j * SZ + k];
+    __syncthreads();  // keys of step k visible; prow2 of step k - 1 consumed
+    unsigned best = 0u;
+#pragma unroll
+    for (int g4 = 0; g4 < 4; ++g4) {
+      const uint4 kq = *reinterpret_cast<const uint4*>(&wkey2[k & 1][4 * g4]);
+      best = max(best, max(max(kq.x, kq.y), max(kq.z, kq.w)));
+    }
+    const int r = 63 - (int)(best & 63u);
+    if (tid == 0) {
+      slist[k] = r;
+      sstep[r] = k;
+      if ((best & ~63u) == 0u) atomicCAS(info, 0, A.leaf0 + blockIdx.x + 1);
+    }
+    if (wp == (r >> 2)) {  // the pivot row's warp publishes it (selects: no local-memory indexing)
+      const int tr = r & 3;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double x = tr == 0 ? a[0][h].x : tr == 1 ? a[1][h].x : tr == 2 ? a[2][h].x : a[3][h].x;
+        const double y = tr == 0 ? a[0][h].y : tr == 1 ? a[1][h].y : tr == 2 ? a[2][h].y : a[3][h].y;
+        prow2[2 * lane + h] = make_double2(x, y);
       }
     }
+    if (tid < 32) wkey2[(k + 1) & 1][tid & 15] = 0u;
     __syncthreads();
-    if (jj < nb) {
-      const int r = slist[k];
-      const zt pv = prow_s[par][k];
-      double d = fma(pv.x, pv.x, pv.y * pv.y), rd = rinv(d);
+    if (gw) {
+      const zt pv = prow2[k];
+      const double rd = rinv(fma(pv.x, pv.x, pv.y * pv.y));
       const zt inv = make_double2(pv.x * rd, -pv.y * rd);
-      const zt pr = prow_s[par][jj];
-      const zt prn = make_double2(pr.x * inv.x - pr.y * inv.y, pr.x * inv.y + pr.y * inv.x);  // pr / pivot
-      for (int m = 0; m < MR; ++m) {
-        const int i = i0 + 8 * m;
-        if (i < nb) {
-          zt v;
-          if (i == r) {
-            v = jj == k ? inv : prn;
-          } else {
-            const zt pc = pcol_s[par][i];
-            if (jj == k) {  // -S(i, k) / pivot
-              v = make_double2(-(pc.x * inv.x - pc.y * inv.y), -(pc.x * inv.y + pc.y * inv.x));
+      zt prn[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const zt pr = prow2[2 * lane + h];
+        prn[h] = make_double2(pr.x * inv.x - pr.y * inv.y, pr.x * inv.y + pr.y * inv.x);
+      }
+      const int src = k >> 1, hk = k & 1;
+      const int c0 = 2 * lane;
+      unsigned key = 0u;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = 4 * wp + t;
+        const zt own = make_double2(hk ? a[t][1].x : a[t][0].x, hk ? a[t][1].y : a[t][0].y);
+        const zt pc = make_double2(__shfl_sync(0xffffffffu, own.x, src), __shfl_sync(0xffffffffu, own.y, src));
+        if (i == r) {
+          pivd[t] = true;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) a[t][h] = (c0 + h == k) ? inv : prn[h];
+        } else {
+          const zt g = make_double2(pc.x * inv.x - pc.y * inv.y, pc.x * inv.y + pc.y * inv.x);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (c0 + h == k) {
+              a[t][h] = make_double2(-g.x, -g.y);
             } else {
-              v = Sz[i * SZ + jj];
-              zfma_c(v, make_double2(-pc.x, -pc.y), prn);
+              zfma_c(a[t][h], make_double2(-pc.x, -pc.y), prn[h]);  // a - S(i, k) S(r, j) / pivot
             }
           }
-          Sz[i * SZ + jj] = v;
         }
       }
+      // owners of column k + 1: lane (k + 1) / 2, slot (k + 1) & 1
+      if (lane == ((k + 1) >> 1) && k + 1 < nb) {
+        const int h1 = (k + 1) & 1;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (!pivd[t] && 4 * wp + t < nb)
+            key = max(key, zkey(make_double2(h1 ? a[t][1].x : a[t][0].x, h1 ? a[t][1].y : a[t][0].y), 4 * wp + t));
+        wkey2[(k + 1) & 1][wp] = key;
+      }
     }
-    __syncthreads();
   }
+  __syncthreads();
+  if (gw) {  // back to shared memory (implicit-pivot order), permuted below
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 4 * wp + t, c = 2 * lane + h;
+        if (i < nb && c < nb) Sz[i * SZ + c] = a[t][h];
+      }
+  }
+  __syncthreads();
+  const int jj = tid & 63, i0 = tid >> 6, MR = (nb + 7) >> 3;
   LR_MARK(43);
   {  // Sigma^{-1}(k, j) = S(slist[k], sstep[j]): gather to registers, then store in natural order
     zt g[8];
@@ -717,7 +776,7 @@ bool leaf_real_fits(int p) {
   const int q = p - 2, ni = q * q;
   const size_t smemA = sizeof(double) * ((size_t)((ni + 15) & ~15) * RL_NB + (size_t)RL_NB * rl_zs(ni));
   const size_t smemB = sizeof(double) * (size_t)RLeafSmem(p).total;
-  return smemA <= 200 * 1024 && smemB <= 200 * 1024;
+  return smemA <= 200 * 1024 && smemB + 8 * 1024 <= 220 * 1024;
 }
 
 // Leaf operators of `batch` leaves (heap leaf0 ...) by the real interior elimination.  work:
@@ -736,7 +795,7 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
   if (!attr) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(leaf_real_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(leaf_real_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
   const double nid = ni, nbd = nb;
