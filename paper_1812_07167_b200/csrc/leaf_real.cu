@@ -370,21 +370,32 @@ template <typename ARow, typename Pre, typename Store>
 __device__ __forceinline__ void blk_mma(int MT, int N, int K4, ARow arow, int astep, const double* B, int ldb,
                                         Pre pre, Store store) {
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int NU = (N + 31) >> 5;
-  for (int u = wp; u < MT * NU; u += 16) {
+  const int NU = (N + 31) >> 5, NUNIT = MT * NU;
+  double adn[4][2];
+  auto load_pre = [&](int u) {
+    const int mt = u % MT, n0 = (u / MT) * 32, r = mt * 8 + (lane >> 2);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int c = n0 + t * 8 + (lane & 3) * 2;
+      if (c < N)
+        pre(r, c, adn[t][0], adn[t][1]);
+      else
+        adn[t][0] = adn[t][1] = 0.0;
+    }
+  };
+  if (wp < NUNIT) load_pre(wp);
+  for (int u = wp; u < NUNIT; u += 16) {
     const int mt = u % MT, n0 = (u / MT) * 32;
     const int r = mt * 8 + (lane >> 2);
     const int ntile = min(4, (N - n0 + 7) >> 3);
     double acc[4][2], ad[4][2];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      const int c = n0 + t * 8 + (lane & 3) * 2;
-      if (c < N)
-        pre(r, c, ad[t][0], ad[t][1]);
-      else
-        ad[t][0] = ad[t][1] = 0.0;
+      ad[t][0] = adn[t][0];
+      ad[t][1] = adn[t][1];
       acc[t][0] = acc[t][1] = 0.0;
     }
+    if (u + 16 < NUNIT) load_pre(u + 16);  // the next unit's addends are in flight during this one
     const double* ap = arow(mt * 8 + (lane >> 2)) + (lane & 3) * astep;
     const double* bp = B + (lane & 3) * ldb + n0 + (lane >> 2);
     if (ntile == 4) {
@@ -441,16 +452,48 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
   // gather, double-buffered)
   double* Cr = sm + L.ph1;         // [2][q][ni]  rows of x-line k
   double* Qacc = Cr + 2 * q * ni;  // [2q][ni]    S rows then N rows of Q
+  __shared__ double coef[8 * 16];  // ax, ay, fx, fy (q <= 16)
+  if (tid < 8 * q) coef[tid] = A.KR[tid];
+  ax = coef;
+  ay = coef + 2 * q;
+  fx = coef + 4 * q;
+  fy = coef + 6 * q;
   for (int e = tid; e < 2 * q * ni; e += 512) Qacc[e] = 0.0;
   for (int e = tid; e < (L.mtr - ni) * L.PS; e += 512) Ps[ni * L.PS + e] = 0.0;
-  __syncthreads();  // plist / pstep
+  __syncthreads();  // plist / pstep / coef
+  // per-thread gather slots (independent of the x-line): element e = t * ni + j of the q x ni block
+  constexpr int FS = 6;  // q * n_i <= 6 * 512 (leaf_real_fits)
+  int fsrc[FS], fcol[FS];
+#pragma unroll
+  for (int f = 0; f < FS; ++f) {
+    const int e = tid + 512 * f;
+    fsrc[f] = e < q * ni ? e / ni : -1;
+    fcol[f] = e < q * ni ? pstep[e - (e / ni) * ni] : 0;
+  }
   auto fetch = [&](int k, double* dst) {
-    for (int e = tid; e < q * ni; e += 512) {
-      const int t = e / ni, j = e - t * ni;
-      cpa8(dst + e, Mg + (size_t)plist[k * q + t] * ni + pstep[j]);
-    }
+#pragma unroll
+    for (int f = 0; f < FS; ++f)
+      if (fsrc[f] >= 0) cpa8(dst + tid + 512 * f, Mg + (size_t)plist[k * q + fsrc[f]] * ni + fcol[f]);
     asm volatile("cp.async.commit_group;\n" ::);
   };
+  // per-thread line-sum slots of P: output e = t * nb + b
+  constexpr int PSL = 2;  // q * n_b <= 2 * 512 (leaf_real_fits)
+  int poff[PSL], pst[PSL], prow_[PSL], pcoef[PSL];
+#pragma unroll
+  for (int f = 0; f < PSL; ++f) {
+    const int e = tid + 512 * f;
+    const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
+    prow_[f] = e < q * nb ? t : -1;
+    if (edge == 0 || edge == 2) {  // S / N: y-line ix = kk, nodes iy*q + kk
+      pcoef[f] = 2 * q + (edge == 0 ? 0 : q);
+      poff[f] = t * ni + kk;
+      pst[f] = q;
+    } else {  // E / W: x-line iy = kk, nodes kk*q + ix
+      pcoef[f] = edge == 3 ? 0 : q;
+      poff[f] = t * ni + kk * q;
+      pst[f] = 1;
+    }
+  }
   fetch(0, Cr);
   for (int k = 0; k < q; ++k) {
     double* Ck = Cr + (k & 1) * q * ni;
@@ -461,27 +504,20 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
       asm volatile("cp.async.wait_group 0;\n" ::);
     }
     __syncthreads();
-    for (int e = tid; e < q * nb; e += 512) {
-      const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
-      const double* row = Ck + t * ni;
-      double s0 = 0.0, s1 = 0.0;
-      int off, st;
-      const double* co;
-      if (edge == 0 || edge == 2) {  // S / N: y-line ix = kk, nodes iy*q + kk
-        co = ay + (edge == 0 ? 0 : q);
-        off = kk;
-        st = q;
-      } else {  // E / W: x-line iy = kk, nodes kk*q + ix
-        co = ax + (edge == 3 ? 0 : q);
-        off = kk * q;
-        st = 1;
+#pragma unroll
+    for (int f = 0; f < PSL; ++f) {
+      if (prow_[f] >= 0) {
+        const double* row = Ck + poff[f];
+        const double* co = coef + pcoef[f];
+        const int st = pst[f];
+        double s0 = 0.0, s1 = 0.0;
+        for (int i = 0; i + 1 < q; i += 2) {
+          s0 = fma(row[i * st], co[i], s0);
+          s1 = fma(row[(i + 1) * st], co[i + 1], s1);
+        }
+        if (q & 1) s0 = fma(row[(q - 1) * st], co[q - 1], s0);
+        Ps[(k * q + prow_[f]) * L.PS + (tid + 512 * f) - prow_[f] * nb] = s0 + s1;
       }
-      for (int i = 0; i + 1 < q; i += 2) {
-        s0 = fma(row[off + i * st], co[i], s0);
-        s1 = fma(row[off + (i + 1) * st], co[i + 1], s1);
-      }
-      if (q & 1) s0 = fma(row[off + (q - 1) * st], co[q - 1], s0);
-      Ps[(k * q + t) * L.PS + b] = s0 + s1;
     }
     // Q rows W_k, E_k complete (x-line k); S/N rows accumulate (row k*q + ix is point k of y-line ix)
     for (int j = tid; j < ni; j += 512) {
@@ -773,6 +809,7 @@ size_t leaf_real_scratch_bytes(int p, int batch) {
 
 bool leaf_real_fits(int p) {
   if (p < 4 || 4 * (p - 2) > 64 || (p - 2) * (p - 2) > 256) return false;
+  if ((p - 2) * (p - 2) * (p - 2) > 6 * 512 || 4 * (p - 2) * (p - 2) > 2 * 512) return false;  // ops gather / line-sum slots
   const int q = p - 2, ni = q * q;
   const size_t smemA = sizeof(double) * ((size_t)((ni + 15) & ~15) * RL_NB + (size_t)RL_NB * rl_zs(ni));
   const size_t smemB = sizeof(double) * (size_t)RLeafSmem(p).total;
