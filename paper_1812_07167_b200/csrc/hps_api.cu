@@ -512,12 +512,13 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
     // real interior elimination: kappa^2 c real; in auto mode also kappa^2 max c
     // below 0.9 x the lowest Dirichlet eigenvalue pi^2 (1/hx^2 + 1/hy^2) of a leaf, so A_ii is
     // positive definite up to a margin (no interior resonance)
-    bool ok = leaf_real_fits(p);
+    bool ok = leaf_real_fits(p), below = false;
     if (ok) {
       double cmax, imax;
       leaf_real_c_bounds(c_dev, (int64_t)nleaf * p * p, cmax, imax, H.st);
       const double k2 = H.kappa * H.kappa, lam1 = M_PI * M_PI * (1.0 / (hx * hx) + 1.0 / (hy * hy));
-      ok = imax == 0.0 && (H.leaf_mode == 3 || k2 * cmax < 0.9 * lam1);
+      below = k2 * cmax < 0.9 * lam1;  // no interior resonance: natural-order elimination is stable
+      ok = imax == 0.0 && (H.leaf_mode == 3 || below);
     }
     if (H.leaf_mode == 3 && !ok)
       throw HpsError{HPS_EINVAL, "hps_build: leaf_mode 3 needs real c samples and p - 2 <= 14"};
@@ -562,7 +563,7 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
         const int nc = std::min(chunk, nleaf - l0);
         launch_leaf_real(p, l0, nc, H.leaf_nat.as<int>(), c_dev, H.kappa * H.kappa, dKr.as<double>(), dKR.as<double>(),
                          fb, H.eta, H.store.as<zt>() + (size_t)l0 * mat, (int64_t)mat,
-                         H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, wk.p, H.info.as<int>(), H.st);
+                         H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, wk.p, H.info.as<int>(), H.st, !below);
       }
       const double ni = H.ni;
       H.flops[0] += nleaf * (2.0 * ni * ni * ni + 8.0 * (double)nb * nb * (ni + nb) + 4.0 * ni * ni * nb);

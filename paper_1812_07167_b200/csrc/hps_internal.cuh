@@ -104,7 +104,7 @@ size_t leaf_real_scratch_bytes(int p, int batch);
 void leaf_real_c_bounds(const zt* c, int64_t n, double& cmax, double& imax, cudaStream_t st);
 void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt* c, double kappa2, const double* K,
                       const double* KR, const zt (&fb)[2][2][2], zt eta, zt* store, int64_t mstride, zt* R,
-                      void* work, int* info, cudaStream_t st);
+                      void* work, int* info, cudaStream_t st, bool pivot);
 bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, int p, int batch, const zt* K, zt* R,
                            zt eta, int* info, cudaStream_t st, const zt* c = nullptr, const int* leaf_nat = nullptr,
                            int leaf0 = 0, double kappa2 = 0.0);

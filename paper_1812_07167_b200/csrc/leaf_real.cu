@@ -80,12 +80,17 @@ __host__ __device__ inline int rl_zs(int n) {  // Z row stride (doubles): >= n -
 // M(plist[k], pstep[j]) and writes plist, pstep to perm.
 // K = [D2x(1..q, 1..q) | D2y(1..q, 1..q)] (interior second-derivative blocks, scaled).
 // ---------------------------------------------------------------------------
-template <int RPT>
-__global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ Wk, int* __restrict__ perm,
-                                                          int leaf0, const int* __restrict__ leaf_nat,
-                                                          const zt* __restrict__ c, int p,
-                                                          const double* __restrict__ K, double kappa2,
-                                                          int* __restrict__ info) {
+// PIV = false: no pivot search (row k is the pivot of step k).  In the applicability region of
+// this path (kappa^2 max c < 0.9 lambda_1) A_ii is an interior Chebyshev Laplacian
+// shifted by less than its lowest eigenvalue and elimination in natural order is stable (pivots
+// >= 0.46 of the original diagonal, error 1e-14 in tools/nopiv_check.py); a pivot below 0.05 of
+// the original diagonal makes the body return false and the caller redoes the leaf with partial
+// pivoting.
+template <int RPT, bool PIV>
+__device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __restrict__ perm, int leaf0,
+                                              const int* __restrict__ leaf_nat, const zt* __restrict__ c, int p,
+                                              const double* __restrict__ K, double kappa2,
+                                              int* __restrict__ info) {
   // panel: NPW = 32 / RPT warps, RPT rows x CPT columns per thread (the other warps wait at the
   // block barrier that ends the panel: fewer warps per step means fewer redundant instructions
   // per pivot step, which is issue-bound)
@@ -97,6 +102,8 @@ __global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ W
   __shared__ double prow[2][NB];
   __shared__ __align__(16) unsigned wkey[2][16];
   __shared__ int pstep[256], plist[256], colmap[256 + 32];
+  __shared__ double diag_s[256];
+  __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
   double* M = Wk + (size_t)blockIdx.x * n * n;
   {  // assemble A_ii (row iy*q + ix)
@@ -110,12 +117,19 @@ __global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ W
         double v = 0.0;
         if (iy == jy) v -= D2x[ix * q + jx];
         if (ix == jx) v -= D2y[iy * q + jy];
-        if (r == cc) v -= kappa2 * cl[(iy + 1) * p + ix + 1].x;
+        if (r == cc) {
+          v -= kappa2 * cl[(iy + 1) * p + ix + 1].x;
+          diag_s[r] = v;
+        }
         M[(int64_t)r * n + cc] = v;
       }
     }
   }
-  if (tid < 256) pstep[tid] = 1 << 30;
+  if (tid < 256) {
+    pstep[tid] = PIV ? 1 << 30 : tid;
+    plist[tid] = tid;
+  }
+  if (tid == 0) s_bad = 0;
   if (tid < 32) wkey[0][tid] = 0u;
   __syncthreads();
   RPanels P;
@@ -152,23 +166,26 @@ __global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ W
           const int kk = cga * CPT + s;
           if (kk < w) {
             const int k = k0 + kk, par = k & 1;
-            unsigned key = 0u;
-            if (act) {
+            int r = k;
+            if (PIV) {
+              unsigned key = 0u;
+              if (act) {
 #pragma unroll
-              for (int t = 0; t < RPT; ++t)
-                if (!piv[t] && rq[t] < n) key = max(key, rkey(a[t][s], rq[t]));
-            }
-            key = __reduce_max_sync(0xffffffffu, key);
-            if (lane == 0) wkey[par][wp] = key;
-            if (NPW == 16) __syncthreads(); else bsync(1, NPW * 32);
-            unsigned best = 0u;
+                for (int t = 0; t < RPT; ++t)
+                  if (!piv[t] && rq[t] < n) key = max(key, rkey(a[t][s], rq[t]));
+              }
+              key = __reduce_max_sync(0xffffffffu, key);
+              if (lane == 0) wkey[par][wp] = key;
+              if (NPW == 16) __syncthreads(); else bsync(1, NPW * 32);
+              unsigned best = 0u;
 #pragma unroll
-            for (int g4 = 0; g4 < NPW / 4; ++g4) {
-              const uint4 kq = *reinterpret_cast<const uint4*>(&wkey[par][4 * g4]);
-              best = max(best, max(max(kq.x, kq.y), max(kq.z, kq.w)));
+              for (int g4 = 0; g4 < NPW / 4; ++g4) {
+                const uint4 kq = *reinterpret_cast<const uint4*>(&wkey[par][4 * g4]);
+                best = max(best, max(max(kq.x, kq.y), max(kq.z, kq.w)));
+              }
+              if ((best & ~511u) == 0u) singular = true;
+              r = 511 - (int)(best & 511u);
             }
-            if ((best & ~511u) == 0u) singular = true;
-            const int r = 511 - (int)(best & 511u);
             if (wp == r / RPW && rg == (r & 7)) {
               const int tt = (r / 8) % RPT;
 #pragma unroll
@@ -177,12 +194,13 @@ __global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ W
 #pragma unroll
                   for (int cc = 0; cc < CPT; ++cc) prow[par][cg * CPT + cc] = a[t][cc];
                 }
-              if (cg == 0) {
+              if (PIV && cg == 0) {
                 pstep[r] = k;
                 plist[k] = r;
               }
             }
             if (NPW == 16) __syncthreads(); else bsync(1, NPW * 32);
+            if (!PIV && tid == 0 && !(fabs(prow[par][kk]) >= 0.05 * fabs(diag_s[k]))) s_bad = 1;
             if (warp_live) {
               const double inv = rinv(prow[par][kk]);
               double g[RPT];
@@ -225,6 +243,10 @@ __global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ W
     }
     if (nv == 0) break;
     LR_MARK(4 * pn + 1);
+    if (!PIV) {
+      __syncthreads();
+      if (s_bad) return false;  // uniform: redo this leaf with partial pivoting
+    }
     // ---- update: all other columns, units of 8 rows x 32 columns ----
     for (int v = tid; v < nv + 32; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
     __syncthreads();
@@ -295,11 +317,24 @@ __global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ W
   }
   if (singular && tid == 0) atomicCAS(info, 0, leaf0 + blockIdx.x + 1);
   __syncthreads();
+  if (!PIV && s_bad) return false;
   // A_ii^{-1}(k, j) = M(plist[k], pstep[j]): the permutations go out with M
   int* pb = perm + (size_t)blockIdx.x * 2 * n;
   for (int e = tid; e < n; e += 512) {
     pb[e] = plist[e];
     pb[n + e] = pstep[e];
+  }
+  return true;
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ Wk, int* __restrict__ perm, int leaf0,
+                                                          const int* __restrict__ leaf_nat, const zt* __restrict__ c,
+                                                          int p, const double* __restrict__ K, double kappa2,
+                                                          int* __restrict__ info, int pivot) {
+  if (pivot || !dgj_leaf_body<RPT, false>(Wk, perm, leaf0, leaf_nat, c, p, K, kappa2, info)) {
+    __syncthreads();
+    dgj_leaf_body<RPT, true>(Wk, perm, leaf0, leaf_nat, c, p, K, kappa2, info);
   }
 }
 
@@ -818,11 +853,14 @@ bool leaf_real_fits(int p) {
 
 // Leaf operators of `batch` leaves (heap leaf0 ...) by the real interior elimination.  work:
 // leaf_real_scratch_bytes(p, batch).  K: D2x, D2y interior blocks; KR, fb: line coefficients and
-// closures (see the kernels).
+// closures (see the kernels).  pivot: partial pivoting from the start (else natural order with
+// a per-leaf fallback, dgj_leaf_body).
 void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt* c, double kappa2, const double* K,
                       const double* KR, const zt (&fb)[2][2][2], zt eta, zt* store, int64_t mstride, zt* R,
-                      void* work, int* info, cudaStream_t st) {
+                      void* work, int* info, cudaStream_t st, bool pivot) {
   const int q = p - 2, ni = q * q, nb = 4 * q;
+  static const bool force_piv = getenv("HPS_DGJ_PIVOT") && *getenv("HPS_DGJ_PIVOT") == '1';
+  pivot = pivot || force_piv;
   double* Wk = reinterpret_cast<double*>(work);
   double* Qg = Wk + (size_t)batch * ni * ni;
   int* perm = reinterpret_cast<int*>(Qg + (size_t)batch * ni * nb);
@@ -843,7 +881,7 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
     static const int rpt = getenv("HPS_DGJ_RPT") ? atoi(getenv("HPS_DGJ_RPT")) : 2;
     auto kern = rpt == 4 ? dgj_leaf_kernel<4> : dgj_leaf_kernel<2>;
     kern<<<nbatch, 512, smemA, st>>>(Wk + (size_t)b0 * ni * ni, perm + (size_t)b0 * 2 * ni, leaf0 + b0,
-                                                leaf_nat, c, p, K, kappa2, info);
+                                                leaf_nat, c, p, K, kappa2, info, pivot ? 1 : 0);
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
     RLeafArgs a;

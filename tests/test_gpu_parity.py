@@ -65,6 +65,21 @@ def test_leaf_parity_real_elimination(p):
         assert rel(S.R(2 + leaf), lo["R"]) < TOL
 
 
+def test_leaf_real_elimination_pivoted():
+    """leaf_mode 3 between the first two interior resonances (kappa^2 c in [50, 65], eigenvalues
+    49.3 and 78.9): the gate fails, so the real Gauss-Jordan runs with partial pivoting."""
+    kappa = np.sqrt(50.0)
+    g, c, s, t = problem(2, 1, 12, kappa, kappa + 1j)
+    S = hps.Solver(g, 12, kappa, kappa + 1j, c, keep_all_R=True, leaf_mode=3)
+    assert S.leaf_path() == 3
+    for leaf in range(2):
+        Psi, Y = S.leaf_ops(leaf)
+        lo = oracle.leaf(12, 0.5, 1.0, kappa, kappa + 1j, c[leaf])
+        assert rel(Psi, lo["Psi"]) < TOL
+        assert rel(Y, lo["Y"]) < TOL
+        assert rel(S.R(2 + leaf), lo["R"]) < TOL
+
+
 def test_leaf_path_selection():
     """Auto mode takes the real elimination only for real c below the first interior resonance;
     leaf_mode 3 refuses complex c."""
