@@ -80,6 +80,30 @@ def test_leaf_real_elimination_pivoted():
         assert rel(S.R(2 + leaf), lo["R"]) < TOL
 
 
+def test_leaf_real_elimination_forced_pivoting():
+    """HPS_DGJ_PIVOT=1 (fresh process): both real eliminations (A_ii and Sigma) with partial
+    pivoting from the first step, the fallback the natural-order path takes on a small pivot."""
+    import os, subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import os, sys
+        sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+        import numpy as np, oracle
+        from paper_1812_07167_b200 import hps
+        from test_gpu_parity import problem, rel
+        g, c, s, t = problem(2, 1, 16, 4.0, 4.0 + 1j)
+        S = hps.Solver(g, 16, 4.0, 4.0 + 1j, c, keep_all_R=True, leaf_mode=3)
+        Psi, Y = S.leaf_ops(1)
+        lo = oracle.leaf(16, 0.5, 1.0, 4.0, 4.0 + 1j, c[1])
+        print(max(rel(Psi, lo["Psi"]), rel(Y, lo["Y"]), rel(S.R(3), lo["R"])))
+    """)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HPS_DGJ_PIVOT="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) < TOL
+
+
 def test_leaf_path_selection():
     """Auto mode takes the real elimination only for real c below the first interior resonance;
     leaf_mode 3 refuses complex c."""
