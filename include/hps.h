@@ -82,6 +82,14 @@ typedef struct {
                            Sigma = F_b - F_i A_ii^{-1} A_ib (eq. 7 rows reordered); needs real
                            c samples and p - 2 <= 14 (else HPS_EINVAL), no resonance check.
                            Other values: HPS_EINVAL */
+  int32_t boundary_basis; /* root boundary data t of hps_solve / hps_solve_top sampled at
+                           0 (default): the q = p - 2 corner-free Chebyshev-Lobatto nodes of each
+                             leaf edge (hps_root_boundary_nodes; the paper's scheme);
+                           1: the q Gauss-Legendre nodes of each leaf edge (hps_boundary_nodes_gl,
+                             same segment order): the library
+                             interpolates each segment's degree-(q-1) polynomial to its Chebyshev
+                             nodes.  u is always returned at the Chebyshev leaf nodes.
+                           Other values: HPS_EINVAL */
 } hps_opts;
 
 /* Precomputation stage (Algorithm 1).
@@ -152,6 +160,11 @@ int hps_export_leaf(const hps_handle* h, int64_t leaf, hps_c128* psi, hps_c128* 
 /* Sizes: n_b of a box (heap id), number of boxes, leaf depth. Returns -1 on a bad id. */
 int64_t hps_box_nb(const hps_handle* h, int64_t box);
 int64_t hps_num_boxes(const hps_handle* h);
+
+/* Gauss-Legendre root boundary nodes (boundary_basis 1): the q = p - 2 Gauss-Legendre nodes of
+ * every leaf-edge segment, canonical order [S, E, N, W], increasing coordinate within an edge;
+ * x, y, nx, ny as for hps_root_boundary_nodes (2 (nx + ny) q entries each, host memory). */
+int hps_boundary_nodes_gl(const hps_grid* g, int p, double* x, double* y, double* nx, double* ny);
 
 /* Tensor-node coordinates of every leaf, [nx*ny][p*p] (x fastest), and the root boundary
  * nodes with their outward unit normals, [2(nx+ny)(p-2)] in [S,E,N,W] order.  Host pointers.

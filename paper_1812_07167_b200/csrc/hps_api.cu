@@ -230,6 +230,8 @@ struct hps_handle {
                       // 3: real interior elimination
   bool leaf_fused = true;
   int leaf_path = -1;  // the path build_leaves took (leaf_mode values; 0 = complex Schur, fused)
+  bool gl = false;     // root boundary data given at Gauss-Legendre nodes (hps_opts.boundary_basis 1)
+  DevBuf PglT;         // [q][q] transpose of the GL -> Chebyshev segment interpolation (gl only)
   std::vector<Depth> depth;
   std::vector<int> leaf_nat_h, nat_to_heap_h;
   DevBuf leaf_nat, nat_to_heap;
@@ -249,6 +251,7 @@ struct hps_handle {
     leaf_nat.release();
     nat_to_heap.release();
     store.release();
+    PglT.release();
     for (auto& m : lev) {
       m.maps.release();
       m.ops.release();
@@ -954,6 +957,10 @@ struct LaunchScope {
 // ===========================================================================
 // C-ABI
 // ===========================================================================
+namespace {
+std::vector<double> gl_nodes(int q);  // Gauss-Legendre nodes (defined with the handle set-up)
+}  // namespace
+
 extern "C" {
 
 const char* hps_last_error(void) { return g_err_msg.c_str(); }
@@ -975,6 +982,32 @@ int hps_leaf_nodes(const hps_grid* g, int p, double* x, double* y) {
           y[base + iy * p + ix] = g->y0 + ly * hy + (1.0 + xi[iy]) * 0.5 * hy;
         }
     }
+  return HPS_OK;
+}
+
+int hps_boundary_nodes_gl(const hps_grid* g, int p, double* x, double* y, double* nx, double* ny) {
+  if (!g || p < 4 || g->nx < 1 || g->ny < 1 || !x || !y || !nx || !ny) {
+    hps_set_error("hps_boundary_nodes_gl: invalid argument");
+    return HPS_EINVAL;
+  }
+  const std::vector<double> xi = gl_nodes(p - 2);
+  const double hx = (g->x1 - g->x0) / g->nx, hy = (g->y1 - g->y0) / g->ny;
+  size_t o = 0;
+  auto push = [&](double px, double py, double vx, double vy) {
+    x[o] = px;
+    y[o] = py;
+    nx[o] = vx;
+    ny[o] = vy;
+    ++o;
+  };
+  for (int l = 0; l < g->nx; ++l)
+    for (double z : xi) push(g->x0 + l * hx + (1 + z) * 0.5 * hx, g->y0, 0, -1);  // S
+  for (int l = 0; l < g->ny; ++l)
+    for (double z : xi) push(g->x1, g->y0 + l * hy + (1 + z) * 0.5 * hy, 1, 0);   // E
+  for (int l = 0; l < g->nx; ++l)
+    for (double z : xi) push(g->x0 + l * hx + (1 + z) * 0.5 * hx, g->y1, 0, 1);   // N
+  for (int l = 0; l < g->ny; ++l)
+    for (double z : xi) push(g->x0, g->y0 + l * hy + (1 + z) * 0.5 * hy, -1, 0);  // W
   return HPS_OK;
 }
 
@@ -1026,6 +1059,67 @@ int validate_problem(const hps_grid* g, int p, int q, double kappa, hps_c128 eta
   return HPS_OK;
 }
 
+// Gauss-Legendre nodes on [-1, 1], ascending: Newton iteration on P_q (three-term recurrence)
+// from the Tricomi initial guesses (the oracle uses Golub-Welsch instead).
+std::vector<double> gl_nodes(int q) {
+  std::vector<double> x(q);
+  for (int i = 0; i < q; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (q + 0.5));
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = z;  // P_0, P_1
+      for (int k = 2; k <= q; ++k) {
+        const double p2 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      const double pq = q == 1 ? z : p1, pq1 = q == 1 ? 1.0 : p0;  // P_q, P_{q-1}
+      const double dp = q * (z * pq - pq1) / (z * z - 1.0);
+      const double dz = pq / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    x[i] = z;
+  }
+  std::sort(x.begin(), x.end());
+  return x;
+}
+
+// P[j][g] = l_g(x_j): the degree-(q-1) interpolant of segment samples at the Gauss-Legendre
+// nodes xi, evaluated at the q interior Chebyshev-Lobatto nodes x_j of the segment.
+std::vector<double> gl_to_cheb_matrix(int p) {
+  const int q = p - 2;
+  const std::vector<double> xi = gl_nodes(q);
+  std::vector<double> P((size_t)q * q);
+  for (int j = 0; j < q; ++j) {
+    const double xj = -std::cos(M_PI * (j + 1) / (p - 1));
+    for (int g = 0; g < q; ++g) {
+      double l = 1.0;
+      for (int m = 0; m < q; ++m)
+        if (m != g) l *= (xj - xi[m]) / (xi[g] - xi[m]);
+      P[(size_t)j * q + g] = l;
+    }
+  }
+  return P;
+}
+
+// t at the Gauss-Legendre nodes -> t at the Chebyshev nodes, per leaf-edge segment of q nodes:
+// one batched product [nrhs * nseg][q] x P^T on the device.
+void t_gl_to_cheb(hps_handle& H, int nrhs, const zt* t_gl, DevBuf& out) {
+  const int q = H.q, nseg = H.depth[0].nb / q;
+  out.alloc(sizeof(zt) * (size_t)nrhs * H.depth[0].nb);
+  ZGemm gm;
+  gm.M = nrhs * nseg;
+  gm.N = q;
+  gm.K = q;
+  gm.A.ptr = t_gl;
+  gm.A.rs = q;
+  gm.B.ptr = H.PglT.as<zt>();
+  gm.B.rs = q;
+  gm.C.ptr = out.as<zt>();
+  gm.C.rs = q;
+  zgemm(gm, H.st);
+}
+
 // Common handle set-up: stream, plan, maps, per-level operator stores.
 void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_opts* opt) {
   if (opt && opt->device >= 0) HPS_CUDA_CHECK(cudaSetDevice(opt->device));
@@ -1047,6 +1141,14 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   H.leaf_mode = opt ? opt->leaf_mode : 0;
   H.leaf_fused = H.leaf_mode == 0;
   H.prof.timing = opt ? (unsigned)opt->profile : 0u;
+  H.gl = opt && opt->boundary_basis == 1;
+  if (H.gl) {
+    const std::vector<double> P = gl_to_cheb_matrix(p);
+    std::vector<zt> PT((size_t)q * q);
+    for (int j = 0; j < q; ++j)
+      for (int g = 0; g < q; ++g) PT[(size_t)g * q + j] = make_double2(P[(size_t)j * q + g], 0.0);
+    upload(H.PglT, PT, H.st);
+  }
 }
 
 void plan_all(hps_handle& H, int Lb) {
@@ -1135,6 +1237,10 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     return HPS_EINVAL;
   }
   if (int rc = validate_problem(g, p, q, kappa, eta, "hps_build")) return rc;
+  if (opt && (opt->boundary_basis < 0 || opt->boundary_basis > 1)) {
+    hps_set_error("hps_build: boundary_basis must be 0 (Chebyshev) or 1 (Gauss-Legendre)");
+    return HPS_EINVAL;
+  }
   if (opt && (opt->leaf_mode < 0 || opt->leaf_mode > 3)) {
     hps_set_error("hps_build: leaf_mode must be 0, 1, 2 or 3");
     return HPS_EINVAL;
@@ -1213,6 +1319,11 @@ int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps
     DevBuf sd, td;
     const zt* s_dev = dev_in(s, sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni, sd, h->st);
     const zt* t_dev = dev_in(t, sizeof(zt) * (size_t)nrhs * h->depth[0].nb, td, h->st);
+    DevBuf tc;
+    if (h->gl) {
+      t_gl_to_cheb(*h, nrhs, t_dev, tc);
+      t_dev = tc.as<zt>();
+    }
     DevOut uo(u, sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt, h->st);
     HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
     solve_up_impl(*h, nrhs, s_dev, nullptr);
@@ -1292,6 +1403,11 @@ int hps_solve_top(hps_handle* h, int nrhs, const hps_c128* h_sub, const hps_c128
     DevBuf hd, td;
     const zt* h_dev = dev_in(h_sub, sizeof(zt) * nbot * nrhs * nbb, hd, h->st);
     const zt* t_dev = dev_in(t_root, sizeof(zt) * (size_t)nrhs * h->depth[0].nb, td, h->st);
+    DevBuf tc;
+    if (h->gl) {
+      t_gl_to_cheb(*h, nrhs, t_dev, tc);
+      t_dev = tc.as<zt>();
+    }
     DevOut to(t_sub, sizeof(zt) * nbot * nrhs * nbb, h->st);
     HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
     solve_up_impl(*h, nrhs, h_dev, nullptr);

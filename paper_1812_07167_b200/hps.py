@@ -33,11 +33,12 @@ class hps_c128(C.Structure):
 
 class hps_opts(C.Structure):
     _fields_ = [("keep_root_R", C.c_int32), ("keep_all_R", C.c_int32), ("device", C.c_int32),
-                ("leaf_chunk", C.c_int32), ("profile", C.c_int32), ("leaf_mode", C.c_int32)]
+                ("leaf_chunk", C.c_int32), ("profile", C.c_int32), ("leaf_mode", C.c_int32),
+                ("boundary_basis", C.c_int32)]
 
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
-           "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_last_time_ms", "hps_last_launches",
+           "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_last_time_ms", "hps_last_launches",
            "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free",
            "hps_last_error"]
@@ -64,6 +65,7 @@ def lib():
         L.hps_num_boxes.restype = i64
         L.hps_leaf_nodes.argtypes = [C.POINTER(hps_grid), i32, dp, dp]
         L.hps_root_boundary_nodes.argtypes = [C.POINTER(hps_grid), i32, dp, dp, dp, dp]
+        L.hps_boundary_nodes_gl.argtypes = [C.POINTER(hps_grid), i32, dp, dp, dp, dp]
         L.hps_last_time_ms.argtypes = [vp, i32]
         L.hps_last_time_ms.restype = C.c_double
         L.hps_last_launches.argtypes = [vp, i32]
@@ -133,11 +135,12 @@ def leaf_nodes(g, p):
     return X, Y
 
 
-def root_boundary_nodes(g, p):
+def root_boundary_nodes(g, p, basis=0):
+    """Root boundary nodes and outward normals; basis 1: Gauss-Legendre nodes per leaf edge."""
     n = 2 * (g.nx + g.ny) * (p - 2)
     X, Y, NX, NY = (np.zeros(n) for _ in range(4))
-    _check(lib().hps_root_boundary_nodes(C.byref(g), p, X.ctypes.data, Y.ctypes.data, NX.ctypes.data,
-                                         NY.ctypes.data))
+    fn = lib().hps_boundary_nodes_gl if basis == 1 else lib().hps_root_boundary_nodes
+    _check(fn(C.byref(g), p, X.ctypes.data, Y.ctypes.data, NX.ctypes.data, NY.ctypes.data))
     return X, Y, NX, NY
 
 
@@ -242,13 +245,14 @@ class Solver:
     """hps_build on construction; solve() is hps_solve."""
 
     def __init__(self, g, p, kappa, eta, c, keep_root_R=True, keep_all_R=False, device=-1, leaf_chunk=0,
-                 profile=False, leaf_mode=0):
+                 profile=False, leaf_mode=0, boundary_basis=0):
         self.g, self.p = g, p
         self.nleaf = g.nx * g.ny
         self.q, self.nt, self.ni = p - 2, p * p - 4, (p - 2) ** 2
         self.nb_root = 2 * (g.nx + g.ny) * (p - 2)
         mask = -1 if profile is True else int(profile)
-        opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk), mask, int(leaf_mode))
+        opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk), mask, int(leaf_mode),
+                        int(boundary_basis))
         eta = complex(eta)
         h = C.c_void_p()
         cp = _ptr(c, self.nleaf * p * p, "c_samples")
@@ -345,13 +349,14 @@ class Solver:
 class TopSolver:
     """hps_build_top: the merge tree above `depth` from the gathered subtree-root operators."""
 
-    def __init__(self, g, p, kappa, eta, depth, R_sub, keep_root_R=True, device=-1, profile=False):
+    def __init__(self, g, p, kappa, eta, depth, R_sub, keep_root_R=True, device=-1, profile=False, boundary_basis=0):
         self.g, self.p, self.depth = g, p, depth
         sub, _, _ = subtree_grid(g, depth, 0)
         self.nb_sub = nb_of(sub, p)
         self.nb_root = nb_of(g, p)
         self.nsub = 1 << depth
-        opts = hps_opts(int(keep_root_R), 0, int(device), 0, -1 if profile is True else int(profile), 0)
+        opts = hps_opts(int(keep_root_R), 0, int(device), 0, -1 if profile is True else int(profile), 0,
+                        int(boundary_basis))
         eta = complex(eta)
         h = C.c_void_p()
         _check(lib().hps_build_top(C.byref(g), p, p - 2, float(kappa), hps_c128(eta.real, eta.imag), depth,

@@ -39,6 +39,17 @@ def test_geometry_matches_oracle(L, orc, nx, ny, p):
         assert np.max(np.abs(u - v)) < 1e-15
 
 
+@pytest.mark.parametrize("nx,ny,p", [(1, 1, 4), (2, 4, 8), (4, 2, 16)])
+def test_gl_boundary_nodes_match_oracle(L, orc, nx, ny, p):
+    """hps_boundary_nodes_gl (Newton on P_q) vs oracle.gl (Golub-Welsch), boundary_basis 1."""
+    from oracle import gl
+    g = hps.grid(0.1, 0.9, -0.3, 0.5, nx, ny)
+    b = hps.root_boundary_nodes(g, p, basis=1)
+    bo = gl.root_boundary_gl(0.1, 0.9, -0.3, 0.5, nx, ny, p)
+    for u, v in zip(b, bo):
+        assert np.max(np.abs(u - v)) < 1e-14
+
+
 def _build_rc(L, **kw):
     args = dict(g=hps.grid(0, 1, 0, 1, 2, 2), p=8, q=6, kappa=1.0, eta=hps.hps_c128(1.0, 0.0))
     args.update(kw)

@@ -174,6 +174,34 @@ def test_config1_plane_wave():
     assert np.max(np.abs(u[0][:, 4 * (cfg.p - 2):] - exact_i)) < 1e-4
 
 
+@pytest.mark.parametrize("nx,ny,p", [(2, 2, 8), (4, 2, 12)])
+def test_gl_boundary_basis_parity(nx, ny, p):
+    """boundary_basis 1: t given at the Gauss-Legendre nodes; u equals the
+    oracle's Chebyshev-basis solve of the oracle's own per-segment interpolation of t."""
+    from oracle import gl
+    kappa, eta = 9.0, 9.0 - 2j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx)
+    S = hps.Solver(g, p, kappa, eta, c, boundary_basis=1)
+    u = S.solve(s, t)
+    O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c)
+    assert rel(u, O.solve(s, gl.t_to_cheb(p, t))) < TOL
+    # the same data in the Chebyshev basis gives a different (correctly interpolated) problem
+    assert rel(hps.Solver(g, p, kappa, eta, c).solve(s, t), u) > 1e-6
+
+
+def test_gl_boundary_basis_plane_wave():
+    """Plane wave with Robin data sampled at the Gauss-Legendre nodes: same accuracy as at the
+    Chebyshev nodes (C1 geometry and discretisation)."""
+    cfg = inputs.CONFIGS[1]
+    g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
+    X, Y = hps.leaf_nodes(g, cfg.p)
+    c, s, t = inputs.make_inputs(cfg, X, Y, *hps.root_boundary_nodes(g, cfg.p, basis=1))
+    u = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c, boundary_basis=1).solve(s, t)
+    Xi, Yi = inputs.interior_of(cfg.p, X), inputs.interior_of(cfg.p, Y)
+    exact_i = inputs.plane_wave(cfg.kappa, cfg.theta, Xi, Yi)
+    assert np.max(np.abs(u[0][:, 4 * (cfg.p - 2):] - exact_i)) < 1e-4
+
+
 def test_torch_device_buffers():
     import torch
     g, c, s, t = problem(4, 2, 8, 5.0, 5.0)
