@@ -137,9 +137,10 @@ def _stack(xs):
 # Backend: the CUDA library (product path)
 # ---------------------------------------------------------------------------
 class CudaBackend:
-    def __init__(self, device=-1, profile=False):
+    def __init__(self, device=-1, profile=False, boundary_basis=0):
         self.device = device
         self.profile = profile
+        self.boundary_basis = boundary_basis  # 1: root t at Gauss-Legendre nodes (hps_solve_top converts)
 
     def build_subtree(self, g_sub, p, kappa, eta, c_local):
         return hps.Solver(g_sub, p, kappa, eta, c_local, keep_root_R=True, device=self.device, profile=self.profile)
@@ -151,7 +152,8 @@ class CudaBackend:
         return out
 
     def build_top(self, g, p, kappa, eta, depth, R_all):
-        return hps.TopSolver(g, p, kappa, eta, depth, R_all, device=self.device, profile=self.profile)
+        return hps.TopSolver(g, p, kappa, eta, depth, R_all, device=self.device, profile=self.profile,
+                             boundary_basis=self.boundary_basis)
 
     def solve_up(self, sub, s_local, nrhs, like):
         return sub.solve_up(s_local, nrhs, hps._empty_like_ref(like, (nrhs, sub.nb_root)))

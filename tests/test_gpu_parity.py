@@ -202,6 +202,28 @@ def test_gl_boundary_basis_plane_wave():
     assert np.max(np.abs(u[0][:, 4 * (cfg.p - 2):] - exact_i)) < 1e-4
 
 
+def test_gl_boundary_basis_sharded():
+    """Gauss-Legendre root data through the subtree-sharded path (hps_solve_top converts it):
+    2 virtual ranks equal the single-handle GL solve."""
+    import torch
+    from paper_1812_07167_b200 import dist
+    kappa, eta, nx, ny, p = 11.0, 11.0 + 2j, 4, 4, 8
+    g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=2)
+    u_ref = hps.Solver(g, p, kappa, eta, c, boundary_basis=1).solve(s, t)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+    def rank_fn(comm):
+        sub, i0, j0 = dist.local_block(g, comm.world, comm.rank)
+        D = dist.DistributedHPS(comm, dist.CudaBackend(boundary_basis=1), g, p, kappa, eta,
+                                d(dist.slice_leaves(c, g, sub, i0, j0)))
+        u = D.solve(d(dist.slice_leaves(s, g, sub, i0, j0)), d(t)).cpu().numpy()
+        D.close()
+        return u, (sub, i0, j0)
+
+    for u, (sub, i0, j0) in dist.run_threads(2, rank_fn):
+        assert rel(u, dist.slice_leaves(u_ref, g, sub, i0, j0)) < 1e-11
+
+
 def test_torch_device_buffers():
     import torch
     g, c, s, t = problem(4, 2, 8, 5.0, 5.0)
