@@ -829,14 +829,26 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
   LR_MARK(45);
   // ---- phase 4: W = Sigma^{-1} Q by column chunks; Y_b = -W, Y_i = A_ii^{-1} + P W ----
   const int JB = L.JB;
-  for (int j0 = 0; j0 < ni; j0 += JB) {
+  // Q chunks by cp.async: chunk c + 1 is fetched while Y_i of chunk c is formed (Qb is free once
+  // W of chunk c is in Wb)
+  auto fetch_q = [&](int j0) {
     const int jw = min(JB, ni - j0);
-    __syncthreads();  // previous chunk's Qb / Wb consumed
     for (int e = tid; e < nb * JB; e += 512) {
       const int b = e / JB, j = e - b * JB;
-      Qb[b * L.QL + j] = j < jw ? __ldcg(Qg + (size_t)b * ni + j0 + j) : 0.0;
+      if (j < jw)
+        cpa8(Qb + b * L.QL + j, Qg + (size_t)b * ni + j0 + j);
+      else
+        Qb[b * L.QL + j] = 0.0;
     }
-    __syncthreads();
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  __syncthreads();  // Qg complete (phase 1) and Qb / Wb region free
+  fetch_q(0);
+  for (int j0 = 0; j0 < ni; j0 += JB) {
+    const int jw = min(JB, ni - j0);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();  // Q chunk staged; previous chunk's Wb consumed
+    if (j0 == 0) LR_MARK(47);
     // rows 0..nb-1: Re Sigma^{-1} Q, rows nb..2nb-1: Im (A(row, k) = Sg[(row mod nb) SL + 2k + part])
     blk_mma(
         (2 * nb) >> 3, JB, K4,
@@ -847,6 +859,8 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
           Wb[b * L.WL + 2 * c + 2 + part] = a1;
         });
     __syncthreads();
+    if (j0 == 0) LR_MARK(48);
+    if (j0 + JB < ni) fetch_q(j0 + JB);
     for (int e = tid; e < nb * jw; e += 512) {
       const int b = e / jw, j = e - b * jw;
       __stcs(&base[(int64_t)b * nt + nb + j0 + j], make_double2(-Wb[b * L.WL + 2 * j], -Wb[b * L.WL + 2 * j + 1]));
@@ -860,6 +874,7 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
         [&](int r, int c, double a0, double a1) {
           if (r < ni) __stcs(&base[(int64_t)(nb + r) * nt + nb + j0 + (c >> 1)], make_double2(a0, a1));
         });
+    if (j0 == 0) LR_MARK(49);
   }  LR_MARK(46);
 }
 
@@ -986,8 +1001,10 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
     HPS_CUDA_CHECK(cudaMemcpyFromSymbol(t, g_lr_trace, sizeof(t)));
     fprintf(stderr, "[leaf_real] dgj CTA0 (kclk from start): ");
     for (int i = 0; i < 28; ++i) fprintf(stderr, "%s%.1f", i % 4 ? " " : " | ", (t[i] - t[0]) / 1e3);
-    fprintf(stderr, "\n[leaf_real] ops CTA0 phases (kclk): p1 %.1f  sigma %.1f  gj %.1f  perm %.1f  psi %.1f  p4 %.1f\n",
+    fprintf(stderr, "\n[leaf_real] ops CTA0 phases (kclk): p1 %.1f  sigma %.1f  gj %.1f  perm %.1f  psi %.1f  p4 %.1f"
+            "  (chunk 0: q %.1f  W %.1f  Y %.1f)\n",
             (t[41] - t[40]) / 1e3, (t[42] - t[41]) / 1e3, (t[43] - t[42]) / 1e3, (t[44] - t[43]) / 1e3,
-            (t[45] - t[44]) / 1e3, (t[46] - t[45]) / 1e3);
+            (t[45] - t[44]) / 1e3, (t[46] - t[45]) / 1e3, (t[47] - t[45]) / 1e3, (t[48] - t[47]) / 1e3,
+            (t[49] - t[48]) / 1e3);
   }
 }
