@@ -402,57 +402,85 @@ struct RLeafSmem {  // offsets in doubles
 // (element k at arow(r)[k * astep]); B row-major with stride ldb.  pre(r, c, a0, a1) loads addends
 // for the accumulator pair (columns c, c + 1) before the product (their latency hides behind
 // it); store(r, c, a0, a1) consumes A B + addends (r < MT*8, c < N).
-template <typename ARow, typename Pre, typename Store>
+template <int MI = 1, bool FULL = false, typename ARow, typename Pre, typename Store>
 __device__ __forceinline__ void blk_mma(int MT, int N, int K4, ARow arow, int astep, const double* B, int ldb,
                                         Pre pre, Store store) {
+  // FULL: B is readable (finite or not) up to the next multiple of 32 columns, so every unit runs
+  // the unpredicated 4-tile loop (predicated mma.sync costs a WARPSYNC per instruction); the
+  // padding columns are computed and dropped
+  // units of (8 MI) rows x 32 columns: MI row tiles share every B fragment (4 MI accumulators)
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const int NU = (N + 31) >> 5, NUNIT = MT * NU;
-  double adn[4][2];
+  const int MU = (MT + MI - 1) / MI, NU = (N + 31) >> 5, NUNIT = MU * NU;
+  double adn[MI][4][2];
   auto load_pre = [&](int u) {
-    const int mt = u % MT, n0 = (u / MT) * 32, r = mt * 8 + (lane >> 2);
+    const int mu = u % MU, n0 = (u / MU) * 32;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int c = n0 + t * 8 + (lane & 3) * 2;
-      if (c < N)
-        pre(r, c, adn[t][0], adn[t][1]);
-      else
-        adn[t][0] = adn[t][1] = 0.0;
+    for (int m = 0; m < MI; ++m) {
+      const int r = (mu * MI + m) * 8 + (lane >> 2);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c = n0 + t * 8 + (lane & 3) * 2;
+        if (c < N && mu * MI + m < MT)
+          pre(r, c, adn[m][t][0], adn[m][t][1]);
+        else
+          adn[m][t][0] = adn[m][t][1] = 0.0;
+      }
     }
   };
   if (wp < NUNIT) load_pre(wp);
   for (int u = wp; u < NUNIT; u += 16) {
-    const int mt = u % MT, n0 = (u / MT) * 32;
-    const int r = mt * 8 + (lane >> 2);
-    const int ntile = min(4, (N - n0 + 7) >> 3);
-    double acc[4][2], ad[4][2];
+    const int mu = u % MU, n0 = (u / MU) * 32;
+    const int ntile = FULL ? 4 : min(4, (N - n0 + 7) >> 3);
+    double acc[MI][4][2], ad[MI][4][2];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      ad[t][0] = adn[t][0];
-      ad[t][1] = adn[t][1];
-      acc[t][0] = acc[t][1] = 0.0;
-    }
+    for (int m = 0; m < MI; ++m)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        ad[m][t][0] = adn[m][t][0];
+        ad[m][t][1] = adn[m][t][1];
+        acc[m][t][0] = acc[m][t][1] = 0.0;
+      }
     if (u + 16 < NUNIT) load_pre(u + 16);  // the next unit's addends are in flight during this one
-    const double* ap = arow(mt * 8 + (lane >> 2)) + (lane & 3) * astep;
+    const double* ap[MI];
+#pragma unroll
+    for (int m = 0; m < MI; ++m) ap[m] = arow((mu * MI + m) * 8 + (lane >> 2)) + (lane & 3) * astep;
     const double* bp = B + (lane & 3) * ldb + n0 + (lane >> 2);
     if (ntile == 4) {
 #pragma unroll 2
       for (int k4 = 0; k4 < K4; ++k4) {
-        const double av = ap[k4 * 4 * astep];
+        double bv[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) dmma884r(acc[t][0], acc[t][1], av, bp[k4 * 4 * ldb + t * 8]);
+        for (int t = 0; t < 4; ++t) bv[t] = bp[k4 * 4 * ldb + t * 8];
+#pragma unroll
+        for (int m = 0; m < MI; ++m) {
+          const double av = ap[m][k4 * 4 * astep];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) dmma884r(acc[m][t][0], acc[m][t][1], av, bv[t]);
+        }
       }
     } else {
       for (int k4 = 0; k4 < K4; ++k4) {
-        const double av = ap[k4 * 4 * astep];
+        double bv[4];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (t < ntile) dmma884r(acc[t][0], acc[t][1], av, bp[k4 * 4 * ldb + t * 8]);
+        for (int t = 0; t < 4; ++t) bv[t] = t < ntile ? bp[k4 * 4 * ldb + t * 8] : 0.0;
+#pragma unroll
+        for (int m = 0; m < MI; ++m) {
+          const double av = ap[m][k4 * 4 * astep];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (t < ntile) dmma884r(acc[m][t][0], acc[m][t][1], av, bv[t]);
+        }
       }
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int c = n0 + t * 8 + (lane & 3) * 2;
-      if (t < ntile && c < N) store(r, c, acc[t][0] + ad[t][0], acc[t][1] + ad[t][1]);
+    for (int m = 0; m < MI; ++m) {
+      if (mu * MI + m >= MT) continue;
+      const int r = (mu * MI + m) * 8 + (lane >> 2);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c = n0 + t * 8 + (lane & 3) * 2;
+        if (t < ntile && c < N) store(r, c, acc[m][t][0] + ad[m][t][0], acc[m][t][1] + ad[m][t][1]);
+      }
     }
   }
 }
@@ -821,7 +849,7 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
   }
   const int MTi = L.mtr >> 3, K4 = nb >> 2;
   auto nopre = [](int, int, double& a0, double& a1) { a0 = a1 = 0.0; };
-  blk_mma(
+  blk_mma<1, true>(
       MTi, 2 * nb, K4, [&](int r) { return Ps + r * L.PS; }, 1, Sg, L.SL, nopre,
       [&](int r, int c, double a0, double a1) {
         if (r < ni) __stcs(&base[(int64_t)(nb + r) * nt + (c >> 1)], make_double2(-a0, -a1));
@@ -865,7 +893,7 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
       const int b = e / jw, j = e - b * jw;
       __stcs(&base[(int64_t)b * nt + nb + j0 + j], make_double2(-Wb[b * L.WL + 2 * j], -Wb[b * L.WL + 2 * j + 1]));
     }
-    blk_mma(
+    blk_mma<1, true>(
         MTi, 2 * jw, K4, [&](int r) { return Ps + r * L.PS; }, 1, Wb, L.WL,
         [&](int r, int c, double& a0, double& a1) {
           a0 = r < ni ? __ldcg(Mg + (size_t)plist[r] * ni + pstep[j0 + (c >> 1)]) : 0.0;
