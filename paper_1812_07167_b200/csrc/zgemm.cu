@@ -353,10 +353,105 @@ __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
   }
 }
 
+// Short-K variant (K <= 128): LPR lanes per output row (32 / LPR rows per warp), no shared-memory
+// reduction; the 32-lane form leaves most lanes idle when K is a few dozen (the solve's Psi t,
+// K = n_b = 56).
+template <int NMAX, int LPR>
+__global__ void __launch_bounds__(256) zgemv_short_kernel(const ZGemm g) {
+  constexpr int RW = 32 / LPR;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, li = lane % LPR;
+  const int row = (blockIdx.x * 8 + warp) * RW + lane / LPR;
+  const bool live = row < g.M;
+  for (int b = blockIdx.y; b < g.batch; b += gridDim.y) {
+    const int* Arm = g.A.rmap ? g.A.rmap + (int64_t)b * g.A.rmap_bs : nullptr;
+    const int* Brm = g.B.rmap ? g.B.rmap + (int64_t)b * g.B.rmap_bs : nullptr;
+    const int* Crm = g.C.rmap ? g.C.rmap + (int64_t)b * g.C.rmap_bs : nullptr;
+    const int* Irm = g.Cin.rmap ? g.Cin.rmap + (int64_t)b * g.Cin.rmap_bs : nullptr;
+    const int ra = live ? (Arm ? Arm[row] : row) : -1;
+    double accr[NMAX], acci[NMAX];
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r) accr[r] = acci[r] = 0.0;
+    if (ra >= 0) {
+      const zt* Ab = g.A.ptr + (int64_t)b * g.A.bs + (int64_t)ra * g.A.rs;
+      const zt* Bb = g.B.ptr + (int64_t)b * g.B.bs;
+      int64_t bco[NMAX];
+      bool bok[NMAX];
+#pragma unroll
+      for (int r = 0; r < NMAX; ++r) {
+        const int cj = r < g.N ? zcol(g.B.cmap, r, g.B.cskip_at, g.B.cskip_len) : -1;
+        bok[r] = cj >= 0;
+        bco[r] = (int64_t)(cj < 0 ? 0 : cj) * g.B.cs;
+      }
+      constexpr int U = 4;
+      for (int k0 = li; k0 < g.K; k0 += LPR * U) {
+        zt av[U], bv[U][NMAX];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int k = k0 + u * LPR;
+          const int ck = k < g.K ? zcol(g.A.cmap, k, g.A.cskip_at, g.A.cskip_len) : -1;
+          const int rk = k < g.K ? (Brm ? Brm[k] : k) : -1;
+          const bool ok = ck >= 0 && rk >= 0;
+          av[u] = ok ? Ab[(int64_t)ck * g.A.cs] : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int r = 0; r < NMAX; ++r)
+            bv[u][r] = (ok && bok[r]) ? Bb[(int64_t)rk * g.B.rs + bco[r]] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int r = 0; r < NMAX; ++r) {
+            accr[r] = fma(av[u].x, bv[u][r].x, accr[r]);
+            accr[r] = fma(-av[u].y, bv[u][r].y, accr[r]);
+            acci[r] = fma(av[u].x, bv[u][r].y, acci[r]);
+            acci[r] = fma(av[u].y, bv[u][r].x, acci[r]);
+          }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r)
+#pragma unroll
+      for (int o = LPR / 2; o; o >>= 1) {
+        accr[r] += __shfl_xor_sync(0xffffffffu, accr[r], o);
+        acci[r] += __shfl_xor_sync(0xffffffffu, acci[r], o);
+      }
+    if (!live) continue;
+    const int ro = Crm ? Crm[row] : row;
+    if (ro < 0) continue;
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r) {
+      if (li != r || r >= g.N) continue;
+      zt v = zmul(g.alpha, make_double2(accr[r], acci[r]));
+      if (g.Cin.ptr) {
+        const int ri = Irm ? Irm[row] : row;
+        const int cj = zcol(g.Cin.cmap, r, g.Cin.cskip_at, g.Cin.cskip_len);
+        if (ri >= 0 && cj >= 0) {
+          const zt cv = zmul(g.beta, g.Cin.ptr[(int64_t)b * g.Cin.bs + (int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
+          v.x += cv.x;
+          v.y += cv.y;
+        }
+      }
+      if (row == r) {
+        v.x += g.diag.x;
+        v.y += g.diag.y;
+      }
+      const int co = zcol(g.C.cmap, r, g.C.cskip_at, g.C.cskip_len);
+      if (co >= 0) g.C.ptr[(int64_t)b * g.C.bs + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
+    }
+  }
+}
+
 // Skinny-product launcher: KS from the work size (enough warps to fill the GPU, K >= 64 per warp)
 template <int NMAX>
 void launch_gemv(const ZGemm& g, cudaStream_t st) {
   const int64_t rows = (int64_t)g.M * g.batch;
+  static const bool short_off = getenv("HPS_GEMV_SHORT") && *getenv("HPS_GEMV_SHORT") == '0';
+  if (g.K <= 128 && !short_off) {  // 8 lanes per row: 32 rows per 256-thread block
+    dim3 grid((g.M + 31) / 32, g.batch < 65535 ? g.batch : 65535);
+    zgemv_short_kernel<NMAX, 8><<<grid, 256, 0, st>>>(g);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
   int ks = 1;
   while (ks < 8 && rows * ks < 148 * 48 && g.K / (2 * ks) >= 64) ks *= 2;
   const int rpb = 8 / ks;
