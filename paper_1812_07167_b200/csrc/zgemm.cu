@@ -445,9 +445,17 @@ template <int NMAX>
 void launch_gemv(const ZGemm& g, cudaStream_t st) {
   const int64_t rows = (int64_t)g.M * g.batch;
   static const bool short_off = getenv("HPS_GEMV_SHORT") && *getenv("HPS_GEMV_SHORT") == '0';
+  static const int short16 = getenv("HPS_GEMV_K16") ? atoi(getenv("HPS_GEMV_K16")) : 256;
   if (g.K <= 128 && !short_off) {  // 8 lanes per row: 32 rows per 256-thread block
     dim3 grid((g.M + 31) / 32, g.batch < 65535 ? g.batch : 65535);
     zgemv_short_kernel<NMAX, 8><<<grid, 256, 0, st>>>(g);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
+  if (g.K <= short16 && !short_off && rows >= 148 * 64) {  // 16 lanes per row (the leaf Y s, K = n_i)
+    dim3 grid((g.M + 15) / 16, g.batch < 65535 ? g.batch : 65535);
+    zgemv_short_kernel<NMAX, 16><<<grid, 256, 0, st>>>(g);
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
     return;
