@@ -474,13 +474,17 @@ void launch_gemv(const ZGemm& g, cudaStream_t st) {
   count_launch();
 }
 
+template <typename IT>
 __global__ void zcopy_kernel(const ZCopy c) {
-  const int64_t total = (int64_t)c.batch * c.M * c.N;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int j = (int)(e % c.N);
-    const int64_t t = e / c.N;
-    const int i = (int)(t % c.M);
-    const int b = (int)(t / c.M);
+  // IT = unsigned for totals below 2^32 (32-bit index arithmetic: a 64-bit division per element
+  // costs more than the copy itself)
+  const IT total = (IT)c.batch * c.M * c.N;
+  for (IT e = blockIdx.x * (IT)blockDim.x + threadIdx.x; e < total; e += (IT)gridDim.x * blockDim.x) {
+    const IT t = e / (IT)c.N;
+    const int j = (int)(e - t * (IT)c.N);
+    const IT bq = t / (IT)c.M;
+    const int i = (int)(t - bq * (IT)c.M);
+    const int b = (int)bq;
     const int ro = c.C.rmap ? c.C.rmap[(int64_t)b * c.C.rmap_bs + i] : i;
     const int co = zcol(c.C.cmap, j, c.C.cskip_at, c.C.cskip_len);
     if (ro < 0 || co < 0) continue;
@@ -582,7 +586,10 @@ void zcopy(const ZCopy& c, cudaStream_t st) {
   ProfScope ps(K_LAYOUT, 0.0, 32.0 * total, st);
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 32) blocks = 148 * 32;
-  zcopy_kernel<<<blocks, 256, 0, st>>>(c);
+  if (total < ((int64_t)1 << 32))
+    zcopy_kernel<unsigned><<<blocks, 256, 0, st>>>(c);
+  else
+    zcopy_kernel<uint64_t><<<blocks, 256, 0, st>>>(c);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
