@@ -230,6 +230,7 @@ struct hps_handle {
                       // 3: real interior elimination
   bool leaf_fused = true;
   int leaf_path = -1;  // the path build_leaves took (leaf_mode values; 0 = complex Schur, fused)
+  int nat_levels = 0;  // merge levels whose W was inverted in natural order
   bool gl = false;     // root boundary data given at Gauss-Legendre nodes (hps_opts.boundary_basis 1)
   DevBuf PglT;         // [q][q] transpose of the GL -> Chebyshev segment interpolation (gl only)
   std::vector<Depth> depth;
@@ -659,9 +660,38 @@ void build_merge(hps_handle& H, int d) {
     g.diag = Z(1, 0);
     zgemm(g, st);
   }
-  // (c) W^{-1}
-  ws.alloc(std::max<size_t>(zgj_workspace_bytes(n3, np), 16));
-  zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>() + 1 + d, st, nullptr);
+  // (c) W^{-1}.  For 200 <= n3 <= 512 (the few, latency-bound top-level inverses) natural order
+  // first (W = I - C with ||C|| < 1 needs no pivoting); if a pivot fails its check
+  // W is formed again and inverted with partial pivoting.
+  static const int nat_min = getenv("HPS_NAT_MIN") ? atoi(getenv("HPS_NAT_MIN")) : 200;
+  bool done = false;
+  if (n3 >= nat_min && n3 <= 512) {
+    ws.alloc(std::max<size_t>(zgj_natural_workspace_bytes(n3, np), 16));
+    DevBuf flag;
+    flag.alloc(sizeof(int));
+    HPS_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    zgj_invert_natural(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, flag.as<int>(), st);
+    int hflag = 0;
+    HPS_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    done = hflag == 0;
+    H.nat_levels += done ? 1 : 0;
+    if (!done) {  // W again: I - R33b R33a
+      ZGemm g;
+      g.M = g.N = g.K = n3;
+      g.batch = np;
+      g.A = op(M.R33b, n3, s33);
+      g.B = op(M.R33a, n3, s33);
+      g.C = out(Wk.as<zt>(), n3, s33);
+      g.alpha = Z(-1, 0);
+      g.diag = Z(1, 0);
+      zgemm(g, st);
+    }
+  }
+  if (!done) {
+    ws.alloc(std::max<size_t>(zgj_workspace_bytes(n3, np), 16));
+    zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>() + 1 + d, st, nullptr);
+  }
   // (d) X = [R33b R31a | -R32b] ; Phi^a = W^{-1} X  (line 8)
   const int64_t sx = (int64_t)n3 * nt;
   X.alloc(sizeof(zt) * sx * np);

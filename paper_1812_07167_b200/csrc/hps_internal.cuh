@@ -87,6 +87,12 @@ size_t zgj_workspace_bytes(int n, int batch);
 void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
                 void* ws, int* info, cudaStream_t st, int64_t* launches);
 
+// Natural-order blocked inverse of the merge matrices W (n <= 512); *flag (device
+// int) is set to 1 if a pivot failed its check (A destroyed, out invalid: redo with zgj_invert).
+void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
+                        void* ws, int* flag, cudaStream_t st);
+size_t zgj_natural_workspace_bytes(int n, int batch);
+
 // Leaf S^{-1} by the warp-specialised Gauss-Jordan kernel with the fused Schur epilogue: writes
 // the whole leaf operator [Psi | Y] (n_t x n_t, stride mstride) and the leaf R (nb x nb, batch
 // stride nb*nb) for `batch` leaves; S (n_i x n_i, stride sstride) is destroyed.  K =

@@ -311,6 +311,183 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) zgj_panel_reg_kernel(c
 }
 
 // ---------------------------------------------------------------------------
+// Natural-order panel (no pivot search), n <= 512, w <= 16, for the merge matrices W = I - C with
+// ||C|| < 1: 512 threads, 4 rows x 4 columns per thread; per step the owner
+// lanes of row k publish it and ONE barrier separates publication from the update.  A pivot
+// with |pivot|^2 < 1e-6 raises *a.pflag (the caller redoes the matrix with partial pivoting).
+// Same interface and outputs as zgj_panel_reg_kernel with identity permutations.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512, 1) zgj_panel_nat_kernel(const PanelArgs a) {
+  constexpr int CPT = 4, NB = 16, RPT = 4;
+  __shared__ zt prow[2][NB];
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  const int b = blockIdx.x, n = a.n, k0 = a.k0, w = a.w;
+  const zt* Xb = a.X + (int64_t)b * a.bsx;
+  zt* Yb = a.Y + (int64_t)b * a.bsy;
+  int* piv = a.piv + (int64_t)b * n;
+  int rq[RPT];
+  zt v[RPT][CPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    rq[t] = wp * 32 + t * 8 + rg;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int j = cg * CPT + c;
+      v[t][c] = (rq[t] < n && j < w) ? Xb[(int64_t)rq[t] * a.ldx + k0 + j] : make_double2(0.0, 0.0);
+    }
+  }
+  bool bad = false;
+#pragma unroll 1
+  for (int cga = 0; cga * CPT < w; ++cga) {
+    const bool act = cg == cga;
+    const int src = (lane & ~3) | cga;
+#pragma unroll
+    for (int s = 0; s < CPT; ++s) {
+      const int kk = cga * CPT + s;
+      if (kk >= w) break;
+      const int k = k0 + kk, par = kk & 1;
+      if (wp == (k >> 5) && rg == (k & 7)) {
+        const int tt = (k >> 3) & 3;
+#pragma unroll
+        for (int t = 0; t < RPT; ++t)
+          if (t == tt) {
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) prow[par][cg * CPT + c] = v[t][c];
+          }
+      }
+      __syncthreads();
+      const zt pv = prow[par][kk];
+      if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 1e-6)) bad = true;
+      const zt inv = zinv_fast(pv);
+      zt pr[CPT];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) pr[c] = prow[par][cg * CPT + c];
+#pragma unroll
+      for (int t = 0; t < RPT; ++t) {
+        const zt own = v[t][s];
+        zt g = zmul(make_double2(__shfl_sync(0xffffffffu, own.x, src), __shfl_sync(0xffffffffu, own.y, src)), inv);
+        if (rq[t] == k) {  // the pivot row: pr / pivot (as 0 - (-inv) pr), slot kk <- 1 / pivot
+          g = make_double2(-inv.x, -inv.y);
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) v[t][c] = make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          v[t][c].x = fma(-g.x, pr[c].x, v[t][c].x);
+          v[t][c].y = fma(-g.x, pr[c].y, v[t][c].y);
+          v[t][c].x = fma(g.y, pr[c].y, v[t][c].x);
+          v[t][c].y = fma(-g.y, pr[c].x, v[t][c].y);
+        }
+        if (act) v[t][s] = make_double2(-g.x, -g.y);
+      }
+      if (tid == 0) piv[k] = k;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) {
+    const int i = rq[t];
+    if (i < n) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const int j = cg * CPT + c;
+        if (j < w) Yb[(int64_t)i * a.ldy + k0 + j] = v[t][c];
+      }
+      if (cg == 0) write_maps(a, b, i, i);
+    }
+  }
+  if (bad && tid == 0) atomicExch(a.pflag, 1);
+}
+
+// Cluster form of zgj_panel_nat_kernel: a cluster of CS = ceil(n / 128) CTAs per matrix, CTA c
+// owns rows 128 c .. 128 c + 127 (one row x 4 columns per thread, 4 lanes per row).  Per step the
+// owner lanes of row k publish it in their CTA's shared memory, one cluster barrier, and every
+// CTA reads it through distributed shared memory: the per-step FP64 work of a 448-row panel is
+// spread over 4 SMs instead of 1.
+__device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[192..255])
+__device__ int g_nat_trace_on;
+__global__ void __launch_bounds__(512, 1) zgj_panel_natc_kernel(const PanelArgs a) {
+  constexpr int CPT = 4, NB = 16, RPC = 128;
+  const bool ntr = g_nat_trace_on == 7 && blockIdx.x == 0 && threadIdx.x == 0 && a.k0 == 0;
+  if (ntr) g_nat_trace[0] = clock64();
+  cg::cluster_group cluster = cg::this_cluster();
+  const int CS = (int)cluster.num_blocks();
+  const int cr = (int)cluster.block_rank();
+  __shared__ zt prow[2][NB];
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  const int b = blockIdx.x / CS, n = a.n, k0 = a.k0, w = a.w;
+  const zt* Xb = a.X + (int64_t)b * a.bsx;
+  zt* Yb = a.Y + (int64_t)b * a.bsy;
+  int* piv = a.piv + (int64_t)b * n;
+  const int i = cr * RPC + wp * 8 + rg;
+  zt v[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int j = cg * CPT + c;
+    v[c] = (i < n && j < w) ? Xb[(int64_t)i * a.ldx + k0 + j] : make_double2(0.0, 0.0);
+  }
+  bool bad = false;
+  if (ntr) g_nat_trace[1] = clock64();
+#pragma unroll 1
+  for (int cga = 0; cga * CPT < w; ++cga) {
+    const bool act = cg == cga;
+    const int src = (lane & ~3) | cga;
+#pragma unroll
+    for (int s = 0; s < CPT; ++s) {
+      const int kk = cga * CPT + s;
+      if (kk >= w) break;
+      const int k = k0 + kk, par = kk & 1;
+      if (ntr) g_nat_trace[2 + kk] = clock64();
+      if (i == k) {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) prow[par][cg * CPT + c] = v[c];
+      }
+      // only the owner CTA publishes: release there, relaxed elsewhere (a reader's loads of step
+      // k feed its update before it arrives at step k + 1, so the double buffer stays safe)
+      if (cr == k / RPC)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      else
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+      const zt* rp = cluster.map_shared_rank(&prow[par][0], k / RPC);
+      const zt pv = rp[kk];
+      zt pr[CPT];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) pr[c] = rp[cg * CPT + c];
+      if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 1e-6)) bad = true;
+      const zt inv = zinv_fast(pv);
+      const zt own = v[s];
+      zt g = zmul(make_double2(__shfl_sync(0xffffffffu, own.x, src), __shfl_sync(0xffffffffu, own.y, src)), inv);
+      if (i == k) {  // the pivot row: pr / pivot (as 0 - (-inv) pr), slot kk <- 1 / pivot
+        g = make_double2(-inv.x, -inv.y);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) v[c] = make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        v[c].x = fma(-g.x, pr[c].x, v[c].x);
+        v[c].y = fma(-g.x, pr[c].y, v[c].y);
+        v[c].x = fma(g.y, pr[c].y, v[c].x);
+        v[c].y = fma(-g.y, pr[c].x, v[c].y);
+      }
+      if (act) v[s] = make_double2(-g.x, -g.y);
+      if (cr == 0 && tid == 0) piv[k] = k;
+    }
+  }
+  if (ntr) g_nat_trace[40] = clock64();
+  if (i < n) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int j = cg * CPT + c;
+      if (j < w) Yb[(int64_t)i * a.ldy + k0 + j] = v[c];
+    }
+    if (cg == 0) write_maps(a, b, i, i);
+  }
+  if (bad && tid == 0) atomicExch(a.pflag, 1);
+  cluster.sync();  // no CTA exits while another may still read its shared memory
+  if (ntr) g_nat_trace[41] = clock64();
+}
+
+// ---------------------------------------------------------------------------
 // Cluster version, 256 < n <= 4096: CTA c owns rows c*256 + t in registers.  Two cluster
 // barriers per step: (1) after the per-CTA pivot candidates, (2) after the owner of the
 // pivot row (and of row k) published them in its shared memory.
@@ -1998,7 +2175,9 @@ int g_gj_mode_force = 0;
 // debug: timeline of CTA 0 of the next zgj_ws launch (on = 1 arms it; out[160] clock64 values)
 void zgj_ws_trace(int on, long long* out) {
   HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_ws_trace_on, &on, sizeof(int)));
-  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_ws_trace, sizeof(long long) * 256));
+  HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_nat_trace_on, &on, sizeof(int)));
+  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_ws_trace, sizeof(long long) * 192));
+  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out + 192, g_nat_trace, sizeof(long long) * 64));
 }  // hps_zinv_timed: 1 = fused, 2 = blocked (0 = library choice / HPS_GJ)
 namespace {
 int gj_mode_env() {
@@ -2521,6 +2700,103 @@ void zgj_plan_clear() {
 
 int zgj_regime_of(int n, int nbox) { return choose_regime(n, nbox); }
 void zgj_force_regime(int r) { g_regime_force = r; }
+
+// Natural-order blocked Gauss-Jordan: 16-column zgj_panel_nat_kernel panels and
+// the blocked explicit-swap update with identity maps.  n <= 512.  Workspace as
+// zgj_workspace_bytes(n, batch) for the blocked regime; *flag (device) is set to 1 when a pivot
+// failed the check — out is then not the inverse and A is destroyed (the caller keeps a copy).
+void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
+                        void* ws, int* flag, cudaStream_t st) {
+  char* wsp = static_cast<char*>(ws);
+  const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
+  zt* B2 = reinterpret_cast<zt*>(wsp);
+  int* piv = reinterpret_cast<int*>(wsp + mbytes);
+  int* rowsrc = piv + (size_t)batch * n;
+  int* cinmap = rowsrc + (size_t)batch * n;
+  int* pi = cinmap + (size_t)batch * n;
+  zt* buf[2] = {A, B2};
+  const int64_t ld[2] = {lda, n}, bsz[2] = {bs, (int64_t)n * n};
+  const int npan = (n + 15) / 16, nbw = (n + npan - 1) / npan;
+  int cur = 0;
+  for (int k0 = 0; k0 < n; k0 += nbw) {
+    const int w = std::min(nbw, n - k0);
+    PanelArgs pa{buf[cur], buf[1 - cur], ld[cur], bsz[cur], ld[1 - cur], bsz[1 - cur], n, k0, w, piv, rowsrc, cinmap,
+                 flag};
+    pa.pflag = flag;
+    {
+      ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)w * w * batch, 32.0 * n * (double)w * batch, st);
+      static const bool single = getenv("HPS_NATC") && *getenv("HPS_NATC") == '0';
+      const int cs = (n + 127) / 128;
+      if (single || cs > 8) {
+        zgj_panel_nat_kernel<<<batch, 512, 0, st>>>(pa);
+      } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(batch * cs);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel, pa));
+      }
+      HPS_CUDA_CHECK(cudaGetLastError());
+      count_launch();
+    }
+    const int nc = n - w;
+    if (nc > 0) {
+      ZGemm gm;
+      gm.M = n;
+      gm.N = nc;
+      gm.K = w;
+      gm.batch = batch;
+      gm.A.ptr = buf[1 - cur] + k0;
+      gm.A.rs = ld[1 - cur];
+      gm.A.bs = bsz[1 - cur];
+      gm.B.ptr = buf[cur];
+      gm.B.rs = ld[cur];
+      gm.B.bs = bsz[cur];
+      gm.B.rmap = rowsrc + k0;
+      gm.B.rmap_bs = n;
+      gm.B.cskip_at = k0;
+      gm.B.cskip_len = w;
+      gm.Cin.ptr = buf[cur];
+      gm.Cin.rs = ld[cur];
+      gm.Cin.bs = bsz[cur];
+      gm.Cin.rmap = cinmap;
+      gm.Cin.rmap_bs = n;
+      gm.Cin.cskip_at = k0;
+      gm.Cin.cskip_len = w;
+      gm.C.ptr = buf[1 - cur];
+      gm.C.rs = ld[1 - cur];
+      gm.C.bs = bsz[1 - cur];
+      gm.C.cskip_at = k0;
+      gm.C.cskip_len = w;
+      gm.beta = make_double2(1.0, 0.0);
+      zgemm(gm, st);
+    }
+    cur = 1 - cur;
+  }
+  // no permutation: the result is buf[cur] itself
+  ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)batch * n * n, st);
+  if (ld[cur] == n && bsz[cur] == (int64_t)n * n && ldo == n && obs == (int64_t)n * n) {
+    HPS_CUDA_CHECK(cudaMemcpyAsync(out, buf[cur], sizeof(zt) * (size_t)batch * n * n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    for (int b = 0; b < batch; ++b)
+      HPS_CUDA_CHECK(cudaMemcpy2DAsync(out + (int64_t)b * obs, sizeof(zt) * ldo, buf[cur] + (int64_t)b * bsz[cur],
+                                       sizeof(zt) * ld[cur], sizeof(zt) * n, n, cudaMemcpyDeviceToDevice, st));
+  }
+  (void)pi;
+}
+
+size_t zgj_natural_workspace_bytes(int n, int batch) {
+  const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
+  return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256;
+}
 
 size_t zgj_workspace_bytes(int n, int batch) {
   const int reg = choose_regime(n, batch);

@@ -104,6 +104,34 @@ def test_leaf_real_elimination_forced_pivoting():
     assert float(out.stdout.strip().splitlines()[-1]) < TOL
 
 
+def test_natural_order_merge_inverses_all_levels():
+    """HPS_NAT_MIN=14 (fresh process): every merge W with 14 <= n3 <= 512 is inverted in natural
+    order — every box's R and u vs the oracle, complex eta included."""
+    import os, subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import os, sys
+        sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+        import numpy as np, oracle
+        from paper_1812_07167_b200 import hps
+        from test_gpu_parity import problem, rel
+        worst = 0.0
+        for nx, ny, p, kappa, eta in [(4, 4, 8, 9.0, 9.0 - 2j), (8, 4, 6, 9.0, 9.0), (4, 8, 10, 20.0, 20.0)]:
+            g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx)
+            S = hps.Solver(g, p, kappa, eta, c, keep_all_R=True)
+            O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c, keep_all_R=True)
+            for box in range(1, 2 * nx * ny):
+                worst = max(worst, rel(S.R(box), O.R(box)))
+            worst = max(worst, rel(S.solve(s, t), O.solve(s, t)))
+        print(worst)
+    """)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HPS_NAT_MIN="14", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) < TOL
+
+
 def test_leaf_path_selection():
     """Auto mode takes the real elimination only for real c below the first interior resonance;
     leaf_mode 3 refuses complex c."""

@@ -1,0 +1,20 @@
+"""Timeline of the first natural-order panel (CTA 0, k0 = 0) of the C2 top-level inverse."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_1812_07167_b200 import hps, inputs
+import bench
+cfg = inputs.CONFIGS[2]
+g, c, s, t = bench.setup(cfg, hps)
+d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, d(c))
+S.close()
+hps.lib().hps_debug_ws_trace(7, None)
+S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, d(c))
+torch.cuda.synchronize()
+buf = np.zeros(256, dtype=np.int64)
+hps.lib().hps_debug_ws_trace(0, buf.ctypes.data)
+tr = buf[192:]
+t0 = tr[0]
+print("load %d clk; steps:" % (tr[1] - t0), np.diff(tr[2:18]).tolist(), "after loop %d, end %d" % (tr[40] - t0, tr[41] - t0))
