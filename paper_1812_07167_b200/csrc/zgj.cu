@@ -405,8 +405,9 @@ __global__ void __launch_bounds__(512, 1) zgj_panel_nat_kernel(const PanelArgs a
 // spread over 4 SMs instead of 1.
 __device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[192..255])
 __device__ int g_nat_trace_on;
+template <int CPT>
 __global__ void __launch_bounds__(512, 1) zgj_panel_natc_kernel(const PanelArgs a) {
-  constexpr int CPT = 4, NB = 16, RPC = 128;
+  constexpr int NB = 4 * CPT, RPC = 128;
   const bool ntr = g_nat_trace_on == 7 && blockIdx.x == 0 && threadIdx.x == 0 && a.k0 == 0;
   if (ntr) g_nat_trace[0] = clock64();
   cg::cluster_group cluster = cg::this_cluster();
@@ -2716,7 +2717,11 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
   int* pi = cinmap + (size_t)batch * n;
   zt* buf[2] = {A, B2};
   const int64_t ld[2] = {lda, n}, bsz[2] = {bs, (int64_t)n * n};
-  const int npan = (n + 15) / 16, nbw = (n + npan - 1) / npan;
+  static const int wide = getenv("HPS_NAT_W") ? atoi(getenv("HPS_NAT_W")) : 16;  // 32: measured slower (C2 merges 5.20 -> 5.76 ms)
+  const int cs = (n + 127) / 128;
+  const bool use_c = !(getenv("HPS_NATC") && *getenv("HPS_NATC") == '0') && cs <= 8;
+  const int wmax = use_c && wide == 32 ? 32 : 16;
+  const int npan = (n + wmax - 1) / wmax, nbw = (n + npan - 1) / npan;
   int cur = 0;
   for (int k0 = 0; k0 < n; k0 += nbw) {
     const int w = std::min(nbw, n - k0);
@@ -2725,9 +2730,7 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
     pa.pflag = flag;
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)w * w * batch, 32.0 * n * (double)w * batch, st);
-      static const bool single = getenv("HPS_NATC") && *getenv("HPS_NATC") == '0';
-      const int cs = (n + 127) / 128;
-      if (single || cs > 8) {
+      if (!use_c) {
         zgj_panel_nat_kernel<<<batch, 512, 0, st>>>(pa);
       } else {
         cudaLaunchConfig_t cfg = {};
@@ -2742,7 +2745,10 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel, pa));
+        if (wmax == 32)
+          HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel<8>, pa));
+        else
+          HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel<4>, pa));
       }
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
