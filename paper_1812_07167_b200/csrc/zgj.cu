@@ -405,21 +405,22 @@ __global__ void __launch_bounds__(512, 1) zgj_panel_nat_kernel(const PanelArgs a
 // spread over 4 SMs instead of 1.
 __device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[192..255])
 __device__ int g_nat_trace_on;
-template <int CPT>
+template <int CPT, int LPR = 4>
 __global__ void __launch_bounds__(512, 1) zgj_panel_natc_kernel(const PanelArgs a) {
-  constexpr int NB = 4 * CPT, RPC = 128;
+  // LPR lanes per row (CPT columns each), RPC = 512 / LPR rows per CTA
+  constexpr int NB = LPR * CPT, RPC = 512 / LPR;
   const bool ntr = g_nat_trace_on == 7 && blockIdx.x == 0 && threadIdx.x == 0 && a.k0 == 0;
   if (ntr) g_nat_trace[0] = clock64();
   cg::cluster_group cluster = cg::this_cluster();
   const int CS = (int)cluster.num_blocks();
   const int cr = (int)cluster.block_rank();
   __shared__ zt prow[2][NB];
-  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane % LPR, rg = lane / LPR;
   const int b = blockIdx.x / CS, n = a.n, k0 = a.k0, w = a.w;
   const zt* Xb = a.X + (int64_t)b * a.bsx;
   zt* Yb = a.Y + (int64_t)b * a.bsy;
   int* piv = a.piv + (int64_t)b * n;
-  const int i = cr * RPC + wp * 8 + rg;
+  const int i = cr * RPC + wp * (32 / LPR) + rg;
   zt v[CPT];
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(512, 1) zgj_panel_natc_kernel(const PanelArgs 
 #pragma unroll 1
   for (int cga = 0; cga * CPT < w; ++cga) {
     const bool act = cg == cga;
-    const int src = (lane & ~3) | cga;
+    const int src = (lane & ~(LPR - 1)) | cga;
 #pragma unroll
     for (int s = 0; s < CPT; ++s) {
       const int kk = cga * CPT + s;
@@ -2718,7 +2719,8 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
   zt* buf[2] = {A, B2};
   const int64_t ld[2] = {lda, n}, bsz[2] = {bs, (int64_t)n * n};
   static const int wide = getenv("HPS_NAT_W") ? atoi(getenv("HPS_NAT_W")) : 16;  // 32: measured slower (C2 merges 5.20 -> 5.76 ms)
-  const int cs = (n + 127) / 128;
+  static const int lpr = getenv("HPS_NAT_LPR") ? atoi(getenv("HPS_NAT_LPR")) : 4;
+  const int cs = (n + 512 / lpr - 1) / (512 / lpr);
   const bool use_c = !(getenv("HPS_NATC") && *getenv("HPS_NATC") == '0') && cs <= 8;
   const int wmax = use_c && wide == 32 ? 32 : 16;
   const int npan = (n + wmax - 1) / wmax, nbw = (n + npan - 1) / npan;
@@ -2747,8 +2749,10 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
         cfg.numAttrs = 1;
         if (wmax == 32)
           HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel<8>, pa));
+        else if (lpr == 8)
+          HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel<2, 8>, pa));
         else
-          HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel<4>, pa));
+          HPS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, zgj_panel_natc_kernel<4, 4>, pa));
       }
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
