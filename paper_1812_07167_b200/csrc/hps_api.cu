@@ -626,28 +626,37 @@ void build_merge(hps_handle& H, int d) {
   cudaStream_t st = H.st;
   const int64_t s33 = (int64_t)n3 * n3;
   // (a) retained child blocks
+  // X = [R33b R31a | -R32b] (line 8) is allocated here so that its copied half joins the gathers
+  const int64_t sx = (int64_t)n3 * nt;
+  DevBuf X;
+  X.alloc(sizeof(zt) * sx * np);
   {
-    ZCopy c;
-    c.batch = np;
-    c.M = n3;
-    c.N = n3;
-    c.A = op(Ra, nbc, cbs, M.I3a, M.I3a);
-    c.C = out(M.R33a, n3, s33);
-    zcopy(c, st);
-    c.A = op(Rb, nbc, cbs, M.I3b, M.I3b);
-    c.C = out(M.R33b, n3, s33);
-    zcopy(c, st);
-    c.M = n1;
-    c.A = op(Ra, nbc, cbs, M.I1a, M.I3a);
-    c.C = out(M.R13a, n3, (int64_t)n1 * n3);
-    zcopy(c, st);
-    c.M = n2;
-    c.A = op(Rb, nbc, cbs, M.I2b, M.I3b);
-    c.C = out(M.R23b, n3, (int64_t)n2 * n3);
-    zcopy(c, st);
+    ZCopy c[5];
+    for (auto& x : c) {
+      x.batch = np;
+      x.N = n3;
+    }
+    c[0].M = n3;
+    c[0].A = op(Ra, nbc, cbs, M.I3a, M.I3a);
+    c[0].C = out(M.R33a, n3, s33);
+    c[1].M = n3;
+    c[1].A = op(Rb, nbc, cbs, M.I3b, M.I3b);
+    c[1].C = out(M.R33b, n3, s33);
+    c[2].M = n1;
+    c[2].A = op(Ra, nbc, cbs, M.I1a, M.I3a);
+    c[2].C = out(M.R13a, n3, (int64_t)n1 * n3);
+    c[3].M = n2;
+    c[3].A = op(Rb, nbc, cbs, M.I2b, M.I3b);
+    c[3].C = out(M.R23b, n3, (int64_t)n2 * n3);
+    c[4].M = n3;
+    c[4].N = n2;
+    c[4].A = op(Rb, nbc, cbs, M.I3b, M.I2b);
+    c[4].C = out(X.as<zt>() + n1, nt, sx);
+    c[4].alpha = Z(-1, 0);
+    zcopy_multi(c, 5, st);
   }
   // (b) W = I - R33b R33a  (Algorithm 1 line 7)
-  DevBuf Wk, X, ws;
+  DevBuf Wk, ws;
   Wk.alloc(sizeof(zt) * s33 * np);
   {
     ZGemm g;
@@ -693,8 +702,6 @@ void build_merge(hps_handle& H, int d) {
     zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>() + 1 + d, st, nullptr);
   }
   // (d) X = [R33b R31a | -R32b] ; Phi^a = W^{-1} X  (line 8)
-  const int64_t sx = (int64_t)n3 * nt;
-  X.alloc(sizeof(zt) * sx * np);
   {
     ZGemm g;
     g.M = n3;
@@ -705,14 +712,6 @@ void build_merge(hps_handle& H, int d) {
     g.B = op(Ra, nbc, cbs, M.I3a, M.I1a);
     g.C = out(X.as<zt>(), nt, sx);
     zgemm(g, st);
-    ZCopy c;
-    c.batch = np;
-    c.M = n3;
-    c.N = n2;
-    c.A = op(Rb, nbc, cbs, M.I3b, M.I2b);
-    c.C = out(X.as<zt>() + n1, nt, sx);
-    c.alpha = Z(-1, 0);
-    zcopy(c, st);
     g.N = nt;
     g.A = op(M.Winv, n3, s33);
     g.B = op(X.as<zt>(), nt, sx);
@@ -918,17 +917,18 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
     g.C = out(tb, R, cb, M.I3b);
     zgemm(g, st);  // t3b = Phi^b t + t~b
     fl += 8.0 * np * 2.0 * n3 * ntau * R;
-    ZCopy c;
-    c.batch = np;
-    c.N = nrhs;
-    c.M = n1;
-    c.A = op(t[d].as<zt>(), R, pb, M.pp);
-    c.C = out(ta, R, cb, M.I1a);
-    zcopy(c, st);
-    c.M = n2;
-    c.A = op(t[d].as<zt>(), R, pb, M.pp + n1);
-    c.C = out(tb, R, cb, M.I2b);
-    zcopy(c, st);
+    ZCopy c[2];
+    for (auto& x : c) {
+      x.batch = np;
+      x.N = nrhs;
+    }
+    c[0].M = n1;
+    c[0].A = op(t[d].as<zt>(), R, pb, M.pp);
+    c[0].C = out(ta, R, cb, M.I1a);
+    c[1].M = n2;
+    c[1].A = op(t[d].as<zt>(), R, pb, M.pp + n1);
+    c[1].C = out(tb, R, cb, M.I2b);
+    zcopy_multi(c, 2, st);
     t[d].release();
   }
   const int nbot = 1 << Lb;

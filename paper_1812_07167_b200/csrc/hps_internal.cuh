@@ -75,6 +75,7 @@ struct ZCopy {
   zt alpha = {1.0, 0.0};
 };
 void zcopy(const ZCopy& c, cudaStream_t st);
+void zcopy_multi(const ZCopy* cs, int n, cudaStream_t st);  // independent copies, one launch per 6
 
 // ---------------------------------------------------------------------------
 // Batched explicit inverse by Gauss-Jordan with partial pivoting, zgj.cu

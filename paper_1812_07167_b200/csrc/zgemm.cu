@@ -10,6 +10,7 @@
 // chosen so that the 8x4 / 4x8 DMMA fragments load as conflict-free 16-byte LDS.
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "hps_internal.cuh"
 
@@ -578,6 +579,57 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
     launch<64, 32, 32, 16>(g, st);
   else
     launch<32, 32, 16, 16>(g, st);
+}
+
+// Several independent copies in one launch (blockIdx.y selects the copy): the merge gathers are a
+// few microseconds each and launch-latency bound.
+struct ZCopyList {
+  ZCopy c[6];
+};
+template <typename IT>
+__global__ void zcopy_multi_kernel(const ZCopyList L) {
+  const ZCopy& c = L.c[blockIdx.y];
+  const IT total = (IT)c.batch * c.M * c.N;
+  for (IT e = blockIdx.x * (IT)blockDim.x + threadIdx.x; e < total; e += (IT)gridDim.x * blockDim.x) {
+    const IT t = e / (IT)c.N;
+    const int j = (int)(e - t * (IT)c.N);
+    const IT bq = t / (IT)c.M;
+    const int i = (int)(t - bq * (IT)c.M);
+    const int b = (int)bq;
+    const int ro = c.C.rmap ? c.C.rmap[(int64_t)b * c.C.rmap_bs + i] : i;
+    const int co = zcol(c.C.cmap, j, c.C.cskip_at, c.C.cskip_len);
+    if (ro < 0 || co < 0) continue;
+    const int ri = c.A.rmap ? c.A.rmap[(int64_t)b * c.A.rmap_bs + i] : i;
+    const int ci = zcol(c.A.cmap, j, c.A.cskip_at, c.A.cskip_len);
+    zt v = make_double2(0.0, 0.0);
+    if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[(int64_t)b * c.A.bs + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
+    c.C.ptr[(int64_t)b * c.C.bs + (int64_t)ro * c.C.rs + (int64_t)co * c.C.cs] = v;
+  }
+}
+
+void zcopy_multi(const ZCopy* cs, int n, cudaStream_t st) {
+  std::vector<const ZCopy*> live;
+  for (int k = 0; k < n; ++k)
+    if ((int64_t)cs[k].batch * cs[k].M * cs[k].N > 0) live.push_back(&cs[k]);
+  for (size_t g0 = 0; g0 < live.size(); g0 += 6) {
+    const int m = (int)std::min<size_t>(6, live.size() - g0);
+    ZCopyList L;
+    int64_t maxt = 0, bytes = 0;
+    for (int u = 0; u < m; ++u) {
+      L.c[u] = *live[g0 + u];
+      const int64_t total = (int64_t)L.c[u].batch * L.c[u].M * L.c[u].N;
+      maxt = std::max(maxt, total);
+      bytes += 32 * total;
+    }
+    ProfScope ps(K_LAYOUT, 0.0, (double)bytes, st);
+    const int blocks = (int)std::min<int64_t>((maxt + 255) / 256, 148 * 32 / m + 1);
+    if (maxt < ((int64_t)1 << 32))
+      zcopy_multi_kernel<unsigned><<<dim3(blocks, m), 256, 0, st>>>(L);
+    else
+      zcopy_multi_kernel<uint64_t><<<dim3(blocks, m), 256, 0, st>>>(L);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+  }
 }
 
 void zcopy(const ZCopy& c, cudaStream_t st) {
