@@ -244,6 +244,8 @@ struct hps_handle {
   int64_t launches[2] = {0, 0};
   double flops[2] = {0, 0};
   cudaEvent_t ev[6] = {};
+  cudaStream_t st2 = nullptr;                  // side stream: merge GEMMs independent of W^{-1}
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   Prof prof;
   ~hps_handle() {
     // return every buffer to the pool on our stream, then retire the stream
@@ -260,8 +262,12 @@ struct hps_handle {
     for (auto& r : R) r.release();
     info.release();
     if (st) cudaStreamSynchronize(st);
+    if (st2) cudaStreamSynchronize(st2);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (st2) cudaStreamDestroy(st2);
     if (st) cudaStreamDestroy(st);
   }
 };
@@ -655,6 +661,22 @@ void build_merge(hps_handle& H, int d) {
     c[4].alpha = Z(-1, 0);
     zcopy_multi(c, 5, st);
   }
+  // first half of X = [R33b R31a | -R32b] on the side stream: it does not need W^{-1}, so it runs
+  // while the (latency-bound, few-CTA) inverse of the top levels occupies the main stream
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
+  HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+  {
+    ZGemm g;
+    g.M = n3;
+    g.N = n1;
+    g.K = n3;
+    g.batch = np;
+    g.A = op(M.R33b, n3, s33);
+    g.B = op(Ra, nbc, cbs, M.I3a, M.I1a);
+    g.C = out(X.as<zt>(), nt, sx);
+    zgemm(g, H.st2);
+  }
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
   // (b) W = I - R33b R33a  (Algorithm 1 line 7)
   DevBuf Wk, ws;
   Wk.alloc(sizeof(zt) * s33 * np);
@@ -702,16 +724,12 @@ void build_merge(hps_handle& H, int d) {
     zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>() + 1 + d, st, nullptr);
   }
   // (d) X = [R33b R31a | -R32b] ; Phi^a = W^{-1} X  (line 8)
+  HPS_CUDA_CHECK(cudaStreamWaitEvent(st, H.ev_join, 0));  // X complete
   {
     ZGemm g;
     g.M = n3;
-    g.N = n1;
     g.K = n3;
     g.batch = np;
-    g.A = op(M.R33b, n3, s33);
-    g.B = op(Ra, nbc, cbs, M.I3a, M.I1a);
-    g.C = out(X.as<zt>(), nt, sx);
-    zgemm(g, st);
     g.N = nt;
     g.A = op(M.Winv, n3, s33);
     g.B = op(X.as<zt>(), nt, sx);
@@ -1158,6 +1176,9 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   retain_pool(H.dev);
   g_alloc_stream = H.st;
   for (auto& e : H.ev) HPS_CUDA_CHECK(cudaEventCreate(&e));
+  HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H.st2, cudaStreamNonBlocking));
+  HPS_CUDA_CHECK(cudaEventCreateWithFlags(&H.ev_fork, cudaEventDisableTiming));
+  HPS_CUDA_CHECK(cudaEventCreateWithFlags(&H.ev_join, cudaEventDisableTiming));
   H.g = *g;
   H.p = p;
   H.q = q;
