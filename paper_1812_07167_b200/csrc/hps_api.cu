@@ -862,6 +862,22 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
     g.beta = Z(0, 0);
     g.C = out(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
     zgemm(g, st);
+    const bool need_h = d > 0 || h_root;
+    if (need_h) {  // h^tau part 1 = h1a + R13a t~a needs only t~a: side stream, beside t~b
+      h[d].alloc(sizeof(zt) * (size_t)np * ntau * R);
+      HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
+      HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+      ZGemm g1 = g;
+      g1.M = n1;
+      g1.A = op(M.R13a, n3, (int64_t)n1 * n3);
+      g1.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
+      g1.Cin = op(ha, R, cb, M.I1a);
+      g1.alpha = Z(1, 0);
+      g1.beta = Z(1, 0);
+      g1.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp);
+      zgemm(g1, H.st2);
+      HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
+    }
     g.A = op(M.R33a, n3, s33);
     g.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
     g.Cin = op(ha, R, cb, M.I3a);
@@ -870,16 +886,9 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
     g.C = out(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
     zgemm(g, st);
     fl += 8.0 * np * 3.0 * n3 * n3 * R;
-    if (d > 0 || h_root) {  // h^tau = [h1a; h2b] + [R13a t~a; R23b t~b]  (eq. flux_part), canonical order
-      h[d].alloc(sizeof(zt) * (size_t)np * ntau * R);
+    if (need_h) {  // h^tau = [h1a; h2b] + [R13a t~a; R23b t~b]  (eq. flux_part), canonical order
       g.alpha = Z(1, 0);
       g.beta = Z(1, 0);
-      g.M = n1;
-      g.A = op(M.R13a, n3, (int64_t)n1 * n3);
-      g.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
-      g.Cin = op(ha, R, cb, M.I1a);
-      g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp);
-      zgemm(g, st);
       g.M = n2;
       g.A = op(M.R23b, n3, (int64_t)n2 * n3);
       g.B = op(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
@@ -887,6 +896,7 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
       g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp + n1);
       zgemm(g, st);
       fl += 8.0 * np * (double)(n1 + n2) * n3 * R;
+      HPS_CUDA_CHECK(cudaStreamWaitEvent(st, H.ev_join, 0));  // part 1 done
     }
     h[d + 1].release();
   }
@@ -929,11 +939,17 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
       g.beta = Z(1, 0);
     }
     g.C = out(ta, R, cb, M.I3a);
+    HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+    {
+      ZGemm g2 = g;  // t3b = Phi^b t + t~b on the side stream (independent of t3a)
+      g2.A = op(M.PhiB, ntau, (int64_t)n3 * ntau);
+      if (has_s) g2.Cin = op(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
+      g2.C = out(tb, R, cb, M.I3b);
+      zgemm(g2, H.st2);
+      HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
+    }
     zgemm(g, st);  // t3a = Phi^a t + t~a
-    g.A = op(M.PhiB, ntau, (int64_t)n3 * ntau);
-    if (has_s) g.Cin = op(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
-    g.C = out(tb, R, cb, M.I3b);
-    zgemm(g, st);  // t3b = Phi^b t + t~b
     fl += 8.0 * np * 2.0 * n3 * ntau * R;
     ZCopy c[2];
     for (auto& x : c) {
@@ -947,6 +963,7 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
     c[1].A = op(t[d].as<zt>(), R, pb, M.pp + n1);
     c[1].C = out(tb, R, cb, M.I2b);
     zcopy_multi(c, 2, st);
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(st, H.ev_join, 0));  // t3b done
     t[d].release();
   }
   const int nbot = 1 << Lb;
