@@ -736,6 +736,26 @@ void build_merge(hps_handle& H, int d) {
     g.C = out(M.PhiA, nt, sx);
     zgemm(g, st);
   }
+  // (f, first half) R^tau rows of I1 = R11a + R13a Phi^a need only Phi^a: side stream, beside (e)
+  const bool need_R = (d > 0) || H.keep_root_R || H.keep_all_R;
+  const int64_t ps = (int64_t)nt * nt;
+  if (need_R) {
+    H.R[d].alloc(sizeof(zt) * (size_t)nt * nt * np);
+    HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+    ZGemm g;
+    g.M = n1;
+    g.N = nt;
+    g.K = n3;
+    g.batch = np;
+    g.A = op(M.R13a, n3, (int64_t)n1 * n3);
+    g.B = op(M.PhiA, nt, sx);
+    g.Cin = op(Ra, nbc, cbs, M.I1a, M.cmapA);
+    g.beta = Z(1, 0);
+    g.C = out(H.R[d].as<zt>(), nt, ps, M.pp, M.pp);
+    zgemm(g, H.st2);
+    HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
+  }
   // (e) Phi^b = -[R31a | 0] - R33a Phi^a  (line 10, equivalent form)
   {
     ZGemm g;
@@ -753,21 +773,12 @@ void build_merge(hps_handle& H, int d) {
   }
   double fl = 8.0 * np * ((double)n3 * n3 * n3 * 2 + (double)n3 * n3 * n1 + 2.0 * n3 * n3 * nt);
   // (f) R^tau = diag(R11a, R22b) + [R13a Phi^a ; R23b Phi^b], scattered to canonical order (line 12)
-  const bool need_R = (d > 0) || H.keep_root_R || H.keep_all_R;
   if (need_R) {
-    H.R[d].alloc(sizeof(zt) * (size_t)nt * nt * np);
-    const int64_t ps = (int64_t)nt * nt;
     ZGemm g;
-    g.M = n1;
     g.N = nt;
     g.K = n3;
     g.batch = np;
-    g.A = op(M.R13a, n3, (int64_t)n1 * n3);
-    g.B = op(M.PhiA, nt, sx);
-    g.Cin = op(Ra, nbc, cbs, M.I1a, M.cmapA);
     g.beta = Z(1, 0);
-    g.C = out(H.R[d].as<zt>(), nt, ps, M.pp, M.pp);
-    zgemm(g, st);
     g.M = n2;
     g.A = op(M.R23b, n3, (int64_t)n2 * n3);
     g.B = op(M.PhiB, nt, sx);
@@ -775,6 +786,7 @@ void build_merge(hps_handle& H, int d) {
     g.C = out(H.R[d].as<zt>(), nt, ps, M.pp + n1, M.pp);
     zgemm(g, st);
     fl += 8.0 * np * (double)nt * nt * n3;
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(st, H.ev_join, 0));  // first half done
   }
   H.flops[0] += fl;
   if (!H.keep_all_R) H.R[d + 1].release();    // Algorithm 1 line 14 (stream-ordered free)
