@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -115,7 +117,12 @@ struct DevBuf {
     release();
     if (n == 0) return;
     st = g_alloc_stream;
+    static const bool dbg = getenv("HPS_DEBUG_ALLOC") && *getenv("HPS_DEBUG_ALLOC") == '1';
+    const auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMallocAsync(&p, n, st);
+    if (dbg && n >= ((size_t)1 << 28))
+      fprintf(stderr, "[alloc] %.2f GB in %.3f ms\n", n / 1e9,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
@@ -622,6 +629,17 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   H.leaf_path = schur ? (fused_all ? 0 : 2) : 1;
 }
 
+// side stream for products independent of the current chain; HPS_SIDE=0 (build)
+// or HPS_SIDE_SOLVE=0 (solve) run them on the main stream instead
+cudaStream_t side_build(const hps_handle& H) {
+  static const bool off = getenv("HPS_SIDE") && *getenv("HPS_SIDE") == '0';
+  return off ? H.st : H.st2;
+}
+cudaStream_t side_solve(const hps_handle& H) {
+  static const bool off = getenv("HPS_SIDE_SOLVE") && *getenv("HPS_SIDE_SOLVE") == '0';
+  return off ? H.st : H.st2;
+}
+
 void build_merge(hps_handle& H, int d) {
   MergeLevel& M = H.lev[d];
   const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau, nbc = M.nbc;
@@ -664,7 +682,7 @@ void build_merge(hps_handle& H, int d) {
   // first half of X = [R33b R31a | -R32b] on the side stream: it does not need W^{-1}, so it runs
   // while the (latency-bound, few-CTA) inverse of the top levels occupies the main stream
   HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
-  HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+  HPS_CUDA_CHECK(cudaStreamWaitEvent(side_build(H), H.ev_fork, 0));
   {
     ZGemm g;
     g.M = n3;
@@ -674,9 +692,9 @@ void build_merge(hps_handle& H, int d) {
     g.A = op(M.R33b, n3, s33);
     g.B = op(Ra, nbc, cbs, M.I3a, M.I1a);
     g.C = out(X.as<zt>(), nt, sx);
-    zgemm(g, H.st2);
+    zgemm(g, side_build(H));
   }
-  HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, side_build(H)));
   // (b) W = I - R33b R33a  (Algorithm 1 line 7)
   DevBuf Wk, ws;
   Wk.alloc(sizeof(zt) * s33 * np);
@@ -742,7 +760,7 @@ void build_merge(hps_handle& H, int d) {
   if (need_R) {
     H.R[d].alloc(sizeof(zt) * (size_t)nt * nt * np);
     HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
-    HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(side_build(H), H.ev_fork, 0));
     ZGemm g;
     g.M = n1;
     g.N = nt;
@@ -753,8 +771,8 @@ void build_merge(hps_handle& H, int d) {
     g.Cin = op(Ra, nbc, cbs, M.I1a, M.cmapA);
     g.beta = Z(1, 0);
     g.C = out(H.R[d].as<zt>(), nt, ps, M.pp, M.pp);
-    zgemm(g, H.st2);
-    HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
+    zgemm(g, side_build(H));
+    HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, side_build(H)));
   }
   // (e) Phi^b = -[R31a | 0] - R33a Phi^a  (line 10, equivalent form)
   {
@@ -878,7 +896,7 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
     if (need_h) {  // h^tau part 1 = h1a + R13a t~a needs only t~a: side stream, beside t~b
       h[d].alloc(sizeof(zt) * (size_t)np * ntau * R);
       HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
-      HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+      HPS_CUDA_CHECK(cudaStreamWaitEvent(side_solve(H), H.ev_fork, 0));
       ZGemm g1 = g;
       g1.M = n1;
       g1.A = op(M.R13a, n3, (int64_t)n1 * n3);
@@ -887,8 +905,8 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
       g1.alpha = Z(1, 0);
       g1.beta = Z(1, 0);
       g1.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp);
-      zgemm(g1, H.st2);
-      HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
+      zgemm(g1, side_solve(H));
+      HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, side_solve(H)));
     }
     g.A = op(M.R33a, n3, s33);
     g.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
@@ -952,14 +970,14 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
     }
     g.C = out(ta, R, cb, M.I3a);
     HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
-    HPS_CUDA_CHECK(cudaStreamWaitEvent(H.st2, H.ev_fork, 0));
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(side_solve(H), H.ev_fork, 0));
     {
       ZGemm g2 = g;  // t3b = Phi^b t + t~b on the side stream (independent of t3a)
       g2.A = op(M.PhiB, ntau, (int64_t)n3 * ntau);
       if (has_s) g2.Cin = op(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
       g2.C = out(tb, R, cb, M.I3b);
-      zgemm(g2, H.st2);
-      HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, H.st2));
+      zgemm(g2, side_solve(H));
+      HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, side_solve(H)));
     }
     zgemm(g, st);  // t3a = Phi^a t + t~a
     fl += 8.0 * np * 2.0 * n3 * ntau * R;
