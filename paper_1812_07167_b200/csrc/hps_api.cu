@@ -631,13 +631,15 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
 
 // side stream for products independent of the current chain; HPS_SIDE=0 (build)
 // or HPS_SIDE_SOLVE=0 (solve) run them on the main stream instead
+// (with per-kernel event timing on, everything stays on the main stream so that each launch's
+// event pair brackets that launch alone)
 cudaStream_t side_build(const hps_handle& H) {
   static const bool off = getenv("HPS_SIDE") && *getenv("HPS_SIDE") == '0';
-  return off ? H.st : H.st2;
+  return off || H.prof.timing ? H.st : H.st2;
 }
 cudaStream_t side_solve(const hps_handle& H) {
   static const bool off = getenv("HPS_SIDE_SOLVE") && *getenv("HPS_SIDE_SOLVE") == '0';
-  return off ? H.st : H.st2;
+  return off || H.prof.timing ? H.st : H.st2;
 }
 
 void build_merge(hps_handle& H, int d) {
