@@ -316,6 +316,139 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) zgj_panel_reg_kernel(c
 // lanes of row k publish it and ONE barrier separates publication from the update.  A pivot
 // with |pivot|^2 < 1e-6 raises *a.pflag (the caller redoes the matrix with partial pivoting).
 // Same interface and outputs as zgj_panel_reg_kernel with identity permutations.
+__device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[192..255])
+__device__ int g_nat_trace_on;
+// ---------------------------------------------------------------------------
+// Blocked natural-order panel: with natural pivots the w pivot rows are rows
+// k0 .. k0+w-1, so the w x w diagonal block is eliminated first on its own (one warp; every CTA
+// does it redundantly, no inter-CTA communication) and records the w scaled pivot rows; every
+// other row then applies the w recorded steps locally (shuffles only, no barrier per step).
+// Grid (ceil(n / 128), batch), 512 threads: 4 lanes x 4 columns per row, 128 rows per CTA.
+// w <= 16.  A pivot with |pivot|^2 < 1e-6 raises *a.pflag.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) zgj_panel_natb_kernel(const PanelArgs a) {
+  constexpr int CPT = 4, NB = 16, RPC = 128;
+  __shared__ zt blk[NB][NB + 1];  // the block rows (panel columns), eliminated in place
+  __shared__ zt phat[NB][NB];     // raw pivot row of step kk divided by its pivot
+  __shared__ zt pinv[NB];         // 1 / pivot of step kk
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  const int b = blockIdx.y, n = a.n, k0 = a.k0, w = a.w;
+  const zt* Xb = a.X + (int64_t)b * a.bsx;
+  zt* Yb = a.Y + (int64_t)b * a.bsy;
+  const int i = blockIdx.x * RPC + wp * 8 + rg;  // this thread's row
+  const bool ntr = g_nat_trace_on == 7 && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0 && k0 == 0;
+  if (ntr) g_nat_trace[0] = clock64();
+  // this thread's 4 panel values (loads in flight during stage 1)
+  zt v[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int j = cg * CPT + c;
+    v[c] = (i < n && j < w) ? Xb[(int64_t)i * a.ldx + k0 + j] : make_double2(0.0, 0.0);
+  }
+  if (wp == 0) {  // ---- stage 1: the diagonal block, in registers (lane: column c, rows 8h .. 8h+7) ----
+    const int c = lane & 15, h = lane >> 4;
+    zt bv[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int r = h * 8 + m;
+      bv[m] = (r < w && c < w) ? Xb[(int64_t)(k0 + r) * a.ldx + k0 + c] : make_double2(0.0, 0.0);
+    }
+    if (ntr) {
+      volatile double sink = bv[0].x + bv[7].y;
+      (void)sink;
+      g_nat_trace[4] = clock64();
+    }
+    bool bad = false;
+#pragma unroll
+    for (int kk = 0; kk < NB; ++kk) {
+      if (kk < w) {
+        const int mk = kk & 7, hk = kk >> 3;
+        // pivot row kk at this lane's column, the pivot, and column kk at this lane's rows
+        const zt pr = make_double2(__shfl_sync(0xffffffffu, bv[mk].x, (hk << 4) | c),
+                                   __shfl_sync(0xffffffffu, bv[mk].y, (hk << 4) | c));
+        const zt pv = make_double2(__shfl_sync(0xffffffffu, bv[mk].x, (hk << 4) | kk),
+                                   __shfl_sync(0xffffffffu, bv[mk].y, (hk << 4) | kk));
+        zt aik[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m)
+          aik[m] = make_double2(__shfl_sync(0xffffffffu, bv[m].x, (h << 4) | kk),
+                                __shfl_sync(0xffffffffu, bv[m].y, (h << 4) | kk));
+        bad = bad || !(fma(pv.x, pv.x, pv.y * pv.y) >= 1e-6);
+        const zt inv = zinv_fast(pv);
+        const zt prn = zmul(pr, inv);  // pr / pivot
+        if (h == 0) phat[kk][c] = c == kk ? make_double2(0.0, 0.0) : prn;
+        if (lane == 0) pinv[kk] = inv;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int r = h * 8 + m;
+          zt nv;
+          if (r == kk) {
+            nv = c == kk ? inv : prn;
+          } else if (c == kk) {
+            const zt g = zmul(aik[m], inv);
+            nv = make_double2(-g.x, -g.y);
+          } else {
+            nv = bv[m];
+            nv.x = fma(-aik[m].x, prn.x, nv.x);
+            nv.x = fma(aik[m].y, prn.y, nv.x);
+            nv.y = fma(-aik[m].x, prn.y, nv.y);
+            nv.y = fma(-aik[m].y, prn.x, nv.y);
+          }
+          bv[m] = nv;
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) blk[h * 8 + m][c] = bv[m];
+    if (lane == 0) s_bad = bad ? 1 : 0;
+    if (ntr) g_nat_trace[5] = clock64();
+  }
+  __syncthreads();
+  if (ntr) g_nat_trace[1] = clock64();
+  // ---- stage 2: rows outside the block apply the w recorded steps ----
+  const bool inblk = i >= k0 && i < k0 + w;
+  if (i < n && !inblk) {
+#pragma unroll
+    for (int kk = 0; kk < NB; ++kk) {
+      if (kk < w) {
+        const int src = (lane & ~3) | (kk >> 2);
+        const zt own = v[kk & 3];
+        const zt t = make_double2(__shfl_sync(0xffffffffu, own.x, src), __shfl_sync(0xffffffffu, own.y, src));
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const zt ph = phat[kk][cg * CPT + c];
+          v[c].x = fma(-t.x, ph.x, v[c].x);
+          v[c].x = fma(t.y, ph.y, v[c].x);
+          v[c].y = fma(-t.x, ph.y, v[c].y);
+          v[c].y = fma(-t.y, ph.x, v[c].y);
+        }
+        if (cg == (kk >> 2)) {  // column kk <- -t / pivot
+          const zt g = zmul(t, pinv[kk]);
+          v[kk & 3] = make_double2(-g.x, -g.y);
+        }
+      }
+    }
+  } else if (i < n) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) v[c] = blk[i - k0][cg * CPT + c];
+  }
+  if (ntr) g_nat_trace[2] = clock64();
+  if (i < n) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int j = cg * CPT + c;
+      if (j < w) Yb[(int64_t)i * a.ldy + k0 + j] = v[c];
+    }
+    if (cg == 0) write_maps(a, b, i, i);
+  }
+  if (blockIdx.x == 0) {
+    if (tid < w) a.piv[(int64_t)b * n + k0 + tid] = k0 + tid;
+    if (tid == 0 && s_bad) atomicExch(a.pflag, 1);
+  }
+  if (ntr) g_nat_trace[3] = clock64();
+}
+
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(512, 1) zgj_panel_nat_kernel(const PanelArgs a) {
   constexpr int CPT = 4, NB = 16, RPT = 4;
@@ -403,8 +536,6 @@ __global__ void __launch_bounds__(512, 1) zgj_panel_nat_kernel(const PanelArgs a
 // owner lanes of row k publish it in their CTA's shared memory, one cluster barrier, and every
 // CTA reads it through distributed shared memory: the per-step FP64 work of a 448-row panel is
 // spread over 4 SMs instead of 1.
-__device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[192..255])
-__device__ int g_nat_trace_on;
 template <int CPT, int LPR = 4>
 __global__ void __launch_bounds__(512, 1) zgj_panel_natc_kernel(const PanelArgs a) {
   // LPR lanes per row (CPT columns each), RPC = 512 / LPR rows per CTA
@@ -2732,7 +2863,10 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
     pa.pflag = flag;
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)w * w * batch, 32.0 * n * (double)w * batch, st);
-      if (!use_c) {
+      static const bool blocked = !(getenv("HPS_NATB") && *getenv("HPS_NATB") == '0');
+      if (blocked && wmax == 16) {
+        zgj_panel_natb_kernel<<<dim3((n + 127) / 128, batch), 512, 0, st>>>(pa);
+      } else if (!use_c) {
         zgj_panel_nat_kernel<<<batch, 512, 0, st>>>(pa);
       } else {
         cudaLaunchConfig_t cfg = {};
