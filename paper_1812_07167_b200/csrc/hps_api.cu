@@ -716,7 +716,8 @@ void build_merge(hps_handle& H, int d) {
   // W is formed again and inverted with partial pivoting.
   static const int nat_min = getenv("HPS_NAT_MIN") ? atoi(getenv("HPS_NAT_MIN")) : 200;
   bool done = false;
-  if (n3 >= nat_min && n3 <= 512) {
+  static const int nat_max = getenv("HPS_NAT_MAX") ? atoi(getenv("HPS_NAT_MAX")) : 1 << 30;
+  if (n3 >= nat_min && n3 <= nat_max) {
     ws.alloc(std::max<size_t>(zgj_natural_workspace_bytes(n3, np), 16));
     DevBuf flag;
     flag.alloc(sizeof(int));

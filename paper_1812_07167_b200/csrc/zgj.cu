@@ -2835,7 +2835,7 @@ int zgj_regime_of(int n, int nbox) { return choose_regime(n, nbox); }
 void zgj_force_regime(int r) { g_regime_force = r; }
 
 // Natural-order blocked Gauss-Jordan: 16-column zgj_panel_nat_kernel panels and
-// the blocked explicit-swap update with identity maps.  n <= 512.  Workspace as
+// the blocked explicit-swap update with identity maps (any n).  Workspace as
 // zgj_workspace_bytes(n, batch) for the blocked regime; *flag (device) is set to 1 when a pivot
 // failed the check — out is then not the inverse and A is destroyed (the caller keeps a copy).
 void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
