@@ -125,11 +125,12 @@ def test_natural_order_merge_inverses_all_levels():
         print(worst)
     """)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, HPS_NAT_MIN="14", PYTHONPATH=root)
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
-                         timeout=900)
-    assert out.returncode == 0, out.stderr[-2000:]
-    assert float(out.stdout.strip().splitlines()[-1]) < TOL
+    for extra in ({}, {"HPS_NAT_FORCE_FAIL": "1"}):  # second run: every level takes the pivoted fallback
+        env = dict(os.environ, HPS_NAT_MIN="14", PYTHONPATH=root, **extra)
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                             timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert float(out.stdout.strip().splitlines()[-1]) < TOL
 
 
 def test_leaf_path_selection():
