@@ -25,6 +25,10 @@ namespace {
 
 constexpr int RL_NB = 28;  // panel width of the real Gauss-Jordan
 
+// 1: the natural-order elimination reports a failed pivot at the first check (tests the in-kernel
+// fallback to partial pivoting; HPS_DGJ_FORCE_BAD=1)
+__constant__ int g_dgj_force_bad;
+
 // phase timeline of CTA 0 (clock64), printed by launch_leaf_real when HPS_LR_TRACE=1 (debug)
 __device__ long long g_lr_trace[64];
 #define LR_MARK(i)                                                   \
@@ -129,7 +133,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
     pstep[tid] = PIV ? 1 << 30 : tid;
     plist[tid] = tid;
   }
-  if (tid == 0) s_bad = 0;
+  if (tid == 0) s_bad = PIV ? 0 : g_dgj_force_bad;
   if (tid < 32) wkey[0][tid] = 0u;
   __syncthreads();
   RPanels P;
@@ -987,6 +991,8 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
   const size_t smemB = sizeof(double) * (size_t)RLeafSmem(p).total;
   static bool attr = false;
   if (!attr) {
+    const int force_bad = getenv("HPS_DGJ_FORCE_BAD") && *getenv("HPS_DGJ_FORCE_BAD") == '1';
+    HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_dgj_force_bad, &force_bad, sizeof(int)));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(leaf_real_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));

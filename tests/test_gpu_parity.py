@@ -97,11 +97,14 @@ def test_leaf_real_elimination_forced_pivoting():
         print(max(rel(Psi, lo["Psi"]), rel(Y, lo["Y"]), rel(S.R(3), lo["R"])))
     """)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, HPS_DGJ_PIVOT="1", PYTHONPATH=root)
-    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
-                         timeout=600)
-    assert out.returncode == 0, out.stderr[-2000:]
-    assert float(out.stdout.strip().splitlines()[-1]) < TOL
+    # pivoting from the start; and the natural-order attempt failing its first pivot check (the
+    # in-kernel fallback redoes the leaf with partial pivoting)
+    for extra in ({"HPS_DGJ_PIVOT": "1"}, {"HPS_DGJ_FORCE_BAD": "1"}):
+        env = dict(os.environ, PYTHONPATH=root, **extra)
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert float(out.stdout.strip().splitlines()[-1]) < TOL
 
 
 def test_natural_order_merge_inverses_all_levels():
