@@ -71,9 +71,16 @@ class ClockSampler:
 
     def __enter__(self):
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=self.f, stderr=subprocess.DEVNULL)
+            import shutil
+            cmd = ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                   "-lms", "20"]
+            if shutil.which("stdbuf"):   # line-buffered: samples reach the file as they are taken
+                cmd = ["stdbuf", "-oL"] + cmd
+            self.p = subprocess.Popen(cmd, stdout=self.f, stderr=subprocess.DEVNULL)
+            # the timed region of a small config lasts tens of ms: wait until the sampler runs
+            t0 = time.time()
+            while time.time() - t0 < 3.0 and os.path.getsize(self.f.name) == 0:
+                time.sleep(0.01)
         except Exception:
             self.p = None
         return self
