@@ -1065,6 +1065,8 @@ __global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A
 // writes it once; T and Z live in shared memory.
 // ---------------------------------------------------------------------------
 constexpr int WS_NB = 28, WS_NMAX = 240;
+// 1: the leaf Schur inverse pivots from the start (HPS_SEQ_PIVOT=1; tests of the fallback path)
+__constant__ int g_seq_pivot;
 // optional timeline of CTA 0 (clock64 per milestone, hps_debug_ws_trace): [panel][10]
 __device__ long long g_ws_trace[16 * 16];
 __device__ int g_ws_trace_on;
@@ -1994,9 +1996,14 @@ __global__ void zgj_implicit_out_kernel(const zt* __restrict__ M, int64_t ldm, i
 // steps with the tensor-core update (zgj_ws_kernel) stretches the pivot steps 2-4x; here the
 // pivot steps run alone and the update runs at 4 warps per sub-partition.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
-                                                         zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
-                                                         int* __restrict__ info, const WsFinish fin) {
+// NAT: natural order (row k is the pivot of step k, one barrier per step) for the leaf Schur
+// complement S assembled by the kernel itself (fin.c): in the configs' regimes natural-order
+// elimination of S keeps every pivot >= 0.37 of its original diagonal; a pivot
+// below 0.05 of it makes the body return false and the caller re-assembles S and pivots.
+template <bool NAT>
+__device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, int64_t bs, zt* __restrict__ out,
+                                             int64_t ldo, int64_t obs, int n, int* __restrict__ info,
+                                             const WsFinish& fin) {
   constexpr int NB = WS_NB, CPT = WS_NB / 4;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int mtr = (n + 15) & ~15, zs = ws_zs(n);
@@ -2005,13 +2012,19 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
   __shared__ zt prow4[2][NB];
   __shared__ __align__(16) unsigned wkey[2][16];
   __shared__ int pstep[256], plist[256], colmap[WS_NMAX + 16];
+  __shared__ double diag2[NAT ? 256 : 1];  // |S_kk|^2 of the assembled S (NAT)
+  __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
   zt* M = A + (int64_t)blockIdx.x * bs;
   WsPanels P;
   P.npan = (n + NB - 1) / NB;
   P.base = n / P.npan;
   P.rem = n % P.npan;
-  if (tid < 256) pstep[tid] = 1 << 30;
+  if (tid < 256) {
+    pstep[tid] = NAT ? tid : 1 << 30;
+    if (NAT) plist[tid] = tid;
+  }
+  if (tid == 0) s_bad = 0;
   if (fin.c) {  // assemble S in place (as zgj_ws_kernel)
     const int q = fin.p - 2;
     const zt* Lx = fin.K;
@@ -2031,6 +2044,7 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
           const zt cv = cl[(iy + 1) * fin.p + ix + 1];
           v.x -= fin.kappa2 * cv.x;
           v.y -= fin.kappa2 * cv.y;
+          if (NAT) diag2[r] = fma(v.x, v.x, v.y * v.y);
         }
         M[(int64_t)r * lda + cc] = v;
       }
@@ -2065,23 +2079,26 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
         const int kk = cga * CPT + s;
         if (kk < w) {
           const int k = k0 + kk, par = k & 1;
-          unsigned key = 0u;
-          if (act) {
+          int r = k;
+          if (!NAT) {
+            unsigned key = 0u;
+            if (act) {
 #pragma unroll
-            for (int q = 0; q < 2; ++q)
-              if (!piv[q] && rq[q] < n) key = max(key, pivot_key(a[q][s], rq[q], true));
-          }
-          key = __reduce_max_sync(0xffffffffu, key);
-          if (lane == 0) wkey[par][wp] = key;
-          __syncthreads();
-          unsigned best = 0u;
+              for (int q = 0; q < 2; ++q)
+                if (!piv[q] && rq[q] < n) key = max(key, pivot_key(a[q][s], rq[q], true));
+            }
+            key = __reduce_max_sync(0xffffffffu, key);
+            if (lane == 0) wkey[par][wp] = key;
+            __syncthreads();
+            unsigned best = 0u;
 #pragma unroll
-          for (int g4 = 0; g4 < 4; ++g4) {
-            const uint4 kq = *reinterpret_cast<const uint4*>(&wkey[par][4 * g4]);
-            best = max(best, max(max(kq.x, kq.y), max(kq.z, kq.w)));
+            for (int g4 = 0; g4 < 4; ++g4) {
+              const uint4 kq = *reinterpret_cast<const uint4*>(&wkey[par][4 * g4]);
+              best = max(best, max(max(kq.x, kq.y), max(kq.z, kq.w)));
+            }
+            if ((best & ~511u) == 0u) singular = true;
+            r = 511 - (int)(best & 511u);
           }
-          if ((best & ~511u) == 0u) singular = true;
-          const int r = 511 - (int)(best & 511u);
           if (wp == (r >> 4) && rg == (r & 7)) {  // the 4 lanes of row r publish it raw
             const int qq = (r >> 3) & 1;
 #pragma unroll
@@ -2090,12 +2107,16 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
 #pragma unroll
                 for (int c = 0; c < CPT; ++c) prow4[par][cg * CPT + c] = a[q][c];
               }
-            if (cg == 0) {
+            if (!NAT && cg == 0) {
               pstep[r] = k;
               plist[k] = r;
             }
           }
           __syncthreads();
+          if (NAT && tid == 0) {
+            const zt pv = prow4[par][kk];
+            if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 0.0025 * diag2[k])) s_bad = 1;
+          }
           if (warp_live) {
             const zt inv = zinv_fast(prow4[par][kk]);
             zt g[2];
@@ -2145,6 +2166,10 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
           if (j < w && rq[q] < n) M[(int64_t)rq[q] * lda + k0 + j] = a[q][c];
         }
       }
+    if (NAT) {
+      __syncthreads();
+      if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
+    }
     if (p + 1 == P.npan && nv == 0) break;
     // ---------------- update: C(i, J) = [i not a pivot of p] C(i, J) + T(i,:) Z(:, J) -------------
     for (int v = tid; v < nv + 16; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
@@ -2239,6 +2264,17 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
   WS_MARK(15, 0);
   ws_output(M, lda, out, ldo, obs, n, fin, plist, pstep, smem_raw);
   WS_MARK(15, 1);
+  return true;
+}
+
+__global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
+                                                         zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
+                                                         int* __restrict__ info, const WsFinish fin) {
+  if (fin.c && !g_seq_pivot && n <= 256) {
+    if (zgj_seq_body<true>(A, lda, bs, out, ldo, obs, n, info, fin)) return;
+    __syncthreads();
+  }
+  zgj_seq_body<false>(A, lda, bs, out, ldo, obs, n, info, fin);
 }
 
 // pi = S_{n-1} o ... o S_0 (one thread per matrix)
@@ -2683,6 +2719,8 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
   if (!zgj_leaf_fused_applies(p, batch)) return false;
   static bool wattr = false;
   if (!wattr) {
+    const int piv = getenv("HPS_SEQ_PIVOT") && *getenv("HPS_SEQ_PIVOT") == '1';
+    HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_seq_pivot, &piv, sizeof(int)));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)ws_smem(WS_NMAX)));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

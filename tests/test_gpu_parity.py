@@ -136,6 +136,36 @@ def test_natural_order_merge_inverses_all_levels():
         assert float(out.stdout.strip().splitlines()[-1]) < TOL
 
 
+def test_leaf_schur_natural_and_pivoted_paths():
+    """The complex interior Schur inverse (leaf_mode 0 with complex c) runs in natural order
+    (DESIGN.md 3.12); HPS_SEQ_PIVOT=1 (fresh process) forces the pivoted path. Both vs the oracle."""
+    import os, subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import os, sys
+        sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+        import numpy as np, oracle
+        from paper_1812_07167_b200 import hps
+        from test_gpu_parity import problem, rel
+        g, c, s, t = problem(2, 1, 16, 7.0, 7.0 + 1j)
+        c = c + 0.05j
+        S = hps.Solver(g, 16, 7.0, 7.0 + 1j, c, keep_all_R=True)
+        assert S.leaf_path() == 0
+        w = 0.0
+        for leaf in range(2):
+            Psi, Y = S.leaf_ops(leaf)
+            lo = oracle.leaf(16, 0.5, 1.0, 7.0, 7.0 + 1j, c[leaf])
+            w = max(w, rel(Psi, lo["Psi"]), rel(Y, lo["Y"]), rel(S.R(2 + leaf), lo["R"]))
+        print(w)
+    """)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for extra in ({}, {"HPS_SEQ_PIVOT": "1"}):
+        env = dict(os.environ, PYTHONPATH=root, **extra)
+        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert float(out.stdout.strip().splitlines()[-1]) < TOL
+
+
 def test_leaf_path_selection():
     """Auto mode takes the real elimination only for real c below the first interior resonance;
     leaf_mode 3 refuses complex c."""
