@@ -17,6 +17,7 @@
 #include <complex>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -99,6 +100,87 @@ namespace {
 // level are freed without synchronising and re-used by the next build without a driver call.
 thread_local cudaStream_t g_alloc_stream = nullptr;
 
+// Blocks of >= 256 MB (the leaf operators, the merge operators of the big levels) are parked in a
+// process-wide cache when a buffer is released and handed to the next request of a similar size:
+// a large cudaMallocAsync that has to map new physical memory took 0.25 s for the 16.6 GB leaf
+// store of C3 (HPS_DEBUG_ALLOC), and the stream-ordered pool did not reliably reuse freed blocks
+// across handles (each handle owns its stream).  Stream order is kept with an event recorded at
+// release and waited on at reuse.
+constexpr size_t kBigBlock = (size_t)256 << 20;
+struct BigBlock {
+  int dev;
+  void* p;
+  size_t bytes;
+  cudaEvent_t ev;
+};
+std::mutex g_big_mu;
+std::vector<BigBlock> g_big;
+size_t g_big_total = 0;
+constexpr size_t kBigCacheMax = (size_t)96 << 30;  // parked bytes per process
+
+void big_free_block(BigBlock& b) {
+  cudaEventSynchronize(b.ev);
+  cudaEventDestroy(b.ev);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(b.dev);
+  cudaFree(b.p);
+  cudaSetDevice(cur);
+}
+
+void* big_take(size_t n, cudaStream_t st, size_t& got) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  int best = -1;
+  for (int k = 0; k < (int)g_big.size(); ++k)
+    if (g_big[k].dev == dev && g_big[k].bytes >= n && g_big[k].bytes <= n + n / 4 &&
+        (best < 0 || g_big[k].bytes < g_big[best].bytes))
+      best = k;
+  if (best < 0) return nullptr;
+  BigBlock b = g_big[best];
+  g_big.erase(g_big.begin() + best);
+  g_big_total -= b.bytes;
+  cudaStreamWaitEvent(st, b.ev, 0);
+  cudaEventDestroy(b.ev);
+  got = b.bytes;
+  return b.p;
+}
+
+void big_put(void* p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  BigBlock b{dev, p, bytes, nullptr};
+  if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(b.ev, st) != cudaSuccess) {
+    cudaGetLastError();
+    if (b.ev) cudaEventDestroy(b.ev);
+    cudaFreeAsync(p, st);
+    return;
+  }
+  std::vector<BigBlock> evict;
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    g_big.push_back(b);
+    g_big_total += bytes;
+    while (g_big_total > kBigCacheMax && g_big.size() > 1) {  // oldest first
+      evict.push_back(g_big.front());
+      g_big_total -= g_big.front().bytes;
+      g_big.erase(g_big.begin());
+    }
+  }
+  for (auto& e : evict) big_free_block(e);
+}
+
+void big_flush() {  // on an allocation failure: give the parked blocks back
+  std::vector<BigBlock> all;
+  {
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    all.swap(g_big);
+    g_big_total = 0;
+  }
+  for (auto& e : all) big_free_block(e);
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -109,7 +191,12 @@ struct DevBuf {
   DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; o.bytes = 0; }
   ~DevBuf() { release(); }
   void release() {
-    if (p) cudaFreeAsync(p, st);
+    if (p) {
+      if (bytes >= kBigBlock)
+        big_put(p, bytes, st);
+      else
+        cudaFreeAsync(p, st);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -118,9 +205,24 @@ struct DevBuf {
     if (n == 0) return;
     st = g_alloc_stream;
     static const bool dbg = getenv("HPS_DEBUG_ALLOC") && *getenv("HPS_DEBUG_ALLOC") == '1';
+    static const bool nocache = getenv("HPS_BIG_CACHE") && *getenv("HPS_BIG_CACHE") == '0';
     const auto t0 = std::chrono::steady_clock::now();
-    cudaError_t e = cudaMallocAsync(&p, n, st);
-    if (dbg && n >= ((size_t)1 << 28))
+    if (n >= kBigBlock && !nocache) {
+      size_t got = 0;
+      p = big_take(n, st, got);
+      if (p) {
+        bytes = got;
+        if (dbg) fprintf(stderr, "[alloc] %.2f GB reused\n", n / 1e9);
+        return;
+      }
+    }
+    cudaError_t e = n >= kBigBlock && !nocache ? cudaMalloc(&p, n) : cudaMallocAsync(&p, n, st);
+    if (e != cudaSuccess) {  // the parked blocks may be what is missing
+      cudaGetLastError();
+      big_flush();
+      e = n >= kBigBlock && !nocache ? cudaMalloc(&p, n) : cudaMallocAsync(&p, n, st);
+    }
+    if (dbg && n >= kBigBlock)
       fprintf(stderr, "[alloc] %.2f GB in %.3f ms\n", n / 1e9,
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
     if (e != cudaSuccess) {
