@@ -116,7 +116,17 @@ struct BigBlock {
 std::mutex g_big_mu;
 std::vector<BigBlock> g_big;
 size_t g_big_total = 0;
-constexpr size_t kBigCacheMax = (size_t)96 << 30;  // parked bytes per process
+// parked bytes per process: up to 90 % of the device (a failed allocation flushes the cache first,
+// so parked blocks never cost a run its memory; a lower cap made C4 free and re-map every step)
+size_t big_cache_max() {
+  static size_t cap = 0;
+  if (!cap) {
+    size_t fr = 0, tot = 0;
+    cap = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? tot / 10 * 9 : ((size_t)96 << 30);
+    cudaGetLastError();
+  }
+  return cap;
+}
 
 void big_free_block(BigBlock& b) {
   cudaEventSynchronize(b.ev);
@@ -162,7 +172,7 @@ void big_put(void* p, size_t bytes, cudaStream_t st) {
     std::lock_guard<std::mutex> lk(g_big_mu);
     g_big.push_back(b);
     g_big_total += bytes;
-    while (g_big_total > kBigCacheMax && g_big.size() > 1) {  // oldest first
+    while (g_big_total > big_cache_max() && g_big.size() > 1) {  // oldest first
       evict.push_back(g_big.front());
       g_big_total -= g_big.front().bytes;
       g_big.erase(g_big.begin());
