@@ -247,6 +247,13 @@ int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A
                       const hps_c128* Cin, hps_c128* C, hps_c128 alpha, hps_c128 beta, int reps, double* ms);
 
 void hps_free(hps_handle* h);
+
+/* Device blocks of >= 256 MB freed by hps_free (leaf and merge operator stores, solve vectors) are
+ * kept in a process-wide cache and handed to later handles of the same shapes (a fresh mapping of
+ * tens of GB costs ~0.25 s).  The cache holds at most 90 % of the device and is
+ * emptied before any allocation is allowed to fail.  hps_release_cache returns every cached block
+ * to the driver now (synchronises the devices that own them).  Returns 0. */
+int hps_release_cache(void);
 const char* hps_last_error(void);
 
 #ifdef __cplusplus

@@ -1996,4 +1996,9 @@ int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A
 
 void hps_free(hps_handle* h) { delete h; }
 
+int hps_release_cache(void) {
+  big_flush();
+  return HPS_OK;
+}
+
 }  // extern "C"

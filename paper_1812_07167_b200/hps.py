@@ -40,7 +40,7 @@ class hps_opts(C.Structure):
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_last_time_ms", "hps_last_launches",
            "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
-           "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free",
+           "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free", "hps_release_cache",
            "hps_last_error"]
 
 KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout", "zgj_fused", "leaf_gj", "zgemv"]
@@ -133,6 +133,11 @@ def leaf_nodes(g, p):
     del n
     _check(lib().hps_leaf_nodes(C.byref(g), p, X.ctypes.data, Y.ctypes.data))
     return X, Y
+
+
+def release_cache():
+    """Return the cached large device blocks of freed handles to the driver (hps_release_cache)."""
+    _check(lib().hps_release_cache())
 
 
 def root_boundary_nodes(g, p, basis=0):

@@ -286,6 +286,20 @@ def test_gl_boundary_basis_sharded():
         assert rel(u, dist.slice_leaves(u_ref, g, sub, i0, j0)) < 1e-11
 
 
+def test_block_cache_reuse_and_release():
+    """Large device blocks (>= 256 MB: the 32x16-leaf store here) are re-used by the next handle and
+    returned by hps_release_cache; results are identical either way."""
+    g, c, s, t = problem(32, 16, 16, 20.0, 20.0 + 1j, nrhs=1)
+    u = []
+    for k in range(3):
+        S = hps.Solver(g, 16, 20.0, 20.0 + 1j, c)
+        u.append(S.solve(s, t))
+        S.close()
+        if k == 1:
+            hps.release_cache()
+    assert np.array_equal(u[0], u[1]) and np.array_equal(u[0], u[2])
+
+
 def test_torch_device_buffers():
     import torch
     g, c, s, t = problem(4, 2, 8, 5.0, 5.0)
