@@ -571,10 +571,12 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   // Tile choice from the sweep in profiles/r01_gemm_tune.txt: 32x32 tiles (5 CTAs / SM) win
   // for the short-K and Cin-heavy shapes of the merges and the Gauss-Jordan updates; 64x32 tiles
   // win once K is long enough to amortise the tile loads.
+  const int64_t tiles32 = (int64_t)((g.M + 31) / 32) * ((g.N + 31) / 32) * g.batch;
+  static const bool small_k16 = !(getenv("HPS_GEMM_SMALLK") && *getenv("HPS_GEMM_SMALLK") == '0');
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
-  else if (g.M <= 16)
-    launch<16, 16, 8, 8>(g, st);
+  else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * 148))
+    launch<16, 16, 8, 8>(g, st);  // short K on a grid of few 32x32 tiles: more, smaller CTAs
   else if (g.K >= 512)
     launch<64, 32, 32, 16>(g, st);
   else
