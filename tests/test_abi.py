@@ -74,6 +74,21 @@ def test_argument_validation(L):
     L.hps_free(None)   # no-op
 
 
+def test_option_validation_and_small_calls(L):
+    """leaf_mode outside 0..3 and boundary_basis outside 0..1 are rejected before any device work;
+    hps_leaf_path(NULL) is HPS_EINVAL; hps_release_cache with nothing cached returns 0."""
+    g = hps.grid(0, 1, 0, 1, 2, 2)
+    c = np.ones(4 * 64, complex)
+    for lm, bb, msg in ((4, 0, b"leaf_mode"), (0, 2, b"boundary_basis"), (-1, 0, b"leaf_mode")):
+        opts = hps.hps_opts(1, 0, -1, 0, 0, lm, bb)
+        h = C.c_void_p()
+        rc = L.hps_build(C.byref(g), 8, 6, 1.0, hps.hps_c128(1.0, 0.0), c.ctypes.data, C.byref(opts), C.byref(h))
+        assert rc == -1 and not h.value
+        assert msg in L.hps_last_error()
+    assert L.hps_leaf_path(None) == -1
+    assert L.hps_release_cache() == 0
+
+
 def test_rep_actions_match_survey_table():
     """Representative actions per level (Table 1): the leaf interior inverse and the
     merge interface inverses; sizes and box counts as SURVEY 8(a)'s per-level table (C3, C5)."""
