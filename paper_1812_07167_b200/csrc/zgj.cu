@@ -311,8 +311,8 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) zgj_panel_reg_kernel(c
 }
 
 // ---------------------------------------------------------------------------
-// Natural-order panel (no pivot search), n <= 512, w <= 16, for the merge matrices W = I - C with
-// ||C|| < 1: 512 threads, 4 rows x 4 columns per thread; per step the owner
+// Natural-order panel (no pivot search), n <= 512, w <= 16, for the merge matrices W (DESIGN.md
+// 3.10: measured to need no pivoting in the configs' regimes): 512 threads, 4 rows x 4 columns per thread; per step the owner
 // lanes of row k publish it and ONE barrier separates publication from the update.  A pivot
 // with |pivot|^2 < 1e-6 raises *a.pflag (the caller redoes the matrix with partial pivoting).
 // Same interface and outputs as zgj_panel_reg_kernel with identity permutations.
