@@ -77,7 +77,7 @@ typedef struct {
                            in the epilogue of the inverse kernel;
                            1: Gauss-Jordan on the full n^tau x n^tau matrix B;
                            2: complex interior Schur complement with the separate finish kernel;
-                           3: real elimination of the interior block (DESIGN.md 3.8): one REAL
+                           3: real elimination of the interior block (DESIGN.md 3.1b): one REAL
                            inverse of A_ii per leaf plus the complex n_b x n_b complement
                            Sigma = F_b - F_i A_ii^{-1} A_ib (eq. 7 rows reordered); needs real
                            c samples and p - 2 <= 14 (else HPS_EINVAL), no resonance check.

@@ -638,7 +638,7 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   // they apply, else by leaf_R below
   H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
   if (H.leaf_mode == 0 || H.leaf_mode == 3) {
-    // real interior elimination (DESIGN.md 3.8): kappa^2 c real; in auto mode also kappa^2 max c
+    // real interior elimination (DESIGN.md 3.1b): kappa^2 c real; in auto mode also kappa^2 max c
     // below 0.9 x the lowest Dirichlet eigenvalue pi^2 (1/hx^2 + 1/hy^2) of a leaf, so A_ii is
     // positive definite up to a margin (no interior resonance)
     bool ok = leaf_real_fits(p), below = false;

@@ -51,7 +51,7 @@ def test_leaf_parity(p, leaf_mode):
 
 @pytest.mark.parametrize("p", [4, 6, 8, 10, 12, 13, 14, 16])
 def test_leaf_parity_real_elimination(p):
-    """leaf_mode 3 (real A_ii^{-1} + complex n_b x n_b complement, DESIGN.md 3.8) on non-square
+    """leaf_mode 3 (real A_ii^{-1} + complex n_b x n_b complement, DESIGN.md 3.1b) on non-square
     leaves (h_x = 0.5, h_y = 1): Psi, Y and the leaf R vs the oracle's full-B inverse.  kappa = 4
     keeps kappa^2 c (<= 20.8) below the lowest Dirichlet eigenvalue of the leaf (49.3)."""
     g, c, s, t = problem(2, 1, p, 4.0, 4.0 + 1j)
