@@ -157,16 +157,21 @@ void* big_take(size_t n, cudaStream_t st, size_t& got) {
   return b.p;
 }
 
-void big_put(void* p, size_t bytes, cudaStream_t st) {
-  int dev = 0;
-  cudaGetDevice(&dev);
+void big_put(void* p, size_t bytes, cudaStream_t st, int dev) {
   BigBlock b{dev, p, bytes, nullptr};
-  if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) != cudaSuccess || cudaEventRecord(b.ev, st) != cudaSuccess) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);  // the event must live on the stream's device
+  const bool ok =
+      cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) == cudaSuccess && cudaEventRecord(b.ev, st) == cudaSuccess;
+  if (!ok) {
     cudaGetLastError();
     if (b.ev) cudaEventDestroy(b.ev);
-    cudaFreeAsync(p, st);
-    return;
+    cudaStreamSynchronize(st);
+    cudaFree(p);
   }
+  if (cur != dev) cudaSetDevice(cur);
+  if (!ok) return;
   std::vector<BigBlock> evict;
   {
     std::lock_guard<std::mutex> lk(g_big_mu);
@@ -195,15 +200,16 @@ struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   cudaStream_t st = nullptr;
+  int dev = 0;  // device of the allocation (the cache is per device)
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), dev(o.dev) { o.p = nullptr; o.bytes = 0; }
   ~DevBuf() { release(); }
   void release() {
     if (p) {
       if (bytes >= kBigBlock)
-        big_put(p, bytes, st);
+        big_put(p, bytes, st, dev);
       else
         cudaFreeAsync(p, st);
     }
@@ -214,6 +220,7 @@ struct DevBuf {
     release();
     if (n == 0) return;
     st = g_alloc_stream;
+    cudaGetDevice(&dev);
     static const bool dbg = getenv("HPS_DEBUG_ALLOC") && *getenv("HPS_DEBUG_ALLOC") == '1';
     static const bool nocache = getenv("HPS_BIG_CACHE") && *getenv("HPS_BIG_CACHE") == '0';
     const auto t0 = std::chrono::steady_clock::now();
