@@ -25,6 +25,13 @@ namespace {
 
 constexpr int RL_NB = 28;  // panel width of the real Gauss-Jordan
 
+// Plain global loads for data this CTA (or an earlier kernel) wrote: ld.global.cg compiles to
+// LDG.STRONG.GPU, whose ordering against the CTA's outstanding stores showed up as "membar" stalls
+template <typename T>
+__device__ __forceinline__ T ldplain(const T* p) {
+  return *p;
+}
+
 // 1: the natural-order elimination reports a failed pivot at the first check (tests the in-kernel
 // fallback to partial pivoting; HPS_DGJ_FORCE_BAD=1)
 __constant__ int g_dgj_force_bad;
@@ -160,7 +167,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
 #pragma unroll
         for (int cc = 0; cc < CPT; ++cc) {
           const int j = cg * CPT + cc;
-          a[t][cc] = (rq[t] < n && j < w) ? __ldcg(M + (int64_t)rq[t] * n + k0 + j) : 0.0;
+          a[t][cc] = (rq[t] < n && j < w) ? ldplain(M + (int64_t)rq[t] * n + k0 + j) : 0.0;
         }
       for (int cga = 0; cga * CPT < w; ++cga) {
         const bool act = cg == cga;
@@ -282,7 +289,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
         for (int h = 0; h < 2; ++h) {
           const int v = vb + t * 8 + (lane & 3) * 2 + h;
           U.col[t][h] = v < nv ? colmap[v] : -1;
-          U.seed[t][h] = (rok && U.col[t][h] >= 0) ? __ldcg(M + (int64_t)rc * n + U.col[t][h]) : 0.0;
+          U.seed[t][h] = (rok && U.col[t][h] >= 0) ? ldplain(M + (int64_t)rc * n + U.col[t][h]) : 0.0;
         }
     };
     Unit cur, nxt;
@@ -900,7 +907,7 @@ __global__ void __launch_bounds__(512, 1) leaf_real_ops_kernel(const RLeafArgs A
     blk_mma<1, true>(
         MTi, 2 * jw, K4, [&](int r) { return Ps + r * L.PS; }, 1, Wb, L.WL,
         [&](int r, int c, double& a0, double& a1) {
-          a0 = r < ni ? __ldcg(Mg + (size_t)plist[r] * ni + pstep[j0 + (c >> 1)]) : 0.0;
+          a0 = r < ni ? ldplain(Mg + (size_t)plist[r] * ni + pstep[j0 + (c >> 1)]) : 0.0;
           a1 = 0.0;
         },
         [&](int r, int c, double a0, double a1) {
