@@ -183,6 +183,14 @@ __device__ __forceinline__ void row_rotate(zt (&row)[NB]) {
 }
 
 // 1 / z for the pivot: conj(z) / |z|^2 with an IEEE round-to-nearest reciprocal.
+// Plain global loads for data the same CTA wrote (after a barrier) or an earlier kernel wrote:
+// ld.global.cg compiles to LDG.STRONG.GPU, whose ordering against the CTA's outstanding stores
+// showed up as "membar" stalls in the single-CTA Gauss-Jordan kernels.
+template <typename T>
+__device__ __forceinline__ T ldplain(const T* p) {
+  return *p;
+}
+
 __device__ __forceinline__ zt zinv_fast(zt a) {
   // 1/|a|^2: hardware reciprocal estimate (MUFU.RCP64H) refined by two branch-free Newton steps
   // (relative error ~1e-28 before rounding; pivots are never denormal here).
@@ -1132,7 +1140,7 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
     // A^{-1}(k, j) = M(plist[k], pstep[j])
     for (int e = tid; e < n * n; e += 512) {
       const int k = e / n, j = e - k * n;
-      __stcs(&ob[(int64_t)k * ldo + j], __ldcg(M + (int64_t)plist[k] * lda + pstep[j]));
+      __stcs(&ob[(int64_t)k * ldo + j], ldplain(M + (int64_t)plist[k] * lda + pstep[j]));
     }
     return;
   }
@@ -1185,7 +1193,7 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
     emark(0);
     for (int e = tid; e < nl * q * ni; e += 512) {
       const int t = e / ni, j = e - t * ni;  // t = line-local row l*q + t'
-      const zt v = __ldcg(M + (int64_t)plist[kx0 * q + t] * lda + pstep[j]);
+      const zt v = ldplain(M + (int64_t)plist[kx0 * q + t] * lda + pstep[j]);
       C[e] = v;
       __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + nb + j], v);  // Y_i
     }
@@ -1387,7 +1395,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           const int j = cg * CPT + c;
-          a[q][c] = (rq[q] < n && j < w) ? __ldcg(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
+          a[q][c] = (rq[q] < n && j < w) ? ldplain(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
         }
       for (int cga = 0; cga * CPT < w; ++cga) {
         const bool act = cg == cga;
@@ -1545,7 +1553,7 @@ __global__ void __launch_bounds__(512, 1) zgj_ws_kernel(zt* __restrict__ A, int6
             for (int h = 0; h < 2; ++h) {
               const int v = vb + t * 8 + h;
               U.col[t][h] = v < v1 ? colmap[v] : -1;
-              U.seed[t][h] = __ldcg(rowp + max(U.col[t][h], 0));  // masked at use: no wait here
+              U.seed[t][h] = ldplain(rowp + max(U.col[t][h], 0));  // masked at use: no wait here
             }
         };
         Unit cur, nxt;
@@ -2069,7 +2077,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const int j = cg * CPT + c;
-        a[q][c] = (rq[q] < n && j < w) ? __ldcg(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
+        a[q][c] = (rq[q] < n && j < w) ? ldplain(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
       }
     for (int cga = 0; cga * CPT < w; ++cga) {
       const bool act = cg == cga;
@@ -2202,7 +2210,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
         for (int h = 0; h < 2; ++h) {
           const int v = vb + t * 8 + h;
           U.col[t][h] = v < nv ? colmap[v] : -1;
-          U.seed[t][h] = __ldcg(rowp + max(U.col[t][h], 0));
+          U.seed[t][h] = ldplain(rowp + max(U.col[t][h], 0));
         }
     };
     Unit cur, nxt;
