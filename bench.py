@@ -258,7 +258,7 @@ def run_hps(args, rank, world, dist):
                  for k, v in probe["kstats"].items()}
     out = {
         "metric": METRIC, "value": round(value, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
                    "dof": dof, "kappa": round(cfg.kappa, 4), "keep_root_R": True,
