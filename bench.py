@@ -443,7 +443,7 @@ def run_reference(args, rank, world):
     val = cfg.n_unique / step_s
     return {"metric": METRIC, "value": round(val, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * step_s, 1), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "impl": "reference",
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
                        "dof": cfg.n_unique},
             "cpu_baseline": {"value": round(val, 1), "unit": "DOF/s", "cores": cpu_cores(), "kind": "oracle",
