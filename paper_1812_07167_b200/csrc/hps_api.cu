@@ -711,6 +711,12 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   const int ninv = schur ? H.ni : nt;  // matrix inverted per leaf
   const size_t wmat = (size_t)ninv * ninv;
   int chunk = chunk_opt > 0 ? chunk_opt : (int)std::max<size_t>(1, ((size_t)1 << 30) / (wmat * sizeof(zt)));
+  if (chunk_opt <= 0 && chunk >= 148 && chunk < nleaf) {
+    // one CTA per leaf and SM: equal chunks in whole waves of 148 (C3: 9 x 1746 + 670 leaves,
+    // 113 waves -> 9 x 1776 + 400, 111 waves)
+    const int nch = (nleaf + chunk - 1) / chunk;
+    chunk = ((nleaf + nch - 1) / nch + 147) / 148 * 148;
+  }
   chunk = std::min(chunk, nleaf);
   DevBuf work, ws, dK;
   work.alloc(sizeof(zt) * wmat * chunk);
