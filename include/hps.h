@@ -248,12 +248,28 @@ int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A
 
 void hps_free(hps_handle* h);
 
-/* Device blocks of >= 256 MB freed by hps_free (leaf and merge operator stores, solve vectors) are
- * kept in a process-wide cache and handed to later handles of the same shapes (a fresh mapping of
- * tens of GB costs ~0.25 s).  The cache holds at most 90 % of the device and is
- * emptied before any allocation is allowed to fail.  hps_release_cache returns every cached block
- * to the driver now (synchronises the devices that own them).  Returns 0. */
+/* Memory policy.  Device memory comes from the device's stream-ordered pool (cudaMallocAsync on
+ * the handle's stream).  When the last live handle is freed the pool is trimmed, so the memory is
+ * available to other allocators in the process (torch, NCCL) again.
+ * hps_set_cache_limit(bytes > 0) OPTS IN to a process-wide cache of blocks >= 256 MB freed by
+ * hps_free (leaf and merge operator stores, solve vectors), handed to later handles of the same
+ * shapes: a fresh mapping of tens of GB costs ~0.25 s.  At most `bytes` are parked;
+ * the cache is emptied before any library allocation is allowed to fail; 0 (default) disables it
+ * and frees what it holds.  hps_release_cache returns every cached block to the driver and trims
+ * the pool now (synchronises the devices concerned).  hps_cache_bytes: bytes parked now.
+ * Return 0 / HPS_EINVAL (negative limit). */
+int hps_set_cache_limit(int64_t bytes);
+int64_t hps_cache_bytes(void);
 int hps_release_cache(void);
+
+/* Debug and tuning knobs (process-wide; the library reads no environment variables).  `name` is
+ * one of: debug_alloc, big_cache, side, side_solve, nat_min, nat_max, nat_force_fail, dgj_pivot,
+ * dgj_force_bad, dgj_rpt, lr_trace, gemv_short, gemv_k16, trace, gemm_smallk, gj, seq_pivot,
+ * nat_w, nat_lpr, natc, natb, nat_pivot_rel (meanings in csrc/hps_internal.cuh).  The *_force_*
+ * and *_pivot knobs are FAULT INJECTION for the tests of the pivoted fallback paths: never set
+ * them in production.  value -1 restores the default.  Returns 0 or HPS_EINVAL (unknown name). */
+int hps_debug_set(const char* name, int value);
+int hps_debug_get(const char* name, int* value);
 const char* hps_last_error(void);
 
 #ifdef __cplusplus

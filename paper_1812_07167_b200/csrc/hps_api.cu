@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cmath>
@@ -30,15 +31,68 @@ static thread_local std::string g_err_msg;
 void hps_set_error(const std::string& m) { g_err_msg = m; }
 
 // ---------------------------------------------------------------------------
+// Debug / tuning knobs (hps_debug_set)
+// ---------------------------------------------------------------------------
+namespace {
+struct KnobDef {
+  const char* name;
+  int def;
+};
+const KnobDef g_knob_defs[KN_COUNT] = {
+    {"debug_alloc", 0}, {"big_cache", 1}, {"side", 1},       {"side_solve", 1},     {"nat_min", 200},
+    {"nat_max", 1 << 30}, {"nat_force_fail", 0}, {"dgj_pivot", 0}, {"dgj_force_bad", 0}, {"dgj_rpt", 2},
+    {"lr_trace", 0},    {"gemv_short", 1}, {"gemv_k16", 256}, {"trace", 0},          {"gemm_smallk", 1},
+    {"gj", 0},          {"seq_pivot", 0},  {"nat_w", 16},     {"nat_lpr", 4},        {"natc", 1},
+    {"natb", 1},        {"nat_pivot_rel", 25}};
+std::atomic<int> g_knobs[KN_COUNT];
+std::once_flag g_knob_once;
+void knob_init() {
+  for (int k = 0; k < KN_COUNT; ++k) g_knobs[k].store(g_knob_defs[k].def);
+}
+}  // namespace
+
+int knob(HpsKnob k) {
+  std::call_once(g_knob_once, knob_init);
+  return g_knobs[k].load(std::memory_order_relaxed);
+}
+
+int hps_num_sms() {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 148;
+  }
+  std::lock_guard<std::mutex> lk(mu);
+  if ((int)cache.size() <= dev) cache.resize(dev + 1, 0);
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+// ---------------------------------------------------------------------------
 // Per-kernel-class statistics (see hps_internal.cuh)
 // ---------------------------------------------------------------------------
-thread_local std::vector<cudaEvent_t> g_ev_pool;  // reused across handles (one device per process)
+// event pools reused across handles, one per device (an event must be recorded on a stream of the
+// device it was created on)
+thread_local std::vector<std::vector<cudaEvent_t>> g_ev_pools;
 
 struct Prof {
   unsigned timing = 0;  // bit mask of kernel classes timed with events
   KStats stats;
-  std::vector<cudaEvent_t>& pool = g_ev_pool;
+  int dev = 0;
   size_t used = 0;
+  std::vector<cudaEvent_t>& pool() {
+    if ((int)g_ev_pools.size() <= dev) g_ev_pools.resize(dev + 1);
+    return g_ev_pools[dev];
+  }
   struct Rec {
     int cls;
     size_t e0, e1;
@@ -46,19 +100,23 @@ struct Prof {
   std::vector<Rec> recs;
   std::vector<std::pair<int, size_t>> open;
   cudaEvent_t ev() {
-    if (used == pool.size()) {
+    auto& pl = pool();
+    if (used == pl.size()) {
       cudaEvent_t e;
       HPS_CUDA_CHECK(cudaEventCreate(&e));
-      pool.push_back(e);
+      pl.push_back(e);
     }
-    return pool[used++];
+    return pl[used++];
   }
   void finalize() {  // caller has synchronised the stream
+    auto& pl = pool();
     for (const Rec& r : recs) {
       float ms = 0;
-      if (cudaEventElapsedTime(&ms, pool[r.e0], pool[r.e1]) == cudaSuccess) stats.ms[r.cls] += ms;
+      if (cudaEventElapsedTime(&ms, pl[r.e0], pl[r.e1]) == cudaSuccess) stats.ms[r.cls] += ms;
     }
+    cudaGetLastError();
     recs.clear();
+    open.clear();
     used = 0;
   }
 };
@@ -116,17 +174,12 @@ struct BigBlock {
 std::mutex g_big_mu;
 std::vector<BigBlock> g_big;
 size_t g_big_total = 0;
-// parked bytes per process: up to 90 % of the device (a failed allocation flushes the cache first,
-// so parked blocks never cost a run its memory; a lower cap made C4 free and re-map every step)
-size_t big_cache_max() {
-  static size_t cap = 0;
-  if (!cap) {
-    size_t fr = 0, tot = 0;
-    cap = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? tot / 10 * 9 : ((size_t)96 << 30);
-    cudaGetLastError();
-  }
-  return cap;
-}
+// parked bytes per process: 0 (default) disables the cache -- blocks go back to the stream-ordered
+// pool, which is trimmed when the last handle is freed; hps_set_cache_limit opts in (the bench
+// does, so that repeated builds of the same shape do not re-map tens of GB every step)
+std::atomic<size_t> g_big_cap{0};
+size_t big_cache_max() { return g_big_cap.load(); }
+std::atomic<int> g_live_handles{0};
 
 void big_free_block(BigBlock& b) {
   cudaEventSynchronize(b.ev);
@@ -201,44 +254,63 @@ struct DevBuf {
   size_t bytes = 0;
   cudaStream_t st = nullptr;
   int dev = 0;  // device of the allocation (the cache is per device)
+  bool big_direct = false;  // allocated by cudaMalloc for the cache
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), dev(o.dev) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), dev(o.dev), big_direct(o.big_direct) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
   ~DevBuf() { release(); }
   void release() {
     if (p) {
-      if (bytes >= kBigBlock)
+      if (big_direct && big_cache_max() > 0)
         big_put(p, bytes, st, dev);
+      else if (big_direct)
+        big_free_direct();
       else
         cudaFreeAsync(p, st);
     }
     p = nullptr;
     bytes = 0;
+    big_direct = false;
+  }
+  // a block taken with cudaMalloc (cache on at allocation time) but released with the cache off
+  void big_free_direct() {
+    cudaStreamSynchronize(st);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != dev) cudaSetDevice(dev);
+    cudaFree(p);
+    if (cur != dev) cudaSetDevice(cur);
   }
   void alloc(size_t n) {
     release();
     if (n == 0) return;
     st = g_alloc_stream;
     cudaGetDevice(&dev);
-    static const bool dbg = getenv("HPS_DEBUG_ALLOC") && *getenv("HPS_DEBUG_ALLOC") == '1';
-    static const bool nocache = getenv("HPS_BIG_CACHE") && *getenv("HPS_BIG_CACHE") == '0';
+    const bool dbg = knob(KN_DEBUG_ALLOC) != 0;
+    const bool cache = big_cache_max() > 0;
     const auto t0 = std::chrono::steady_clock::now();
-    if (n >= kBigBlock && !nocache) {
+    if (n >= kBigBlock && cache) {
       size_t got = 0;
       p = big_take(n, st, got);
       if (p) {
         bytes = got;
+        big_direct = true;
         if (dbg) fprintf(stderr, "[alloc] %.2f GB reused\n", n / 1e9);
         return;
       }
     }
-    cudaError_t e = n >= kBigBlock && !nocache ? cudaMalloc(&p, n) : cudaMallocAsync(&p, n, st);
+    const bool direct = n >= kBigBlock && cache;
+    cudaError_t e = direct ? cudaMalloc(&p, n) : cudaMallocAsync(&p, n, st);
     if (e != cudaSuccess) {  // the parked blocks may be what is missing
       cudaGetLastError();
       big_flush();
-      e = n >= kBigBlock && !nocache ? cudaMalloc(&p, n) : cudaMallocAsync(&p, n, st);
+      e = direct ? cudaMalloc(&p, n) : cudaMallocAsync(&p, n, st);
     }
+    big_direct = direct && e == cudaSuccess;
     if (dbg && n >= kBigBlock)
       fprintf(stderr, "[alloc] %.2f GB in %.3f ms\n", n / 1e9,
               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
@@ -299,6 +371,17 @@ template <class T>
 void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
   b.alloc(sizeof(T) * std::max<size_t>(v.size(), 1));
   if (!v.empty()) HPS_CUDA_CHECK(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+}
+
+void trim_pool(int dev) {
+  cudaMemPool_t pool;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != dev) cudaSetDevice(dev);
+  cudaDeviceSynchronize();
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  cudaGetLastError();
+  if (cur != dev) cudaSetDevice(cur);
 }
 
 void retain_pool(int dev) {
@@ -711,11 +794,13 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   const int ninv = schur ? H.ni : nt;  // matrix inverted per leaf
   const size_t wmat = (size_t)ninv * ninv;
   int chunk = chunk_opt > 0 ? chunk_opt : (int)std::max<size_t>(1, ((size_t)1 << 30) / (wmat * sizeof(zt)));
-  if (chunk_opt <= 0 && chunk >= 148 && chunk < nleaf) {
-    // one CTA per leaf and SM: equal chunks in whole waves of 148 (C3: 9 x 1746 + 670 leaves,
-    // 113 waves -> 9 x 1776 + 400, 111 waves)
+  const int nsm = hps_num_sms();
+  if (chunk_opt <= 0 && chunk >= nsm && chunk < nleaf) {
+    // one CTA per leaf and SM: equal chunks in whole waves of the SM count (C3: 9 x 1746 + 670
+    // leaves, 113 waves -> 9 x 1776 + 400, 111 waves), never above the size-driven chunk
     const int nch = (nleaf + chunk - 1) / chunk;
-    chunk = ((nleaf + nch - 1) / nch + 147) / 148 * 148;
+    const int up = ((nleaf + nch - 1) / nch + nsm - 1) / nsm * nsm;
+    chunk = up <= chunk ? up : std::max(nsm, chunk / nsm * nsm);
   }
   chunk = std::min(chunk, nleaf);
   DevBuf work, ws, dK;
@@ -759,11 +844,11 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
 // (with per-kernel event timing on, everything stays on the main stream so that each launch's
 // event pair brackets that launch alone)
 cudaStream_t side_build(const hps_handle& H) {
-  static const bool off = getenv("HPS_SIDE") && *getenv("HPS_SIDE") == '0';
+  const bool off = knob(KN_SIDE) == 0;
   return off || H.prof.timing ? H.st : H.st2;
 }
 cudaStream_t side_solve(const hps_handle& H) {
-  static const bool off = getenv("HPS_SIDE_SOLVE") && *getenv("HPS_SIDE_SOLVE") == '0';
+  const bool off = knob(KN_SIDE_SOLVE) == 0;
   return off || H.prof.timing ? H.st : H.st2;
 }
 
@@ -839,9 +924,9 @@ void build_merge(hps_handle& H, int d) {
   // (c) W^{-1}.  For 200 <= n3 <= 512 (the few, latency-bound top-level inverses) natural order
   // first (measured pivots >= 0.8 of the diagonal at every C2 level); if a pivot fails its check
   // W is formed again and inverted with partial pivoting.
-  static const int nat_min = getenv("HPS_NAT_MIN") ? atoi(getenv("HPS_NAT_MIN")) : 200;
+  const int nat_min = knob(KN_NAT_MIN);
   bool done = false;
-  static const int nat_max = getenv("HPS_NAT_MAX") ? atoi(getenv("HPS_NAT_MAX")) : 1 << 30;
+  const int nat_max = knob(KN_NAT_MAX);
   if (n3 >= nat_min && n3 <= nat_max) {
     ws.alloc(std::max<size_t>(zgj_natural_workspace_bytes(n3, np), 16));
     DevBuf flag;
@@ -851,7 +936,7 @@ void build_merge(hps_handle& H, int d) {
     int hflag = 0;
     HPS_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     HPS_CUDA_CHECK(cudaStreamSynchronize(st));
-    static const bool force_fail = getenv("HPS_NAT_FORCE_FAIL") && *getenv("HPS_NAT_FORCE_FAIL") == '1';  // tests
+    const bool force_fail = knob(KN_NAT_FORCE_FAIL) != 0;  // tests
     done = hflag == 0 && !force_fail;
     H.nat_levels += done ? 1 : 0;
     if (!done) {  // W again: I - R33b R33a
@@ -1170,6 +1255,10 @@ struct LaunchScope {
     if (mine && mine->timing) {
       cudaDeviceSynchronize();
       mine->finalize();
+    } else if (mine) {
+      mine->open.clear();  // an exception may have left begin/end pairs unmatched
+      mine->recs.clear();
+      mine->used = 0;
     }
     g_launch_counter = prev;
     g_prof = prev_prof;
@@ -1348,6 +1437,7 @@ void t_gl_to_cheb(hps_handle& H, int nrhs, const zt* t_gl, DevBuf& out) {
 void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_opts* opt) {
   if (opt && opt->device >= 0) HPS_CUDA_CHECK(cudaSetDevice(opt->device));
   HPS_CUDA_CHECK(cudaGetDevice(&H.dev));
+  H.prof.dev = H.dev;
   HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
   retain_pool(H.dev);
   g_alloc_stream = H.st;
@@ -1493,6 +1583,7 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     return fail(HpsError{HPS_ECUDA, e.what()});
   }
   *outp = H.release();
+  g_live_handles.fetch_add(1);
   return HPS_OK;
 }
 
@@ -1530,6 +1621,7 @@ int hps_build_top(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, i
     return fail(HpsError{HPS_ECUDA, e.what()});
   }
   *outp = H.release();
+  g_live_handles.fetch_add(1);
   return HPS_OK;
 }
 
@@ -2007,11 +2099,65 @@ int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A
   return HPS_OK;
 }
 
-void hps_free(hps_handle* h) { delete h; }
+void hps_free(hps_handle* h) {
+  if (!h) return;
+  const int dev = h->dev;
+  delete h;
+  // the last handle gone and no cache opted in: give the pool's retained memory back to the
+  // driver so that co-resident allocators (torch, NCCL) can use it
+  if (g_live_handles.fetch_sub(1) == 1 && big_cache_max() == 0) trim_pool(dev);
+}
 
 int hps_release_cache(void) {
   big_flush();
+  int dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) trim_pool(dev);
+  cudaGetLastError();
   return HPS_OK;
+}
+
+int hps_set_cache_limit(int64_t bytes) {
+  if (bytes < 0) {
+    hps_set_error("hps_set_cache_limit: negative limit");
+    return HPS_EINVAL;
+  }
+  g_big_cap.store((size_t)bytes);
+  if (bytes == 0) big_flush();
+  return HPS_OK;
+}
+
+int64_t hps_cache_bytes(void) {
+  std::lock_guard<std::mutex> lk(g_big_mu);
+  return (int64_t)g_big_total;
+}
+
+int hps_debug_set(const char* name, int value) {
+  if (!name) {
+    hps_set_error("hps_debug_set: NULL name");
+    return HPS_EINVAL;
+  }
+  knob(KN_DEBUG_ALLOC);  // initialise the table
+  for (int k = 0; k < KN_COUNT; ++k)
+    if (!strcmp(name, g_knob_defs[k].name)) {
+      g_knobs[k].store(value == -1 ? g_knob_defs[k].def : value);  // -1 restores the default
+      return HPS_OK;
+    }
+  hps_set_error(std::string("hps_debug_set: unknown knob ") + name);
+  return HPS_EINVAL;
+}
+
+int hps_debug_get(const char* name, int* value) {
+  if (!name || !value) {
+    hps_set_error("hps_debug_get: NULL argument");
+    return HPS_EINVAL;
+  }
+  for (int k = 0; k < KN_COUNT; ++k)
+    if (!strcmp(name, g_knob_defs[k].name)) {
+      *value = knob((HpsKnob)k);
+      return HPS_OK;
+    }
+  hps_set_error(std::string("hps_debug_get: unknown knob ") + name);
+  return HPS_EINVAL;
 }
 
 }  // extern "C"

@@ -16,6 +16,39 @@ struct HpsError {
 };
 void hps_set_error(const std::string& msg);
 
+// ---------------------------------------------------------------------------
+// Debug / tuning knobs (hps_debug_set in hps.h).  Process-wide, set only through the explicit
+// debug ABI — the library reads no environment variables.  Fault-injection knobs (*_FORCE_*,
+// *_PIVOT) exist for the tests of the fallback paths; their defaults are the product behaviour.
+// ---------------------------------------------------------------------------
+enum HpsKnob {
+  KN_DEBUG_ALLOC = 0,  // print large-allocation timings to stderr
+  KN_BIG_CACHE,        // 1: cache large blocks across handles (hps_release_cache)
+  KN_SIDE,             // 1: side stream for the build's independent products (DESIGN 3.11)
+  KN_SIDE_SOLVE,       // 1: side stream in the solve
+  KN_NAT_MIN,          // natural-order W^{-1} for NAT_MIN <= n3 <= NAT_MAX (DESIGN 3.10)
+  KN_NAT_MAX,
+  KN_NAT_FORCE_FAIL,   // test: every natural-order W^{-1} reports a failed pivot check
+  KN_DGJ_PIVOT,        // test: real leaf eliminations pivot from the start
+  KN_DGJ_FORCE_BAD,    // test: the natural-order real leaf elimination fails its first check
+  KN_DGJ_RPT,          // rows per thread of the real leaf Gauss-Jordan (2 or 4)
+  KN_LR_TRACE,         // print the real-leaf CTA-0 timeline
+  KN_GEMV_SHORT,       // 1: 8/16-lane GEMV rows for short K
+  KN_GEMV_K16,         // largest K of the 16-lane GEMV
+  KN_TRACE,            // time and print every ZGEMM / inverse (synchronous)
+  KN_GEMM_SMALLK,      // 1: 16x16 tiles for short-K GEMMs on small grids
+  KN_GJ,               // kernel family of the batched inverse: 0 library, 1 fused, 2 blocked, 3 ws
+  KN_SEQ_PIVOT,        // test: the complex leaf Schur inverse pivots from the start
+  KN_NAT_W,            // natural-order panel width (16 or 32)
+  KN_NAT_LPR,          // natural-order update lanes per row
+  KN_NATC,             // 1: cluster panel for the natural-order inverse
+  KN_NATB,             // 1: blocked natural-order panel (DESIGN 3.10)
+  KN_NAT_PIVOT_REL,    // natural-order W^{-1}: pivot accepted if |p|^2 >= REL/1e4 * |W_kk|^2
+  KN_COUNT
+};
+int knob(HpsKnob k);
+int hps_num_sms();  // multiprocessors of the current device (cached per device)
+
 #define HPS_CUDA_CHECK(x)                                                                     \
   do {                                                                                        \
     cudaError_t e_ = (x);                                                                     \

@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256) leaf_schur_finish_kernel(zt* __restrict__
 
 inline int grid_for(int64_t total) {
   int64_t b = (total + 255) / 256;
-  if (b > 148 * 32) b = 148 * 32;
+  if (b > hps_num_sms() * 32) b = hps_num_sms() * 32;
   if (b < 1) b = 1;
   return (int)b;
 }

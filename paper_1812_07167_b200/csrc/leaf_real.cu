@@ -989,17 +989,21 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
                       const double* KR, const zt (&fb)[2][2][2], zt eta, zt* store, int64_t mstride, zt* R,
                       void* work, int* info, cudaStream_t st, bool pivot) {
   const int q = p - 2, ni = q * q, nb = 4 * q;
-  static const bool force_piv = getenv("HPS_DGJ_PIVOT") && *getenv("HPS_DGJ_PIVOT") == '1';
+  const bool force_piv = knob(KN_DGJ_PIVOT) != 0;
   pivot = pivot || force_piv;
   double* Wk = reinterpret_cast<double*>(work);
   double* Qg = Wk + (size_t)batch * ni * ni;
   int* perm = reinterpret_cast<int*>(Qg + (size_t)batch * ni * nb);
   const size_t smemA = sizeof(double) * ((size_t)((ni + 15) & ~15) * RL_NB + (size_t)RL_NB * rl_zs(ni));
   const size_t smemB = sizeof(double) * (size_t)RLeafSmem(p).total;
+  static int force_bad_set = -1;  // value last copied to the device symbol
+  const int force_bad = knob(KN_DGJ_FORCE_BAD) != 0;
+  if (force_bad != force_bad_set) {
+    HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_dgj_force_bad, &force_bad, sizeof(int)));
+    force_bad_set = force_bad;
+  }
   static bool attr = false;
   if (!attr) {
-    const int force_bad = getenv("HPS_DGJ_FORCE_BAD") && *getenv("HPS_DGJ_FORCE_BAD") == '1';
-    HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_dgj_force_bad, &force_bad, sizeof(int)));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(leaf_real_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
@@ -1010,7 +1014,7 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
                8.0 * batch * nid * nid + 16.0 * batch * ((nbd + nid) * (nbd + nid) + nbd * nbd), st);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nbatch = std::min(65535, batch - b0);
-    static const int rpt = getenv("HPS_DGJ_RPT") ? atoi(getenv("HPS_DGJ_RPT")) : 2;
+    const int rpt = knob(KN_DGJ_RPT);
     auto kern = rpt == 4 ? dgj_leaf_kernel<4> : dgj_leaf_kernel<2>;
     kern<<<nbatch, 512, smemA, st>>>(Wk + (size_t)b0 * ni * ni, perm + (size_t)b0 * 2 * ni, leaf0 + b0,
                                                 leaf_nat, c, p, K, kappa2, info, pivot ? 1 : 0);
@@ -1035,7 +1039,7 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
   }
-  static const bool trace = getenv("HPS_LR_TRACE") && *getenv("HPS_LR_TRACE") == '1';
+  const bool trace = knob(KN_LR_TRACE) != 0;
   if (trace) {
     long long t[64];
     HPS_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -445,8 +445,9 @@ __global__ void __launch_bounds__(256) zgemv_short_kernel(const ZGemm g) {
 template <int NMAX>
 void launch_gemv(const ZGemm& g, cudaStream_t st) {
   const int64_t rows = (int64_t)g.M * g.batch;
-  static const bool short_off = getenv("HPS_GEMV_SHORT") && *getenv("HPS_GEMV_SHORT") == '0';
-  static const int short16 = getenv("HPS_GEMV_K16") ? atoi(getenv("HPS_GEMV_K16")) : 256;
+  const bool short_off = knob(KN_GEMV_SHORT) == 0;
+  const int short16 = knob(KN_GEMV_K16);
+  const int nsm = hps_num_sms();
   if (g.K <= 128 && !short_off) {  // 8 lanes per row: 32 rows per 256-thread block
     dim3 grid((g.M + 31) / 32, g.batch < 65535 ? g.batch : 65535);
     zgemv_short_kernel<NMAX, 8><<<grid, 256, 0, st>>>(g);
@@ -454,7 +455,7 @@ void launch_gemv(const ZGemm& g, cudaStream_t st) {
     count_launch();
     return;
   }
-  if (g.K <= short16 && !short_off && rows >= 148 * 64) {  // 16 lanes per row (the leaf Y s, K = n_i)
+  if (g.K <= short16 && !short_off && rows >= nsm * 64) {  // 16 lanes per row (the leaf Y s, K = n_i)
     dim3 grid((g.M + 15) / 16, g.batch < 65535 ? g.batch : 65535);
     zgemv_short_kernel<NMAX, 16><<<grid, 256, 0, st>>>(g);
     HPS_CUDA_CHECK(cudaGetLastError());
@@ -462,7 +463,7 @@ void launch_gemv(const ZGemm& g, cudaStream_t st) {
     return;
   }
   int ks = 1;
-  while (ks < 8 && rows * ks < 148 * 48 && g.K / (2 * ks) >= 64) ks *= 2;
+  while (ks < 8 && rows * ks < nsm * 48 && g.K / (2 * ks) >= 64) ks *= 2;
   const int rpb = 8 / ks;
   dim3 grid((g.M + rpb - 1) / rpb, g.batch < 65535 ? g.batch : 65535);
   switch (ks) {
@@ -501,12 +502,7 @@ __global__ void zcopy_kernel(const ZCopy c) {
 
 // HPS_TRACE=1: time every ZGEMM with events (synchronous) and print its shape to stderr.
 static bool trace_on() {
-  static int t = -1;
-  if (t < 0) {
-    const char* e = getenv("HPS_TRACE");
-    t = (e && *e == '1') ? 1 : 0;
-  }
-  return t == 1;
+  return knob(KN_TRACE) != 0;
 }
 
 void zgemm_impl(const ZGemm& g, cudaStream_t st);
@@ -572,10 +568,11 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   // for the short-K and Cin-heavy shapes of the merges and the Gauss-Jordan updates; 64x32 tiles
   // win once K is long enough to amortise the tile loads.
   const int64_t tiles32 = (int64_t)((g.M + 31) / 32) * ((g.N + 31) / 32) * g.batch;
-  static const bool small_k16 = !(getenv("HPS_GEMM_SMALLK") && *getenv("HPS_GEMM_SMALLK") == '0');
+  const bool small_k16 = knob(KN_GEMM_SMALLK) != 0;
+  const int nsm = hps_num_sms();
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
-  else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * 148))
+  else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * nsm))
     launch<16, 16, 8, 8>(g, st);  // short K on a grid of few 32x32 tiles: more, smaller CTAs
   else if (g.K >= 512)
     launch<64, 32, 32, 16>(g, st);
@@ -624,7 +621,7 @@ void zcopy_multi(const ZCopy* cs, int n, cudaStream_t st) {
       bytes += 32 * total;
     }
     ProfScope ps(K_LAYOUT, 0.0, (double)bytes, st);
-    const int blocks = (int)std::min<int64_t>((maxt + 255) / 256, 148 * 32 / m + 1);
+    const int blocks = (int)std::min<int64_t>((maxt + 255) / 256, hps_num_sms() * 32 / m + 1);
     if (maxt < ((int64_t)1 << 32))
       zcopy_multi_kernel<unsigned><<<dim3(blocks, m), 256, 0, st>>>(L);
     else
@@ -639,7 +636,7 @@ void zcopy(const ZCopy& c, cudaStream_t st) {
   if (total <= 0) return;
   ProfScope ps(K_LAYOUT, 0.0, 32.0 * total, st);
   int blocks = (int)((total + 255) / 256);
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > hps_num_sms() * 32) blocks = hps_num_sms() * 32;
   if (total < ((int64_t)1 << 32))
     zcopy_kernel<unsigned><<<blocks, 256, 0, st>>>(c);
   else

@@ -161,7 +161,16 @@ struct PanelArgs {
   int* cinmap;
   int* info;
   int* pflag = nullptr;  // implicit-pivoting path: 1 = row already pivoted
+  // natural-order panels: |A_kk|^2 of the ORIGINAL matrix per (batch, k); a pivot p of step k
+  // passes if |p|^2 >= rel2 * d0[k] (relative check, reading Q21)
+  const double* d0 = nullptr;
+  double rel2 = 0.0;
 };
+
+__device__ __forceinline__ bool nat_pivot_ok(const PanelArgs& a, int b, int k, zt pv) {
+  const double m = fma(pv.x, pv.x, pv.y * pv.y);
+  return m > 0.0 && m >= a.rel2 * a.d0[(int64_t)b * a.n + k];
+}
 
 __device__ __forceinline__ void write_maps(const PanelArgs& a, int b, int i, int orig) {
   if (i < a.n) {
@@ -322,7 +331,8 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) zgj_panel_reg_kernel(c
 // Natural-order panel (no pivot search), n <= 512, w <= 16, for the merge matrices W (DESIGN.md
 // 3.10: measured to need no pivoting in the configs' regimes): 512 threads, 4 rows x 4 columns per thread; per step the owner
 // lanes of row k publish it and ONE barrier separates publication from the update.  A pivot
-// with |pivot|^2 < 1e-6 raises *a.pflag (the caller redoes the matrix with partial pivoting).
+// whose |pivot|^2 is below rel2 x the original |A_kk|^2 raises *a.pflag (the caller redoes the
+// matrix with partial pivoting).
 // Same interface and outputs as zgj_panel_reg_kernel with identity permutations.
 __device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[192..255])
 __device__ int g_nat_trace_on;
@@ -332,7 +342,7 @@ __device__ int g_nat_trace_on;
 // does it redundantly, no inter-CTA communication) and records the w scaled pivot rows; every
 // other row then applies the w recorded steps locally (shuffles only, no barrier per step).
 // Grid (ceil(n / 128), batch), 512 threads: 4 lanes x 4 columns per row, 128 rows per CTA.
-// w <= 16.  A pivot with |pivot|^2 < 1e-6 raises *a.pflag.
+// w <= 16.  A pivot failing nat_pivot_ok raises *a.pflag.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(512) zgj_panel_natb_kernel(const PanelArgs a) {
   constexpr int CPT = 4, NB = 16, RPC = 128;
@@ -382,7 +392,7 @@ __global__ void __launch_bounds__(512) zgj_panel_natb_kernel(const PanelArgs a) 
         for (int m = 0; m < 8; ++m)
           aik[m] = make_double2(__shfl_sync(0xffffffffu, bv[m].x, (h << 4) | kk),
                                 __shfl_sync(0xffffffffu, bv[m].y, (h << 4) | kk));
-        bad = bad || !(fma(pv.x, pv.x, pv.y * pv.y) >= 1e-6);
+        bad = bad || !nat_pivot_ok(a, b, k0 + kk, pv);
         const zt inv = zinv_fast(pv);
         const zt prn = zmul(pr, inv);  // pr / pivot
         if (h == 0) phat[kk][c] = c == kk ? make_double2(0.0, 0.0) : prn;
@@ -498,7 +508,7 @@ __global__ void __launch_bounds__(512, 1) zgj_panel_nat_kernel(const PanelArgs a
       }
       __syncthreads();
       const zt pv = prow[par][kk];
-      if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 1e-6)) bad = true;
+      if (!nat_pivot_ok(a, b, k, pv)) bad = true;
       const zt inv = zinv_fast(pv);
       zt pr[CPT];
 #pragma unroll
@@ -594,7 +604,7 @@ __global__ void __launch_bounds__(512, 1) zgj_panel_natc_kernel(const PanelArgs 
       zt pr[CPT];
 #pragma unroll
       for (int c = 0; c < CPT; ++c) pr[c] = rp[cg * CPT + c];
-      if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 1e-6)) bad = true;
+      if (!nat_pivot_ok(a, b, k, pv)) bad = true;
       const zt inv = zinv_fast(pv);
       const zt own = v[s];
       zt g = zmul(make_double2(__shfl_sync(0xffffffffu, own.x, src), __shfl_sync(0xffffffffu, own.y, src)), inv);
@@ -2358,12 +2368,7 @@ void zgj_ws_trace(int on, long long* out) {
 }  // hps_zinv_timed: 1 = fused, 2 = blocked (0 = library choice / HPS_GJ)
 namespace {
 int gj_mode_env() {
-  static int m = -1;
-  if (m < 0) {
-    const char* e = getenv("HPS_GJ");
-    m = (e && !strcmp(e, "fused")) ? 1 : (e && !strcmp(e, "blocked")) ? 2 : 0;
-  }
-  return g_gj_mode_force ? g_gj_mode_force : m;
+  return g_gj_mode_force ? g_gj_mode_force : knob(KN_GJ);
 }
 // measured (tools/gj_tune.py): the warp-specialised kernel wins for 100 <= n <= 200 at every batch size;
 // above that its panel phase (8 warps x 4 rows) outgrows the update
@@ -2538,7 +2543,7 @@ void zgj_invert_p47(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_
     cur = 1 - cur;
   }
   ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)batch * n * n, st);
-  const int bx = (int)std::min<int64_t>(((int64_t)n * n + 255) / 256, std::max(1, 148 * 8 / batch));
+  const int bx = (int)std::min<int64_t>(((int64_t)n * n + 255) / 256, std::max(1, hps_num_sms() * 8 / batch));
   zgj_implicit_out_kernel<<<dim3(bx, batch), 256, sizeof(int) * 2 * n, st>>>(buf[cur], ld[cur], bsz[cur], out, ldo,
                                                                              obs, piv, n);
   HPS_CUDA_CHECK(cudaGetLastError());
@@ -2603,7 +2608,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
       }
       // large batches: two CTAs per SM overlap one matrix's pivot steps with the other's update;
       // small batches: one CTA per SM with wider chunks has the shorter critical path
-      if (batch >= 148)
+      if (batch >= hps_num_sms())
         zgj_fused_kernel<8, 2><<<nbatch, 256, sizeof(zt) * 2 * (size_t)n * 10, st>>>(
             A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo, obs, n, info);
       else
@@ -2703,7 +2708,7 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
   }
   const int64_t total = (int64_t)batch * n * n;
   ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)total, st);
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)hps_num_sms() * 32);
   zgj_colperm_kernel<<<blocks, 256, 0, st>>>(buf[cur], ld[cur], bsz[cur], out, ldo, obs, pi, n, batch);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
@@ -2725,10 +2730,14 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
                            double kappa2) {
   const int q = p - 2, n = q * q, nb = 4 * q, nt = nb + n;
   if (!zgj_leaf_fused_applies(p, batch)) return false;
+  static int piv_set = -1;  // value last copied to the device symbol
+  const int piv = knob(KN_SEQ_PIVOT) != 0;
+  if (piv != piv_set) {
+    HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_seq_pivot, &piv, sizeof(int)));
+    piv_set = piv;
+  }
   static bool wattr = false;
   if (!wattr) {
-    const int piv = getenv("HPS_SEQ_PIVOT") && *getenv("HPS_SEQ_PIVOT") == '1';
-    HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_seq_pivot, &piv, sizeof(int)));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)ws_smem(WS_NMAX)));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2808,7 +2817,7 @@ int zgj_plan_inverse(int n, int nbox, double* eps, double* rt, int* theta) {
   HPS_CUDA_CHECK(cudaMalloc(&o, bytes));
   HPS_CUDA_CHECK(cudaMalloc(&ws, wsb));
   HPS_CUDA_CHECK(cudaMalloc(&info, sizeof(int)));
-  plan_fill_kernel<<<148 * 8, 256, 0, st>>>((zt*)src, n, (int64_t)mat * mmax);
+  plan_fill_kernel<<<hps_num_sms() * 8, 256, 0, st>>>((zt*)src, n, (int64_t)mat * mmax);
   HPS_CUDA_CHECK(cudaGetLastError());
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -2880,6 +2889,14 @@ void zgj_plan_clear() {
 int zgj_regime_of(int n, int nbox) { return choose_regime(n, nbox); }
 void zgj_force_regime(int r) { g_regime_force = r; }
 
+// |A_kk|^2 of the original matrices (reference of the natural-order pivot check)
+__global__ void nat_diag_kernel(const zt* A, int64_t lda, int64_t bs, int n, double* d0) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x, b = blockIdx.y;
+  if (k >= n) return;
+  const zt v = A[(int64_t)b * bs + (int64_t)k * lda + k];
+  d0[(int64_t)b * n + k] = fma(v.x, v.x, v.y * v.y);
+}
+
 // Natural-order blocked Gauss-Jordan: 16-column zgj_panel_nat_kernel panels and
 // the blocked explicit-swap update with identity maps (any n).  Workspace as
 // zgj_workspace_bytes(n, batch) for the blocked regime; *flag (device) is set to 1 when a pivot
@@ -2893,12 +2910,21 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
   int* rowsrc = piv + (size_t)batch * n;
   int* cinmap = rowsrc + (size_t)batch * n;
   int* pi = cinmap + (size_t)batch * n;
+  double* d0 = reinterpret_cast<double*>(pi + (size_t)batch * n + 64);  // 256-byte aligned
+  d0 = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(d0) + 255) & ~(uintptr_t)255);
   zt* buf[2] = {A, B2};
   const int64_t ld[2] = {lda, n}, bsz[2] = {bs, (int64_t)n * n};
-  static const int wide = getenv("HPS_NAT_W") ? atoi(getenv("HPS_NAT_W")) : 16;  // 32: measured slower (C2 merges 5.20 -> 5.76 ms)
-  static const int lpr = getenv("HPS_NAT_LPR") ? atoi(getenv("HPS_NAT_LPR")) : 4;
+  {
+    ProfScope ps(K_GJ_AUX, 0.0, 24.0 * (double)batch * n, st);
+    nat_diag_kernel<<<dim3((n + 255) / 256, batch), 256, 0, st>>>(A, lda, bs, n, d0);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+  }
+  const double rel2 = knob(KN_NAT_PIVOT_REL) * 1e-4;
+  const int wide = knob(KN_NAT_W);  // 32: measured slower (C2 merges 5.20 -> 5.76 ms)
+  const int lpr = knob(KN_NAT_LPR);
   const int cs = (n + 512 / lpr - 1) / (512 / lpr);
-  const bool use_c = !(getenv("HPS_NATC") && *getenv("HPS_NATC") == '0') && cs <= 8;
+  const bool use_c = knob(KN_NATC) != 0 && cs <= 8;
   const int wmax = use_c && wide == 32 ? 32 : 16;
   const int npan = (n + wmax - 1) / wmax, nbw = (n + npan - 1) / npan;
   int cur = 0;
@@ -2907,9 +2933,11 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
     PanelArgs pa{buf[cur], buf[1 - cur], ld[cur], bsz[cur], ld[1 - cur], bsz[1 - cur], n, k0, w, piv, rowsrc, cinmap,
                  flag};
     pa.pflag = flag;
+    pa.d0 = d0;
+    pa.rel2 = rel2;
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * n * (double)w * w * batch, 32.0 * n * (double)w * batch, st);
-      static const bool blocked = !(getenv("HPS_NATB") && *getenv("HPS_NATB") == '0');
+      const bool blocked = knob(KN_NATB) != 0;
       if (blocked && wmax == 16) {
         zgj_panel_natb_kernel<<<dim3((n + 127) / 128, batch), 512, 0, st>>>(pa);
       } else if (!use_c) {
@@ -2985,7 +3013,7 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
 
 size_t zgj_natural_workspace_bytes(int n, int batch) {
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
-  return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256;
+  return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256 + 512 + sizeof(double) * (size_t)batch * n;
 }
 
 size_t zgj_workspace_bytes(int n, int batch) {
@@ -2998,8 +3026,7 @@ size_t zgj_workspace_bytes(int n, int batch) {
 void zgj_invert(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch, void* ws,
                 int* info, cudaStream_t st, int64_t* launches) {
   (void)launches;
-  const char* e = getenv("HPS_TRACE");
-  if (!(e && *e == '1')) return zgj_invert_impl(A, lda, bs, out, ldo, obs, n, batch, ws, info, st);
+  if (!knob(KN_TRACE)) return zgj_invert_impl(A, lda, bs, out, ldo, obs, n, batch, ws, info, st);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);

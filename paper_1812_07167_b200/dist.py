@@ -129,7 +129,12 @@ def slice_leaves(arr, g, sub, i0, j0):
 def _stack(xs):
     if hasattr(xs[0], "data_ptr"):
         import torch
-        return torch.stack(xs).contiguous()
+        out = torch.stack(xs).contiguous()
+        if out.is_cuda:
+            # the library reads this buffer on its own stream: the stack kernel (on torch's
+            # current stream) must be complete first
+            torch.cuda.current_stream(out.device).synchronize()
+        return out
     return np.ascontiguousarray(np.stack(xs))
 
 

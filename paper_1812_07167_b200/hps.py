@@ -41,7 +41,7 @@ SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_last_time_ms", "hps_last_launches",
            "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free", "hps_release_cache",
-           "hps_last_error"]
+           "hps_set_cache_limit", "hps_cache_bytes", "hps_debug_set", "hps_debug_get", "hps_last_error"]
 
 KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout", "zgj_fused", "leaf_gj", "zgemv"]
 
@@ -94,6 +94,10 @@ def lib():
         L.hps_solve_down.argtypes = [vp, i32, dp, dp]
         L.hps_solve_top.argtypes = [vp, i32, dp, dp, dp]
         L.hps_free.argtypes = [vp]
+        L.hps_set_cache_limit.argtypes = [i64]
+        L.hps_cache_bytes.restype = i64
+        L.hps_debug_set.argtypes = [C.c_char_p, i32]
+        L.hps_debug_get.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
         L.hps_last_error.restype = C.c_char_p
         _lib = L
     return _lib
@@ -138,6 +142,35 @@ def leaf_nodes(g, p):
 def release_cache():
     """Return the cached large device blocks of freed handles to the driver (hps_release_cache)."""
     _check(lib().hps_release_cache())
+
+
+def set_cache_limit(nbytes):
+    """Opt in (nbytes > 0) to the cross-handle cache of large blocks, or disable it (0)."""
+    _check(lib().hps_set_cache_limit(int(nbytes)))
+
+
+def debug_get(name):
+    v = C.c_int()
+    _check(lib().hps_debug_get(name.encode(), C.byref(v)))
+    return v.value
+
+
+class debug_knobs:
+    """Context manager: set library debug/tuning knobs (hps_debug_set), restore them on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = debug_get(k)
+            _check(lib().hps_debug_set(k.encode(), int(v)))
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            lib().hps_debug_set(k.encode(), int(v))
 
 
 def root_boundary_nodes(g, p, basis=0):

@@ -81,89 +81,55 @@ def test_leaf_real_elimination_pivoted():
 
 
 def test_leaf_real_elimination_forced_pivoting():
-    """HPS_DGJ_PIVOT=1 (fresh process): both real eliminations (A_ii and Sigma) with partial
-    pivoting from the first step, the fallback the natural-order path takes on a small pivot."""
-    import os, subprocess, sys, textwrap
-    code = textwrap.dedent("""
-        import os, sys
-        sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
-        import numpy as np, oracle
-        from paper_1812_07167_b200 import hps
-        from test_gpu_parity import problem, rel
-        g, c, s, t = problem(2, 1, 16, 4.0, 4.0 + 1j)
-        S = hps.Solver(g, 16, 4.0, 4.0 + 1j, c, keep_all_R=True, leaf_mode=3)
-        Psi, Y = S.leaf_ops(1)
-        lo = oracle.leaf(16, 0.5, 1.0, 4.0, 4.0 + 1j, c[1])
-        print(max(rel(Psi, lo["Psi"]), rel(Y, lo["Y"]), rel(S.R(3), lo["R"])))
-    """)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    # pivoting from the start; and the natural-order attempt failing its first pivot check (the
-    # in-kernel fallback redoes the leaf with partial pivoting)
-    for extra in ({"HPS_DGJ_PIVOT": "1"}, {"HPS_DGJ_FORCE_BAD": "1"}):
-        env = dict(os.environ, PYTHONPATH=root, **extra)
-        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
-                             timeout=600)
-        assert out.returncode == 0, out.stderr[-2000:]
-        assert float(out.stdout.strip().splitlines()[-1]) < TOL
+    """Fault injection (hps_debug_set): both real eliminations (A_ii and Sigma) with partial
+    pivoting from the first step, and the natural-order attempt failing its first pivot check
+    (the in-kernel fallback redoes the leaf with partial pivoting)."""
+    g, c, s, t = problem(2, 1, 16, 4.0, 4.0 + 1j)
+    lo = oracle.leaf(16, 0.5, 1.0, 4.0, 4.0 + 1j, c[1])
+    for knobs in ({"dgj_pivot": 1}, {"dgj_force_bad": 1}):
+        with hps.debug_knobs(**knobs):
+            S = hps.Solver(g, 16, 4.0, 4.0 + 1j, c, keep_all_R=True, leaf_mode=3)
+            Psi, Y = S.leaf_ops(1)
+            err = max(rel(Psi, lo["Psi"]), rel(Y, lo["Y"]), rel(S.R(3), lo["R"]))
+            S.close()
+        assert err < TOL, (knobs, err)
 
 
 def test_natural_order_merge_inverses_all_levels():
-    """HPS_NAT_MIN=14 (fresh process): every merge W with 14 <= n3 <= 512 is inverted in natural
-    order — every box's R and u vs the oracle, complex eta included."""
-    import os, subprocess, sys, textwrap
-    code = textwrap.dedent("""
-        import os, sys
-        sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
-        import numpy as np, oracle
-        from paper_1812_07167_b200 import hps
-        from test_gpu_parity import problem, rel
+    """nat_min = 14: every merge W with n3 >= 14 is inverted in natural order —
+    every box's R and u vs the oracle, complex eta included; second pass with every natural-order
+    attempt forced to fail its pivot check (the pivoted fallback), third with the relative pivot
+    threshold at 1.0 (any pivot smaller than its original diagonal falls back)."""
+    for knobs in ({"nat_min": 14}, {"nat_min": 14, "nat_force_fail": 1}, {"nat_min": 14, "nat_pivot_rel": 10000}):
         worst = 0.0
-        for nx, ny, p, kappa, eta in [(4, 4, 8, 9.0, 9.0 - 2j), (8, 4, 6, 9.0, 9.0), (4, 8, 10, 20.0, 20.0)]:
-            g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx)
-            S = hps.Solver(g, p, kappa, eta, c, keep_all_R=True)
-            O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c, keep_all_R=True)
-            for box in range(1, 2 * nx * ny):
-                worst = max(worst, rel(S.R(box), O.R(box)))
-            worst = max(worst, rel(S.solve(s, t), O.solve(s, t)))
-        print(worst)
-    """)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for extra in ({}, {"HPS_NAT_FORCE_FAIL": "1"}):  # second run: every level takes the pivoted fallback
-        env = dict(os.environ, HPS_NAT_MIN="14", PYTHONPATH=root, **extra)
-        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
-                             timeout=900)
-        assert out.returncode == 0, out.stderr[-2000:]
-        assert float(out.stdout.strip().splitlines()[-1]) < TOL
+        with hps.debug_knobs(**knobs):
+            for nx, ny, p, kappa, eta in [(4, 4, 8, 9.0, 9.0 - 2j), (8, 4, 6, 9.0, 9.0), (4, 8, 10, 20.0, 20.0)]:
+                g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx)
+                S = hps.Solver(g, p, kappa, eta, c, keep_all_R=True)
+                O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c, keep_all_R=True)
+                for box in range(1, 2 * nx * ny):
+                    worst = max(worst, rel(S.R(box), O.R(box)))
+                worst = max(worst, rel(S.solve(s, t), O.solve(s, t)))
+                S.close()
+        assert worst < TOL, (knobs, worst)
 
 
 def test_leaf_schur_natural_and_pivoted_paths():
     """The complex interior Schur inverse (leaf_mode 0 with complex c) runs in natural order
-    (DESIGN.md 3.12); HPS_SEQ_PIVOT=1 (fresh process) forces the pivoted path. Both vs the oracle."""
-    import os, subprocess, sys, textwrap
-    code = textwrap.dedent("""
-        import os, sys
-        sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
-        import numpy as np, oracle
-        from paper_1812_07167_b200 import hps
-        from test_gpu_parity import problem, rel
-        g, c, s, t = problem(2, 1, 16, 7.0, 7.0 + 1j)
-        c = c + 0.05j
-        S = hps.Solver(g, 16, 7.0, 7.0 + 1j, c, keep_all_R=True)
-        assert S.leaf_path() == 0
-        w = 0.0
-        for leaf in range(2):
-            Psi, Y = S.leaf_ops(leaf)
-            lo = oracle.leaf(16, 0.5, 1.0, 7.0, 7.0 + 1j, c[leaf])
-            w = max(w, rel(Psi, lo["Psi"]), rel(Y, lo["Y"]), rel(S.R(2 + leaf), lo["R"]))
-        print(w)
-    """)
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    for extra in ({}, {"HPS_SEQ_PIVOT": "1"}):
-        env = dict(os.environ, PYTHONPATH=root, **extra)
-        out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
-                             timeout=600)
-        assert out.returncode == 0, out.stderr[-2000:]
-        assert float(out.stdout.strip().splitlines()[-1]) < TOL
+    (DESIGN.md 3.12); the seq_pivot knob forces the pivoted path.  Both vs the oracle."""
+    g, c, s, t = problem(2, 1, 16, 7.0, 7.0 + 1j)
+    c = c + 0.05j
+    for knobs in ({}, {"seq_pivot": 1}):
+        with hps.debug_knobs(**knobs):
+            S = hps.Solver(g, 16, 7.0, 7.0 + 1j, c, keep_all_R=True)
+            assert S.leaf_path() == 0
+            w = 0.0
+            for leaf in range(2):
+                Psi, Y = S.leaf_ops(leaf)
+                lo = oracle.leaf(16, 0.5, 1.0, 7.0, 7.0 + 1j, c[leaf])
+                w = max(w, rel(Psi, lo["Psi"]), rel(Y, lo["Y"]), rel(S.R(2 + leaf), lo["R"]))
+            S.close()
+        assert w < TOL, (knobs, w)
 
 
 def test_leaf_path_selection():

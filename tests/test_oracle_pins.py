@@ -138,16 +138,18 @@ def leaf_boundary_geometry(p, x0, y0, hx, hy, orc):
     return Xb, Yb, NX, NY, inputs.interior_of(p, X[0]), inputs.interior_of(p, Y[0])
 
 
+@pytest.mark.parametrize("hx,hy", [(0.25, 0.25), (0.25, 0.5), (0.4, 0.15)])
 @pytest.mark.parametrize("p,kappa,eta", [(6, 3.0, 3.0), (10, 7.0, 2.0 - 1.0j), (16, 20.0, 20.0)])
-def test_leaf_polynomial_exact(orc, p, kappa, eta):
+def test_leaf_polynomial_exact(orc, p, kappa, eta, hx, hy):
     """u = Psi t + Y s reproduces a degree-(p-1) polynomial exactly for any
-    kappa, c, eta (PAPER.md:433-445 Remark; collocation is exact on it)."""
-    x0, y0, h = 0.3, -0.2, 0.25
-    P = Poly2D(p - 1, (x0, x0 + h, y0, y0 + h), seed=p)
-    X, Y = orc.leaf_nodes(x0, x0 + h, y0, y0 + h, 1, 1, p)
+    kappa, c, eta (PAPER.md:433-445 Remark; collocation is exact on it) — on square AND
+    rectangular leaves (h_x != h_y: a swapped 2/h_x, 2/h_y scaling of D_x, D_y fails here)."""
+    x0, y0 = 0.3, -0.2
+    P = Poly2D(p - 1, (x0, x0 + hx, y0, y0 + hy), seed=p)
+    X, Y = orc.leaf_nodes(x0, x0 + hx, y0, y0 + hy, 1, 1, p)
     c = (1 + 0.3 * np.sin(3 * X[0]) * np.cos(2 * Y[0])).astype(complex)
-    lf = orc.leaf(p, h, h, kappa, eta, c)
-    Xb, Yb, NX, NY, Xi, Yi = leaf_boundary_geometry(p, x0, y0, h, h, orc)
+    lf = orc.leaf(p, hx, hy, kappa, eta, c)
+    Xb, Yb, NX, NY, Xi, Yi = leaf_boundary_geometry(p, x0, y0, hx, hy, orc)
     dn = NX * P.val(Xb, Yb, dx=1) + NY * P.val(Xb, Yb, dy=1)
     t = dn + 1j * eta * P.val(Xb, Yb)
     ci = inputs.interior_of(p, c)
@@ -243,11 +245,13 @@ def test_kappa0_harmonic_polynomials(orc, nx, ny):
 # ---------------------------------------------------------------------------
 # Merge: brute-force global collocation, decoupling, explicit vs action forms
 # ---------------------------------------------------------------------------
-@pytest.mark.parametrize("nx,ny,p,kappa", [(2, 1, 10, 7.0), (1, 2, 8, 2.0), (2, 2, 8, 9.0), (4, 4, 6, 5.0)])
-def test_tree_vs_global_dense(orc, nx, ny, p, kappa):
+@pytest.mark.parametrize("nx,ny,p,kappa,ar", [(2, 1, 10, 7.0, 1.0), (1, 2, 8, 2.0, 1.0), (2, 2, 8, 9.0, 1.0),
+                                             (4, 4, 6, 5.0, 1.0), (2, 1, 8, 6.0, 2.0), (2, 2, 6, 4.0, 0.5)])
+def test_tree_vs_global_dense(orc, nx, ny, p, kappa, ar):
     """Merged root R and the solve u equal the dense global collocation system
-     — independent elimination of the same equations."""
-    x0, x1, y0, y1 = 0.0, 0.3 * nx, 0.0, 0.3 * ny
+     — independent elimination of the same equations; ar = h_y / h_x
+    (rectangular leaves in the last two cases)."""
+    x0, x1, y0, y1 = 0.0, 0.3 * nx, 0.0, 0.3 * ny * ar
     X, Y = orc.leaf_nodes(x0, x1, y0, y1, nx, ny, p)
     c = (1 - 0.4 * np.exp(-((X - 0.2) ** 2 + (Y - 0.25) ** 2) / 0.02)).astype(complex)
     eta = kappa * (1 + 0.5j)
@@ -368,11 +372,15 @@ def test_zero_data_zero_solution(orc):
     assert np.all(u == 0)
 
 
-@pytest.mark.parametrize("nx,ny,p", [(4, 4, 8), (2, 4, 6), (4, 2, 10)])
-def test_tree_polynomial_exact(orc, nx, ny, p):
+@pytest.mark.parametrize("nx,ny,p,y1", [(4, 4, 8, None), (2, 4, 6, None), (4, 2, 10, None),
+                                         (2, 1, 8, 1.0), (4, 2, 6, 1.0), (1, 2, 10, 0.6)])
+def test_tree_polynomial_exact(orc, nx, ny, p, y1):
     """Algorithm 2 reproduces a global polynomial of degree p-1 exactly,
-    including the upward pass (Y, Gamma, Upsilon, Gamma^tau) — SURVEY §8(c)."""
-    x0, x1, y0, y1 = 0.0, 1.0, 0.0, 1.0 * ny / nx
+    including the upward pass (Y, Gamma, Upsilon, Gamma^tau) — SURVEY §8(c).  The last three
+    cases have rectangular leaves (2x1 grid on the unit square: 0.5 x 1 leaves; 4x2: 0.25 x 0.5;
+    1x2 on [0,1]x[0,0.6]: 1 x 0.3), so a swapped h_x / h_y anywhere in the tree fails."""
+    x0, x1, y0 = 0.0, 1.0, 0.0
+    y1 = 1.0 * ny / nx if y1 is None else y1
     kappa, eta = 6.0, 6.0 + 2j
     P = Poly2D(p - 1, (x0, x1, y0, y1), seed=11)
     X, Y = orc.leaf_nodes(x0, x1, y0, y1, nx, ny, p)
