@@ -3,8 +3,10 @@
 precomputation (batched leaf build + merge tree, Algorithm 1) followed by the solve sweeps
 (Algorithm 2) — through the C-ABI of libhps.so.
 
-Default workload: BASELINE.json configs[1] (C2: unit square, 32x32 leaves, p = 16,
-kappa = eta = 40 pi, 1 RHS).  `--config 3` runs C3 (128x128 leaves, 64 RHS).
+Default workload: BASELINE.json configs[3] (C4: unit square, 256x256 leaves = 16.7M Chebyshev
+nodes, p = 16, kappa = eta at 10 points per wavelength, 16 RHS) -- the largest configuration that
+fits one GPU (BASELINE.json names no config for the metric; C5 needs 8 GPUs).  `--config 2`
+runs C2 (32x32 leaves, 1 RHS), `--config 3` C3 (128x128 leaves, 64 RHS).
 
 Metric (BASELINE.json): "HPS precompute sec & DOF/s; solve ms per RHS; FP64-TC % of peak;
 HBM GB/s".  `value` is DOF/s of one full step (DOF = unique discretisation nodes, reading
@@ -113,6 +115,60 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cfg_dict(cfg, nrhs, world):
+    """The workload description -- identical in both arms (the driver compares them)."""
+    return {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs, "dof": cfg.n_unique,
+            "kappa": round(cfg.kappa, 4), "keep_root_R": True,
+            "l2": "256 MiB buffer written between steps; stored operators (> 1 GB) exceed L2",
+            "parallelism": "single GPU" if world == 1 else f"subtree shards x{world}"}
+
+
+def merge_levels(cfg):
+    """(depth d, n3, n1, ntau) of every merge level (SURVEY 8(a) A1 split rule)."""
+    q = cfg.p - 2
+    a, b = cfg.nx, cfg.ny
+    dims = [(a, b)]
+    while (a, b) != (1, 1):
+        if a >= b:
+            a //= 2
+        else:
+            b //= 2
+        dims.append((a, b))
+    out = []
+    for d in range(len(dims) - 1):
+        pa, pb = dims[d]
+        ca, cb = dims[d + 1]
+        n3 = (cb if pa >= pb else ca) * q
+        n1 = 2 * (ca + cb) * q - n3
+        out.append((d, n3, n1, 2 * n1))
+    return out
+
+
+def solve_model(cfg, nrhs):
+    """SURVEY 8(d) algorithmic solve work per RHS batch: (bytes, flops).  Bytes: every stored
+    operator read once (leaf [Psi | Y], and per merge W^-1, R33a, R33b, R13a, R23b, Phi^a, Phi^b) +
+    s read, u~ written and read back, u written; flops: 8 per complex multiply-add."""
+    p, q = cfg.p, cfg.p - 2
+    nt, ni, nb = p * p - 4, q * q, 4 * q
+    by = 16.0 * cfg.nleaf * (nt * nt + (ni + 3 * nt) * nrhs)
+    fl = 8.0 * cfg.nleaf * nt * (ni + nb) * nrhs
+    for d, n3, n1, ntau in merge_levels(cfg):
+        m = 2 ** d
+        by += 16.0 * m * (3 * n3 * n3 + 2 * n1 * n3 + 2 * n3 * ntau)
+        fl += 8.0 * m * (3 * n3 * n3 + 2 * n1 * n3 + 2 * n3 * ntau) * nrhs
+    return by, fl
+
+
 def setup(cfg, hps):
     g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
     X, Y = hps.leaf_nodes(g, cfg.p)
@@ -144,14 +200,18 @@ def run_hps(args, rank, world, dist):
     t_d = torch.from_numpy(np.ascontiguousarray(t)).to(dev)
     u_d = torch.empty((nrhs, cfg.nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128, device=dev)
     l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
+    # opt in to the library's cross-handle cache of large blocks: every step builds a fresh handle
+    # of the same shapes, and re-mapping tens of GB per step would time the driver, not the method
+    total_mem = torch.cuda.get_device_properties(local).total_memory
+    hps.set_cache_limit(int(0.9 * total_mem))
     plan = None
     if not args.no_plan:
         # representative-action planner: measured once per machine/process,
         # outside the timed region, like the paper's representative times
         plan = {lab: hps.REGIMES[reg] for lab, n, nb, reg, tab in hps.plan_problem(g, cfg.p)}
 
-    def step(profile=0):
-        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=True, device=local, profile=profile)
+    def step(profile=0, keep_root_R=True):
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=keep_root_R, device=local, profile=profile)
         S.solve(s_d, t_d, u_d)
         rec = dict(build_ms=S.time_ms(0), leaf_ms=S.time_ms(1), merge_ms=S.time_ms(2), solve_ms=S.time_ms(3),
                    up_ms=S.time_ms(4), down_ms=S.time_ms(5), launches=S.launches(0) + S.launches(1),
@@ -183,11 +243,18 @@ def run_hps(args, rank, world, dist):
             dist.barrier()
         wall = time.perf_counter() - w0
         # the dominant class's launches timed with CUDA events on the library stream over a second
-        # set of K steps (events between hundreds of small launches would lengthen the step)
-        for _ in range(args.steps):
+        # set of steps (events between hundreds of small launches would lengthen the step)
+        kx = min(args.steps, 3)
+        for _ in range(kx):
             flush_l2(torch, l2buf)
             torch.cuda.synchronize()
             krecs.append(step(profile=dom_mask))
+        # the build without the root operator R^1 (Algorithm 2 never reads it)
+        nrecs = []
+        for _ in range(kx):
+            flush_l2(torch, l2buf)
+            torch.cuda.synchronize()
+            nrecs.append(step(keep_root_R=False))
     clocks = clk.summary()
     step_ms = statistics.mean(r["build_ms"] + r["solve_ms"] for r in recs)
     build_ms = statistics.mean(r["build_ms"] for r in recs)
@@ -222,10 +289,32 @@ def run_hps(args, rank, world, dist):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = tt.item()
 
+    hps.set_cache_limit(0)   # give the parked blocks back
     if rank != 0:
         return None
     dof = cfg.n_unique
     value = world * dof / (step_ms / 1e3)
+    build_nr_ms = statistics.mean(r["build_ms"] for r in nrecs)
+    peak64, peak64_src = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    fl_build = flop_model(cfg)
+    fl_build_nr = flop_model(cfg, root_R=False)
+    sb, sf = solve_model(cfg, nrhs)
+    t_build_roof = fl_build / (peak64 * 1e12)
+    t_solve_roof = max(sb / (hbm * 1e9), sf / (peak64 * 1e12))
+    roofs = {
+        "model": "SURVEY 8(d): build = leaf 8 n_tau^3 + merges (8 flop per complex MAC) / FP64 DMMA peak; "
+                 "solve = max(bytes / HBM, flop / DMMA) with every stored operator read once",
+        "build_flop": fl_build, "build_roofline_s": round(t_build_roof, 6),
+        "build_frac": round(t_build_roof / (build_ms / 1e3), 4),
+        "build_flop_no_root_R": fl_build_nr,
+        "build_frac_no_root_R": round(fl_build_nr / (peak64 * 1e12) / (build_nr_ms / 1e3), 4),
+        "build_executed_tflops": round(statistics.mean(r["build_flops"] for r in recs) / (build_ms / 1e3) / 1e12, 3),
+        "solve_bytes": sb, "solve_flop": sf, "solve_roofline_ms": round(1e3 * t_solve_roof, 3),
+        "solve_bound": "hbm" if sb / (hbm * 1e9) >= sf / (peak64 * 1e12) else "fp64",
+        "solve_frac": round(t_solve_roof / (solve_ms / 1e3), 4),
+        "solve_hbm_gbs": round(sb / (solve_ms / 1e3) / 1e9, 1),
+    }
     # ---- roofline of the dominant kernel class (device time from CUDA events) ----
     agg = {}
     for r in krecs:
@@ -237,6 +326,8 @@ def run_hps(args, rank, world, dist):
     A = agg[dom]
     traffic_tab = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json"), {})
     traffic = traffic_tab.get(f"C{args.config}", {}).get(dom)
+    if isinstance(traffic, dict):   # class average over every launch of one ncu-captured step
+        traffic = traffic.get("avg_dram_bytes_per_launch")
     if A["flops"] > 0 and dom not in HBM_CLASSES:
         peak, src = fp64_peak()
         achieved = A["flops"] / (A["ms"] / 1e3) / 1e12
@@ -260,15 +351,14 @@ def run_hps(args, rank, world, dist):
         "metric": METRIC, "value": round(value, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
-                   "dof": dof, "kappa": round(cfg.kappa, 4), "keep_root_R": True,
-                   "l2": "256 MiB buffer written between steps; stored operators > L2",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+        "config": cfg_dict(cfg, nrhs, world),
         "build_s": round(build_ms / 1e3, 6), "build_dof_per_s": round(world * dof / (build_ms / 1e3), 1),
+        "build_s_no_root_R": round(build_nr_ms / 1e3, 6),
         "solve_ms_per_rhs": round(solve_ms / nrhs, 4),
         "build_tflops": round(statistics.mean(r["build_flops"] for r in recs) / (build_ms / 1e3) / 1e12, 3),
         "phase_ms": {k: round(statistics.mean(r[k] for r in recs), 3)
                      for k in ["leaf_ms", "merge_ms", "up_ms", "down_ms"]},
+        "roofline_phases": roofs,
         "kernel_classes_probe_step": per_class,
         "plan": plan,
         "roofline": roof,
@@ -279,6 +369,7 @@ def run_hps(args, rank, world, dist):
                 "h2d_bytes_per_step": int(c.nbytes + s.nbytes + t.nbytes),
                 "d2h_bytes_per_step": int(nrhs * cfg.nleaf * (cfg.p * cfg.p - 4) * 16), "s_per_step": round(e2e_s, 4)},
     }
+    out["host"] = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, c, s, t, args)
     return out
@@ -385,8 +476,10 @@ def cpu_baseline(cfg, c, s, t, args):
                       f"method's flop count to {cfg.nx}x{cfg.ny} leaves, {nrhs} RHS"}
 
 
-def flop_model(cfg):
-    """Algorithmic build flops (leaf 8 nt^3 + merges incl. root R), as counted by libhps."""
+def flop_model(cfg, root_R=True):
+    """SURVEY 8(d) algorithmic build flops: leaf LU + inverse of B (8 n_tau^3) + every merge's
+    W, W^-1, Phi^a, Phi^b and R^tau (8 flop per complex multiply-add); root_R=False drops the root
+    level's R^tau product (Algorithm 2 never reads R^1)."""
     q, p = cfg.p - 2, cfg.p
     nt = p * p - 4
     fl = 8.0 * nt ** 3 * cfg.nleaf
@@ -405,7 +498,7 @@ def flop_model(cfg):
         nbc = 2 * (ca + cb) * q
         n1 = nbc - n3
         ntau = 2 * n1
-        fl += 8.0 * 2 ** d * (2 * n3 ** 3 + n3 * n3 * n1 + 2 * n3 * n3 * ntau + ntau * ntau * n3)
+        fl += 8.0 * 2 ** d * (2 * n3 ** 3 + n3 * n3 * n1 + 2 * n3 * n3 * ntau + (ntau * ntau * n3 if (d or root_R) else 0))
     return fl
 
 
@@ -444,10 +537,9 @@ def run_reference(args, rank, world):
     return {"metric": METRIC, "value": round(val, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * step_s, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
-                       "dof": cfg.n_unique},
+            "config": cfg_dict(cfg, nrhs, world),
             "cpu_baseline": {"value": round(val, 1), "unit": "DOF/s", "cores": cpu_cores(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": round(val, 1), "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -456,7 +548,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--nrhs", type=int, default=0)
     ap.add_argument("--impl", default="hps", choices=["hps", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
