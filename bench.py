@@ -14,10 +14,11 @@ Q16; step time = device time of build + solve on the library stream), summed ove
 the extra keys carry the build seconds, build DOF/s and solve ms per RHS.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl hps|reference]
-Under torchrun (N > 1) the workload is SHARDED by subtree (paper_1812_07167_b200.dist): each
-rank builds and solves its 1/N of the leaves and its subtree with no communication, the
-subtree-root operators / outgoing data are all-gathered over NCCL and the top log2(N) levels
-are merged on every rank (strong scaling of the same workload).
+Under torchrun (N > 1) the workload is SHARDED by subtree inside libhps:
+each rank builds and solves its 1/N of the leaves and its subtree with no communication; the top
+log2(N) levels run with the group split (W, W^-1 replicated in a group, Phi and R^tau split by
+columns) over NCCL.  Strong scaling of the same workload; device time (library events, including
+the collectives) max over ranks.
 """
 import argparse
 import json
@@ -194,11 +195,20 @@ def run_hps(args, rank, world, dist):
     nrhs = args.nrhs or cfg.nrhs
     g, c, s, t = setup(cfg, hps)
     s, t = s[:nrhs], t[:nrhs]
+    comm, g_plan, nleaf = None, g, cfg.nleaf
+    if world > 1:
+        # subtree sharding: this rank's rectangle of c, s, u; the exchange runs inside libhps over NCCL
+        from paper_1812_07167_b200 import dist as hdist
+        comm = hdist.init_nccl()
+        sub, i0, j0 = hdist.local_block(g, world, rank)
+        c = np.ascontiguousarray(hdist.slice_leaves(c, g, sub, i0, j0))
+        s = np.ascontiguousarray(hdist.slice_leaves(s, g, sub, i0, j0))
+        g_plan, nleaf = sub, sub.nx * sub.ny
     dev = f"cuda:{local}"
     c_d = torch.from_numpy(c).to(dev)
     s_d = torch.from_numpy(np.ascontiguousarray(s)).to(dev)
     t_d = torch.from_numpy(np.ascontiguousarray(t)).to(dev)
-    u_d = torch.empty((nrhs, cfg.nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128, device=dev)
+    u_d = torch.empty((nrhs, nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128, device=dev)
     l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
     # opt in to the library's cross-handle cache of large blocks: every step builds a fresh handle
     # of the same shapes, and re-mapping tens of GB per step would time the driver, not the method
@@ -208,10 +218,11 @@ def run_hps(args, rank, world, dist):
     if not args.no_plan:
         # representative-action planner: measured once per machine/process,
         # outside the timed region, like the paper's representative times
-        plan = {lab: hps.REGIMES[reg] for lab, n, nb, reg, tab in hps.plan_problem(g, cfg.p)}
+        plan = {lab: hps.REGIMES[reg] for lab, n, nb, reg, tab in hps.plan_problem(g_plan, cfg.p)}
 
     def step(profile=0, keep_root_R=True):
-        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=keep_root_R, device=local, profile=profile)
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=keep_root_R, device=local, profile=profile,
+                       comm=comm)
         S.solve(s_d, t_d, u_d)
         rec = dict(build_ms=S.time_ms(0), leaf_ms=S.time_ms(1), merge_ms=S.time_ms(2), solve_ms=S.time_ms(3),
                    up_ms=S.time_ms(4), down_ms=S.time_ms(5), launches=S.launches(0) + S.launches(1),
@@ -268,7 +279,7 @@ def run_hps(args, rank, world, dist):
     c_h = torch.from_numpy(c).pin_memory()
     s_h = torch.from_numpy(np.ascontiguousarray(s)).pin_memory()
     t_h = torch.from_numpy(np.ascontiguousarray(t)).pin_memory()
-    u_h = torch.empty((nrhs, cfg.nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128).pin_memory()
+    u_h = torch.empty((nrhs, nleaf, cfg.p * cfg.p - 4), dtype=torch.complex128).pin_memory()
     e2e = []
     for k in range(args.warmup + args.steps):
         flush_l2(torch, l2buf)
@@ -276,7 +287,7 @@ def run_hps(args, rank, world, dist):
         if world > 1:
             dist.barrier()
         e0 = time.perf_counter()
-        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_h, keep_root_R=True, device=local)
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_h, keep_root_R=True, device=local, comm=comm)
         S.solve(s_h, t_h, u_h)
         _ = complex(u_h[0, 0, 0])        # result read on the host
         e1 = time.perf_counter()
@@ -290,28 +301,33 @@ def run_hps(args, rank, world, dist):
         e2e_s = tt.item()
 
     hps.set_cache_limit(0)   # give the parked blocks back
+    build_nr_ms = statistics.mean(r["build_ms"] for r in nrecs)
+    if world > 1:
+        tt = torch.tensor([build_nr_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        build_nr_ms = tt.item()
+        comm.close()
     if rank != 0:
         return None
-    dof = cfg.n_unique
-    value = world * dof / (step_ms / 1e3)
-    build_nr_ms = statistics.mean(r["build_ms"] for r in nrecs)
+    dof = cfg.n_unique       # the whole job's unknowns (strong scaling: the same problem on N GPUs)
+    value = dof / (step_ms / 1e3)
     peak64, peak64_src = fp64_peak()
     hbm, hbm_src = hbm_peak()
     fl_build = flop_model(cfg)
     fl_build_nr = flop_model(cfg, root_R=False)
     sb, sf = solve_model(cfg, nrhs)
-    t_build_roof = fl_build / (peak64 * 1e12)
-    t_solve_roof = max(sb / (hbm * 1e9), sf / (peak64 * 1e12))
+    t_build_roof = fl_build / (world * peak64 * 1e12)          # N GPUs: N x the per-GPU peaks
+    t_solve_roof = max(sb / (world * hbm * 1e9), sf / (world * peak64 * 1e12))
     roofs = {
         "model": "SURVEY 8(d): build = leaf 8 n_tau^3 + merges (8 flop per complex MAC) / FP64 DMMA peak; "
                  "solve = max(bytes / HBM, flop / DMMA) with every stored operator read once",
         "build_flop": fl_build, "build_roofline_s": round(t_build_roof, 6),
         "build_frac": round(t_build_roof / (build_ms / 1e3), 4),
         "build_flop_no_root_R": fl_build_nr,
-        "build_frac_no_root_R": round(fl_build_nr / (peak64 * 1e12) / (build_nr_ms / 1e3), 4),
+        "build_frac_no_root_R": round(fl_build_nr / (world * peak64 * 1e12) / (build_nr_ms / 1e3), 4),
         "build_executed_tflops": round(statistics.mean(r["build_flops"] for r in recs) / (build_ms / 1e3) / 1e12, 3),
         "solve_bytes": sb, "solve_flop": sf, "solve_roofline_ms": round(1e3 * t_solve_roof, 3),
-        "solve_bound": "hbm" if sb / (hbm * 1e9) >= sf / (peak64 * 1e12) else "fp64",
+        "solve_bound": "hbm" if sb / hbm / 1e9 >= sf / peak64 / 1e12 else "fp64",
         "solve_frac": round(t_solve_roof / (solve_ms / 1e3), 4),
         "solve_hbm_gbs": round(sb / (solve_ms / 1e3) / 1e9, 1),
     }
@@ -352,7 +368,7 @@ def run_hps(args, rank, world, dist):
         "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "config": cfg_dict(cfg, nrhs, world),
-        "build_s": round(build_ms / 1e3, 6), "build_dof_per_s": round(world * dof / (build_ms / 1e3), 1),
+        "build_s": round(build_ms / 1e3, 6), "build_dof_per_s": round(dof / (build_ms / 1e3), 1),
         "build_s_no_root_R": round(build_nr_ms / 1e3, 6),
         "solve_ms_per_rhs": round(solve_ms / nrhs, 4),
         "build_tflops": round(statistics.mean(r["build_flops"] for r in recs) / (build_ms / 1e3) / 1e12, 3),
@@ -365,78 +381,15 @@ def run_hps(args, rank, world, dist):
         "clocks": clocks,
         "wall_s_timed_region": round(wall, 3),
         "gpu_launches": int(sum(r["launches"] for r in recs)),
-        "e2e": {"value": round(world * dof / e2e_s, 1), "unit": "DOF/s",
-                "h2d_bytes_per_step": int(c.nbytes + s.nbytes + t.nbytes),
-                "d2h_bytes_per_step": int(nrhs * cfg.nleaf * (cfg.p * cfg.p - 4) * 16), "s_per_step": round(e2e_s, 4)},
+        "e2e": {"value": round(dof / e2e_s, 1), "unit": "DOF/s",
+                "h2d_bytes_per_step": int(world * (c.nbytes + s.nbytes + t.nbytes)),
+                "d2h_bytes_per_step": int(world * nrhs * nleaf * (cfg.p * cfg.p - 4) * 16), "s_per_step": round(e2e_s, 4),
+                "note": "per-rank host buffers summed over ranks; time = max over ranks"},
     }
     out["host"] = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, c, s, t, args)
     return out
-
-
-def run_sharded(args, rank, world, dist_mod):
-    """N > 1: subtree-sharded build + solve over NCCL (strong scaling of one workload)."""
-    import torch
-    from paper_1812_07167_b200 import dist as hdist
-    from paper_1812_07167_b200 import hps
-    import __graft_entry__
-    if rank == 0:
-        __graft_entry__.build()
-    dist_mod.barrier()
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dev = f"cuda:{local}"
-    cfg = inputs.CONFIGS[args.config]
-    nrhs = args.nrhs or cfg.nrhs
-    g, c, s, t = setup(cfg, hps)
-    s, t = s[:nrhs], t[:nrhs]
-    sub, i0, j0 = hdist.local_block(g, world, rank)
-    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-    c_l, s_l, t_d = d(hdist.slice_leaves(c, g, sub, i0, j0)), d(hdist.slice_leaves(s, g, sub, i0, j0)), d(t)
-    comm = hdist.TorchComm()
-    be = hdist.CudaBackend(device=local)
-    l2buf = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=dev)
-    launches = 0
-
-    def step():
-        nonlocal launches
-        D = hdist.DistributedHPS(comm, be, g, cfg.p, cfg.kappa, cfg.eta, c_l)
-        D.solve(s_l, t_d)
-        torch.cuda.synchronize()
-        launches += D.sub.launches(0) + D.sub.launches(1) + hps.lib().hps_last_launches(D.top.h, 0) + \
-            hps.lib().hps_last_launches(D.top.h, 1)
-        D.close()
-
-    for _ in range(args.warmup):
-        flush_l2(torch, l2buf)
-        step()
-    launches = 0
-    times = []
-    with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            flush_l2(torch, l2buf)
-            torch.cuda.synchronize()
-            dist_mod.barrier()
-            t0 = time.perf_counter()
-            step()
-            dist_mod.barrier()
-            times.append(time.perf_counter() - t0)
-    tt = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
-    dist_mod.all_reduce(tt, op=dist_mod.ReduceOp.MAX)
-    step_s = tt.item()
-    if rank != 0:
-        return None
-    return {"metric": METRIC, "value": round(cfg.n_unique / step_s, 1), "unit": "DOF/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * step_s, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
-            "data": "synthetic",
-            "config": {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs,
-                       "dof": cfg.n_unique, "parallelism": f"subtree shards x{world}, top {int(np.log2(world))} "
-                                                            f"levels replicated after an NCCL all-gather",
-                       "l2": "256 MiB buffer written between steps"},
-            "clocks": clk.summary(), "gpu_launches": int(launches),
-            "timing": "host wall clock between barriers + device synchronize, max over ranks"}
 
 
 def oracle_run(cfg, c, s, t):
@@ -565,7 +518,7 @@ def main():
             import torch.distributed as dist
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
             dist.init_process_group("nccl")
-            out = run_sharded(args, rank, world, dist)
+            out = run_hps(args, rank, world, dist)
         else:
             out = run_hps(args, rank, world, dist)
         if dist is not None:

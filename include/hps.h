@@ -50,6 +50,9 @@ extern "C" {
 #define HPS_ENOMEM (-3)    /* device allocation failed */
 #define HPS_ECUDA (-4)     /* CUDA runtime / launch error */
 #define HPS_ENOTKEPT (-5)  /* export of an operator the handle did not keep */
+#define HPS_ENCCL (-6)     /* NCCL failure / NCCL not loadable (multi-GPU only) */
+
+#define HPS_NCCL_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
 
 typedef struct {
   double x0, x1, y0, y1; /* the rectangle Omega, x1 > x0, y1 > y0 */
@@ -61,6 +64,7 @@ typedef struct {
 } hps_c128;
 
 typedef struct hps_handle hps_handle;
+typedef struct hps_comm hps_comm; /* communicator of the subtree-sharded build / solve (below) */
 
 typedef struct {
   int32_t keep_root_R;  /* 1: form the root ItI operator R^1 (Algorithm 1, tau = 1).  Algorithm 2
@@ -90,9 +94,29 @@ typedef struct {
                              interpolates each segment's degree-(q-1) polynomial to its Chebyshev
                              nodes.  u is always returned at the Chebyshev leaf nodes.
                            Other values: HPS_EINVAL */
+  /* ---- multi-GPU and stream; zero-initialised = single GPU ---- */
+  int32_t n_gpus;       /* 1, 2, 4, 8, ... (power of two): SPMD, one process (or virtual rank) per GPU;
+                           0 = the communicator's size (1 without one) */
+  void* nccl_comm;      /* an ncclComm_t of n_gpus ranks (hps_nccl_comm_init, or the caller's own);
+                           the library wraps it (collective: every rank's hps_build must run) */
+  void* stream;         /* cudaStream_t to order ALL of the handle's work on; NULL = a stream the
+                           library creates.  Device inputs must be complete in this stream's order.
+                           hps_build always returns synchronised (it reads pivot flags); with a
+                           caller stream and device pointers hps_solve returns WITHOUT waiting
+                           (hps_sync waits); host pointers make it synchronous */
+  hps_comm* comm;       /* library communicator (hps_comm_wrap_nccl, hps_vcomm_rank); takes
+                           precedence over nccl_comm */
 } hps_opts;
 
 /* Precomputation stage (Algorithm 1).
+ *  Multi-GPU (n_gpus = G > 1, a communicator in opts): SPMD -- every rank calls hps_build with the
+ *  SAME g, p, q, kappa, eta and its own c_samples.  The top log2(G) splits of the tree give G
+ *  congruent rectangles (hps_subtree_grid(g, log2 G, rank)); rank r builds the leaves and every
+ *  merge of its rectangle with no communication, then the top log2(G) levels run with the group
+ *  split of SURVEY §8(e): at a level with 2^k merges, the G / 2^k ranks under a box all-gather
+ *  the children's ItI maps, form W and W^{-1} (replicated in the group) and each computes a
+ *  1 / (G / 2^k) column slice of Phi^alpha, Phi^beta and R^tau (R^tau stays column-distributed
+ *  until the next level's all-gather).  With keep_root_R the root R is gathered at the end.
  *  g         : domain and leaf grid (nx, ny powers of two; leaves must be congruent rectangles).
  *  p         : Chebyshev points per leaf side, p >= 4.
  *  q         : boundary nodes per leaf edge; must equal p - 2 (corner-free scheme).
@@ -100,6 +124,8 @@ typedef struct {
  *  eta       : impedance parameter, Re(eta) != 0.
  *  c_samples : c(x) at every leaf's p*p tensor nodes, [nx*ny leaves, natural order][p*p]; corner
  *              values are ignored.  Host or device memory; complex (the PDE allows complex c).
+ *              Multi-GPU: this rank's rectangle only, [nx*ny/G][p*p] in the rectangle's own
+ *              natural order.
  *  opt       : NULL for defaults.
  *  out       : receives the handle (NULL on error). */
 int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_c128* c_samples,
@@ -111,8 +137,40 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
  *  t : incoming impedance data on the root boundary, [nrhs][2(nx+ny)q] in [S,E,N,W] order.
  *  u : output, [nrhs][nx*ny leaves][p*p-4]; each leaf in [I_b (S,E,N,W); I_i] order
  *      (PAPER.md:321-325).  Nodes on a shared edge appear once per leaf.
- *  Host or device pointers. */
+ *  Host or device pointers.  Multi-GPU (collective): s and u are this rank's rectangle
+ *  ([nrhs][nx*ny/G][...], local natural order), t is the whole root boundary on every rank. */
 int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps_c128* u);
+
+/* Wait for the handle's enqueued work (a stream-ordered hps_solve) and finish its timings.
+ * Returns 0 or HPS_ECUDA. */
+int hps_sync(hps_handle* h);
+
+/* ---- Communicators (multi-GPU) ----------------------------------------------------------
+ * NCCL: rank 0 calls hps_nccl_unique_id and sends the HPS_NCCL_ID_BYTES bytes to every rank
+ * (the Python layer uses torch.distributed); every rank then calls hps_nccl_comm_init on its own
+ * device (ncclCommInitRank) and passes the result as opts.nccl_comm, or wraps it once with
+ * hps_comm_wrap_nccl (collective; creates the group split communicators) and passes opts.comm.
+ * NCCL is loaded at run time (libnccl.so.2 already in the process, else the loader's path):
+ * HPS_ENCCL if it is missing.
+ * Virtual ranks (tests, one GPU): hps_vcomm_create(G) makes a group, hps_vcomm_rank(group, r) the
+ * communicator of rank r; rank r's calls must run on their own host thread, all on one device.
+ * hps_comm_selftest: collective all-gather of rank-stamped data in groups of gs, checked. */
+int hps_nccl_unique_id(char* id /* HPS_NCCL_ID_BYTES */);
+int hps_nccl_comm_init(int nranks, int rank, const char* id, void** nccl_comm);
+int hps_nccl_comm_destroy(void* nccl_comm);
+int hps_comm_wrap_nccl(void* nccl_comm, hps_comm** out);
+int hps_vcomm_create(int nranks, void** group);
+int hps_vcomm_rank(void* group, int rank, hps_comm** out);
+int hps_vcomm_destroy(void* group);
+int hps_comm_info(const hps_comm* c, int* rank, int* size);
+int hps_comm_selftest(hps_comm* c, int gs);
+void hps_comm_free(hps_comm* c);
+
+/* Host-only plan of the sharded top levels for rank `rank` of G: for each top depth d = 0 ..
+ * log2(G) - 1 (root first) writes 8 ints to info[8 d ...]: group size gs, rank in the group,
+ * side (0: under the alpha child, 1: beta), n3, n1, n_tau, first column j0 and width w of this
+ * rank's column slice of Phi / R^tau (in [I1, I2] order).  Returns log2(G) or HPS_EINVAL. */
+int hps_dist_plan(const hps_grid* g, int p, int G, int rank, int32_t* info, int maxlev);
 
 /* ---- Subtree sharding (multi-GPU) ---------------------------------------
  * The tree's top `depth` levels are split off: rank r builds the subtree of the depth-`depth`

@@ -39,6 +39,9 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -67,9 +70,12 @@ static Mat identity(int n) {
   return I;
 }
 
-// C = A * B, triple loop.
+// C = A * B, triple loop.  Rows of C are independent: for big products they are spread over
+// OpenMP threads (each element still accumulates over k in increasing order, so the result is
+// bitwise the same for any thread count; nested inside the per-box loops it runs serially).
 static Mat matmul(const Mat& A, const Mat& B) {
   Mat C(A.m, B.n);
+#pragma omp parallel for schedule(static) if ((double)A.m * A.n * B.n > 4e6)
   for (int i = 0; i < A.m; ++i)
     for (int k = 0; k < A.n; ++k) {
       const cplx aik = A(i, k);
@@ -134,6 +140,8 @@ static int lu_factor(Mat& A, std::vector<int>& perm) {
       for (int j = 0; j < n; ++j) std::swap(A(k, j), A(r, j));
       std::swap(perm[k], perm[r]);
     }
+    // rows below the pivot are independent (same per-element operations for any thread count)
+#pragma omp parallel for schedule(static) if ((double)(n - k) * (n - k) > 1e5)
     for (int i = k + 1; i < n; ++i) {
       A(i, k) /= A(k, k);
       const cplx l = A(i, k);
@@ -144,25 +152,32 @@ static int lu_factor(Mat& A, std::vector<int>& perm) {
 }
 
 // Solve A X = Bm given the LU factors of A (forward then back substitution).
+// Columns of X are independent: big solves split the columns over OpenMP threads (every element
+// sees the same operations in the same order for any thread count).
 static Mat lu_solve(const Mat& LU, const std::vector<int>& perm, const Mat& Bm) {
   const int n = LU.n, nr = Bm.n;
   Mat X(n, nr);
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < nr; ++j) X(i, j) = Bm(perm[i], j);
-  for (int i = 0; i < n; ++i)          // L y = P b (unit lower)
-    for (int k = 0; k < i; ++k) {
-      const cplx l = LU(i, k);
-      if (l == cplx(0, 0)) continue;
-      for (int j = 0; j < nr; ++j) X(i, j) -= l * X(k, j);
+  const int cw = 32;  // column block
+#pragma omp parallel for schedule(dynamic, 1) if ((double)n * n * nr > 4e6)
+  for (int j0 = 0; j0 < nr; j0 += cw) {
+    const int j1 = std::min(nr, j0 + cw);
+    for (int i = 0; i < n; ++i)          // L y = P b (unit lower)
+      for (int k = 0; k < i; ++k) {
+        const cplx l = LU(i, k);
+        if (l == cplx(0, 0)) continue;
+        for (int j = j0; j < j1; ++j) X(i, j) -= l * X(k, j);
+      }
+    for (int i = n - 1; i >= 0; --i) {   // U x = y
+      for (int k = i + 1; k < n; ++k) {
+        const cplx u = LU(i, k);
+        if (u == cplx(0, 0)) continue;
+        for (int j = j0; j < j1; ++j) X(i, j) -= u * X(k, j);
+      }
+      const cplx d = LU(i, i);
+      for (int j = j0; j < j1; ++j) X(i, j) /= d;
     }
-  for (int i = n - 1; i >= 0; --i) {   // U x = y
-    for (int k = i + 1; k < n; ++k) {
-      const cplx u = LU(i, k);
-      if (u == cplx(0, 0)) continue;
-      for (int j = 0; j < nr; ++j) X(i, j) -= u * X(k, j);
-    }
-    const cplx d = LU(i, i);
-    for (int j = 0; j < nr; ++j) X(i, j) /= d;
   }
   return X;
 }
@@ -886,6 +901,17 @@ int oracle_invert(int n, const cplx* A, cplx* Ainv) {
   if (inverse(M, Mi)) return -2;
   std::copy(Mi.a.begin(), Mi.a.end(), Ainv);
   return 0;
+}
+
+// Thread count of the oracle's OpenMP loops (tests pin that results do not depend on it).
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
 }
 
 int oracle_matmul(int m, int k, int n, const cplx* A, const cplx* B, cplx* C) {

@@ -12,8 +12,13 @@ _lib = None
 
 __all__ = [
     "build", "lib", "cheb", "leaf_nodes", "root_boundary", "leaf", "leaf_disc", "merge", "box_rect", "tree_info",
-    "Oracle", "global_dense", "invert", "matmul",
+    "Oracle", "global_dense", "invert", "matmul", "set_threads",
 ]
+
+
+def set_threads(n):
+    """Set the OpenMP thread count of the oracle (0: query); returns the count in effect."""
+    return lib().oracle_set_threads(int(n))
 
 
 def build(force=False):
@@ -56,6 +61,7 @@ def lib():
         L.oracle_global_dense.argtypes = [d, d, d, d, i32, i32, i32, d, d, d, dp, i32, dp, dp, dp, dp]
         L.oracle_invert.argtypes = [i32, dp, dp]
         L.oracle_matmul.argtypes = [i32, i32, i32, dp, dp, dp]
+        L.oracle_set_threads.argtypes = [i32]
         L.oracle_last_error.restype = C.c_char_p
         _lib = L
     return _lib

@@ -24,6 +24,7 @@
 
 #include "hps.h"
 #include "hps_internal.cuh"
+#include "hps_comm.cuh"
 #include "hps_kernels.cuh"
 
 thread_local int64_t* g_launch_counter = nullptr;
@@ -258,6 +259,20 @@ struct DevBuf {
   DevBuf() = default;
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      st = o.st;
+      dev = o.dev;
+      big_direct = o.big_direct;
+      o.p = nullptr;
+      o.bytes = 0;
+      o.big_direct = false;
+    }
+    return *this;
+  }
   DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), st(o.st), dev(o.dev), big_direct(o.big_direct) {
     o.p = nullptr;
     o.bytes = 0;
@@ -422,9 +437,28 @@ struct SolveState {
   }
 };
 
+// Column-slice plan of one sharded top level: the gs = G >> d ranks under a depth-d
+// box form its W, W^{-1} (replicated) and each the columns [j0, j0 + w) (in [I1, I2] order; padded
+// width wpad = ceil(ntau / gs), the same on every rank) of Phi^a, Phi^b and R^tau.
+struct DistLevel {
+  int gs = 1, grank = 0, side = 0, j0 = 0, w = 0, wpad = 0;
+};
+
 struct hps_handle {
   int dev = 0;
   cudaStream_t st = nullptr;
+  bool own_stream = true;          // false: the caller's stream (hps_opts.stream)
+  bool pending = false;            // a stream-ordered solve whose timings are not read yet
+  int solve_kind = 3;              // phases of the last solve: 1 up, 2 down, 3 both
+  // multi-GPU: G ranks, this one `rank`; D = log2 G sharded top levels.  The user's
+  // handle holds the rank's subtree (depth 0 = its subtree root); `top` the global tree above
+  // depth D (has_leaves = false, one merge per level with the column slices `dl`).
+  HpsComm* comm = nullptr;
+  bool comm_owned = false;
+  int G = 1, D = 0, rank = 0;
+  std::unique_ptr<hps_handle> top;
+  bool dist_top = false;           // this is the top handle of a sharded build
+  std::vector<DistLevel> dl;
   hps_grid g{};
   int p = 0, q = 0, nbl = 0, ni = 0, nt = 0;
   double kappa = 0;
@@ -470,14 +504,16 @@ struct hps_handle {
     }
     for (auto& r : R) r.release();
     info.release();
+    top.reset();
     if (st) cudaStreamSynchronize(st);
     if (st2) cudaStreamSynchronize(st2);
+    if (comm_owned) delete comm;
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (st2) cudaStreamDestroy(st2);
-    if (st) cudaStreamDestroy(st);
+    if (st && own_stream) cudaStreamDestroy(st);
   }
 };
 
@@ -583,8 +619,11 @@ void plan_level(hps_handle& H, int d, MergeLevel& M) {
   M.pp = base + o5;
   M.cmapA = base + o6;
   M.cmapB = base + o7;
-  // stored operators: Phi^a, Phi^b, W^{-1}, R33a, R33b, R13a, R23b
-  const size_t n3 = M.n3, nt = M.ntau, n1 = M.n1, n2 = M.n2, np = M.nparent;
+  // stored operators: Phi^a, Phi^b, W^{-1}, R33a, R33b, R13a, R23b.  A sharded
+  // top level (H.G > 1) stores ONE merge with this rank's column slices of Phi^a, Phi^b.
+  const bool dist = H.dist_top;
+  const size_t n3 = M.n3, nt = dist ? (size_t)H.dl[d].wpad : (size_t)M.ntau, n1 = M.n1, n2 = M.n2,
+               np = dist ? 1 : M.nparent;
   const size_t per = 2 * n3 * nt + 3 * n3 * n3 + n1 * n3 + n2 * n3;
   M.ops.alloc(sizeof(zt) * per * np);
   zt* o = M.ops.as<zt>();
@@ -852,6 +891,48 @@ cudaStream_t side_solve(const hps_handle& H) {
   return off || H.prof.timing ? H.st : H.st2;
 }
 
+// W = I - R33b R33a (Algorithm 1 line 7) for `np` merges and its explicit inverse into Winv.
+// For nat_min <= n3 <= nat_max (the few, latency-bound top-level inverses) natural order first
+// (DESIGN.md 3.10); if a pivot fails its relative check W is formed again and inverted with partial
+// pivoting (reading Q21).
+void form_and_invert_W(hps_handle& H, int d, int np, const zt* R33a, const zt* R33b, zt* Winv) {
+  const int n3 = H.lev[d].n3;
+  const int64_t s33 = (int64_t)n3 * n3;
+  cudaStream_t st = H.st;
+  DevBuf Wk, ws;
+  Wk.alloc(sizeof(zt) * s33 * np);
+  auto form = [&] {
+    ZGemm g;
+    g.M = g.N = g.K = n3;
+    g.batch = np;
+    g.A = op(R33b, n3, s33);
+    g.B = op(R33a, n3, s33);
+    g.C = out(Wk.as<zt>(), n3, s33);
+    g.alpha = Z(-1, 0);
+    g.diag = Z(1, 0);
+    zgemm(g, st);
+  };
+  form();
+  bool done = false;
+  if (n3 >= knob(KN_NAT_MIN) && n3 <= knob(KN_NAT_MAX)) {
+    ws.alloc(std::max<size_t>(zgj_natural_workspace_bytes(n3, np), 16));
+    DevBuf flag;
+    flag.alloc(sizeof(int));
+    HPS_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    zgj_invert_natural(Wk.as<zt>(), n3, s33, Winv, n3, s33, n3, np, ws.p, flag.as<int>(), st);
+    int hflag = 0;
+    HPS_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+    done = hflag == 0 && knob(KN_NAT_FORCE_FAIL) == 0;
+    H.nat_levels += done ? 1 : 0;
+    if (!done) form();  // the natural-order attempt destroyed W
+  }
+  if (!done) {
+    ws.alloc(std::max<size_t>(zgj_workspace_bytes(n3, np), 16));
+    zgj_invert(Wk.as<zt>(), n3, s33, Winv, n3, s33, n3, np, ws.p, H.info.as<int>() + 1 + d, st, nullptr);
+  }
+}
+
 void build_merge(hps_handle& H, int d) {
   MergeLevel& M = H.lev[d];
   const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau, nbc = M.nbc;
@@ -907,54 +988,8 @@ void build_merge(hps_handle& H, int d) {
     zgemm(g, side_build(H));
   }
   HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, side_build(H)));
-  // (b) W = I - R33b R33a  (Algorithm 1 line 7)
-  DevBuf Wk, ws;
-  Wk.alloc(sizeof(zt) * s33 * np);
-  {
-    ZGemm g;
-    g.M = g.N = g.K = n3;
-    g.batch = np;
-    g.A = op(M.R33b, n3, s33);
-    g.B = op(M.R33a, n3, s33);
-    g.C = out(Wk.as<zt>(), n3, s33);
-    g.alpha = Z(-1, 0);
-    g.diag = Z(1, 0);
-    zgemm(g, st);
-  }
-  // (c) W^{-1}.  For 200 <= n3 <= 512 (the few, latency-bound top-level inverses) natural order
-  // first (measured pivots >= 0.8 of the diagonal at every C2 level); if a pivot fails its check
-  // W is formed again and inverted with partial pivoting.
-  const int nat_min = knob(KN_NAT_MIN);
-  bool done = false;
-  const int nat_max = knob(KN_NAT_MAX);
-  if (n3 >= nat_min && n3 <= nat_max) {
-    ws.alloc(std::max<size_t>(zgj_natural_workspace_bytes(n3, np), 16));
-    DevBuf flag;
-    flag.alloc(sizeof(int));
-    HPS_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
-    zgj_invert_natural(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, flag.as<int>(), st);
-    int hflag = 0;
-    HPS_CUDA_CHECK(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    HPS_CUDA_CHECK(cudaStreamSynchronize(st));
-    const bool force_fail = knob(KN_NAT_FORCE_FAIL) != 0;  // tests
-    done = hflag == 0 && !force_fail;
-    H.nat_levels += done ? 1 : 0;
-    if (!done) {  // W again: I - R33b R33a
-      ZGemm g;
-      g.M = g.N = g.K = n3;
-      g.batch = np;
-      g.A = op(M.R33b, n3, s33);
-      g.B = op(M.R33a, n3, s33);
-      g.C = out(Wk.as<zt>(), n3, s33);
-      g.alpha = Z(-1, 0);
-      g.diag = Z(1, 0);
-      zgemm(g, st);
-    }
-  }
-  if (!done) {
-    ws.alloc(std::max<size_t>(zgj_workspace_bytes(n3, np), 16));
-    zgj_invert(Wk.as<zt>(), n3, s33, M.Winv, n3, s33, n3, np, ws.p, H.info.as<int>() + 1 + d, st, nullptr);
-  }
+  // (b) W = I - R33b R33a (Algorithm 1 line 7) and (c) W^{-1}
+  form_and_invert_W(H, d, np, M.R33a, M.R33b, M.Winv);
   // (d) X = [R33b R31a | -R32b] ; Phi^a = W^{-1} X  (line 8)
   HPS_CUDA_CHECK(cudaStreamWaitEvent(st, H.ev_join, 0));  // X complete
   {
@@ -1025,8 +1060,253 @@ void build_merge(hps_handle& H, int d) {
 }
 
 // ---------------------------------------------------------------------------
+// Sharded top levels (PAPER.md:1336-1338 names distributed memory as the next
+// step).  H is the TOP handle of a multi-GPU build: global tree, bottom depth D = log2 G, one merge
+// per level per rank (the box above this rank's subtree), group of gs = G >> d ranks under it.
+// ---------------------------------------------------------------------------
+// The children's ItI maps of this rank's depth-d merge, whole, into Ra / Rb (nbc x nbc each,
+// canonical order): at d = D - 1 the children are two subtree roots (pair all-gather); above, each
+// child's R^tau is column-distributed over its gs / 2 ranks ([nbc][wpad] slices in the child
+// merge's [I1, I2] column order) and is all-gathered and scattered to canonical columns.
+void gather_children_R(hps_handle& H, int d, zt* Ra, zt* Rb) {
+  const MergeLevel& M = H.lev[d];
+  const DistLevel& P = H.dl[d];
+  const int nbc = M.nbc;
+  const int64_t cs2 = (int64_t)nbc * nbc;
+  cudaStream_t st = H.st;
+  if (d + 1 == H.D) {
+    H.comm->allgather(2, H.R[d + 1].p, Ra, sizeof(zt) * cs2, st);  // Rb == Ra + cs2
+    return;
+  }
+  const DistLevel& Pc = H.dl[d + 1];
+  const MergeLevel& Mc = H.lev[d + 1];
+  const int wc = Pc.wpad, half = P.gs / 2;
+  DevBuf gat;
+  gat.alloc(sizeof(zt) * (size_t)P.gs * nbc * wc);
+  H.comm->allgather(P.gs, H.R[d + 1].p, gat.p, sizeof(zt) * (size_t)nbc * wc, st);
+  std::vector<ZCopy> cps;
+  for (int k = 0; k < P.gs; ++k) {
+    const int kk = k % half, j0 = kk * wc, we = std::min(wc, nbc - j0);
+    if (we <= 0) continue;
+    ZCopy c;
+    c.batch = 1;
+    c.M = nbc;
+    c.N = we;
+    c.A = op(gat.as<zt>() + (int64_t)k * nbc * wc, wc, 0);
+    c.C = out(k < half ? Ra : Rb, nbc, 0, nullptr, Mc.pp + j0);
+    cps.push_back(c);
+  }
+  zcopy_multi(cps.data(), (int)cps.size(), st);
+}
+
+void build_merge_dist(hps_handle& H, int d) {
+  MergeLevel& M = H.lev[d];
+  const DistLevel& P = H.dl[d];
+  const int n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau, nbc = M.nbc;
+  const int j0 = P.j0, w = P.w, wp = P.wpad;
+  const int64_t cs2 = (int64_t)nbc * nbc, s33 = (int64_t)n3 * n3;
+  cudaStream_t st = H.st;
+  DevBuf Rab;
+  Rab.alloc(sizeof(zt) * 2 * cs2);
+  zt* Ra = Rab.as<zt>();
+  zt* Rb = Ra + cs2;
+  gather_children_R(H, d, Ra, Rb);
+  H.R[d + 1].release();
+  // (a) retained child blocks, replicated in the group
+  {
+    ZCopy c[4];
+    for (auto& x : c) {
+      x.batch = 1;
+      x.N = n3;
+    }
+    c[0].M = n3;
+    c[0].A = op(Ra, nbc, 0, M.I3a, M.I3a);
+    c[0].C = out(M.R33a, n3, 0);
+    c[1].M = n3;
+    c[1].A = op(Rb, nbc, 0, M.I3b, M.I3b);
+    c[1].C = out(M.R33b, n3, 0);
+    c[2].M = n1;
+    c[2].A = op(Ra, nbc, 0, M.I1a, M.I3a);
+    c[2].C = out(M.R13a, n3, 0);
+    c[3].M = n2;
+    c[3].A = op(Rb, nbc, 0, M.I2b, M.I3b);
+    c[3].C = out(M.R23b, n3, 0);
+    zcopy_multi(c, 4, st);
+  }
+  // (b) this rank's columns J = [j0, j0 + w) of X = [R33b R31a | -R32b] (line 8)
+  DevBuf X;
+  X.alloc(sizeof(zt) * (size_t)n3 * wp);
+  const int nA = std::max(0, std::min(j0 + w, n1) - j0);
+  const int jb0 = std::max(j0, n1), nB = std::max(0, j0 + w - jb0);
+  if (nA > 0) {
+    ZGemm g;
+    g.M = n3;
+    g.N = nA;
+    g.K = n3;
+    g.A = op(M.R33b, n3, 0);
+    g.B = op(Ra, nbc, 0, M.I3a, M.I1a + j0);
+    g.C = out(X.as<zt>(), wp, 0);
+    zgemm(g, st);
+  }
+  if (nB > 0) {
+    ZCopy c;
+    c.M = n3;
+    c.N = nB;
+    c.A = op(Rb, nbc, 0, M.I3b, M.I2b + (jb0 - n1));
+    c.C = out(X.as<zt>() + (jb0 - j0), wp, 0);
+    c.alpha = Z(-1, 0);
+    zcopy(c, st);
+  }
+  // (c) W = I - R33b R33a and W^{-1}, replicated (the latency-critical serial step)
+  form_and_invert_W(H, d, 1, M.R33a, M.R33b, M.Winv);
+  double fl = 8.0 * (2.0 * n3 * n3 * n3 + (double)n3 * n3 * nA);
+  if (w > 0) {
+    // (d) Phi^a_J = W^{-1} X_J ; (e) Phi^b_J = -[R31a | 0]_J - R33a Phi^a_J
+    ZGemm g;
+    g.M = n3;
+    g.N = w;
+    g.K = n3;
+    g.A = op(M.Winv, n3, 0);
+    g.B = op(X.as<zt>(), wp, 0);
+    g.C = out(M.PhiA, wp, 0);
+    zgemm(g, st);
+    ZGemm h;
+    h.M = n3;
+    h.N = w;
+    h.K = n3;
+    h.A = op(M.R33a, n3, 0);
+    h.B = op(M.PhiA, wp, 0);
+    h.Cin = op(Ra, nbc, 0, M.I3a, M.cmapA + j0);
+    h.C = out(M.PhiB, wp, 0);
+    h.alpha = Z(-1, 0);
+    h.beta = Z(-1, 0);
+    zgemm(h, st);
+    fl += 8.0 * 2.0 * n3 * n3 * (double)w;
+  }
+  // (f) columns J of R^tau = diag(R11a, R22b) + [R13a Phi^a ; R23b Phi^b], rows in canonical
+  // order, kept column-distributed ([ntau][wpad]) for the next level's all-gather (line 12)
+  const bool need_R = d > 0 || H.keep_root_R || H.keep_all_R;
+  if (need_R) {
+    H.R[d].alloc(sizeof(zt) * (size_t)nt * wp);
+    if (w > 0) {
+      ZGemm g;
+      g.N = w;
+      g.K = n3;
+      g.beta = Z(1, 0);
+      g.M = n1;
+      g.A = op(M.R13a, n3, 0);
+      g.B = op(M.PhiA, wp, 0);
+      g.Cin = op(Ra, nbc, 0, M.I1a, M.cmapA + j0);
+      g.C = out(H.R[d].as<zt>(), wp, 0, M.pp, nullptr);
+      zgemm(g, st);
+      g.M = n2;
+      g.A = op(M.R23b, n3, 0);
+      g.B = op(M.PhiB, wp, 0);
+      g.Cin = op(Rb, nbc, 0, M.I2b, M.cmapB + j0);
+      g.C = out(H.R[d].as<zt>(), wp, 0, M.pp + n1, nullptr);
+      zgemm(g, st);
+      fl += 8.0 * (double)nt * n3 * w;
+    }
+  }
+  (void)s33;
+  H.flops[0] += fl;
+}
+
+// keep_root_R on a sharded build: all-gather the root's column slices into the whole R^1.
+void gather_root_R(hps_handle& H) {
+  const MergeLevel& M = H.lev[0];
+  const DistLevel& P = H.dl[0];
+  const int nt = M.ntau, wp = P.wpad;
+  DevBuf gat, full;
+  gat.alloc(sizeof(zt) * (size_t)P.gs * nt * wp);
+  H.comm->allgather(P.gs, H.R[0].p, gat.p, sizeof(zt) * (size_t)nt * wp, H.st);
+  full.alloc(sizeof(zt) * (size_t)nt * nt);
+  std::vector<ZCopy> cps;
+  for (int k = 0; k < P.gs; ++k) {
+    const int j0 = k * wp, we = std::min(wp, nt - j0);
+    if (we <= 0) continue;
+    ZCopy c;
+    c.M = nt;
+    c.N = we;
+    c.A = op(gat.as<zt>() + (int64_t)k * nt * wp, wp, 0);
+    c.C = out(full.as<zt>(), nt, 0, nullptr, M.pp + j0);
+    cps.push_back(c);
+  }
+  zcopy_multi(cps.data(), (int)cps.size(), H.st);
+  H.R[0] = std::move(full);
+}
+
+// ---------------------------------------------------------------------------
 // Solve (Algorithm 2).  Internal vectors: [box][n][nrhs] (RHS innermost).
 // ---------------------------------------------------------------------------
+// One upward merge level (Algorithm 2 lines 5-7) for np merges: children's outgoing data ha, hb
+// ([box][nbc][R], batch stride cb), interface corrections t~a, t~b kept in TTa, TTb, parent data
+// h^tau ([np][ntau][R], canonical order) into hout if non-NULL.  Returns the flops.
+double solve_up_level(hps_handle& H, MergeLevel& M, int np, int nrhs, const zt* ha, const zt* hb, int64_t cb,
+                      DevBuf& TTa, DevBuf& TTb, zt* hout) {
+  cudaStream_t st = H.st;
+  const int n1 = M.n1, n2 = M.n2, n3 = M.n3, ntau = M.ntau;
+  const int64_t R = nrhs, s33 = (int64_t)n3 * n3;
+  double fl = 0;
+  DevBuf tmp;
+  tmp.alloc(sizeof(zt) * (size_t)np * n3 * R);
+  TTa.alloc(sizeof(zt) * (size_t)np * n3 * R);
+  TTb.alloc(sizeof(zt) * (size_t)np * n3 * R);
+  ZGemm g;
+  g.batch = np;
+  g.N = nrhs;
+  // tmp = R33b h3a - h3b ; t~a = W^{-1} tmp ; t~b = -h3a - R33a t~a   (Upsilon actions)
+  g.M = n3;
+  g.K = n3;
+  g.A = op(M.R33b, n3, s33);
+  g.B = op(ha, R, cb, M.I3a);
+  g.Cin = op(hb, R, cb, M.I3b);
+  g.beta = Z(-1, 0);
+  g.C = out(tmp.as<zt>(), R, (int64_t)n3 * R);
+  zgemm(g, st);
+  g.A = op(M.Winv, n3, s33);
+  g.B = op(tmp.as<zt>(), R, (int64_t)n3 * R);
+  g.Cin = ZOp();
+  g.beta = Z(0, 0);
+  g.C = out(TTa.as<zt>(), R, (int64_t)n3 * R);
+  zgemm(g, st);
+  if (hout) {  // h^tau part 1 = h1a + R13a t~a needs only t~a: side stream, beside t~b
+    HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(side_solve(H), H.ev_fork, 0));
+    ZGemm g1 = g;
+    g1.M = n1;
+    g1.A = op(M.R13a, n3, (int64_t)n1 * n3);
+    g1.B = op(TTa.as<zt>(), R, (int64_t)n3 * R);
+    g1.Cin = op(ha, R, cb, M.I1a);
+    g1.alpha = Z(1, 0);
+    g1.beta = Z(1, 0);
+    g1.C = out(hout, R, (int64_t)ntau * R, M.pp);
+    zgemm(g1, side_solve(H));
+    HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, side_solve(H)));
+  }
+  g.A = op(M.R33a, n3, s33);
+  g.B = op(TTa.as<zt>(), R, (int64_t)n3 * R);
+  g.Cin = op(ha, R, cb, M.I3a);
+  g.alpha = Z(-1, 0);
+  g.beta = Z(-1, 0);
+  g.C = out(TTb.as<zt>(), R, (int64_t)n3 * R);
+  zgemm(g, st);
+  fl += 8.0 * np * 3.0 * n3 * n3 * R;
+  if (hout) {  // h^tau = [h1a; h2b] + [R13a t~a; R23b t~b]  (eq. flux_part), canonical order
+    g.alpha = Z(1, 0);
+    g.beta = Z(1, 0);
+    g.M = n2;
+    g.A = op(M.R23b, n3, (int64_t)n2 * n3);
+    g.B = op(TTb.as<zt>(), R, (int64_t)n3 * R);
+    g.Cin = op(hb, R, cb, M.I2b);
+    g.C = out(hout, R, (int64_t)ntau * R, M.pp + n1);
+    zgemm(g, st);
+    fl += 8.0 * np * (double)(n1 + n2) * n3 * R;
+    HPS_CUDA_CHECK(cudaStreamWaitEvent(st, H.ev_join, 0));  // part 1 done
+  }
+  return fl;
+}
+
 // Upward pass (Algorithm 2 lines 1-9).  Bottom data: leaf s (ABI [R][nleaf][ni], natural
 // order) for a leaf handle, or the outgoing particular data of the depth-Lb boxes
 // (ABI [2^Lb][R][nb(Lb)]) for a top handle; NULL = zero body load.  Keeps u~, t~ in H.ss.
@@ -1038,6 +1318,7 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
   SolveState& S = H.ss;
   S.reset(Lb);
   S.nrhs = nrhs;
+  S.flops_up = 0;
   S.has_s = bottom != nullptr;
   if (!S.has_s) {
     if (h_root) HPS_CUDA_CHECK(cudaMemsetAsync(h_root, 0, sizeof(zt) * (size_t)H.depth[0].nb * R, st));
@@ -1080,68 +1361,12 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
   }
   for (int d = Lb - 1; d >= 0; --d) {
     MergeLevel& M = H.lev[d];
-    const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, ntau = M.ntau, nbc = M.nbc;
-    const int64_t s33 = (int64_t)n3 * n3, cb = 2 * (int64_t)nbc * R;
+    const int64_t cb = 2 * (int64_t)M.nbc * R;
     const zt* ha = h[d + 1].as<zt>();
-    const zt* hb = ha + (int64_t)nbc * R;
-    DevBuf tmp;
-    tmp.alloc(sizeof(zt) * (size_t)np * n3 * R);
-    S.TTa[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
-    S.TTb[d].alloc(sizeof(zt) * (size_t)np * n3 * R);
-    ZGemm g;
-    g.batch = np;
-    g.N = nrhs;
-    // tmp = R33b h3a - h3b ; t~a = W^{-1} tmp ; t~b = -h3a - R33a t~a   (Upsilon actions)
-    g.M = n3;
-    g.K = n3;
-    g.A = op(M.R33b, n3, s33);
-    g.B = op(ha, R, cb, M.I3a);
-    g.Cin = op(hb, R, cb, M.I3b);
-    g.beta = Z(-1, 0);
-    g.C = out(tmp.as<zt>(), R, (int64_t)n3 * R);
-    zgemm(g, st);
-    g.A = op(M.Winv, n3, s33);
-    g.B = op(tmp.as<zt>(), R, (int64_t)n3 * R);
-    g.Cin = ZOp();
-    g.beta = Z(0, 0);
-    g.C = out(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
-    zgemm(g, st);
     const bool need_h = d > 0 || h_root;
-    if (need_h) {  // h^tau part 1 = h1a + R13a t~a needs only t~a: side stream, beside t~b
-      h[d].alloc(sizeof(zt) * (size_t)np * ntau * R);
-      HPS_CUDA_CHECK(cudaEventRecord(H.ev_fork, st));
-      HPS_CUDA_CHECK(cudaStreamWaitEvent(side_solve(H), H.ev_fork, 0));
-      ZGemm g1 = g;
-      g1.M = n1;
-      g1.A = op(M.R13a, n3, (int64_t)n1 * n3);
-      g1.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
-      g1.Cin = op(ha, R, cb, M.I1a);
-      g1.alpha = Z(1, 0);
-      g1.beta = Z(1, 0);
-      g1.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp);
-      zgemm(g1, side_solve(H));
-      HPS_CUDA_CHECK(cudaEventRecord(H.ev_join, side_solve(H)));
-    }
-    g.A = op(M.R33a, n3, s33);
-    g.B = op(S.TTa[d].as<zt>(), R, (int64_t)n3 * R);
-    g.Cin = op(ha, R, cb, M.I3a);
-    g.alpha = Z(-1, 0);
-    g.beta = Z(-1, 0);
-    g.C = out(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
-    zgemm(g, st);
-    fl += 8.0 * np * 3.0 * n3 * n3 * R;
-    if (need_h) {  // h^tau = [h1a; h2b] + [R13a t~a; R23b t~b]  (eq. flux_part), canonical order
-      g.alpha = Z(1, 0);
-      g.beta = Z(1, 0);
-      g.M = n2;
-      g.A = op(M.R23b, n3, (int64_t)n2 * n3);
-      g.B = op(S.TTb[d].as<zt>(), R, (int64_t)n3 * R);
-      g.Cin = op(hb, R, cb, M.I2b);
-      g.C = out(h[d].as<zt>(), R, (int64_t)ntau * R, M.pp + n1);
-      zgemm(g, st);
-      fl += 8.0 * np * (double)(n1 + n2) * n3 * R;
-      HPS_CUDA_CHECK(cudaStreamWaitEvent(st, H.ev_join, 0));  // part 1 done
-    }
+    if (need_h) h[d].alloc(sizeof(zt) * (size_t)M.nparent * M.ntau * R);
+    fl += solve_up_level(H, M, M.nparent, nrhs, ha, ha + (int64_t)M.nbc * R, cb, S.TTa[d], S.TTb[d],
+                         need_h ? h[d].as<zt>() : nullptr);
     h[d + 1].release();
   }
   if (h_root) {
@@ -1235,6 +1460,101 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
   }
   S.flops_down = fl;
   S.reset(Lb);
+}
+
+// Sharded top levels of the solve.  Upward: each level all-gathers the group's
+// box data h (tiny) and every rank of the group forms t~a, t~b (replicated).  Downward: each rank
+// applies its column slice of Phi^a, Phi^b; the group all-gathers the partial products and sums
+// them in rank order (so the result does not depend on the transport).
+// h_mine: ABI [R][nb(D)] outgoing data of this rank's subtree root (NULL: s = 0, no upward pass).
+void solve_up_dist(hps_handle& T, int nrhs, const zt* h_mine) {
+  cudaStream_t st = T.st;
+  SolveState& S = T.ss;
+  S.reset(T.D);
+  S.nrhs = nrhs;
+  S.flops_up = 0;
+  S.has_s = h_mine != nullptr;
+  if (!S.has_s) return;
+  const int64_t R = nrhs;
+  const int nbD = T.depth[T.D].nb;
+  DevBuf hm;
+  hm.alloc(sizeof(zt) * (size_t)nbD * R);
+  launch_rhs_in(h_mine, hm.as<zt>(), T.ident.as<int>(), 1, nbD, nrhs, nbD, nbD, st);
+  double fl = 0;
+  for (int d = T.D - 1; d >= 0; --d) {
+    MergeLevel& M = T.lev[d];
+    const DistLevel& P = T.dl[d];
+    const int64_t blk = (int64_t)M.nbc * R;
+    DevBuf gat;
+    gat.alloc(sizeof(zt) * (size_t)P.gs * blk);
+    T.comm->allgather(P.gs, hm.p, gat.p, sizeof(zt) * blk, st);
+    const zt* ha = gat.as<zt>();
+    const zt* hb = ha + (int64_t)(P.gs / 2) * blk;
+    DevBuf hn;
+    if (d > 0) hn.alloc(sizeof(zt) * (size_t)M.ntau * R);
+    fl += solve_up_level(T, M, 1, nrhs, ha, hb, 0, S.TTa[d], S.TTb[d], d > 0 ? hn.as<zt>() : nullptr);
+    hm = std::move(hn);
+  }
+  S.flops_up = fl;
+}
+
+// t_root: ABI [R][nb(0)]; t_mine (out): ABI [R][nb(D)] incoming data of this rank's subtree root.
+void solve_down_dist(hps_handle& T, int nrhs, const zt* t_root, zt* t_mine) {
+  cudaStream_t st = T.st;
+  SolveState& S = T.ss;
+  const bool has_s = S.has_s && S.nrhs == nrhs;
+  const int64_t R = nrhs;
+  double fl = 0;
+  DevBuf tc;
+  const int nb0 = T.depth[0].nb;
+  tc.alloc(sizeof(zt) * (size_t)nb0 * R);
+  launch_rhs_in(t_root, tc.as<zt>(), T.ident.as<int>(), 1, nb0, nrhs, nb0, nb0, st);
+  for (int d = 0; d < T.D; ++d) {
+    MergeLevel& M = T.lev[d];
+    const DistLevel& P = T.dl[d];
+    const int n1 = M.n1, n3 = M.n3, nbc = M.nbc;
+    const int64_t pr = (int64_t)n3 * R;
+    DevBuf part, gat, t3, tn;
+    part.alloc(sizeof(zt) * 2 * (size_t)pr);
+    if (P.w > 0) {
+      ZGemm g;  // partial t3 = Phi_J t^tau(pp[J])
+      g.M = n3;
+      g.N = nrhs;
+      g.K = P.w;
+      g.A = op(M.PhiA, P.wpad, 0);
+      g.B = op(tc.as<zt>(), R, 0, M.pp + P.j0);
+      g.C = out(part.as<zt>(), R, 0);
+      zgemm(g, st);
+      g.A = op(M.PhiB, P.wpad, 0);
+      g.C = out(part.as<zt>() + pr, R, 0);
+      zgemm(g, st);
+      fl += 8.0 * 2.0 * n3 * (double)P.w * R;
+    } else {
+      HPS_CUDA_CHECK(cudaMemsetAsync(part.p, 0, sizeof(zt) * 2 * (size_t)pr, st));
+    }
+    gat.alloc(sizeof(zt) * 2 * (size_t)pr * P.gs);
+    T.comm->allgather(P.gs, part.p, gat.p, sizeof(zt) * 2 * (size_t)pr, st);
+    // t3 of this rank's side = t~ + sum of the group's partials, in rank order
+    t3.alloc(sizeof(zt) * (size_t)pr);
+    const zt* base = has_s ? (P.side ? S.TTb[d] : S.TTa[d]).as<zt>() : nullptr;
+    launch_zsum_slots(t3.as<zt>(), base, gat.as<zt>() + (P.side ? pr : 0), P.gs, 2 * pr, pr, st);
+    // this rank's child: t on I1 (alpha) / I2 (beta) from t^tau, t3 on I3
+    tn.alloc(sizeof(zt) * (size_t)nbc * R);
+    ZCopy c[2];
+    for (auto& x : c) x.N = nrhs;
+    c[0].M = P.side ? M.n2 : n1;
+    c[0].A = op(tc.as<zt>(), R, 0, P.side ? M.pp + n1 : M.pp);
+    c[0].C = out(tn.as<zt>(), R, 0, P.side ? M.I2b : M.I1a);
+    c[1].M = n3;
+    c[1].A = op(t3.as<zt>(), R, 0);
+    c[1].C = out(tn.as<zt>(), R, 0, P.side ? M.I3b : M.I3a);
+    zcopy_multi(c, 2, st);
+    tc = std::move(tn);
+  }
+  const int nbD = T.depth[T.D].nb;
+  launch_rhs_out(tc.as<zt>(), t_mine, T.ident.as<int>(), 1, nbD, nrhs, nbD, nbD, st);
+  S.flops_down = fl;
+  S.reset(T.D);
 }
 
 int fail(const HpsError& e) {
@@ -1438,7 +1758,12 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   if (opt && opt->device >= 0) HPS_CUDA_CHECK(cudaSetDevice(opt->device));
   HPS_CUDA_CHECK(cudaGetDevice(&H.dev));
   H.prof.dev = H.dev;
-  HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
+  if (opt && opt->stream) {
+    H.st = static_cast<cudaStream_t>(opt->stream);
+    H.own_stream = false;
+  } else {
+    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&H.st, cudaStreamNonBlocking));
+  }
   retain_pool(H.dev);
   g_alloc_stream = H.st;
   for (auto& e : H.ev) HPS_CUDA_CHECK(cudaEventCreate(&e));
@@ -1468,9 +1793,28 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   }
 }
 
+// Column slices of the sharded top levels for this rank (H.G, H.rank; H.depth planned).
+void plan_dist_levels(hps_handle& H) {
+  H.dl.assign(H.D, DistLevel());
+  const int q = H.q;
+  for (int d = 0; d < H.D; ++d) {
+    DistLevel& P = H.dl[d];
+    const Depth& C = H.depth[d + 1];
+    const bool vertical = H.depth[d].a >= H.depth[d].b;
+    const int n3 = vertical ? C.b * q : C.a * q, ntau = 2 * (C.nb - n3);
+    P.gs = H.G >> d;
+    P.grank = H.rank % P.gs;
+    P.side = P.grank >= P.gs / 2 ? 1 : 0;
+    P.wpad = (ntau + P.gs - 1) / P.gs;
+    P.j0 = P.grank * P.wpad;
+    P.w = std::max(0, std::min(P.wpad, ntau - P.j0));
+  }
+}
+
 void plan_all(hps_handle& H, int Lb) {
   plan_tree(H);
   H.Lb = Lb;
+  if (H.dist_top) plan_dist_levels(H);
   upload(H.leaf_nat, H.leaf_nat_h, H.st);
   upload(H.nat_to_heap, H.nat_to_heap_h, H.st);
   std::vector<int> id(std::max(1, 1 << Lb));
@@ -1524,9 +1868,11 @@ struct DevOut {
   }
 };
 
-void record_solve_times(hps_handle& H, bool up, bool down) {
-  HPS_CUDA_CHECK(cudaEventRecord(H.ev[5], H.st));
+// Solve timings (events ev[3] .. ev[5] on the handle's stream) once the work has finished.
+// solve_kind: 1 upward only, 2 downward only, 3 both.
+void finish_pending(hps_handle& H) {
   HPS_CUDA_CHECK(cudaEventSynchronize(H.ev[5]));
+  const bool up = H.solve_kind & 1, down = H.solve_kind & 2;
   float a = 0, b = 0;
   if (up && down) {
     cudaEventElapsedTime(&a, H.ev[3], H.ev[4]);
@@ -1540,6 +1886,14 @@ void record_solve_times(hps_handle& H, bool up, bool down) {
   H.times[4] = a;
   H.times[5] = b;
   H.flops[1] = (up ? H.ss.flops_up : 0) + (down ? H.ss.flops_down : 0);
+  H.pending = false;
+}
+
+void record_solve_times(hps_handle& H, bool up, bool down) {
+  HPS_CUDA_CHECK(cudaEventRecord(H.ev[5], H.st));
+  H.solve_kind = (up ? 1 : 0) | (down ? 2 : 0);
+  H.pending = true;
+  finish_pending(H);
 }
 
 }  // namespace
@@ -1564,9 +1918,23 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
   }
   std::unique_ptr<hps_handle> H(new hps_handle());
   try {
-    init_handle(*H, g, p, q, kappa, eta, opt);
+    bool owned = false;
+    HpsComm* comm = opt ? hps_comm_from_opts(opt->comm, opt->nccl_comm, opt->n_gpus, owned) : nullptr;
+    H->comm = comm;
+    H->comm_owned = owned;
+    hps_grid gl = *g;  // this rank's rectangle
+    if (comm) {
+      H->G = comm->size;
+      H->rank = comm->rank;
+      while ((1 << H->D) < H->G) ++H->D;
+      int32_t i0, j0;
+      if (hps_subtree_grid(g, H->D, H->rank, &gl, &i0, &j0) != HPS_OK)
+        throw HpsError{HPS_EINVAL, "hps_build: the tree has fewer than log2(n_gpus) levels"};
+    }
+    init_handle(*H, &gl, p, q, kappa, eta, opt);
     LaunchScope ls(&H->launches[0], &H->prof);
     H->flops[0] = 0;
+    if (comm) H->keep_root_R = true;  // the subtree root R feeds the sharded top levels
     plan_tree(*H);
     plan_all(*H, H->L);  // (plan_tree runs again inside; cheap)
     H->has_leaves = true;
@@ -1576,7 +1944,30 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     build_leaves(*H, c_dev, opt ? opt->leaf_chunk : 0);
     HPS_CUDA_CHECK(cudaEventRecord(H->ev[1], H->st));
     for (int d = H->L - 1; d >= 0; --d) build_merge(*H, d);
+    if (comm) {
+      // the global tree above depth D: same stream, this rank's merge per level, column slices
+      std::unique_ptr<hps_handle> T(new hps_handle());
+      T->comm = comm;
+      T->G = H->G;
+      T->rank = H->rank;
+      T->D = H->D;
+      T->dist_top = true;
+      hps_opts to = opt ? *opt : hps_opts{};
+      to.stream = H->st;
+      to.keep_all_R = 0;
+      init_handle(*T, g, p, q, kappa, eta, &to);
+      T->keep_root_R = opt ? opt->keep_root_R != 0 : true;
+      T->prof.timing = 0;  // the user handle's profiler (g_prof) accounts every launch
+      plan_all(*T, T->D);
+      T->has_leaves = false;
+      T->R[T->D] = std::move(H->R[0]);  // this rank's subtree root R
+      for (int d = T->D - 1; d >= 0; --d) build_merge_dist(*T, d);
+      if (T->keep_root_R) gather_root_R(*T);
+      H->flops[0] += T->flops[0];
+      H->top = std::move(T);
+    }
     finish_build_timing(*H);
+    if (H->top) check_info(*H->top);
   } catch (const HpsError& e) {
     return fail(e);
   } catch (const std::exception& e) {
@@ -1633,28 +2024,64 @@ int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps
   if (nrhs == 0) return HPS_OK;
   try {
     HPS_CUDA_CHECK(cudaSetDevice(h->dev));
+    if (h->pending) finish_pending(*h);
     g_alloc_stream = h->st;
     LaunchScope ls(&h->launches[1], &h->prof);
     DevBuf sd, td;
     const zt* s_dev = dev_in(s, sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni, sd, h->st);
-    const zt* t_dev = dev_in(t, sizeof(zt) * (size_t)nrhs * h->depth[0].nb, td, h->st);
+    hps_handle* T = h->top.get();
+    const int nb_root = T ? T->depth[0].nb : h->depth[0].nb;
+    const zt* t_dev = dev_in(t, sizeof(zt) * (size_t)nrhs * nb_root, td, h->st);
     DevBuf tc;
     if (h->gl) {
-      t_gl_to_cheb(*h, nrhs, t_dev, tc);
+      t_gl_to_cheb(T ? *T : *h, nrhs, t_dev, tc);
       t_dev = tc.as<zt>();
     }
     DevOut uo(u, sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt, h->st);
     HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
-    solve_up_impl(*h, nrhs, s_dev, nullptr);
-    HPS_CUDA_CHECK(cudaEventRecord(h->ev[4], h->st));
-    solve_down_impl(*h, nrhs, t_dev, uo.dev);
-    record_solve_times(*h, true, true);
+    if (!T) {
+      solve_up_impl(*h, nrhs, s_dev, nullptr);
+      HPS_CUDA_CHECK(cudaEventRecord(h->ev[4], h->st));
+      solve_down_impl(*h, nrhs, t_dev, uo.dev);
+    } else {  // sharded: subtree up, top levels (collective), subtree down
+      const size_t nbs = (size_t)h->depth[0].nb * nrhs;
+      DevBuf hsub, tsub;
+      if (s_dev) hsub.alloc(sizeof(zt) * nbs);
+      solve_up_impl(*h, nrhs, s_dev, s_dev ? hsub.as<zt>() : nullptr);
+      solve_up_dist(*T, nrhs, s_dev ? hsub.as<zt>() : nullptr);
+      HPS_CUDA_CHECK(cudaEventRecord(h->ev[4], h->st));
+      tsub.alloc(sizeof(zt) * nbs);
+      solve_down_dist(*T, nrhs, t_dev, tsub.as<zt>());
+      solve_down_impl(*h, nrhs, tsub.as<zt>(), uo.dev);
+      h->ss.flops_up += T->ss.flops_up;
+      h->ss.flops_down += T->ss.flops_down;
+    }
+    HPS_CUDA_CHECK(cudaEventRecord(h->ev[5], h->st));
     uo.finish(h->st);
-    HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
+    h->pending = true;
+    h->solve_kind = 3;
+    const bool host_io = (s && s_dev != reinterpret_cast<const zt*>(s)) || t_dev != reinterpret_cast<const zt*>(t) ||
+                         uo.dev != reinterpret_cast<zt*>(u);
+    if (h->own_stream || host_io || h->prof.timing) finish_pending(*h);  // else: stream-ordered, hps_sync waits
   } catch (const HpsError& e) {
     return fail(e);
   } catch (const std::exception& e) {
     return fail(HpsError{HPS_ECUDA, e.what()});
+  }
+  return HPS_OK;
+}
+
+int hps_sync(hps_handle* h) {
+  if (!h) {
+    hps_set_error("hps_sync: NULL handle");
+    return HPS_EINVAL;
+  }
+  try {
+    HPS_CUDA_CHECK(cudaSetDevice(h->dev));
+    if (h->pending) finish_pending(*h);
+    HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
+  } catch (const HpsError& e) {
+    return fail(e);
   }
   return HPS_OK;
 }
@@ -1743,6 +2170,36 @@ int hps_solve_top(hps_handle* h, int nrhs, const hps_c128* h_sub, const hps_c128
   return HPS_OK;
 }
 
+int hps_dist_plan(const hps_grid* g, int p, int G, int rank, int32_t* info, int maxlev) {
+  if (!g || p < 4 || G < 1 || (G & (G - 1)) || rank < 0 || rank >= G || !info || !is_pow2(g->nx) ||
+      !is_pow2(g->ny)) {
+    hps_set_error("hps_dist_plan: invalid argument");
+    return HPS_EINVAL;
+  }
+  hps_handle H;  // host-side planning only (no stream, no device memory)
+  H.g = *g;
+  H.p = p;
+  H.q = p - 2;
+  H.G = G;
+  H.rank = rank;
+  while ((1 << H.D) < G) ++H.D;
+  plan_tree(H);
+  if (H.D > H.L || maxlev < H.D) {
+    hps_set_error("hps_dist_plan: tree too shallow for G ranks, or maxlev too small");
+    return HPS_EINVAL;
+  }
+  plan_dist_levels(H);
+  for (int d = 0; d < H.D; ++d) {
+    const DistLevel& P = H.dl[d];
+    const Depth& C = H.depth[d + 1];
+    const bool vertical = H.depth[d].a >= H.depth[d].b;
+    const int n3 = vertical ? C.b * H.q : C.a * H.q, n1 = C.nb - n3;
+    const int32_t row[8] = {P.gs, P.grank, P.side, n3, n1, 2 * n1, P.j0, P.w};
+    std::memcpy(info + 8 * d, row, sizeof(row));
+  }
+  return H.D;
+}
+
 int hps_subtree_grid(const hps_grid* g, int depth, int64_t index, hps_grid* sub, int32_t* leaf_i0, int32_t* leaf_j0) {
   if (!g || !sub || depth < 0 || index < 0 || index >= ((int64_t)1 << depth) || !is_pow2(g->nx) || !is_pow2(g->ny)) {
     hps_set_error("hps_subtree_grid: invalid argument");
@@ -1777,18 +2234,32 @@ int hps_subtree_grid(const hps_grid* g, int depth, int64_t index, hps_grid* sub,
 
 int64_t hps_box_nb(const hps_handle* h, int64_t box) {
   if (!h || box < 1) return -1;
+  if (h->top) {  // sharded: global box ids
+    if (box == 1) return h->top->depth[0].nb;
+    h = h->top.get();
+  }
   int d = 0;
   while (((int64_t)1 << (d + 1)) <= box) ++d;
   if (d > h->L) return -1;
   return h->depth[d].nb;
 }
 
-int64_t hps_num_boxes(const hps_handle* h) { return h ? ((int64_t)2 << h->L) - 1 : -1; }
+int64_t hps_num_boxes(const hps_handle* h) {
+  if (h && h->top) return ((int64_t)2 << (h->top->L)) - 1;
+  return h ? ((int64_t)2 << h->L) - 1 : -1;
+}
 
 int hps_export_R(const hps_handle* h, int64_t box, hps_c128* outR) {
   if (!h || !outR || box < 1) {
     hps_set_error("hps_export_R: invalid argument");
     return HPS_EINVAL;
+  }
+  if (h->top) {  // sharded build: only the (gathered) root operator is exportable
+    if (box != 1) {
+      hps_set_error("hps_export_R: a sharded handle exports the root R only");
+      return HPS_ENOTKEPT;
+    }
+    h = h->top.get();
   }
   int d = 0;
   while (((int64_t)1 << (d + 1)) <= box) ++d;
@@ -1831,6 +2302,14 @@ int hps_export_leaf(const hps_handle* h, int64_t leaf, hps_c128* psi, hps_c128* 
 
 double hps_last_time_ms(const hps_handle* h, int which) {
   if (!h || which < 0 || which > 5) return -1;
+  if (h->pending && which >= 3) {
+    try {
+      finish_pending(const_cast<hps_handle&>(*h));
+    } catch (const HpsError& e) {
+      fail(e);
+      return -1;
+    }
+  }
   return h->times[which];
 }
 
@@ -1841,6 +2320,14 @@ int64_t hps_last_launches(const hps_handle* h, int which) {
 
 double hps_last_flops(const hps_handle* h, int which) {
   if (!h || which < 0 || which > 1) return -1;
+  if (h->pending && which == 1) {
+    try {
+      finish_pending(const_cast<hps_handle&>(*h));
+    } catch (const HpsError& e) {
+      fail(e);
+      return -1;
+    }
+  }
   return h->flops[which];
 }
 

@@ -14,3 +14,7 @@ void launch_leaf_schur_assemble(zt* S, int64_t sstride, int leaf0, int nchunk, c
                                 const zt* consts, double kappa2, cudaStream_t st);
 void launch_leaf_schur_finish(zt* store, int64_t sstride, int leaf0, int nchunk, int p, const zt* consts,
                               cudaStream_t st);
+// out[i] = (base ? base[i] : 0) + sum_{k < nslot} slots[k * slot_stride + i], k in increasing order
+// (the deterministic reduction of the sharded solve), i < n.
+void launch_zsum_slots(zt* out, const zt* base, const zt* slots, int nslot, int64_t slot_stride, int64_t n,
+                       cudaStream_t st);

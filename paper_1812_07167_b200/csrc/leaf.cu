@@ -76,6 +76,19 @@ __global__ void leaf_R_kernel(const zt* __restrict__ store, int64_t sstride, zt*
   }
 }
 
+__global__ void zsum_slots_kernel(zt* out, const zt* base, const zt* slots, int nslot, int64_t slot_stride,
+                                  int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    zt a = base ? base[i] : make_double2(0.0, 0.0);
+    for (int k = 0; k < nslot; ++k) {
+      const zt v = slots[k * slot_stride + i];
+      a.x += v.x;
+      a.y += v.y;
+    }
+    out[i] = a;
+  }
+}
+
 // external [r * sr + map[l] * sb + i] -> internal [l][n][nrhs]   (ABI: sr = nleaf n, sb = n)
 __global__ void rhs_in_kernel(const zt* __restrict__ src, zt* __restrict__ dst, const int* __restrict__ map,
                               int nbox, int n, int nrhs, int64_t sr, int64_t sb) {
@@ -334,6 +347,15 @@ void launch_rhs_in(const zt* src, zt* dst, const int* map, int nbox, int n, int 
         src, dst, map, nbox, n, nrhs, sr, sb);
   else
     rhs_in_kernel<<<grid_for((int64_t)nbox * n * nrhs), 256, 0, st>>>(src, dst, map, nbox, n, nrhs, sr, sb);
+  HPS_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_zsum_slots(zt* out, const zt* base, const zt* slots, int nslot, int64_t slot_stride, int64_t n,
+                       cudaStream_t st) {
+  if (n <= 0) return;
+  ProfScope ps(K_LAYOUT, 0.0, 16.0 * (double)n * (nslot + 1 + (base ? 1 : 0)), st);
+  zsum_slots_kernel<<<grid_for(n), 256, 0, st>>>(out, base, slots, nslot, slot_stride, n);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

@@ -34,14 +34,18 @@ class hps_c128(C.Structure):
 class hps_opts(C.Structure):
     _fields_ = [("keep_root_R", C.c_int32), ("keep_all_R", C.c_int32), ("device", C.c_int32),
                 ("leaf_chunk", C.c_int32), ("profile", C.c_int32), ("leaf_mode", C.c_int32),
-                ("boundary_basis", C.c_int32)]
+                ("boundary_basis", C.c_int32), ("n_gpus", C.c_int32), ("nccl_comm", C.c_void_p),
+                ("stream", C.c_void_p), ("comm", C.c_void_p)]
 
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_last_time_ms", "hps_last_launches",
            "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free", "hps_release_cache",
-           "hps_set_cache_limit", "hps_cache_bytes", "hps_debug_set", "hps_debug_get", "hps_last_error"]
+           "hps_set_cache_limit", "hps_cache_bytes", "hps_debug_set", "hps_debug_get", "hps_last_error",
+           "hps_sync", "hps_nccl_unique_id", "hps_nccl_comm_init", "hps_nccl_comm_destroy", "hps_comm_wrap_nccl",
+           "hps_vcomm_create", "hps_vcomm_rank", "hps_vcomm_destroy", "hps_comm_info", "hps_comm_selftest",
+           "hps_comm_free", "hps_dist_plan"]
 
 KCLASSES = ["zgemm_dmma", "zgj_panel", "zgj_small", "zgj_aux", "leaf_assemble", "layout", "zgj_fused", "leaf_gj", "zgemv"]
 
@@ -95,6 +99,18 @@ def lib():
         L.hps_solve_top.argtypes = [vp, i32, dp, dp, dp]
         L.hps_free.argtypes = [vp]
         L.hps_set_cache_limit.argtypes = [i64]
+        L.hps_sync.argtypes = [vp]
+        L.hps_nccl_unique_id.argtypes = [C.c_char_p]
+        L.hps_nccl_comm_init.argtypes = [i32, i32, C.c_char_p, C.POINTER(vp)]
+        L.hps_nccl_comm_destroy.argtypes = [vp]
+        L.hps_comm_wrap_nccl.argtypes = [vp, C.POINTER(vp)]
+        L.hps_vcomm_create.argtypes = [i32, C.POINTER(vp)]
+        L.hps_vcomm_rank.argtypes = [vp, i32, C.POINTER(vp)]
+        L.hps_vcomm_destroy.argtypes = [vp]
+        L.hps_comm_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.hps_comm_selftest.argtypes = [vp, i32]
+        L.hps_comm_free.argtypes = [vp]
+        L.hps_dist_plan.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp, i32]
         L.hps_cache_bytes.restype = i64
         L.hps_debug_set.argtypes = [C.c_char_p, i32]
         L.hps_debug_get.argtypes = [C.c_char_p, C.POINTER(C.c_int)]
@@ -279,18 +295,97 @@ def zinv_timed(A, mode=0, reps=3):
     return out, ms.value
 
 
+def dist_plan(g, p, G, rank):
+    """Host-only plan of the sharded top levels (hps_dist_plan): one dict per top depth."""
+    info = np.zeros(8 * 32, np.int32)
+    k = lib().hps_dist_plan(C.byref(g), p, G, rank, info.ctypes.data, 32)
+    if k < 0:
+        _check(k)
+    keys = ("gs", "grank", "side", "n3", "n1", "ntau", "j0", "w")
+    return [dict(zip(keys, (int(v) for v in info[8 * d:8 * d + 8]))) for d in range(k)]
+
+
+class Comm:
+    """A library communicator (hps_comm): NCCL (one process per GPU) or a virtual rank."""
+
+    def __init__(self, handle, owner=None, nccl_comm=None):
+        self.h = handle
+        self._owner = owner          # keeps a virtual group alive
+        self._nccl = nccl_comm       # raw ncclComm_t we created (destroyed with us)
+
+    @staticmethod
+    def nccl_unique_id():
+        buf = C.create_string_buffer(128)
+        _check(lib().hps_nccl_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, nranks, rank, uid):
+        """ncclCommInitRank on the current device + the library wrapper (collective)."""
+        raw = C.c_void_p()
+        _check(lib().hps_nccl_comm_init(nranks, rank, C.c_char_p(uid), C.byref(raw)))
+        h = C.c_void_p()
+        _check(lib().hps_comm_wrap_nccl(raw, C.byref(h)))
+        return cls(h, nccl_comm=raw)
+
+    def info(self):
+        r, n = C.c_int(), C.c_int()
+        _check(lib().hps_comm_info(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+    def selftest(self, gs):
+        _check(lib().hps_comm_selftest(self.h, gs))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hps_comm_free(self.h)
+            self.h = None
+        if getattr(self, "_nccl", None):
+            lib().hps_nccl_comm_destroy(self._nccl)
+            self._nccl = None
+
+
+class VirtualGroup:
+    """G virtual ranks in one process (host threads sharing one GPU): hps_vcomm_create."""
+
+    def __init__(self, G):
+        self.g = C.c_void_p()
+        _check(lib().hps_vcomm_create(G, C.byref(self.g)))
+        self.G = G
+
+    def comm(self, rank):
+        h = C.c_void_p()
+        _check(lib().hps_vcomm_rank(self.g, rank, C.byref(h)))
+        return Comm(h, owner=self)
+
+    def close(self):
+        if getattr(self, "g", None):
+            lib().hps_vcomm_destroy(self.g)
+            self.g = None
+
+
 class Solver:
-    """hps_build on construction; solve() is hps_solve."""
+    """hps_build on construction; solve() is hps_solve.  With comm (a Comm of G ranks) the build
+    and solve are sharded by subtree (c, s, u: this rank's rectangle; t: the whole root boundary)."""
 
     def __init__(self, g, p, kappa, eta, c, keep_root_R=True, keep_all_R=False, device=-1, leaf_chunk=0,
-                 profile=False, leaf_mode=0, boundary_basis=0):
+                 profile=False, leaf_mode=0, boundary_basis=0, comm=None, stream=None):
         self.g, self.p = g, p
-        self.nleaf = g.nx * g.ny
+        self.comm = comm
+        G, rank = 1, 0
+        if comm is not None:
+            rank, G = comm.info()
+        self.G, self.rank = G, rank
+        self.sub = subtree_grid(g, int(round(np.log2(G))), rank)[0] if G > 1 else g
+        self.nleaf = self.sub.nx * self.sub.ny
         self.q, self.nt, self.ni = p - 2, p * p - 4, (p - 2) ** 2
         self.nb_root = 2 * (g.nx + g.ny) * (p - 2)
         mask = -1 if profile is True else int(profile)
+        st = None
+        if stream is not None:
+            st = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         opts = hps_opts(int(keep_root_R), int(keep_all_R), int(device), int(leaf_chunk), mask, int(leaf_mode),
-                        int(boundary_basis))
+                        int(boundary_basis), int(G), None, st, comm.h if comm is not None else None)
         eta = complex(eta)
         h = C.c_void_p()
         cp = _ptr(c, self.nleaf * p * p, "c_samples")
@@ -311,6 +406,10 @@ class Solver:
         _check(lib().hps_solve(self.h, nrhs, _ptr(s, nrhs * self.nleaf * self.ni, "s"),
                                _ptr(t, nrhs * self.nb_root, "t"), _ptr(u, nrhs * self.nleaf * self.nt, "u")))
         return u
+
+    def sync(self):
+        """Wait for a stream-ordered solve (hps_sync)."""
+        _check(lib().hps_sync(self.h))
 
     def solve_up(self, s, nrhs, h_root=None):
         """Upward pass only; returns the root's outgoing particular data [nrhs][nb_root]."""

@@ -1,9 +1,9 @@
-"""Multi-rank subtree sharding on CPU (no GPU): the partition geometry, and the SPMD driver
-(paper_1812_07167_b200.dist) over real torch.distributed gloo ranks (world size 2 and 4) and
-over virtual thread ranks.  The numerics of the build are the ORACLE's here (an oracle-backed
-backend, test-only): subtree roots built by oracle.Oracle on each rank's rectangle, gathered,
-merged upward with oracle.merge — and compared with the single-process oracle root R.  The
-solve plumbing (gather order, own-slice selection) is checked with a tagging backend."""
+"""Multi-rank subtree sharding on CPU (no GPU): the partition geometry, the host plan of the
+group split of the top levels (hps_dist_plan), and the communicator plumbing of
+paper_1812_07167_b200.dist over real torch.distributed gloo ranks (world size 2 and 4): the NCCL
+unique id made by the library on rank 0 reaches every rank, and the per-rank plans gathered over
+gloo tile every top-level merge's columns exactly once.  The sharded numerics themselves run in
+libhps on the GPU (tests/test_gpu_parity.py: virtual ranks vs the single-GPU build)."""
 import os
 import socket
 
@@ -29,82 +29,71 @@ def test_subtree_grid_matches_oracle_tree(nx, ny):
         assert np.all(cover == 1)
 
 
-class OracleBackend:
-    """Test-only backend: oracle numerics for the build; tagging functions for the solve."""
-
-    def __init__(self, g):
-        self.g = g
-
-    def build_subtree(self, g_sub, p, kappa, eta, c_local):
-        return oracle.Oracle(g_sub.x0, g_sub.x1, g_sub.y0, g_sub.y1, g_sub.nx, g_sub.ny, p, kappa, eta, c_local)
-
-    def root_R(self, sub, like):
-        return sub.R(1)
-
-    def build_top(self, g, p, kappa, eta, depth, R_all):
-        Rs = {(1 << depth) + r: R_all[r] for r in range(1 << depth)}
-        for d in range(depth - 1, -1, -1):
-            for m in range(1 << d):
-                box = (1 << d) + m
-                ci0, ci1, cj0, cj1, _ = oracle.box_rect(g.nx, g.ny, 2 * box)
-                vertical = oracle.box_rect(g.nx, g.ny, box)[4]
-                Rs[box] = oracle.merge(p, ci1 - ci0, cj1 - cj0, vertical, Rs[2 * box], Rs[2 * box + 1])["Rtau"]
-        return {"R": Rs[1]}
-
-    def solve_up(self, sub, s_local, nrhs, like):
-        return np.ones((nrhs, sub.nb(1)), complex) * s_local.sum()
-
-    def solve_top(self, top, h_all, t_root):
-        nb = h_all.shape[-1]
-        return 2 * h_all + t_root[None, :, :nb]
-
-    def solve_down(self, sub, t_sub):
-        return t_sub
-
-
-def problem(nx=4, ny=4, p=6):
-    g = hps.grid(0.0, 1.0, 0.0, ny / nx, nx, ny)
-    X, Y = oracle.leaf_nodes(0.0, 1.0, 0.0, ny / nx, nx, ny, p)
-    c = (1 + 0.3 * np.exp(-((X - 0.3) ** 2 + (Y - 0.4) ** 2) / 0.05)).astype(complex)
-    rng = np.random.default_rng(nx * ny)
-    s = rng.standard_normal((2, nx * ny, (p - 2) ** 2)) + 0j
-    t = rng.standard_normal((2, 2 * (nx + ny) * (p - 2))) + 0j
-    return g, p, 7.0, 7.0 + 0.5j, c, s, t
+def check_plans(g, p, plans):
+    """plans[r] = hps.dist_plan(g, p, G, r).  Every top-level merge (depth d, box m) is handled by
+    the aligned group of gs = G >> d ranks above it; their column slices tile [0, ntau) exactly;
+    the first half of the group sits under the alpha child; n3 / ntau are the oracle tree's."""
+    G = len(plans)
+    D = len(plans[0])
+    assert 1 << D == G
+    for d in range(D):
+        gs = G >> d
+        for m in range(1 << d):
+            box = (1 << d) + m
+            ci0, ci1, cj0, cj1, _ = oracle.box_rect(g.nx, g.ny, 2 * box)
+            vertical = oracle.box_rect(g.nx, g.ny, box)[4]
+            q = p - 2
+            n3 = (cj1 - cj0) * q if vertical else (ci1 - ci0) * q
+            nbc = 2 * ((ci1 - ci0) + (cj1 - cj0)) * q
+            ranks = range(m * gs, (m + 1) * gs)
+            cover = np.zeros(2 * (nbc - n3), int)
+            for r in ranks:
+                lv = plans[r][d]
+                assert lv["gs"] == gs and lv["grank"] == r - m * gs
+                assert lv["side"] == (1 if lv["grank"] >= gs // 2 else 0)
+                assert lv["n3"] == n3 and lv["ntau"] == 2 * (nbc - n3) and lv["n1"] == nbc - n3
+                cover[lv["j0"]:lv["j0"] + lv["w"]] += 1
+            assert np.all(cover == 1), (d, m)
+            # the alpha side's ranks own the subtrees inside child 2 box
+            for r in ranks:
+                sub, i0, j0 = hps.subtree_grid(g, D, r)
+                inside_alpha = ci0 <= i0 < ci1 and cj0 <= j0 < cj1
+                assert inside_alpha == (plans[r][d]["side"] == 0)
 
 
-def run_rank(comm):
-    g, p, kappa, eta, c, s, t = problem()
-    sub, i0, j0 = dist.local_block(g, comm.world, comm.rank)
-    D = dist.DistributedHPS(comm, OracleBackend(g), g, p, kappa, eta, dist.slice_leaves(c, g, sub, i0, j0))
-    s_loc = dist.slice_leaves(s, g, sub, i0, j0)
-    out = D.solve(s_loc, t)
-    nb = out.shape[-1]
-    expect = 2 * np.ones((2, nb), complex) * s_loc.sum() + t[:, :nb]
-    return D.top["R"], np.max(np.abs(out - expect))
+@pytest.mark.parametrize("nx,ny,G", [(256, 256, 8), (1024, 512, 8), (8, 8, 4), (16, 8, 2), (4, 4, 16)])
+def test_dist_plan_tiles_every_top_merge(nx, ny, G):
+    g = hps.grid(0.0, nx / max(nx, ny), 0.0, ny / max(nx, ny), nx, ny)
+    check_plans(g, 16, [hps.dist_plan(g, 16, G, r) for r in range(G)])
 
 
-def reference_root():
-    g, p, kappa, eta, c, s, t = problem()
-    return oracle.Oracle(g.x0, g.x1, g.y0, g.y1, g.nx, g.ny, p, kappa, eta, c).R(1)
-
-
-@pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_thread_ranks_oracle_backend(world):
-    res = dist.run_threads(world, run_rank)
-    Rref = reference_root()
-    for R, err in res:
-        assert np.max(np.abs(R - Rref)) / np.max(np.abs(Rref)) < 1e-10
-        assert err == 0.0
+def test_dist_plan_rejects_shallow_tree():
+    with pytest.raises(hps.HpsError):
+        hps.dist_plan(hps.grid(0, 1, 0, 1, 2, 1), 8, 4, 0)
 
 
 def _gloo_worker(rank, world, port, q):
+    import torch
     import torch.distributed as tdist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        R, err = run_rank(dist.TorchComm())
-        q.put((rank, R, err))
+        # the NCCL unique id made by the library on rank 0 travels over the process group
+        uid = dist.broadcast_unique_id(hps.Comm.nccl_unique_id)
+        # every rank's host plan of the split, gathered over gloo
+        g = hps.grid(0.0, 2.0, 0.0, 1.0, 64, 32)
+        plan = hps.dist_plan(g, 16, world, rank)
+        flat = torch.tensor([[v for lv in plan for v in lv.values()]], dtype=torch.int64)
+        out = [torch.zeros_like(flat) for _ in range(world)]
+        tdist.all_gather(out, flat)
+        keys = list(plan[0].keys())
+        plans = [[dict(zip(keys, o[0, 8 * d:8 * d + 8].tolist())) for d in range(len(plan))] for o in out]
+        # this rank's leaf slice of a natural-order array
+        sub, i0, j0 = dist.local_block(g, world, rank)
+        a = np.arange(g.nx * g.ny * 3).reshape(1, g.nx * g.ny, 3)
+        loc = dist.slice_leaves(a, g, sub, i0, j0)
+        q.put((rank, uid, plans, (sub.nx, sub.ny, i0, j0), loc.sum()))
     finally:
         tdist.destroy_process_group()
 
@@ -118,7 +107,7 @@ def _free_port():
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_gloo_ranks_oracle_backend(world):
+def test_gloo_ranks_split_plumbing(world):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -126,12 +115,18 @@ def test_gloo_ranks_oracle_backend(world):
     procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    out = [q.get(timeout=300) for _ in range(world)]
+    out = sorted([q.get(timeout=300) for _ in range(world)], key=lambda o: o[0])
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    Rref = reference_root()
-    assert sorted(o[0] for o in out) == list(range(world))
-    for _, R, err in out:
-        assert np.max(np.abs(R - Rref)) / np.max(np.abs(Rref)) < 1e-10
-        assert err == 0.0
+    assert [o[0] for o in out] == list(range(world))
+    uids = {o[1] for o in out}
+    assert len(uids) == 1 and len(out[0][1]) == 128
+    g = hps.grid(0.0, 2.0, 0.0, 1.0, 64, 32)
+    for o in out:   # every rank saw the same gathered plans, and they tile the top merges
+        assert o[2] == out[0][2]
+    check_plans(g, 16, out[0][2])
+    # the local leaf slices partition the leaves
+    a = np.arange(g.nx * g.ny * 3)
+    assert sum(o[4] for o in out) == a.sum()
+    assert sum(o[3][0] * o[3][1] for o in out) == g.nx * g.ny

@@ -441,3 +441,29 @@ def test_shared_edge_duplicates_agree(orc):
     q = p - 2
     # leaf 0 east edge = leaf 1 west edge
     assert rel(u[0][q:2 * q], u[1][3 * q:4 * q]) < 1e-10
+
+
+def test_oracle_threading_bitwise(orc):
+    """The oracle's row/column-parallel loops (matmul rows, LU row updates, LU-solve column
+    blocks) keep every element's operation order: results are BITWISE equal for 1 and many
+    threads, so parallelising the checker changes no expected value."""
+    rng = np.random.default_rng(12)
+    A = rng.standard_normal((300, 280)) + 1j * rng.standard_normal((300, 280))
+    B = rng.standard_normal((280, 310)) + 1j * rng.standard_normal((280, 310))
+    M = rng.standard_normal((420, 420)) + 1j * rng.standard_normal((420, 420))
+    nthr = orc.set_threads(0)
+    try:
+        orc.set_threads(1)
+        C1, I1 = orc.matmul(A, B), orc.invert(M)
+        p, nb = 8, 4 * 8 - 8
+        X, Y = orc.leaf_nodes(0, 4, 0, 2, 4, 2, p)
+        Ra = orc.Oracle(0, 2, 0, 2, 2, 2, p, 5.0, 5.0 + 1j, np.ones((4, p * p), complex)).R(1)
+        Rb = orc.Oracle(2, 4, 0, 2, 2, 2, p, 5.0, 5.0 + 1j, np.ones((4, p * p), complex)).R(1)
+        m1 = orc.merge(p, 2, 2, 1, Ra, Rb)["Rtau"]
+        orc.set_threads(max(nthr, 4))
+        C2, I2 = orc.matmul(A, B), orc.invert(M)
+        m2 = orc.merge(p, 2, 2, 1, Ra, Rb)["Rtau"]
+    finally:
+        orc.set_threads(nthr)
+    assert np.array_equal(C1, C2) and np.array_equal(I1, I2) and np.array_equal(m1, m2)
+    del X, Y, nb

@@ -1,0 +1,54 @@
+"""Measured polynomial-manufactured-solution errors at C3 and C4 (collocation is
+exact on degree <= p-1 polynomials, so u - P at the interior nodes is pure rounding).  Prints one
+JSON line per config: max |u - P| / max |P| over interior nodes and over all nodes, for a few
+seeds.  Used to set the tolerance of tests/test_gpu_parity.py::test_config{3,4}_*polynomial*."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import numpy.polynomial.chebyshev as npc
+import torch
+
+from paper_1812_07167_b200 import hps, inputs
+
+
+def run(cfgno, seed):
+    cfg = inputs.CONFIGS[cfgno]
+    p = cfg.p
+    g = hps.grid(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny)
+    X, Y = hps.leaf_nodes(g, p)
+    Xb, Yb, NX, NY = hps.root_boundary_nodes(g, p)
+    rng = np.random.default_rng(seed)
+    a = (rng.standard_normal((p, p)) + 1j * rng.standard_normal((p, p))) / np.outer(np.arange(1, p + 1),
+                                                                                     np.arange(1, p + 1))
+
+    def val(x, y, dx=0, dy=0):
+        co = a
+        if dx:
+            co = npc.chebder(co, dx, axis=0) * 2 ** dx
+        if dy:
+            co = npc.chebder(co, dy, axis=1) * 2 ** dy
+        return npc.chebval2d(2 * x - 1, 2 * y - 1, co)
+
+    c = inputs.c_at(cfg, X, Y)
+    Xi, Yi, ci = inputs.interior_of(p, X), inputs.interior_of(p, Y), inputs.interior_of(p, c)
+    s = (-(val(Xi, Yi, 2, 0) + val(Xi, Yi, 0, 2)) - cfg.kappa ** 2 * ci * val(Xi, Yi))[None]
+    t = (NX * val(Xb, Yb, 1, 0) + NY * val(Xb, Yb, 0, 1) + 1j * cfg.eta * val(Xb, Yb))[None]
+    dev = lambda z: torch.from_numpy(np.ascontiguousarray(z)).cuda()
+    S = hps.Solver(g, p, cfg.kappa, cfg.eta, dev(c), keep_root_R=False)
+    u = S.solve(dev(s), dev(t))[0].cpu().numpy()
+    S.close()
+    ex = val(Xi, Yi)
+    scale = np.max(np.abs(ex))
+    return float(np.max(np.abs(u[:, 4 * (p - 2):] - ex)) / scale), float(np.max(np.abs(s)) / scale)
+
+
+if __name__ == "__main__":
+    import __graft_entry__
+    __graft_entry__.build()
+    for cfgno, seeds in [(3, (9, 1, 2)), (4, (11, 1))]:
+        errs = [run(cfgno, sd) for sd in seeds]
+        print(json.dumps({"config": cfgno, "seeds": list(seeds), "rel_err_interior": [e for e, _ in errs],
+                          "s_over_u": [r for _, r in errs]}), flush=True)
