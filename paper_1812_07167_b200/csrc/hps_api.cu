@@ -1330,18 +1330,19 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
   const int nbb = H.depth[Lb].nb;
   h[Lb].alloc(sizeof(zt) * (size_t)nbot * nbb * R);
   if (H.has_leaves) {
-    DevBuf sint;
-    sint.alloc(sizeof(zt) * (size_t)nbot * ni * R);
-    launch_rhs_in(bottom, sint.as<zt>(), H.leaf_nat.as<int>(), nbot, ni, nrhs, (int64_t)nbot * ni, ni, st);
     S.ut.alloc(sizeof(zt) * (size_t)nbot * nt * R);
-    {  // u~ = Y s
+    {  // u~ = Y s, s read in the ABI layout [R][natural leaf][n_i] (no layout pass)
       ZGemm g;
       g.M = nt;
       g.N = nrhs;
       g.K = ni;
       g.batch = nbot;
       g.A = op(H.store.as<zt>() + nb, nt, (int64_t)nt * nt);
-      g.B = op(sint.as<zt>(), R, (int64_t)ni * R);
+      g.B.ptr = bottom;
+      g.B.rs = 1;
+      g.B.cs = (int64_t)nbot * ni;
+      g.B.bs = ni;
+      g.B.bmap = H.leaf_nat.as<int>();
       g.C = out(S.ut.as<zt>(), R, (int64_t)nt * R);
       zgemm(g, st);
       fl += 8.0 * nbot * (double)nt * ni * R;
@@ -1437,9 +1438,7 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
   }
   const int nbot = 1 << Lb;
   if (H.has_leaves) {
-    DevBuf uint_;
-    uint_.alloc(sizeof(zt) * (size_t)nbot * nt * R);
-    ZGemm g;  // u = Psi t + u~  (line 13)
+    ZGemm g;  // u = Psi t + u~  (line 13), written straight to the ABI layout [R][natural leaf][n_t]
     g.M = nt;
     g.N = nrhs;
     g.K = nb;
@@ -1450,10 +1449,13 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
       g.Cin = op(S.ut.as<zt>(), R, (int64_t)nt * R);
       g.beta = Z(1, 0);
     }
-    g.C = out(uint_.as<zt>(), R, (int64_t)nt * R);
+    g.C.ptr = outp;
+    g.C.rs = 1;
+    g.C.cs = (int64_t)nbot * nt;
+    g.C.bs = nt;
+    g.C.bmap = H.leaf_nat.as<int>();
     zgemm(g, st);
     fl += 8.0 * nbot * (double)nt * nb * R;
-    launch_rhs_out(uint_.as<zt>(), outp, H.nat_to_heap.as<int>(), nbot, nt, nrhs, (int64_t)nbot * nt, nt, st);
   } else {
     const int nbb = H.depth[Lb].nb;
     launch_rhs_out(t[Lb].as<zt>(), outp, H.ident.as<int>(), nbot, nbb, nrhs, nbb, R * nbb, st);

@@ -67,6 +67,8 @@ int hps_num_sms();  // multiprocessors of the current device (cached per device)
 // Without a column map, column j may skip a window: j -> j + (j >= cskip_at ? cskip_len : 0)
 // (used by the blocked Gauss-Jordan update, which touches every column but the panel).
 // rmap_bs: batch stride of the row map (0 = one map shared by the whole batch).
+// bmap: batch map -- batch entry b lives at ptr + bmap[b]*bs (the solve reads s and writes u in
+// the ABI's natural leaf order while the leaves are stored in heap order).
 struct ZOp {
   const zt* ptr = nullptr;
   int64_t rs = 0, cs = 1, bs = 0;
@@ -74,6 +76,7 @@ struct ZOp {
   const int* cmap = nullptr;
   int cskip_at = 0x7fffffff, cskip_len = 0;
   int64_t rmap_bs = 0;
+  const int* bmap = nullptr;
 };
 
 struct ZOut {
@@ -83,7 +86,13 @@ struct ZOut {
   const int* cmap = nullptr;
   int cskip_at = 0x7fffffff, cskip_len = 0;
   int64_t rmap_bs = 0;
+  const int* bmap = nullptr;
 };
+
+template <class T>
+__device__ __forceinline__ int64_t zboff(const T& o, int b) {
+  return (int64_t)(o.bmap ? o.bmap[b] : b) * o.bs;
+}
 
 __device__ __forceinline__ int zcol(const int* cmap, int j, int skip_at, int skip_len) {
   return cmap ? cmap[j] : j + (j >= skip_at ? skip_len : 0);

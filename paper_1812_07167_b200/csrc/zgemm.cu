@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
   constexpr int B_RSTEP = (NT >= BN) ? NT / BN : 1;
 
   for (int b = blockIdx.y; b < g.batch; b += gridDim.y) {
-    const zt* Ab = g.A.ptr + (int64_t)b * g.A.bs;
-    const zt* Bb = g.B.ptr + (int64_t)b * g.B.bs;
+    const zt* Ab = g.A.ptr + zboff(g.A, b);
+    const zt* Bb = g.B.ptr + zboff(g.B, b);
     const int* Arm = g.A.rmap ? g.A.rmap + (int64_t)b * g.A.rmap_bs : nullptr;
     const int* Brm = g.B.rmap ? g.B.rmap + (int64_t)b * g.B.rmap_bs : nullptr;
     const int* Crm = g.C.rmap ? g.C.rmap + (int64_t)b * g.C.rmap_bs : nullptr;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
     // beta == alpha (every use but one) the raw values are loaded with no arithmetic, so all
     // loads are in flight together and the first DMMA is the first consumer.
     double accr[TM][TN][2], acci[TM][TN][2];
-    const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + (int64_t)b * g.Cin.bs : nullptr;
+    const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + zboff(g.Cin, b) : nullptr;
     const bool raw = g.beta.x == g.alpha.x && g.beta.y == g.alpha.y;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
     }
 
     // Epilogue: C = alpha * acc + diag * [i == j]
-    zt* Cb = g.C.ptr + (int64_t)b * g.C.bs;
+    zt* Cb = g.C.ptr + zboff(g.C, b);
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
 #pragma unroll
     for (int r = 0; r < NMAX; ++r) accr[r] = acci[r] = 0.0;
     if (ra >= 0) {
-      const zt* Ab = g.A.ptr + (int64_t)b * g.A.bs + (int64_t)ra * g.A.rs;
-      const zt* Bb = g.B.ptr + (int64_t)b * g.B.bs;
+      const zt* Ab = g.A.ptr + zboff(g.A, b) + (int64_t)ra * g.A.rs;
+      const zt* Bb = g.B.ptr + zboff(g.B, b);
       int64_t bco[NMAX];
       bool bok[NMAX];
 #pragma unroll
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
         const int ri = Irm ? Irm[row] : row;
         const int cj = zcol(g.Cin.cmap, r, g.Cin.cskip_at, g.Cin.cskip_len);
         if (ri >= 0 && cj >= 0) {
-          const zt cv = zmul(g.beta, g.Cin.ptr[(int64_t)b * g.Cin.bs + (int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
+          const zt cv = zmul(g.beta, g.Cin.ptr[zboff(g.Cin, b) + (int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
           v.x += cv.x;
           v.y += cv.y;
         }
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(256) zgemv_kernel(const ZGemm g) {
         v.y += g.diag.y;
       }
       const int co = zcol(g.C.cmap, r, g.C.cskip_at, g.C.cskip_len);
-      if (co >= 0) g.C.ptr[(int64_t)b * g.C.bs + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
+      if (co >= 0) g.C.ptr[zboff(g.C, b) + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
     }
   }
 }
@@ -373,8 +373,8 @@ __global__ void __launch_bounds__(256) zgemv_short_kernel(const ZGemm g) {
 #pragma unroll
     for (int r = 0; r < NMAX; ++r) accr[r] = acci[r] = 0.0;
     if (ra >= 0) {
-      const zt* Ab = g.A.ptr + (int64_t)b * g.A.bs + (int64_t)ra * g.A.rs;
-      const zt* Bb = g.B.ptr + (int64_t)b * g.B.bs;
+      const zt* Ab = g.A.ptr + zboff(g.A, b) + (int64_t)ra * g.A.rs;
+      const zt* Bb = g.B.ptr + zboff(g.B, b);
       int64_t bco[NMAX];
       bool bok[NMAX];
 #pragma unroll
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(256) zgemv_short_kernel(const ZGemm g) {
         const int ri = Irm ? Irm[row] : row;
         const int cj = zcol(g.Cin.cmap, r, g.Cin.cskip_at, g.Cin.cskip_len);
         if (ri >= 0 && cj >= 0) {
-          const zt cv = zmul(g.beta, g.Cin.ptr[(int64_t)b * g.Cin.bs + (int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
+          const zt cv = zmul(g.beta, g.Cin.ptr[zboff(g.Cin, b) + (int64_t)ri * g.Cin.rs + (int64_t)cj * g.Cin.cs]);
           v.x += cv.x;
           v.y += cv.y;
         }
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(256) zgemv_short_kernel(const ZGemm g) {
         v.y += g.diag.y;
       }
       const int co = zcol(g.C.cmap, r, g.C.cskip_at, g.C.cskip_len);
-      if (co >= 0) g.C.ptr[(int64_t)b * g.C.bs + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
+      if (co >= 0) g.C.ptr[zboff(g.C, b) + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
     }
   }
 }
@@ -493,8 +493,8 @@ __global__ void zcopy_kernel(const ZCopy c) {
     const int ri = c.A.rmap ? c.A.rmap[(int64_t)b * c.A.rmap_bs + i] : i;
     const int ci = zcol(c.A.cmap, j, c.A.cskip_at, c.A.cskip_len);
     zt v = make_double2(0.0, 0.0);
-    if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[(int64_t)b * c.A.bs + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
-    c.C.ptr[(int64_t)b * c.C.bs + (int64_t)ro * c.C.rs + (int64_t)co * c.C.cs] = v;
+    if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[zboff(c.A, b) + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
+    c.C.ptr[zboff(c.C, b) + (int64_t)ro * c.C.rs + (int64_t)co * c.C.cs] = v;
   }
 }
 
@@ -539,6 +539,9 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
     case 6: launch<32, 64, 16, 32>(g, st); return true;
     case 7: launch<128, 64, 32, 32>(g, st); return true;
     case 8: launch<64, 64, 16, 32>(g, st); return true;
+    case 10: launch<64, 16, 16, 16>(g, st); return true;
+    case 11: launch<128, 16, 32, 16>(g, st); return true;
+    case 12: launch<64, 16, 32, 8>(g, st); return true;
     case 9: {
       if (g.N == 1) launch_gemv<1>(g, st);
       else if (g.N <= 4) launch_gemv<4>(g, st);
@@ -572,6 +575,8 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   const int nsm = hps_num_sms();
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
+  else if (g.N <= 16 && g.M > 16)
+    launch<64, 16, 16, 16>(g, st);  // the solve sweeps at 16 right-hand sides: no half-empty tiles
   else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * nsm))
     launch<16, 16, 8, 8>(g, st);  // short K on a grid of few 32x32 tiles: more, smaller CTAs
   else if (g.K >= 512)
@@ -601,8 +606,8 @@ __global__ void zcopy_multi_kernel(const ZCopyList L) {
     const int ri = c.A.rmap ? c.A.rmap[(int64_t)b * c.A.rmap_bs + i] : i;
     const int ci = zcol(c.A.cmap, j, c.A.cskip_at, c.A.cskip_len);
     zt v = make_double2(0.0, 0.0);
-    if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[(int64_t)b * c.A.bs + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
-    c.C.ptr[(int64_t)b * c.C.bs + (int64_t)ro * c.C.rs + (int64_t)co * c.C.cs] = v;
+    if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[zboff(c.A, b) + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
+    c.C.ptr[zboff(c.C, b) + (int64_t)ro * c.C.rs + (int64_t)co * c.C.cs] = v;
   }
 }
 

@@ -371,9 +371,11 @@ def test_sharded_top_flops_split():
     extra = sum((lv["gs"] - 1) * (1 << d) * 16.0 * lv["n3"] ** 3 for d, lv in enumerate(plan))
     f_sum = sum(fl[0] for _, _, fl, _ in res)
     assert abs(f_sum - (f_single + extra)) <= 1e-9 * f_single, (f_sum, f_single, extra)
-    # per rank: the same work (congruent subtrees, equal column slices)
+    # per rank: the same work up to the first half of X = [R33b R31a | -R32b] (its I1 columns are a
+    # product, its I2 columns a copy): at most 8 n3^2 w per level apart
     per = [fl[0] for _, _, fl, _ in res]
-    assert max(per) - min(per) <= 1e-9 * max(per)
+    slack = sum(8.0 * lv["n3"] ** 2 * lv["w"] for lv in plan)
+    assert max(per) - min(per) <= slack * (1 + 1e-12), (per, slack)
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
@@ -455,7 +457,7 @@ def test_virtual_comm_selftest():
     assert all(dist.run_virtual(8, fn))
 
 
-@pytest.mark.parametrize("cfg", list(range(10)))
+@pytest.mark.parametrize("cfg", list(range(13)))
 @pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1),
                                          (70, 1, 300, 2), (33, 3, 45, 3)])
 def test_zgemm_configs(cfg, M, N, K, batch):
@@ -544,7 +546,9 @@ def test_config3_polynomial_exact():
     u = S.solve(np.ascontiguousarray(s), np.ascontiguousarray(t))[0]
     ex_i = val(Xi, Yi)
     scale = np.max(np.abs(ex_i))
-    assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / scale < 1e-7
+    # measured 1.1e-13 .. 2.0e-13 over three seeds (tools/poly_errors.py, profiles/r02_poly_errors.txt);
+    # bound = 10x the worst, see DESIGN.md 6 for the conditioning argument
+    assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / scale < 2e-12
 
 
 def test_paper_experiment_convergence():
@@ -629,7 +633,8 @@ def test_config4_sampled_leaves_and_polynomial():
     u = S.solve(dev(s), dev(t))[0].cpu().numpy()
     S.close()
     ex_i = val(Xi, Yi)
-    assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / np.max(np.abs(ex_i)) < 1e-7
+    # measured 2.3e-13 / 2.7e-13 (two seeds, tools/poly_errors.py); bound = 10x the worst
+    assert np.max(np.abs(u[:, 4 * (p - 2):] - ex_i)) / np.max(np.abs(ex_i)) < 3e-12
 
 
 @pytest.mark.parametrize("nx,ny,p,nrhs", [(4, 4, 8, 37), (8, 4, 10, 64), (2, 2, 16, 9)])
