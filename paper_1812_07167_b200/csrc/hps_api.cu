@@ -44,7 +44,7 @@ const KnobDef g_knob_defs[KN_COUNT] = {
     {"nat_max", 1 << 30}, {"nat_force_fail", 0}, {"dgj_pivot", 0}, {"dgj_force_bad", 0}, {"dgj_rpt", 2},
     {"lr_trace", 0},    {"gemv_short", 1}, {"gemv_k16", 256}, {"trace", 0},          {"gemm_smallk", 1},
     {"gj", 0},          {"seq_pivot", 0},  {"nat_w", 16},     {"nat_lpr", 4},        {"natc", 1},
-    {"natb", 1},        {"nat_pivot_rel", 25}};
+    {"natb", 1},        {"nat_pivot_rel", 25}, {"nat_bb_min", 1024}};
 std::atomic<int> g_knobs[KN_COUNT];
 std::once_flag g_knob_once;
 void knob_init() {
@@ -354,6 +354,14 @@ struct MergeLevel {
   int *I1a, *I2b, *I3a, *I3b, *pp, *cmapA, *cmapB;
   DevBuf ops;
   zt *PhiA, *PhiB, *Winv, *R33a, *R33b, *R13a, *R23b;
+  // host copies of the maps (the sharded top levels compose them, below)
+  std::vector<int> hI1a, hI2b, hI3a, hI3b, hpp, hcmA, hcmB;
+  // sharded top level whose children are column slices of the level below: the children's ItI
+  // maps arrive column-major with columns in the child merge's [I1, I2] order, so every column
+  // index is composed with the inverse of the child level's pp (the *_c maps)
+  DevBuf cmaps;
+  int *I1a_c = nullptr, *I2b_c = nullptr, *I3a_c = nullptr, *I3b_c = nullptr, *cmapA_c = nullptr,
+      *cmapB_c = nullptr;
 };
 
 bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -611,6 +619,13 @@ void plan_level(hps_handle& H, int d, MergeLevel& M) {
   for (int j = 0; j < M.n2; ++j) cmB[M.n1 + j] = I2b[j];
   size_t o1 = put(I1a), o2 = put(I2b), o3 = put(I3a), o4 = put(I3b), o5 = put(pp), o6 = put(cmA), o7 = put(cmB);
   upload(M.maps, all, H.st);
+  M.hI1a = I1a;
+  M.hI2b = I2b;
+  M.hI3a = I3a;
+  M.hI3b = I3b;
+  M.hpp = pp;
+  M.hcmA = cmA;
+  M.hcmB = cmB;
   int* base = M.maps.as<int>();
   M.I1a = base + o1;
   M.I2b = base + o2;
@@ -1064,54 +1079,64 @@ void build_merge(hps_handle& H, int d) {
 // step).  H is the TOP handle of a multi-GPU build: global tree, bottom depth D = log2 G, one merge
 // per level per rank (the box above this rank's subtree), group of gs = G >> d ranks under it.
 // ---------------------------------------------------------------------------
-// The children's ItI maps of this rank's depth-d merge, whole, into Ra / Rb (nbc x nbc each,
-// canonical order): at d = D - 1 the children are two subtree roots (pair all-gather); above, each
-// child's R^tau is column-distributed over its gs / 2 ranks ([nbc][wpad] slices in the child
-// merge's [I1, I2] column order) and is all-gathered and scattered to canonical columns.
-void gather_children_R(hps_handle& H, int d, zt* Ra, zt* Rb) {
+// The children's ItI maps of this rank's depth-d merge, whole, on every rank of the group.  At
+// d = D - 1 the children are two subtree roots (row-major, canonical order; pair all-gather).
+// Above, each child's R^tau is column-distributed over its gs / 2 ranks: slices [w][nbc] stored
+// COLUMN-major, columns in the child merge's [I1, I2] order, so the group's all-gather lands every
+// column at column-major offset j * nbc -- the gathered buffer IS the two matrices, no layout pass
+// (C5's root level gathers 26 GB; a conversion copy would double that).
+struct ChildR {
+  const zt* a;
+  const zt* b;
+  bool colmajor;
+  int64_t ld;
+  // element (i, j) (canonical indices via the maps) of child alpha / beta
+  ZOp op(const zt* base, const int* rmap, const int* cmap, const int* cmap_c) const {
+    ZOp o;
+    o.ptr = base;
+    o.rmap = rmap;
+    if (colmajor) {
+      o.rs = 1;
+      o.cs = ld;
+      o.cmap = cmap_c;
+    } else {
+      o.rs = ld;
+      o.cs = 1;
+      o.cmap = cmap;
+    }
+    return o;
+  }
+};
+
+ChildR gather_children_R(hps_handle& H, int d, DevBuf& buf) {
   const MergeLevel& M = H.lev[d];
   const DistLevel& P = H.dl[d];
   const int nbc = M.nbc;
   const int64_t cs2 = (int64_t)nbc * nbc;
   cudaStream_t st = H.st;
   if (d + 1 == H.D) {
-    H.comm->allgather(2, H.R[d + 1].p, Ra, sizeof(zt) * cs2, st);  // Rb == Ra + cs2
-    return;
+    buf.alloc(sizeof(zt) * 2 * cs2);
+    H.comm->allgather(2, H.R[d + 1].p, buf.p, sizeof(zt) * cs2, st);
+    return ChildR{buf.as<zt>(), buf.as<zt>() + cs2, false, nbc};
   }
-  const DistLevel& Pc = H.dl[d + 1];
-  const MergeLevel& Mc = H.lev[d + 1];
-  const int wc = Pc.wpad, half = P.gs / 2;
-  DevBuf gat;
-  gat.alloc(sizeof(zt) * (size_t)P.gs * nbc * wc);
-  H.comm->allgather(P.gs, H.R[d + 1].p, gat.p, sizeof(zt) * (size_t)nbc * wc, st);
-  std::vector<ZCopy> cps;
-  for (int k = 0; k < P.gs; ++k) {
-    const int kk = k % half, j0 = kk * wc, we = std::min(wc, nbc - j0);
-    if (we <= 0) continue;
-    ZCopy c;
-    c.batch = 1;
-    c.M = nbc;
-    c.N = we;
-    c.A = op(gat.as<zt>() + (int64_t)k * nbc * wc, wc, 0);
-    c.C = out(k < half ? Ra : Rb, nbc, 0, nullptr, Mc.pp + j0);
-    cps.push_back(c);
-  }
-  zcopy_multi(cps.data(), (int)cps.size(), st);
+  const int wc = H.dl[d + 1].wpad;
+  buf.alloc(sizeof(zt) * (size_t)P.gs * nbc * wc);
+  H.comm->allgather(P.gs, H.R[d + 1].p, buf.p, sizeof(zt) * (size_t)nbc * wc, st);
+  return ChildR{buf.as<zt>(), buf.as<zt>() + (int64_t)(P.gs / 2) * wc * nbc, true, nbc};
 }
 
 void build_merge_dist(hps_handle& H, int d) {
   MergeLevel& M = H.lev[d];
   const DistLevel& P = H.dl[d];
-  const int n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau, nbc = M.nbc;
+  const int n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau;
   const int j0 = P.j0, w = P.w, wp = P.wpad;
-  const int64_t cs2 = (int64_t)nbc * nbc, s33 = (int64_t)n3 * n3;
   cudaStream_t st = H.st;
-  DevBuf Rab;
-  Rab.alloc(sizeof(zt) * 2 * cs2);
-  zt* Ra = Rab.as<zt>();
-  zt* Rb = Ra + cs2;
-  gather_children_R(H, d, Ra, Rb);
+  DevBuf Rbuf;
+  const ChildR CR = gather_children_R(H, d, Rbuf);
   H.R[d + 1].release();
+  auto RA = [&](const int* rm, const int* cm, const int* cm_c) { return CR.op(CR.a, rm, cm, cm_c); };
+  auto RB = [&](const int* rm, const int* cm, const int* cm_c) { return CR.op(CR.b, rm, cm, cm_c); };
+  auto off = [](const int* m, int o) { return m ? m + o : nullptr; };
   // (a) retained child blocks, replicated in the group
   {
     ZCopy c[4];
@@ -1120,16 +1145,16 @@ void build_merge_dist(hps_handle& H, int d) {
       x.N = n3;
     }
     c[0].M = n3;
-    c[0].A = op(Ra, nbc, 0, M.I3a, M.I3a);
+    c[0].A = RA(M.I3a, M.I3a, M.I3a_c);
     c[0].C = out(M.R33a, n3, 0);
     c[1].M = n3;
-    c[1].A = op(Rb, nbc, 0, M.I3b, M.I3b);
+    c[1].A = RB(M.I3b, M.I3b, M.I3b_c);
     c[1].C = out(M.R33b, n3, 0);
     c[2].M = n1;
-    c[2].A = op(Ra, nbc, 0, M.I1a, M.I3a);
+    c[2].A = RA(M.I1a, M.I3a, M.I3a_c);
     c[2].C = out(M.R13a, n3, 0);
     c[3].M = n2;
-    c[3].A = op(Rb, nbc, 0, M.I2b, M.I3b);
+    c[3].A = RB(M.I2b, M.I3b, M.I3b_c);
     c[3].C = out(M.R23b, n3, 0);
     zcopy_multi(c, 4, st);
   }
@@ -1144,7 +1169,7 @@ void build_merge_dist(hps_handle& H, int d) {
     g.N = nA;
     g.K = n3;
     g.A = op(M.R33b, n3, 0);
-    g.B = op(Ra, nbc, 0, M.I3a, M.I1a + j0);
+    g.B = RA(M.I3a, M.I1a + j0, off(M.I1a_c, j0));
     g.C = out(X.as<zt>(), wp, 0);
     zgemm(g, st);
   }
@@ -1152,7 +1177,7 @@ void build_merge_dist(hps_handle& H, int d) {
     ZCopy c;
     c.M = n3;
     c.N = nB;
-    c.A = op(Rb, nbc, 0, M.I3b, M.I2b + (jb0 - n1));
+    c.A = RB(M.I3b, M.I2b + (jb0 - n1), off(M.I2b_c, jb0 - n1));
     c.C = out(X.as<zt>() + (jb0 - j0), wp, 0);
     c.alpha = Z(-1, 0);
     zcopy(c, st);
@@ -1176,7 +1201,7 @@ void build_merge_dist(hps_handle& H, int d) {
     h.K = n3;
     h.A = op(M.R33a, n3, 0);
     h.B = op(M.PhiA, wp, 0);
-    h.Cin = op(Ra, nbc, 0, M.I3a, M.cmapA + j0);
+    h.Cin = RA(M.I3a, M.cmapA + j0, off(M.cmapA_c, j0));
     h.C = out(M.PhiB, wp, 0);
     h.alpha = Z(-1, 0);
     h.beta = Z(-1, 0);
@@ -1184,7 +1209,7 @@ void build_merge_dist(hps_handle& H, int d) {
     fl += 8.0 * 2.0 * n3 * n3 * (double)w;
   }
   // (f) columns J of R^tau = diag(R11a, R22b) + [R13a Phi^a ; R23b Phi^b], rows in canonical
-  // order, kept column-distributed ([ntau][wpad]) for the next level's all-gather (line 12)
+  // order, kept column-distributed: slice [wpad][ntau] column-major (line 12)
   const bool need_R = d > 0 || H.keep_root_R || H.keep_all_R;
   if (need_R) {
     H.R[d].alloc(sizeof(zt) * (size_t)nt * wp);
@@ -1196,23 +1221,26 @@ void build_merge_dist(hps_handle& H, int d) {
       g.M = n1;
       g.A = op(M.R13a, n3, 0);
       g.B = op(M.PhiA, wp, 0);
-      g.Cin = op(Ra, nbc, 0, M.I1a, M.cmapA + j0);
-      g.C = out(H.R[d].as<zt>(), wp, 0, M.pp, nullptr);
+      g.Cin = RA(M.I1a, M.cmapA + j0, off(M.cmapA_c, j0));
+      g.C.ptr = H.R[d].as<zt>();
+      g.C.rs = 1;
+      g.C.cs = nt;
+      g.C.rmap = M.pp;
       zgemm(g, st);
       g.M = n2;
       g.A = op(M.R23b, n3, 0);
       g.B = op(M.PhiB, wp, 0);
-      g.Cin = op(Rb, nbc, 0, M.I2b, M.cmapB + j0);
-      g.C = out(H.R[d].as<zt>(), wp, 0, M.pp + n1, nullptr);
+      g.Cin = RB(M.I2b, M.cmapB + j0, off(M.cmapB_c, j0));
+      g.C.rmap = M.pp + n1;
       zgemm(g, st);
       fl += 8.0 * (double)nt * n3 * w;
     }
   }
-  (void)s33;
   H.flops[0] += fl;
 }
 
-// keep_root_R on a sharded build: all-gather the root's column slices into the whole R^1.
+// keep_root_R on a sharded build: all-gather the root's column slices (column-major, [I1, I2]
+// column order) and transpose them into the whole R^1 (row-major, canonical order).
 void gather_root_R(hps_handle& H) {
   const MergeLevel& M = H.lev[0];
   const DistLevel& P = H.dl[0];
@@ -1221,18 +1249,14 @@ void gather_root_R(hps_handle& H) {
   gat.alloc(sizeof(zt) * (size_t)P.gs * nt * wp);
   H.comm->allgather(P.gs, H.R[0].p, gat.p, sizeof(zt) * (size_t)nt * wp, H.st);
   full.alloc(sizeof(zt) * (size_t)nt * nt);
-  std::vector<ZCopy> cps;
-  for (int k = 0; k < P.gs; ++k) {
-    const int j0 = k * wp, we = std::min(wp, nt - j0);
-    if (we <= 0) continue;
-    ZCopy c;
-    c.M = nt;
-    c.N = we;
-    c.A = op(gat.as<zt>() + (int64_t)k * nt * wp, wp, 0);
-    c.C = out(full.as<zt>(), nt, 0, nullptr, M.pp + j0);
-    cps.push_back(c);
-  }
-  zcopy_multi(cps.data(), (int)cps.size(), H.st);
+  ZCopy c;
+  c.M = nt;
+  c.N = nt;
+  c.A.ptr = gat.as<zt>();
+  c.A.rs = 1;
+  c.A.cs = nt;
+  c.C = out(full.as<zt>(), nt, 0, nullptr, M.pp);
+  zcopy(c, H.st);
   H.R[0] = std::move(full);
 }
 
@@ -1827,6 +1851,28 @@ void plan_all(hps_handle& H, int Lb) {
   H.R.resize(H.L + 1);
   H.lev.resize(Lb);
   for (int d = 0; d < Lb; ++d) plan_level(H, d, H.lev[d]);
+  if (H.dist_top) {  // composed column maps of the levels whose children are column slices
+    for (int d = 0; d + 1 < Lb; ++d) {
+      MergeLevel& M = H.lev[d];
+      const std::vector<int>& ppc = H.lev[d + 1].hpp;  // [I1, I2] index -> canonical, child level
+      std::vector<int> inv(ppc.size(), -1);
+      for (size_t j = 0; j < ppc.size(); ++j) inv[ppc[j]] = (int)j;
+      std::vector<int> all;
+      std::vector<size_t> off;
+      for (const std::vector<int>* v : {&M.hI1a, &M.hI2b, &M.hI3a, &M.hI3b, &M.hcmA, &M.hcmB}) {
+        off.push_back(all.size());
+        for (int x : *v) all.push_back(x < 0 ? -1 : inv[x]);
+      }
+      upload(M.cmaps, all, H.st);
+      int* base = M.cmaps.as<int>();
+      M.I1a_c = base + off[0];
+      M.I2b_c = base + off[1];
+      M.I3a_c = base + off[2];
+      M.I3b_c = base + off[3];
+      M.cmapA_c = base + off[4];
+      M.cmapB_c = base + off[5];
+    }
+  }
   H.ss.reset(Lb);
 }
 

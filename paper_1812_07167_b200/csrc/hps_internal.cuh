@@ -44,6 +44,7 @@ enum HpsKnob {
   KN_NATC,             // 1: cluster panel for the natural-order inverse
   KN_NATB,             // 1: blocked natural-order panel (DESIGN 3.10)
   KN_NAT_PIVOT_REL,    // natural-order W^{-1}: pivot accepted if |p|^2 >= REL/1e4 * |W_kk|^2
+  KN_NAT_BB_MIN,       // natural-order W^{-1} with 64-wide block steps (D^{-1} kernel + GEMMs) for n >= this
   KN_COUNT
 };
 int knob(HpsKnob k);
@@ -77,6 +78,7 @@ struct ZOp {
   int cskip_at = 0x7fffffff, cskip_len = 0;
   int64_t rmap_bs = 0;
   const int* bmap = nullptr;
+  int rskip_at = 0x7fffffff, rskip_len = 0;  // row window skipped like cskip (no row map)
 };
 
 struct ZOut {
@@ -87,6 +89,7 @@ struct ZOut {
   int cskip_at = 0x7fffffff, cskip_len = 0;
   int64_t rmap_bs = 0;
   const int* bmap = nullptr;
+  int rskip_at = 0x7fffffff, rskip_len = 0;
 };
 
 template <class T>
@@ -96,6 +99,11 @@ __device__ __forceinline__ int64_t zboff(const T& o, int b) {
 
 __device__ __forceinline__ int zcol(const int* cmap, int j, int skip_at, int skip_len) {
   return cmap ? cmap[j] : j + (j >= skip_at ? skip_len : 0);
+}
+// row i of an operand: its row map, else i with the row window [rskip_at, rskip_at + rskip_len) skipped
+template <class T>
+__device__ __forceinline__ int zrow(const T& o, const int* rm, int i) {
+  return rm ? rm[i] : i + (i >= o.rskip_at ? o.rskip_len : 0);
 }
 
 struct ZGemm {

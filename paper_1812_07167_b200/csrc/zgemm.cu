@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
 #pragma unroll
     for (int it = 0; it < ITA; ++it) {
       const int gi = m0 + a_r0 + it * A_RSTEP;
-      int ri = gi < g.M ? (Arm ? Arm[gi] : gi) : -1;
+      int ri = gi < g.M ? zrow(g.A, Arm, gi) : -1;
       a_rok[it] = ri >= 0;
       a_roff[it] = (int64_t)(ri < 0 ? 0 : ri) * g.A.rs;
     }
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
-      const int ri = (Cinb && gi < g.M) ? (Irm ? Irm[gi] : gi) : -1;
+      const int ri = (Cinb && gi < g.M) ? zrow(g.Cin, Irm, gi) : -1;
 #pragma unroll
       for (int j = 0; j < TN; ++j)
 #pragma unroll
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
     for (int i = 0; i < TM; ++i) {
       const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
       if (gi >= g.M) continue;
-      const int ro = Crm ? Crm[gi] : gi;
+      const int ro = zrow(g.C, Crm, gi);
       if (ro < 0) continue;
 #pragma unroll
       for (int j = 0; j < TN; ++j) {
@@ -487,10 +487,10 @@ __global__ void zcopy_kernel(const ZCopy c) {
     const IT bq = t / (IT)c.M;
     const int i = (int)(t - bq * (IT)c.M);
     const int b = (int)bq;
-    const int ro = c.C.rmap ? c.C.rmap[(int64_t)b * c.C.rmap_bs + i] : i;
+    const int ro = zrow(c.C, c.C.rmap ? c.C.rmap + (int64_t)b * c.C.rmap_bs : nullptr, i);
     const int co = zcol(c.C.cmap, j, c.C.cskip_at, c.C.cskip_len);
     if (ro < 0 || co < 0) continue;
-    const int ri = c.A.rmap ? c.A.rmap[(int64_t)b * c.A.rmap_bs + i] : i;
+    const int ri = zrow(c.A, c.A.rmap ? c.A.rmap + (int64_t)b * c.A.rmap_bs : nullptr, i);
     const int ci = zcol(c.A.cmap, j, c.A.cskip_at, c.A.cskip_len);
     zt v = make_double2(0.0, 0.0);
     if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[zboff(c.A, b) + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);
@@ -575,6 +575,8 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   const int nsm = hps_num_sms();
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
+  else if (g.N <= 16 && g.M > 16 && g.K >= 1024 && (int64_t)((g.M + 63) / 64) * g.batch < nsm)
+    launch<16, 16, 8, 8>(g, st);    // long-K products of the top levels' solve: more, smaller CTAs
   else if (g.N <= 16 && g.M > 16)
     launch<64, 16, 16, 16>(g, st);  // the solve sweeps at 16 right-hand sides: no half-empty tiles
   else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * nsm))
@@ -600,10 +602,10 @@ __global__ void zcopy_multi_kernel(const ZCopyList L) {
     const IT bq = t / (IT)c.M;
     const int i = (int)(t - bq * (IT)c.M);
     const int b = (int)bq;
-    const int ro = c.C.rmap ? c.C.rmap[(int64_t)b * c.C.rmap_bs + i] : i;
+    const int ro = zrow(c.C, c.C.rmap ? c.C.rmap + (int64_t)b * c.C.rmap_bs : nullptr, i);
     const int co = zcol(c.C.cmap, j, c.C.cskip_at, c.C.cskip_len);
     if (ro < 0 || co < 0) continue;
-    const int ri = c.A.rmap ? c.A.rmap[(int64_t)b * c.A.rmap_bs + i] : i;
+    const int ri = zrow(c.A, c.A.rmap ? c.A.rmap + (int64_t)b * c.A.rmap_bs : nullptr, i);
     const int ci = zcol(c.A.cmap, j, c.A.cskip_at, c.A.cskip_len);
     zt v = make_double2(0.0, 0.0);
     if (ri >= 0 && ci >= 0) v = zmul(c.alpha, c.A.ptr[zboff(c.A, b) + (int64_t)ri * c.A.rs + (int64_t)ci * c.A.cs]);

@@ -2901,8 +2901,22 @@ __global__ void nat_diag_kernel(const zt* A, int64_t lda, int64_t bs, int n, dou
 // the blocked explicit-swap update with identity maps (any n).  Workspace as
 // zgj_workspace_bytes(n, batch) for the blocked regime; *flag (device) is set to 1 when a pivot
 // failed the check — out is then not the inverse and A is destroyed (the caller keeps a copy).
+void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st);
+
 void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
                         void* ws, int* flag, cudaStream_t st) {
+  if (n >= knob(KN_NAT_BB_MIN)) {  // in place in A, then copied out
+    zgj_invert_natural_blocked(A, lda, bs, n, batch, ws, flag, st);
+    ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)batch * n * n, st);
+    if (lda == n && bs == (int64_t)n * n && ldo == n && obs == (int64_t)n * n) {
+      HPS_CUDA_CHECK(cudaMemcpyAsync(out, A, sizeof(zt) * (size_t)batch * n * n, cudaMemcpyDeviceToDevice, st));
+    } else {
+      for (int b = 0; b < batch; ++b)
+        HPS_CUDA_CHECK(cudaMemcpy2DAsync(out + (int64_t)b * obs, sizeof(zt) * ldo, A + (int64_t)b * bs, sizeof(zt) * lda,
+                                         sizeof(zt) * n, n, cudaMemcpyDeviceToDevice, st));
+    }
+    return;
+  }
   char* wsp = static_cast<char*>(ws);
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   zt* B2 = reinterpret_cast<zt*>(wsp);
@@ -3011,7 +3025,208 @@ void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, in
   (void)pi;
 }
 
+// ---------------------------------------------------------------------------
+// Natural-order Gauss-Jordan in 64-wide BLOCK steps for the large top-level W (n >= nat_bb_min,
+// DESIGN.md 3.10).  Pivot rows known in advance make a block step exact algebra:
+//   D = A[K, K] (K = [k0, k0 + b)), D^{-1} in natural order (its pivots ARE the global natural-order
+//   pivots of steps k0 .. k0 + b - 1, checked against the original diagonal as in the panels);
+//   T = -A[:, K] D^{-1} (rows outside K), T[K] = D^{-1} - I;  Z = A[K, :] (old);
+//   A[:, j not in K] += T Z[:, j]  (one in-place K = b GEMM: rows outside K get the rank-b update,
+//   rows K become D^{-1} Z);  A[rows outside K, K] = T,  A[K, K] = D^{-1}.
+// The trailing update then reads and writes W once per 64 columns instead of once per 16
+// (C4: n3 = 3584, W = 205 MB > L2: the K = 16 updates ran at ~10 TFLOP/s, memory-bound).
+// ---------------------------------------------------------------------------
+constexpr int NBB = 64;
+
+// One CTA per matrix: D^{-1} of the bb x bb block at (k0, k0) in shared memory, natural order.
+__global__ void __launch_bounds__(512) nat_block_inv_kernel(const zt* __restrict__ A, int64_t lda, int64_t bs, int n,
+                                                            int k0, int bb, const double* __restrict__ d0,
+                                                            double rel2, zt* __restrict__ Dt,
+                                                            zt* __restrict__ T, int* __restrict__ flag) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zt(*D)[NBB + 1] = reinterpret_cast<zt(*)[NBB + 1]>(smem_raw);  // [NBB][NBB + 1], dynamic (66.5 KB)
+  __shared__ zt prow[NBB], colk[NBB];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, b = blockIdx.x;
+  const zt* Ab = A + (int64_t)b * bs + (int64_t)k0 * lda + k0;
+  for (int e = tid; e < NBB * NBB; e += 512) {
+    const int i = e / NBB, j = e % NBB;
+    D[i][j] = (i < bb && j < bb) ? Ab[(int64_t)i * lda + j] : make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (int k = 0; k < bb; ++k) {
+    const zt pv = D[k][k];
+    const zt inv = zinv_fast(pv);
+    if (tid == 0) {
+      const double m = fma(pv.x, pv.x, pv.y * pv.y);
+      if (!(m > 0.0 && m >= rel2 * d0[(int64_t)b * n + k0 + k])) s_bad = 1;
+    }
+    if (tid < NBB) {
+      prow[tid] = tid == k ? inv : zmul(D[k][tid], inv);
+      colk[tid] = D[tid][k];
+    }
+    __syncthreads();
+    for (int e = tid; e < NBB * NBB; e += 512) {
+      const int i = e / NBB, j = e % NBB;
+      if (i == k) {
+        D[i][j] = prow[j];
+      } else if (j == k) {
+        const zt g = zmul(colk[i], inv);
+        D[i][j] = make_double2(-g.x, -g.y);
+      } else {
+        const zt f = colk[i], pr = prow[j];
+        zt v = D[i][j];
+        v.x = fma(-f.x, pr.x, v.x);
+        v.x = fma(f.y, pr.y, v.x);
+        v.y = fma(-f.x, pr.y, v.y);
+        v.y = fma(-f.y, pr.x, v.y);
+        D[i][j] = v;
+      }
+    }
+    __syncthreads();
+  }
+  zt* Db = Dt + (int64_t)b * NBB * NBB;
+  zt* Tb = T + (int64_t)b * n * NBB + (int64_t)k0 * NBB;  // T: [n][NBB] per matrix
+  for (int e = tid; e < bb * bb; e += 512) {
+    const int i = e / bb, j = e % bb;
+    const zt v = D[i][j];
+    Db[i * NBB + j] = v;
+    Tb[i * NBB + j] = make_double2(v.x - (i == j ? 1.0 : 0.0), v.y);
+  }
+  if (tid == 0 && s_bad) atomicExch(flag, 1);
+}
+
+void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st) {
+  char* wsp = static_cast<char*>(ws);
+  auto carve = [&](size_t bytes) {
+    void* p = wsp;
+    wsp += (bytes + 255) / 256 * 256;
+    return p;
+  };
+  double* d0 = static_cast<double*>(carve(sizeof(double) * (size_t)batch * n));
+  zt* Z = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * NBB * n));
+  zt* T = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * n * NBB));
+  zt* Dt = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * NBB * NBB));
+  {
+    ProfScope ps(K_GJ_AUX, 0.0, 24.0 * (double)batch * n, st);
+    nat_diag_kernel<<<dim3((n + 255) / 256, batch), 256, 0, st>>>(A, lda, bs, n, d0);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+  }
+  const double rel2 = knob(KN_NAT_PIVOT_REL) * 1e-4;
+  const int nblk = (n + NBB - 1) / NBB;
+  for (int q = 0; q < nblk; ++q) {
+    const int k0 = (int)((int64_t)q * n / nblk), bb = (int)((int64_t)(q + 1) * n / nblk) - k0;  // equal blocks
+    {
+      ProfScope ps(K_GJ_PANEL, 8.0 * (double)bb * bb * bb * batch, 32.0 * (double)bb * bb * batch, st);
+      constexpr int smem = (int)(sizeof(zt) * NBB * (NBB + 1));
+      static bool attr = false;
+      if (!attr) {
+        HPS_CUDA_CHECK(cudaFuncSetAttribute(nat_block_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr = true;
+      }
+      nat_block_inv_kernel<<<batch, 512, smem, st>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
+      HPS_CUDA_CHECK(cudaGetLastError());
+      count_launch();
+    }
+    {  // Z = A[K, :]
+      ZCopy c;
+      c.M = bb;
+      c.N = n;
+      c.batch = batch;
+      c.A.ptr = A + (int64_t)k0 * lda;
+      c.A.rs = lda;
+      c.A.bs = bs;
+      c.C.ptr = Z;
+      c.C.rs = n;
+      c.C.bs = (int64_t)NBB * n;
+      zcopy(c, st);
+    }
+    {  // T[rows outside K] = -A[rows outside K, K] D^{-1}
+      ZGemm g;
+      g.M = n - bb;
+      g.N = bb;
+      g.K = bb;
+      g.batch = batch;
+      g.A.ptr = A + k0;
+      g.A.rs = lda;
+      g.A.bs = bs;
+      g.A.rskip_at = k0;
+      g.A.rskip_len = bb;
+      g.B.ptr = Dt;
+      g.B.rs = NBB;
+      g.B.bs = (int64_t)NBB * NBB;
+      g.C.ptr = T;
+      g.C.rs = NBB;
+      g.C.bs = (int64_t)n * NBB;
+      g.C.rskip_at = k0;
+      g.C.rskip_len = bb;
+      g.alpha = make_double2(-1.0, 0.0);
+      if (n > bb) zgemm(g, st);
+    }
+    if (n > bb) {  // A[:, j not in K] += T Z[:, j]  (in place)
+      ZGemm g;
+      g.M = n;
+      g.N = n - bb;
+      g.K = bb;
+      g.batch = batch;
+      g.A.ptr = T;
+      g.A.rs = NBB;
+      g.A.bs = (int64_t)n * NBB;
+      g.B.ptr = Z;
+      g.B.rs = n;
+      g.B.bs = (int64_t)NBB * n;
+      g.B.cskip_at = k0;
+      g.B.cskip_len = bb;
+      g.Cin.ptr = A;
+      g.Cin.rs = lda;
+      g.Cin.bs = bs;
+      g.Cin.cskip_at = k0;
+      g.Cin.cskip_len = bb;
+      g.C.ptr = A;
+      g.C.rs = lda;
+      g.C.bs = bs;
+      g.C.cskip_at = k0;
+      g.C.cskip_len = bb;
+      g.beta = make_double2(1.0, 0.0);
+      zgemm(g, st);
+    }
+    {  // A[rows outside K, K] = T, A[K, K] = D^{-1}
+      ZCopy c[2];
+      c[0].M = n - bb;
+      c[0].N = bb;
+      c[0].batch = batch;
+      c[0].A.ptr = T;
+      c[0].A.rs = NBB;
+      c[0].A.bs = (int64_t)n * NBB;
+      c[0].A.rskip_at = k0;
+      c[0].A.rskip_len = bb;
+      c[0].C.ptr = A + k0;
+      c[0].C.rs = lda;
+      c[0].C.bs = bs;
+      c[0].C.rskip_at = k0;
+      c[0].C.rskip_len = bb;
+      c[1].M = bb;
+      c[1].N = bb;
+      c[1].batch = batch;
+      c[1].A.ptr = Dt;
+      c[1].A.rs = NBB;
+      c[1].A.bs = (int64_t)NBB * NBB;
+      c[1].C.ptr = A + (int64_t)k0 * lda + k0;
+      c[1].C.rs = lda;
+      c[1].C.bs = bs;
+      zcopy_multi(c, n > bb ? 2 : 1, st);
+    }
+  }
+}
+
+size_t zgj_natural_blocked_workspace_bytes(int n, int batch) {
+  return 4 * 256 + sizeof(double) * (size_t)batch * n + sizeof(zt) * (size_t)batch * (2 * (size_t)NBB * n + NBB * NBB);
+}
+
 size_t zgj_natural_workspace_bytes(int n, int batch) {
+  if (n >= knob(KN_NAT_BB_MIN)) return zgj_natural_blocked_workspace_bytes(n, batch);
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256 + 512 + sizeof(double) * (size_t)batch * n;
 }

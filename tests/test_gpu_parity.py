@@ -99,8 +99,10 @@ def test_natural_order_merge_inverses_all_levels():
     """nat_min = 14: every merge W with n3 >= 14 is inverted in natural order —
     every box's R and u vs the oracle, complex eta included; second pass with every natural-order
     attempt forced to fail its pivot check (the pivoted fallback), third with the relative pivot
-    threshold at 1.0 (any pivot smaller than its original diagonal falls back)."""
-    for knobs in ({"nat_min": 14}, {"nat_min": 14, "nat_force_fail": 1}, {"nat_min": 14, "nat_pivot_rel": 10000}):
+    threshold at 1.0 (any pivot smaller than its original diagonal falls back); the last two with
+    the 64-wide block steps (nat_bb_min = 20: every W with n3 >= 20, one to two blocks)."""
+    for knobs in ({"nat_min": 14}, {"nat_min": 14, "nat_force_fail": 1}, {"nat_min": 14, "nat_pivot_rel": 10000},
+                  {"nat_min": 14, "nat_bb_min": 20}, {"nat_min": 14, "nat_bb_min": 20, "nat_pivot_rel": 10000}):
         worst = 0.0
         with hps.debug_knobs(**knobs):
             for nx, ny, p, kappa, eta in [(4, 4, 8, 9.0, 9.0 - 2j), (8, 4, 6, 9.0, 9.0), (4, 8, 10, 20.0, 20.0)]:
