@@ -2080,109 +2080,6 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   for (int p = 0; p < P.npan; ++p) {
     const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
     WS_MARK(p, 0);
-    if (NAT) {
-      // ---------------- natural-order panel in block form ----------------
-      // The pivot rows of this panel are rows k0 .. k0 + w - 1, so the panel step is exact block
-      // algebra: D = M[K, K] is inverted by ONE warp in registers (lane j holds column j; no CTA
-      // barrier per pivot step), then T = -M[rows outside K, K] D^{-1} is a small DMMA product of
-      // all 16 warps; T[K] = D^{-1}.  Same T as the step-by-step panel, up to rounding.
-      if (wp == 0) {
-        // D in shared memory (the Z staging area is free during the panel), lane j owns column j;
-        // per step the rows are processed in chunks of 4: read column k, __syncwarp, update
-        zt(*Ds)[NB + 1] = reinterpret_cast<zt(*)[NB + 1]>(Zs);
-        for (int i = 0; i < NB; ++i)
-          if (lane < NB)
-            Ds[i][lane] = (lane < w && i < w) ? ldplain(M + (int64_t)(k0 + i) * lda + k0 + lane)
-                                              : make_double2(i == lane ? 1.0 : 0.0, 0.0);
-        __syncwarp();
-        bool bad = false;
-        const int jl = lane < NB ? lane : NB - 1;
-        for (int k = 0; k < w; ++k) {
-          const zt pv = Ds[k][k];
-          bad = bad || !(fma(pv.x, pv.x, pv.y * pv.y) >= 0.0025 * diag2[k0 + k]);
-          const zt inv = zinv_fast(pv);
-          const zt prj = jl == k ? inv : zmul(Ds[k][jl], inv);  // this lane's pivot-row entry, scaled
-          for (int i0 = 0; i0 < w; i0 += 4) {
-            zt f[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) f[t] = Ds[min(i0 + t, NB - 1)][k];
-            __syncwarp();
-            if (lane < w) {
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const int i = i0 + t;
-                if (i < w && i != k) {
-                  if (lane == k) {
-                    const zt g = zmul(f[t], inv);
-                    Ds[i][lane] = make_double2(-g.x, -g.y);
-                  } else {
-                    zt v = Ds[i][lane];
-                    v.x = fma(-f[t].x, prj.x, v.x);
-                    v.x = fma(f[t].y, prj.y, v.x);
-                    v.y = fma(-f[t].x, prj.y, v.y);
-                    v.y = fma(-f[t].y, prj.x, v.y);
-                    Ds[i][lane] = v;
-                  }
-                }
-              }
-            }
-            __syncwarp();
-          }
-          if (lane < w) Ds[k][lane] = prj;
-          __syncwarp();
-        }
-        for (int i = 0; i < w; ++i)
-          if (lane < NB) Ts[(k0 + i) * NB + lane] = lane < w ? Ds[i][lane] : make_double2(0.0, 0.0);
-        if (lane == 0 && bad) s_bad = 1;
-      }
-      __syncthreads();
-      if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
-      // T[i, :] = -M[i, K] D^{-1} for rows i outside K (D^{-1} = Ts rows K), DMMA m8n8k4
-      {
-        const int nunits = MT * 4;
-        for (int u = wp; u < nunits; u += 16) {
-          const int mt = u >> 2, ct = u & 3;
-          const int ra = mt * 8 + (lane >> 2);  // A fragment row, C fragment row
-          const bool rin = ra < n && !(ra >= k0 && ra < k0 + w);
-          double tr[2] = {0.0, 0.0}, ti[2] = {0.0, 0.0};
-#pragma unroll
-          for (int k4 = 0; k4 < NB / 4; ++k4) {
-            if (k4 * 4 < w) {
-              const int ka = k4 * 4 + (lane & 3);
-              zt av = (ra < n && ka < w) ? ldplain(M + (int64_t)ra * lda + k0 + ka) : make_double2(0.0, 0.0);
-              av = make_double2(-av.x, -av.y);
-              const int kb = k4 * 4 + (lane & 3), nb_ = ct * 8 + (lane >> 2);
-              const zt bv = (kb < w && nb_ < w) ? Ts[(k0 + kb) * NB + nb_] : make_double2(0.0, 0.0);
-              dmma884(tr[0], tr[1], av.x, bv.x);
-              dmma884(ti[0], ti[1], av.x, bv.y);
-              dmma884(tr[0], tr[1], -av.y, bv.y);
-              dmma884(ti[0], ti[1], av.y, bv.x);
-            }
-          }
-          if (rin) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int cc = ct * 8 + (lane & 3) * 2 + h;
-              if (cc < NB) Ts[ra * NB + cc] = cc < w ? make_double2(tr[h], ti[h]) : make_double2(0.0, 0.0);
-            }
-          }
-          if (ra < mtr && ra >= n) {  // padding rows of T stay zero
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int cc = ct * 8 + (lane & 3) * 2 + h;
-              if (cc < NB) Ts[ra * NB + cc] = make_double2(0.0, 0.0);
-            }
-          }
-        }
-      }
-      __syncthreads();
-      // the panel columns of M <- T (in place)
-      for (int e = tid; e < n * w; e += 512) {
-        const int i = e / w, j = e - i * w;
-        M[(int64_t)i * lda + k0 + j] = Ts[i * NB + j];
-      }
-      WS_MARK(p, 1);
-    } else {
     // ---------------- panel: w pivot steps on the n x w panel ----------------
     zt a[2][CPT];
 #pragma unroll
@@ -2234,6 +2131,10 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
             }
           }
           __syncthreads();
+          if (NAT && tid == 0) {
+            const zt pv = prow4[par][kk];
+            if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 0.0025 * diag2[k])) s_bad = 1;
+          }
           if (warp_live) {
             const zt inv = zinv_fast(prow4[par][kk]);
             zt g[2];
@@ -2283,7 +2184,10 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
           if (j < w && rq[q] < n) M[(int64_t)rq[q] * lda + k0 + j] = a[q][c];
         }
       }
-    }  // pivoted panel
+    if (NAT) {
+      __syncthreads();
+      if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
+    }
     if (p + 1 == P.npan && nv == 0) break;
     // ---------------- update: C(i, J) = [i not a pivot of p] C(i, J) + T(i,:) Z(:, J) -------------
     for (int v = tid; v < nv + 16; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;

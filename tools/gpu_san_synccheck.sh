@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 1700 compute-sanitizer --tool synccheck --target-processes all --log-file gpurun_out/san_synccheck.log \
+  python tools/sanitize_case.py > gpurun_out/san_synccheck_stdout.txt 2>&1
+echo "rc=$?" >> gpurun_out/san_synccheck_stdout.txt
