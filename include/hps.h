@@ -28,6 +28,10 @@
  * Input pointers are borrowed for the duration of the call; they may be host
  * or device (CUDA-visible) memory — the library asks the driver which.
  * Output buffers are caller-allocated, host or device.
+ * Ordering: without hps_opts.stream the library works on a non-blocking stream
+ * of its own that waits for NO other stream: device inputs must be complete
+ * when a call is made (the Python layer synchronises torch's current stream
+ * first).  With hps_opts.stream, everything is ordered on the caller's stream.
  *
  * Errors: every int-returning call returns 0 or a negative HPS_E* code; the
  * message of the last failure on the calling thread is hps_last_error().  No
@@ -323,7 +327,7 @@ int hps_release_cache(void);
 /* Debug and tuning knobs (process-wide; the library reads no environment variables).  `name` is
  * one of: debug_alloc, big_cache, side, side_solve, nat_min, nat_max, nat_force_fail, dgj_pivot,
  * dgj_force_bad, dgj_rpt, lr_trace, gemv_short, gemv_k16, trace, gemm_smallk, gj, seq_pivot,
- * nat_w, nat_lpr, natc, natb, nat_pivot_rel, nat_bb_min (meanings in csrc/hps_internal.cuh).  The *_force_*
+ * nat_w, nat_lpr, natc, natb, nat_pivot_rel, nat_bb_min, gemm_group (meanings in csrc/hps_internal.cuh).  The *_force_*
  * and *_pivot knobs are FAULT INJECTION for the tests of the pivoted fallback paths: never set
  * them in production.  value -1 restores the default.  Returns 0 or HPS_EINVAL (unknown name). */
 int hps_debug_set(const char* name, int value);

@@ -2902,10 +2902,18 @@ __global__ void nat_diag_kernel(const zt* A, int64_t lda, int64_t bs, int n, dou
 // zgj_workspace_bytes(n, batch) for the blocked regime; *flag (device) is set to 1 when a pivot
 // failed the check — out is then not the inverse and A is destroyed (the caller keeps a copy).
 void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st);
+size_t zgj_natural_blocked_workspace_bytes(int n, int batch);
+
+// 64-wide block steps where the 16-column panels' K = 16 updates are memory-bound: n >= nat_bb_min,
+// or a level whose matrices (batch x n^2 x 16 B) exceed a quarter of L2 (C4's n3 = 448 level,
+// 64 x 3.2 MB, gains; C2's single n3 = 448 matrix stays in L2 and the 16-column panels win).
+bool use_block_steps(int n, int batch) {
+  return n >= knob(KN_NAT_BB_MIN) || (n >= 224 && sizeof(zt) * (double)batch * n * n >= 32.0 * (1 << 20));
+}
 
 void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
                         void* ws, int* flag, cudaStream_t st) {
-  if (n >= knob(KN_NAT_BB_MIN)) {  // in place in A, then copied out
+  if (use_block_steps(n, batch)) {  // in place in A, then copied out
     zgj_invert_natural_blocked(A, lda, bs, n, batch, ws, flag, st);
     ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)batch * n * n, st);
     if (lda == n && bs == (int64_t)n * n && ldo == n && obs == (int64_t)n * n) {
@@ -3226,7 +3234,7 @@ size_t zgj_natural_blocked_workspace_bytes(int n, int batch) {
 }
 
 size_t zgj_natural_workspace_bytes(int n, int batch) {
-  if (n >= knob(KN_NAT_BB_MIN)) return zgj_natural_blocked_workspace_bytes(n, batch);
+  if (use_block_steps(n, batch)) return zgj_natural_blocked_workspace_bytes(n, batch);
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256 + 512 + sizeof(double) * (size_t)batch * n;
 }

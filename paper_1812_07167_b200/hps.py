@@ -142,6 +142,20 @@ def _ptr(a, nelem, what):
     return a.ctypes.data
 
 
+def _torch_ready(*arrays, stream=None):
+    """Device inputs must be complete when the library reads them on its own stream: if any
+    argument is a CUDA torch tensor and the handle does not order its work on torch's stream,
+    wait for torch's current stream first (ADVICE r1: a torch.stack still running on torch's
+    stream was read by the library's non-blocking stream)."""
+    if stream is not None:
+        return
+    for a in arrays:
+        if a is not None and hasattr(a, "is_cuda") and a.is_cuda:
+            import torch
+            torch.cuda.current_stream(a.device).synchronize()
+            return
+
+
 def grid(x0, x1, y0, y1, nx, ny):
     return hps_grid(x0, x1, y0, y1, nx, ny)
 
@@ -390,6 +404,8 @@ class Solver:
         h = C.c_void_p()
         cp = _ptr(c, self.nleaf * p * p, "c_samples")
         self._c = c   # keep alive during the call
+        self._stream = st
+        _torch_ready(c, stream=st)
         _check(lib().hps_build(C.byref(g), p, p - 2, float(kappa), hps_c128(eta.real, eta.imag), cp,
                                C.byref(opts), C.byref(h)))
         self.h = h
@@ -403,6 +419,7 @@ class Solver:
                 u = torch.empty((nrhs, self.nleaf, self.nt), dtype=torch.complex128, device=t.device)
             else:
                 u = np.zeros((nrhs, self.nleaf, self.nt), complex)
+        _torch_ready(s, t, u, stream=self._stream)
         _check(lib().hps_solve(self.h, nrhs, _ptr(s, nrhs * self.nleaf * self.ni, "s"),
                                _ptr(t, nrhs * self.nb_root, "t"), _ptr(u, nrhs * self.nleaf * self.nt, "u")))
         return u
@@ -415,6 +432,7 @@ class Solver:
         """Upward pass only; returns the root's outgoing particular data [nrhs][nb_root]."""
         if h_root is None:
             h_root = _empty_like_ref(s if s is not None else np.zeros(1, complex), (nrhs, self.nb_root))
+        _torch_ready(s, h_root, stream=self._stream)
         _check(lib().hps_solve_up(self.h, nrhs, _ptr(s, nrhs * self.nleaf * self.ni, "s"),
                                   _ptr(h_root, nrhs * self.nb_root, "h_root")))
         return h_root
@@ -423,6 +441,7 @@ class Solver:
         nrhs = int(t.shape[0])
         if u is None:
             u = _empty_like_ref(t, (nrhs, self.nleaf, self.nt))
+        _torch_ready(t, u, stream=self._stream)
         _check(lib().hps_solve_down(self.h, nrhs, _ptr(t, nrhs * self.nb_root, "t"),
                                     _ptr(u, nrhs * self.nleaf * self.nt, "u")))
         return u
@@ -496,6 +515,7 @@ class TopSolver:
                         int(boundary_basis))
         eta = complex(eta)
         h = C.c_void_p()
+        _torch_ready(R_sub)
         _check(lib().hps_build_top(C.byref(g), p, p - 2, float(kappa), hps_c128(eta.real, eta.imag), depth,
                                    _ptr(R_sub, self.nsub * self.nb_sub ** 2, "R_sub"), C.byref(opts), C.byref(h)))
         self.h = h
@@ -505,6 +525,7 @@ class TopSolver:
         nrhs = int(t_root.shape[0])
         if t_sub is None:
             t_sub = _empty_like_ref(t_root, (self.nsub, nrhs, self.nb_sub))
+        _torch_ready(h_sub, t_root, t_sub)
         _check(lib().hps_solve_top(self.h, nrhs, _ptr(h_sub, self.nsub * nrhs * self.nb_sub, "h_sub"),
                                    _ptr(t_root, nrhs * self.nb_root, "t_root"),
                                    _ptr(t_sub, self.nsub * nrhs * self.nb_sub, "t_sub")))
