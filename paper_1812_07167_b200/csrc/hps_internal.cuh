@@ -45,7 +45,7 @@ enum HpsKnob {
   KN_NATB,             // 1: blocked natural-order panel (DESIGN 3.10)
   KN_NAT_PIVOT_REL,    // natural-order W^{-1}: pivot accepted if |p|^2 >= REL/1e4 * |W_kk|^2
   KN_NAT_BB_MIN,       // natural-order W^{-1} with 64-wide block steps (D^{-1} kernel + GEMMs) for n >= this
-  KN_GEMM_GROUP,       // GEMM tile order: row blocks per group (1 = row-major)
+  KN_LEAF_PANEL,       // complex leaf Schur inverse, natural order: 0 step-by-step panels, 1 block form
   KN_COUNT
 };
 int knob(HpsKnob k);
@@ -114,7 +114,6 @@ struct ZGemm {
   zt alpha = {1.0, 0.0};
   zt beta = {0.0, 0.0};
   zt diag = {0.0, 0.0};
-  int group_m = 1;  // tile order: row blocks per group (zgemm.cu)
 };
 
 void zgemm(const ZGemm& g, cudaStream_t st);

@@ -59,16 +59,11 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / C::NWN, wn = warp % C::NWN;
-  // Optional grouped tile order (L2): consecutive CTAs sweep a group of GM row blocks column by
-  // column, so the CTAs in flight share a few A row blocks and B column blocks instead of streaming
-  // all of B once per row block.  GM = 16 cut the C4 GEMM DRAM traffic 1134 -> 468 GB per step but
-  // made the step 8 % SLOWER (merges 993 -> 1098 ms): the products are compute-bound and the
-  // row-major order keeps the in-flight CTAs on one A row block.
-  const int tilesN = (g.N + BN - 1) / BN, tilesM = (g.M + BM - 1) / BM;
-  const int GM = g.group_m;  // 1: row-major tile order (measured fastest at C4; knob gemm_group)
-  const int per_group = GM * tilesN, grp = blockIdx.x / per_group, first_m = grp * GM;
-  const int gm = min(tilesM - first_m, GM), local = blockIdx.x - grp * per_group;
-  const int m0 = (first_m + local % gm) * BM, n0 = (local / gm) * BN;
+  // Row-major tile order.  A grouped order (GM = 16 row blocks swept column by column) cut the C4
+  // GEMM DRAM traffic 1134 -> 468 GB per step but cost registers: the 64 x 32 tile kernel went
+  // 166 -> 180 registers, 3 -> 2 CTAs per SM, and the C4 merges 993 -> 1098 ms (round 2).
+  const int tilesN = (g.N + BN - 1) / BN;
+  const int m0 = (blockIdx.x / tilesN) * BM, n0 = (blockIdx.x % tilesN) * BN;
 
   // Fixed per-thread load coordinates: A column (k) and B column (n) are fixed across the
   // unrolled iterations; A rows / B rows step by NT/BK and NT/BN.
@@ -560,10 +555,8 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
   }
 }
 
-void zgemm_impl(const ZGemm& g0, cudaStream_t st) {
-  if (g0.M <= 0 || g0.N <= 0 || g0.batch <= 0) return;
-  ZGemm g = g0;
-  g.group_m = std::max(1, knob(KN_GEMM_GROUP));
+void zgemm_impl(const ZGemm& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return;
   const double mn = (double)g.M * g.N, bt = (double)g.batch;
   // N <= 4 runs the GEMV kernel: bound by HBM (the A operand is read once), its own class
   const bool gemv = (g_zgemm_force < 0 && g.N <= 4) || g_zgemm_force == 9;

@@ -1128,6 +1128,7 @@ struct WsFinish {
   const int* leaf_nat;   // heap leaf -> natural leaf
   int leaf0;             // heap index of batch entry 0
   double kappa2;
+  int blockpanel = 0;    // natural-order panels in block form (knob leaf_panel, DESIGN 3.12)
 };
 
 __host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16, == 2 (mod 8)
@@ -2028,6 +2029,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   zt* Ts = reinterpret_cast<zt*>(smem_raw);  // [mtr][NB]
   zt* Zs = Ts + (size_t)mtr * NB;            // [NB][zs]
   __shared__ zt prow4[2][NB];
+  __shared__ zt pinv2[2];
   __shared__ __align__(16) unsigned wkey[2][16];
   __shared__ int pstep[256], plist[256], colmap[WS_NMAX + 16];
   __shared__ double diag2[NAT ? 256 : 1];  // |S_kk|^2 of the assembled S (NAT)
@@ -2080,6 +2082,105 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   for (int p = 0; p < P.npan; ++p) {
     const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
     WS_MARK(p, 0);
+    if (NAT && fin.blockpanel) {
+      // ---- natural-order panel in block form (knob leaf_panel = 1): the pivot rows are rows
+      // k0 .. k0 + w - 1, so D = M[K, K] is inverted by warps 0-3 (7 rows each, lane j holds column
+      // j in registers, one 128-thread named barrier per step), then T = -M[rows outside K, K] D^{-1}
+      // runs on DMMA in all 16 warps from the panel staged in shared memory; T[K] = D^{-1}. ----
+      for (int e = tid; e < mtr * NB; e += 512) {  // stage the panel (zero padding rows / columns)
+        const int i = e / NB, j = e - i * NB;
+        Ts[e] = (i < n && j < w) ? ldplain(M + (int64_t)i * lda + k0 + j) : make_double2(0.0, 0.0);
+      }
+      __syncthreads();
+      zt(*Dv)[NB + 1] = reinterpret_cast<zt(*)[NB + 1]>(Zs);  // D^{-1} (Z staging area is free now)
+      if (wp < 4) {
+        constexpr int RW = NB / 4;  // rows per warp
+        zt d[RW];
+        const int jl = lane < NB ? lane : 0;
+#pragma unroll
+        for (int t = 0; t < RW; ++t) {
+          const int r = wp * RW + t;
+          d[t] = (r < w && jl < w) ? Ts[(k0 + r) * NB + jl] : make_double2(r == jl ? 1.0 : 0.0, 0.0);
+        }
+        for (int k = 0; k < w; ++k) {
+          const int vk = k / RW, tk = k - vk * RW, par = k & 1;
+          if (wp == vk) {
+            zt dk = d[0];
+#pragma unroll
+            for (int t = 1; t < RW; ++t)
+              if (t == tk) dk = d[t];
+            const zt pv = make_double2(__shfl_sync(0xffffffffu, dk.x, k), __shfl_sync(0xffffffffu, dk.y, k));
+            const zt inv = zinv_fast(pv);
+            if (lane < NB) prow4[par][lane] = lane == k ? inv : zmul(dk, inv);
+            if (lane == 0) {
+              pinv2[par] = inv;
+              if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 0.0025 * diag2[k0 + k])) s_bad = 1;
+            }
+          }
+          bar_sync_n(BAR_PANEL, 128);
+          const zt prj = prow4[par][jl], inv = pinv2[par];
+#pragma unroll
+          for (int t = 0; t < RW; ++t) {
+            const int r = wp * RW + t;
+            const zt f = make_double2(__shfl_sync(0xffffffffu, d[t].x, k), __shfl_sync(0xffffffffu, d[t].y, k));
+            if (r == k) {
+              d[t] = prj;
+            } else if (lane == k) {
+              const zt g = zmul(f, inv);
+              d[t] = make_double2(-g.x, -g.y);
+            } else {
+              d[t].x = fma(-f.x, prj.x, d[t].x);
+              d[t].x = fma(f.y, prj.y, d[t].x);
+              d[t].y = fma(-f.x, prj.y, d[t].y);
+              d[t].y = fma(-f.y, prj.x, d[t].y);
+            }
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < RW; ++t)
+          if (lane < NB) Dv[wp * RW + t][lane] = d[t];
+      }
+      __syncthreads();
+      if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
+      // T[r, :] = -M[r, K] D^{-1} for rows r outside K, D^{-1} for rows in K (one row tile per unit)
+      for (int mt = wp; mt < MT; mt += 16) {
+        const int r = mt * 8 + (lane >> 2);
+        zt af[NB / 4];
+#pragma unroll
+        for (int k4 = 0; k4 < NB / 4; ++k4) af[k4] = Ts[r * NB + k4 * 4 + (lane & 3)];
+        const bool inK = r >= k0 && r < k0 + w;
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) {
+          double tr[2] = {0.0, 0.0}, ti[2] = {0.0, 0.0};
+#pragma unroll
+          for (int k4 = 0; k4 < NB / 4; ++k4) {
+            const int kb = k4 * 4 + (lane & 3), cb = ct * 8 + (lane >> 2);
+            const zt bv = (kb < w && cb < w) ? Dv[kb][cb] : make_double2(0.0, 0.0);
+            dmma884(tr[0], tr[1], -af[k4].x, bv.x);
+            dmma884(ti[0], ti[1], -af[k4].x, bv.y);
+            dmma884(tr[0], tr[1], af[k4].y, bv.y);
+            dmma884(ti[0], ti[1], -af[k4].y, bv.x);
+          }
+          __syncwarp();  // every lane's A fragments of this row tile are read before any write
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = ct * 8 + (lane & 3) * 2 + h;
+            if (cc < NB) {
+              zt v = cc < w ? make_double2(tr[h], ti[h]) : make_double2(0.0, 0.0);
+              if (inK) v = cc < w ? Dv[r - k0][cc] : make_double2(0.0, 0.0);
+              if (r >= n) v = make_double2(0.0, 0.0);
+              Ts[r * NB + cc] = v;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      for (int e = tid; e < n * w; e += 512) {  // the panel columns of M <- T (in place)
+        const int i = e / w, j = e - i * w;
+        M[(int64_t)i * lda + k0 + j] = Ts[i * NB + j];
+      }
+      WS_MARK(p, 1);
+    } else {
     // ---------------- panel: w pivot steps on the n x w panel ----------------
     zt a[2][CPT];
 #pragma unroll
@@ -2188,6 +2289,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       __syncthreads();
       if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
     }
+    }  // panel form
     if (p + 1 == P.npan && nv == 0) break;
     // ---------------- update: C(i, J) = [i not a pivot of p] C(i, J) + T(i,:) Z(:, J) -------------
     for (int v = tid; v < nv + 16; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
@@ -2753,7 +2855,7 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
     auto kern = choose_regime(n, batch) == REG_SEQ ? zgj_seq_kernel : zgj_ws_kernel;
     kern<<<nbatch, 512, ws_smem(n), st>>>(
         S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
-        info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2});
+        info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2, knob(KN_LEAF_PANEL)});
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
   }
