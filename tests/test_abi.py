@@ -102,3 +102,36 @@ def test_rep_actions_match_survey_table():
     ra5 = hps.rep_actions(g5, 16)
     assert len(ra5) == 20 and ra5[0] == (196, 524288)
     assert [n for n, _ in ra5[-5:]] == [1792, 3584, 3584, 7168, 7168]   # levels 15-19
+
+
+def test_opts_layout_and_multi_gpu_validation(L):
+    """hps_opts matches include/hps.h (7 int32 + n_gpus, then nccl_comm, stream, comm pointers);
+    the multi-GPU fields are validated before any device work: n_gpus > 1 without a communicator,
+    and a non-power-of-two virtual group, are HPS_EINVAL."""
+    assert C.sizeof(hps.hps_opts) == 8 * 4 + 3 * C.sizeof(C.c_void_p)
+    assert hps.hps_opts.nccl_comm.offset == 32 and hps.hps_opts.comm.offset == 48
+    g = hps.grid(0, 1, 0, 1, 2, 2)
+    c = np.ones(4 * 64, complex)
+    opts = hps.hps_opts(1, 0, -1, 0, 0, 0, 0, 2, None, None, None)
+    h = C.c_void_p()
+    rc = L.hps_build(C.byref(g), 8, 6, 1.0, hps.hps_c128(1.0, 0.0), c.ctypes.data, C.byref(opts), C.byref(h))
+    assert rc == -1 and not h.value and b"communicator" in L.hps_last_error()
+    grp = C.c_void_p()
+    assert L.hps_vcomm_create(3, C.byref(grp)) == -1
+    assert L.hps_sync(None) == -1
+
+
+def test_debug_knobs_roundtrip(L):
+    """Knobs are set only through hps_debug_set (no environment); -1 restores the default;
+    unknown names are HPS_EINVAL."""
+    v = C.c_int()
+    assert L.hps_debug_get(b"nat_min", C.byref(v)) == 0 and v.value == 200
+    assert L.hps_debug_set(b"nat_min", 14) == 0
+    assert L.hps_debug_get(b"nat_min", C.byref(v)) == 0 and v.value == 14
+    assert L.hps_debug_set(b"nat_min", -1) == 0
+    assert L.hps_debug_get(b"nat_min", C.byref(v)) == 0 and v.value == 200
+    assert L.hps_debug_set(b"no_such_knob", 1) == -1
+    src = open(os.path.join(os.path.dirname(hps.__file__), "csrc", "hps_api.cu")).read()
+    for f in ("zgj.cu", "zgemm.cu", "leaf.cu", "leaf_real.cu", "comm.cu"):
+        src += open(os.path.join(os.path.dirname(hps.__file__), "csrc", f)).read()
+    assert "getenv" not in src
