@@ -204,6 +204,36 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
 
     // Epilogue: C = alpha * acc + diag * [i == j]
     zt* Cb = g.C.ptr + zboff(g.C, b);
+    // Column-contiguous output (rs == 1: the solve writes u straight into the ABI layout, RHS
+    // outermost): the tile goes through shared memory so that each column is stored as BM
+    // consecutive elements instead of 16-byte pieces 0.26 GB apart.
+    constexpr bool kTr = BN * (BM + 1) <= 2 * (BM * AS + BK * BS);
+    if (kTr && g.C.rs == 1 && !Crm && !g.C.cmap && g.C.rskip_len == 0) {
+      zt* Ct = As;  // [BN][BM + 1]; the operand tiles are free (the K loop ended with a barrier)
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int lr = wm * C::TM * 8 + i * 8 + (lane >> 2);
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int lc = wn * C::TN * 8 + j * 8 + (lane & 3) * 2 + h;
+            zt v = zmul(g.alpha, make_double2(accr[i][j][h], acci[i][j][h]));
+            if (m0 + lr == n0 + lc) {
+              v.x += g.diag.x;
+              v.y += g.diag.y;
+            }
+            Ct[lc * (BM + 1) + lr] = v;
+          }
+      }
+      __syncthreads();
+      for (int e = tid; e < BM * BN; e += NT) {
+        const int lc = e / BM, lr = e - lc * BM, gi = m0 + lr, gj = n0 + lc;
+        if (gi < g.M && gj < g.N) Cb[(int64_t)gi + (int64_t)gj * g.C.cs] = Ct[lc * (BM + 1) + lr];
+      }
+      __syncthreads();  // Ct is the next batch entry's operand buffer
+      continue;
+    }
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
       const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
@@ -545,6 +575,7 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
     case 10: launch<64, 16, 16, 16>(g, st); return true;
     case 11: launch<128, 16, 32, 16>(g, st); return true;
     case 12: launch<64, 16, 32, 8>(g, st); return true;
+    case 13: launch<32, 16, 16, 16>(g, st); return true;
     case 9: {
       if (g.N == 1) launch_gemv<1>(g, st);
       else if (g.N <= 4) launch_gemv<4>(g, st);
@@ -580,6 +611,8 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
     launch<64, 8, 16, 8>(g, st);
   else if (g.N <= 16 && g.M > 16 && g.K >= 1024 && (int64_t)((g.M + 63) / 64) * g.batch < nsm)
     launch<16, 16, 8, 8>(g, st);    // long-K products of the top levels' solve: more, smaller CTAs
+  else if (g.N <= 16 && g.M > 16 && g.M <= 48)
+    launch<32, 16, 16, 16>(g, st);  // the low levels' solve products (n3 = 28, 42): less padding
   else if (g.N <= 16 && g.M > 16)
     launch<64, 16, 16, 16>(g, st);  // the solve sweeps at 16 right-hand sides: no half-empty tiles
   else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * nsm))

@@ -2456,9 +2456,8 @@ PanelPlan panel_plan(int n) {
   return PanelPlan{2, 16, 16, rp, sizeof(zt) * ((size_t)rp * 16 + 32) + 64 + sizeof(int) * rp};
 }
 
-bool use_small(int n, int batch) { return n <= 32; }
 bool use_fused(int n, int batch) { return n > 32 && n <= 256 && (batch >= 16 || n <= 128); }
-// HPS_GJ=fused|blocked forces the older paths (kernel comparisons in tools/gj_tune.py)
+// the gj knob (1 fused, 2 blocked, 3 warp-specialised) forces a kernel family (tools/gj_tune.py)
 }  // namespace
 int g_gj_mode_force = 0;
 // debug: timeline of CTA 0 of the next zgj_ws launch (on = 1 arms it; out[160] clock64 values)
@@ -2471,11 +2470,6 @@ void zgj_ws_trace(int on, long long* out) {
 namespace {
 int gj_mode_env() {
   return g_gj_mode_force ? g_gj_mode_force : knob(KN_GJ);
-}
-// measured (tools/gj_tune.py): the warp-specialised kernel wins for 100 <= n <= 200 at every batch size;
-// above that its panel phase (8 warps x 4 rows) outgrows the update
-bool use_ws(int n, int batch) {
-  return (gj_mode_env() == 0 && n >= 100 && n <= 200) || (gj_mode_env() == 3 && n > 32 && n <= WS_NMAX);
 }
 
 // ---------------------------------------------------------------------------

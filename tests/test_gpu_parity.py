@@ -460,7 +460,7 @@ def test_virtual_comm_selftest():
     assert all(dist.run_virtual(8, fn))
 
 
-@pytest.mark.parametrize("cfg", list(range(13)))
+@pytest.mark.parametrize("cfg", list(range(14)))
 @pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1),
                                          (70, 1, 300, 2), (33, 3, 45, 3)])
 def test_zgemm_configs(cfg, M, N, K, batch):
