@@ -40,10 +40,19 @@ def lagrange_matrix(src, dst):
     return L
 
 
-def gl_to_cheb(p):
-    """q x q matrix taking segment samples at the Gauss-Legendre nodes to the Chebyshev nodes."""
-    xi, _ = gl_nodes_weights(p - 2)
+def gl_to_cheb(p, q=None):
+    """(p - 2) x q matrix taking segment samples at the q Gauss-Legendre nodes (the degree-(q-1)
+    polynomial through them) to the segment's p - 2 Chebyshev nodes; q defaults to p - 2."""
+    xi, _ = gl_nodes_weights(p - 2 if q is None else q)
     return lagrange_matrix(xi, cheb_edge_nodes(p))
+
+
+def cheb_to_gl(p, q=None):
+    """q x (p - 2) matrix taking segment samples at the p - 2 Chebyshev nodes (the degree-(p-3)
+    polynomial through them) to the segment's q Gauss-Legendre nodes (GL edge representation,
+    the outgoing side).  For q = p - 2 it is the inverse of gl_to_cheb(p)."""
+    xi, _ = gl_nodes_weights(p - 2 if q is None else q)
+    return lagrange_matrix(cheb_edge_nodes(p), xi)
 
 
 def t_to_cheb(p, t_gl):
@@ -56,10 +65,11 @@ def t_to_cheb(p, t_gl):
     return np.einsum("jg,...sg->...sj", P, seg).reshape(t.shape)
 
 
-def root_boundary_gl(x0, x1, y0, y1, nx, ny, p):
+def root_boundary_gl(x0, x1, y0, y1, nx, ny, p, q=None):
     """Root boundary Gauss-Legendre node coordinates and outward normals, canonical order [S, E, N,
-    W], each leaf-edge segment in increasing coordinate (the segment layout of root_boundary)."""
-    q = p - 2
+    W], each leaf-edge segment in increasing coordinate (the segment layout of root_boundary);
+    q nodes per segment (default p - 2)."""
+    q = p - 2 if q is None else q
     xi, _ = gl_nodes_weights(q)
     hx, hy = (x1 - x0) / nx, (y1 - y0) / ny
     X, Y, NX, NY = [], [], [], []
@@ -80,5 +90,6 @@ def root_boundary_gl(x0, x1, y0, y1, nx, ny, p):
     return np.array(X), np.array(Y), np.array(NX), np.array(NY)
 
 
-__all__ = ["gl_nodes_weights", "cheb_edge_nodes", "lagrange_matrix", "gl_to_cheb", "t_to_cheb", "root_boundary_gl",
+__all__ = ["gl_nodes_weights", "cheb_edge_nodes", "lagrange_matrix", "gl_to_cheb", "cheb_to_gl", "t_to_cheb",
+           "root_boundary_gl",
            "root_boundary"]

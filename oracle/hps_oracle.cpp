@@ -345,17 +345,19 @@ struct Box {
   int vertical = 0;    // split orientation for non-leaves (1 = alpha west | beta east)
 };
 
-// Canonical boundary key list: [S, E, N, W], each edge increasing coordinate.
-static std::vector<Key> box_keys(const Box& b, int p) {
+// Canonical boundary key list: [S, E, N, W], each edge increasing coordinate; ne nodes per
+// leaf-edge segment (p - 2 Chebyshev nodes, or the q Gauss-Legendre nodes of the GL edge
+// representation, oracle_build_gl).
+static std::vector<Key> box_keys(const Box& b, int ne) {
   std::vector<Key> K;
   for (int i = b.i0; i < b.i1; ++i)
-    for (int k = 1; k <= p - 2; ++k) K.push_back(make_key(0, b.j0, i, k));  // S
+    for (int k = 1; k <= ne; ++k) K.push_back(make_key(0, b.j0, i, k));  // S
   for (int j = b.j0; j < b.j1; ++j)
-    for (int k = 1; k <= p - 2; ++k) K.push_back(make_key(1, b.i1, j, k));  // E
+    for (int k = 1; k <= ne; ++k) K.push_back(make_key(1, b.i1, j, k));  // E
   for (int i = b.i0; i < b.i1; ++i)
-    for (int k = 1; k <= p - 2; ++k) K.push_back(make_key(0, b.j1, i, k));  // N
+    for (int k = 1; k <= ne; ++k) K.push_back(make_key(0, b.j1, i, k));  // N
   for (int j = b.j0; j < b.j1; ++j)
-    for (int k = 1; k <= p - 2; ++k) K.push_back(make_key(1, b.i0, j, k));  // W
+    for (int k = 1; k <= ne; ++k) K.push_back(make_key(1, b.i0, j, k));  // W
   return K;
 }
 
@@ -525,7 +527,7 @@ int oracle_root_boundary(double x0, double x1, double y0, double y1, int nx, int
   std::vector<double> xi = cheb_nodes(p);
   const double hx = (x1 - x0) / nx, hy = (y1 - y0) / ny;
   Box root{0, nx, 0, ny, 0, false, 0};
-  std::vector<Key> K = box_keys(root, p);
+  std::vector<Key> K = box_keys(root, p - 2);
   for (size_t j = 0; j < K.size(); ++j) {
     const int vertical = (int)(K[j] >> 60), line = (int)((K[j] >> 36) & 0xFFFFFF);
     const int seg = (int)((K[j] >> 12) & 0xFFFFFF), k = (int)(K[j] & 0xFFF);
@@ -583,7 +585,7 @@ int oracle_merge(int p, int cnx, int cny, int vertical, const cplx* Ra, const cp
   Box a{0, cnx, 0, cny, 1, false, 0}, b = a, t{0, cnx, 0, cny, 0, false, vertical};
   if (vertical) { b.i0 = cnx; b.i1 = 2 * cnx; t.i1 = 2 * cnx; }
   else { b.j0 = cny; b.j1 = 2 * cny; t.j1 = 2 * cny; }
-  std::vector<Key> ka = box_keys(a, p), kb = box_keys(b, p), kt = box_keys(t, p);
+  std::vector<Key> ka = box_keys(a, p - 2), kb = box_keys(b, p - 2), kt = box_keys(t, p - 2);
   Mat RA((int)ka.size(), (int)ka.size()), RB((int)kb.size(), (int)kb.size());
   std::copy(Ra, Ra + RA.a.size(), RA.a.begin());
   std::copy(Rb, Rb + RB.a.size(), RB.a.begin());
@@ -621,10 +623,44 @@ int oracle_tree_info(int nx, int ny, int p, int64_t* nboxes, int* depth) {
   return 0;
 }
 
-// Algorithm 1 (precomputation).  c: [nleaf natural (iy, ix)][p*p].
-void* oracle_build(double x0, double x1, double y0, double y1, int nx, int ny, int p, double kappa,
-                   double eta_re, double eta_im, const cplx* c, int keep_all_R) {
+}  // extern "C"
+
+// Gauss-Legendre edge representation (beyond the paper, which samples every
+// leaf edge at its p - 2 corner-free Chebyshev nodes; the ItI representation it
+// cites, uses q Gauss-Legendre nodes per edge).  Incoming data f on an edge
+// is given at the q GL nodes; the Chebyshev leaf sees P f (P: (p-2) x q, the degree-(q-1)
+// Lagrange interpolant through the GL nodes evaluated at the edge's Chebyshev nodes) and its
+// outgoing data g at the Chebyshev nodes is returned as Q g (Q: q x (p-2), the degree-(p-3)
+// interpolant through the Chebyshev nodes evaluated at the GL nodes).  With the edge maps
+// block-diagonal over [S, E, N, W]:  Psi <- Psi Pblk,  R <- Qblk R Pblk,  Gamma <- Qblk Gamma.
+static Mat edge_blocks(const double* A, int m, int n) {  // 4 copies of the m x n edge map
+  Mat B(4 * m, 4 * n);
+  for (int e = 0; e < 4; ++e)
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) B(e * m + i, e * n + j) = cplx(A[(size_t)i * n + j], 0.0);
+  return B;
+}
+
+static void leaf_to_gl(LeafOps& L, const Mat& Pblk, const Mat& Qblk) {
+  L.Psi = matmul(L.Psi, Pblk);
+  L.R = matmul(matmul(Qblk, L.R), Pblk);
+  L.Gamma = matmul(Qblk, L.Gamma);
+}
+
+// Algorithm 1 (precomputation).  c: [nleaf natural (iy, ix)][p*p].  qe = 0: the paper's
+// Chebyshev edges; qe > 0: the GL edge representation with the maps P ((p-2) x qe) and
+// Qm (qe x (p-2)), row-major.
+static void* build_impl(double x0, double x1, double y0, double y1, int nx, int ny, int p, int qe,
+                        const double* P, const double* Qm, double kappa, double eta_re, double eta_im,
+                        const cplx* c, int keep_all_R) {
   if (p < 4 || nx < 1 || ny < 1 || !(x1 > x0) || !(y1 > y0)) { g_err = "invalid arguments"; return nullptr; }
+  if (qe < 0 || (qe > 0 && (!P || !Qm))) { g_err = "invalid GL edge maps"; return nullptr; }
+  const int ne = qe > 0 ? qe : p - 2;
+  Mat Pblk, Qblk;
+  if (qe > 0) {
+    Pblk = edge_blocks(P, p - 2, qe);
+    Qblk = edge_blocks(Qm, qe, p - 2);
+  }
   auto t0 = std::chrono::steady_clock::now();
   Oracle* O = new Oracle();
   O->x0 = x0; O->x1 = x1; O->y0 = y0; O->y1 = y1;
@@ -636,7 +672,7 @@ void* oracle_build(double x0, double x1, double y0, double y1, int nx, int ny, i
   O->merge.resize(nbox);
   O->R.resize(nbox);
   O->keys.resize(nbox);
-  for (int tau = 1; tau < nbox; ++tau) O->keys[tau] = box_keys(O->T.box[tau], p);
+  for (int tau = 1; tau < nbox; ++tau) O->keys[tau] = box_keys(O->T.box[tau], ne);
   const double hx = (x1 - x0) / nx, hy = (y1 - y0) / ny;
   int fail = 0;
   // Algorithm 1 loops tau = N_boxes ... 1; boxes of one level are independent
@@ -656,6 +692,7 @@ void* oracle_build(double x0, double x1, double y0, double y1, int nx, int ny, i
           fail = tau;
           continue;
         }
+        if (qe > 0) leaf_to_gl(O->leaf[tau], Pblk, Qblk);
         O->R[tau] = O->leaf[tau].R;
       } else {
         const int a = 2 * tau, bb = 2 * tau + 1;
@@ -680,6 +717,22 @@ void* oracle_build(double x0, double x1, double y0, double y1, int nx, int ny, i
   }
   O->build_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return O;
+}
+
+extern "C" {
+
+void* oracle_build(double x0, double x1, double y0, double y1, int nx, int ny, int p, double kappa,
+                   double eta_re, double eta_im, const cplx* c, int keep_all_R) {
+  return build_impl(x0, x1, y0, y1, nx, ny, p, 0, nullptr, nullptr, kappa, eta_re, eta_im, c, keep_all_R);
+}
+
+// The same tree with the Gauss-Legendre edge representation: qe nodes per leaf edge, P and Qm
+// the edge maps above (the caller computes them; tests/ pins them).  t of oracle_solve is then
+// given at the root's GL nodes, [nrhs][2 (nx + ny) qe].
+void* oracle_build_gl(double x0, double x1, double y0, double y1, int nx, int ny, int p, int qe, const double* P,
+                      const double* Qm, double kappa, double eta_re, double eta_im, const cplx* c, int keep_all_R) {
+  if (qe < 1) { g_err = "qe < 1"; return nullptr; }
+  return build_impl(x0, x1, y0, y1, nx, ny, p, qe, P, Qm, kappa, eta_re, eta_im, c, keep_all_R);
 }
 
 double oracle_build_seconds(void* h) { return h ? ((Oracle*)h)->build_seconds : -1; }
@@ -826,11 +879,11 @@ int oracle_global_dense(double x0, double x1, double y0, double y1, int nx, int 
       const int l = ly * nx + lx;
       D[l] = leaf_disc(p, hx, hy, kappa, eta, c + (size_t)l * p * p);
       Box b{lx, lx + 1, ly, ly + 1, 0, true, 0};
-      K[l] = box_keys(b, p);
+      K[l] = box_keys(b, p - 2);
       for (int j = 0; j < nb; ++j) owners[K[l][j]].push_back({l, j});
     }
   Box root{0, nx, 0, ny, 0, false, 0};
-  std::vector<Key> kr = box_keys(root, p);
+  std::vector<Key> kr = box_keys(root, p - 2);
   std::map<Key, int> rootpos;
   for (size_t j = 0; j < kr.size(); ++j) rootpos[kr[j]] = (int)j;
   const int nbr = (int)kr.size();

@@ -46,6 +46,8 @@ def lib():
         L.oracle_tree_info.argtypes = [i32, i32, i32, C.POINTER(i64), C.POINTER(i32)]
         L.oracle_build.argtypes = [d, d, d, d, i32, i32, i32, d, d, d, dp, i32]
         L.oracle_build.restype = vp
+        L.oracle_build_gl.argtypes = [d, d, d, d, i32, i32, i32, i32, dp, dp, d, d, d, dp, i32]
+        L.oracle_build_gl.restype = vp
         L.oracle_solve.argtypes = [vp, i32, dp, dp, dp]
         L.oracle_box_nb.argtypes = [vp, i64]
         L.oracle_box_nb.restype = i64
@@ -128,9 +130,11 @@ def leaf_disc(p, hx, hy, kappa, eta, c):
     return out
 
 
-def merge(p, cnx, cny, vertical, Ra, Rb):
-    """Standalone merge of two congruent children (cnx x cny leaves each)."""
-    q = p - 2
+def merge(p, cnx, cny, vertical, Ra, Rb, q=None):
+    """Standalone merge of two congruent children (cnx x cny leaves each); q boundary nodes per
+    leaf edge (default p - 2; the merge sees only the edge node count)."""
+    q = p - 2 if q is None else q
+    p = q + 2
     nba = 2 * (cnx + cny) * q
     n3 = (cny if vertical else cnx) * q
     ntau = 2 * (nba - n3)
@@ -162,12 +166,23 @@ def tree_info(nx, ny, p=4):
 class Oracle:
     """Algorithm 1 build + Algorithm 2 solve on host cores."""
 
-    def __init__(self, x0, x1, y0, y1, nx, ny, p, kappa, eta, c, keep_all_R=False):
+    def __init__(self, x0, x1, y0, y1, nx, ny, p, kappa, eta, c, keep_all_R=False, qe=None):
+        """qe: None for the paper's p - 2 Chebyshev nodes per leaf edge; an int for the
+        Gauss-Legendre edge representation with qe nodes per edge (oracle/gl.py maps; t of solve()
+        is then given at the root's GL nodes, gl.root_boundary_gl(..., q=qe))."""
         self.nx, self.ny, self.p = nx, ny, p
+        self.ne = p - 2 if qe is None else qe
         c = _c(c).reshape(nx * ny, p * p)
         eta = complex(eta)
-        self.h = lib().oracle_build(x0, x1, y0, y1, nx, ny, p, kappa, eta.real, eta.imag, _p(c),
-                                    int(keep_all_R))
+        if qe is None:
+            self.h = lib().oracle_build(x0, x1, y0, y1, nx, ny, p, kappa, eta.real, eta.imag, _p(c),
+                                        int(keep_all_R))
+        else:
+            from . import gl
+            P = np.ascontiguousarray(gl.gl_to_cheb(p, qe), dtype=np.float64)
+            Q = np.ascontiguousarray(gl.cheb_to_gl(p, qe), dtype=np.float64)
+            self.h = lib().oracle_build_gl(x0, x1, y0, y1, nx, ny, p, int(qe), _p(P), _p(Q), kappa, eta.real,
+                                           eta.imag, _p(c), int(keep_all_R))
         if not self.h:
             raise RuntimeError("oracle_build failed: " + lib().oracle_last_error().decode())
 
@@ -202,7 +217,7 @@ class Oracle:
 
     def leaf_ops(self, box):
         p = self.p
-        Psi = np.zeros((p * p - 4, 4 * p - 8), complex)
+        Psi = np.zeros((p * p - 4, 4 * self.ne), complex)
         Y = np.zeros((p * p - 4, (p - 2) ** 2), complex)
         _check(lib().oracle_export_leaf(self.h, box, _p(Psi), _p(Y)), "oracle_export_leaf")
         return Psi, Y
