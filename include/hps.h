@@ -93,11 +93,21 @@ typedef struct {
   int32_t boundary_basis; /* root boundary data t of hps_solve / hps_solve_top sampled at
                            0 (default): the q = p - 2 corner-free Chebyshev-Lobatto nodes of each
                              leaf edge (hps_root_boundary_nodes; the paper's scheme);
-                           1: the q Gauss-Legendre nodes of each leaf edge (hps_boundary_nodes_gl,
-                             same segment order): the library
-                             interpolates each segment's degree-(q-1) polynomial to its Chebyshev
-                             nodes.  u is always returned at the Chebyshev leaf nodes.
-                           Other values: HPS_EINVAL */
+                           1: the q = p - 2 Gauss-Legendre nodes of each leaf edge
+                             (hps_boundary_nodes_gl, same segment order; SURVEY 8(f) NEXT-2,
+                             DESIGN.md 3.9): the library interpolates each segment's degree-(q-1)
+                             polynomial to its Chebyshev nodes.
+                           2: the Gauss-Legendre EDGE representation (beyond the
+                             paper, which only cites it): q GL nodes on EVERY
+                             leaf edge, any 2 <= q <= p - 2 (the q argument of hps_build).  Leaf
+                             incoming data are interpolated from the q GL nodes to the edge's p - 2
+                             Chebyshev nodes (P), outgoing data from the Chebyshev nodes to the GL
+                             nodes (Q): R_leaf = Qblk R Pblk, Psi = Psi Pblk, so every merge works
+                             on q nodes per leaf edge; t is given at hps_boundary_nodes_glq(g, q),
+                             hps_export_R returns the GL-based maps, hps_export_leaf Psi Pblk
+                             ((p^2-4) x 4q).  Exact for solutions whose edge traces are polynomials
+                             of degree < q.
+                           u is always returned at the Chebyshev leaf nodes.  Other values: HPS_EINVAL */
   /* ---- multi-GPU and stream; zero-initialised = single GPU ---- */
   int32_t n_gpus;       /* 1, 2, 4, 8, ... (power of two): SPMD, one process (or virtual rank) per GPU;
                            0 = the communicator's size (1 without one) */
@@ -123,7 +133,8 @@ typedef struct {
  *  until the next level's all-gather).  With keep_root_R the root R is gathered at the end.
  *  g         : domain and leaf grid (nx, ny powers of two; leaves must be congruent rectangles).
  *  p         : Chebyshev points per leaf side, p >= 4.
- *  q         : boundary nodes per leaf edge; must equal p - 2 (corner-free scheme).
+ *  q         : boundary nodes per leaf edge; must equal p - 2 (corner-free scheme),
+ *              except with opts.boundary_basis = 2 (Gauss-Legendre edges): 2 <= q <= p - 2.
  *  kappa     : wavenumber, kappa >= 0 (PAPER.md:227 has kappa > 0; 0 is allowed).
  *  eta       : impedance parameter, Re(eta) != 0.
  *  c_samples : c(x) at every leaf's p*p tensor nodes, [nx*ny leaves, natural order][p*p]; corner
@@ -216,7 +227,8 @@ int hps_solve_top(hps_handle* h, int nrhs, const hps_c128* h_sub, const hps_c128
 int hps_export_R(const hps_handle* h, int64_t box, hps_c128* out);
 
 /* Leaf operators Psi ((p^2-4) x (4p-8)) and Y ((p^2-4) x (p-2)^2), row-major, of the leaf with
- * natural index `leaf`.  Either output may be NULL. */
+ * natural index `leaf`.  Either output may be NULL.  With boundary_basis 2 Psi
+ * is the Gauss-Legendre-edge operator Psi Pblk, (p^2-4) x 4q. */
 int hps_export_leaf(const hps_handle* h, int64_t leaf, hps_c128* psi, hps_c128* y);
 
 /* Sizes: n_b of a box (heap id), number of boxes, leaf depth. Returns -1 on a bad id. */
@@ -227,6 +239,8 @@ int64_t hps_num_boxes(const hps_handle* h);
  * every leaf-edge segment, canonical order [S, E, N, W], increasing coordinate within an edge;
  * x, y, nx, ny as for hps_root_boundary_nodes (2 (nx + ny) q entries each, host memory). */
 int hps_boundary_nodes_gl(const hps_grid* g, int p, double* x, double* y, double* nx, double* ny);
+/* The same with q Gauss-Legendre nodes per segment (boundary_basis 2): 2 (nx + ny) q entries each. */
+int hps_boundary_nodes_glq(const hps_grid* g, int q, double* x, double* y, double* nx, double* ny);
 
 /* Tensor-node coordinates of every leaf, [nx*ny][p*p] (x fastest), and the root boundary
  * nodes with their outward unit normals, [2(nx+ny)(p-2)] in [S,E,N,W] order.  Host pointers.

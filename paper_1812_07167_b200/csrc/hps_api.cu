@@ -468,7 +468,10 @@ struct hps_handle {
   bool dist_top = false;           // this is the top handle of a sharded build
   std::vector<DistLevel> dl;
   hps_grid g{};
-  int p = 0, q = 0, nbl = 0, ni = 0, nt = 0;
+  // q: boundary nodes per leaf edge (the merges' unit); qi = p - 2: interior grid lines of a leaf.
+  // nbl = 4 q: leaf boundary size seen by the merges and the solve; nbc = 4 qi: the Chebyshev
+  // leaf's own boundary (= nbl unless the Gauss-Legendre edge representation is on).
+  int p = 0, q = 0, qi = 0, nbl = 0, nbc = 0, ni = 0, nt = 0;
   double kappa = 0;
   zt eta{};
   int L = 0, nleaf = 0;
@@ -484,6 +487,11 @@ struct hps_handle {
   int nat_levels = 0;  // merge levels whose W was inverted in natural order
   bool gl = false;     // root boundary data given at Gauss-Legendre nodes (hps_opts.boundary_basis 1)
   DevBuf PglT;         // [q][q] transpose of the GL -> Chebyshev segment interpolation (gl only)
+  // Gauss-Legendre EDGE representation (hps_opts.boundary_basis 2): q GL nodes on
+  // every leaf edge, 1 <= q <= p - 2.  Pg: [qi][q] GL -> Chebyshev edge map, Qg: [q][qi]
+  // Chebyshev -> GL; psi_gl: [nleaf heap][nt][nbl] = Psi Pblk (the leaf R is Qblk R Pblk).
+  bool gle = false;
+  DevBuf Pg, Qg, psi_gl;
   std::vector<Depth> depth;
   std::vector<int> leaf_nat_h, nat_to_heap_h;
   DevBuf leaf_nat, nat_to_heap;
@@ -506,6 +514,9 @@ struct hps_handle {
     nat_to_heap.release();
     store.release();
     PglT.release();
+    Pg.release();
+    Qg.release();
+    psi_gl.release();
     for (auto& m : lev) {
       m.maps.release();
       m.ops.release();
@@ -741,8 +752,19 @@ std::vector<zt> schur_consts(int p, double hx, double hy, zt eta_z, const std::v
 // ---------------------------------------------------------------------------
 // Precomputation: leaves then merges bottom-up (Algorithm 1)
 // ---------------------------------------------------------------------------
+void leaves_to_gl(hps_handle& H, const zt* Rc);
+void build_leaves_cheb(hps_handle& H, const zt* c_dev, int chunk_opt, DevBuf& Rcheb);
+
 void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
-  const int p = H.p, nt = H.nt, nb = H.nbl, nleaf = H.nleaf;
+  DevBuf Rcheb;  // Chebyshev leaf R when the merges see the Gauss-Legendre edge representation
+  build_leaves_cheb(H, c_dev, chunk_opt, Rcheb);
+  if (H.gle) leaves_to_gl(H, Rcheb.as<zt>());
+}
+
+// The leaves in the paper's corner-free Chebyshev scheme: [Psi | Y] into H.store and the leaf R
+// (nbc x nbc) into H.R[L], or into Rcheb for the GL edge representation.
+void build_leaves_cheb(hps_handle& H, const zt* c_dev, int chunk_opt, DevBuf& Rcheb) {
+  const int p = H.p, nt = H.nt, nb = H.nbc, nleaf = H.nleaf;
   std::vector<double> x, D;
   cheb(p, x, D);
   const double hx = (H.g.x1 - H.g.x0) / H.g.nx, hy = (H.g.y1 - H.g.y0) / H.g.ny;
@@ -780,7 +802,8 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   H.store.alloc(sizeof(zt) * mat * nleaf);
   // leaf R (PAPER.md:398-402 via R = I - 2 i eta Psi_b): written by the fused leaf epilogues where
   // they apply, else by leaf_R below
-  H.R[H.L].alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
+  DevBuf& Rl = H.gle ? Rcheb : H.R[H.L];
+  Rl.alloc(sizeof(zt) * (size_t)nb * nb * nleaf);
   if (H.leaf_mode == 0 || H.leaf_mode == 3) {
     // real interior elimination: kappa^2 c real; in auto mode also kappa^2 max c
     // below 0.9 x the lowest Dirichlet eigenvalue pi^2 (1/hx^2 + 1/hy^2) of a leaf, so A_ii is
@@ -836,7 +859,7 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
         const int nc = std::min(chunk, nleaf - l0);
         launch_leaf_real(p, l0, nc, H.leaf_nat.as<int>(), c_dev, H.kappa * H.kappa, dKr.as<double>(), dKR.as<double>(),
                          fb, H.eta, H.store.as<zt>() + (size_t)l0 * mat, (int64_t)mat,
-                         H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, wk.p, H.info.as<int>(), H.st, !below);
+                         Rl.as<zt>() + (size_t)l0 * nb * nb, wk.p, H.info.as<int>(), H.st, !below);
       }
       const double ni = H.ni;
       H.flops[0] += nleaf * (2.0 * ni * ni * ni + 8.0 * (double)nb * nb * (ni + nb) + 4.0 * ni * ni * nb);
@@ -867,7 +890,7 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
     if (schur) {
       if (H.leaf_fused && zgj_leaf_fused_applies(p, nc) &&
           zgj_invert_leaf_schur(work.as<zt>(), (int64_t)wmat, H.store.as<zt>() + (size_t)l0 * mat, (int64_t)mat, p, nc,
-                                dK.as<zt>(), H.R[H.L].as<zt>() + (size_t)l0 * nb * nb, H.eta, H.info.as<int>(), H.st,
+                                dK.as<zt>(), Rl.as<zt>() + (size_t)l0 * nb * nb, H.eta, H.info.as<int>(), H.st,
                                 c_dev, H.leaf_nat.as<int>(), l0, H.kappa * H.kappa))
         continue;  // assembly, inverse, [Psi | Y] and R in one kernel
       launch_leaf_schur_assemble(work.as<zt>(), (int64_t)wmat, l0, nc, H.leaf_nat.as<int>(), c_dev, p, dK.as<zt>(),
@@ -889,8 +912,50 @@ void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
   } else {
     H.flops[0] += 8.0 * (double)nt * nt * nt * nleaf;
   }
-  if (!fused_all) launch_leaf_R(H.store.as<zt>(), (int64_t)mat, H.R[H.L].as<zt>(), nleaf, nt, nb, H.eta, H.st);
+  if (!fused_all) launch_leaf_R(H.store.as<zt>(), (int64_t)mat, Rl.as<zt>(), nleaf, nt, nb, H.eta, H.st);
   H.leaf_path = schur ? (fused_all ? 0 : 2) : 1;
+}
+
+// Gauss-Legendre edge representation: with Pblk = diag(P, P, P, P) (GL -> the
+// Chebyshev nodes of each edge) and Qblk = diag(Q, Q, Q, Q) (Chebyshev -> GL), every leaf gets
+// Psi_gl = Psi Pblk and R_gl = Qblk R Pblk; Y is unchanged and the solve applies Gamma_gl =
+// Qblk Gamma as -2 i eta Qblk u~(I_b).  One batched DMMA product per edge and factor.
+void leaves_to_gl(hps_handle& H, const zt* Rc) {
+  const int nt = H.nt, nbc = H.nbc, nbl = H.nbl, q = H.q, qi = H.qi, nleaf = H.nleaf;
+  H.psi_gl.alloc(sizeof(zt) * (size_t)nt * nbl * nleaf);
+  H.R[H.L].alloc(sizeof(zt) * (size_t)nbl * nbl * nleaf);
+  DevBuf T;  // R Pblk, [nleaf][nbc][nbl]
+  T.alloc(sizeof(zt) * (size_t)nbc * nbl * nleaf);
+  const zt* P = H.Pg.as<zt>();
+  const zt* Q = H.Qg.as<zt>();
+  for (int e = 0; e < 4; ++e) {
+    ZGemm g;  // Psi_gl(:, e q .. e q + q) = Psi(:, e qi .. e qi + qi) P
+    g.M = nt;
+    g.N = q;
+    g.K = qi;
+    g.batch = nleaf;
+    g.A = op(H.store.as<zt>() + e * qi, nt, (int64_t)nt * nt);
+    g.B = op(P, q, 0);
+    g.C = out(H.psi_gl.as<zt>() + e * q, nbl, (int64_t)nt * nbl);
+    zgemm(g, H.st);
+    ZGemm r = g;  // T(:, e-block) = R(:, e-block) P
+    r.M = nbc;
+    r.A = op(Rc + e * qi, nbc, (int64_t)nbc * nbc);
+    r.C = out(T.as<zt>() + e * q, nbl, (int64_t)nbc * nbl);
+    zgemm(r, H.st);
+  }
+  for (int e = 0; e < 4; ++e) {
+    ZGemm g;  // R_gl(e-block, :) = Q T(e-block, :)
+    g.M = q;
+    g.N = nbl;
+    g.K = qi;
+    g.batch = nleaf;
+    g.A = op(Q, qi, 0);
+    g.B = op(T.as<zt>() + (int64_t)e * qi * nbl, nbl, (int64_t)nbc * nbl);
+    g.C = out(H.R[H.L].as<zt>() + (int64_t)e * q * nbl, nbl, (int64_t)nbl * nbl);
+    zgemm(g, H.st);
+  }
+  H.flops[0] += 8.0 * nleaf * ((double)nt * nbl * qi + (double)nbc * nbl * qi + (double)nbl * nbl * qi);
 }
 
 // side stream for products independent of the current chain; HPS_SIDE=0 (build)
@@ -1337,7 +1402,7 @@ double solve_up_level(hps_handle& H, MergeLevel& M, int np, int nrhs, const zt* 
 // h_root (ABI [R][nb(0)], device) receives the root's outgoing particular data if non-NULL.
 void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
   cudaStream_t st = H.st;
-  const int Lb = H.Lb, nt = H.nt, nb = H.nbl, ni = H.ni;
+  const int Lb = H.Lb, nt = H.nt, nb = H.nbc, ni = H.ni;
   const int64_t R = nrhs;
   SolveState& S = H.ss;
   S.reset(Lb);
@@ -1371,7 +1436,7 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
       zgemm(g, st);
       fl += 8.0 * nbot * (double)nt * ni * R;
     }
-    {  // h = Gamma s = -2 i eta u~(I_b)
+    if (!H.gle) {  // h = Gamma s = -2 i eta u~(I_b)
       ZCopy c;
       c.batch = nbot;
       c.M = nb;
@@ -1380,6 +1445,21 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
       c.C = out(h[Lb].as<zt>(), R, (int64_t)nb * R);
       c.alpha = Z(2.0 * H.eta.y, -2.0 * H.eta.x);
       zcopy(c, st);
+    } else {  // GL edges: h = Qblk Gamma s = -2 i eta Qblk u~(I_b), one product per edge
+      const int q = H.q, qi = H.qi, nbl = H.nbl;
+      for (int e = 0; e < 4; ++e) {
+        ZGemm g;
+        g.M = q;
+        g.N = nrhs;
+        g.K = qi;
+        g.batch = nbot;
+        g.A = op(H.Qg.as<zt>(), qi, 0);
+        g.B = op(S.ut.as<zt>() + (int64_t)e * qi * R, R, (int64_t)nt * R);
+        g.C = out(h[Lb].as<zt>() + (int64_t)e * q * R, R, (int64_t)nbl * R);
+        g.alpha = Z(2.0 * H.eta.y, -2.0 * H.eta.x);
+        zgemm(g, st);
+      }
+      fl += 8.0 * nbot * (double)nbl * qi * R;
     }
   } else {  // given [box][R][nbb]
     launch_rhs_in(bottom, h[Lb].as<zt>(), H.ident.as<int>(), nbot, nbb, nrhs, nbb, R * nbb, st);
@@ -1467,7 +1547,7 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
     g.N = nrhs;
     g.K = nb;
     g.batch = nbot;
-    g.A = op(H.store.as<zt>(), nt, (int64_t)nt * nt);
+    g.A = H.gle ? op(H.psi_gl.as<zt>(), nb, (int64_t)nt * nb) : op(H.store.as<zt>(), nt, (int64_t)nt * nt);
     g.B = op(t[Lb].as<zt>(), R, (int64_t)nb * R);
     if (has_s) {
       g.Cin = op(S.ut.as<zt>(), R, (int64_t)nt * R);
@@ -1645,11 +1725,19 @@ int hps_leaf_nodes(const hps_grid* g, int p, double* x, double* y) {
 }
 
 int hps_boundary_nodes_gl(const hps_grid* g, int p, double* x, double* y, double* nx, double* ny) {
-  if (!g || p < 4 || g->nx < 1 || g->ny < 1 || !x || !y || !nx || !ny) {
+  if (p < 4) {
     hps_set_error("hps_boundary_nodes_gl: invalid argument");
     return HPS_EINVAL;
   }
-  const std::vector<double> xi = gl_nodes(p - 2);
+  return hps_boundary_nodes_glq(g, p - 2, x, y, nx, ny);
+}
+
+int hps_boundary_nodes_glq(const hps_grid* g, int q, double* x, double* y, double* nx, double* ny) {
+  if (!g || q < 1 || g->nx < 1 || g->ny < 1 || !x || !y || !nx || !ny) {
+    hps_set_error("hps_boundary_nodes_glq: invalid argument");
+    return HPS_EINVAL;
+  }
+  const std::vector<double> xi = gl_nodes(q);
   const double hx = (g->x1 - g->x0) / g->nx, hy = (g->y1 - g->y0) / g->ny;
   size_t o = 0;
   auto push = [&](double px, double py, double vx, double vy) {
@@ -1701,14 +1789,23 @@ int hps_root_boundary_nodes(const hps_grid* g, int p, double* x, double* y, doub
 
 namespace {
 
-int validate_problem(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const char* who) {
+int validate_problem(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const hps_opts* opt,
+                     const char* who) {
   auto bad = [&](const std::string& m) {
     hps_set_error(std::string(who) + ": " + m);
     return HPS_EINVAL;
   };
   if (!g) return bad("NULL grid");
   if (p < 4) return bad("p must be >= 4");
-  if (q != p - 2) return bad("q must equal p - 2 (corner-free Chebyshev boundary nodes)");
+  const int basis = opt ? opt->boundary_basis : 0;
+  if (basis < 0 || basis > 2)
+    return bad("boundary_basis must be 0 (Chebyshev), 1 (Gauss-Legendre root data) or 2 (Gauss-Legendre edges)");
+  if (basis == 2) {
+    if (q < 2 || q > p - 2) return bad("with boundary_basis 2, q (Gauss-Legendre nodes per leaf edge) must be in [2, p - 2]");
+  } else if (q != p - 2) {
+    return bad("q must equal p - 2 (corner-free Chebyshev boundary nodes; boundary_basis 2 for q Gauss-Legendre "
+               "nodes per edge)");
+  }
   if (!is_pow2(g->nx) || !is_pow2(g->ny)) return bad("nx and ny must be powers of two");
   if (!(g->x1 > g->x0) || !(g->y1 > g->y0) || !std::isfinite(g->x0) || !std::isfinite(g->x1) ||
       !std::isfinite(g->y0) || !std::isfinite(g->y1))
@@ -1745,11 +1842,11 @@ std::vector<double> gl_nodes(int q) {
 
 // P[j][g] = l_g(x_j): the degree-(q-1) interpolant of segment samples at the Gauss-Legendre
 // nodes xi, evaluated at the q interior Chebyshev-Lobatto nodes x_j of the segment.
-std::vector<double> gl_to_cheb_matrix(int p) {
-  const int q = p - 2;
+std::vector<double> gl_to_cheb_matrix(int p, int q) {
+  const int qi = p - 2;
   const std::vector<double> xi = gl_nodes(q);
-  std::vector<double> P((size_t)q * q);
-  for (int j = 0; j < q; ++j) {
+  std::vector<double> P((size_t)qi * q);
+  for (int j = 0; j < qi; ++j) {
     const double xj = -std::cos(M_PI * (j + 1) / (p - 1));
     for (int g = 0; g < q; ++g) {
       double l = 1.0;
@@ -1759,6 +1856,26 @@ std::vector<double> gl_to_cheb_matrix(int p) {
     }
   }
   return P;
+}
+std::vector<double> gl_to_cheb_matrix(int p) { return gl_to_cheb_matrix(p, p - 2); }
+
+// Q[g][j] = L_j(xi_g): the degree-(p-3) interpolant of segment samples at the p - 2 interior
+// Chebyshev-Lobatto nodes x_j, evaluated at the q Gauss-Legendre nodes xi_g (GL edge
+// representation, outgoing side; for q = p - 2 the inverse of gl_to_cheb_matrix(p)).
+std::vector<double> cheb_to_gl_matrix(int p, int q) {
+  const int qi = p - 2;
+  const std::vector<double> xi = gl_nodes(q);
+  std::vector<double> xc(qi);
+  for (int j = 0; j < qi; ++j) xc[j] = -std::cos(M_PI * (j + 1) / (p - 1));
+  std::vector<double> Q((size_t)q * qi);
+  for (int g = 0; g < q; ++g)
+    for (int j = 0; j < qi; ++j) {
+      double l = 1.0;
+      for (int m = 0; m < qi; ++m)
+        if (m != j) l *= (xi[g] - xc[m]) / (xc[j] - xc[m]);
+      Q[(size_t)g * qi + j] = l;
+    }
+  return Q;
 }
 
 // t at the Gauss-Legendre nodes -> t at the Chebyshev nodes, per leaf-edge segment of q nodes:
@@ -1799,8 +1916,10 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   H.g = *g;
   H.p = p;
   H.q = q;
+  H.qi = p - 2;
   H.nbl = 4 * q;
-  H.ni = q * q;
+  H.nbc = 4 * H.qi;
+  H.ni = H.qi * H.qi;
   H.nt = p * p - 4;
   H.kappa = kappa;
   H.eta = make_double2(eta.re, eta.im);
@@ -1810,6 +1929,15 @@ void init_handle(hps_handle& H, const hps_grid* g, int p, int q, double kappa, h
   H.leaf_fused = H.leaf_mode == 0;
   H.prof.timing = opt ? (unsigned)opt->profile : 0u;
   H.gl = opt && opt->boundary_basis == 1;
+  H.gle = opt && opt->boundary_basis == 2;
+  if (H.gle) {
+    const std::vector<double> P = gl_to_cheb_matrix(p, q), Q = cheb_to_gl_matrix(p, q);
+    std::vector<zt> Pz(P.size()), Qz(Q.size());
+    for (size_t i = 0; i < P.size(); ++i) Pz[i] = make_double2(P[i], 0.0);
+    for (size_t i = 0; i < Q.size(); ++i) Qz[i] = make_double2(Q[i], 0.0);
+    upload(H.Pg, Pz, H.st);
+    upload(H.Qg, Qz, H.st);
+  }
   if (H.gl) {
     const std::vector<double> P = gl_to_cheb_matrix(p);
     std::vector<zt> PT((size_t)q * q);
@@ -1955,11 +2083,7 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
     hps_set_error("hps_build: NULL argument");
     return HPS_EINVAL;
   }
-  if (int rc = validate_problem(g, p, q, kappa, eta, "hps_build")) return rc;
-  if (opt && (opt->boundary_basis < 0 || opt->boundary_basis > 1)) {
-    hps_set_error("hps_build: boundary_basis must be 0 (Chebyshev) or 1 (Gauss-Legendre)");
-    return HPS_EINVAL;
-  }
+  if (int rc = validate_problem(g, p, q, kappa, eta, opt, "hps_build")) return rc;
   if (opt && (opt->leaf_mode < 0 || opt->leaf_mode > 3)) {
     hps_set_error("hps_build: leaf_mode must be 0, 1, 2 or 3");
     return HPS_EINVAL;
@@ -2033,7 +2157,7 @@ int hps_build_top(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, i
     hps_set_error("hps_build_top: NULL argument");
     return HPS_EINVAL;
   }
-  if (int rc = validate_problem(g, p, q, kappa, eta, "hps_build_top")) return rc;
+  if (int rc = validate_problem(g, p, q, kappa, eta, opt, "hps_build_top")) return rc;
   std::unique_ptr<hps_handle> H(new hps_handle());
   try {
     init_handle(*H, g, p, q, kappa, eta, opt);
@@ -2335,9 +2459,12 @@ int hps_export_leaf(const hps_handle* h, int64_t leaf, hps_c128* psi, hps_c128* 
     return HPS_EINVAL;
   }
   try {
-    const int nt = h->nt, nb = h->nbl, ni = h->ni;
+    const int nt = h->nt, nb = h->nbc, ni = h->ni;
     const zt* base = h->store.as<zt>() + (size_t)h->nat_to_heap_h[leaf] * nt * nt;
-    if (psi)
+    if (psi && h->gle)  // Psi_gl = Psi Pblk, (p^2 - 4) x 4q
+      HPS_CUDA_CHECK(cudaMemcpy(psi, h->psi_gl.as<zt>() + (size_t)h->nat_to_heap_h[leaf] * nt * h->nbl,
+                                sizeof(zt) * nt * h->nbl, cudaMemcpyDefault));
+    else if (psi)
       HPS_CUDA_CHECK(cudaMemcpy2D(psi, sizeof(zt) * nb, base, sizeof(zt) * nt, sizeof(zt) * nb, nt, cudaMemcpyDefault));
     if (y)
       HPS_CUDA_CHECK(

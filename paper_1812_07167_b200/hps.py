@@ -39,7 +39,8 @@ class hps_opts(C.Structure):
 
 
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
-           "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_last_time_ms", "hps_last_launches",
+           "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_boundary_nodes_glq",
+           "hps_last_time_ms", "hps_last_launches",
            "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free", "hps_release_cache",
            "hps_set_cache_limit", "hps_cache_bytes", "hps_debug_set", "hps_debug_get", "hps_last_error",
@@ -70,6 +71,7 @@ def lib():
         L.hps_leaf_nodes.argtypes = [C.POINTER(hps_grid), i32, dp, dp]
         L.hps_root_boundary_nodes.argtypes = [C.POINTER(hps_grid), i32, dp, dp, dp, dp]
         L.hps_boundary_nodes_gl.argtypes = [C.POINTER(hps_grid), i32, dp, dp, dp, dp]
+        L.hps_boundary_nodes_glq.argtypes = [C.POINTER(hps_grid), i32, dp, dp, dp, dp]
         L.hps_last_time_ms.argtypes = [vp, i32]
         L.hps_last_time_ms.restype = C.c_double
         L.hps_last_launches.argtypes = [vp, i32]
@@ -203,10 +205,16 @@ class debug_knobs:
             lib().hps_debug_set(k.encode(), int(v))
 
 
-def root_boundary_nodes(g, p, basis=0):
-    """Root boundary nodes and outward normals; basis 1: Gauss-Legendre nodes per leaf edge."""
-    n = 2 * (g.nx + g.ny) * (p - 2)
+def root_boundary_nodes(g, p, basis=0, q=None):
+    """Root boundary nodes and outward normals; basis 1: the p - 2 Gauss-Legendre nodes per leaf
+    edge; basis 2: q Gauss-Legendre nodes per leaf edge (q defaults to p - 2)."""
+    q = p - 2 if q is None else q
+    n = 2 * (g.nx + g.ny) * (q if basis == 2 else p - 2)
     X, Y, NX, NY = (np.zeros(n) for _ in range(4))
+    if basis == 2:
+        _check(lib().hps_boundary_nodes_glq(C.byref(g), q, X.ctypes.data, Y.ctypes.data, NX.ctypes.data,
+                                            NY.ctypes.data))
+        return X, Y, NX, NY
     fn = lib().hps_boundary_nodes_gl if basis == 1 else lib().hps_root_boundary_nodes
     _check(fn(C.byref(g), p, X.ctypes.data, Y.ctypes.data, NX.ctypes.data, NY.ctypes.data))
     return X, Y, NX, NY
@@ -383,7 +391,8 @@ class Solver:
     and solve are sharded by subtree (c, s, u: this rank's rectangle; t: the whole root boundary)."""
 
     def __init__(self, g, p, kappa, eta, c, keep_root_R=True, keep_all_R=False, device=-1, leaf_chunk=0,
-                 profile=False, leaf_mode=0, boundary_basis=0, comm=None, stream=None):
+                 profile=False, leaf_mode=0, boundary_basis=0, comm=None, stream=None, q=None):
+        """q: boundary nodes per leaf edge (p - 2; any 2 <= q <= p - 2 with boundary_basis 2)."""
         self.g, self.p = g, p
         self.comm = comm
         G, rank = 1, 0
@@ -392,8 +401,9 @@ class Solver:
         self.G, self.rank = G, rank
         self.sub = subtree_grid(g, int(round(np.log2(G))), rank)[0] if G > 1 else g
         self.nleaf = self.sub.nx * self.sub.ny
-        self.q, self.nt, self.ni = p - 2, p * p - 4, (p - 2) ** 2
-        self.nb_root = 2 * (g.nx + g.ny) * (p - 2)
+        self.q = p - 2 if q is None else int(q)
+        self.nt, self.ni = p * p - 4, (p - 2) ** 2
+        self.nb_root = 2 * (g.nx + g.ny) * self.q
         mask = -1 if profile is True else int(profile)
         st = None
         if stream is not None:
@@ -406,7 +416,7 @@ class Solver:
         self._c = c   # keep alive during the call
         self._stream = st
         _torch_ready(c, stream=st)
-        _check(lib().hps_build(C.byref(g), p, p - 2, float(kappa), hps_c128(eta.real, eta.imag), cp,
+        _check(lib().hps_build(C.byref(g), p, self.q, float(kappa), hps_c128(eta.real, eta.imag), cp,
                                C.byref(opts), C.byref(h)))
         self.h = h
 

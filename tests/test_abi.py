@@ -50,6 +50,18 @@ def test_gl_boundary_nodes_match_oracle(L, orc, nx, ny, p):
         assert np.max(np.abs(u - v)) < 1e-14
 
 
+@pytest.mark.parametrize("nx,ny,q", [(1, 1, 2), (2, 4, 5), (4, 2, 9)])
+def test_glq_boundary_nodes_match_oracle(L, orc, nx, ny, q):
+    """hps_boundary_nodes_glq (q nodes per segment, boundary_basis 2) vs oracle.gl at 1e-14."""
+    from oracle import gl
+    g = hps.grid(0.1, 0.9, -0.3, 0.5, nx, ny)
+    b = hps.root_boundary_nodes(g, 16, basis=2, q=q)
+    bo = gl.root_boundary_gl(0.1, 0.9, -0.3, 0.5, nx, ny, 16, q=q)
+    assert b[0].shape == (2 * (nx + ny) * q,)
+    for u, v in zip(b, bo):
+        assert np.max(np.abs(u - v)) < 1e-14
+
+
 def _build_rc(L, **kw):
     args = dict(g=hps.grid(0, 1, 0, 1, 2, 2), p=8, q=6, kappa=1.0, eta=hps.hps_c128(1.0, 0.0))
     args.update(kw)
@@ -75,14 +87,17 @@ def test_argument_validation(L):
 
 
 def test_option_validation_and_small_calls(L):
-    """leaf_mode outside 0..3 and boundary_basis outside 0..1 are rejected before any device work;
-    hps_leaf_path(NULL) is HPS_EINVAL; hps_release_cache with nothing cached returns 0."""
+    """leaf_mode outside 0..3, boundary_basis outside 0..2 and a q outside [2, p - 2] for the
+    Gauss-Legendre edge representation (q != p - 2 for the others) are rejected before any device
+    work; hps_leaf_path(NULL) is HPS_EINVAL; hps_release_cache with nothing cached returns 0."""
     g = hps.grid(0, 1, 0, 1, 2, 2)
     c = np.ones(4 * 64, complex)
-    for lm, bb, msg in ((4, 0, b"leaf_mode"), (0, 2, b"boundary_basis"), (-1, 0, b"leaf_mode")):
+    for lm, bb, q, msg in ((4, 0, 6, b"leaf_mode"), (0, 3, 6, b"boundary_basis"), (-1, 0, 6, b"leaf_mode"),
+                           (0, 2, 7, b"[2, p - 2]"), (0, 2, 1, b"[2, p - 2]"), (0, 0, 5, b"p - 2"),
+                           (0, 1, 4, b"p - 2")):
         opts = hps.hps_opts(1, 0, -1, 0, 0, lm, bb)
         h = C.c_void_p()
-        rc = L.hps_build(C.byref(g), 8, 6, 1.0, hps.hps_c128(1.0, 0.0), c.ctypes.data, C.byref(opts), C.byref(h))
+        rc = L.hps_build(C.byref(g), 8, q, 1.0, hps.hps_c128(1.0, 0.0), c.ctypes.data, C.byref(opts), C.byref(h))
         assert rc == -1 and not h.value
         assert msg in L.hps_last_error()
     assert L.hps_leaf_path(None) == -1

@@ -255,6 +255,96 @@ def test_gl_boundary_basis_sharded():
         assert rel(u, dist.slice_leaves(u_ref, g, sub, i0, j0)) < 1e-11
 
 
+def gl_problem(nx, ny, p, q, kappa, eta, nrhs=2, seed=3):
+    """problem() with root data at the q Gauss-Legendre nodes of every boundary segment."""
+    g, c, s, _ = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx, nrhs=nrhs, seed=seed)
+    rng = np.random.default_rng(seed + 100)
+    nbr = 2 * (nx + ny) * q
+    t = rng.standard_normal((nrhs, nbr)) + 1j * rng.standard_normal((nrhs, nbr))
+    return g, c, s, t
+
+
+@pytest.mark.parametrize("leaf_mode", [0, 1])
+@pytest.mark.parametrize("nx,ny,p,q,kappa", [(1, 1, 8, 4, 9.0), (2, 2, 8, 4, 9.0), (4, 2, 10, 5, 9.0),
+                                             (4, 4, 16, 9, 9.0), (2, 1, 6, 2, 5.0), (8, 4, 16, 12, 30.0),
+                                             (4, 4, 12, 10, 9.0)])
+def test_gl_edges_parity(nx, ny, p, q, kappa, leaf_mode):
+    """boundary_basis 2, the Gauss-Legendre EDGE representation with q independent of p (SURVEY
+    8(f) NEXT-2): every box's R, the leaf Psi Pblk and Y, and u (with and without
+    a body load) against the oracle's GL-edge tree (oracle.Oracle(..., qe=q)) at 1e-9.  Leaf mode 0
+    covers the real interior elimination (4x4 and finer at kappa = 9) and the complex Schur path
+    (1x1, 2x2, and 8x4 at kappa = 30); leaf mode 1 the full-B inverse."""
+    eta = kappa - 2j
+    g, c, s, t = gl_problem(nx, ny, p, q, kappa, eta)
+    S = hps.Solver(g, p, kappa, eta, c, boundary_basis=2, q=q, keep_all_R=True, leaf_mode=leaf_mode)
+    O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c, keep_all_R=True, qe=q)
+    assert rel(S.solve(s, t), O.solve(s, t)) < TOL
+    assert rel(S.solve(None, t), O.solve(np.zeros_like(s), t)) < TOL
+    nbox, _ = oracle.tree_info(nx, ny)
+    for box in range(1, nbox + 1):
+        assert S.nb(box) == O.nb(box)
+        assert rel(S.R(box), O.R(box)) < TOL, box
+    for leaf in (0, nx * ny - 1):
+        Psi, Y = S.leaf_ops(leaf)
+        Po, Yo = O.leaf_ops(O.leaf_box(leaf % nx, leaf // nx))
+        assert Psi.shape == (p * p - 4, 4 * q)
+        assert rel(Psi, Po) < TOL and rel(Y, Yo) < TOL
+
+
+def test_gl_edges_full_q_equals_gl_root_data():
+    """q = p - 2: the GL-edge tree (basis 2) and the Chebyshev tree fed GL root data (basis 1)
+    solve the same problem in two bases: u agrees to rounding."""
+    nx, ny, p, kappa, eta = 4, 4, 10, 12.0, 12.0 + 1j
+    g, c, s, t = gl_problem(nx, ny, p, p - 2, kappa, eta)
+    u2 = hps.Solver(g, p, kappa, eta, c, boundary_basis=2, q=p - 2).solve(s, t)
+    u1 = hps.Solver(g, p, kappa, eta, c, boundary_basis=1).solve(s, t)
+    assert rel(u2, u1) < 1e-11
+
+
+def test_gl_edges_polynomial_exact():
+    """A global polynomial of degree q - 1 is reproduced to rounding through the GPU GL-edge tree
+    (q = 6 < p - 2 = 10, 8x8 leaves); degree q is not (the representation truncates at q)."""
+    from test_oracle_pins import Poly2D
+    nx, ny, p, q, kappa, eta = 8, 8, 12, 6, 7.0, 7.0 + 1j
+    g = hps.grid(0.0, 1.0, 0.0, 1.0, nx, ny)
+    X, Y = hps.leaf_nodes(g, p)
+    c = (1 + 0.25 * np.cos(3 * X) * np.sin(2 * Y)).astype(complex)
+    Xi, Yi = inputs.interior_of(p, X), inputs.interior_of(p, Y)
+    Xb, Yb, NX, NY = hps.root_boundary_nodes(g, p, basis=2, q=q)
+    S = hps.Solver(g, p, kappa, eta, c, boundary_basis=2, q=q)
+    errs = []
+    for deg in (q - 1, q):
+        P = Poly2D(deg, (0.0, 1.0, 0.0, 1.0), seed=5)
+        s = -(P.val(Xi, Yi, dx=2) + P.val(Xi, Yi, dy=2)) - kappa ** 2 * inputs.interior_of(p, c) * P.val(Xi, Yi)
+        t = NX * P.val(Xb, Yb, dx=1) + NY * P.val(Xb, Yb, dy=1) + 1j * eta * P.val(Xb, Yb)
+        u = S.solve(s[None], t[None])[0]
+        errs.append(np.max(np.abs(u[:, 4 * (p - 2):] - P.val(Xi, Yi))) / np.max(np.abs(P.val(Xi, Yi))))
+    assert errs[0] < 1e-11 and errs[1] > 1e-7, errs
+
+
+def test_gl_edges_sharded():
+    """GL edges through the subtree-sharded path (4 virtual ranks, group split of the top levels)
+    equal the single-GPU GL-edge solve."""
+    import torch
+    from paper_1812_07167_b200 import dist
+    kappa, eta, nx, ny, p, q = 11.0, 11.0 + 2j, 4, 4, 10, 6
+    g, c, s, t = gl_problem(nx, ny, p, q, kappa, eta)
+    u_ref = hps.Solver(g, p, kappa, eta, c, boundary_basis=2, q=q).solve(s, t)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+    def rank_fn(comm):
+        rank, world = comm.info()
+        sub, i0, j0 = dist.local_block(g, world, rank)
+        D = dist.DistributedHPS(comm, g, p, kappa, eta, d(dist.slice_leaves(c, g, sub, i0, j0)), boundary_basis=2,
+                                q=q)
+        u = D.solve(d(dist.slice_leaves(s, g, sub, i0, j0)), d(t)).cpu().numpy()
+        D.close()
+        return u, (sub, i0, j0)
+
+    for u, (sub, i0, j0) in dist.run_virtual(4, rank_fn):
+        assert rel(u, dist.slice_leaves(u_ref, g, sub, i0, j0)) < 1e-11
+
+
 def test_block_cache_reuse_and_release():
     """Opt-in cache (hps_set_cache_limit): large device blocks (>= 256 MB: the 32x16-leaf store
     here) are parked by hps_free, re-used by the next handle and returned by hps_release_cache /
