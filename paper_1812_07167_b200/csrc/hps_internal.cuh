@@ -46,6 +46,7 @@ enum HpsKnob {
   KN_NAT_PIVOT_REL,    // natural-order W^{-1}: pivot accepted if |p|^2 >= REL/1e4 * |W_kk|^2
   KN_NAT_BB_MIN,       // natural-order W^{-1} with 64-wide block steps (D^{-1} kernel + GEMMs) for n >= this
   KN_LEAF_PANEL,       // complex leaf Schur inverse, natural order: 0 step-by-step panels, 1 block form
+  KN_GEMM_BCOL,        // 1: k-fastest B loader for column-major B (s in the ABI layout)
   KN_COUNT
 };
 int knob(HpsKnob k);

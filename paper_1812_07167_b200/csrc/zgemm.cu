@@ -49,7 +49,10 @@ struct Cfg {
   static_assert(NT % BN == 0 || BN % NT == 0, "cfg");
 };
 
-template <int BM, int BN, int WM, int WN>
+// BCOL: B is column-major (rs == 1, no maps: the solve reads s in the ABI layout [RHS][leaf][n_i],
+// columns 0.2-3 GB apart): the B tile is loaded k-fastest, so that a warp's cp.async requests cover
+// runs of BK consecutive elements of a column instead of one 16-byte piece per column.
+template <int BM, int BN, int WM, int WN, bool BCOL = false>
 __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZGemm g) {
   using C = Cfg<BM, BN, WM, WN>;
   constexpr int NT = C::NT, TM = C::TM, TN = C::TN, AS = C::AS, BS = C::BS, ITA = C::ITA, ITB = C::ITB;
@@ -98,6 +101,18 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
       b_cok = cj >= 0;
       b_coff = (int64_t)(cj < 0 ? 0 : cj) * g.B.cs;
     }
+    // BCOL: thread (k = tid % BK, columns tid / BK + it * NT / BK)
+    constexpr int BC_JSTEP = NT / BK;
+    int64_t bc_off[BCOL ? ITB : 1];
+    bool bc_ok[BCOL ? ITB : 1];
+    if constexpr (BCOL) {
+#pragma unroll
+      for (int it = 0; it < ITB; ++it) {
+        const int gj = n0 + tid / BK + it * BC_JSTEP;
+        bc_ok[it] = gj < g.N;
+        bc_off[it] = (int64_t)(gj < g.N ? gj : 0) * g.B.cs;
+      }
+    }
 
     auto load_stage = [&](int stage, int k0) {
       {
@@ -110,13 +125,23 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
           cp_async16(&As[(stage * BM + a_r0 + it * A_RSTEP) * AS + a_c], ok ? Ab + a_roff[it] + coff : g.A.ptr, ok);
         }
       }
+      if constexpr (BCOL) {
+        const int kk = tid % BK, gk = k0 + kk;
 #pragma unroll
-      for (int it = 0; it < ITB; ++it) {
-        const int r = b_r0 + it * B_RSTEP;
-        const int gk = k0 + r;
-        int rk = gk < g.K ? (Brm ? Brm[gk] : gk) : -1;
-        const bool ok = b_cok && rk >= 0;
-        cp_async16(&Bs[(stage * BK + r) * BS + b_c], ok ? Bb + (int64_t)rk * g.B.rs + b_coff : g.B.ptr, ok);
+        for (int it = 0; it < ITB; ++it) {
+          const int jj = tid / BK + it * BC_JSTEP;
+          const bool ok = bc_ok[it] && gk < g.K;
+          cp_async16(&Bs[(stage * BK + kk) * BS + jj], ok ? Bb + gk + bc_off[it] : g.B.ptr, ok);
+        }
+      } else {
+#pragma unroll
+        for (int it = 0; it < ITB; ++it) {
+          const int r = b_r0 + it * B_RSTEP;
+          const int gk = k0 + r;
+          int rk = gk < g.K ? (Brm ? Brm[gk] : gk) : -1;
+          const bool ok = b_cok && rk >= 0;
+          cp_async16(&Bs[(stage * BK + r) * BS + b_c], ok ? Bb + (int64_t)rk * g.B.rs + b_coff : g.B.ptr, ok);
+        }
       }
       cp_async_commit();
     };
@@ -259,11 +284,11 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
   }
 }
 
-template <int BM, int BN, int WM, int WN>
+template <int BM, int BN, int WM, int WN, bool BCOL = false>
 void launch(const ZGemm& g, cudaStream_t st) {
   using C = Cfg<BM, BN, WM, WN>;
   static bool attr_set = false;
-  auto kern = zgemm_kernel<BM, BN, WM, WN>;
+  auto kern = zgemm_kernel<BM, BN, WM, WN, BCOL>;
   if (!attr_set) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr_set = true;
@@ -607,6 +632,8 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   const int64_t tiles32 = (int64_t)((g.M + 31) / 32) * ((g.N + 31) / 32) * g.batch;
   const bool small_k16 = knob(KN_GEMM_SMALLK) != 0;
   const int nsm = hps_num_sms();
+  // column-major B without maps (s in the ABI layout): the k-fastest B loader
+  const bool bcol = g.B.rs == 1 && g.B.cs > 1 && !g.B.rmap && !g.B.cmap && g.B.cskip_len == 0 && knob(KN_GEMM_BCOL);
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
   else if (g.N <= 16 && g.M > 16 && g.K >= 1024 && (int64_t)((g.M + 63) / 64) * g.batch < nsm)
@@ -614,13 +641,13 @@ void zgemm_impl(const ZGemm& g, cudaStream_t st) {
   else if (g.N <= 16 && g.M > 16 && g.M <= 48)
     launch<32, 16, 16, 16>(g, st);  // the low levels' solve products (n3 = 28, 42): less padding
   else if (g.N <= 16 && g.M > 16)
-    launch<64, 16, 16, 16>(g, st);  // the solve sweeps at 16 right-hand sides: no half-empty tiles
+    bcol ? launch<64, 16, 16, 16, true>(g, st) : launch<64, 16, 16, 16>(g, st);  // 16 RHS: no half-empty tiles
   else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * nsm))
     launch<16, 16, 8, 8>(g, st);  // short K on a grid of few 32x32 tiles: more, smaller CTAs
   else if (g.K >= 512)
     launch<64, 32, 32, 16>(g, st);
   else
-    launch<32, 32, 16, 16>(g, st);
+    bcol ? launch<32, 32, 16, 16, true>(g, st) : launch<32, 32, 16, 16>(g, st);
 }
 
 // Several independent copies in one launch (blockIdx.y selects the copy): the merge gathers are a

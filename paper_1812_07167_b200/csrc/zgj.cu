@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) zgj_panel_reg_kernel(c
 // whose |pivot|^2 is below rel2 x the original |A_kk|^2 raises *a.pflag (the caller redoes the
 // matrix with partial pivoting).
 // Same interface and outputs as zgj_panel_reg_kernel with identity permutations.
-__device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[192..255])
+__device__ long long g_nat_trace[64];  // debug timeline (hps_debug_ws_trace(7, out): out[256..319])
 __device__ int g_nat_trace_on;
 // ---------------------------------------------------------------------------
 // Blocked natural-order panel: with natural pivots the w pivot rows are rows
@@ -2035,6 +2035,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   __shared__ double diag2[NAT ? 256 : 1];  // |S_kk|^2 of the assembled S (NAT)
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, cg = lane & 3, rg = lane >> 2;
+  const long long t_start = clock64();
   zt* M = A + (int64_t)blockIdx.x * bs;
   WsPanels P;
   P.npan = (n + NB - 1) / NB;
@@ -2079,6 +2080,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   const int MT = mtr >> 3;
   // trace armed with 1 (every launch) or with the matrix size n to trace
   const bool trace = (g_ws_trace_on == 1 || g_ws_trace_on == n) && blockIdx.x == 0 && tid == 0;
+  if (trace) g_ws_trace[15 * 16 + 2] = t_start;
   for (int p = 0; p < P.npan; ++p) {
     const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
     WS_MARK(p, 0);
@@ -2464,8 +2466,8 @@ int g_gj_mode_force = 0;
 void zgj_ws_trace(int on, long long* out) {
   HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_ws_trace_on, &on, sizeof(int)));
   HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_nat_trace_on, &on, sizeof(int)));
-  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_ws_trace, sizeof(long long) * 192));
-  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out + 192, g_nat_trace, sizeof(long long) * 64));
+  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_ws_trace, sizeof(long long) * 256));
+  if (out) HPS_CUDA_CHECK(cudaMemcpyFromSymbol(out + 256, g_nat_trace, sizeof(long long) * 64));
 }  // hps_zinv_timed: 1 = fused, 2 = blocked (0 = library choice / HPS_GJ)
 namespace {
 int gj_mode_env() {

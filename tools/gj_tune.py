@@ -32,9 +32,9 @@ if os.environ.get("WS_TRACE"):
     A = torch.randn(batch, n, n, dtype=torch.complex128, device="cuda", generator=g)
     hps.lib().hps_debug_ws_trace(1, None)
     hps.zinv_timed(A, mode=int(os.environ.get("WS_TRACE_MODE", "3")), reps=1)
-    buf = np.zeros(256, dtype=np.int64)
+    buf = np.zeros(320, dtype=np.int64)
     hps.lib().hps_debug_ws_trace(0, buf.ctypes.data)
-    t = buf.reshape(16, 16)
+    t = buf[:256].reshape(16, 16)
     t0 = t[0, 4]
     names = ["P:ready", "P:factored", "P:tfree", "P:tready", "U:tready", "U:z1", "U:ph1", "U:z2", "U:ph2", "-"]
     print("n", n, "batch", batch, "(kclk relative to pass 0 start)")

@@ -11,10 +11,10 @@ cd = torch.from_numpy(np.ascontiguousarray(c)).cuda()
 S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, cd); S.close()
 hps.lib().hps_debug_ws_trace((cfg.p - 2) ** 2, None)   # trace the leaf launch only
 S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, cd)
-buf = np.zeros(256, dtype=np.int64)
+buf = np.zeros(320, dtype=np.int64)
 hps.lib().hps_debug_ws_trace(0, buf.ctypes.data)
 S.close()
-T = buf.reshape(16, 16)
+T = buf[:256].reshape(16, 16)
 t0 = T[0, 0]
 for p in range(7):
     print(f"pass {p}: panel {(T[p,1]-T[p,0])/1e3:6.1f}k  staging {(T[p,2]-T[p,1])/1e3:5.1f}k  update {(T[p,3]-T[p,2])/1e3:6.1f}k clk")

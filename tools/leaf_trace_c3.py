@@ -17,16 +17,16 @@ S = hps.Solver(g, sub.p, sub.kappa, sub.eta, cd); S.close()
 for rep in range(2):
     hps.lib().hps_debug_ws_trace((sub.p - 2) ** 2, None)   # trace the leaf launch only
     S = hps.Solver(g, sub.p, sub.kappa, sub.eta, cd, profile=1 << 7)
-    buf = np.zeros(256, dtype=np.int64)
+    buf = np.zeros(320, dtype=np.int64)
     hps.lib().hps_debug_ws_trace(0, buf.ctypes.data)
     ks = S.kernel_stats()
     path = S.leaf_path()
     S.close()
-T = buf.reshape(16, 16)
+T = buf[:256].reshape(16, 16)
 t0 = T[0, 0]
 print(f"leaf path {path}, {n * n} leaves; leaf class {ks.get('leaf_gj')}")
 for p in range(7):
     print(f"pass {p}: panel {(T[p,1]-T[p,0])/1e3:6.1f}k  staging {(T[p,2]-T[p,1])/1e3:5.1f}k  update {(T[p,3]-T[p,2])/1e3:6.1f}k clk")
-print(f"GJ total {(T[6,3]-t0)/1e3:.1f}k clk, epilogue {(T[15,1]-T[15,0])/1e3:.1f}k clk, kernel start->GJ {(t0 - T[15,2])/1e3 if T[15,2] else 0:.1f}k")
+print(f"GJ total {(T[6,3]-t0)/1e3:.1f}k clk, epilogue {(T[15,1]-T[15,0])/1e3:.1f}k clk, kernel start->GJ (assembly) {(t0 - T[15,2])/1e3 if T[15,2] else 0:.1f}k, kernel total {(T[15,1]-T[15,2])/1e3:.1f}k")
 print("epilogue per phase (k clk, CTA 0, all chunks): wait %.1f | load+Y_i %.1f | Psi_i %.1f | Y_b+accY %.1f | Psi_b+accP %.1f"
       % tuple(T[15, 4:9] / 1e3))

@@ -13,8 +13,8 @@ S.close()
 hps.lib().hps_debug_ws_trace(7, None)
 S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, d(c))
 torch.cuda.synchronize()
-buf = np.zeros(256, dtype=np.int64)
+buf = np.zeros(320, dtype=np.int64)
 hps.lib().hps_debug_ws_trace(0, buf.ctypes.data)
-tr = buf[192:]
+tr = buf[256:]
 t0 = tr[0]
 print("load %d clk; steps:" % (tr[1] - t0), np.diff(tr[2:18]).tolist(), "after loop %d, end %d" % (tr[40] - t0, tr[41] - t0))

@@ -13,7 +13,7 @@ S.close()
 hps.lib().hps_debug_ws_trace(7, None)
 S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, d(c))
 torch.cuda.synchronize()
-buf = np.zeros(256, dtype=np.int64)
+buf = np.zeros(320, dtype=np.int64)
 hps.lib().hps_debug_ws_trace(0, buf.ctypes.data)
-tr = buf[192:]
+tr = buf[256:]
 print("block load %d, block GJ %d, stage1 total %d clk, stage2 %d clk, store %d clk" % (tr[4] - tr[0], tr[5] - tr[4], tr[1] - tr[0], tr[2] - tr[1], tr[3] - tr[2]))
