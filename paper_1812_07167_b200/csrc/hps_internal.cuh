@@ -47,6 +47,7 @@ enum HpsKnob {
   KN_NAT_BB_MIN,       // natural-order W^{-1} with 64-wide block steps (D^{-1} kernel + GEMMs) for n >= this
   KN_LEAF_PANEL,       // complex leaf Schur inverse, natural order: 0 step-by-step panels, 1 block form
   KN_GEMM_BCOL,        // 1: k-fastest B loader for column-major B (s in the ABI layout)
+  KN_GEMM_GROUP,       // GEMM tile order: 1 row-major, G > 1 grouped by G row blocks (L2 reuse)
   KN_COUNT
 };
 int knob(HpsKnob k);
@@ -110,6 +111,7 @@ __device__ __forceinline__ int zrow(const T& o, const int* rm, int i) {
 
 struct ZGemm {
   int M = 0, N = 0, K = 0, batch = 1;
+  int group_m = 1;  // tile order: 1 row-major, > 1 grouped by group_m row blocks (set by zgemm from the knob)
   ZOp A, B, Cin;  // Cin.ptr == nullptr => beta term omitted
   ZOut C;
   zt alpha = {1.0, 0.0};

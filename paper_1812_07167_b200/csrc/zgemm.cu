@@ -53,7 +53,7 @@ struct Cfg {
 // columns 0.2-3 GB apart): the B tile is loaded k-fastest, so that a warp's cp.async requests cover
 // runs of BK consecutive elements of a column instead of one 16-byte piece per column.
 template <int BM, int BN, int WM, int WN, bool BCOL = false>
-__global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZGemm g) {
+__global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32) ? 3 : 0) zgemm_kernel(const ZGemm g) {
   using C = Cfg<BM, BN, WM, WN>;
   constexpr int NT = C::NT, TM = C::TM, TN = C::TN, AS = C::AS, BS = C::BS, ITA = C::ITA, ITB = C::ITB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -62,11 +62,23 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT) zgemm_kernel(const ZG
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / C::NWN, wn = warp % C::NWN;
-  // Row-major tile order.  A grouped order (GM = 16 row blocks swept column by column) cut the C4
-  // GEMM DRAM traffic 1134 -> 468 GB per step but cost registers: the 64 x 32 tile kernel went
-  // 166 -> 180 registers, 3 -> 2 CTAs per SM, and the C4 merges 993 -> 1098 ms (round 2).
+  // Tile order: row-major (group_m = 1), or grouped -- consecutive CTAs sweep a group of group_m
+  // row blocks column by column, so the CTAs in flight share a few A row blocks and B column
+  // blocks instead of streaming all of B once per row block (L2 reuse: the C4 root product read
+  // 96 GB of DRAM for 4.5 GB of operands).  The 64 x 32 kernel is held to 3 CTAs per SM by its
+  // launch bounds (round 2's first grouped order raised it to 180 registers, 2 CTAs per SM).
   const int tilesN = (g.N + BN - 1) / BN;
-  const int m0 = (blockIdx.x / tilesN) * BM, n0 = (blockIdx.x % tilesN) * BN;
+  int m0, n0;
+  constexpr bool kGroup = BM == 64 && BN == 32;  // only the long-K merge tile (registers elsewhere)
+  if (!kGroup || g.group_m <= 1) {
+    m0 = (blockIdx.x / tilesN) * BM;
+    n0 = (blockIdx.x % tilesN) * BN;
+  } else {
+    const int tilesM = (g.M + BM - 1) / BM, per_group = g.group_m * tilesN, grp = blockIdx.x / per_group;
+    const int first_m = grp * g.group_m, gm = min(tilesM - first_m, g.group_m), local = blockIdx.x - grp * per_group;
+    m0 = (first_m + local % gm) * BM;
+    n0 = (local / gm) * BN;
+  }
 
   // Fixed per-thread load coordinates: A column (k) and B column (n) are fixed across the
   // unrolled iterations; A rows / B rows step by NT/BK and NT/BN.
@@ -611,8 +623,10 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
   }
 }
 
-void zgemm_impl(const ZGemm& g, cudaStream_t st) {
-  if (g.M <= 0 || g.N <= 0 || g.batch <= 0) return;
+void zgemm_impl(const ZGemm& g0, cudaStream_t st) {
+  if (g0.M <= 0 || g0.N <= 0 || g0.batch <= 0) return;
+  ZGemm g = g0;
+  g.group_m = std::max(1, knob(KN_GEMM_GROUP));
   const double mn = (double)g.M * g.N, bt = (double)g.batch;
   // N <= 4 runs the GEMV kernel: bound by HBM (the A operand is read once), its own class
   const bool gemv = (g_zgemm_force < 0 && g.N <= 4) || g_zgemm_force == 9;
