@@ -48,6 +48,8 @@ enum HpsKnob {
   KN_LEAF_PANEL,       // complex leaf Schur inverse, natural order: 0 step-by-step panels, 1 block form
   KN_GEMM_BCOL,        // 1: k-fastest B loader for column-major B (s in the ABI layout)
   KN_GEMM_GROUP,       // GEMM tile order: 1 row-major, G > 1 grouped by G row blocks (L2 reuse)
+  KN_LEAF_INPLACE,     // 1: natural-order complex leaf inverse in the store's Y_i block (no Y_i copy)
+  KN_SEQ_FORCE_BAD,    // test: the natural-order complex leaf inverse fails its check at step 100
   KN_COUNT
 };
 int knob(HpsKnob k);

@@ -1085,6 +1085,9 @@ __global__ void __launch_bounds__(256, MINB) zgj_fused_kernel(zt* __restrict__ A
 constexpr int WS_NB = 28, WS_NMAX = 240;
 // 1: the leaf Schur inverse pivots from the start (HPS_SEQ_PIVOT=1; tests of the fallback path)
 __constant__ int g_seq_pivot;
+// test: the natural-order leaf Schur elimination reports a failed pivot check at step 100 (after
+// it has overwritten its in-place work matrix), so the pivoted fallback must rebuild everything
+__constant__ int g_seq_force_bad;
 // optional timeline of CTA 0 (clock64 per milestone, hps_debug_ws_trace): [panel][10]
 __device__ long long g_ws_trace[16 * 16];
 __device__ int g_ws_trace_on;
@@ -1129,6 +1132,7 @@ struct WsFinish {
   int leaf0;             // heap index of batch entry 0
   double kappa2;
   int blockpanel = 0;    // natural-order panels in block form (knob leaf_panel, DESIGN 3.12)
+  int inplace = 1;       // natural order: eliminate in the store's Y_i block (knob leaf_inplace)
 };
 
 __host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16, == 2 (mod 8)
@@ -1142,11 +1146,15 @@ __host__ __device__ inline size_t ws_smem(int n) {
 
 // Output of the in-place Gauss-Jordan result M (pivot lists plist / pstep in shared memory):
 // the plain inverse (fin.p == 0) or the fused leaf epilogue.  All 512 threads of the CTA.
+// ident: the pivot lists are the identity (natural order); then the fused epilogue fetches each
+// chunk of S^{-1} rows with cp.async (all requests in flight at once), and if M is the output's
+// own Y_i block (the natural-order leaf inverse runs in place in the store) Y_i is not copied.
 __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda, zt* __restrict__ out, int64_t ldo,
                                           int64_t obs, int n, const WsFinish& fin, const int* plist,
-                                          const int* pstep, unsigned char* smem_raw) {
+                                          const int* pstep, unsigned char* smem_raw, bool ident = false) {
   const int tid = threadIdx.x;
   zt* ob = out + (int64_t)blockIdx.x * obs;
+  const bool inplace = ident && M == ob && lda == ldo;
   if (fin.p == 0) {
     // A^{-1}(k, j) = M(plist[k], pstep[j])
     for (int e = tid; e < n * n; e += 512) {
@@ -1202,13 +1210,28 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
     const int nl = min(LPC, q - kx0);
     __syncthreads();
     emark(0);
-    for (int e = tid; e < nl * q * ni; e += 512) {
-      const int t = e / ni, j = e - t * ni;  // t = line-local row l*q + t'
-      const zt v = ldplain(M + (int64_t)plist[kx0 * q + t] * lda + pstep[j]);
-      C[e] = v;
-      __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + nb + j], v);  // Y_i
+    if (ident) {
+      for (int e = tid; e < nl * q * ni; e += 512) {
+        const int t = e / ni, j = e - t * ni;  // t = line-local row l*q + t'
+        cpa16_zfill(C + e, M + (int64_t)(kx0 * q + t) * lda + j, true);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+      asm volatile("cp.async.wait_group 0;\n" ::);
+      __syncthreads();
+      if (!inplace)
+        for (int e = tid; e < nl * q * ni; e += 512) {
+          const int t = e / ni, j = e - t * ni;
+          __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + nb + j], C[e]);  // Y_i
+        }
+    } else {
+      for (int e = tid; e < nl * q * ni; e += 512) {
+        const int t = e / ni, j = e - t * ni;  // t = line-local row l*q + t'
+        const zt v = ldplain(M + (int64_t)plist[kx0 * q + t] * lda + pstep[j]);
+        C[e] = v;
+        __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + nb + j], v);  // Y_i
+      }
+      __syncthreads();
     }
-    __syncthreads();
     emark(1);
     // Psi_i rows of these lines
     for (int e = tid; e < nl * q * nb; e += 512) {
@@ -2081,9 +2104,21 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   // trace armed with 1 (every launch) or with the matrix size n to trace
   const bool trace = (g_ws_trace_on == 1 || g_ws_trace_on == n) && blockIdx.x == 0 && tid == 0;
   if (trace) g_ws_trace[15 * 16 + 2] = t_start;
+  // natural order: the pivot rows of panel p are rows k0 .. k0 + w - 1, and their entries outside
+  // the panel (Z of the update) are final once the previous update has finished, so Z is fetched
+  // by cp.async while the panel is being factored (no staging phase)
+  const bool zpre = NAT && !fin.blockpanel;
   for (int p = 0; p < P.npan; ++p) {
     const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
     WS_MARK(p, 0);
+    if (zpre && !(p + 1 == P.npan && nv == 0)) {
+      for (int e = tid; e < w4 * nv; e += 512) {
+        const int m = e / nv, v = e - m * nv;
+        const bool ok = m < w;
+        cpa16_zfill(Zs + m * zs + v, M + (int64_t)(ok ? k0 + m : 0) * lda + (v < k0 ? v : v + w), ok);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    }
     if (NAT && fin.blockpanel) {
       // ---- natural-order panel in block form (knob leaf_panel = 1): the pivot rows are rows
       // k0 .. k0 + w - 1, so D = M[K, K] is inverted by warps 0-3 (7 rows each, lane j holds column
@@ -2236,7 +2271,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
           __syncthreads();
           if (NAT && tid == 0) {
             const zt pv = prow4[par][kk];
-            if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 0.0025 * diag2[k])) s_bad = 1;
+            if (!(fma(pv.x, pv.x, pv.y * pv.y) >= 0.0025 * diag2[k]) || (g_seq_force_bad && k == 100)) s_bad = 1;
           }
           if (warp_live) {
             const zt inv = zinv_fast(prow4[par][kk]);
@@ -2289,20 +2324,25 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       }
     if (NAT) {
       __syncthreads();
-      if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
+      if (s_bad) {  // uniform: the caller re-assembles S and pivots
+        asm volatile("cp.async.wait_group 0;\n" ::);  // no prefetched Z lands in the fallback's buffers
+        return false;
+      }
     }
     }  // panel form
     if (p + 1 == P.npan && nv == 0) break;
     // ---------------- update: C(i, J) = [i not a pivot of p] C(i, J) + T(i,:) Z(:, J) -------------
     for (int v = tid; v < nv + 16; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
     __syncthreads();  // T, pivots, colmap visible
-    for (int e = tid; e < w4 * nv; e += 512) {
-      const int m = e / nv, v = e - m * nv;
-      const bool ok = m < w;
-      const int srow = ok ? plist[k0 + m] : 0;
-      cpa16_zfill(Zs + m * zs + v, M + (int64_t)srow * lda + colmap[v], ok);
+    if (!zpre) {
+      for (int e = tid; e < w4 * nv; e += 512) {
+        const int m = e / nv, v = e - m * nv;
+        const bool ok = m < w;
+        const int srow = ok ? plist[k0 + m] : 0;
+        cpa16_zfill(Zs + m * zs + v, M + (int64_t)srow * lda + colmap[v], ok);
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
     }
-    asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
     WS_MARK(p, 2);
@@ -2384,7 +2424,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   if (singular && tid == 0) atomicCAS(info, 0, blockIdx.x + 1);
   __syncthreads();
   WS_MARK(15, 0);
-  ws_output(M, lda, out, ldo, obs, n, fin, plist, pstep, smem_raw);
+  ws_output(M, lda, out, ldo, obs, n, fin, plist, pstep, smem_raw, NAT);
   WS_MARK(15, 1);
   return true;
 }
@@ -2393,7 +2433,12 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
                                                          zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
                                                          int* __restrict__ info, const WsFinish fin) {
   if (fin.c && !g_seq_pivot && n <= 256) {
-    if (zgj_seq_body<true>(A, lda, bs, out, ldo, obs, n, info, fin)) return;
+    // natural order in place: the work matrix is the leaf operator's own Y_i block (the epilogue
+    // then leaves Y_i = S^{-1} where it is; the pivoted fallback uses the scratch matrix A)
+    const bool inpl = fin.p != 0 && fin.inplace;
+    if (inpl ? zgj_seq_body<true>(out, ldo, obs, out, ldo, obs, n, info, fin)
+             : zgj_seq_body<true>(A, lda, bs, out, ldo, obs, n, info, fin))
+      return;
     __syncthreads();
   }
   zgj_seq_body<false>(A, lda, bs, out, ldo, obs, n, info, fin);
@@ -2828,11 +2873,15 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
                            double kappa2) {
   const int q = p - 2, n = q * q, nb = 4 * q, nt = nb + n;
   if (!zgj_leaf_fused_applies(p, batch)) return false;
-  static int piv_set = -1;  // value last copied to the device symbol
-  const int piv = knob(KN_SEQ_PIVOT) != 0;
+  static int piv_set = -1, bad_set = -1;  // values last copied to the device symbols
+  const int piv = knob(KN_SEQ_PIVOT) != 0, bad = knob(KN_SEQ_FORCE_BAD) != 0;
   if (piv != piv_set) {
     HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_seq_pivot, &piv, sizeof(int)));
     piv_set = piv;
+  }
+  if (bad != bad_set) {
+    HPS_CUDA_CHECK(cudaMemcpyToSymbol(g_seq_force_bad, &bad, sizeof(int)));
+    bad_set = bad;
   }
   static bool wattr = false;
   if (!wattr) {
@@ -2851,7 +2900,8 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
     auto kern = choose_regime(n, batch) == REG_SEQ ? zgj_seq_kernel : zgj_ws_kernel;
     kern<<<nbatch, 512, ws_smem(n), st>>>(
         S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
-        info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2, knob(KN_LEAF_PANEL)});
+        info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2, knob(KN_LEAF_PANEL),
+                       knob(KN_LEAF_INPLACE)});
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
   }

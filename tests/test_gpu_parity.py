@@ -119,10 +119,14 @@ def test_natural_order_merge_inverses_all_levels():
 def test_leaf_schur_natural_and_pivoted_paths():
     """The complex interior Schur inverse (leaf_mode 0 with complex c) runs in natural order
     (DESIGN.md 3.12); the seq_pivot knob forces the pivoted path; leaf_panel switches the natural-order
-    panels between the step-by-step and the block form.  All vs the oracle."""
+    panels between the step-by-step and the block form; leaf_inplace 0 eliminates in the scratch matrix
+    instead of the store's Y_i block; seq_force_bad makes the natural-order elimination fail at step 100
+    (after it has overwritten its work matrix), so the pivoted fallback must redo the leaf.  All vs the
+    oracle."""
     g, c, s, t = problem(2, 1, 16, 7.0, 7.0 + 1j)
     c = c + 0.05j
-    for knobs in ({}, {"seq_pivot": 1}, {"leaf_panel": 1}, {"leaf_panel": 1 - hps.debug_get("leaf_panel")}):
+    for knobs in ({}, {"seq_pivot": 1}, {"leaf_panel": 1}, {"leaf_panel": 1 - hps.debug_get("leaf_panel")},
+                  {"leaf_inplace": 0}, {"seq_force_bad": 1}, {"seq_force_bad": 1, "leaf_inplace": 0}):
         with hps.debug_knobs(**knobs):
             S = hps.Solver(g, 16, 7.0, 7.0 + 1j, c, keep_all_R=True)
             assert S.leaf_path() == 0
