@@ -1233,40 +1233,26 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
       __syncthreads();
     }
     emark(1);
-    // Psi_i rows of these lines: two outputs per thread and iteration, two chains each (the dot
-    // products are latency-bound; four independent chains keep the FP64 pipe busy)
-    {
-      const int tot = nl * q * nb;
-      auto psi_dot = [&](int e, zt& acc) {
-        const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
-        const zt* Cr = C + t * ni;
-        zt acc1 = make_double2(0.0, 0.0);
-        acc = make_double2(0.0, 0.0);
-        const bool yl = edge == 0 || edge == 2;  // S / N: y-line ix = kk; E / W: x-line iy = kk
-        const int side = yl ? (edge == 0 ? 0 : 1) : (edge == 3 ? 0 : 1);
-        const zt* Ub = yl ? Uby : Ubx;
-        const int cs = yl ? q : 1, c0 = yl ? kk : kk * q;
+    // Psi_i rows of these lines
+    for (int e = tid; e < nl * q * nb; e += 512) {
+      const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
+      const zt* Cr = C + t * ni;
+      // two independent accumulation chains (even / odd terms): the dot products are latency-bound
+      zt acc = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
+      const bool yl = edge == 0 || edge == 2;  // S / N: y-line ix = kk; E / W: x-line iy = kk
+      const int side = yl ? (edge == 0 ? 0 : 1) : (edge == 3 ? 0 : 1);
+      const zt* Ub = yl ? Uby : Ubx;
+      const int cs = yl ? q : 1, c0 = yl ? kk : kk * q;
 #pragma unroll 7
-        for (int t2 = 0; t2 + 1 < q; t2 += 2) {
-          zmac(acc, Cr[c0 + t2 * cs], Ub[t2 * 2 + side]);
-          zmac(acc1, Cr[c0 + (t2 + 1) * cs], Ub[t2 * 2 + 2 + side]);
-        }
-        if (q & 1) zmac(acc, Cr[c0 + (q - 1) * cs], Ub[(q - 1) * 2 + side]);
-        acc.x += acc1.x;
-        acc.y += acc1.y;
-      };
-      for (int e = tid; e < tot; e += 1024) {
-        const int e2 = e + 512;
-        zt a0, a1 = make_double2(0.0, 0.0);
-        psi_dot(e, a0);
-        if (e2 < tot) psi_dot(e2, a1);
-        Pc[e] = a0;
-        __stcs(&base[(int64_t)(nb + kx0 * q + e / nb) * nt + (e % nb)], a0);
-        if (e2 < tot) {
-          Pc[e2] = a1;
-          __stcs(&base[(int64_t)(nb + kx0 * q + e2 / nb) * nt + (e2 % nb)], a1);
-        }
+      for (int t2 = 0; t2 + 1 < q; t2 += 2) {
+        zmac(acc, Cr[c0 + t2 * cs], Ub[t2 * 2 + side]);
+        zmac(acc1, Cr[c0 + (t2 + 1) * cs], Ub[t2 * 2 + 2 + side]);
       }
+      if (q & 1) zmac(acc, Cr[c0 + (q - 1) * cs], Ub[(q - 1) * 2 + side]);
+      acc.x += acc1.x;
+      acc.y += acc1.y;
+      Pc[e] = acc;
+      __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + b], acc);
     }
     emark(2);
     // Y_b: W_kx, E_kx complete on each line; S/N (y-lines) accumulate in registers
@@ -2143,6 +2129,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
         Ts[e] = (i < n && j < w) ? ldplain(M + (int64_t)i * lda + k0 + j) : make_double2(0.0, 0.0);
       }
       __syncthreads();
+      WS_MARK(p, 4);
       zt(*Dv)[NB + 1] = reinterpret_cast<zt(*)[NB + 1]>(Zs);  // D^{-1} (Z staging area is free now)
       if (wp < 4) {
         constexpr int RW = NB / 4;  // rows per warp
@@ -2192,6 +2179,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
           if (lane < NB) Dv[wp * RW + t][lane] = d[t];
       }
       __syncthreads();
+      WS_MARK(p, 5);
       if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
       // T[r, :] = -M[r, K] D^{-1} for rows r outside K, D^{-1} for rows in K (one row tile per unit)
       for (int mt = wp; mt < MT; mt += 16) {
@@ -2226,6 +2214,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
         }
       }
       __syncthreads();
+      WS_MARK(p, 6);
       for (int e = tid; e < n * w; e += 512) {  // the panel columns of M <- T (in place)
         const int i = e / w, j = e - i * w;
         M[(int64_t)i * lda + k0 + j] = Ts[i * NB + j];
