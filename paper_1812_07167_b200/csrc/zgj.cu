@@ -2107,7 +2107,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   // natural order: the pivot rows of panel p are rows k0 .. k0 + w - 1, and their entries outside
   // the panel (Z of the update) are final once the previous update has finished, so Z is fetched
   // by cp.async while the panel is being factored (no staging phase)
-  const bool zpre = NAT && !fin.blockpanel;
+  const bool zpre = NAT && fin.blockpanel != 1;
   for (int p = 0; p < P.npan; ++p) {
     const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
     WS_MARK(p, 0);
@@ -2124,14 +2124,64 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       // k0 .. k0 + w - 1, so D = M[K, K] is inverted by warps 0-3 (7 rows each, lane j holds column
       // j in registers, one 128-thread named barrier per step), then T = -M[rows outside K, K] D^{-1}
       // runs on DMMA in all 16 warps from the panel staged in shared memory; T[K] = D^{-1}. ----
-      for (int e = tid; e < mtr * NB; e += 512) {  // stage the panel (zero padding rows / columns)
-        const int i = e / NB, j = e - i * NB;
-        Ts[e] = (i < n && j < w) ? ldplain(M + (int64_t)i * lda + k0 + j) : make_double2(0.0, 0.0);
+      // (leaf_panel = 2: the panel is staged by cp.async and D^{-1} is formed by all 512 threads,
+      // one natural-order step per barrier on ping-pong copies of D in shared memory placed after
+      // Z, so Z is still prefetched during the panel)
+      const bool pp = fin.blockpanel == 2;
+      if (pp) {
+        for (int e = tid; e < mtr * NB; e += 512) {
+          const int i = e / NB, j = e - i * NB;
+          const bool ok = i < n && j < w;
+          cpa16_zfill(Ts + e, M + (int64_t)(ok ? i : 0) * lda + k0 + (ok ? j : 0), ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 0;\n" ::);  // the panel (and the Z prefetch issued before it)
+      } else {
+        for (int e = tid; e < mtr * NB; e += 512) {  // stage the panel (zero padding rows / columns)
+          const int i = e / NB, j = e - i * NB;
+          Ts[e] = (i < n && j < w) ? ldplain(M + (int64_t)i * lda + k0 + j) : make_double2(0.0, 0.0);
+        }
       }
       __syncthreads();
       WS_MARK(p, 4);
       zt(*Dv)[NB + 1] = reinterpret_cast<zt(*)[NB + 1]>(Zs);  // D^{-1} (Z staging area is free now)
-      if (wp < 4) {
+      if (pp) {
+        zt* Da = Zs + NB * zs;            // [NB][NB + 1] x 2 after Z
+        zt* Db = Da + NB * (NB + 1);
+        constexpr int DS = NB + 1;
+        for (int e = tid; e < NB * NB; e += 512) {
+          const int r = e / NB, c = e - r * NB;
+          Da[r * DS + c] = (r < w && c < w) ? Ts[(k0 + r) * NB + c] : make_double2(r == c ? 1.0 : 0.0, 0.0);
+        }
+        __syncthreads();
+        for (int k = 0; k < w; ++k) {
+          const zt* src = (k & 1) ? Db : Da;
+          zt* dst = (k & 1) ? Da : Db;
+          const zt pv = src[k * DS + k];
+          const zt inv = zinv_fast(pv);
+          if (tid == 0 && !(fma(pv.x, pv.x, pv.y * pv.y) >= 0.0025 * diag2[k0 + k])) s_bad = 1;
+          for (int e = tid; e < NB * NB; e += 512) {
+            const int i = e / NB, j = e - i * NB;
+            zt v;
+            if (i == k) {
+              v = j == k ? inv : zmul(src[k * DS + j], inv);
+            } else {
+              const zt fi = zmul(src[i * DS + k], inv);
+              if (j == k) {
+                v = make_double2(-fi.x, -fi.y);
+              } else {
+                const zt pk = src[k * DS + j];
+                v = src[i * DS + j];
+                v.x = fma(-fi.x, pk.x, fma(fi.y, pk.y, v.x));
+                v.y = fma(-fi.x, pk.y, fma(-fi.y, pk.x, v.y));
+              }
+            }
+            dst[i * DS + j] = v;
+          }
+          __syncthreads();
+        }
+        Dv = reinterpret_cast<zt(*)[NB + 1]>((w & 1) ? Db : Da);
+      } else if (wp < 4) {
         constexpr int RW = NB / 4;  // rows per warp
         zt d[RW];
         const int jl = lane < NB ? lane : 0;
@@ -2180,7 +2230,10 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       }
       __syncthreads();
       WS_MARK(p, 5);
-      if (s_bad) return false;  // uniform: the caller re-assembles S and pivots
+      if (s_bad) {  // uniform: the caller re-assembles S and pivots
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        return false;
+      }
       // T[r, :] = -M[r, K] D^{-1} for rows r outside K, D^{-1} for rows in K (one row tile per unit)
       for (int mt = wp; mt < MT; mt += 16) {
         const int r = mt * 8 + (lane >> 2);
@@ -2901,7 +2954,11 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nbatch = std::min(65535, batch - b0);
     auto kern = choose_regime(n, batch) == REG_SEQ ? zgj_seq_kernel : zgj_ws_kernel;
-    kern<<<nbatch, 512, ws_smem(n), st>>>(
+    // leaf_panel 2: two (NB x NB+1) ping-pong copies of the panel's diagonal block after Z
+    const int bp = knob(KN_LEAF_PANEL);
+    const size_t dbytes = bp == 2 ? sizeof(zt) * 2 * WS_NB * (WS_NB + 1) : 0;
+    if (ws_smem(n) + dbytes > ws_smem(WS_NMAX)) throw HpsError{-1, "leaf_panel 2: shared memory"};
+    kern<<<nbatch, 512, ws_smem(n) + dbytes, st>>>(
         S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
         info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2, knob(KN_LEAF_PANEL),
                        knob(KN_LEAF_INPLACE)});
