@@ -2424,9 +2424,12 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
         }
     };
     Unit cur, nxt;
+    // row tiles of 8 up to n (the padding rows of the last 16-row block carry no work), and a last
+    // column block with only 8 valid columns runs half the DMMAs
+    const int MTu = (n + 7) >> 3;
     int mt = wp, npr = 0;
-    while (mt >= MT) {
-      mt -= MT;
+    while (mt >= MTu) {
+      mt -= MTu;
       ++npr;
     }
     bool have = npr < NPR;
@@ -2435,8 +2438,8 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       cur = nxt;
       const int cmt = mt, cnpr = npr;
       mt += 16;
-      while (mt >= MT) {
-        mt -= MT;
+      while (mt >= MTu) {
+        mt -= MTu;
         ++npr;
       }
       have = npr < NPR;
@@ -2452,18 +2455,30 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
         }
       const zt* Trow = Ts + (cmt * 8 + (lane >> 2)) * NB + (lane & 3);
       const zt* Zc = Zs + (lane & 3) * zs + cnpr * 16 + (lane >> 2);
+      if (cnpr * 16 + 8 < nv) {
 #pragma unroll 7
-      for (int k4 = 0; k4 < K4; ++k4) {
-        const zt av = Trow[k4 * 4];
-        const zt b0 = Zc[k4 * 4 * zs], b1 = Zc[k4 * 4 * zs + 8];
-        dmma884(ar[0][0], ar[0][1], av.x, b0.x);
-        dmma884(ar[1][0], ar[1][1], av.x, b1.x);
-        dmma884(ai[0][0], ai[0][1], av.x, b0.y);
-        dmma884(ai[1][0], ai[1][1], av.x, b1.y);
-        dmma884(ar[0][0], ar[0][1], -av.y, b0.y);
-        dmma884(ar[1][0], ar[1][1], -av.y, b1.y);
-        dmma884(ai[0][0], ai[0][1], av.y, b0.x);
-        dmma884(ai[1][0], ai[1][1], av.y, b1.x);
+        for (int k4 = 0; k4 < K4; ++k4) {
+          const zt av = Trow[k4 * 4];
+          const zt b0 = Zc[k4 * 4 * zs], b1 = Zc[k4 * 4 * zs + 8];
+          dmma884(ar[0][0], ar[0][1], av.x, b0.x);
+          dmma884(ar[1][0], ar[1][1], av.x, b1.x);
+          dmma884(ai[0][0], ai[0][1], av.x, b0.y);
+          dmma884(ai[1][0], ai[1][1], av.x, b1.y);
+          dmma884(ar[0][0], ar[0][1], -av.y, b0.y);
+          dmma884(ar[1][0], ar[1][1], -av.y, b1.y);
+          dmma884(ai[0][0], ai[0][1], av.y, b0.x);
+          dmma884(ai[1][0], ai[1][1], av.y, b1.x);
+        }
+      } else {
+#pragma unroll 7
+        for (int k4 = 0; k4 < K4; ++k4) {
+          const zt av = Trow[k4 * 4];
+          const zt b0 = Zc[k4 * 4 * zs];
+          dmma884(ar[0][0], ar[0][1], av.x, b0.x);
+          dmma884(ai[0][0], ai[0][1], av.x, b0.y);
+          dmma884(ar[0][0], ar[0][1], -av.y, b0.y);
+          dmma884(ai[0][0], ai[0][1], av.y, b0.x);
+        }
       }
       if (cur.rr < n) {
         zt* rowp = M + (int64_t)cur.rr * lda;
