@@ -757,6 +757,7 @@ void leaves_to_gl(hps_handle& H, const zt* Rc);
 void build_leaves_cheb(hps_handle& H, const zt* c_dev, int chunk_opt, DevBuf& Rcheb);
 
 void build_leaves(hps_handle& H, const zt* c_dev, int chunk_opt) {
+  NvtxRange nv("hps leaves (%d)", H.nleaf);
   DevBuf Rcheb;  // Chebyshev leaf R when the merges see the Gauss-Legendre edge representation
   build_leaves_cheb(H, c_dev, chunk_opt, Rcheb);
   if (H.gle) leaves_to_gl(H, Rcheb.as<zt>());
@@ -1016,6 +1017,7 @@ void form_and_invert_W(hps_handle& H, int d, int np, const zt* R33a, const zt* R
 
 void build_merge(hps_handle& H, int d) {
   MergeLevel& M = H.lev[d];
+  NvtxRange nv("hps merge d=%d n3=%d x%d", d, M.n3, M.nparent);
   const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau, nbc = M.nbc;
   const int64_t cs2 = (int64_t)nbc * nbc;
   const zt* Ra = H.R[d + 1].as<zt>();
@@ -1192,6 +1194,7 @@ ChildR gather_children_R(hps_handle& H, int d, DevBuf& buf) {
 }
 
 void build_merge_dist(hps_handle& H, int d) {
+  NvtxRange nv("hps merge (sharded) d=%d", d);
   MergeLevel& M = H.lev[d];
   const DistLevel& P = H.dl[d];
   const int n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau;
@@ -1402,6 +1405,7 @@ double solve_up_level(hps_handle& H, MergeLevel& M, int np, int nrhs, const zt* 
 // (ABI [2^Lb][R][nb(Lb)]) for a top handle; NULL = zero body load.  Keeps u~, t~ in H.ss.
 // h_root (ABI [R][nb(0)], device) receives the root's outgoing particular data if non-NULL.
 void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
+  NvtxRange nv("hps solve up (%d rhs)", nrhs);
   cudaStream_t st = H.st;
   const int Lb = H.Lb, nt = H.nt, nb = H.nbc, ni = H.ni;
   const int64_t R = nrhs;
@@ -1485,6 +1489,7 @@ void solve_up_impl(hps_handle& H, int nrhs, const zt* bottom, zt* h_root) {
 // Downward pass (lines 10-18).  t_root: ABI [R][nb(0)].  Leaf handle: u out (ABI
 // [R][nleaf][nt], natural order).  Top handle: t of the depth-Lb boxes (ABI [2^Lb][R][nb(Lb)]).
 void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
+  NvtxRange nv("hps solve down (%d rhs)", nrhs);
   cudaStream_t st = H.st;
   const int Lb = H.Lb, nt = H.nt, nb = H.nbl;
   const int64_t R = nrhs;
@@ -1575,6 +1580,7 @@ void solve_down_impl(hps_handle& H, int nrhs, const zt* t_root, zt* outp) {
 // them in rank order (so the result does not depend on the transport).
 // h_mine: ABI [R][nb(D)] outgoing data of this rank's subtree root (NULL: s = 0, no upward pass).
 void solve_up_dist(hps_handle& T, int nrhs, const zt* h_mine) {
+  NvtxRange nv("hps solve up (sharded top)");
   cudaStream_t st = T.st;
   SolveState& S = T.ss;
   S.reset(T.D);
@@ -1607,6 +1613,7 @@ void solve_up_dist(hps_handle& T, int nrhs, const zt* h_mine) {
 
 // t_root: ABI [R][nb(0)]; t_mine (out): ABI [R][nb(D)] incoming data of this rank's subtree root.
 void solve_down_dist(hps_handle& T, int nrhs, const zt* t_root, zt* t_mine) {
+  NvtxRange nv("hps solve down (sharded top)");
   cudaStream_t st = T.st;
   SolveState& S = T.ss;
   const bool has_s = S.has_s && S.nrhs == nrhs;

@@ -3,7 +3,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
 #include <string>
+
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges are no-ops unless a tool (nsys, ncu) injects
 
 typedef double2 zt;  // complex128, interleaved (re, im)
 
@@ -212,4 +215,19 @@ struct ProfScope {
   cudaStream_t st;
   ProfScope(int cls, double flops, double bytes, cudaStream_t s) : st(s) { prof_begin(cls, flops, bytes, s); }
   ~ProfScope() { prof_end(st); }
+};
+
+// NVTX range for the duration of a scope (build / solve phases and merge levels; visible in
+// ncu --nvtx and nsys timelines, free when no tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  template <class... A>
+  NvtxRange(const char* fmt, A... a) {
+    char buf[96];
+    snprintf(buf, sizeof(buf), fmt, a...);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
