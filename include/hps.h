@@ -301,9 +301,29 @@ int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* out,
  * (n <= 496), 7 sequential-phase CTA per matrix (n <= 240).  eps, rep_ms (ms), theta_o: caller
  * arrays of length 8;
  * infeasible regimes get -1.  Returns the chosen regime (> 0) or a negative error code.
- * hps_plan_set / hps_plan_clear: set (regime 0 = remove) / forget plan entries.
+ * hps_plan_set / hps_plan_clear: set (regime 0 = remove) / forget plan entries (hps_plan_clear also
+ * forgets the GEMM tile plan of hps_plan_solve).
  * hps_plan_regime: the regime the library will use for (n, nbox). */
 int hps_rep_actions(const hps_grid* g, int p, int maxlev, int* n_out, int* nbox_out);
+
+/* Solve-stage representative actions (Table 1's upward and downward matvec rows, the
+ * solve half of the planner).  hps_solve_actions: host-only; writes for
+ * every batched matrix product of Algorithm 2 on the tree of g at order p with nrhs right-hand
+ * sides 7 ints to out[7 i ...]: level (-1 = leaf level, d = merge depth of the parent boxes),
+ * kind (0 leaf u~ = Y s, 1 leaf u = Psi t (+ u~), 2 Upsilon action R33b h3a - h3b and R33a t~a +
+ * h3a, 3 W^{-1} (.), 4 Gamma^tau action R13a t~a + h1a (and R23b t~b + h2b), 5 Phi t (+ t~)), M, N
+ * (= nrhs), K, batch (boxes of the level), cin (1: the product adds a vector).  Returns the
+ * number of actions, or HPS_EINVAL (also when maxn > 0 is too small; maxn = 0 only counts).
+ * hps_plan_solve: times every distinct shape on the current device with each candidate tile
+ * configuration of the library's GEMM (synthetic operands, a sample of the batch covering several
+ * waves, extrapolated to the full batch) and records, for later calls in this process, the
+ * fastest one where it beats the fixed rule by more than 3 %.  actions: [maxn][7] as above;
+ * chosen[i]: the configuration recorded for action i (-1: the fixed rule stays); t_rule / t_best
+ * (ms): the rule's and the chosen configuration's extrapolated times.  Returns the number of
+ * actions or a negative error code.  hps_plan_clear forgets these entries too. */
+int hps_solve_actions(const hps_grid* g, int p, int nrhs, int maxn, int32_t* out);
+int hps_plan_solve(const hps_grid* g, int p, int nrhs, int maxn, int32_t* actions, int32_t* chosen, double* t_rule,
+                   double* t_best);
 int hps_plan_inverse(int n, int nbox, double* eps, double* rep_ms, int* theta_o);
 int hps_plan_set(int n, int nbox, int regime);
 int hps_plan_clear(void);

@@ -11,12 +11,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cmath>
 #include <complex>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -2642,7 +2644,83 @@ int hps_plan_set(int n, int nbox, int regime) {
 
 int hps_plan_clear(void) {
   zgj_plan_clear();
+  zgemm_plan_clear();
   return HPS_OK;
+}
+
+int hps_solve_actions(const hps_grid* g, int p, int nrhs, int maxn, int32_t* out) {
+  if (!g || p < 4 || nrhs < 1 || !is_pow2(g->nx) || !is_pow2(g->ny) || maxn < 0 || (!out && maxn > 0)) {
+    hps_set_error("hps_solve_actions: invalid argument");
+    return HPS_EINVAL;
+  }
+  const int q = p - 2, nt = p * p - 4, ni = q * q, nb = 4 * q, nleaf = g->nx * g->ny;
+  std::vector<std::array<int32_t, 7>> A;
+  // leaf level (Algorithm 2 lines 2-3 and 13): u~ = Y s, u = Psi t (+ u~)
+  A.push_back({-1, 0, nt, nrhs, ni, nleaf, 0});
+  A.push_back({-1, 1, nt, nrhs, nb, nleaf, 1});
+  A.push_back({-1, 1, nt, nrhs, nb, nleaf, 0});
+  int a = g->nx, b = g->ny, d = 0;
+  while (!(a == 1 && b == 1)) {
+    const bool vertical = a >= b;
+    if (vertical) a /= 2;
+    else b /= 2;
+    const int nbc = 2 * (a + b) * q, n3 = vertical ? b * q : a * q, n1 = nbc - n3, ntau = 2 * n1, np = 1 << d;
+    // upward (lines 5-8, the Upsilon and Gamma^tau actions): R33b h3a - h3b, W^{-1} (.), R13a t~a + h1a,
+    // R33a t~a + h3a, R23b t~b + h2b;  downward (line 16): Phi t (+ t~)
+    A.push_back({d, 2, n3, nrhs, n3, np, 1});
+    A.push_back({d, 3, n3, nrhs, n3, np, 0});
+    A.push_back({d, 4, n1, nrhs, n3, np, 1});
+    A.push_back({d, 5, n3, nrhs, ntau, np, 1});
+    A.push_back({d, 5, n3, nrhs, ntau, np, 0});
+    ++d;
+  }
+  const int n = (int)A.size();
+  for (int i = 0; i < std::min(n, maxn); ++i) std::memcpy(out + 7 * i, A[i].data(), sizeof(int32_t) * 7);
+  if (maxn > 0 && maxn < n) {
+    hps_set_error("hps_solve_actions: maxn too small");
+    return HPS_EINVAL;
+  }
+  return n;
+}
+
+int hps_plan_solve(const hps_grid* g, int p, int nrhs, int maxn, int32_t* actions, int32_t* chosen, double* t_rule,
+                   double* t_best) {
+  const int n = hps_solve_actions(g, p, nrhs, 0, nullptr);
+  if (n < 0) return n;
+  if (maxn < n || !actions || !chosen || !t_rule || !t_best) {
+    hps_set_error("hps_plan_solve: invalid argument (maxn must hold every action)");
+    return HPS_EINVAL;
+  }
+  hps_solve_actions(g, p, nrhs, maxn, actions);
+  try {
+    cudaStream_t st;
+    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int dev;
+    HPS_CUDA_CHECK(cudaGetDevice(&dev));
+    retain_pool(dev);
+    std::map<std::array<int32_t, 5>, std::array<double, 3>> done;  // shape -> (cfg, rule, best)
+    for (int i = 0; i < n; ++i) {
+      const int32_t* a = actions + 7 * i;
+      const std::array<int32_t, 5> key{a[2], a[3], a[4], a[5], a[6]};
+      auto it = done.find(key);
+      if (it == done.end()) {
+        double tc[16], tr = 0;
+        int cands[16], nc = 0;
+        const int c = zgemm_plan_shape(a[2], a[3], a[4], a[5], a[6] != 0, tc, &tr, cands, &nc, st);
+        double best = tr;
+        for (int k = 0; k < nc; ++k)
+          if (tc[k] > 0 && tc[k] < best) best = tc[k];
+        it = done.emplace(key, std::array<double, 3>{(double)c, tr, c >= 0 ? best : tr}).first;
+      }
+      chosen[i] = (int32_t)it->second[0];
+      t_rule[i] = it->second[1];
+      t_best[i] = it->second[2];
+    }
+    cudaStreamDestroy(st);
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+  return n;
 }
 
 int hps_plan_regime(int n, int nbox) { return n > 0 && nbox > 0 ? zgj_regime_of(n, nbox) : HPS_EINVAL; }

@@ -126,6 +126,16 @@ struct ZGemm {
 
 void zgemm(const ZGemm& g, cudaStream_t st);
 
+// Planned tile configurations of batched products (zgemm.cu, representative-action planner of the
+// solve's matrix products): lookup (-1: none), set (cfg -1 removes), clear, candidates for N,
+// and timing of one shape (records the fastest configuration if it beats the fixed rule by 3 %).
+int zgemm_plan_lookup(int M, int N, int K, int batch, bool cin);
+void zgemm_plan_set(int M, int N, int K, int batch, bool cin, int cfg);
+void zgemm_plan_clear();
+int zgemm_candidates(int N, int* out);
+int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, double* t_rule, int* cands, int* ncand,
+                     cudaStream_t st);
+
 // Batched 2-D gather/scale copy: C[b](i, j) = alpha * A[b](i, j) (+ beta * Cin), maps as above.
 struct ZCopy {
   int M = 0, N = 0, batch = 1;

@@ -8,8 +8,12 @@
 // Operands are staged global -> shared with cp.async (16 B = one complex element, zero-fill
 // for ragged edges and for "zero" map entries), double-buffered.  Shared-memory strides are
 // chosen so that the 8x4 / 4x8 DMMA fragments load as conflict-free 16-byte LDS.
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <vector>
 
 #include "hps_internal.cuh"
@@ -598,18 +602,22 @@ void zgemm(const ZGemm& g, cudaStream_t st) {
 
 thread_local int g_zgemm_force = -1;  // tile configuration override (tests / tuning)
 
+static bool bcol_applies(const ZGemm& g) {
+  return g.B.rs == 1 && g.B.cs > 1 && !g.B.rmap && !g.B.cmap && g.B.cskip_len == 0 && knob(KN_GEMM_BCOL);
+}
+
 bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
   switch (cfg) {
     case 0: launch<64, 8, 16, 8>(g, st); return true;
     case 1: launch<16, 16, 8, 8>(g, st); return true;
-    case 2: launch<32, 32, 16, 16>(g, st); return true;
+    case 2: bcol_applies(g) ? launch<32, 32, 16, 16, true>(g, st) : launch<32, 32, 16, 16>(g, st); return true;
     case 3: launch<64, 64, 32, 32>(g, st); return true;
     case 4: launch<64, 64, 32, 16>(g, st); return true;
     case 5: launch<64, 32, 32, 16>(g, st); return true;
     case 6: launch<32, 64, 16, 32>(g, st); return true;
     case 7: launch<128, 64, 32, 32>(g, st); return true;
     case 8: launch<64, 64, 16, 32>(g, st); return true;
-    case 10: launch<64, 16, 16, 16>(g, st); return true;
+    case 10: bcol_applies(g) ? launch<64, 16, 16, 16, true>(g, st) : launch<64, 16, 16, 16>(g, st); return true;
     case 11: launch<128, 16, 32, 16>(g, st); return true;
     case 12: launch<64, 16, 32, 8>(g, st); return true;
     case 13: launch<32, 16, 16, 16>(g, st); return true;
@@ -628,12 +636,18 @@ void zgemm_impl(const ZGemm& g0, cudaStream_t st) {
   ZGemm g = g0;
   g.group_m = std::max(1, knob(KN_GEMM_GROUP));
   const double mn = (double)g.M * g.N, bt = (double)g.batch;
+  // a forced configuration (tests / tuning), else the planned one of this shape (zgemm_plan_shape)
+  int force = g_zgemm_force;
+  if (force == -1) {
+    const int pc = zgemm_plan_lookup(g.M, g.N, g.K, g.batch, g.Cin.ptr != nullptr);
+    if (pc >= 0) force = pc;
+  }
   // N <= 4 runs the GEMV kernel: bound by HBM (the A operand is read once), its own class
-  const bool gemv = (g_zgemm_force < 0 && g.N <= 4) || g_zgemm_force == 9;
+  const bool gemv = (force < 0 && g.N <= 4) || force == 9;
   ProfScope ps(gemv ? K_ZGEMV : K_ZGEMM, 8.0 * mn * g.K * bt,
                16.0 * bt * ((double)g.M * g.K + (double)g.K * g.N + mn * (g.Cin.ptr ? 2.0 : 1.0)), st);
-  if (g_zgemm_force >= 0 && launch_cfg(g_zgemm_force, g, st)) return;
-  if (g.N <= 4 && g_zgemm_force != -2) {
+  if (force >= 0 && launch_cfg(force, g, st)) return;
+  if (g.N <= 4 && force != -2) {
     if (g.N == 1)
       launch_gemv<1>(g, st);
     else
@@ -647,7 +661,7 @@ void zgemm_impl(const ZGemm& g0, cudaStream_t st) {
   const bool small_k16 = knob(KN_GEMM_SMALLK) != 0;
   const int nsm = hps_num_sms();
   // column-major B without maps (s in the ABI layout): the k-fastest B loader
-  const bool bcol = g.B.rs == 1 && g.B.cs > 1 && !g.B.rmap && !g.B.cmap && g.B.cskip_len == 0 && knob(KN_GEMM_BCOL);
+  const bool bcol = bcol_applies(g);
   if (g.N <= 8)
     launch<64, 8, 16, 8>(g, st);
   else if (g.N <= 16 && g.M > 16 && g.K >= 1024 && (int64_t)((g.M + 63) / 64) * g.batch < nsm)
@@ -727,4 +741,144 @@ void zcopy(const ZCopy& c, cudaStream_t st) {
     zcopy_kernel<uint64_t><<<blocks, 256, 0, st>>>(c);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
+}
+
+// ---------------------------------------------------------------------------
+// Representative-action plan of the GEMM tile configuration (Table 1's
+// upward / downward matvec rows): the paper times each level's representative action for every
+// thread split once per machine and keeps the fastest; here the "split" of a batched product is
+// its tile configuration (CTA granularity), timed on synthetic operands of the same shape (a
+// sample of the batch covering several waves) and recorded per (M, N, K, batch, Cin) for the
+// rest of the process.  Shapes without an entry use the fixed rules of zgemm_impl.
+// ---------------------------------------------------------------------------
+namespace {
+std::mutex g_plan_mu;
+std::map<std::tuple<int, int, int, int, int>, int> g_plan;
+std::atomic<int> g_plan_n{0};
+
+__global__ void zfill_kernel(zt* p, int64_t n, uint64_t seed) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t h = ((uint64_t)e + seed) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 31;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 29;
+    p[e] = make_double2((double)(h >> 11) * 1.1102230246251565e-16 - 0.5,
+                        (double)((h * 0x94D049BB133111EBull) >> 11) * 1.1102230246251565e-16 - 0.5);
+  }
+}
+}  // namespace
+
+int zgemm_plan_lookup(int M, int N, int K, int batch, bool cin) {
+  if (g_plan_n.load(std::memory_order_relaxed) == 0) return -1;
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto it = g_plan.find(std::make_tuple(M, N, K, batch, (int)cin));
+  return it == g_plan.end() ? -1 : it->second;
+}
+
+void zgemm_plan_set(int M, int N, int K, int batch, bool cin, int cfg) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  const auto key = std::make_tuple(M, N, K, batch, (int)cin);
+  if (cfg < 0) g_plan.erase(key);
+  else g_plan[key] = cfg;
+  g_plan_n.store((int)g_plan.size());
+}
+
+void zgemm_plan_clear() {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_plan.clear();
+  g_plan_n.store(0);
+}
+
+int zgemm_candidates(int N, int* out) {
+  static const int c4[] = {9, 0, 1}, c16[] = {0, 1, 10, 12, 13, 2}, cbig[] = {2, 5, 1, 6, 13, 10};
+  const int* c = N <= 4 ? c4 : N <= 16 ? c16 : cbig;
+  const int n = N <= 4 ? 3 : 6;
+  for (int i = 0; i < n; ++i) out[i] = c[i];
+  return n;
+}
+
+// Times every candidate configuration (and the fixed rule, cfg -1) of one shape on a sample of
+// the batch; records the fastest in the plan if it beats the rule by more than 3 %.  Writes the
+// per-candidate times extrapolated to the full batch (ms, -1 where infeasible) to t_out[0..ncand)
+// and the rule's to *t_rule; returns the chosen configuration (-1: the rule).
+int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, double* t_rule, int* cands, int* ncand,
+                     cudaStream_t st) {
+  const int nc = zgemm_candidates(N, cands);
+  *ncand = nc;
+  // sample: enough 16 x 16 tiles for ~8 waves of 8 resident CTAs on every SM
+  const int64_t t16 = (int64_t)((M + 15) / 16) * ((N + 15) / 16);
+  const int64_t want = std::max<int64_t>(1, (8LL * 8 * hps_num_sms() + t16 - 1) / t16);
+  const int bs = (int)std::min<int64_t>(batch, want);
+  const double scale = (double)batch / bs;
+  zt *A, *B, *C, *Ci = nullptr;
+  const size_t na = (size_t)M * K * bs, nb = (size_t)K * N * bs, nm = (size_t)M * N * bs;
+  HPS_CUDA_CHECK(cudaMallocAsync(&A, sizeof(zt) * std::max<size_t>(na, 1), st));
+  HPS_CUDA_CHECK(cudaMallocAsync(&B, sizeof(zt) * std::max<size_t>(nb, 1), st));
+  HPS_CUDA_CHECK(cudaMallocAsync(&C, sizeof(zt) * nm, st));
+  if (cin) HPS_CUDA_CHECK(cudaMallocAsync(&Ci, sizeof(zt) * nm, st));
+  zfill_kernel<<<592, 256, 0, st>>>(A, (int64_t)na, 1);
+  zfill_kernel<<<592, 256, 0, st>>>(B, (int64_t)nb, 2);
+  if (cin) zfill_kernel<<<592, 256, 0, st>>>(Ci, (int64_t)nm, 3);
+  ZGemm g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.batch = bs;
+  g.A.ptr = A;
+  g.A.rs = K;
+  g.A.bs = (int64_t)M * K;
+  g.B.ptr = B;
+  g.B.rs = N;
+  g.B.bs = (int64_t)K * N;
+  if (cin) {
+    g.Cin.ptr = Ci;
+    g.Cin.rs = N;
+    g.Cin.bs = (int64_t)M * N;
+    g.beta = make_double2(1.0, 0.0);
+  }
+  g.C.ptr = C;
+  g.C.rs = N;
+  g.C.bs = (int64_t)M * N;
+  cudaEvent_t e0, e1;
+  HPS_CUDA_CHECK(cudaEventCreate(&e0));
+  HPS_CUDA_CHECK(cudaEventCreate(&e1));
+  auto time_cfg = [&](int cfg) {
+    g_zgemm_force = cfg < 0 ? -3 : cfg;  // -3: the fixed rule, ignoring the plan
+    double best = 1e30;
+    for (int r = 0; r < 4; ++r) {  // first run warms up
+      HPS_CUDA_CHECK(cudaEventRecord(e0, st));
+      zgemm_impl(g, st);
+      HPS_CUDA_CHECK(cudaEventRecord(e1, st));
+      HPS_CUDA_CHECK(cudaEventSynchronize(e1));
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r) best = std::min(best, (double)ms);
+    }
+    g_zgemm_force = -1;
+    return best * scale;
+  };
+  *t_rule = time_cfg(-1);
+  int bi = -1;
+  double bt = *t_rule;
+  for (int i = 0; i < nc; ++i) {
+    if (cands[i] == 9 && N > 4) {
+      t_out[i] = -1;
+      continue;
+    }
+    t_out[i] = time_cfg(cands[i]);
+    if (t_out[i] < bt) {
+      bt = t_out[i];
+      bi = i;
+    }
+  }
+  const int chosen = (bi >= 0 && bt < 0.97 * *t_rule) ? cands[bi] : -1;
+  zgemm_plan_set(M, N, K, batch, cin, chosen);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(A, st);
+  cudaFreeAsync(B, st);
+  cudaFreeAsync(C, st);
+  if (Ci) cudaFreeAsync(Ci, st);
+  HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return chosen;
 }

@@ -150,3 +150,25 @@ def test_debug_knobs_roundtrip(L):
     for f in ("zgj.cu", "zgemm.cu", "leaf.cu", "leaf_real.cu", "comm.cu"):
         src += open(os.path.join(os.path.dirname(hps.__file__), "csrc", f)).read()
     assert "getenv" not in src
+
+
+def test_solve_actions_small_tree(L):
+    """Solve-stage representative actions (host only) for 4 x 2 leaves at p = 6, nrhs = 3: the
+    leaf products and five products per merge level with n3, n1, n_tau of the split schedule
+    (written out by hand: q = 4; d = 0 parent 4x2 -> 2x2 children, vertical, n3 = 8, n_b = 32;
+    d = 1 parent 2x2 -> 1x2, vertical, n3 = 8, n_b = 24; d = 2 parent 1x2 -> 1x1, horizontal,
+    n3 = 4, n_b = 16)."""
+    g = hps.grid(0, 2, 0, 1, 4, 2)
+    acts = hps.solve_actions(g, 6, 3)
+    got = [(a["level"], a["kind"], a["M"], a["N"], a["K"], a["batch"], a["cin"]) for a in acts]
+    exp = [(-1, 0, 32, 3, 16, 8, 0), (-1, 1, 32, 3, 16, 8, 1), (-1, 1, 32, 3, 16, 8, 0)]
+    for d, n3, nbc in ((0, 8, 32), (1, 8, 24), (2, 4, 16)):
+        n1 = nbc - n3
+        exp += [(d, 2, n3, 3, n3, 2 ** d, 1), (d, 3, n3, 3, n3, 2 ** d, 0), (d, 4, n1, 3, n3, 2 ** d, 1),
+                (d, 5, n3, 3, 2 * n1, 2 ** d, 1), (d, 5, n3, 3, 2 * n1, 2 ** d, 0)]
+    assert got == exp
+    # the W^{-1} actions are the merge levels' representative inverses of hps_rep_actions
+    ra = hps.rep_actions(g, 6)
+    w = [(a["M"], a["batch"]) for a in acts if a["kind"] == 3]
+    assert sorted(w) == sorted((n, nb) for n, nb in ra[1:])
+    assert L.hps_solve_actions(C.byref(g), 6, 3, 2, np.zeros(14, np.int32).ctypes.data) == -1   # maxn too small

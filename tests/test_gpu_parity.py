@@ -773,3 +773,24 @@ def test_planned_regimes_parity():
             S.close()
     finally:
         hps.plan_clear()
+
+
+def test_plan_solve_parity():
+    """Solve-stage planner (hps_plan_solve): every action's shape is timed with each candidate tile
+    configuration and the fastest recorded; the planned solve still matches the oracle at 1e-9 and
+    the unplanned solve to rounding (the configurations differ in tiling, not in arithmetic order
+    along K, except the GEMV kernel of N <= 4)."""
+    nx, ny, p, kappa, eta = 8, 4, 12, 15.0, 15.0 - 1j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=0.5, nrhs=16)
+    hps.plan_clear()
+    u0 = hps.Solver(g, p, kappa, eta, c).solve(s, t)
+    try:
+        plan = hps.plan_solve(g, p, 16)
+        assert len(plan) == len(hps.solve_actions(g, p, 16))
+        assert all(a["rule_ms"] > 0 and a["best_ms"] <= a["rule_ms"] * 1.0001 for a in plan)
+        u1 = hps.Solver(g, p, kappa, eta, c).solve(s, t)
+    finally:
+        hps.plan_clear()
+    O = oracle.Oracle(0.0, 1.0, 0.0, 0.5, nx, ny, p, kappa, eta, c)
+    assert rel(u1, O.solve(s, t)) < TOL
+    assert rel(u1, u0) < 1e-12
