@@ -219,6 +219,11 @@ def run_hps(args, rank, world, dist):
         # representative-action planner: measured once per machine/process,
         # outside the timed region, like the paper's representative times
         plan = {lab: hps.REGIMES[reg] for lab, n, nb, reg, tab in hps.plan_problem(g_plan, cfg.p)}
+        # the solve's matvec actions (Table 1's upward / downward rows): GEMM tile configuration per shape
+        ps = hps.plan_solve(g_plan, cfg.p, nrhs)
+        plan["solve_actions"] = {"actions": len(ps), "planned": sum(a["cfg"] >= 0 for a in ps),
+                                 "rule_ms": round(sum(a["rule_ms"] for a in ps), 3),
+                                 "planned_ms": round(sum(a["best_ms"] for a in ps), 3)}
 
     def step(profile=0, keep_root_R=True):
         S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=keep_root_R, device=local, profile=profile,
