@@ -1233,26 +1233,32 @@ __device__ __forceinline__ void ws_output(const zt* __restrict__ M, int64_t lda,
       __syncthreads();
     }
     emark(1);
-    // Psi_i rows of these lines
-    for (int e = tid; e < nl * q * nb; e += 512) {
-      const int t = e / nb, b = e - t * nb, edge = b / q, kk = b - edge * q;
-      const zt* Cr = C + t * ni;
-      // two independent accumulation chains (even / odd terms): the dot products are latency-bound
-      zt acc = make_double2(0.0, 0.0), acc1 = make_double2(0.0, 0.0);
-      const bool yl = edge == 0 || edge == 2;  // S / N: y-line ix = kk; E / W: x-line iy = kk
-      const int side = yl ? (edge == 0 ? 0 : 1) : (edge == 3 ? 0 : 1);
-      const zt* Ub = yl ? Uby : Ubx;
-      const int cs = yl ? q : 1, c0 = yl ? kk : kk * q;
+    // Psi_i rows of these lines: thread (row t, line kk) forms the four entries fed by line kk --
+    // W, E from x-line iy = kk (14 contiguous entries of the row) and S, N from y-line ix = kk --
+    // as four independent accumulation chains over one pass of 14 terms
+    for (int e = tid; e < nl * q * q; e += 512) {
+      const int t = e / q, kk = e - t * q;
+      const zt* Cx = C + t * ni + kk * q;  // x-line iy = kk
+      const zt* Cy = C + t * ni + kk;      // y-line ix = kk (stride q)
+      zt aw = make_double2(0.0, 0.0), ae = aw, as = aw, an = aw;
 #pragma unroll 7
-      for (int t2 = 0; t2 + 1 < q; t2 += 2) {
-        zmac(acc, Cr[c0 + t2 * cs], Ub[t2 * 2 + side]);
-        zmac(acc1, Cr[c0 + (t2 + 1) * cs], Ub[t2 * 2 + 2 + side]);
+      for (int t2 = 0; t2 < q; ++t2) {
+        const zt vx = Cx[t2], vy = Cy[t2 * q];
+        zmac(aw, vx, Ubx[t2 * 2 + 0]);
+        zmac(ae, vx, Ubx[t2 * 2 + 1]);
+        zmac(as, vy, Uby[t2 * 2 + 0]);
+        zmac(an, vy, Uby[t2 * 2 + 1]);
       }
-      if (q & 1) zmac(acc, Cr[c0 + (q - 1) * cs], Ub[(q - 1) * 2 + side]);
-      acc.x += acc1.x;
-      acc.y += acc1.y;
-      Pc[e] = acc;
-      __stcs(&base[(int64_t)(nb + kx0 * q + t) * nt + b], acc);
+      zt* pr = Pc + t * nb;
+      pr[kk] = as;
+      pr[q + kk] = ae;
+      pr[2 * q + kk] = an;
+      pr[3 * q + kk] = aw;
+      zt* orow = base + (int64_t)(nb + kx0 * q + t) * nt;
+      __stcs(&orow[kk], as);
+      __stcs(&orow[q + kk], ae);
+      __stcs(&orow[2 * q + kk], an);
+      __stcs(&orow[3 * q + kk], aw);
     }
     emark(2);
     // Y_b: W_kx, E_kx complete on each line; S/N (y-lines) accumulate in registers
