@@ -14,7 +14,8 @@ import sys
 CLASSES = [  # (substring of the kernel name, class) -- first match wins
     ("zgemv", "zgemv"), ("zgemm_kernel", "zgemm_dmma"), ("zgj_seq_kernel", "leaf_gj"), ("zgj_ws_kernel", "leaf_gj"),
     ("dgj_leaf_kernel", "leaf_gj"), ("leaf_real_ops_kernel", "leaf_gj"), ("zgj_panel", "zgj_panel"),
-    ("zgj_small", "zgj_small"), ("zgj_fused", "zgj_fused"), ("nat_diag", "zgj_aux"), ("zgj_", "zgj_aux"),
+    ("zgj_small", "zgj_small"), ("zgj_fused", "zgj_fused"), ("nat_block_inv", "zgj_panel"), ("nat_diag", "zgj_aux"),
+    ("zgj_", "zgj_aux"),
     ("leaf_schur_assemble", "leaf_assemble"), ("leaf_assemble", "leaf_assemble"), ("zcopy", "layout"),
     ("rhs_", "layout"), ("zsum_slots", "layout"), ("c_bounds", "leaf_assemble"), ("leaf_R", "layout"),
 ]
