@@ -224,6 +224,11 @@ def run_hps(args, rank, world, dist):
         plan["solve_actions"] = {"actions": len(ps), "planned": sum(a["cfg"] >= 0 for a in ps),
                                  "rule_ms": round(sum(a["rule_ms"] for a in ps), 3),
                                  "planned_ms": round(sum(a["best_ms"] for a in ps), 3)}
+        # and the build's merge products (Algorithm 1 lines 7-12) the same way
+        pb = hps.plan_build(g_plan, cfg.p, keep_root_R=True)
+        plan["build_actions"] = {"actions": len(pb), "planned": sum(a["cfg"] >= 0 for a in pb),
+                                 "rule_ms": round(sum(a["rule_ms"] for a in pb), 3),
+                                 "planned_ms": round(sum(a["best_ms"] for a in pb), 3)}
 
     def step(profile=0, keep_root_R=True):
         S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=keep_root_R, device=local, profile=profile,

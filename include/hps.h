@@ -322,6 +322,14 @@ int hps_rep_actions(const hps_grid* g, int p, int maxlev, int* n_out, int* nbox_
  * (ms): the rule's and the chosen configuration's extrapolated times.  Returns the number of
  * actions or a negative error code.  hps_plan_clear forgets these entries too. */
 int hps_solve_actions(const hps_grid* g, int p, int nrhs, int maxn, int32_t* out);
+/* The build's batched products (Algorithm 1 lines 7-12 per merge level, and
+ * the trailing updates of the natural-order W^{-1}), same 7-int layout; kinds
+ * 6 R33b R31a, 7 W = I - R33b R33a, 8 Phi^a = W^{-1} X, 9 R^tau rows of I1 (and I2; absent at the
+ * root with keep_root_R = 0), 10 Phi^b, 11 W^{-1} block-step update.  hps_plan_build plans them
+ * like hps_plan_solve. */
+int hps_build_actions(const hps_grid* g, int p, int keep_root_R, int maxn, int32_t* out);
+int hps_plan_build(const hps_grid* g, int p, int keep_root_R, int maxn, int32_t* actions, int32_t* chosen,
+                   double* t_rule, double* t_best);
 int hps_plan_solve(const hps_grid* g, int p, int nrhs, int maxn, int32_t* actions, int32_t* chosen, double* t_rule,
                    double* t_best);
 int hps_plan_inverse(int n, int nbox, double* eps, double* rep_ms, int* theta_o);

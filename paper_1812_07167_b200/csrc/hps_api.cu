@@ -2683,15 +2683,49 @@ int hps_solve_actions(const hps_grid* g, int p, int nrhs, int maxn, int32_t* out
   return n;
 }
 
-int hps_plan_solve(const hps_grid* g, int p, int nrhs, int maxn, int32_t* actions, int32_t* chosen, double* t_rule,
-                   double* t_best) {
-  const int n = hps_solve_actions(g, p, nrhs, 0, nullptr);
-  if (n < 0) return n;
-  if (maxn < n || !actions || !chosen || !t_rule || !t_best) {
-    hps_set_error("hps_plan_solve: invalid argument (maxn must hold every action)");
+int hps_build_actions(const hps_grid* g, int p, int keep_root_R, int maxn, int32_t* out) {
+  if (!g || p < 4 || !is_pow2(g->nx) || !is_pow2(g->ny) || maxn < 0 || (!out && maxn > 0)) {
+    hps_set_error("hps_build_actions: invalid argument");
     return HPS_EINVAL;
   }
-  hps_solve_actions(g, p, nrhs, maxn, actions);
+  const int q = p - 2;
+  std::vector<std::array<int32_t, 7>> A;
+  int a = g->nx, b = g->ny, d = 0;
+  const int bb_min = knob(KN_NAT_BB_MIN), nat_min = knob(KN_NAT_MIN), nat_max = knob(KN_NAT_MAX);
+  const int nat_w = knob(KN_NAT_W);
+  while (!(a == 1 && b == 1)) {
+    const bool vertical = a >= b;
+    if (vertical) a /= 2;
+    else b /= 2;
+    const int nbc = 2 * (a + b) * q, n3 = vertical ? b * q : a * q, n1 = nbc - n3, ntau = 2 * n1, np = 1 << d;
+    // Algorithm 1 lines 7-12: R33b R31a, W = I - R33b R33a, Phi^a = W^{-1} X, Phi^b, R^tau rows
+    A.push_back({d, 6, n3, n1, n3, np, 0});
+    A.push_back({d, 7, n3, n3, n3, np, 0});
+    A.push_back({d, 8, n3, ntau, n3, np, 0});
+    A.push_back({d, 10, n3, ntau, n3, np, 1});
+    if (d > 0 || keep_root_R) A.push_back({d, 9, n1, ntau, n3, np, 1});
+    // the trailing updates of the natural-order W^{-1}: 64-wide block steps, else panels
+    if (n3 >= nat_min && n3 <= nat_max) {
+      const int w = n3 >= bb_min ? 64 : nat_w;
+      if (n3 > w) A.push_back({d, 11, n3, n3 - w, w, np, 1});
+    }
+    ++d;
+  }
+  const int n = (int)A.size();
+  for (int i = 0; i < std::min(n, maxn); ++i) std::memcpy(out + 7 * i, A[i].data(), sizeof(int32_t) * 7);
+  if (maxn > 0 && maxn < n) {
+    hps_set_error("hps_build_actions: maxn too small");
+    return HPS_EINVAL;
+  }
+  return n;
+}
+
+}  // extern "C"
+
+namespace {
+// Times every distinct shape of the action list (7 ints per action: level, kind, M, N, K, batch,
+// cin) and records the fastest tile configuration per shape (zgemm_plan_shape).
+int plan_gemm_actions(int n, const int32_t* actions, int32_t* chosen, double* t_rule, double* t_best) {
   try {
     cudaStream_t st;
     HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -2721,6 +2755,33 @@ int hps_plan_solve(const hps_grid* g, int p, int nrhs, int maxn, int32_t* action
     return fail(e);
   }
   return n;
+}
+}  // namespace
+
+extern "C" {
+
+int hps_plan_solve(const hps_grid* g, int p, int nrhs, int maxn, int32_t* actions, int32_t* chosen, double* t_rule,
+                   double* t_best) {
+  const int n = hps_solve_actions(g, p, nrhs, 0, nullptr);
+  if (n < 0) return n;
+  if (maxn < n || !actions || !chosen || !t_rule || !t_best) {
+    hps_set_error("hps_plan_solve: invalid argument (maxn must hold every action)");
+    return HPS_EINVAL;
+  }
+  hps_solve_actions(g, p, nrhs, maxn, actions);
+  return plan_gemm_actions(n, actions, chosen, t_rule, t_best);
+}
+
+int hps_plan_build(const hps_grid* g, int p, int keep_root_R, int maxn, int32_t* actions, int32_t* chosen,
+                   double* t_rule, double* t_best) {
+  const int n = hps_build_actions(g, p, keep_root_R, 0, nullptr);
+  if (n < 0) return n;
+  if (maxn < n || !actions || !chosen || !t_rule || !t_best) {
+    hps_set_error("hps_plan_build: invalid argument (maxn must hold every action)");
+    return HPS_EINVAL;
+  }
+  hps_build_actions(g, p, keep_root_R, maxn, actions);
+  return plan_gemm_actions(n, actions, chosen, t_rule, t_best);
 }
 
 int hps_plan_regime(int n, int nbox) { return n > 0 && nbox > 0 ? zgj_regime_of(n, nbox) : HPS_EINVAL; }

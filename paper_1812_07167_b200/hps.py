@@ -41,7 +41,8 @@ class hps_opts(C.Structure):
 SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box_nb", "hps_num_boxes",
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_boundary_nodes_glq",
            "hps_last_time_ms", "hps_last_launches",
-           "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_solve_actions", "hps_plan_solve", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
+           "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_solve_actions", "hps_plan_solve",
+           "hps_build_actions", "hps_plan_build", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free", "hps_release_cache",
            "hps_set_cache_limit", "hps_cache_bytes", "hps_debug_set", "hps_debug_get", "hps_last_error",
            "hps_sync", "hps_nccl_unique_id", "hps_nccl_comm_init", "hps_nccl_comm_destroy", "hps_comm_wrap_nccl",
@@ -92,6 +93,8 @@ def lib():
         L.hps_plan_regime.argtypes = [i32, i32]
         L.hps_solve_actions.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp]
         L.hps_plan_solve.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp, dp, dp, dp]
+        L.hps_build_actions.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp]
+        L.hps_plan_build.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp, dp, dp, dp]
         L.hps_zgemm_batched.argtypes = [i32, i32, i32, i32, i32, dp, dp, dp, dp, hps_c128, hps_c128, i32,
                                         C.POINTER(C.c_double)]
         L.hps_subtree_grid.argtypes = [C.POINTER(hps_grid), i32, i64, C.POINTER(hps_grid), C.POINTER(C.c_int32),
@@ -300,8 +303,39 @@ def plan_problem(g, p):
     return rows
 
 
-SOLVE_KINDS = ["leaf u~ = Y s", "leaf u = Psi t (+ u~)", "Upsilon R33 h", "W^-1", "Gamma^tau R13 t~",
-               "Phi t (+ t~)"]
+GEMM_KINDS = ["leaf u~ = Y s", "leaf u = Psi t (+ u~)", "Upsilon R33 h", "W^-1", "Gamma^tau R13 t~",
+              "Phi t (+ t~)", "R33b R31a", "W = I - R33b R33a", "Phi^a = W^-1 X", "R^tau rows", "Phi^b",
+              "W^-1 block-step update"]
+_KEYS = ("level", "kind", "M", "N", "K", "batch", "cin")
+
+
+def _actions(fn, *args):
+    n = fn(*args, 0, None)
+    if n < 0:
+        _check(n)
+    out = np.zeros((n, 7), dtype=np.int32)
+    _check(0 if fn(*args, n, out.ctypes.data) == n else -1)
+    return out
+
+
+def build_actions(g, p, keep_root_R=True):
+    """The build's batched products per merge level (host only): list of dicts."""
+    acts = _actions(lib().hps_build_actions, C.byref(g), p, int(keep_root_R))
+    return [dict(zip(_KEYS, map(int, r))) for r in acts]
+
+
+def plan_build(g, p, keep_root_R=True):
+    """Time every build product's shape with each GEMM tile configuration and record the fastest."""
+    n = len(build_actions(g, p, keep_root_R))
+    acts = np.zeros((n, 7), dtype=np.int32)
+    ch = np.zeros(n, dtype=np.int32)
+    tr, tb = np.zeros(n), np.zeros(n)
+    rc = lib().hps_plan_build(C.byref(g), p, int(keep_root_R), n, acts.ctypes.data, ch.ctypes.data, tr.ctypes.data,
+                              tb.ctypes.data)
+    if rc < 0:
+        _check(rc)
+    return [dict(zip(_KEYS, map(int, acts[i])), cfg=int(ch[i]), rule_ms=float(tr[i]), best_ms=float(tb[i]))
+            for i in range(n)]
 
 
 def solve_actions(g, p, nrhs):

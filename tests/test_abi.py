@@ -172,3 +172,26 @@ def test_solve_actions_small_tree(L):
     w = [(a["M"], a["batch"]) for a in acts if a["kind"] == 3]
     assert sorted(w) == sorted((n, nb) for n, nb in ra[1:])
     assert L.hps_solve_actions(C.byref(g), 6, 3, 2, np.zeros(14, np.int32).ctypes.data) == -1   # maxn too small
+    assert L.hps_build_actions(C.byref(g), 6, 1, 2, np.zeros(14, np.int32).ctypes.data) == -1
+
+
+def test_build_actions_small_tree(L):
+    """The build's batched products per merge level (host only) for the 4 x 2 tree at p = 6 (same
+    hand-written n3 / n_b as test_solve_actions_small_tree); no R^tau product at the root with
+    keep_root_R = 0; no W^{-1} update product below the natural-order range (n3 < 200)."""
+    g = hps.grid(0, 2, 0, 1, 4, 2)
+    for keep in (1, 0):
+        acts = hps.build_actions(g, 6, keep_root_R=bool(keep))
+        got = [(a["level"], a["kind"], a["M"], a["N"], a["K"], a["batch"], a["cin"]) for a in acts]
+        exp = []
+        for d, n3, nbc in ((0, 8, 32), (1, 8, 24), (2, 4, 16)):
+            n1, np_ = nbc - n3, 2 ** d
+            exp += [(d, 6, n3, n1, n3, np_, 0), (d, 7, n3, n3, n3, np_, 0), (d, 8, n3, 2 * n1, n3, np_, 0),
+                    (d, 10, n3, 2 * n1, n3, np_, 1)]
+            if d > 0 or keep:
+                exp.append((d, 9, n1, 2 * n1, n3, np_, 1))
+        assert got == exp
+    # C4's root level carries the 64-wide block-step update of its natural-order W^{-1}
+    c4 = hps.build_actions(hps.grid(0, 1, 0, 1, 256, 256), 16)
+    assert (0, 11, 3584, 3520, 64, 1, 1) in [(a["level"], a["kind"], a["M"], a["N"], a["K"], a["batch"], a["cin"])
+                                             for a in c4]

@@ -794,3 +794,23 @@ def test_plan_solve_parity():
     O = oracle.Oracle(0.0, 1.0, 0.0, 0.5, nx, ny, p, kappa, eta, c)
     assert rel(u1, O.solve(s, t)) < TOL
     assert rel(u1, u0) < 1e-12
+
+
+def test_plan_build_parity():
+    """Build-stage GEMM planner (hps_plan_build): the planned build's root R and u match the
+    oracle at 1e-9 and the unplanned build to rounding."""
+    nx, ny, p, kappa, eta = 16, 16, 12, 20.0, 20.0 + 2j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=2)
+    hps.plan_clear()
+    S0 = hps.Solver(g, p, kappa, eta, c)
+    u0, R0 = S0.solve(s, t), S0.R(1)
+    try:
+        plan = hps.plan_build(g, p)
+        assert len(plan) == len(hps.build_actions(g, p)) and any(a["kind"] == 9 for a in plan)
+        S1 = hps.Solver(g, p, kappa, eta, c)
+        u1, R1 = S1.solve(s, t), S1.R(1)
+    finally:
+        hps.plan_clear()
+    O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
+    assert rel(R1, O.R(1)) < TOL and rel(u1, O.solve(s, t)) < TOL
+    assert rel(R1, R0) < 1e-12 and rel(u1, u0) < 1e-12
