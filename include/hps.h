@@ -347,6 +347,12 @@ int hps_debug_ws_trace(int on, int64_t* out);
  * NULL).  cfg selects a tile configuration (-1 = the library's choice); the call runs `reps`
  * times after one warm-up and returns the mean device time in *ms.  Exposed for kernel tests
  * and tuning. */
+/* Live FP64 tensor-core peak of the current device: 8 independent m8n8k4 DMMA chains per warp, 8
+ * CTAs of 8 warps per SM, best of 3 timed launches (~0.1 s).  The roofline denominator of the
+ * FP64-bound kernels measured in the same process and at the same clocks (MEASURED_PEAKS.json has no
+ * FP64 entry).  Returns 0 or HPS_ECUDA. */
+int hps_fp64_peak(double* tflops);
+
 int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A, const hps_c128* B,
                       const hps_c128* Cin, hps_c128* C, hps_c128 alpha, hps_c128 beta, int reps, double* ms);
 

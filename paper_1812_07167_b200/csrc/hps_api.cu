@@ -2784,6 +2784,22 @@ int hps_plan_build(const hps_grid* g, int p, int keep_root_R, int maxn, int32_t*
   return plan_gemm_actions(n, actions, chosen, t_rule, t_best);
 }
 
+int hps_fp64_peak(double* tflops) {
+  if (!tflops) {
+    hps_set_error("hps_fp64_peak: NULL argument");
+    return HPS_EINVAL;
+  }
+  try {
+    cudaStream_t st;
+    HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    *tflops = fp64_dmma_peak_tflops(st);
+    cudaStreamDestroy(st);
+  } catch (const HpsError& e) {
+    return fail(e);
+  }
+  return HPS_OK;
+}
+
 int hps_plan_regime(int n, int nbox) { return n > 0 && nbox > 0 ? zgj_regime_of(n, nbox) : HPS_EINVAL; }
 
 int hps_zinv_timed(int mode, int n, int batch, const hps_c128* A, hps_c128* outp, int reps, double* ms) {

@@ -135,6 +135,7 @@ void zgemm_plan_clear();
 int zgemm_candidates(int N, int* out);
 int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, double* t_rule, int* cands, int* ncand,
                      cudaStream_t st);
+double fp64_dmma_peak_tflops(cudaStream_t st);  // live DMMA m8n8k4 throughput of this device
 
 // Batched 2-D gather/scale copy: C[b](i, j) = alpha * A[b](i, j) (+ beta * Cin), maps as above.
 struct ZCopy {

@@ -884,3 +884,57 @@ int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, do
   HPS_CUDA_CHECK(cudaStreamSynchronize(st));
   return chosen;
 }
+
+// ---------------------------------------------------------------------------
+// Live FP64 tensor peak (hps_fp64_peak): every warp of 8 per CTA, 8 CTAs per SM runs 8
+// independent m8n8k4 DMMA chains -- the roofline denominator measured in the same process and
+// at the same clocks as the kernels it is compared with (tools/fp64_peaks.cu is the standalone form).
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters, double a0, double b0) {
+  double d[8][2];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    d[c][0] = 0;
+    d[c][1] = threadIdx.x;
+  }
+  const double a = a0 + threadIdx.x * 1e-9, b = b0;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(d[c][0]), "+d"(d[c][1])
+                   : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += d[c][0] + d[c][1];
+  if (s == 1234.5) out[threadIdx.x] = s;
+}
+}  // namespace
+
+double fp64_dmma_peak_tflops(cudaStream_t st) {
+  const int nsm = hps_num_sms(), blocks = nsm * 8, threads = 256, iters = 1 << 14;
+  double* out;
+  HPS_CUDA_CHECK(cudaMallocAsync(&out, sizeof(double) * threads, st));
+  cudaEvent_t e0, e1;
+  HPS_CUDA_CHECK(cudaEventCreate(&e0));
+  HPS_CUDA_CHECK(cudaEventCreate(&e1));
+  dmma_peak_kernel<<<blocks, threads, 0, st>>>(out, 256, 1.0, 1e-7);  // warm-up (clocks up)
+  double best = 0;
+  for (int r = 0; r < 3; ++r) {
+    HPS_CUDA_CHECK(cudaEventRecord(e0, st));
+    dmma_peak_kernel<<<blocks, threads, 0, st>>>(out, iters, 1.0, 1e-7);
+    HPS_CUDA_CHECK(cudaEventRecord(e1, st));
+    HPS_CUDA_CHECK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double fl = 2.0 * 8 * 8 * 4 * 8 * (double)iters * (threads / 32) * blocks;
+    best = std::max(best, fl / ms / 1e9);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFreeAsync(out, st);
+  HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return best;
+}

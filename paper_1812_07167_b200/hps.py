@@ -42,7 +42,7 @@ SYMBOLS = ["hps_build", "hps_solve", "hps_export_R", "hps_export_leaf", "hps_box
            "hps_leaf_nodes", "hps_root_boundary_nodes", "hps_boundary_nodes_gl", "hps_boundary_nodes_glq",
            "hps_last_time_ms", "hps_last_launches",
            "hps_last_flops", "hps_leaf_path", "hps_set_profiling", "hps_kernel_stats", "hps_reset_stats", "hps_zinv_batched", "hps_zinv_timed", "hps_debug_ws_trace", "hps_rep_actions", "hps_plan_inverse", "hps_plan_set", "hps_plan_clear", "hps_plan_regime", "hps_solve_actions", "hps_plan_solve",
-           "hps_build_actions", "hps_plan_build", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
+           "hps_build_actions", "hps_plan_build", "hps_fp64_peak", "hps_subtree_grid", "hps_build_top", "hps_solve_up",
            "hps_solve_down", "hps_solve_top", "hps_zgemm_batched", "hps_free", "hps_release_cache",
            "hps_set_cache_limit", "hps_cache_bytes", "hps_debug_set", "hps_debug_get", "hps_last_error",
            "hps_sync", "hps_nccl_unique_id", "hps_nccl_comm_init", "hps_nccl_comm_destroy", "hps_comm_wrap_nccl",
@@ -94,6 +94,7 @@ def lib():
         L.hps_solve_actions.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp]
         L.hps_plan_solve.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp, dp, dp, dp]
         L.hps_build_actions.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp]
+        L.hps_fp64_peak.argtypes = [C.POINTER(C.c_double)]
         L.hps_plan_build.argtypes = [C.POINTER(hps_grid), i32, i32, i32, dp, dp, dp, dp]
         L.hps_zgemm_batched.argtypes = [i32, i32, i32, i32, i32, dp, dp, dp, dp, hps_c128, hps_c128, i32,
                                         C.POINTER(C.c_double)]
@@ -316,6 +317,13 @@ def _actions(fn, *args):
     out = np.zeros((n, 7), dtype=np.int32)
     _check(0 if fn(*args, n, out.ctypes.data) == n else -1)
     return out
+
+
+def fp64_peak():
+    """Live FP64 tensor (DMMA m8n8k4) throughput of the current device, TFLOP/s (hps_fp64_peak)."""
+    v = C.c_double()
+    _check(lib().hps_fp64_peak(C.byref(v)))
+    return v.value
 
 
 def build_actions(g, p, keep_root_R=True):
