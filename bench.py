@@ -405,6 +405,9 @@ def run_hps(args, rank, world, dist):
                 "note": "per-rank host buffers summed over ranks; time = max over ranks"},
     }
     out["host"] = {"cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    out["fp64_tensor_peak_tflops"] = {"live": round(_LIVE_PEAK, 3) if _LIVE_PEAK else None,
+                                      "builder": load_json(os.path.join(ROOT, "bench", "peaks_fp64.json"), {}).get(
+                                          "dmma_m8n8k4_tflops")}
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, c, s, t, args)
     return out
