@@ -2732,15 +2732,17 @@ int plan_gemm_actions(int n, const int32_t* actions, int32_t* chosen, double* t_
     int dev;
     HPS_CUDA_CHECK(cudaGetDevice(&dev));
     retain_pool(dev);
-    std::map<std::array<int32_t, 5>, std::array<double, 3>> done;  // shape -> (cfg, rule, best)
+    std::map<std::array<int32_t, 6>, std::array<double, 3>> done;  // shape -> (cfg, rule, best)
     for (int i = 0; i < n; ++i) {
       const int32_t* a = actions + 7 * i;
-      const std::array<int32_t, 5> key{a[2], a[3], a[4], a[5], a[6]};
+      // the leaf products read s / write u in the ABI layout (column-major B / C)
+      const int lay = a[0] == -1 ? (a[1] == 0 ? 1 : 2) : 0;
+      const std::array<int32_t, 6> key{a[2], a[3], a[4], a[5], a[6], lay};
       auto it = done.find(key);
       if (it == done.end()) {
         double tc[16], tr = 0;
         int cands[16], nc = 0;
-        const int c = zgemm_plan_shape(a[2], a[3], a[4], a[5], a[6] != 0, tc, &tr, cands, &nc, st);
+        const int c = zgemm_plan_shape(a[2], a[3], a[4], a[5], a[6] != 0, lay, tc, &tr, cands, &nc, st);
         double best = tr;
         for (int k = 0; k < nc; ++k)
           if (tc[k] > 0 && tc[k] < best) best = tc[k];

@@ -129,12 +129,13 @@ void zgemm(const ZGemm& g, cudaStream_t st);
 // Planned tile configurations of batched products (zgemm.cu, representative-action planner of the
 // solve's matrix products): lookup (-1: none), set (cfg -1 removes), clear, candidates for N,
 // and timing of one shape (records the fastest configuration if it beats the fixed rule by 3 %).
-int zgemm_plan_lookup(int M, int N, int K, int batch, bool cin);
-void zgemm_plan_set(int M, int N, int K, int batch, bool cin, int cfg);
+// lay: operand layouts of the shape (bit 0: column-major B, s in the ABI layout; bit 1: column-major C, u)
+int zgemm_plan_lookup(int M, int N, int K, int batch, bool cin, int lay);
+void zgemm_plan_set(int M, int N, int K, int batch, bool cin, int lay, int cfg);
 void zgemm_plan_clear();
 int zgemm_candidates(int N, int* out);
-int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, double* t_rule, int* cands, int* ncand,
-                     cudaStream_t st);
+int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, int lay, double* t_out, double* t_rule, int* cands,
+                     int* ncand, cudaStream_t st);
 double fp64_dmma_peak_tflops(cudaStream_t st);  // live DMMA m8n8k4 throughput of this device
 
 // Batched 2-D gather/scale copy: C[b](i, j) = alpha * A[b](i, j) (+ beta * Cin), maps as above.

@@ -639,7 +639,8 @@ void zgemm_impl(const ZGemm& g0, cudaStream_t st) {
   // a forced configuration (tests / tuning), else the planned one of this shape (zgemm_plan_shape)
   int force = g_zgemm_force;
   if (force == -1) {
-    const int pc = zgemm_plan_lookup(g.M, g.N, g.K, g.batch, g.Cin.ptr != nullptr);
+    const int lay = (g.B.rs == 1 && g.B.cs > 1 && !g.B.rmap && !g.B.cmap ? 1 : 0) | (g.C.rs == 1 && g.C.cs > 1 ? 2 : 0);
+    const int pc = zgemm_plan_lookup(g.M, g.N, g.K, g.batch, g.Cin.ptr != nullptr, lay);
     if (pc >= 0) force = pc;
   }
   // N <= 4 runs the GEMV kernel: bound by HBM (the A operand is read once), its own class
@@ -753,7 +754,7 @@ void zcopy(const ZCopy& c, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 namespace {
 std::mutex g_plan_mu;
-std::map<std::tuple<int, int, int, int, int>, int> g_plan;
+std::map<std::tuple<int, int, int, int, int, int>, int> g_plan;
 std::atomic<int> g_plan_n{0};
 
 __global__ void zfill_kernel(zt* p, int64_t n, uint64_t seed) {
@@ -768,16 +769,16 @@ __global__ void zfill_kernel(zt* p, int64_t n, uint64_t seed) {
 }
 }  // namespace
 
-int zgemm_plan_lookup(int M, int N, int K, int batch, bool cin) {
+int zgemm_plan_lookup(int M, int N, int K, int batch, bool cin, int lay) {
   if (g_plan_n.load(std::memory_order_relaxed) == 0) return -1;
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  auto it = g_plan.find(std::make_tuple(M, N, K, batch, (int)cin));
+  auto it = g_plan.find(std::make_tuple(M, N, K, batch, (int)cin, lay));
   return it == g_plan.end() ? -1 : it->second;
 }
 
-void zgemm_plan_set(int M, int N, int K, int batch, bool cin, int cfg) {
+void zgemm_plan_set(int M, int N, int K, int batch, bool cin, int lay, int cfg) {
   std::lock_guard<std::mutex> lk(g_plan_mu);
-  const auto key = std::make_tuple(M, N, K, batch, (int)cin);
+  const auto key = std::make_tuple(M, N, K, batch, (int)cin, lay);
   if (cfg < 0) g_plan.erase(key);
   else g_plan[key] = cfg;
   g_plan_n.store((int)g_plan.size());
@@ -801,8 +802,8 @@ int zgemm_candidates(int N, int* out) {
 // the batch; records the fastest in the plan if it beats the rule by more than 3 %.  Writes the
 // per-candidate times extrapolated to the full batch (ms, -1 where infeasible) to t_out[0..ncand)
 // and the rule's to *t_rule; returns the chosen configuration (-1: the rule).
-int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, double* t_rule, int* cands, int* ncand,
-                     cudaStream_t st) {
+int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, int lay, double* t_out, double* t_rule, int* cands,
+                     int* ncand, cudaStream_t st) {
   const int nc = zgemm_candidates(N, cands);
   *ncand = nc;
   // sample: enough 16 x 16 tiles for ~8 waves of 8 resident CTAs on every SM
@@ -830,6 +831,11 @@ int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, do
   g.B.ptr = B;
   g.B.rs = N;
   g.B.bs = (int64_t)K * N;
+  if (lay & 1) {  // column-major B as s in the ABI layout [RHS][box][K]
+    g.B.rs = 1;
+    g.B.cs = (int64_t)K * bs;
+    g.B.bs = K;
+  }
   if (cin) {
     g.Cin.ptr = Ci;
     g.Cin.rs = N;
@@ -839,6 +845,11 @@ int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, do
   g.C.ptr = C;
   g.C.rs = N;
   g.C.bs = (int64_t)M * N;
+  if (lay & 2) {  // column-major C as u in the ABI layout [RHS][box][M]
+    g.C.rs = 1;
+    g.C.cs = (int64_t)M * bs;
+    g.C.bs = M;
+  }
   cudaEvent_t e0, e1;
   HPS_CUDA_CHECK(cudaEventCreate(&e0));
   HPS_CUDA_CHECK(cudaEventCreate(&e1));
@@ -874,7 +885,7 @@ int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, double* t_out, do
     }
   }
   const int chosen = (bi >= 0 && bt < 0.97 * *t_rule) ? cands[bi] : -1;
-  zgemm_plan_set(M, N, K, batch, cin, chosen);
+  zgemm_plan_set(M, N, K, batch, cin, lay, chosen);
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFreeAsync(A, st);
