@@ -53,7 +53,6 @@ enum HpsKnob {
   KN_GEMM_GROUP,       // GEMM tile order: 1 row-major, G > 1 grouped by G row blocks (L2 reuse)
   KN_LEAF_INPLACE,     // 1: natural-order complex leaf inverse in the store's Y_i block (no Y_i copy)
   KN_SEQ_FORCE_BAD,    // test: the natural-order complex leaf inverse fails its check at step 100
-  KN_LEAF_UPD32,       // 1: 8 x 32 update units in the complex leaf inverse (0: 8 x 16 with prefetch)
   KN_COUNT
 };
 int knob(HpsKnob k);

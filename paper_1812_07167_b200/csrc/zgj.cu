@@ -1133,7 +1133,6 @@ struct WsFinish {
   double kappa2;
   int blockpanel = 0;    // natural-order panels in block form (knob leaf_panel, DESIGN 3.12)
   int inplace = 1;       // natural order: eliminate in the store's Y_i block (knob leaf_inplace)
-  int upd32 = 1;         // 8 x 32 update units (knob leaf_upd32; 0: 8 x 16 units with seed prefetch)
 };
 
 __host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16, == 2 (mod 8)
@@ -2409,63 +2408,6 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
     WS_MARK(p, 2);
-    if (fin.upd32) {
-      // 8 x 32 units (four 8-column tiles, eight accumulator fragments per warp: twice the DMMAs per
-      // A fragment and per unit of bookkeeping), seeds loaded at the start of each unit (the other
-      // warps' DMMAs cover the latency), 8-column tiles beyond nv skipped (warp-uniform)
-      const int MTu = (n + 7) >> 3, NPR32 = (nv + 31) >> 5, NU = MTu * NPR32;
-      for (int u = wp; u < NU; u += 16) {
-        const int umt = u % MTu, unpr = u / MTu;
-        const int rr = umt * 8 + (lane >> 2), rc = min(rr, n - 1);
-        const bool rok = rr < n && (unsigned)(pstep[rc] - k0) >= (unsigned)w;
-        const int vb = unpr * 32 + (lane & 3) * 2, ntile = min(4, (nv - unpr * 32 + 7) >> 3);
-        const zt* rowp = M + (int64_t)rc * lda;
-        int col[4][2];
-        double ar[4][2], ai[4][2];
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int v = vb + t * 8 + h;
-            col[t][h] = v < nv ? colmap[v] : -1;
-            const zt sd = (rok && col[t][h] >= 0) ? ldplain(rowp + col[t][h]) : make_double2(0.0, 0.0);
-            ar[t][h] = sd.x;
-            ai[t][h] = sd.y;
-          }
-        const zt* Trow = Ts + (umt * 8 + (lane >> 2)) * NB + (lane & 3);
-        const zt* Zc = Zs + (lane & 3) * zs + unpr * 32 + (lane >> 2);
-#pragma unroll 7
-        for (int k4 = 0; k4 < K4; ++k4) {
-          const zt av = Trow[k4 * 4];
-          const zt* Zk = Zc + k4 * 4 * zs;
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (t < ntile) {
-              const zt bv = Zk[t * 8];
-              dmma884(ar[t][0], ar[t][1], av.x, bv.x);
-              dmma884(ai[t][0], ai[t][1], av.x, bv.y);
-            }
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-            if (t < ntile) {
-              const zt bv = Zk[t * 8];
-              dmma884(ar[t][0], ar[t][1], -av.y, bv.y);
-              dmma884(ai[t][0], ai[t][1], av.y, bv.x);
-            }
-        }
-        if (rr < n) {
-          zt* orow = M + (int64_t)rr * lda;
-#pragma unroll
-          for (int t = 0; t < 4; ++t)
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-              if (col[t][h] >= 0) orow[col[t][h]] = make_double2(ar[t][h], ai[t][h]);
-        }
-      }
-      __syncthreads();  // update stored before the next panel reads its columns
-      WS_MARK(p, 3);
-      continue;
-    }
     const int NPR = (nv + 15) >> 4;
     struct Unit {
       int rr, col[2][2];
@@ -3040,7 +2982,7 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
     kern<<<nbatch, 512, ws_smem(n) + dbytes, st>>>(
         S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
         info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2, knob(KN_LEAF_PANEL),
-                       knob(KN_LEAF_INPLACE), knob(KN_LEAF_UPD32)});
+                       knob(KN_LEAF_INPLACE)});
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
   }
