@@ -609,7 +609,7 @@ static bool bcol_applies(const ZGemm& g) {
 bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
   switch (cfg) {
     case 0: launch<64, 8, 16, 8>(g, st); return true;
-    case 1: launch<16, 16, 8, 8>(g, st); return true;
+    case 1: bcol_applies(g) ? launch<16, 16, 8, 8, true>(g, st) : launch<16, 16, 8, 8>(g, st); return true;
     case 2: bcol_applies(g) ? launch<32, 32, 16, 16, true>(g, st) : launch<32, 32, 16, 16>(g, st); return true;
     case 3: launch<64, 64, 32, 32>(g, st); return true;
     case 4: launch<64, 64, 32, 16>(g, st); return true;
@@ -618,9 +618,9 @@ bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
     case 7: launch<128, 64, 32, 32>(g, st); return true;
     case 8: launch<64, 64, 16, 32>(g, st); return true;
     case 10: bcol_applies(g) ? launch<64, 16, 16, 16, true>(g, st) : launch<64, 16, 16, 16>(g, st); return true;
-    case 11: launch<128, 16, 32, 16>(g, st); return true;
-    case 12: launch<64, 16, 32, 8>(g, st); return true;
-    case 13: launch<32, 16, 16, 16>(g, st); return true;
+    case 11: bcol_applies(g) ? launch<128, 16, 32, 16, true>(g, st) : launch<128, 16, 32, 16>(g, st); return true;
+    case 12: bcol_applies(g) ? launch<64, 16, 32, 8, true>(g, st) : launch<64, 16, 32, 8>(g, st); return true;
+    case 13: bcol_applies(g) ? launch<32, 16, 16, 16, true>(g, st) : launch<32, 16, 16, 16>(g, st); return true;
     case 9: {
       if (g.N == 1) launch_gemv<1>(g, st);
       else if (g.N <= 4) launch_gemv<4>(g, st);
@@ -791,7 +791,7 @@ void zgemm_plan_clear() {
 }
 
 int zgemm_candidates(int N, int* out) {
-  static const int c4[] = {9, 0, 1}, c16[] = {0, 1, 10, 12, 13, 2}, cbig[] = {2, 5, 4, 6, 1, 13};
+  static const int c4[] = {9, 0, 1}, c16[] = {0, 1, 10, 11, 12, 13}, cbig[] = {2, 5, 4, 6, 1, 13};
   const int* c = N <= 4 ? c4 : N <= 16 ? c16 : cbig;
   const int n = N <= 4 ? 3 : 6;
   for (int i = 0; i < n; ++i) out[i] = c[i];
