@@ -812,14 +812,20 @@ int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, int lay, double* 
   const int bs = (int)std::min<int64_t>(batch, want);
   const double scale = (double)batch / bs;
   zt *A, *B, *C, *Ci = nullptr;
-  const size_t na = (size_t)M * K * bs, nb = (size_t)K * N * bs, nm = (size_t)M * N * bs;
+  // column-major B / C keep the FULL batch's column stride (s and u in the ABI layout have columns
+  // K * batch / M * batch elements apart: 50-270 MB at C3/C4, a different TLB regime from the
+  // sample's); only the sampled entries are touched
+  const size_t na = (size_t)M * K * bs;
+  const size_t nb = (lay & 1) ? (size_t)K * batch * (N - 1) + (size_t)K * bs : (size_t)K * N * bs;
+  const size_t nm = (lay & 2) ? (size_t)M * batch * (N - 1) + (size_t)M * bs : (size_t)M * N * bs;
+  const size_t ni = (size_t)M * N * bs;
   HPS_CUDA_CHECK(cudaMallocAsync(&A, sizeof(zt) * std::max<size_t>(na, 1), st));
   HPS_CUDA_CHECK(cudaMallocAsync(&B, sizeof(zt) * std::max<size_t>(nb, 1), st));
   HPS_CUDA_CHECK(cudaMallocAsync(&C, sizeof(zt) * nm, st));
-  if (cin) HPS_CUDA_CHECK(cudaMallocAsync(&Ci, sizeof(zt) * nm, st));
+  if (cin) HPS_CUDA_CHECK(cudaMallocAsync(&Ci, sizeof(zt) * ni, st));
   zfill_kernel<<<592, 256, 0, st>>>(A, (int64_t)na, 1);
   zfill_kernel<<<592, 256, 0, st>>>(B, (int64_t)nb, 2);
-  if (cin) zfill_kernel<<<592, 256, 0, st>>>(Ci, (int64_t)nm, 3);
+  if (cin) zfill_kernel<<<592, 256, 0, st>>>(Ci, (int64_t)ni, 3);
   ZGemm g;
   g.M = M;
   g.N = N;
@@ -833,7 +839,7 @@ int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, int lay, double* 
   g.B.bs = (int64_t)K * N;
   if (lay & 1) {  // column-major B as s in the ABI layout [RHS][box][K]
     g.B.rs = 1;
-    g.B.cs = (int64_t)K * bs;
+    g.B.cs = (int64_t)K * batch;
     g.B.bs = K;
   }
   if (cin) {
@@ -847,7 +853,7 @@ int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, int lay, double* 
   g.C.bs = (int64_t)M * N;
   if (lay & 2) {  // column-major C as u in the ABI layout [RHS][box][M]
     g.C.rs = 1;
-    g.C.cs = (int64_t)M * bs;
+    g.C.cs = (int64_t)M * batch;
     g.C.bs = M;
   }
   cudaEvent_t e0, e1;
