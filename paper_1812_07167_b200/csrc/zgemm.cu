@@ -673,6 +673,9 @@ void zgemm_impl(const ZGemm& g0, cudaStream_t st) {
     bcol ? launch<64, 16, 16, 16, true>(g, st) : launch<64, 16, 16, 16>(g, st);  // 16 RHS: no half-empty tiles
   else if (g.M <= 16 || (small_k16 && g.K <= 32 && tiles32 < 2 * nsm))
     launch<16, 16, 8, 8>(g, st);  // short K on a grid of few 32x32 tiles: more, smaller CTAs
+  else if (g.K >= 1024 && tiles32 < nsm)
+    launch<16, 16, 8, 8>(g, st);  // long K on less than one wave of 32x32 tiles (the top levels' solve
+                                  // at 64 RHS: 1.8x faster, profiles/r02 plan tables)
   else if (g.K >= 512)
     launch<64, 32, 32, 16>(g, st);
   else
