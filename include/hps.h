@@ -152,7 +152,10 @@ int hps_build(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, const
  *  t : incoming impedance data on the root boundary, [nrhs][2(nx+ny)q] in [S,E,N,W] order.
  *  u : output, [nrhs][nx*ny leaves][p*p-4]; each leaf in [I_b (S,E,N,W); I_i] order
  *      (PAPER.md:321-325).  Nodes on a shared edge appear once per leaf.
- *  Host or device pointers.  Multi-GPU (collective): s and u are this rank's rectangle
+ *  Host or device pointers.  Right-hand sides are processed in chunks (each a full upward +
+ *  downward sweep) of as many as fit in 40 % of the free device memory (knob rhs_chunk fixes it;
+ *  SURVEY hard part 7); host buffers are staged chunk by chunk.  Several chunks make the call
+ *  synchronous.  Multi-GPU (collective): s and u are this rank's rectangle
  *  ([nrhs][nx*ny/G][...], local natural order), t is the whole root boundary on every rank. */
 int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps_c128* u);
 
@@ -375,7 +378,7 @@ int hps_release_cache(void);
 /* Debug and tuning knobs (process-wide; the library reads no environment variables).  `name` is
  * one of: debug_alloc, big_cache, side, side_solve, nat_min, nat_max, nat_force_fail, dgj_pivot,
  * dgj_force_bad, dgj_rpt, lr_trace, gemv_short, gemv_k16, trace, gemm_smallk, gj, seq_pivot,
- * nat_w, nat_lpr, natc, natb, nat_pivot_rel, nat_bb_min, leaf_panel, gemm_bcol, gemm_group, leaf_inplace, seq_force_bad (meanings in csrc/hps_internal.cuh).  The *_force_*
+ * nat_w, nat_lpr, natc, natb, nat_pivot_rel, nat_bb_min, leaf_panel, gemm_bcol, gemm_group, leaf_inplace, seq_force_bad, rhs_chunk (meanings in csrc/hps_internal.cuh).  The *_force_*
  * and *_pivot knobs are FAULT INJECTION for the tests of the pivoted fallback paths: never set
  * them in production.  value -1 restores the default.  Returns 0 or HPS_EINVAL (unknown name). */
 int hps_debug_set(const char* name, int value);

@@ -47,7 +47,7 @@ const KnobDef g_knob_defs[KN_COUNT] = {
     {"lr_trace", 0},    {"gemv_short", 1}, {"gemv_k16", 256}, {"trace", 0},          {"gemm_smallk", 1},
     {"gj", 0},          {"seq_pivot", 0},  {"nat_w", 16},     {"nat_lpr", 4},        {"natc", 1},
     {"natb", 1},        {"nat_pivot_rel", 25}, {"nat_bb_min", 512}, {"leaf_panel", 0}, {"gemm_bcol", 1},
-    {"gemm_group", 8}, {"leaf_inplace", 1}, {"seq_force_bad", 0}};
+    {"gemm_group", 8}, {"leaf_inplace", 1}, {"seq_force_bad", 0}, {"rhs_chunk", 0}};
 std::atomic<int> g_knobs[KN_COUNT];
 std::once_flag g_knob_once;
 void knob_init() {
@@ -2198,6 +2198,34 @@ int hps_build_top(const hps_grid* g, int p, int q, double kappa, hps_c128 eta, i
   return HPS_OK;
 }
 
+// Right-hand sides per solve chunk (SURVEY hard part 7: C5's 128 RHS): the knob rhs_chunk, else as
+// many as fit in 40 % of the free device memory at ~1.6 x the leaf particular solutions u~
+// (nleaf x n_t per RHS) -- every vector of the sweeps included.
+int solve_chunk(const hps_handle& h, int nrhs) {
+  const int k = knob(KN_RHS_CHUNK);
+  if (k > 0) return std::min(k, nrhs);
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    cudaGetLastError();
+    return nrhs;
+  }
+  const double per = 16.0 * 1.6 * (double)h.nleaf * h.nt + 16.0 * 8.0 * h.depth[0].nb;
+  return (int)std::max(1.0, std::min((double)nrhs, 0.4 * (double)fr / per));
+}
+
+// The smallest value over the G ranks (every rank must run the same chunks: the top levels' sweeps
+// are collective).  One all-gather of one int.
+int agree_min(HpsComm* c, int G, int v, cudaStream_t st) {
+  DevBuf d;
+  d.alloc(sizeof(int) * (G + 1));
+  HPS_CUDA_CHECK(cudaMemcpyAsync(d.as<int>() + G, &v, sizeof(int), cudaMemcpyHostToDevice, st));
+  c->allgather(G, d.as<int>() + G, d.as<int>(), sizeof(int), st);
+  std::vector<int> all(G);
+  HPS_CUDA_CHECK(cudaMemcpyAsync(all.data(), d.p, sizeof(int) * G, cudaMemcpyDeviceToHost, st));
+  HPS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return *std::min_element(all.begin(), all.end());
+}
+
 int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps_c128* u) {
   if (!h || nrhs < 0 || !t || !u || !h->has_leaves) {
     hps_set_error("hps_solve: invalid argument (needs a leaf handle, t and u)");
@@ -2209,42 +2237,81 @@ int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps
     if (h->pending) finish_pending(*h);
     g_alloc_stream = h->st;
     LaunchScope ls(&h->launches[1], &h->prof);
-    DevBuf sd, td;
-    const zt* s_dev = dev_in(s, sizeof(zt) * (size_t)nrhs * h->nleaf * h->ni, sd, h->st);
     hps_handle* T = h->top.get();
     const int nb_root = T ? T->depth[0].nb : h->depth[0].nb;
-    const zt* t_dev = dev_in(t, sizeof(zt) * (size_t)nrhs * nb_root, td, h->st);
-    DevBuf tc;
-    if (h->gl) {
-      t_gl_to_cheb(T ? *T : *h, nrhs, t_dev, tc);
-      t_dev = tc.as<zt>();
+    // chunks of right-hand sides, each a full upward + downward sweep (s, t, u are RHS-outermost:
+    // a chunk is a contiguous slice); host buffers are staged chunk by chunk
+    int chunk = solve_chunk(*h, nrhs);
+    if (T) chunk = agree_min(T->comm, T->G, chunk, h->st);
+    const bool s_host = s && !is_device_ptr(s), t_host = !is_device_ptr(t), u_host = !is_device_ptr(u);
+    const size_t s_rhs = (size_t)h->nleaf * h->ni, t_rhs = (size_t)nb_root, u_rhs = (size_t)h->nleaf * h->nt;
+    const bool one = chunk >= nrhs;
+    double up_ms = 0, down_ms = 0, fl_up = 0, fl_down = 0;
+    cudaEvent_t* ce = h->ev + 3;  // [3] start, [4] between the sweeps, [5] end
+    for (int r0 = 0; r0 < nrhs; r0 += chunk) {
+      const int nr = std::min(chunk, nrhs - r0);
+      DevBuf sd, td, tc, ud;
+      const zt* s_dev = nullptr;
+      if (s) s_dev = dev_in(reinterpret_cast<const zt*>(s) + r0 * s_rhs, sizeof(zt) * nr * s_rhs, sd, h->st);
+      const zt* t_dev = dev_in(reinterpret_cast<const zt*>(t) + r0 * t_rhs, sizeof(zt) * nr * t_rhs, td, h->st);
+      if (h->gl) {
+        t_gl_to_cheb(T ? *T : *h, nr, t_dev, tc);
+        t_dev = tc.as<zt>();
+      }
+      zt* u_dev = reinterpret_cast<zt*>(u) + r0 * u_rhs;
+      if (u_host) {
+        ud.alloc(sizeof(zt) * nr * u_rhs);
+        u_dev = ud.as<zt>();
+      }
+      HPS_CUDA_CHECK(cudaEventRecord(ce[0], h->st));
+      if (!T) {
+        solve_up_impl(*h, nr, s_dev, nullptr);
+        HPS_CUDA_CHECK(cudaEventRecord(ce[1], h->st));
+        solve_down_impl(*h, nr, t_dev, u_dev);
+      } else {  // sharded: subtree up, top levels (collective), subtree down
+        const size_t nbs = (size_t)h->depth[0].nb * nr;
+        DevBuf hsub, tsub;
+        if (s_dev) hsub.alloc(sizeof(zt) * nbs);
+        solve_up_impl(*h, nr, s_dev, s_dev ? hsub.as<zt>() : nullptr);
+        solve_up_dist(*T, nr, s_dev ? hsub.as<zt>() : nullptr);
+        HPS_CUDA_CHECK(cudaEventRecord(ce[1], h->st));
+        tsub.alloc(sizeof(zt) * nbs);
+        solve_down_dist(*T, nr, t_dev, tsub.as<zt>());
+        solve_down_impl(*h, nr, tsub.as<zt>(), u_dev);
+        h->ss.flops_up += T->ss.flops_up;
+        h->ss.flops_down += T->ss.flops_down;
+      }
+      HPS_CUDA_CHECK(cudaEventRecord(ce[2], h->st));
+      if (u_host)
+        HPS_CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<zt*>(u) + r0 * u_rhs, u_dev, sizeof(zt) * nr * u_rhs,
+                                       cudaMemcpyDeviceToHost, h->st));
+      fl_up += h->ss.flops_up;
+      fl_down += h->ss.flops_down;
+      if (!one) {  // several chunks: phase times summed chunk by chunk (synchronous per chunk)
+        HPS_CUDA_CHECK(cudaEventSynchronize(ce[2]));
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ce[0], ce[1]);
+        cudaEventElapsedTime(&b, ce[1], ce[2]);
+        up_ms += a;
+        down_ms += b;
+      }
     }
-    DevOut uo(u, sizeof(zt) * (size_t)nrhs * h->nleaf * h->nt, h->st);
-    HPS_CUDA_CHECK(cudaEventRecord(h->ev[3], h->st));
-    if (!T) {
-      solve_up_impl(*h, nrhs, s_dev, nullptr);
-      HPS_CUDA_CHECK(cudaEventRecord(h->ev[4], h->st));
-      solve_down_impl(*h, nrhs, t_dev, uo.dev);
-    } else {  // sharded: subtree up, top levels (collective), subtree down
-      const size_t nbs = (size_t)h->depth[0].nb * nrhs;
-      DevBuf hsub, tsub;
-      if (s_dev) hsub.alloc(sizeof(zt) * nbs);
-      solve_up_impl(*h, nrhs, s_dev, s_dev ? hsub.as<zt>() : nullptr);
-      solve_up_dist(*T, nrhs, s_dev ? hsub.as<zt>() : nullptr);
-      HPS_CUDA_CHECK(cudaEventRecord(h->ev[4], h->st));
-      tsub.alloc(sizeof(zt) * nbs);
-      solve_down_dist(*T, nrhs, t_dev, tsub.as<zt>());
-      solve_down_impl(*h, nrhs, tsub.as<zt>(), uo.dev);
-      h->ss.flops_up += T->ss.flops_up;
-      h->ss.flops_down += T->ss.flops_down;
-    }
-    HPS_CUDA_CHECK(cudaEventRecord(h->ev[5], h->st));
-    uo.finish(h->st);
-    h->pending = true;
+    h->ss.flops_up = fl_up;
+    h->ss.flops_down = fl_down;
     h->solve_kind = 3;
-    const bool host_io = (s && s_dev != reinterpret_cast<const zt*>(s)) || t_dev != reinterpret_cast<const zt*>(t) ||
-                         uo.dev != reinterpret_cast<zt*>(u);
-    if (h->own_stream || host_io || h->prof.timing) finish_pending(*h);  // else: stream-ordered, hps_sync waits
+    const bool host_io = s_host || t_host || u_host;
+    if (host_io) HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));  // host u complete on return (pinned: async copy)
+    if (one) {
+      h->pending = true;  // finish_pending reads ev[3..5]
+      if (h->own_stream || host_io || h->prof.timing) finish_pending(*h);  // else: stream-ordered, hps_sync waits
+    } else {
+      HPS_CUDA_CHECK(cudaStreamSynchronize(h->st));
+      h->times[3] = up_ms + down_ms;
+      h->times[4] = up_ms;
+      h->times[5] = down_ms;
+      h->flops[1] = fl_up + fl_down;
+      h->pending = false;
+    }
   } catch (const HpsError& e) {
     return fail(e);
   } catch (const std::exception& e) {

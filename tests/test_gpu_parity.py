@@ -814,3 +814,25 @@ def test_plan_build_parity():
     O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
     assert rel(R1, O.R(1)) < TOL and rel(u1, O.solve(s, t)) < TOL
     assert rel(R1, R0) < 1e-12 and rel(u1, u0) < 1e-12
+
+
+def test_rhs_chunks():
+    """Right-hand sides in chunks (knob rhs_chunk; automatic by free memory otherwise, SURVEY hard
+    part 7): 37 RHS in chunks of 8 (the last of 5) equal one 37-RHS sweep to rounding and the oracle
+    at 1e-9, with host buffers (staged chunk by chunk) and with torch device buffers; the phase
+    times are summed over the chunks."""
+    import torch
+    nx, ny, p, kappa, eta = 4, 4, 12, 11.0, 11.0 + 1j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=37, seed=4)
+    S = hps.Solver(g, p, kappa, eta, c)
+    u_all = S.solve(s, t)
+    with hps.debug_knobs(rhs_chunk=8):
+        u_host = S.solve(s, t)
+        assert S.time_ms(3) > 0 and abs(S.time_ms(3) - S.time_ms(4) - S.time_ms(5)) < 1e-6
+        d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        u_dev = S.solve(d(s), d(t)).cpu().numpy()
+        u_nos = S.solve(None, t)
+    assert rel(u_host, u_all) < 1e-12 and rel(u_dev, u_all) < 1e-12
+    O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
+    assert rel(u_host, O.solve(s, t)) < TOL
+    assert rel(u_nos, O.solve(np.zeros_like(s), t)) < TOL
