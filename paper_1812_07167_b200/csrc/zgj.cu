@@ -2080,10 +2080,13 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
     const zt* Lx = fin.K;
     const zt* Ly = fin.K + q * q;
     const zt* cl = fin.c + (int64_t)fin.leaf_nat[fin.leaf0 + blockIdx.x] * fin.p * fin.p;
+    // column (jx, jy) of entry cc advances incrementally (cc += 32): no division per entry
+    const int dq = 32 / q, dr = 32 - dq * q, jx0 = lane % q, jy0 = lane / q;
     for (int r = tid >> 5; r < n; r += 16) {
       const int ix = r % q, iy = r / q;
+      zt* Mr = M + (int64_t)r * lda;
+      int jx = jx0, jy = jy0;
       for (int cc = lane; cc < n; cc += 32) {
-        const int jx = cc % q, jy = cc / q;
         zt v = make_double2(0.0, 0.0);
         if (iy == jy) v = Lx[ix * q + jx];
         if (ix == jx) {
@@ -2096,7 +2099,13 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
           v.y -= fin.kappa2 * cv.y;
           if (NAT) diag2[r] = fma(v.x, v.x, v.y * v.y);
         }
-        M[(int64_t)r * lda + cc] = v;
+        Mr[cc] = v;
+        jx += dr;
+        jy += dq;
+        if (jx >= q) {
+          jx -= q;
+          ++jy;
+        }
       }
     }
   }
