@@ -2209,6 +2209,10 @@ int solve_chunk(const hps_handle& h, int nrhs) {
     cudaGetLastError();
     return nrhs;
   }
+  {  // parked cache blocks count as free: they are given back before an allocation may fail
+    std::lock_guard<std::mutex> lk(g_big_mu);
+    fr += g_big_total;
+  }
   const double per = 16.0 * 1.6 * (double)h.nleaf * h.nt + 16.0 * 8.0 * h.depth[0].nb;
   return (int)std::max(1.0, std::min((double)nrhs, 0.4 * (double)fr / per));
 }
