@@ -2382,7 +2382,9 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       }
     }
     WS_MARK(p, 1);
-    // T -> shared (A operand) and back in place
+    // T -> shared (the A operand of the update); its copy back into M's panel columns is written
+    // coalesced from shared memory at the start of the update (nothing reads those columns before
+    // the next update)
 #pragma unroll
     for (int q = 0; q < 2; ++q)
       if (rq[q] < mtr) {
@@ -2390,7 +2392,6 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
         for (int c = 0; c < CPT; ++c) {
           const int j = cg * CPT + c;
           Ts[rq[q] * NB + j] = j < w ? a[q][c] : make_double2(0.0, 0.0);
-          if (j < w && rq[q] < n) M[(int64_t)rq[q] * lda + k0 + j] = a[q][c];
         }
       }
     if (NAT) {
@@ -2405,6 +2406,11 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
     // ---------------- update: C(i, J) = [i not a pivot of p] C(i, J) + T(i,:) Z(:, J) -------------
     for (int v = tid; v < nv + 16; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
     __syncthreads();  // T, pivots, colmap visible
+    if (!(NAT && fin.blockpanel))  // (the block-form panels wrote M already)
+      for (int e = tid; e < n * w; e += 512) {
+        const int i = e / w, j = e - i * w;
+        M[(int64_t)i * lda + k0 + j] = Ts[i * NB + j];
+      }
     if (!zpre) {
       for (int e = tid; e < w4 * nv; e += 512) {
         const int m = e / nv, v = e - m * nv;
