@@ -247,12 +247,18 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
 #pragma unroll
           for (int cc = 0; cc < CPT; ++cc) {
             const int j = cg * CPT + cc;
-            Ts[rq[t] * NB + j] = j < w ? a[t][cc] : 0.0;
-            if (j < w && rq[t] < n) M[(int64_t)rq[t] * n + k0 + j] = a[t][cc];
+            Ts[rq[t] * NB + j] = j < w ? a[t][cc] : 0.0;  // (M's panel columns: coalesced below)
           }
         }
     }
-    if (nv == 0) break;
+    if (nv == 0) {  // a single panel: T is the result
+      __syncthreads();
+      for (int e = tid; e < n * w; e += 512) {
+        const int i = e / w, j = e - i * w;
+        M[(int64_t)i * n + k0 + j] = Ts[i * NB + j];
+      }
+      break;
+    }
     LR_MARK(4 * pn + 1);
     if (!PIV) {
       __syncthreads();
@@ -261,6 +267,12 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
     // ---- update: all other columns, units of 8 rows x 32 columns ----
     for (int v = tid; v < nv + 32; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
     __syncthreads();
+    // T back into M's panel columns, coalesced from shared memory (nothing reads them before the
+    // next update; was one scattered 8-byte store per thread and column)
+    for (int e = tid; e < n * w; e += 512) {
+      const int i = e / w, j = e - i * w;
+      M[(int64_t)i * n + k0 + j] = Ts[i * NB + j];
+    }
     for (int e = tid; e < w4 * nv; e += 512) {
       const int m = e / nv, v = e - m * nv;
       if (m < w)

@@ -2402,7 +2402,15 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       }
     }
     }  // panel form
-    if (p + 1 == P.npan && nv == 0) break;
+    if (p + 1 == P.npan && nv == 0) {  // a single panel: T is the result; write it back and stop
+      __syncthreads();
+      if (!(NAT && fin.blockpanel))
+        for (int e = tid; e < n * w; e += 512) {
+          const int i = e / w, j = e - i * w;
+          M[(int64_t)i * lda + k0 + j] = Ts[i * NB + j];
+        }
+      break;
+    }
     // ---------------- update: C(i, J) = [i not a pivot of p] C(i, J) + T(i,:) Z(:, J) -------------
     for (int v = tid; v < nv + 16; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
     __syncthreads();  // T, pivots, colmap visible
