@@ -9,7 +9,9 @@ import bench
 cfg = inputs.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 g, c, s, t = bench.setup(cfg, hps)
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-hps.plan_problem(g, cfg.p)
+hps.plan_problem(g, cfg.p)          # as bench.py: the inverse regimes and the GEMM tile plans
+hps.plan_build(g, cfg.p)
+hps.plan_solve(g, cfg.p, s.shape[0])
 cd, sd, td = d(c), d(s), d(t)
 for it in range(2):
     if it == 1:
