@@ -54,7 +54,6 @@ enum HpsKnob {
   KN_LEAF_INPLACE,     // 1: natural-order complex leaf inverse in the store's Y_i block (no Y_i copy)
   KN_SEQ_FORCE_BAD,    // test: the natural-order complex leaf inverse fails its check at step 100
   KN_RHS_CHUNK,        // right-hand sides per solve chunk (0: as many as fit in 40 % of free memory)
-  KN_LEAF_FUSE_ASM,    // 1: natural-order leaf inverse computes S where its first pass reads it (no assembly)
   KN_COUNT
 };
 int knob(HpsKnob k);

@@ -1133,7 +1133,6 @@ struct WsFinish {
   double kappa2;
   int blockpanel = 0;    // natural-order panels in block form (knob leaf_panel, DESIGN 3.12)
   int inplace = 1;       // natural order: eliminate in the store's Y_i block (knob leaf_inplace)
-  int fuse_asm = 1;      // natural order: S computed where the first pass reads it (knob leaf_fuse_asm)
 };
 
 __host__ __device__ inline int ws_zs(int n) {  // Z row stride: >= n - wmin + 16, == 2 (mod 8)
@@ -2076,36 +2075,11 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
     if (NAT) plist[tid] = tid;
   }
   if (tid == 0) s_bad = 0;
-  // S = Lx (+) Ly - kappa^2 diag(c) (fin.c set).  Natural order with the step-by-step panels
-  // (knob leaf_fuse_asm): S is never stored -- the first pass computes the entries it reads (its
-  // panel, Z and the update's seeds) and writes the whole matrix through its update and T copy.
-  const int sq = fin.p - 2;
-  const zt* Lx = fin.K;
-  const zt* Ly = fin.K + sq * sq;
-  const zt* cl = fin.c ? fin.c + (int64_t)fin.leaf_nat[fin.leaf0 + blockIdx.x] * fin.p * fin.p : nullptr;
-  const bool fuse = NAT && fin.c && !fin.blockpanel && fin.fuse_asm;
-  auto sval = [&](int r, int cc) {
-    const int ix = r % sq, iy = r / sq, jx = cc % sq, jy = cc / sq;
-    zt v = make_double2(0.0, 0.0);
-    if (iy == jy) v = Lx[ix * sq + jx];
-    if (ix == jx) {
-      v.x += Ly[iy * sq + jy].x;
-      v.y += Ly[iy * sq + jy].y;
-    }
-    if (r == cc) {
-      const zt cv = cl[(iy + 1) * fin.p + ix + 1];
-      v.x -= fin.kappa2 * cv.x;
-      v.y -= fin.kappa2 * cv.y;
-    }
-    return v;
-  };
-  if (fuse) {
-    for (int r = tid; r < n; r += 512) {
-      const zt v = sval(r, r);
-      diag2[r] = fma(v.x, v.x, v.y * v.y);
-    }
-  } else if (fin.c) {  // assemble S in place (as zgj_ws_kernel)
-    const int q = sq;
+  if (fin.c) {  // assemble S in place (as zgj_ws_kernel)
+    const int q = fin.p - 2;
+    const zt* Lx = fin.K;
+    const zt* Ly = fin.K + q * q;
+    const zt* cl = fin.c + (int64_t)fin.leaf_nat[fin.leaf0 + blockIdx.x] * fin.p * fin.p;
     // column (jx, jy) of entry cc advances incrementally (cc += 32): no division per entry
     const int dq = 32 / q, dr = 32 - dq * q, jx0 = lane % q, jy0 = lane / q;
     for (int r = tid >> 5; r < n; r += 16) {
@@ -2152,21 +2126,13 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   for (int p = 0; p < P.npan; ++p) {
     const int k0 = P.k0(p), w = P.w(p), w4 = (w + 3) & ~3, K4 = w4 >> 2, nv = n - w;
     WS_MARK(p, 0);
-    const bool first = fuse && p == 0;  // pass 0 computes the S entries it reads
     if (zpre && !(p + 1 == P.npan && nv == 0)) {
-      if (first) {
-        for (int e = tid; e < w4 * nv; e += 512) {
-          const int m = e / nv, v = e - m * nv;
-          Zs[m * zs + v] = m < w ? sval(k0 + m, v < k0 ? v : v + w) : make_double2(0.0, 0.0);
-        }
-      } else {
-        for (int e = tid; e < w4 * nv; e += 512) {
-          const int m = e / nv, v = e - m * nv;
-          const bool ok = m < w;
-          cpa16_zfill(Zs + m * zs + v, M + (int64_t)(ok ? k0 + m : 0) * lda + (v < k0 ? v : v + w), ok);
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
+      for (int e = tid; e < w4 * nv; e += 512) {
+        const int m = e / nv, v = e - m * nv;
+        const bool ok = m < w;
+        cpa16_zfill(Zs + m * zs + v, M + (int64_t)(ok ? k0 + m : 0) * lda + (v < k0 ? v : v + w), ok);
       }
+      asm volatile("cp.async.commit_group;\n" ::);
     }
     if (NAT && fin.blockpanel) {
       // ---- natural-order panel in block form (knob leaf_panel = 1): the pivot rows are rows
@@ -2330,8 +2296,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         const int j = cg * CPT + c;
-        a[q][c] = (rq[q] < n && j < w) ? (first ? sval(rq[q], k0 + j) : ldplain(M + (int64_t)rq[q] * lda + k0 + j))
-                                       : make_double2(0.0, 0.0);
+        a[q][c] = (rq[q] < n && j < w) ? ldplain(M + (int64_t)rq[q] * lda + k0 + j) : make_double2(0.0, 0.0);
       }
     for (int cga = 0; cga * CPT < w; ++cga) {
       const bool act = cg == cga;
@@ -2484,8 +2449,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
         for (int h = 0; h < 2; ++h) {
           const int v = vb + t * 8 + h;
           U.col[t][h] = v < nv ? colmap[v] : -1;
-          U.seed[t][h] = first ? (U.col[t][h] >= 0 ? sval(rc, U.col[t][h]) : make_double2(0.0, 0.0))
-                               : ldplain(rowp + max(U.col[t][h], 0));
+          U.seed[t][h] = ldplain(rowp + max(U.col[t][h], 0));
         }
     };
     Unit cur, nxt;
@@ -3041,7 +3005,7 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
     kern<<<nbatch, 512, ws_smem(n) + dbytes, st>>>(
         S + (int64_t)b0 * sstride, n, sstride, store + (int64_t)b0 * mstride + (int64_t)nb * nt + nb, nt, mstride, n,
         info, WsFinish{K, R + (int64_t)b0 * nb * nb, m2ieta, p, c, leaf_nat, leaf0 + b0, kappa2, knob(KN_LEAF_PANEL),
-                       knob(KN_LEAF_INPLACE), knob(KN_LEAF_FUSE_ASM)});
+                       knob(KN_LEAF_INPLACE)});
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();
   }

@@ -127,8 +127,7 @@ def test_leaf_schur_natural_and_pivoted_paths():
     c = c + 0.05j
     for knobs in ({}, {"seq_pivot": 1}, {"leaf_panel": 1}, {"leaf_panel": 1 - hps.debug_get("leaf_panel")},
                   {"leaf_inplace": 0}, {"seq_force_bad": 1}, {"seq_force_bad": 1, "leaf_inplace": 0},
-                  {"leaf_panel": 2}, {"leaf_panel": 2, "seq_force_bad": 1}, {"leaf_fuse_asm": 0},
-                  {"leaf_fuse_asm": 0, "seq_force_bad": 1}):
+                  {"leaf_panel": 2}, {"leaf_panel": 2, "seq_force_bad": 1}):
         with hps.debug_knobs(**knobs):
             S = hps.Solver(g, 16, 7.0, 7.0 + 1j, c, keep_all_R=True)
             assert S.leaf_path() == 0
