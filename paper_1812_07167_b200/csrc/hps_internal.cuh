@@ -54,6 +54,7 @@ enum HpsKnob {
   KN_LEAF_INPLACE,     // 1: natural-order complex leaf inverse in the store's Y_i block (no Y_i copy)
   KN_SEQ_FORCE_BAD,    // test: the natural-order complex leaf inverse fails its check at step 100
   KN_RHS_CHUNK,        // right-hand sides per solve chunk (0: as many as fit in 40 % of free memory)
+  KN_DGJ_NT,           // threads per CTA of the real leaf Gauss-Jordan: 512 (one leaf per SM) or 256 (two)
   KN_COUNT
 };
 int knob(HpsKnob k);

@@ -97,7 +97,9 @@ __host__ __device__ inline int rl_zs(int n) {  // Z row stride (doubles): >= n -
 // >= 0.46 of the original diagonal, error 1e-14 in tools/nopiv_check.py); a pivot below 0.05 of
 // the original diagonal makes the body return false and the caller redoes the leaf with partial
 // pivoting.
-template <int RPT, bool PIV>
+// NT threads per CTA: 512 (one leaf per SM) or 256 with RPT = 4 (two leaves per SM: their
+// latency-bound pivot steps and DMMA updates interleave on the SM).
+template <int RPT, bool PIV, int NT = 512>
 __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __restrict__ perm, int leaf0,
                                               const int* __restrict__ leaf_nat, const zt* __restrict__ c, int p,
                                               const double* __restrict__ K, double kappa2,
@@ -105,7 +107,8 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
   // panel: NPW = 32 / RPT warps, RPT rows x CPT columns per thread (the other warps wait at the
   // block barrier that ends the panel: fewer warps per step means fewer redundant instructions
   // per pivot step, which is issue-bound)
-  constexpr int NB = RL_NB, CPT = NB / 4, NPW = 32 / RPT, RPW = 8 * RPT;
+  constexpr int NB = RL_NB, CPT = NB / 4, NPW = 32 / RPT, RPW = 8 * RPT, NW = NT / 32;
+  static_assert(NPW <= NW, "panel warps exceed the CTA");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int q = p - 2, n = q * q, mtr = (n + 15) & ~15, zs = rl_zs(n);
   double* Ts = reinterpret_cast<double*>(smem_raw);  // [mtr][NB]
@@ -121,7 +124,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
     const double* D2x = K;
     const double* D2y = K + q * q;
     const zt* cl = c + (int64_t)leaf_nat[leaf0 + blockIdx.x] * p * p;
-    for (int r = wp; r < n; r += 16) {
+    for (int r = wp; r < n; r += NW) {
       const int ix = r % q, iy = r / q;
       for (int cc = lane; cc < n; cc += 32) {
         const int jx = cc % q, jy = cc / q;
@@ -187,7 +190,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
               }
               key = __reduce_max_sync(0xffffffffu, key);
               if (lane == 0) wkey[par][wp] = key;
-              if (NPW == 16) __syncthreads(); else bsync(1, NPW * 32);
+              if (NPW == NW) __syncthreads(); else bsync(1, NPW * 32);
               unsigned best = 0u;
 #pragma unroll
               for (int g4 = 0; g4 < NPW / 4; ++g4) {
@@ -210,7 +213,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
                 plist[k] = r;
               }
             }
-            if (NPW == 16) __syncthreads(); else bsync(1, NPW * 32);
+            if (NPW == NW) __syncthreads(); else bsync(1, NPW * 32);
             if (!PIV && tid == 0 && !(fabs(prow[par][kk]) >= 0.05 * fabs(diag_s[k]))) s_bad = 1;
             if (warp_live) {
               const double inv = rinv(prow[par][kk]);
@@ -253,7 +256,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
     }
     if (nv == 0) {  // a single panel: T is the result
       __syncthreads();
-      for (int e = tid; e < n * w; e += 512) {
+      for (int e = tid; e < n * w; e += NT) {
         const int i = e / w, j = e - i * w;
         M[(int64_t)i * n + k0 + j] = Ts[i * NB + j];
       }
@@ -265,15 +268,15 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
       if (s_bad) return false;  // uniform: redo this leaf with partial pivoting
     }
     // ---- update: all other columns, units of 8 rows x 32 columns ----
-    for (int v = tid; v < nv + 32; v += 512) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
+    for (int v = tid; v < nv + 32; v += NT) colmap[v] = v < nv ? (v < k0 ? v : v + w) : -1;
     __syncthreads();
     // T back into M's panel columns, coalesced from shared memory (nothing reads them before the
     // next update; was one scattered 8-byte store per thread and column)
-    for (int e = tid; e < n * w; e += 512) {
+    for (int e = tid; e < n * w; e += NT) {
       const int i = e / w, j = e - i * w;
       M[(int64_t)i * n + k0 + j] = Ts[i * NB + j];
     }
-    for (int e = tid; e < w4 * nv; e += 512) {
+    for (int e = tid; e < w4 * nv; e += NT) {
       const int m = e / nv, v = e - m * nv;
       if (m < w)
         cpa8(Zs + m * zs + v, M + (int64_t)plist[k0 + m] * n + colmap[v]);
@@ -310,7 +313,7 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
     while (un < NU) {
       cur = nxt;
       const int cun = un;
-      un += 16;
+      un += NW;
       if (un < NU) load_unit(un, nxt);
       const int mt = cun % MT, vb = (cun / MT) * 32;
       double acc[4][2];
@@ -343,21 +346,22 @@ __device__ __forceinline__ bool dgj_leaf_body(double* __restrict__ Wk, int* __re
   if (!PIV && s_bad) return false;
   // A_ii^{-1}(k, j) = M(plist[k], pstep[j]): the permutations go out with M
   int* pb = perm + (size_t)blockIdx.x * 2 * n;
-  for (int e = tid; e < n; e += 512) {
+  for (int e = tid; e < n; e += NT) {
     pb[e] = plist[e];
     pb[n + e] = pstep[e];
   }
   return true;
 }
 
-template <int RPT>
-__global__ void __launch_bounds__(512, 1) dgj_leaf_kernel(double* __restrict__ Wk, int* __restrict__ perm, int leaf0,
-                                                          const int* __restrict__ leaf_nat, const zt* __restrict__ c,
-                                                          int p, const double* __restrict__ K, double kappa2,
-                                                          int* __restrict__ info, int pivot) {
-  if (pivot || !dgj_leaf_body<RPT, false>(Wk, perm, leaf0, leaf_nat, c, p, K, kappa2, info)) {
+template <int RPT, int NT = 512>
+__global__ void __launch_bounds__(NT, 512 / NT) dgj_leaf_kernel(double* __restrict__ Wk, int* __restrict__ perm,
+                                                                int leaf0, const int* __restrict__ leaf_nat,
+                                                                const zt* __restrict__ c, int p,
+                                                                const double* __restrict__ K, double kappa2,
+                                                                int* __restrict__ info, int pivot) {
+  if (pivot || !dgj_leaf_body<RPT, false, NT>(Wk, perm, leaf0, leaf_nat, c, p, K, kappa2, info)) {
     __syncthreads();
-    dgj_leaf_body<RPT, true>(Wk, perm, leaf0, leaf_nat, c, p, K, kappa2, info);
+    dgj_leaf_body<RPT, true, NT>(Wk, perm, leaf0, leaf_nat, c, p, K, kappa2, info);
   }
 }
 
@@ -1018,6 +1022,8 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
   if (!attr) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(dgj_leaf_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HPS_CUDA_CHECK(
+        cudaFuncSetAttribute(dgj_leaf_kernel<4, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
     HPS_CUDA_CHECK(cudaFuncSetAttribute(leaf_real_ops_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr = true;
   }
@@ -1026,9 +1032,9 @@ void launch_leaf_real(int p, int leaf0, int batch, const int* leaf_nat, const zt
                8.0 * batch * nid * nid + 16.0 * batch * ((nbd + nid) * (nbd + nid) + nbd * nbd), st);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nbatch = std::min(65535, batch - b0);
-    const int rpt = knob(KN_DGJ_RPT);
-    auto kern = rpt == 4 ? dgj_leaf_kernel<4> : dgj_leaf_kernel<2>;
-    kern<<<nbatch, 512, smemA, st>>>(Wk + (size_t)b0 * ni * ni, perm + (size_t)b0 * 2 * ni, leaf0 + b0,
+    const int rpt = knob(KN_DGJ_RPT), nt = knob(KN_DGJ_NT) == 256 && smemA <= 110 * 1024 ? 256 : 512;
+    auto kern = nt == 256 ? dgj_leaf_kernel<4, 256> : rpt == 4 ? dgj_leaf_kernel<4> : dgj_leaf_kernel<2>;
+    kern<<<nbatch, nt, smemA, st>>>(Wk + (size_t)b0 * ni * ni, perm + (size_t)b0 * 2 * ni, leaf0 + b0,
                                                 leaf_nat, c, p, K, kappa2, info, pivot ? 1 : 0);
     HPS_CUDA_CHECK(cudaGetLastError());
     count_launch();

@@ -155,16 +155,21 @@ def test_leaf_path_selection():
         hps.Solver(g, 8, 4.0, 4.0 + 1j, cc, leaf_mode=3)
 
 
-def test_leaf_real_batched_p16_many_leaves():
-    """64 leaves at p = 16 on the real path (several CTAs per SM wave), sampled leaves vs oracle."""
+@pytest.mark.parametrize("knobs", [{}, {"dgj_nt": 256}, {"dgj_nt": 256, "dgj_pivot": 1},
+                                   {"dgj_nt": 256, "dgj_force_bad": 1}])
+def test_leaf_real_batched_p16_many_leaves(knobs):
+    """64 leaves at p = 16 on the real path (several CTAs per SM wave), sampled leaves vs oracle; also
+    with two 256-thread leaves per SM (dgj_nt), pivoting from the start, and the natural-order
+    elimination failing its first check."""
     g, c, s, t = problem(8, 8, 16, 25.0, 25.0 + 3j)
-    S = hps.Solver(g, 16, 25.0, 25.0 + 3j, c)
-    assert S.leaf_path() == 3
-    for leaf in [0, 17, 63]:
-        Psi, Y = S.leaf_ops(leaf)
-        lo = oracle.leaf(16, 0.125, 0.125, 25.0, 25.0 + 3j, c[leaf])
-        assert rel(Psi, lo["Psi"]) < TOL
-        assert rel(Y, lo["Y"]) < TOL
+    with hps.debug_knobs(**knobs):
+        S = hps.Solver(g, 16, 25.0, 25.0 + 3j, c)
+        assert S.leaf_path() == 3
+        for leaf in [0, 17, 63]:
+            Psi, Y = S.leaf_ops(leaf)
+            lo = oracle.leaf(16, 0.125, 0.125, 25.0, 25.0 + 3j, c[leaf])
+            assert rel(Psi, lo["Psi"]) < TOL
+            assert rel(Y, lo["Y"]) < TOL
 
 
 @pytest.mark.parametrize("nx,ny,p", [(1, 1, 8), (2, 1, 8), (1, 2, 6), (4, 4, 8), (8, 4, 6), (4, 8, 10)])
