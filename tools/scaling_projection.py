@@ -47,9 +47,10 @@ for G in (1, 2, 4, 8):
     # Phi^b and R^tau (8 n3^2 n1 + 16 n3^2 ntau + 8 ntau^2 n3) / gs, at the measured big-product rate
     top_ms, gather_bytes = 0.0, 0.0
     rate = 33.5e12
-    for lv in (hps.dist_plan(g, cfg.p, G, 0) if G > 1 else []):
+    for d, lv in enumerate(hps.dist_plan(g, cfg.p, G, 0) if G > 1 else []):
         n3, n1, ntau, gs = lv["n3"], lv["n1"], lv["ntau"], lv["gs"]
-        fl = 16.0 * n3 ** 3 + (8.0 * n3 * n3 * n1 + 16.0 * n3 * n3 * ntau + 8.0 * ntau * ntau * n3) / gs
+        # (no R^tau at the root: keep_root_R = 0 throughout, as the G = 1 baseline)
+        fl = 16.0 * n3 ** 3 + (8.0 * n3 * n3 * n1 + 16.0 * n3 * n3 * ntau + (8.0 * ntau * ntau * n3 if d else 0.0)) / gs
         nbc = n1 + n3
         gb = 16.0 * 2 * nbc * nbc * (gs - 1) / gs      # children's ItI maps arriving in the group
         top_ms += 1e3 * fl / rate + 1e3 * gb / NVLINK
