@@ -48,7 +48,7 @@ const KnobDef g_knob_defs[KN_COUNT] = {
     {"gj", 0},          {"seq_pivot", 0},  {"nat_w", 16},     {"nat_lpr", 4},        {"natc", 1},
     {"natb", 1},        {"nat_pivot_rel", 25}, {"nat_bb_min", 512}, {"leaf_panel", 0}, {"gemm_bcol", 1},
     {"gemm_group", 8}, {"leaf_inplace", 1}, {"seq_force_bad", 0}, {"rhs_chunk", 0},
-    {"dgj_nt", 256}};
+    {"dgj_nt", 256}, {"merge_small", 1}};
 std::atomic<int> g_knobs[KN_COUNT];
 std::once_flag g_knob_once;
 void knob_init() {
@@ -1023,6 +1023,38 @@ void build_merge(hps_handle& H, int d) {
   NvtxRange nv("hps merge d=%d n3=%d x%d", d, M.n3, M.nparent);
   const int np = M.nparent, n1 = M.n1, n2 = M.n2, n3 = M.n3, nt = M.ntau, nbc = M.nbc;
   const int64_t cs2 = (int64_t)nbc * nbc;
+  const bool need_R0 = (d > 0) || H.keep_root_R || H.keep_all_R;
+  if (knob(KN_MERGE_SMALL) && merge_small_applies(n3, n1, n2)) {  // the whole level in one launch
+    MergeSmallArgs a;
+    a.R = H.R[d + 1].as<zt>();
+    a.nbc = nbc;
+    a.n1 = n1;
+    a.n2 = n2;
+    a.n3 = n3;
+    a.ntau = nt;
+    a.I1a = M.I1a;
+    a.I2b = M.I2b;
+    a.I3a = M.I3a;
+    a.I3b = M.I3b;
+    a.pp = M.pp;
+    a.R33a = M.R33a;
+    a.R33b = M.R33b;
+    a.R13a = M.R13a;
+    a.R23b = M.R23b;
+    a.Winv = M.Winv;
+    a.PhiA = M.PhiA;
+    a.PhiB = M.PhiB;
+    if (need_R0) {
+      H.R[d].alloc(sizeof(zt) * (size_t)nt * nt * np);
+      a.Rtau = H.R[d].as<zt>();
+    }
+    a.info = H.info.as<int>() + 1 + d;
+    launch_merge_small(a, np, H.st);
+    H.flops[0] += 8.0 * np * ((double)n3 * n3 * n3 * 2 + (double)n3 * n3 * n1 + 2.0 * n3 * n3 * nt +
+                              (need_R0 ? (double)nt * nt * n3 : 0.0));
+    if (!H.keep_all_R) H.R[d + 1].release();  // Algorithm 1 line 14
+    return;
+  }
   const zt* Ra = H.R[d + 1].as<zt>();
   const zt* Rb = Ra + cs2;
   const int64_t cbs = 2 * cs2;

@@ -55,6 +55,7 @@ enum HpsKnob {
   KN_SEQ_FORCE_BAD,    // test: the natural-order complex leaf inverse fails its check at step 100
   KN_RHS_CHUNK,        // right-hand sides per solve chunk (0: as many as fit in 40 % of free memory)
   KN_DGJ_NT,           // threads per CTA of the real leaf Gauss-Jordan: 512 (one leaf per SM) or 256 (two)
+  KN_MERGE_SMALL,      // 1: levels with n3 <= 28 merged by one CTA per merge (merge_small.cu)
   KN_COUNT
 };
 int knob(HpsKnob k);
@@ -200,6 +201,21 @@ void zgj_force_regime(int r);  // this thread; 0 = none
 
 // Debug timeline of the warp-specialised Gauss-Jordan kernel (hps_debug_ws_trace).
 void zgj_ws_trace(int on, long long* out);
+
+// One CTA per merge for the lowest merge levels (merge_small.cu): gathers, W, W^{-1}, Phi^a,
+// Phi^b and R^tau of a level in one launch, same outputs and layouts as build_merge.
+struct MergeSmallArgs {
+  const zt* R = nullptr;  // children's R: [2 np][nbc][nbc] (alpha = 2b, beta = 2b + 1)
+  int nbc = 0, n1 = 0, n2 = 0, n3 = 0, ntau = 0;
+  const int *I1a = nullptr, *I2b = nullptr, *I3a = nullptr, *I3b = nullptr, *pp = nullptr;
+  zt *R33a = nullptr, *R33b = nullptr, *R13a = nullptr, *R23b = nullptr, *Winv = nullptr, *PhiA = nullptr,
+     *PhiB = nullptr;
+  zt* Rtau = nullptr;  // [np][ntau][ntau] canonical, or nullptr (root without keep_root_R)
+  int* info = nullptr;  // set to 1 on an exactly singular W
+};
+bool merge_small_applies(int n3, int n1, int n2);
+size_t merge_small_smem(int n3, int n1, int n2);
+void launch_merge_small(const MergeSmallArgs& a, int np, cudaStream_t st);
 
 // Launch counter used for the gpu_launches report.
 extern thread_local int64_t* g_launch_counter;

@@ -841,3 +841,26 @@ def test_rhs_chunks():
     O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
     assert rel(u_host, O.solve(s, t)) < TOL
     assert rel(u_nos, O.solve(np.zeros_like(s), t)) < TOL
+
+
+@pytest.mark.parametrize("nx,ny,p", [(4, 4, 16), (8, 4, 10), (2, 2, 8), (16, 8, 6)])
+def test_merge_small_levels(nx, ny, p):
+    """Lowest merge levels (n3 <= 28) fused into one CTA per merge (merge_small.cu, knob merge_small):
+    every box's R and u match the oracle at 1e-9 and the GEMM path to rounding, with and without a
+    body load, complex eta."""
+    kappa, eta = 13.0, 13.0 - 2j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=ny / nx)
+    O = oracle.Oracle(0.0, 1.0, 0.0, ny / nx, nx, ny, p, kappa, eta, c, keep_all_R=True)
+    res = {}
+    for ms in (1, 0):
+        with hps.debug_knobs(merge_small=ms):
+            S = hps.Solver(g, p, kappa, eta, c, keep_all_R=True)
+            res[ms] = (S.solve(s, t), S.solve(None, t), [S.R(b) for b in range(1, oracle.tree_info(nx, ny)[0] + 1)])
+            S.close()
+    u1, u1n, R1 = res[1]
+    u0, u0n, R0 = res[0]
+    assert rel(u1, O.solve(s, t)) < TOL and rel(u1n, O.solve(np.zeros_like(s), t)) < TOL
+    assert rel(u1, u0) < 1e-12 and rel(u1n, u0n) < 1e-12
+    for b, (r1, r0) in enumerate(zip(R1, R0), start=1):
+        assert rel(r1, O.R(b)) < TOL, b
+        assert rel(r1, r0) < 1e-12, b
