@@ -132,10 +132,16 @@ def cpu_model():
     return "unknown"
 
 
-def cfg_dict(cfg, nrhs, world):
+def root_R_default(config):
+    """SURVEY.md hard part 8: the root operator R^1 is formed for the parity configs 1-3 and skipped
+    for 4-5 (Algorithm 2 never reads it)."""
+    return config <= 3
+
+
+def cfg_dict(cfg, nrhs, world, keep_root_R):
     """The workload description -- identical in both arms (the driver compares them)."""
     return {"workload": cfg.name, "leaves": f"{cfg.nx}x{cfg.ny}", "p": cfg.p, "nrhs": nrhs, "dof": cfg.n_unique,
-            "kappa": round(cfg.kappa, 4), "keep_root_R": True,
+            "kappa": round(cfg.kappa, 4), "keep_root_R": keep_root_R,
             "l2": "256 MiB buffer written between steps; stored operators (> 1 GB) exceed L2",
             "parallelism": "single GPU" if world == 1 else f"subtree shards x{world}"}
 
@@ -199,6 +205,7 @@ def run_hps(args, rank, world, dist):
     torch.cuda.set_device(local)
     cfg = inputs.CONFIGS[args.config]
     nrhs = args.nrhs or cfg.nrhs
+    root_R = args.keep_root_R
     g, c, s, t = setup(cfg, hps)
     s, t = s[:nrhs], t[:nrhs]
     comm, g_plan, nleaf = None, g, cfg.nleaf
@@ -231,12 +238,12 @@ def run_hps(args, rank, world, dist):
                                  "rule_ms": round(sum(a["rule_ms"] for a in ps), 3),
                                  "planned_ms": round(sum(a["best_ms"] for a in ps), 3)}
         # and the build's merge products (Algorithm 1 lines 7-12) the same way
-        pb = hps.plan_build(g_plan, cfg.p, keep_root_R=True)
+        pb = hps.plan_build(g_plan, cfg.p, keep_root_R=root_R)
         plan["build_actions"] = {"actions": len(pb), "planned": sum(a["cfg"] >= 0 for a in pb),
                                  "rule_ms": round(sum(a["rule_ms"] for a in pb), 3),
                                  "planned_ms": round(sum(a["best_ms"] for a in pb), 3)}
 
-    def step(profile=0, keep_root_R=True):
+    def step(profile=0, keep_root_R=root_R):
         S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_d, keep_root_R=keep_root_R, device=local, profile=profile,
                        comm=comm)
         S.solve(s_d, t_d, u_d)
@@ -278,12 +285,12 @@ def run_hps(args, rank, world, dist):
             flush_l2(torch, l2buf)
             torch.cuda.synchronize()
             krecs.append(step(profile=dom_mask))
-        # the build without the root operator R^1 (Algorithm 2 never reads it)
+        # the build the other way round (with R^1 where the headline skips it, and vice versa)
         nrecs = []
         for _ in range(kx):
             flush_l2(torch, l2buf)
             torch.cuda.synchronize()
-            nrecs.append(step(keep_root_R=False))
+            nrecs.append(step(keep_root_R=not root_R))
     clocks = clk.summary()
     step_ms = statistics.mean(r["build_ms"] + r["solve_ms"] for r in recs)
     build_ms = statistics.mean(r["build_ms"] for r in recs)
@@ -305,7 +312,7 @@ def run_hps(args, rank, world, dist):
         if world > 1:
             dist.barrier()
         e0 = time.perf_counter()
-        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_h, keep_root_R=True, device=local, comm=comm)
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c_h, keep_root_R=root_R, device=local, comm=comm)
         S.solve(s_h, t_h, u_h)
         _ = complex(u_h[0, 0, 0])        # result read on the host
         e1 = time.perf_counter()
@@ -319,28 +326,33 @@ def run_hps(args, rank, world, dist):
         e2e_s = tt.item()
 
     hps.set_cache_limit(0)   # give the parked blocks back
-    build_nr_ms = statistics.mean(r["build_ms"] for r in nrecs)
+    build_alt_ms = statistics.mean(r["build_ms"] for r in nrecs)
     if world > 1:
-        tt = torch.tensor([build_nr_ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([build_alt_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        build_nr_ms = tt.item()
+        build_alt_ms = tt.item()
         comm.close()
+    build_r_ms, build_nr_ms = (build_ms, build_alt_ms) if root_R else (build_alt_ms, build_ms)
     if rank != 0:
         return None
     dof = cfg.n_unique       # the whole job's unknowns (strong scaling: the same problem on N GPUs)
     value = dof / (step_ms / 1e3)
     peak64, peak64_src = fp64_peak()
     hbm, hbm_src = hbm_peak()
-    fl_build = flop_model(cfg)
+    fl_build_r = flop_model(cfg)
     fl_build_nr = flop_model(cfg, root_R=False)
+    fl_build = fl_build_r if root_R else fl_build_nr
     sb, sf = solve_model(cfg, nrhs)
     t_build_roof = fl_build / (world * peak64 * 1e12)          # N GPUs: N x the per-GPU peaks
     t_solve_roof = max(sb / (world * hbm * 1e9), sf / (world * peak64 * 1e12))
     roofs = {
         "model": "SURVEY 8(d): build = leaf 8 n_tau^3 + merges (8 flop per complex MAC) / FP64 DMMA peak; "
                  "solve = max(bytes / HBM, flop / DMMA) with every stored operator read once",
+        "keep_root_R": root_R,
         "build_flop": fl_build, "build_roofline_s": round(t_build_roof, 6),
         "build_frac": round(t_build_roof / (build_ms / 1e3), 4),
+        "build_flop_with_root_R": fl_build_r,
+        "build_frac_with_root_R": round(fl_build_r / (world * peak64 * 1e12) / (build_r_ms / 1e3), 4),
         "build_flop_no_root_R": fl_build_nr,
         "build_frac_no_root_R": round(fl_build_nr / (world * peak64 * 1e12) / (build_nr_ms / 1e3), 4),
         "build_executed_tflops": round(statistics.mean(r["build_flops"] for r in recs) / (build_ms / 1e3) / 1e12, 3),
@@ -385,8 +397,9 @@ def run_hps(args, rank, world, dist):
         "metric": METRIC, "value": round(value, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(step_ms, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": cfg_dict(cfg, nrhs, world),
+        "config": cfg_dict(cfg, nrhs, world, root_R),
         "build_s": round(build_ms / 1e3, 6), "build_dof_per_s": round(dof / (build_ms / 1e3), 1),
+        "build_s_with_root_R": round(build_r_ms / 1e3, 6),
         "build_s_no_root_R": round(build_nr_ms / 1e3, 6),
         "solve_ms_per_rhs": round(solve_ms / nrhs, 4),
         "build_tflops": round(statistics.mean(r["build_flops"] for r in recs) / (build_ms / 1e3) / 1e12, 3),
@@ -442,8 +455,8 @@ def cpu_baseline(cfg, c, s, t, args):
                            "y1": cfg.y0 + (cfg.y1 - cfg.y0) * 32 / cfg.ny, "nrhs": 1})
     from paper_1812_07167_b200 import hps
     g, cs, ss, ts_ = setup(sub, hps)
-    tb, tsv = oracle_run(sub, cs, ss[:1], ts_[:1])
-    f_full, f_sub = flop_model(cfg), flop_model(sub)
+    tb, tsv = oracle_run(sub, cs, ss[:1], ts_[:1])   # the oracle always forms the corner's R^1
+    f_full, f_sub = flop_model(cfg, root_R=args.keep_root_R), flop_model(sub)
     est = tb * f_full / f_sub + tsv * nrhs * (cfg.nleaf / sub.nleaf)
     return {"value": round(cfg.n_unique / est, 1), "unit": "DOF/s", "cores": cpu_cores(), "kind": "oracle",
             "sample": f"32x32-leaf corner, 1 RHS, build {tb:.2f} s + solve {tsv:.2f} s; extrapolated by the "
@@ -511,7 +524,7 @@ def run_reference(args, rank, world):
     return {"metric": METRIC, "value": round(val, 1), "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * step_s, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic", "impl": "reference",
-            "config": cfg_dict(cfg, nrhs, world),
+            "config": cfg_dict(cfg, nrhs, world, args.keep_root_R),
             "cpu_baseline": {"value": round(val, 1), "unit": "DOF/s", "cores": cpu_cores(), "kind": "oracle",
                              "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": round(val, 1), "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -527,7 +540,10 @@ def main():
     ap.add_argument("--impl", default="hps", choices=["hps", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-plan", action="store_true", help="skip the representative-action planner (default rules)")
+    ap.add_argument("--keep-root-R", type=int, default=None, choices=[0, 1],
+                    help="form the root operator R^1 (default: configs 1-3 yes, 4-5 no; SURVEY hard part 8)")
     args = ap.parse_args()
+    args.keep_root_R = root_R_default(args.config) if args.keep_root_R is None else bool(args.keep_root_R)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None
