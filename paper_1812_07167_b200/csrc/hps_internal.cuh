@@ -56,6 +56,7 @@ enum HpsKnob {
   KN_RHS_CHUNK,        // right-hand sides per solve chunk (0: as many as fit in 40 % of free memory)
   KN_DGJ_NT,           // threads per CTA of the real leaf Gauss-Jordan: 512 (one leaf per SM) or 256 (two)
   KN_MERGE_SMALL,      // 1: levels with n3 <= 28 merged by one CTA per merge (merge_small.cu)
+  KN_GEMM_3M,          // 1: tiled ZGEMM by three real products per complex MAC (3M form, DESIGN 3.14)
   KN_COUNT
 };
 int knob(HpsKnob k);

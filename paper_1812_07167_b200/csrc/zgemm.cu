@@ -4,7 +4,9 @@
 // blocked Gauss-Jordan update (zgj.cu) and of the solve sweeps (Algorithm 2) is one call of
 // this kernel.  sm_100a has no tcgen05 / TMEM path for f64 (ptxas rejects .kind::f64), so the
 // FP64 tensor path is warp-level mma.sync m8n8k4 (SASS DMMA.8x8x4).  A complex product is four
-// real DMMAs: Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br (no 3M trick: it costs accuracy).
+// real DMMAs, Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br, or (M3, knob gemm_3m) three:
+// T1 += Ar Br, T2 += Ai Bi, T3 += (Ar + Ai)(Br + Bi), then Cr = T1 - T2, Ci = T3 - T1 - T2 -- the
+// 3M form of ZGEMM3M, all in FP64 (normwise error bound a small constant times the 4M one).
 // Operands are staged global -> shared with cp.async (16 B = one complex element, zero-fill
 // for ragged edges and for "zero" map entries), double-buffered.  Shared-memory strides are
 // chosen so that the 8x4 / 4x8 DMMA fragments load as conflict-free 16-byte LDS.
@@ -56,7 +58,7 @@ struct Cfg {
 // BCOL: B is column-major (rs == 1, no maps: the solve reads s in the ABI layout [RHS][leaf][n_i],
 // columns 0.2-3 GB apart): the B tile is loaded k-fastest, so that a warp's cp.async requests cover
 // runs of BK consecutive elements of a column instead of one 16-byte piece per column.
-template <int BM, int BN, int WM, int WN, bool BCOL = false>
+template <int BM, int BN, int WM, int WN, bool BCOL = false, bool M3 = false>
 __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32) ? 3 : 0) zgemm_kernel(const ZGemm g) {
   using C = Cfg<BM, BN, WM, WN>;
   constexpr int NT = C::NT, TM = C::TM, TN = C::TN, AS = C::AS, BS = C::BS, ITA = C::ITA, ITB = C::ITB;
@@ -168,7 +170,8 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
     // Accumulators start at (beta / alpha) Cin, so the Cin loads overlap the first stage.  When
     // beta == alpha (every use but one) the raw values are loaded with no arithmetic, so all
     // loads are in flight together and the first DMMA is the first consumer.
-    double accr[TM][TN][2], acci[TM][TN][2];
+    // M3: accr = T1, acci = T3, acc2 = T2 (started at Cr, Cr + Ci and 0; converted before the epilogue)
+    double accr[TM][TN][2], acci[TM][TN][2], acc2[TM][TN][2];
     const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + zboff(g.Cin, b) : nullptr;
     const bool raw = g.beta.x == g.alpha.x && g.beta.y == g.alpha.y;
 #pragma unroll
@@ -203,6 +206,17 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
             acci[i][j][h] = v.y;
           }
     }
+    if constexpr (M3) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            acci[i][j][h] += accr[i][j][h];
+            acc2[i][j][h] = 0.0;
+          }
+    }
 
     for (int kt = 0; kt < nk; ++kt) {
       if (kt + 1 < nk) {
@@ -221,6 +235,25 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
         for (int i = 0; i < TM; ++i) af[i] = Ast[(i * 8 + (lane >> 2)) * AS + kk * 4 + (lane & 3)];
 #pragma unroll
         for (int j = 0; j < TN; ++j) bf[j] = Bst[(kk * 4 + (lane & 3)) * BS + j * 8 + (lane >> 2)];
+        if constexpr (M3) {
+          double as[TM], bs[TN];
+#pragma unroll
+          for (int i = 0; i < TM; ++i) as[i] = af[i].x + af[i].y;
+#pragma unroll
+          for (int j = 0; j < TN; ++j) bs[j] = bf[j].x + bf[j].y;
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(accr[i][j][0], accr[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(acc2[i][j][0], acc2[i][j][1], af[i].y, bf[j].y);
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) dmma(acci[i][j][0], acci[i][j][1], as[i], bs[j]);
+        } else {
         // four real sub-products, ordered so that consecutive DMMAs on one accumulator are
         // 2*TM*TN instructions apart (no back-to-back accumulator dependency)
 #pragma unroll
@@ -239,10 +272,23 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
         for (int i = 0; i < TM; ++i)
 #pragma unroll
           for (int j = 0; j < TN; ++j) dmma(acci[i][j][0], acci[i][j][1], af[i].y, bf[j].x);
+        }
       }
       __syncthreads();
     }
 
+    if constexpr (M3) {  // (T1, T3, T2) -> (Cr, Ci)
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double t1 = accr[i][j][h], t2 = acc2[i][j][h];
+            accr[i][j][h] = t1 - t2;
+            acci[i][j][h] = (acci[i][j][h] - t1) - t2;
+          }
+    }
     // Epilogue: C = alpha * acc + diag * [i == j]
     zt* Cb = g.C.ptr + zboff(g.C, b);
     // Column-contiguous output (rs == 1: the solve writes u straight into the ABI layout, RHS
@@ -304,9 +350,13 @@ template <int BM, int BN, int WM, int WN, bool BCOL = false>
 void launch(const ZGemm& g, cudaStream_t st) {
   using C = Cfg<BM, BN, WM, WN>;
   static bool attr_set = false;
-  auto kern = zgemm_kernel<BM, BN, WM, WN, BCOL>;
+  const bool m3 = knob(KN_GEMM_3M) != 0;
+  auto kern = m3 ? zgemm_kernel<BM, BN, WM, WN, BCOL, true> : zgemm_kernel<BM, BN, WM, WN, BCOL, false>;
   if (!attr_set) {
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<BM, BN, WM, WN, BCOL, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<BM, BN, WM, WN, BCOL, false>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr_set = true;
   }
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);

@@ -560,22 +560,46 @@ def test_virtual_comm_selftest():
     assert all(dist.run_virtual(8, fn))
 
 
+@pytest.mark.parametrize("m3", [1, 0])
 @pytest.mark.parametrize("cfg", list(range(14)))
 @pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1),
                                          (70, 1, 300, 2), (33, 3, 45, 3)])
-def test_zgemm_configs(cfg, M, N, K, batch):
-    """Every DMMA tile configuration vs the oracle's triple-loop product (ragged edges, beta)."""
+def test_zgemm_configs(cfg, M, N, K, batch, m3):
+    """Every DMMA tile configuration vs the oracle's triple-loop product (ragged edges, beta), in
+    the 4M and the 3M form (knob gemm_3m)."""
     rng = np.random.default_rng(M * 1000 + N + K)
     A = rng.standard_normal((batch, M, K)) + 1j * rng.standard_normal((batch, M, K))
     B = rng.standard_normal((batch, K, N)) + 1j * rng.standard_normal((batch, K, N))
     Cin = rng.standard_normal((batch, M, N)) + 1j * rng.standard_normal((batch, M, N))
     if cfg == 9 and N > 4:
         pytest.skip("GEMV path is for N <= 4")
-    for alpha, beta in [(1.0, 1.0), (-1.0, 0.5 - 2j)]:
-        C, _ = hps.zgemm_batched(A, B, Cin, alpha, beta, cfg=cfg)
-        for b in range(batch):
-            ref = alpha * oracle.matmul(A[b], B[b]) + beta * Cin[b]
-            assert rel(C[b], ref) < 1e-13
+    with hps.debug_knobs(gemm_3m=m3):
+        for alpha, beta in [(1.0, 1.0), (-1.0, 0.5 - 2j)]:
+            C, _ = hps.zgemm_batched(A, B, Cin, alpha, beta, cfg=cfg)
+            for b in range(batch):
+                ref = alpha * oracle.matmul(A[b], B[b]) + beta * Cin[b]
+                assert rel(C[b], ref) < 1e-13
+
+
+@pytest.mark.parametrize("cfg", [2, 5])
+def test_zgemm_3m_error_bound(cfg):
+    """3M vs 4M error against the oracle's product at long K and on operands whose imaginary parts
+    are 1e-6 of their real parts (where Ci = T3 - T1 - T2 cancels): normwise, the 3M error stays
+    within a small constant (Higham's bound for the 3M method) of the 4M error, and both <= 1e-14."""
+    rng = np.random.default_rng(7)
+    M, N, K = 96, 80, 3584
+    A = rng.standard_normal((1, M, K)) + 1j * rng.standard_normal((1, M, K))
+    B = rng.standard_normal((1, K, N)) + 1j * rng.standard_normal((1, K, N))
+    As = A.real + 1e-6j * A.imag
+    for a, b in [(A, B), (As, B), (As, B.real + 1e-6j * B.imag)]:
+        ref = oracle.matmul(a[0], b[0])
+        errs = []
+        for m3 in (0, 1):
+            with hps.debug_knobs(gemm_3m=m3):
+                C, _ = hps.zgemm_batched(a, b, None, 1.0, 0.0, cfg=cfg)
+            errs.append(np.linalg.norm(C[0] - ref) / (np.linalg.norm(a[0]) * np.linalg.norm(b[0])))
+        assert errs[0] < 1e-15 and errs[1] < 1e-15
+        assert errs[1] < 8 * errs[0] + 1e-17, errs
 
 
 # ---------------------------------------------------------------------------

@@ -48,7 +48,10 @@ def run(cfgno, seed):
 if __name__ == "__main__":
     import __graft_entry__
     __graft_entry__.build()
-    for cfgno, seeds in [(3, (9, 1, 2)), (4, (11, 1))]:
-        errs = [run(cfgno, sd) for sd in seeds]
-        print(json.dumps({"config": cfgno, "seeds": list(seeds), "rel_err_interior": [e for e, _ in errs],
-                          "s_over_u": [r for _, r in errs]}), flush=True)
+    knobs = {k: int(v) for k, v in (a.split("=") for a in sys.argv[1:])}   # e.g. gemm_3m=0
+    with hps.debug_knobs(**knobs):
+        for cfgno, seeds in [(3, (9, 1, 2)), (4, (11, 1))]:
+            errs = [run(cfgno, sd) for sd in seeds]
+            print(json.dumps({"config": cfgno, "seeds": list(seeds), "knobs": knobs,
+                              "rel_err_interior": [e for e, _ in errs], "s_over_u": [r for _, r in errs]}),
+                  flush=True)
