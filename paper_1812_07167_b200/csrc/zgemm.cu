@@ -844,9 +844,11 @@ void zgemm_plan_clear() {
 }
 
 int zgemm_candidates(int N, int* out) {
-  static const int c4[] = {9, 0, 1}, c16[] = {0, 1, 10, 11, 12, 13}, cbig[] = {2, 5, 4, 6, 1, 13};
+  // cfg 3 (64 x 64, 32 x 32 warps) only in the 3M form: its 96 accumulators spill a little, yet
+  // it beats the 64 x 32 tile there on the top-level products (41.8 vs 40.2 TFLOP/s, DESIGN 3.14)
+  static const int c4[] = {9, 0, 1}, c16[] = {0, 1, 10, 11, 12, 13}, cbig[] = {2, 5, 4, 6, 1, 13, 3};
   const int* c = N <= 4 ? c4 : N <= 16 ? c16 : cbig;
-  const int n = N <= 4 ? 3 : 6;
+  const int n = N <= 4 ? 3 : N <= 16 ? 6 : (knob(KN_GEMM_3M) ? 7 : 6);
   for (int i = 0; i < n; ++i) out[i] = c[i];
   return n;
 }
