@@ -2048,9 +2048,7 @@ __global__ void zgj_implicit_out_kernel(const zt* __restrict__ M, int64_t ldm, i
 // complement S assembled by the kernel itself (fin.c): in the configs' regimes natural-order
 // elimination of S keeps every pivot >= 0.37 of its original diagonal; a pivot
 // below 0.05 of it makes the body return false and the caller re-assembles S and pivots.
-// M3: the update's complex products in the 3M form (knob gemm_3m): 6 DMMAs per
-// 8 x 16 unit and k-step instead of 8.
-template <bool NAT, bool M3>
+template <bool NAT>
 __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, int64_t bs, zt* __restrict__ out,
                                              int64_t ldo, int64_t obs, int n, int* __restrict__ info,
                                              const WsFinish& fin) {
@@ -2475,8 +2473,7 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
       }
       have = npr < NPR;
       if (have) load_unit(mt, npr, nxt);
-      // M3: ar = T1 (from Re seed), ai = T3 (from Re + Im seed), a2 = T2
-      double ar[2][2], ai[2][2], a2[2][2];
+      double ar[2][2], ai[2][2];
 #pragma unroll
       for (int t = 0; t < 2; ++t)
 #pragma unroll
@@ -2484,46 +2481,10 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
           const bool ok = cur.rok && cur.col[t][h] >= 0;
           ar[t][h] = ok ? cur.seed[t][h].x : 0.0;
           ai[t][h] = ok ? cur.seed[t][h].y : 0.0;
-          if (M3) {
-            ai[t][h] += ar[t][h];
-            a2[t][h] = 0.0;
-          }
         }
       const zt* Trow = Ts + (cmt * 8 + (lane >> 2)) * NB + (lane & 3);
       const zt* Zc = Zs + (lane & 3) * zs + cnpr * 16 + (lane >> 2);
-      if (M3) {
-        if (cnpr * 16 + 8 < nv) {
-#pragma unroll 7
-          for (int k4 = 0; k4 < K4; ++k4) {
-            const zt av = Trow[k4 * 4];
-            const zt b0 = Zc[k4 * 4 * zs], b1 = Zc[k4 * 4 * zs + 8];
-            const double as = av.x + av.y, bs0 = b0.x + b0.y, bs1 = b1.x + b1.y;
-            dmma884(ar[0][0], ar[0][1], av.x, b0.x);
-            dmma884(ar[1][0], ar[1][1], av.x, b1.x);
-            dmma884(a2[0][0], a2[0][1], av.y, b0.y);
-            dmma884(a2[1][0], a2[1][1], av.y, b1.y);
-            dmma884(ai[0][0], ai[0][1], as, bs0);
-            dmma884(ai[1][0], ai[1][1], as, bs1);
-          }
-        } else {
-#pragma unroll 7
-          for (int k4 = 0; k4 < K4; ++k4) {
-            const zt av = Trow[k4 * 4];
-            const zt b0 = Zc[k4 * 4 * zs];
-            dmma884(ar[0][0], ar[0][1], av.x, b0.x);
-            dmma884(a2[0][0], a2[0][1], av.y, b0.y);
-            dmma884(ai[0][0], ai[0][1], av.x + av.y, b0.x + b0.y);
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < 2; ++t)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const double t1 = ar[t][h], t2 = a2[t][h];
-            ar[t][h] = t1 - t2;
-            ai[t][h] = (ai[t][h] - t1) - t2;
-          }
-      } else if (cnpr * 16 + 8 < nv) {
+      if (cnpr * 16 + 8 < nv) {
 #pragma unroll 7
         for (int k4 = 0; k4 < K4; ++k4) {
           const zt av = Trow[k4 * 4];
@@ -2568,7 +2529,6 @@ __device__ __forceinline__ bool zgj_seq_body(zt* __restrict__ A, int64_t lda, in
   return true;
 }
 
-template <bool M3>
 __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int64_t lda, int64_t bs,
                                                          zt* __restrict__ out, int64_t ldo, int64_t obs, int n,
                                                          int* __restrict__ info, const WsFinish fin) {
@@ -2576,20 +2536,12 @@ __global__ void __launch_bounds__(512, 1) zgj_seq_kernel(zt* __restrict__ A, int
     // natural order in place: the work matrix is the leaf operator's own Y_i block (the epilogue
     // then leaves Y_i = S^{-1} where it is; the pivoted fallback uses the scratch matrix A)
     const bool inpl = fin.p != 0 && fin.inplace;
-    if (inpl ? zgj_seq_body<true, M3>(out, ldo, obs, out, ldo, obs, n, info, fin)
-             : zgj_seq_body<true, M3>(A, lda, bs, out, ldo, obs, n, info, fin))
+    if (inpl ? zgj_seq_body<true>(out, ldo, obs, out, ldo, obs, n, info, fin)
+             : zgj_seq_body<true>(A, lda, bs, out, ldo, obs, n, info, fin))
       return;
     __syncthreads();
   }
-  zgj_seq_body<false, M3>(A, lda, bs, out, ldo, obs, n, info, fin);
-}
-
-// the leaf / merge sequential-phase inverse in the configured product form (knob gemm_3m)
-using SeqKern = void (*)(zt*, int64_t, int64_t, zt*, int64_t, int64_t, int, int*, const WsFinish);
-SeqKern seq_kernel() { return knob(KN_GEMM_3M) ? zgj_seq_kernel<true> : zgj_seq_kernel<false>; }
-void seq_kernel_attr(int bytes) {
-  HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  zgj_seq_body<false>(A, lda, bs, out, ldo, obs, n, info, fin);
 }
 
 // pi = S_{n-1} o ... o S_0 (one thread per matrix)
@@ -2870,10 +2822,11 @@ void zgj_invert_impl(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64
     if (!wattr) {
       HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)ws_smem(WS_NMAX)));
-      seq_kernel_attr((int)ws_smem(WS_NMAX));
+      HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)ws_smem(WS_NMAX)));
       wattr = true;
     }
-    auto kern = reg == REG_SEQ ? seq_kernel() : zgj_ws_kernel;
+    auto kern = reg == REG_SEQ ? zgj_seq_kernel : zgj_ws_kernel;
     for (int b0 = 0; b0 < batch; b0 += 65535) {
       const int nbatch = std::min(65535, batch - b0);
       kern<<<nbatch, 512, ws_smem(n), st>>>(A + (int64_t)b0 * bs, lda, bs, out + (int64_t)b0 * obs, ldo,
@@ -3034,7 +2987,8 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
   if (!wattr) {
     HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_ws_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)ws_smem(WS_NMAX)));
-    seq_kernel_attr((int)ws_smem(WS_NMAX));
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgj_seq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)ws_smem(WS_NMAX)));
     wattr = true;
   }
   const double ni = n;
@@ -3043,7 +2997,7 @@ bool zgj_invert_leaf_schur(zt* S, int64_t sstride, zt* store, int64_t mstride, i
   const zt m2ieta = make_double2(2.0 * eta.y, -2.0 * eta.x);
   for (int b0 = 0; b0 < batch; b0 += 65535) {
     const int nbatch = std::min(65535, batch - b0);
-    auto kern = choose_regime(n, batch) == REG_SEQ ? seq_kernel() : zgj_ws_kernel;
+    auto kern = choose_regime(n, batch) == REG_SEQ ? zgj_seq_kernel : zgj_ws_kernel;
     // leaf_panel 2: two (NB x NB+1) ping-pong copies of the panel's diagonal block after Z
     const int bp = knob(KN_LEAF_PANEL);
     const size_t dbytes = bp == 2 ? sizeof(zt) * 2 * WS_NB * (WS_NB + 1) : 0;
