@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
   // launch bounds (round 2's first grouped order raised it to 180 registers, 2 CTAs per SM).
   const int tilesN = (g.N + BN - 1) / BN;
   int m0, n0;
-  constexpr bool kGroup = BM == 64 && BN == 32;  // only the long-K merge tile (registers elsewhere)
+  constexpr bool kGroup = BM == 64 && (BN == 32 || (BN == 64 && WN == 32));  // the long-K merge tiles (registers elsewhere)
   if (!kGroup || g.group_m <= 1) {
     m0 = (blockIdx.x / tilesN) * BM;
     n0 = (blockIdx.x % tilesN) * BN;

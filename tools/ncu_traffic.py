@@ -51,8 +51,28 @@ def summarise(launches):
     return agg, tot
 
 
+def per_kernel(launches):
+    """Per kernel name (template arguments kept): launches, serialised time, DRAM bytes."""
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
+    for d in launches:
+        k = d["name"].split("(")[0].replace("<unnamed>::", "").replace("void ", "")
+        agg[k][0] += 1
+        agg[k][1] += d.get("gpu__time_duration.sum", 0.0)
+        agg[k][2] += d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+    tot = sum(a[1] for a in agg.values())
+    out = []
+    for k, (n, ns, by) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        out.append(f"{ns / 1e6:10.3f} ms {100 * ns / tot:5.1f}% {n:6d} launches {by / 1e9:10.2f} GB "
+                   f"{by / max(ns, 1) / 1e3:5.1f} TB/s  {k}")
+    out.append(f"{tot / 1e6:.3f} ms total, {sum(a[0] for a in agg.values())} launches")
+    return "\n".join(out)
+
+
 if __name__ == "__main__":
     L = load(sys.argv[1])
+    if len(sys.argv) > 2 and sys.argv[2] == "--kernels":
+        print(per_kernel(L))
+        sys.exit(0)
     agg, tot = summarise(L)
     for k, a in sorted(agg.items(), key=lambda x: -x[1]["ns"]):
         print(f"{k:14s} {a['launches']:6d} launches {a['ns'] / 1e6:10.3f} ms {100 * a['ns'] / tot:5.1f}%  "
