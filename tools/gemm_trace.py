@@ -16,6 +16,10 @@ g, c, s, t = bench.setup(cfg, hps)
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
 cd, sd, td = d(c), d(s), d(t)
 hps.plan_problem(g, cfg.p)
+if "--plan" in sys.argv:    # as bench.py: the build and solve GEMM plans too
+    hps.plan_build(g, cfg.p, keep_root_R=bench.root_R_default(int(sys.argv[1])))
+    hps.plan_solve(g, cfg.p, s.shape[0])
+print("nrhs", s.shape[0], file=sys.stderr, flush=True)
 S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, cd)   # warm-up
 S.solve(sd, td)
 S.close()
