@@ -37,3 +37,17 @@ def test_reference_arm_line():
 
 def test_reference_arm_nonzero_rank_silent():
     assert _run({"RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+def test_root_R_rule_and_flop_model():
+    """SURVEY hard part 8: R^1 formed for configs 1-3, skipped for 4-5; the flop model drops exactly
+    the root's R^tau product (8 n_tau^2 n3 at the root) when it is skipped."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_1812_07167_b200 import inputs
+    assert [bench.root_R_default(c) for c in (1, 2, 3, 4, 5)] == [True, True, True, False, False]
+    for c in (2, 4):
+        cfg = inputs.CONFIGS[c]
+        d, n3, n1, ntau = bench.merge_levels(cfg)[0]
+        assert d == 0
+        assert bench.flop_model(cfg) - bench.flop_model(cfg, root_R=False) == 8.0 * ntau * ntau * n3

@@ -624,6 +624,24 @@ def test_config2_full_vs_oracle():
     assert rel(u, O.solve(s, t)) < TOL
 
 
+@pytest.mark.parametrize("m3", [0, 1])
+def test_config2_product_forms(m3):
+    """C2 whole problem in each complex-product form (knob gemm_3m): root R and u vs
+    the oracle at the suite's tolerance, and the two forms within 1e-12 of each other."""
+    cfg, g, c, s, t = _bench_inputs(2)
+    with hps.debug_knobs(gemm_3m=m3):
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
+        u = S.solve(s, t)
+        R = S.R(1)
+    with hps.debug_knobs(gemm_3m=1 - m3):
+        S2 = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
+        u2 = S2.solve(s, t)
+    O = oracle.Oracle(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p, cfg.kappa, cfg.eta, c)
+    assert rel(R, O.R(1)) < TOL
+    assert rel(u, O.solve(s, t)) < TOL
+    assert rel(u, u2) < 1e-12
+
+
 def test_config3_sampled_leaves_and_merges():
     """C3 (128x128 leaves, 10 ppw): sampled leaves vs oracle.leaf, and level-local merges — the
     GPU children's R fed to oracle.merge must give the GPU parent R — at EVERY level, one sampled
