@@ -347,17 +347,19 @@ int hps_debug_ws_trace(int on, int64_t* out);
 
 /* Batched complex GEMM through the library's DMMA kernel: C = alpha A B + beta Cin for
  * contiguous row-major A [batch][M][K], B [batch][K][N], Cin / C [batch][M][N] (Cin may be
- * NULL).  cfg selects a tile configuration (-1 = the library's choice); the call runs `reps`
- * times after one warm-up and returns the mean device time in *ms.  Exposed for kernel tests
- * and tuning. */
+ * NULL).  cfg selects a tile configuration (-1 = the library's choice; tile | (slices << 8) with
+ * slices 2, 4 or 8 is the deterministic split-K form of a tiled configuration: per-slice partial
+ * tiles in a stream-ordered workspace summed in slice order); the call runs `reps` times after one
+ * warm-up and returns the mean device time in *ms.  Exposed for kernel tests and tuning.  An unknown
+ * cfg falls back to the library's choice. */
+int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A, const hps_c128* B,
+                      const hps_c128* Cin, hps_c128* C, hps_c128 alpha, hps_c128 beta, int reps, double* ms);
+
 /* Live FP64 tensor-core peak of the current device: 8 independent m8n8k4 DMMA chains per warp, 8
  * CTAs of 8 warps per SM, best of 3 timed launches (~0.1 s).  The roofline denominator of the
  * FP64-bound kernels measured in the same process and at the same clocks (MEASURED_PEAKS.json has no
  * FP64 entry).  Returns 0 or HPS_ECUDA. */
 int hps_fp64_peak(double* tflops);
-
-int hps_zgemm_batched(int cfg, int M, int N, int K, int batch, const hps_c128* A, const hps_c128* B,
-                      const hps_c128* Cin, hps_c128* C, hps_c128 alpha, hps_c128 beta, int reps, double* ms);
 
 void hps_free(hps_handle* h);
 

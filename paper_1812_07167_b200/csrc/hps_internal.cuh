@@ -126,6 +126,10 @@ struct ZGemm {
   zt alpha = {1.0, 0.0};
   zt beta = {0.0, 0.0};
   zt diag = {0.0, 0.0};
+  // split-K (set by zgemm from the plan): ksplit slices of K, each CTA slice writes its raw partial
+  // tile to ws[slice][batch][M][N]; a second kernel sums the slices in slice order (deterministic)
+  int ksplit = 1;
+  zt* ws = nullptr;
 };
 
 void zgemm(const ZGemm& g, cudaStream_t st);

@@ -93,6 +93,10 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
   constexpr int A_RSTEP = NT / BK;
   constexpr int B_RSTEP = (NT >= BN) ? NT / BN : 1;
 
+  // split-K: this CTA's slice [kbeg, kend) of K (whole BK stages; slice 0 carries Cin)
+  const int ksl = blockIdx.z;
+  const int kchunk = ((g.K + (int)gridDim.z - 1) / (int)gridDim.z + BK - 1) / BK * BK;
+  const int kbeg = ksl * kchunk, kend = min(g.K, kbeg + kchunk);
   for (int b = blockIdx.y; b < g.batch; b += gridDim.y) {
     const zt* Ab = g.A.ptr + zboff(g.A, b);
     const zt* Bb = g.B.ptr + zboff(g.B, b);
@@ -135,7 +139,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
     auto load_stage = [&](int stage, int k0) {
       {
         const int gk = k0 + a_c;
-        int ck = gk < g.K ? zcol(g.A.cmap, gk, g.A.cskip_at, g.A.cskip_len) : -1;
+        int ck = gk < kend ? zcol(g.A.cmap, gk, g.A.cskip_at, g.A.cskip_len) : -1;
         const int64_t coff = (int64_t)(ck < 0 ? 0 : ck) * g.A.cs;
 #pragma unroll
         for (int it = 0; it < ITA; ++it) {
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
 #pragma unroll
         for (int it = 0; it < ITB; ++it) {
           const int jj = tid / BK + it * BC_JSTEP;
-          const bool ok = bc_ok[it] && gk < g.K;
+          const bool ok = bc_ok[it] && gk < kend;
           cp_async16(&Bs[(stage * BK + kk) * BS + jj], ok ? Bb + gk + bc_off[it] : g.B.ptr, ok);
         }
       } else {
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
         for (int it = 0; it < ITB; ++it) {
           const int r = b_r0 + it * B_RSTEP;
           const int gk = k0 + r;
-          int rk = gk < g.K ? (Brm ? Brm[gk] : gk) : -1;
+          int rk = gk < kend ? (Brm ? Brm[gk] : gk) : -1;
           const bool ok = b_cok && rk >= 0;
           cp_async16(&Bs[(stage * BK + r) * BS + b_c], ok ? Bb + (int64_t)rk * g.B.rs + b_coff : g.B.ptr, ok);
         }
@@ -164,15 +168,15 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
       cp_async_commit();
     };
 
-    const int nk = (g.K + BK - 1) / BK;
-    if (nk > 0) load_stage(0, 0);
+    const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+    if (nk > 0) load_stage(0, kbeg);
 
     // Accumulators start at (beta / alpha) Cin, so the Cin loads overlap the first stage.  When
     // beta == alpha (every use but one) the raw values are loaded with no arithmetic, so all
     // loads are in flight together and the first DMMA is the first consumer.
     // M3: accr = T1, acci = T3, acc2 = T2 (started at Cr, Cr + Ci and 0; converted before the epilogue)
     double accr[TM][TN][2], acci[TM][TN][2], acc2[TM][TN][2];
-    const zt* Cinb = g.Cin.ptr ? g.Cin.ptr + zboff(g.Cin, b) : nullptr;
+    const zt* Cinb = (g.Cin.ptr && ksl == 0) ? g.Cin.ptr + zboff(g.Cin, b) : nullptr;
     const bool raw = g.beta.x == g.alpha.x && g.beta.y == g.alpha.y;
 #pragma unroll
     for (int i = 0; i < TM; ++i) {
@@ -220,7 +224,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
 
     for (int kt = 0; kt < nk; ++kt) {
       if (kt + 1 < nk) {
-        load_stage((kt + 1) & 1, (kt + 1) * BK);
+        load_stage((kt + 1) & 1, kbeg + (kt + 1) * BK);
         cp_async_wait1();
       } else {
         cp_async_wait0();
@@ -288,6 +292,22 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
             accr[i][j][h] = t1 - t2;
             acci[i][j][h] = (acci[i][j][h] - t1) - t2;
           }
+    }
+    if (g.ws) {  // split-K: the raw partial tile of this slice (alpha, diag and C's maps in the reduction)
+      zt* Wb = g.ws + ((int64_t)ksl * g.batch + b) * g.M * g.N;
+#pragma unroll
+      for (int i = 0; i < TM; ++i) {
+        const int gi = m0 + wm * C::TM * 8 + i * 8 + (lane >> 2);
+        if (gi >= g.M) continue;
+#pragma unroll
+        for (int j = 0; j < TN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int gj = n0 + wn * C::TN * 8 + j * 8 + (lane & 3) * 2 + h;
+            if (gj < g.N) Wb[(int64_t)gi * g.N + gj] = make_double2(accr[i][j][h], acci[i][j][h]);
+          }
+      }
+      continue;
     }
     // Epilogue: C = alpha * acc + diag * [i == j]
     zt* Cb = g.C.ptr + zboff(g.C, b);
@@ -360,7 +380,7 @@ void launch(const ZGemm& g, cudaStream_t st) {
     attr_set = true;
   }
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
-  dim3 grid(tiles, g.batch < 65535 ? g.batch : 65535);
+  dim3 grid(tiles, g.batch < 65535 ? g.batch : 65535, g.ws ? g.ksplit : 1);
   kern<<<grid, C::NT, C::SMEM, st>>>(g);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
@@ -650,13 +670,61 @@ void zgemm(const ZGemm& g, cudaStream_t st) {
   cudaEventDestroy(b);
 }
 
+// split-K reduction: C(i, j) = alpha * sum_s ws[s](i, j) + diag [i == j], slices summed in order
+__global__ void zsplit_reduce_kernel(const ZGemm g) {
+  const int64_t mn = (int64_t)g.M * g.N, total = mn * g.batch;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / mn);
+    const int64_t r = e - (int64_t)b * mn;
+    const int i = (int)(r / g.N), j = (int)(r - (int64_t)i * g.N);
+    const int* Crm = g.C.rmap ? g.C.rmap + (int64_t)b * g.C.rmap_bs : nullptr;
+    const int ro = zrow(g.C, Crm, i), co = zcol(g.C.cmap, j, g.C.cskip_at, g.C.cskip_len);
+    if (ro < 0 || co < 0) continue;
+    zt acc = g.ws[e];
+    for (int s = 1; s < g.ksplit; ++s) {
+      const zt v = g.ws[(int64_t)s * total + e];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    zt v = zmul(g.alpha, acc);
+    if (i == j) {
+      v.x += g.diag.x;
+      v.y += g.diag.y;
+    }
+    g.C.ptr[zboff(g.C, b) + (int64_t)ro * g.C.rs + (int64_t)co * g.C.cs] = v;
+  }
+}
+
 thread_local int g_zgemm_force = -1;  // tile configuration override (tests / tuning)
 
 static bool bcol_applies(const ZGemm& g) {
   return g.B.rs == 1 && g.B.cs > 1 && !g.B.rmap && !g.B.cmap && g.B.cskip_len == 0 && knob(KN_GEMM_BCOL);
 }
 
-bool launch_cfg(int cfg, const ZGemm& g, cudaStream_t st) {
+bool launch_cfg_tile(int cfg, const ZGemm& g, cudaStream_t st);
+
+// A configuration is tile | (split << 8): split-K with `split` slices (2, 4, 8) of the tiled
+// kernels (not the GEMV), partial tiles in a stream-ordered workspace and one reduction launch.
+bool launch_cfg(int cfg, const ZGemm& g0, cudaStream_t st) {
+  const int split = cfg >> 8, tile = cfg & 255;
+  if (split <= 1 || tile == 9) return launch_cfg_tile(tile, g0, st);
+  ZGemm g = g0;
+  g.ksplit = split;
+  const size_t bytes = sizeof(zt) * (size_t)split * g.batch * g.M * g.N;
+  HPS_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&g.ws), bytes, st));
+  const bool ok = launch_cfg_tile(tile, g, st);
+  if (ok) {
+    const int64_t total = (int64_t)g.batch * g.M * g.N;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 8LL * hps_num_sms());
+    zsplit_reduce_kernel<<<blocks, 256, 0, st>>>(g);
+    HPS_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+  }
+  HPS_CUDA_CHECK(cudaFreeAsync(g.ws, st));
+  return ok;
+}
+
+bool launch_cfg_tile(int cfg, const ZGemm& g, cudaStream_t st) {
   switch (cfg) {
     case 0: launch<64, 8, 16, 8>(g, st); return true;
     case 1: bcol_applies(g) ? launch<16, 16, 8, 8, true>(g, st) : launch<16, 16, 8, 8>(g, st); return true;
@@ -859,7 +927,18 @@ int zgemm_candidates(int N, int* out) {
 // and the rule's to *t_rule; returns the chosen configuration (-1: the rule).
 int zgemm_plan_shape(int M, int N, int K, int batch, bool cin, int lay, double* t_out, double* t_rule, int* cands,
                      int* ncand, cudaStream_t st) {
-  const int nc = zgemm_candidates(N, cands);
+  int nc = zgemm_candidates(N, cands);
+  // split-K candidates (deterministic, launch_cfg) for long-K shapes whose tiles do not fill the GPU:
+  // the top levels' merge products at C2 and the top levels' solve products
+  {
+    const int64_t t16 = (int64_t)((M + 15) / 16) * ((N + 15) / 16) * batch;
+    if (K >= 256 && t16 < 4LL * hps_num_sms()) {
+      const int tiles[2] = {1, N <= 16 ? 13 : 2};
+      for (int sp = 2; sp <= 8; sp *= 2)
+        if (K / sp >= 64)
+          for (int t : tiles) cands[nc++] = t | (sp << 8);
+    }
+  }
   *ncand = nc;
   // sample: enough 16 x 16 tiles for ~8 waves of 8 resident CTAs on every SM
   const int64_t t16 = (int64_t)((M + 15) / 16) * ((N + 15) / 16);

@@ -581,6 +581,25 @@ def test_zgemm_configs(cfg, M, N, K, batch, m3):
                 assert rel(C[b], ref) < 1e-13
 
 
+@pytest.mark.parametrize("m3", [1, 0])
+@pytest.mark.parametrize("cfg", [1 | 2 << 8, 2 | 4 << 8, 13 | 8 << 8, 5 | 2 << 8, 6 | 4 << 8])
+@pytest.mark.parametrize("M,N,K,batch", [(196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 671, 1), (33, 16, 1500, 3)])
+def test_zgemm_split_k(cfg, M, N, K, batch, m3):
+    """Split-K configurations (tile | slices << 8, zgemm.cu launch_cfg): partial tiles per K slice
+    (whole BK stages; empty slices when K is short), Cin only in slice 0, slices summed in order by
+    the reduction kernel -- vs the oracle's product with alpha, beta, in both product forms."""
+    rng = np.random.default_rng(M * 7 + N + K)
+    A = rng.standard_normal((batch, M, K)) + 1j * rng.standard_normal((batch, M, K))
+    B = rng.standard_normal((batch, K, N)) + 1j * rng.standard_normal((batch, K, N))
+    Cin = rng.standard_normal((batch, M, N)) + 1j * rng.standard_normal((batch, M, N))
+    with hps.debug_knobs(gemm_3m=m3):
+        for alpha, beta in [(1.0, 1.0), (-1.0, 0.5 - 2j), (0.5j, 0.0)]:
+            C, _ = hps.zgemm_batched(A, B, Cin if beta != 0 else None, alpha, beta, cfg=cfg)
+            for b in range(batch):
+                ref = alpha * oracle.matmul(A[b], B[b]) + beta * Cin[b]
+                assert rel(C[b], ref) < 1e-13
+
+
 @pytest.mark.parametrize("cfg", [2, 5])
 def test_zgemm_3m_error_bound(cfg):
     """3M vs 4M error against the oracle's product at long K and on operands whose imaginary parts
@@ -825,8 +844,8 @@ def test_planned_regimes_parity():
 def test_plan_solve_parity():
     """Solve-stage planner (hps_plan_solve): every action's shape is timed with each candidate tile
     configuration and the fastest recorded; the planned solve still matches the oracle at 1e-9 and
-    the unplanned solve to rounding (the configurations differ in tiling, not in arithmetic order
-    along K, except the GEMV kernel of N <= 4)."""
+    the unplanned solve to rounding (the configurations differ in tiling and, for the GEMV kernel of
+    N <= 4 and the split-K configurations, in the summation order along K)."""
     nx, ny, p, kappa, eta = 8, 4, 12, 15.0, 15.0 - 1j
     g, c, s, t = problem(nx, ny, p, kappa, eta, x1=1.0, y1=0.5, nrhs=16)
     hps.plan_clear()
