@@ -57,6 +57,7 @@ enum HpsKnob {
   KN_DGJ_NT,           // threads per CTA of the real leaf Gauss-Jordan: 512 (one leaf per SM) or 256 (two)
   KN_MERGE_SMALL,      // 1: levels with n3 <= 28 merged by one CTA per merge (merge_small.cu)
   KN_GEMM_3M,          // 1: tiled ZGEMM by three real products per complex MAC (3M form, DESIGN 3.14)
+  KN_NAT_LOOKAHEAD,    // 1: block-step W^{-1} with lookahead (next block's D^{-1} beside the update)
   KN_COUNT
 };
 int knob(HpsKnob k);
@@ -244,6 +245,7 @@ struct KStats {
 struct Prof;
 extern thread_local Prof* g_prof;
 void prof_begin(int cls, double flops, double bytes, cudaStream_t st);
+bool prof_timing_active();  // per-launch event timing on for this thread (side streams stay off)
 void prof_end(cudaStream_t st);
 
 struct ProfScope {

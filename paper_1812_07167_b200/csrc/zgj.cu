@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -3391,6 +3392,22 @@ __global__ void __launch_bounds__(512) nat_block_inv_kernel(const zt* __restrict
   if (tid == 0 && s_bad) atomicExch(flag, 1);
 }
 
+// Lookahead stream of the block steps (one per host thread and device: the virtual ranks of the
+// multi-GPU tests are host threads sharing a device, and must not share its work queue).
+static cudaStream_t lookahead_stream() {
+  thread_local std::vector<cudaStream_t> streams;
+  int dev = 0;
+  HPS_CUDA_CHECK(cudaGetDevice(&dev));
+  if ((int)streams.size() <= dev) streams.resize(dev + 1, nullptr);
+  if (!streams[dev]) HPS_CUDA_CHECK(cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking));
+  return streams[dev];
+}
+
+// With lookahead (knob nat_lookahead, default 1; off while per-launch event timing is on) the block
+// step q's trailing update is split: first the columns of block q + 1, then -- on a second stream,
+// concurrently with the rest of step q's update -- block q + 1's D^{-1} (a handful of CTAs, ~80 us of
+// serial pivot steps) and its T product, so that the serial part of step q + 1 hides behind step q's
+// wide GEMM.  T and D^{-1} are double-buffered; the arithmetic of every entry is unchanged.
 void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st) {
   char* wsp = static_cast<char*>(ws);
   auto carve = [&](size_t bytes) {
@@ -3400,8 +3417,12 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
   };
   double* d0 = static_cast<double*>(carve(sizeof(double) * (size_t)batch * n));
   zt* Z = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * NBB * n));
-  zt* T = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * n * NBB));
-  zt* Dt = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * NBB * NBB));
+  zt* Tb[2];
+  zt* Dtb[2];
+  for (int i = 0; i < 2; ++i) {
+    Tb[i] = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * n * NBB));
+    Dtb[i] = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * NBB * NBB));
+  }
   {
     ProfScope ps(K_GJ_AUX, 0.0, 24.0 * (double)batch * n, st);
     nat_diag_kernel<<<dim3((n + 255) / 256, batch), 256, 0, st>>>(A, lda, bs, n, d0);
@@ -3410,28 +3431,27 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
   }
   const double rel2 = knob(KN_NAT_PIVOT_REL) * 1e-4;
   const int nblk = (n + NBB - 1) / NBB;
-  for (int q = 0; q < nblk; ++q) {
-    const int k0 = (int)((int64_t)q * n / nblk), bb = (int)((int64_t)(q + 1) * n / nblk) - k0;  // equal blocks
+  auto k0of = [&](int q) { return (int)((int64_t)q * n / nblk); };
+  auto bbof = [&](int q) { return (int)((int64_t)(q + 1) * n / nblk) - k0of(q); };  // equal blocks
+  const bool la = knob(KN_NAT_LOOKAHEAD) != 0 && !prof_timing_active() && nblk > 1;
+  cudaStream_t st2 = la ? lookahead_stream() : st;
+  cudaEvent_t evA = nullptr, evB = nullptr;
+  if (la) {
+    HPS_CUDA_CHECK(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
+    HPS_CUDA_CHECK(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+  }
+  // D^{-1} of block q and T[rows outside K] = -A[rows outside K, K] D^{-1} into buffer q & 1
+  auto dinv_T = [&](int q, cudaStream_t s) {
+    const int k0 = k0of(q), bb = bbof(q);
+    zt* T = Tb[q & 1];
+    zt* Dt = Dtb[q & 1];
     {
-      ProfScope ps(K_GJ_PANEL, 8.0 * (double)bb * bb * bb * batch, 32.0 * (double)bb * bb * batch, st);
-      nat_block_inv_kernel<<<batch, 512, 0, st>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
+      ProfScope ps(K_GJ_PANEL, 8.0 * (double)bb * bb * bb * batch, 32.0 * (double)bb * bb * batch, s);
+      nat_block_inv_kernel<<<batch, 512, 0, s>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
     }
-    {  // Z = A[K, :]
-      ZCopy c;
-      c.M = bb;
-      c.N = n;
-      c.batch = batch;
-      c.A.ptr = A + (int64_t)k0 * lda;
-      c.A.rs = lda;
-      c.A.bs = bs;
-      c.C.ptr = Z;
-      c.C.rs = n;
-      c.C.bs = (int64_t)NBB * n;
-      zcopy(c, st);
-    }
-    {  // T[rows outside K] = -A[rows outside K, K] D^{-1}
+    if (n > bb) {
       ZGemm g;
       g.M = n - bb;
       g.N = bb;
@@ -3451,41 +3471,73 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
       g.C.rskip_at = k0;
       g.C.rskip_len = bb;
       g.alpha = make_double2(-1.0, 0.0);
-      if (n > bb) zgemm(g, st);
+      zgemm(g, s);
     }
-    if (n > bb) {  // A[:, j not in K] += T Z[:, j]  (in place)
-      ZGemm g;
-      g.M = n;
-      g.N = n - bb;
-      g.K = bb;
-      g.batch = batch;
-      g.A.ptr = T;
-      g.A.rs = NBB;
-      g.A.bs = (int64_t)n * NBB;
-      g.B.ptr = Z;
-      g.B.rs = n;
-      g.B.bs = (int64_t)NBB * n;
-      g.B.cskip_at = k0;
-      g.B.cskip_len = bb;
-      g.Cin.ptr = A;
-      g.Cin.rs = lda;
-      g.Cin.bs = bs;
-      g.Cin.cskip_at = k0;
-      g.Cin.cskip_len = bb;
-      g.C.ptr = A;
-      g.C.rs = lda;
-      g.C.bs = bs;
-      g.C.cskip_at = k0;
-      g.C.cskip_len = bb;
-      g.beta = make_double2(1.0, 0.0);
-      zgemm(g, st);
+  };
+  // A[:, cols] += T Z[:, cols] (in place) for the columns [c0, c0 + nc) minus the window
+  // [skip_at, skip_at + skip_len) (nc counts the columns actually updated)
+  auto update = [&](int q, int c0, int nc, int skip_at, int skip_len) {
+    if (nc <= 0) return;
+    const int bb = bbof(q);
+    ZGemm g;
+    g.M = n;
+    g.N = nc;
+    g.K = bb;
+    g.batch = batch;
+    g.A.ptr = Tb[q & 1];
+    g.A.rs = NBB;
+    g.A.bs = (int64_t)n * NBB;
+    g.B.ptr = Z + c0;
+    g.B.rs = n;
+    g.B.bs = (int64_t)NBB * n;
+    g.B.cskip_at = skip_at;
+    g.B.cskip_len = skip_len;
+    g.Cin.ptr = A + c0;
+    g.Cin.rs = lda;
+    g.Cin.bs = bs;
+    g.Cin.cskip_at = skip_at;
+    g.Cin.cskip_len = skip_len;
+    g.C.ptr = A + c0;
+    g.C.rs = lda;
+    g.C.bs = bs;
+    g.C.cskip_at = skip_at;
+    g.C.cskip_len = skip_len;
+    g.beta = make_double2(1.0, 0.0);
+    zgemm(g, st);
+  };
+  dinv_T(0, st);
+  for (int q = 0; q < nblk; ++q) {
+    const int k0 = k0of(q), bb = bbof(q);
+    {  // Z = A[K, :]
+      ZCopy c;
+      c.M = bb;
+      c.N = n;
+      c.batch = batch;
+      c.A.ptr = A + (int64_t)k0 * lda;
+      c.A.rs = lda;
+      c.A.bs = bs;
+      c.C.ptr = Z;
+      c.C.rs = n;
+      c.C.bs = (int64_t)NBB * n;
+      zcopy(c, st);
+    }
+    if (q + 1 < nblk && la) {
+      const int k1 = k0of(q + 1), b1 = bbof(q + 1);
+      update(q, k1, b1, 0x7fffffff, 0);  // block q + 1's columns first
+      HPS_CUDA_CHECK(cudaEventRecord(evA, st));
+      HPS_CUDA_CHECK(cudaStreamWaitEvent(st2, evA, 0));
+      dinv_T(q + 1, st2);
+      HPS_CUDA_CHECK(cudaEventRecord(evB, st2));
+      update(q, 0, n - bb - b1, k0, bb + b1);  // the rest, beside block q + 1's serial part
+    } else {
+      update(q, 0, n - bb, k0, bb);
     }
     {  // A[rows outside K, K] = T, A[K, K] = D^{-1}
       ZCopy c[2];
       c[0].M = n - bb;
       c[0].N = bb;
       c[0].batch = batch;
-      c[0].A.ptr = T;
+      c[0].A.ptr = Tb[q & 1];
       c[0].A.rs = NBB;
       c[0].A.bs = (int64_t)n * NBB;
       c[0].A.rskip_at = k0;
@@ -3498,7 +3550,7 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
       c[1].M = bb;
       c[1].N = bb;
       c[1].batch = batch;
-      c[1].A.ptr = Dt;
+      c[1].A.ptr = Dtb[q & 1];
       c[1].A.rs = NBB;
       c[1].A.bs = (int64_t)NBB * NBB;
       c[1].C.ptr = A + (int64_t)k0 * lda + k0;
@@ -3506,11 +3558,19 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
       c[1].C.bs = bs;
       zcopy_multi(c, 2, st);  // (c[0] is empty when the block is the whole matrix)
     }
+    if (q + 1 < nblk) {
+      if (la) HPS_CUDA_CHECK(cudaStreamWaitEvent(st, evB, 0));
+      else dinv_T(q + 1, st);
+    }
+  }
+  if (la) {
+    HPS_CUDA_CHECK(cudaEventDestroy(evA));
+    HPS_CUDA_CHECK(cudaEventDestroy(evB));
   }
 }
 
 size_t zgj_natural_blocked_workspace_bytes(int n, int batch) {
-  return 4 * 256 + sizeof(double) * (size_t)batch * n + sizeof(zt) * (size_t)batch * (2 * (size_t)NBB * n + NBB * NBB);
+  return 6 * 256 + sizeof(double) * (size_t)batch * n + sizeof(zt) * (size_t)batch * (3 * (size_t)NBB * n + 2 * NBB * NBB);
 }
 
 size_t zgj_natural_workspace_bytes(int n, int batch) {

@@ -116,6 +116,26 @@ def test_natural_order_merge_inverses_all_levels():
         assert worst < TOL, (knobs, worst)
 
 
+def test_natural_blocked_lookahead():
+    """Block-step natural-order W^{-1} (nat_bb_min = 100: the top levels' n3 = 160, three 64-wide
+    blocks) with and without lookahead (knob nat_lookahead: block q + 1's D^{-1} and T on
+    a second stream beside block q's trailing update): the same arithmetic per entry,
+    so root R and u are bitwise equal; both vs the oracle."""
+    nx, ny, p, kappa, eta = 16, 16, 12, 20.0, 20.0 + 2j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=2)
+    res = {}
+    for la in (0, 1):
+        with hps.debug_knobs(nat_min=100, nat_bb_min=100, nat_lookahead=la):
+            S = hps.Solver(g, p, kappa, eta, c)
+            res[la] = (S.R(1), S.solve(s, t), S.launches(0))
+            S.close()
+    # the lookahead splits each block step's update in two (one more launch per step): it ran
+    assert res[1][2] > res[0][2], (res[0][2], res[1][2])
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+    O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
+    assert rel(res[1][0], O.R(1)) < TOL and rel(res[1][1], O.solve(s, t)) < TOL
+
+
 def test_leaf_schur_natural_and_pivoted_paths():
     """The complex interior Schur inverse (leaf_mode 0 with complex c) runs in natural order
     (DESIGN.md 3.12); the seq_pivot knob forces the pivoted path; leaf_panel switches the natural-order
