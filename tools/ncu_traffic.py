@@ -12,7 +12,7 @@ import json
 import sys
 
 CLASSES = [  # (substring of the kernel name, class) -- first match wins
-    ("zgemv", "zgemv"), ("zgemm_kernel", "zgemm_dmma"), ("zgj_seq_kernel", "leaf_gj"), ("zgj_ws_kernel", "leaf_gj"),
+    ("zgemv", "zgemv"), ("zgemm_kernel", "zgemm_dmma"), ("zsplit_reduce", "zgemm_dmma"), ("zgj_seq_kernel", "leaf_gj"), ("zgj_ws_kernel", "leaf_gj"),
     ("dgj_leaf_kernel", "leaf_gj"), ("leaf_real_ops_kernel", "leaf_gj"), ("zgj_panel", "zgj_panel"),
     ("zgj_small", "zgj_small"), ("zgj_fused", "zgj_fused"), ("nat_block_inv", "zgj_panel"), ("nat_diag", "zgj_aux"),
     ("zgj_", "zgj_aux"),
