@@ -580,7 +580,7 @@ def test_virtual_comm_selftest():
     assert all(dist.run_virtual(8, fn))
 
 
-@pytest.mark.parametrize("m3", [1, 0])
+@pytest.mark.parametrize("m3", [1, 0, 2])
 @pytest.mark.parametrize("cfg", list(range(14)))
 @pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1),
                                          (70, 1, 300, 2), (33, 3, 45, 3)])
@@ -601,7 +601,7 @@ def test_zgemm_configs(cfg, M, N, K, batch, m3):
                 assert rel(C[b], ref) < 1e-13
 
 
-@pytest.mark.parametrize("m3", [1, 0])
+@pytest.mark.parametrize("m3", [1, 0, 2])
 @pytest.mark.parametrize("cfg", [1 | 2 << 8, 2 | 4 << 8, 13 | 8 << 8, 5 | 2 << 8, 6 | 4 << 8])
 @pytest.mark.parametrize("M,N,K,batch", [(196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 671, 1), (33, 16, 1500, 3)])
 def test_zgemm_split_k(cfg, M, N, K, batch, m3):
@@ -633,12 +633,12 @@ def test_zgemm_3m_error_bound(cfg):
     for a, b in [(A, B), (As, B), (As, B.real + 1e-6j * B.imag)]:
         ref = oracle.matmul(a[0], b[0])
         errs = []
-        for m3 in (0, 1):
+        for m3 in (0, 1, 2):
             with hps.debug_knobs(gemm_3m=m3):
                 C, _ = hps.zgemm_batched(a, b, None, 1.0, 0.0, cfg=cfg)
             errs.append(np.linalg.norm(C[0] - ref) / (np.linalg.norm(a[0]) * np.linalg.norm(b[0])))
-        assert errs[0] < 1e-15 and errs[1] < 1e-15
-        assert errs[1] < 8 * errs[0] + 1e-17, errs
+        assert max(errs) < 1e-15
+        assert errs[1] < 8 * errs[0] + 1e-17 and errs[2] < 8 * errs[0] + 1e-17, errs
 
 
 # ---------------------------------------------------------------------------
@@ -663,16 +663,16 @@ def test_config2_full_vs_oracle():
     assert rel(u, O.solve(s, t)) < TOL
 
 
-@pytest.mark.parametrize("m3", [0, 1])
+@pytest.mark.parametrize("m3", [1, 2])
 def test_config2_product_forms(m3):
-    """C2 whole problem in each complex-product form (knob gemm_3m): root R and u vs
-    the oracle at the suite's tolerance, and the two forms within 1e-12 of each other."""
+    """C2 whole problem in each 3M product form (knob gemm_3m): root R and u vs
+    the oracle at the suite's tolerance, and within 1e-12 of the 4M form."""
     cfg, g, c, s, t = _bench_inputs(2)
     with hps.debug_knobs(gemm_3m=m3):
         S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
         u = S.solve(s, t)
         R = S.R(1)
-    with hps.debug_knobs(gemm_3m=1 - m3):
+    with hps.debug_knobs(gemm_3m=0):
         S2 = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
         u2 = S2.solve(s, t)
     O = oracle.Oracle(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p, cfg.kappa, cfg.eta, c)
