@@ -3154,7 +3154,8 @@ __global__ void nat_diag_kernel(const zt* A, int64_t lda, int64_t bs, int n, dou
 // the blocked explicit-swap update with identity maps (any n).  Workspace as
 // zgj_workspace_bytes(n, batch) for the blocked regime; *flag (device) is set to 1 when a pivot
 // failed the check — out is then not the inverse and A is destroyed (the caller keeps a copy).
-void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st);
+void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st,
+                                int nbw);
 size_t zgj_natural_blocked_workspace_bytes(int n, int batch);
 
 // 64-wide block steps where the 16-column panels' K = 16 updates are memory-bound: n >= nat_bb_min,
@@ -3163,11 +3164,17 @@ size_t zgj_natural_blocked_workspace_bytes(int n, int batch);
 bool use_block_steps(int n, int batch) {
   return n >= knob(KN_NAT_BB_MIN) || (n >= 224 && sizeof(zt) * (double)batch * n * n >= 32.0 * (1 << 20));
 }
+// 32-wide block steps with the one-warp D^{-1} (knob nat_b32: smallest n, 0 = off) for the natural-order
+// inverses that would otherwise take the 16-column panels (C2's top levels)
+bool use_block32(int n, int batch) {
+  const int m = knob(KN_NAT_B32);
+  return !use_block_steps(n, batch) && m > 0 && n >= m;
+}
 
 void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
                         void* ws, int* flag, cudaStream_t st) {
-  if (use_block_steps(n, batch)) {  // in place in A, then copied out
-    zgj_invert_natural_blocked(A, lda, bs, n, batch, ws, flag, st);
+  if (use_block_steps(n, batch) || use_block32(n, batch)) {  // in place in A, then copied out
+    zgj_invert_natural_blocked(A, lda, bs, n, batch, ws, flag, st, use_block32(n, batch) ? 32 : 64);
     ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)batch * n * n, st);
     if (lda == n && bs == (int64_t)n * n && ldo == n && obs == (int64_t)n * n) {
       HPS_CUDA_CHECK(cudaMemcpyAsync(out, A, sizeof(zt) * (size_t)batch * n * n, cudaMemcpyDeviceToDevice, st));
@@ -3392,6 +3399,64 @@ __global__ void __launch_bounds__(512) nat_block_inv_kernel(const zt* __restrict
   if (tid == 0 && s_bad) atomicExch(flag, 1);
 }
 
+// D^{-1} of a bb x bb block (bb <= 32) in natural order by ONE WARP per matrix, register-resident:
+// lane i holds row i (32 complex), the pivot row is broadcast by shuffles, the pivot column entry of
+// a row is the lane's own register (the 32 steps are unrolled, so every index is static).  No
+// barrier in the chain: ~0.2 us per step against ~1.2 us for the 512-thread 64 x 64 kernel, for the
+// latency-bound top-level inverses of the small configurations (32-wide block steps, knob nat_b32).
+// Same textbook step D[i][j] -= D[i][k] (D[k][j] / D[k][k]) and the same relative pivot check.
+__global__ void __launch_bounds__(32) nat_block_inv32_kernel(const zt* __restrict__ A, int64_t lda, int64_t bs, int n,
+                                                             int k0, int bb, const double* __restrict__ d0,
+                                                             double rel2, zt* __restrict__ Dt,
+                                                             zt* __restrict__ T, int* __restrict__ flag) {
+  const int lane = threadIdx.x, b = blockIdx.x;
+  const zt* Ab = A + (int64_t)b * bs + (int64_t)k0 * lda + k0;
+  zt d[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    d[j] = (lane < bb && j < bb) ? Ab[(int64_t)lane * lda + j] : make_double2(lane == j ? 1.0 : 0.0, 0.0);
+  bool bad = false;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (k < bb) {  // uniform
+      const zt f = d[k];
+      const zt pv = make_double2(__shfl_sync(0xffffffffu, f.x, k), __shfl_sync(0xffffffffu, f.y, k));
+      const zt inv = zinv_fast(pv);
+      const double m = fma(pv.x, pv.x, pv.y * pv.y);
+      if (!(m > 0.0 && m >= rel2 * d0[(int64_t)b * n + k0 + k])) bad = true;
+      const zt g = zmul(f, inv);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j == k) continue;
+        const zt pj = make_double2(__shfl_sync(0xffffffffu, d[j].x, k), __shfl_sync(0xffffffffu, d[j].y, k));
+        const zt pr = zmul(pj, inv);
+        if (lane == k) {
+          d[j] = pr;
+        } else {
+          zt v = d[j];
+          v.x = fma(-f.x, pr.x, v.x);
+          v.x = fma(f.y, pr.y, v.x);
+          v.y = fma(-f.x, pr.y, v.y);
+          v.y = fma(-f.y, pr.x, v.y);
+          d[j] = v;
+        }
+      }
+      d[k] = lane == k ? inv : make_double2(-g.x, -g.y);
+    }
+  }
+  zt* Db = Dt + (int64_t)b * NBB * NBB;
+  zt* Tb = T + (int64_t)b * n * NBB + (int64_t)k0 * NBB;  // T: [n][NBB] per matrix
+  if (lane < bb) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < bb) {
+        Db[lane * NBB + j] = d[j];
+        Tb[lane * NBB + j] = make_double2(d[j].x - (lane == j ? 1.0 : 0.0), d[j].y);
+      }
+  }
+  if (lane == 0 && bad) atomicExch(flag, 1);
+}
+
 // Lookahead stream of the block steps (one per host thread and device: the virtual ranks of the
 // multi-GPU tests are host threads sharing a device, and must not share its work queue).
 static cudaStream_t lookahead_stream() {
@@ -3408,7 +3473,8 @@ static cudaStream_t lookahead_stream() {
 // concurrently with the rest of step q's update -- block q + 1's D^{-1} (a handful of CTAs, ~80 us of
 // serial pivot steps) and its T product, so that the serial part of step q + 1 hides behind step q's
 // wide GEMM.  T and D^{-1} are double-buffered; the arithmetic of every entry is unchanged.
-void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st) {
+void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st,
+                                int nbw) {
   char* wsp = static_cast<char*>(ws);
   auto carve = [&](size_t bytes) {
     void* p = wsp;
@@ -3430,7 +3496,7 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
     count_launch();
   }
   const double rel2 = knob(KN_NAT_PIVOT_REL) * 1e-4;
-  const int nblk = (n + NBB - 1) / NBB;
+  const int nblk = (n + nbw - 1) / nbw;  // block width nbw: 64 (512-thread D^{-1}) or 32 (one warp)
   auto k0of = [&](int q) { return (int)((int64_t)q * n / nblk); };
   auto bbof = [&](int q) { return (int)((int64_t)(q + 1) * n / nblk) - k0of(q); };  // equal blocks
   const bool la = knob(KN_NAT_LOOKAHEAD) != 0 && !prof_timing_active() && nblk > 1;
@@ -3447,7 +3513,10 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
     zt* Dt = Dtb[q & 1];
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * (double)bb * bb * bb * batch, 32.0 * (double)bb * bb * batch, s);
-      nat_block_inv_kernel<<<batch, 512, 0, s>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
+      if (nbw <= 32)
+        nat_block_inv32_kernel<<<batch, 32, 0, s>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
+      else
+        nat_block_inv_kernel<<<batch, 512, 0, s>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
     }
@@ -3574,7 +3643,7 @@ size_t zgj_natural_blocked_workspace_bytes(int n, int batch) {
 }
 
 size_t zgj_natural_workspace_bytes(int n, int batch) {
-  if (use_block_steps(n, batch)) return zgj_natural_blocked_workspace_bytes(n, batch);
+  if (use_block_steps(n, batch) || use_block32(n, batch)) return zgj_natural_blocked_workspace_bytes(n, batch);
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256 + 512 + sizeof(double) * (size_t)batch * n;
 }

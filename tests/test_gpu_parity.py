@@ -100,9 +100,11 @@ def test_natural_order_merge_inverses_all_levels():
     every box's R and u vs the oracle, complex eta included; second pass with every natural-order
     attempt forced to fail its pivot check (the pivoted fallback), third with the relative pivot
     threshold at 1.0 (any pivot smaller than its original diagonal falls back); the last two with
-    the 64-wide block steps (nat_bb_min = 20: every W with n3 >= 20, one to two blocks)."""
+    the 64-wide block steps (nat_bb_min = 20: every W with n3 >= 20, one to two blocks); the last two
+    with the 32-wide block steps and their one-warp D^{-1} (nat_b32 = 14)."""
     for knobs in ({"nat_min": 14}, {"nat_min": 14, "nat_force_fail": 1}, {"nat_min": 14, "nat_pivot_rel": 10000},
-                  {"nat_min": 14, "nat_bb_min": 20}, {"nat_min": 14, "nat_bb_min": 20, "nat_pivot_rel": 10000}):
+                  {"nat_min": 14, "nat_bb_min": 20}, {"nat_min": 14, "nat_bb_min": 20, "nat_pivot_rel": 10000},
+                  {"nat_min": 14, "nat_b32": 14}, {"nat_min": 14, "nat_b32": 14, "nat_pivot_rel": 10000}):
         worst = 0.0
         with hps.debug_knobs(**knobs):
             for nx, ny, p, kappa, eta in [(4, 4, 8, 9.0, 9.0 - 2j), (8, 4, 6, 9.0, 9.0), (4, 8, 10, 20.0, 20.0)]:
@@ -134,6 +136,25 @@ def test_natural_blocked_lookahead():
     assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
     O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
     assert rel(res[1][0], O.R(1)) < TOL and rel(res[1][1], O.solve(s, t)) < TOL
+
+
+def test_natural_block32_one_warp():
+    """32-wide block steps with the one-warp D^{-1} (knob nat_b32) on the root W
+    (n3 = 160: five blocks), with and without lookahead (bitwise equal), vs the oracle and vs the
+    16-column panels."""
+    nx, ny, p, kappa, eta = 16, 16, 12, 20.0, 20.0 + 2j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=2)
+    res = {}
+    for key, kn in (("b32", dict(nat_b32=100)), ("b32_nola", dict(nat_b32=100, nat_lookahead=0)),
+                    ("panels", dict(nat_b32=0))):
+        with hps.debug_knobs(nat_min=100, **kn):
+            S = hps.Solver(g, p, kappa, eta, c)
+            res[key] = (S.R(1), S.solve(s, t))
+            S.close()
+    assert np.array_equal(res["b32"][0], res["b32_nola"][0]) and np.array_equal(res["b32"][1], res["b32_nola"][1])
+    O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
+    assert rel(res["b32"][0], O.R(1)) < TOL and rel(res["b32"][1], O.solve(s, t)) < TOL
+    assert rel(res["b32"][0], res["panels"][0]) < 1e-12 and rel(res["b32"][1], res["panels"][1]) < 1e-12
 
 
 def test_leaf_schur_natural_and_pivoted_paths():
