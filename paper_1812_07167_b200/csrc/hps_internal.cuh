@@ -60,6 +60,7 @@ enum HpsKnob {
                        // 2 the 3M form with the operand sums staged once per stage (DESIGN 3.14)
   KN_NAT_LOOKAHEAD,    // 1: block-step W^{-1} with lookahead (next block's D^{-1} beside the update)
   KN_NAT_B32,          // natural-order W^{-1} below nat_bb_min in 32-wide block steps for n >= this (0: panels)
+  KN_NAT_PERSIST,      // natural-order W^{-1} below nat_bb_min in one cooperative launch for batch <= this (0: off)
   KN_COUNT
 };
 int knob(HpsKnob k);

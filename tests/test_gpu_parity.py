@@ -101,10 +101,12 @@ def test_natural_order_merge_inverses_all_levels():
     attempt forced to fail its pivot check (the pivoted fallback), third with the relative pivot
     threshold at 1.0 (any pivot smaller than its original diagonal falls back); the last two with
     the 64-wide block steps (nat_bb_min = 20: every W with n3 >= 20, one to two blocks); the last two
-    with the 32-wide block steps and their one-warp D^{-1} (nat_b32 = 14)."""
+    with the 32-wide block steps and their one-warp D^{-1} (nat_b32 = 14), the last two in one
+    cooperative persistent launch (nat_persist = 8)."""
     for knobs in ({"nat_min": 14}, {"nat_min": 14, "nat_force_fail": 1}, {"nat_min": 14, "nat_pivot_rel": 10000},
                   {"nat_min": 14, "nat_bb_min": 20}, {"nat_min": 14, "nat_bb_min": 20, "nat_pivot_rel": 10000},
-                  {"nat_min": 14, "nat_b32": 14}, {"nat_min": 14, "nat_b32": 14, "nat_pivot_rel": 10000}):
+                  {"nat_min": 14, "nat_b32": 14}, {"nat_min": 14, "nat_b32": 14, "nat_pivot_rel": 10000},
+                  {"nat_min": 14, "nat_persist": 8}, {"nat_min": 14, "nat_persist": 8, "nat_pivot_rel": 10000}):
         worst = 0.0
         with hps.debug_knobs(**knobs):
             for nx, ny, p, kappa, eta in [(4, 4, 8, 9.0, 9.0 - 2j), (8, 4, 6, 9.0, 9.0), (4, 8, 10, 20.0, 20.0)]:
@@ -146,7 +148,7 @@ def test_natural_block32_one_warp():
     g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=2)
     res = {}
     for key, kn in (("b32", dict(nat_b32=100)), ("b32_nola", dict(nat_b32=100, nat_lookahead=0)),
-                    ("panels", dict(nat_b32=0))):
+                    ("panels", dict(nat_b32=0)), ("persist", dict(nat_persist=8))):
         with hps.debug_knobs(nat_min=100, **kn):
             S = hps.Solver(g, p, kappa, eta, c)
             res[key] = (S.R(1), S.solve(s, t))
@@ -155,6 +157,9 @@ def test_natural_block32_one_warp():
     O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
     assert rel(res["b32"][0], O.R(1)) < TOL and rel(res["b32"][1], O.solve(s, t)) < TOL
     assert rel(res["b32"][0], res["panels"][0]) < 1e-12 and rel(res["b32"][1], res["panels"][1]) < 1e-12
+    # the persistent launch: the same block-step algebra with SIMT products (another k-order)
+    assert rel(res["persist"][0], O.R(1)) < TOL and rel(res["persist"][1], O.solve(s, t)) < TOL
+    assert rel(res["persist"][0], res["b32"][0]) < 1e-12
 
 
 def test_leaf_schur_natural_and_pivoted_paths():
