@@ -56,11 +56,8 @@ enum HpsKnob {
   KN_RHS_CHUNK,        // right-hand sides per solve chunk (0: as many as fit in 40 % of free memory)
   KN_DGJ_NT,           // threads per CTA of the real leaf Gauss-Jordan: 512 (one leaf per SM) or 256 (two)
   KN_MERGE_SMALL,      // 1: levels with n3 <= 28 merged by one CTA per merge (merge_small.cu)
-  KN_GEMM_3M,          // tiled ZGEMM: 0 four real products per complex MAC, 1 the 3M form (sums per fragment),
-                       // 2 the 3M form with the operand sums staged once per stage (DESIGN 3.14)
+  KN_GEMM_3M,          // 1: tiled ZGEMM by three real products per complex MAC (3M form, DESIGN 3.14)
   KN_NAT_LOOKAHEAD,    // 1: block-step W^{-1} with lookahead (next block's D^{-1} beside the update)
-  KN_NAT_B32,          // natural-order W^{-1} below nat_bb_min in 32-wide block steps for n >= this (0: panels)
-  KN_NAT_PERSIST,      // natural-order W^{-1} below nat_bb_min in one cooperative launch for batch <= this (0: off)
   KN_COUNT
 };
 int knob(HpsKnob k);

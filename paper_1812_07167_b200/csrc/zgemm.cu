@@ -51,10 +51,6 @@ struct Cfg {
   static constexpr int BS = BN + 2;  // B tile row stride (complex)
   static constexpr int ITA = BM * BK / NT, ITB = BK * BN / NT;
   static constexpr size_t SMEM = sizeof(zt) * 2 * (BM * AS + BK * BS);
-  // M3 == 2: the operand sums A_r + A_i, B_r + B_i of the current stage (one buffer; strides chosen so
-  // that the fragment loads (LDS.64) are conflict-free within each half-warp)
-  static constexpr int SA = BK + 4, SB = BN + 4;
-  static constexpr size_t SMEM_S = sizeof(double) * (BM * SA + BK * SB);
   static_assert(NT % BK == 0 && ITA >= 1 && ITB >= 1 && (BM * BK) % NT == 0 && (BK * BN) % NT == 0, "cfg");
   static_assert(NT % BN == 0 || BN % NT == 0, "cfg");
 };
@@ -62,18 +58,13 @@ struct Cfg {
 // BCOL: B is column-major (rs == 1, no maps: the solve reads s in the ABI layout [RHS][leaf][n_i],
 // columns 0.2-3 GB apart): the B tile is loaded k-fastest, so that a warp's cp.async requests cover
 // runs of BK consecutive elements of a column instead of one 16-byte piece per column.
-// M3: 0 = four real products per complex MAC; 1 = the 3M form with the operand sums formed per
-// fragment in the inner loop; 2 = the 3M form with the sums formed once per stage by the thread that
-// staged each element (after its own cp.async completed) into a shared-memory plane.
-template <int BM, int BN, int WM, int WN, bool BCOL = false, int M3 = 0>
+template <int BM, int BN, int WM, int WN, bool BCOL = false, bool M3 = false>
 __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32) ? 3 : 0) zgemm_kernel(const ZGemm g) {
   using C = Cfg<BM, BN, WM, WN>;
   constexpr int NT = C::NT, TM = C::TM, TN = C::TN, AS = C::AS, BS = C::BS, ITA = C::ITA, ITB = C::ITB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   zt* As = reinterpret_cast<zt*>(smem_raw);  // [2][BM][AS]
   zt* Bs = As + 2 * BM * AS;                 // [2][BK][BS]
-  double* SAs = reinterpret_cast<double*>(Bs + 2 * BK * C::BS);  // M3 == 2: [BM][SA]
-  double* SBs = SAs + BM * C::SA;                                 // M3 == 2: [BK][SB]
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / C::NWN, wn = warp % C::NWN;
@@ -219,7 +210,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
             acci[i][j][h] = v.y;
           }
     }
-    if constexpr (M3 != 0) {
+    if constexpr (M3) {
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -238,31 +229,6 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
       } else {
         cp_async_wait0();
       }
-      if constexpr (M3 == 2) {  // sums of the elements this thread staged (its own cp.async writes)
-        const zt* Asw = As + (kt & 1) * BM * AS;
-        const zt* Bsw = Bs + (kt & 1) * BK * BS;
-#pragma unroll
-        for (int it = 0; it < ITA; ++it) {
-          const int r = a_r0 + it * A_RSTEP;
-          const zt v = Asw[r * AS + a_c];
-          SAs[r * C::SA + a_c] = v.x + v.y;
-        }
-        if constexpr (BCOL) {
-#pragma unroll
-          for (int it = 0; it < ITB; ++it) {
-            const int kq = tid % BK, jj = tid / BK + it * BC_JSTEP;
-            const zt v = Bsw[kq * BS + jj];
-            SBs[kq * C::SB + jj] = v.x + v.y;
-          }
-        } else {
-#pragma unroll
-          for (int it = 0; it < ITB; ++it) {
-            const int r = b_r0 + it * B_RSTEP;
-            const zt v = Bsw[r * BS + b_c];
-            SBs[r * C::SB + b_c] = v.x + v.y;
-          }
-        }
-      }
       __syncthreads();
       const zt* Ast = As + (kt & 1) * BM * AS + (wm * C::TM * 8) * AS;
       const zt* Bst = Bs + (kt & 1) * BK * BS + wn * C::TN * 8;
@@ -273,20 +239,12 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
         for (int i = 0; i < TM; ++i) af[i] = Ast[(i * 8 + (lane >> 2)) * AS + kk * 4 + (lane & 3)];
 #pragma unroll
         for (int j = 0; j < TN; ++j) bf[j] = Bst[(kk * 4 + (lane & 3)) * BS + j * 8 + (lane >> 2)];
-        if constexpr (M3 != 0) {
+        if constexpr (M3) {
           double as[TM], bs[TN];
-          if constexpr (M3 == 2) {
 #pragma unroll
-            for (int i = 0; i < TM; ++i)
-              as[i] = SAs[(wm * C::TM * 8 + i * 8 + (lane >> 2)) * C::SA + kk * 4 + (lane & 3)];
+          for (int i = 0; i < TM; ++i) as[i] = af[i].x + af[i].y;
 #pragma unroll
-            for (int j = 0; j < TN; ++j) bs[j] = SBs[(kk * 4 + (lane & 3)) * C::SB + wn * C::TN * 8 + j * 8 + (lane >> 2)];
-          } else {
-#pragma unroll
-            for (int i = 0; i < TM; ++i) as[i] = af[i].x + af[i].y;
-#pragma unroll
-            for (int j = 0; j < TN; ++j) bs[j] = bf[j].x + bf[j].y;
-          }
+          for (int j = 0; j < TN; ++j) bs[j] = bf[j].x + bf[j].y;
 #pragma unroll
           for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -323,7 +281,7 @@ __global__ void __launch_bounds__(Cfg<BM, BN, WM, WN>::NT, (BM == 64 && BN == 32
       __syncthreads();
     }
 
-    if constexpr (M3 != 0) {  // (T1, T3, T2) -> (Cr, Ci)
+    if constexpr (M3) {  // (T1, T3, T2) -> (Cr, Ci)
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -412,23 +370,18 @@ template <int BM, int BN, int WM, int WN, bool BCOL = false>
 void launch(const ZGemm& g, cudaStream_t st) {
   using C = Cfg<BM, BN, WM, WN>;
   static bool attr_set = false;
-  const int m3 = knob(KN_GEMM_3M);
-  auto kern = m3 == 2   ? zgemm_kernel<BM, BN, WM, WN, BCOL, 2>
-              : m3 != 0 ? zgemm_kernel<BM, BN, WM, WN, BCOL, 1>
-                        : zgemm_kernel<BM, BN, WM, WN, BCOL, 0>;
-  const size_t smem = C::SMEM + (m3 == 2 ? C::SMEM_S : 0);
+  const bool m3 = knob(KN_GEMM_3M) != 0;
+  auto kern = m3 ? zgemm_kernel<BM, BN, WM, WN, BCOL, true> : zgemm_kernel<BM, BN, WM, WN, BCOL, false>;
   if (!attr_set) {
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<BM, BN, WM, WN, BCOL, 2>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(C::SMEM + C::SMEM_S)));
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<BM, BN, WM, WN, BCOL, 1>,
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<BM, BN, WM, WN, BCOL, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<BM, BN, WM, WN, BCOL, 0>,
+    HPS_CUDA_CHECK(cudaFuncSetAttribute(zgemm_kernel<BM, BN, WM, WN, BCOL, false>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
     attr_set = true;
   }
   const int tiles = ((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN);
   dim3 grid(tiles, g.batch < 65535 ? g.batch : 65535, g.ws ? g.ksplit : 1);
-  kern<<<grid, C::NT, smem, st>>>(g);
+  kern<<<grid, C::NT, C::SMEM, st>>>(g);
   HPS_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

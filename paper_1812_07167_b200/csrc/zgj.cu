@@ -3154,8 +3154,7 @@ __global__ void nat_diag_kernel(const zt* A, int64_t lda, int64_t bs, int n, dou
 // the blocked explicit-swap update with identity maps (any n).  Workspace as
 // zgj_workspace_bytes(n, batch) for the blocked regime; *flag (device) is set to 1 when a pivot
 // failed the check — out is then not the inverse and A is destroyed (the caller keeps a copy).
-void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st,
-                                int nbw);
+void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st);
 size_t zgj_natural_blocked_workspace_bytes(int n, int batch);
 
 // 64-wide block steps where the 16-column panels' K = 16 updates are memory-bound: n >= nat_bb_min,
@@ -3164,29 +3163,11 @@ size_t zgj_natural_blocked_workspace_bytes(int n, int batch);
 bool use_block_steps(int n, int batch) {
   return n >= knob(KN_NAT_BB_MIN) || (n >= 224 && sizeof(zt) * (double)batch * n * n >= 32.0 * (1 << 20));
 }
-// 32-wide block steps with the one-warp D^{-1} (knob nat_b32: smallest n, 0 = off) for the natural-order
-// inverses that would otherwise take the 16-column panels (C2's top levels)
-bool use_block32(int n, int batch) {
-  const int m = knob(KN_NAT_B32);
-  return !use_block_steps(n, batch) && m > 0 && n >= m;
-}
-// one cooperative persistent launch (knob nat_persist: largest batch, 0 = off) for the same inverses
-bool use_persist(int n, int batch) {
-  const int m = knob(KN_NAT_PERSIST);
-  return !use_block_steps(n, batch) && m > 0 && batch <= std::min(m, 8);
-}
-size_t persist_workspace_bytes(int n, int batch) {
-  return 4 * 256 + sizeof(double) * (size_t)batch * n + sizeof(zt) * (size_t)batch * (2 * 32 * (size_t)n + 32 * 32);
-}
-void zgj_invert_natural_persist(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st);
 
 void zgj_invert_natural(zt* A, int64_t lda, int64_t bs, zt* out, int64_t ldo, int64_t obs, int n, int batch,
                         void* ws, int* flag, cudaStream_t st) {
-  if (use_block_steps(n, batch) || use_block32(n, batch) || use_persist(n, batch)) {  // in place in A, then copied out
-    if (use_persist(n, batch) && !use_block32(n, batch))
-      zgj_invert_natural_persist(A, lda, bs, n, batch, ws, flag, st);
-    else
-      zgj_invert_natural_blocked(A, lda, bs, n, batch, ws, flag, st, use_block32(n, batch) ? 32 : 64);
+  if (use_block_steps(n, batch)) {  // in place in A, then copied out
+    zgj_invert_natural_blocked(A, lda, bs, n, batch, ws, flag, st);
     ProfScope ps(K_GJ_AUX, 0.0, 32.0 * (double)batch * n * n, st);
     if (lda == n && bs == (int64_t)n * n && ldo == n && obs == (int64_t)n * n) {
       HPS_CUDA_CHECK(cudaMemcpyAsync(out, A, sizeof(zt) * (size_t)batch * n * n, cudaMemcpyDeviceToDevice, st));
@@ -3411,201 +3392,6 @@ __global__ void __launch_bounds__(512) nat_block_inv_kernel(const zt* __restrict
   if (tid == 0 && s_bad) atomicExch(flag, 1);
 }
 
-// D^{-1} of a bb x bb block (bb <= 32) in natural order by ONE WARP per matrix, register-resident:
-// lane i holds row i (32 complex), the pivot row is broadcast by shuffles, the pivot column entry of
-// a row is the lane's own register (the 32 steps are unrolled, so every index is static).  No
-// barrier in the chain: ~0.2 us per step against ~1.2 us for the 512-thread 64 x 64 kernel, for the
-// latency-bound top-level inverses of the small configurations (32-wide block steps, knob nat_b32).
-// Same textbook step D[i][j] -= D[i][k] (D[k][j] / D[k][k]) and the same relative pivot check.
-__global__ void __launch_bounds__(32) nat_block_inv32_kernel(const zt* __restrict__ A, int64_t lda, int64_t bs, int n,
-                                                             int k0, int bb, const double* __restrict__ d0,
-                                                             double rel2, zt* __restrict__ Dt,
-                                                             zt* __restrict__ T, int* __restrict__ flag) {
-  const int lane = threadIdx.x, b = blockIdx.x;
-  const zt* Ab = A + (int64_t)b * bs + (int64_t)k0 * lda + k0;
-  zt d[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j)
-    d[j] = (lane < bb && j < bb) ? Ab[(int64_t)lane * lda + j] : make_double2(lane == j ? 1.0 : 0.0, 0.0);
-  bool bad = false;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    if (k < bb) {  // uniform
-      const zt f = d[k];
-      const zt pv = make_double2(__shfl_sync(0xffffffffu, f.x, k), __shfl_sync(0xffffffffu, f.y, k));
-      const zt inv = zinv_fast(pv);
-      const double m = fma(pv.x, pv.x, pv.y * pv.y);
-      if (!(m > 0.0 && m >= rel2 * d0[(int64_t)b * n + k0 + k])) bad = true;
-      const zt g = zmul(f, inv);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (j == k) continue;
-        const zt pj = make_double2(__shfl_sync(0xffffffffu, d[j].x, k), __shfl_sync(0xffffffffu, d[j].y, k));
-        const zt pr = zmul(pj, inv);
-        if (lane == k) {
-          d[j] = pr;
-        } else {
-          zt v = d[j];
-          v.x = fma(-f.x, pr.x, v.x);
-          v.x = fma(f.y, pr.y, v.x);
-          v.y = fma(-f.x, pr.y, v.y);
-          v.y = fma(-f.y, pr.x, v.y);
-          d[j] = v;
-        }
-      }
-      d[k] = lane == k ? inv : make_double2(-g.x, -g.y);
-    }
-  }
-  zt* Db = Dt + (int64_t)b * NBB * NBB;
-  zt* Tb = T + (int64_t)b * n * NBB + (int64_t)k0 * NBB;  // T: [n][NBB] per matrix
-  if (lane < bb) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (j < bb) {
-        Db[lane * NBB + j] = d[j];
-        Tb[lane * NBB + j] = make_double2(d[j].x - (lane == j ? 1.0 : 0.0), d[j].y);
-      }
-  }
-  if (lane == 0 && bad) atomicExch(flag, 1);
-}
-
-// Natural-order W^{-1} of a FEW matrices (C2's top levels) in ONE cooperative persistent launch:
-// 32-wide block steps, each = (a) one warp per matrix forms D^{-1} in registers (as
-// nat_block_inv32_kernel), (b) every CTA forms its share of T = -W[rows outside K, K] D^{-1} and of
-// Z = W[K, :], (c) every CTA updates its 32 x 32 tiles W[:, j not in K] += T Z[:, j] (T, Z tiles in
-// shared memory) and writes back W[rows outside K, K] = T, W[K, K] = D^{-1}; a grid barrier after each
-// phase.  The block-step algebra of zgj_invert_natural_blocked with three grid barriers per 32 columns
-// instead of five dependent launches (knob nat_persist).
-constexpr int NP_T = 256;
-__global__ void __launch_bounds__(NP_T) nat_inv_persist_kernel(zt* __restrict__ A, int64_t lda, int64_t bs, int n,
-                                                               int batch, const double* __restrict__ d0, double rel2,
-                                                               zt* __restrict__ Dt, zt* __restrict__ T,
-                                                               zt* __restrict__ Z, int* __restrict__ flag) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ zt sT[32][33];
-  __shared__ zt sZ[32][33];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int gt = blockIdx.x * NP_T + tid, gsz = gridDim.x * NP_T;
-  const int nblk = (n + 31) / 32;
-  for (int q = 0; q < nblk; ++q) {
-    const int k0 = (int)((int64_t)q * n / nblk), bb = (int)((int64_t)(q + 1) * n / nblk) - k0;
-    // (a) D^{-1}: warp w of CTA 0 for matrix w (batch <= 8)
-    if (blockIdx.x == 0 && warp < batch) {
-      const int b = warp;
-      const zt* Ab = A + (int64_t)b * bs + (int64_t)k0 * lda + k0;
-      zt d[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        d[j] = (lane < bb && j < bb) ? Ab[(int64_t)lane * lda + j] : make_double2(lane == j ? 1.0 : 0.0, 0.0);
-      bool bad = false;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        if (k < bb) {
-          const zt f = d[k];
-          const zt pv = make_double2(__shfl_sync(0xffffffffu, f.x, k), __shfl_sync(0xffffffffu, f.y, k));
-          const zt inv = zinv_fast(pv);
-          const double m = fma(pv.x, pv.x, pv.y * pv.y);
-          if (!(m > 0.0 && m >= rel2 * d0[(int64_t)b * n + k0 + k])) bad = true;
-          const zt g = zmul(f, inv);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (j == k) continue;
-            const zt pj = make_double2(__shfl_sync(0xffffffffu, d[j].x, k), __shfl_sync(0xffffffffu, d[j].y, k));
-            const zt pr = zmul(pj, inv);
-            if (lane == k) {
-              d[j] = pr;
-            } else {
-              zt v = d[j];
-              v.x = fma(-f.x, pr.x, v.x);
-              v.x = fma(f.y, pr.y, v.x);
-              v.y = fma(-f.x, pr.y, v.y);
-              v.y = fma(-f.y, pr.x, v.y);
-              d[j] = v;
-            }
-          }
-          d[k] = lane == k ? inv : make_double2(-g.x, -g.y);
-        }
-      }
-      if (lane < bb) {
-        zt* Db = Dt + (int64_t)b * 32 * 32;
-        zt* Tb = T + (int64_t)b * n * 32 + (int64_t)k0 * 32;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < bb) {
-            Db[lane * 32 + j] = d[j];
-            Tb[lane * 32 + j] = make_double2(d[j].x - (lane == j ? 1.0 : 0.0), d[j].y);
-          }
-      }
-      if (lane == 0 && bad) atomicExch(flag, 1);
-    }
-    grid.sync();
-    // (b) T[i, :] = -W[i, K] D^{-1} for rows i outside K; Z = W[K, :]
-    {
-      const int64_t nT = (int64_t)batch * n * bb, nZ = (int64_t)batch * bb * n;
-      for (int64_t e = gt; e < nT + nZ; e += gsz) {
-        if (e < nT) {
-          const int b = (int)(e / ((int64_t)n * bb));
-          const int r = (int)((e / bb) % n), c = (int)(e % bb);
-          if (r >= k0 && r < k0 + bb) continue;
-          const zt* Wr = A + (int64_t)b * bs + (int64_t)r * lda + k0;
-          const zt* Db = Dt + (int64_t)b * 32 * 32;
-          zt acc = make_double2(0.0, 0.0);
-          for (int k = 0; k < bb; ++k) {
-            const zt a = Wr[k], dv = Db[k * 32 + c];
-            acc.x = fma(a.x, dv.x, fma(-a.y, dv.y, acc.x));
-            acc.y = fma(a.x, dv.y, fma(a.y, dv.x, acc.y));
-          }
-          T[(int64_t)b * n * 32 + (int64_t)r * 32 + c] = make_double2(-acc.x, -acc.y);
-        } else {
-          const int64_t f = e - nT;
-          const int b = (int)(f / ((int64_t)bb * n));
-          const int r = (int)((f / n) % bb), j = (int)(f % n);
-          Z[(int64_t)b * 32 * n + (int64_t)r * n + j] = A[(int64_t)b * bs + (int64_t)(k0 + r) * lda + j];
-        }
-      }
-    }
-    grid.sync();
-    // (c) W[:, j not in K] += T Z[:, j] by 32 x 32 tiles; then the panel columns
-    {
-      const int ncol = n - bb, tm = (n + 31) / 32, tn = (ncol + 31) / 32;
-      const int ntile = batch * tm * tn;
-      for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
-        const int b = tile / (tm * tn), t2 = tile - b * tm * tn, i0 = (t2 / tn) * 32, j0 = (t2 % tn) * 32;
-        __syncthreads();  // the previous tile's sT / sZ are consumed
-        for (int e = tid; e < 32 * 32; e += NP_T) {
-          const int r = e >> 5, c = e & 31;
-          sT[r][c] = (i0 + r < n && c < bb) ? T[(int64_t)b * n * 32 + (int64_t)(i0 + r) * 32 + c] : make_double2(0.0, 0.0);
-          const int jj = j0 + c, j = jj < k0 ? jj : jj + bb;  // skip the panel columns
-          sZ[r][c] = (r < bb && jj < ncol) ? Z[(int64_t)b * 32 * n + (int64_t)r * n + j] : make_double2(0.0, 0.0);
-        }
-        __syncthreads();
-        for (int e = tid; e < 32 * 32; e += NP_T) {
-          const int r = e >> 5, c = e & 31, i = i0 + r, jj = j0 + c;
-          if (i >= n || jj >= ncol) continue;
-          const int j = jj < k0 ? jj : jj + bb;
-          zt* wp = A + (int64_t)b * bs + (int64_t)i * lda + j;
-          zt acc = *wp;
-          for (int k = 0; k < bb; ++k) {
-            const zt a = sT[r][k], z = sZ[k][c];
-            acc.x = fma(a.x, z.x, fma(-a.y, z.y, acc.x));
-            acc.y = fma(a.x, z.y, fma(a.y, z.x, acc.y));
-          }
-          *wp = acc;
-        }
-      }
-      // W[i, K] = T[i, :] for rows outside K, W[K, K] = D^{-1}
-      for (int64_t e = gt; e < (int64_t)batch * n * bb; e += gsz) {
-        const int b = (int)(e / ((int64_t)n * bb));
-        const int r = (int)((e / bb) % n), c = (int)(e % bb);
-        const bool inK = r >= k0 && r < k0 + bb;
-        A[(int64_t)b * bs + (int64_t)r * lda + k0 + c] =
-            inK ? Dt[(int64_t)b * 32 * 32 + (r - k0) * 32 + c] : T[(int64_t)b * n * 32 + (int64_t)r * 32 + c];
-      }
-    }
-    grid.sync();
-  }
-}
-
 // Lookahead stream of the block steps (one per host thread and device: the virtual ranks of the
 // multi-GPU tests are host threads sharing a device, and must not share its work queue).
 static cudaStream_t lookahead_stream() {
@@ -3622,8 +3408,7 @@ static cudaStream_t lookahead_stream() {
 // concurrently with the rest of step q's update -- block q + 1's D^{-1} (a handful of CTAs, ~80 us of
 // serial pivot steps) and its T product, so that the serial part of step q + 1 hides behind step q's
 // wide GEMM.  T and D^{-1} are double-buffered; the arithmetic of every entry is unchanged.
-void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st,
-                                int nbw) {
+void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st) {
   char* wsp = static_cast<char*>(ws);
   auto carve = [&](size_t bytes) {
     void* p = wsp;
@@ -3645,7 +3430,7 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
     count_launch();
   }
   const double rel2 = knob(KN_NAT_PIVOT_REL) * 1e-4;
-  const int nblk = (n + nbw - 1) / nbw;  // block width nbw: 64 (512-thread D^{-1}) or 32 (one warp)
+  const int nblk = (n + NBB - 1) / NBB;
   auto k0of = [&](int q) { return (int)((int64_t)q * n / nblk); };
   auto bbof = [&](int q) { return (int)((int64_t)(q + 1) * n / nblk) - k0of(q); };  // equal blocks
   const bool la = knob(KN_NAT_LOOKAHEAD) != 0 && !prof_timing_active() && nblk > 1;
@@ -3662,10 +3447,7 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
     zt* Dt = Dtb[q & 1];
     {
       ProfScope ps(K_GJ_PANEL, 8.0 * (double)bb * bb * bb * batch, 32.0 * (double)bb * bb * batch, s);
-      if (nbw <= 32)
-        nat_block_inv32_kernel<<<batch, 32, 0, s>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
-      else
-        nat_block_inv_kernel<<<batch, 512, 0, s>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
+      nat_block_inv_kernel<<<batch, 512, 0, s>>>(A, lda, bs, n, k0, bb, d0, rel2, Dt, T, flag);
       HPS_CUDA_CHECK(cudaGetLastError());
       count_launch();
     }
@@ -3787,41 +3569,12 @@ void zgj_invert_natural_blocked(zt* A, int64_t lda, int64_t bs, int n, int batch
   }
 }
 
-void zgj_invert_natural_persist(zt* A, int64_t lda, int64_t bs, int n, int batch, void* ws, int* flag, cudaStream_t st) {
-  char* wsp = static_cast<char*>(ws);
-  auto carve = [&](size_t bytes) {
-    void* p = wsp;
-    wsp += (bytes + 255) / 256 * 256;
-    return p;
-  };
-  double* d0 = static_cast<double*>(carve(sizeof(double) * (size_t)batch * n));
-  zt* T = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * n * 32));
-  zt* Z = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * 32 * n));
-  zt* Dt = static_cast<zt*>(carve(sizeof(zt) * (size_t)batch * 32 * 32));
-  {
-    ProfScope ps(K_GJ_AUX, 0.0, 24.0 * (double)batch * n, st);
-    nat_diag_kernel<<<dim3((n + 255) / 256, batch), 256, 0, st>>>(A, lda, bs, n, d0);
-    HPS_CUDA_CHECK(cudaGetLastError());
-    count_launch();
-  }
-  double rel2 = knob(KN_NAT_PIVOT_REL) * 1e-4;
-  int blocks_per_sm = 0;
-  HPS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, nat_inv_persist_kernel, NP_T, 0));
-  int grid = hps_num_sms() * std::max(1, std::min(blocks_per_sm, 2));
-  ProfScope ps(K_GJ_PANEL, 8.0 * (double)n * n * n * batch, 32.0 * (double)n * n * batch, st);
-  void* args[] = {&A, &lda, &bs, &n, &batch, &d0, &rel2, &Dt, &T, &Z, &flag};
-  HPS_CUDA_CHECK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(nat_inv_persist_kernel), dim3(grid), dim3(NP_T),
-                                             args, 0, st));
-  count_launch();
-}
-
 size_t zgj_natural_blocked_workspace_bytes(int n, int batch) {
   return 6 * 256 + sizeof(double) * (size_t)batch * n + sizeof(zt) * (size_t)batch * (3 * (size_t)NBB * n + 2 * NBB * NBB);
 }
 
 size_t zgj_natural_workspace_bytes(int n, int batch) {
-  if (use_block_steps(n, batch) || use_block32(n, batch)) return zgj_natural_blocked_workspace_bytes(n, batch);
-  if (use_persist(n, batch)) return persist_workspace_bytes(n, batch);
+  if (use_block_steps(n, batch)) return zgj_natural_blocked_workspace_bytes(n, batch);
   const size_t mbytes = ((sizeof(zt) * (size_t)batch * n * n + 255) / 256) * 256;
   return mbytes + sizeof(int) * (size_t)batch * n * 4 + 256 + 512 + sizeof(double) * (size_t)batch * n;
 }

@@ -100,13 +100,9 @@ def test_natural_order_merge_inverses_all_levels():
     every box's R and u vs the oracle, complex eta included; second pass with every natural-order
     attempt forced to fail its pivot check (the pivoted fallback), third with the relative pivot
     threshold at 1.0 (any pivot smaller than its original diagonal falls back); the last two with
-    the 64-wide block steps (nat_bb_min = 20: every W with n3 >= 20, one to two blocks); the last two
-    with the 32-wide block steps and their one-warp D^{-1} (nat_b32 = 14), the last two in one
-    cooperative persistent launch (nat_persist = 8)."""
+    the 64-wide block steps (nat_bb_min = 20: every W with n3 >= 20, one to two blocks)."""
     for knobs in ({"nat_min": 14}, {"nat_min": 14, "nat_force_fail": 1}, {"nat_min": 14, "nat_pivot_rel": 10000},
-                  {"nat_min": 14, "nat_bb_min": 20}, {"nat_min": 14, "nat_bb_min": 20, "nat_pivot_rel": 10000},
-                  {"nat_min": 14, "nat_b32": 14}, {"nat_min": 14, "nat_b32": 14, "nat_pivot_rel": 10000},
-                  {"nat_min": 14, "nat_persist": 8}, {"nat_min": 14, "nat_persist": 8, "nat_pivot_rel": 10000}):
+                  {"nat_min": 14, "nat_bb_min": 20}, {"nat_min": 14, "nat_bb_min": 20, "nat_pivot_rel": 10000}):
         worst = 0.0
         with hps.debug_knobs(**knobs):
             for nx, ny, p, kappa, eta in [(4, 4, 8, 9.0, 9.0 - 2j), (8, 4, 6, 9.0, 9.0), (4, 8, 10, 20.0, 20.0)]:
@@ -138,28 +134,6 @@ def test_natural_blocked_lookahead():
     assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
     O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
     assert rel(res[1][0], O.R(1)) < TOL and rel(res[1][1], O.solve(s, t)) < TOL
-
-
-def test_natural_block32_one_warp():
-    """32-wide block steps with the one-warp D^{-1} (knob nat_b32) on the root W
-    (n3 = 160: five blocks), with and without lookahead (bitwise equal), vs the oracle and vs the
-    16-column panels."""
-    nx, ny, p, kappa, eta = 16, 16, 12, 20.0, 20.0 + 2j
-    g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=2)
-    res = {}
-    for key, kn in (("b32", dict(nat_b32=100)), ("b32_nola", dict(nat_b32=100, nat_lookahead=0)),
-                    ("panels", dict(nat_b32=0)), ("persist", dict(nat_persist=8))):
-        with hps.debug_knobs(nat_min=100, **kn):
-            S = hps.Solver(g, p, kappa, eta, c)
-            res[key] = (S.R(1), S.solve(s, t))
-            S.close()
-    assert np.array_equal(res["b32"][0], res["b32_nola"][0]) and np.array_equal(res["b32"][1], res["b32_nola"][1])
-    O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
-    assert rel(res["b32"][0], O.R(1)) < TOL and rel(res["b32"][1], O.solve(s, t)) < TOL
-    assert rel(res["b32"][0], res["panels"][0]) < 1e-12 and rel(res["b32"][1], res["panels"][1]) < 1e-12
-    # the persistent launch: the same block-step algebra with SIMT products (another k-order)
-    assert rel(res["persist"][0], O.R(1)) < TOL and rel(res["persist"][1], O.solve(s, t)) < TOL
-    assert rel(res["persist"][0], res["b32"][0]) < 1e-12
 
 
 def test_leaf_schur_natural_and_pivoted_paths():
@@ -606,7 +580,7 @@ def test_virtual_comm_selftest():
     assert all(dist.run_virtual(8, fn))
 
 
-@pytest.mark.parametrize("m3", [1, 0, 2])
+@pytest.mark.parametrize("m3", [1, 0])
 @pytest.mark.parametrize("cfg", list(range(14)))
 @pytest.mark.parametrize("M,N,K,batch", [(14, 84, 14, 3), (196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 67, 1),
                                          (70, 1, 300, 2), (33, 3, 45, 3)])
@@ -627,7 +601,7 @@ def test_zgemm_configs(cfg, M, N, K, batch, m3):
                 assert rel(C[b], ref) < 1e-13
 
 
-@pytest.mark.parametrize("m3", [1, 0, 2])
+@pytest.mark.parametrize("m3", [1, 0])
 @pytest.mark.parametrize("cfg", [1 | 2 << 8, 2 | 4 << 8, 13 | 8 << 8, 5 | 2 << 8, 6 | 4 << 8])
 @pytest.mark.parametrize("M,N,K,batch", [(196, 168, 28, 2), (70, 9, 33, 1), (130, 200, 671, 1), (33, 16, 1500, 3)])
 def test_zgemm_split_k(cfg, M, N, K, batch, m3):
@@ -659,12 +633,12 @@ def test_zgemm_3m_error_bound(cfg):
     for a, b in [(A, B), (As, B), (As, B.real + 1e-6j * B.imag)]:
         ref = oracle.matmul(a[0], b[0])
         errs = []
-        for m3 in (0, 1, 2):
+        for m3 in (0, 1):
             with hps.debug_knobs(gemm_3m=m3):
                 C, _ = hps.zgemm_batched(a, b, None, 1.0, 0.0, cfg=cfg)
             errs.append(np.linalg.norm(C[0] - ref) / (np.linalg.norm(a[0]) * np.linalg.norm(b[0])))
-        assert max(errs) < 1e-15
-        assert errs[1] < 8 * errs[0] + 1e-17 and errs[2] < 8 * errs[0] + 1e-17, errs
+        assert errs[0] < 1e-15 and errs[1] < 1e-15
+        assert errs[1] < 8 * errs[0] + 1e-17, errs
 
 
 # ---------------------------------------------------------------------------
@@ -689,16 +663,16 @@ def test_config2_full_vs_oracle():
     assert rel(u, O.solve(s, t)) < TOL
 
 
-@pytest.mark.parametrize("m3", [1, 2])
+@pytest.mark.parametrize("m3", [0, 1])
 def test_config2_product_forms(m3):
-    """C2 whole problem in each 3M product form (knob gemm_3m): root R and u vs
-    the oracle at the suite's tolerance, and within 1e-12 of the 4M form."""
+    """C2 whole problem in each complex-product form (knob gemm_3m): root R and u vs
+    the oracle at the suite's tolerance, and the two forms within 1e-12 of each other."""
     cfg, g, c, s, t = _bench_inputs(2)
     with hps.debug_knobs(gemm_3m=m3):
         S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
         u = S.solve(s, t)
         R = S.R(1)
-    with hps.debug_knobs(gemm_3m=0):
+    with hps.debug_knobs(gemm_3m=1 - m3):
         S2 = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
         u2 = S2.solve(s, t)
     O = oracle.Oracle(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p, cfg.kappa, cfg.eta, c)

@@ -12,16 +12,14 @@ from paper_1812_07167_b200 import hps, inputs
 
 cfg = inputs.CONFIGS[int(sys.argv[1])]
 knob = sys.argv[2]
-# a value is an int for KNOB, or "k1=v1,k2=v2" (several knobs at once; KNOB is then a label)
-vals = [v if "=" in v else int(v) for v in sys.argv[3:]]
+vals = [int(v) for v in sys.argv[3:]]
 g, c, s, t = bench.setup(cfg, hps)
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
 cd, sd, td = d(c), d(s), d(t)
 hps.set_cache_limit(int(0.9 * torch.cuda.get_device_properties(0).total_memory))
 hps.plan_problem(g, cfg.p)
 for v in vals * 2:
-    kw = dict((k, int(x)) for k, x in (a.split("=") for a in v.split(","))) if isinstance(v, str) else {knob: v}
-    with hps.debug_knobs(**kw):
+    with hps.debug_knobs(**{knob: v}):
         ts = []
         for _ in range(3):
             S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, cd)
