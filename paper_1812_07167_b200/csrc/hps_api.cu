@@ -48,7 +48,7 @@ const KnobDef g_knob_defs[KN_COUNT] = {
     {"gj", 0},          {"seq_pivot", 0},  {"nat_w", 16},     {"nat_lpr", 4},        {"natc", 1},
     {"natb", 1},        {"nat_pivot_rel", 25}, {"nat_bb_min", 512}, {"leaf_panel", 0}, {"gemm_bcol", 1},
     {"gemm_group", 8}, {"leaf_inplace", 1}, {"seq_force_bad", 0}, {"rhs_chunk", 0},
-    {"dgj_nt", 256}, {"merge_small", 0}, {"gemm_3m", 1}, {"nat_lookahead", 1}};
+    {"dgj_nt", 256}, {"merge_small", 0}, {"gemm_3m", 1}, {"nat_lookahead", 1}, {"solve_graph", 1}};
 std::atomic<int> g_knobs[KN_COUNT];
 std::once_flag g_knob_once;
 void knob_init() {
@@ -164,6 +164,18 @@ namespace {
 // library stream, retained across handles: release threshold = max), so temporaries of one
 // level are freed without synchronising and re-used by the next build without a driver call.
 thread_local cudaStream_t g_alloc_stream = nullptr;
+// CUDA-graph capture of a solve in progress on this thread (hps_solve): every
+// allocation is then stream-ordered (a graph memory node) and counted, so that the capture is only
+// kept if everything it allocated is also freed inside it.
+thread_local bool g_capturing = false;
+thread_local int64_t g_cap_allocs = 0, g_cap_frees = 0;
+struct CapDeferred {
+  void* p;
+  size_t bytes;
+  cudaStream_t st;
+  int dev;
+};
+thread_local std::vector<CapDeferred> g_cap_deferred;
 
 // Blocks of >= 256 MB (the leaf operators, the merge operators of the big levels) are parked in a
 // process-wide cache when a buffer is released and handed to the next request of a similar size:
@@ -285,6 +297,18 @@ struct DevBuf {
   }
   ~DevBuf() { release(); }
   void release() {
+    if (p && g_capturing) {
+      if (big_direct) {  // a cached block allocated outside the capture: handed back after it
+        g_cap_deferred.push_back({p, bytes, st, dev});
+      } else {
+        ++g_cap_frees;
+        cudaFreeAsync(p, st);
+      }
+      p = nullptr;
+      bytes = 0;
+      big_direct = false;
+      return;
+    }
     if (p) {
       if (big_direct && big_cache_max() > 0)
         big_put(p, bytes, st, dev);
@@ -312,7 +336,8 @@ struct DevBuf {
     st = g_alloc_stream;
     cudaGetDevice(&dev);
     const bool dbg = knob(KN_DEBUG_ALLOC) != 0;
-    const bool cache = big_cache_max() > 0;
+    const bool cache = big_cache_max() > 0 && !g_capturing;
+    if (g_capturing) ++g_cap_allocs;
     const auto t0 = std::chrono::steady_clock::now();
     if (n >= kBigBlock && cache) {
       size_t got = 0;
@@ -512,7 +537,21 @@ struct hps_handle {
   cudaStream_t st2 = nullptr;                  // side stream: merge GEMMs independent of W^{-1}
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   Prof prof;
+  // CUDA graph of the last repeated solve: captured on the second consecutive call
+  // with the same (nrhs, s, t, u), replayed from the third on.
+  struct SolveKey {
+    int nrhs = -1;
+    const void *s = nullptr, *t = nullptr, *u = nullptr;
+    bool operator==(const SolveKey& o) const { return nrhs == o.nrhs && s == o.s && t == o.t && u == o.u; }
+  };
+  SolveKey g_last, g_key;
+  bool g_bad = false;  // the last capture failed for this key: stay eager
+  cudaGraphExec_t gexec = nullptr;
+  int64_t g_launches = 0;
+  double g_fl_up = 0, g_fl_down = 0;
+  KStats g_stats;  // per-class statistics of one captured solve (added on every replay)
   ~hps_handle() {
+    if (gexec) cudaGraphExecDestroy(gexec);
     // return every buffer to the pool on our stream, then retire the stream
     ss.reset(0);
     ident.release();
@@ -2110,6 +2149,81 @@ void finish_pending(hps_handle& H) {
   H.pending = false;
 }
 
+// Graph eligibility: the leaf handle's own (non-legacy) stream or a caller stream, no per-launch
+// profiling or tracing, and transient buffers well below the big-block size (their allocations
+// become graph memory nodes; C4-sized solves are device-bound anyway).
+bool solve_graph_eligible(const hps_handle& H, int nrhs) {
+  if (knob(KN_SOLVE_GRAPH) == 0 || knob(KN_TRACE) != 0 || H.prof.timing || H.gl || H.gle) return false;
+  if (!H.st || H.st == cudaStreamLegacy || H.st == cudaStreamPerThread) return false;
+  const double u_bytes = 16.0 * nrhs * (double)H.nleaf * H.nt;
+  return u_bytes * 2 < (double)kBigBlock;
+}
+
+void rec_event(cudaEvent_t e, cudaStream_t st) {
+  if (g_capturing)  // an event-record node of the graph (the phase times stay readable per replay)
+    HPS_CUDA_CHECK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+  else
+    HPS_CUDA_CHECK(cudaEventRecord(e, st));
+}
+
+// Capture one whole solve (upward + downward sweep, both streams) into H.gexec and launch it.
+// Returns false (nothing launched, nothing left captured) if anything in the capture failed.
+bool capture_solve(hps_handle& H, int nrhs, const zt* s, const zt* t, zt* u) {
+  if (H.gexec) {
+    cudaGraphExecDestroy(H.gexec);
+    H.gexec = nullptr;
+  }
+  cudaEvent_t* ce = H.ev + 3;
+  KStats before = H.prof.stats;
+  cudaGraph_t graph = nullptr;
+  bool ok = cudaStreamBeginCapture(H.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    g_capturing = true;
+    g_cap_allocs = g_cap_frees = 0;
+    try {
+      rec_event(ce[0], H.st);
+      solve_up_impl(H, nrhs, s, nullptr);
+      rec_event(ce[1], H.st);
+      solve_down_impl(H, nrhs, t, u);
+      rec_event(ce[2], H.st);
+    } catch (...) {
+      ok = false;
+    }
+    g_capturing = false;
+    const cudaError_t e = cudaStreamEndCapture(H.st, &graph);
+    ok = ok && e == cudaSuccess && graph && g_cap_allocs == g_cap_frees;
+  }
+  for (auto& d : g_cap_deferred) {  // cached blocks released during the capture
+    if (big_cache_max() > 0) {
+      big_put(d.p, d.bytes, d.st, d.dev);
+    } else {
+      cudaStreamSynchronize(d.st);
+      cudaFree(d.p);
+    }
+  }
+  g_cap_deferred.clear();
+  if (ok) ok = cudaGraphInstantiate(&H.gexec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  if (ok) ok = cudaGraphLaunch(H.gexec, H.st) == cudaSuccess;
+  if (!ok) {
+    if (H.gexec) cudaGraphExecDestroy(H.gexec);
+    H.gexec = nullptr;
+    H.ss.reset(H.Lb);
+    H.prof.stats = before;
+    cudaGetLastError();  // errors of the abandoned capture (and of freeing its buffers) are not the caller's
+    return false;
+  }
+  H.g_launches = H.launches[1];
+  H.g_fl_up = H.ss.flops_up;
+  H.g_fl_down = H.ss.flops_down;
+  for (int k = 0; k < K_NCLASS; ++k) {
+    H.g_stats.launches[k] = H.prof.stats.launches[k] - before.launches[k];
+    H.g_stats.flops[k] = H.prof.stats.flops[k] - before.flops[k];
+    H.g_stats.bytes[k] = H.prof.stats.bytes[k] - before.bytes[k];
+  }
+  return true;
+}
+
 void record_solve_times(hps_handle& H, bool up, bool down) {
   HPS_CUDA_CHECK(cudaEventRecord(H.ev[5], H.st));
   H.solve_kind = (up ? 1 : 0) | (down ? 2 : 0);
@@ -2287,6 +2401,44 @@ int hps_solve(hps_handle* h, int nrhs, const hps_c128* s, const hps_c128* t, hps
     const bool one = chunk >= nrhs;
     double up_ms = 0, down_ms = 0, fl_up = 0, fl_down = 0;
     cudaEvent_t* ce = h->ev + 3;  // [3] start, [4] between the sweeps, [5] end
+    // Repeated solves on device buffers (build once, solve many: PAPER.md:86-90) run as ONE CUDA
+    // graph launch from the third identical call on: the solve is ~80 launches of a
+    // few microseconds each at C2, and enqueueing them costs the host about as long as the GPU
+    // takes to run them.
+    if (!T && one && !s_host && !t_host && !u_host && solve_graph_eligible(*h, nrhs)) {
+      const hps_handle::SolveKey key{nrhs, s, t, u};
+      if (h->gexec && h->g_key == key) {
+        HPS_CUDA_CHECK(cudaGraphLaunch(h->gexec, h->st));
+        h->launches[1] = h->g_launches;
+        for (int k = 0; k < K_NCLASS; ++k) {
+          h->prof.stats.launches[k] += h->g_stats.launches[k];
+          h->prof.stats.flops[k] += h->g_stats.flops[k];
+          h->prof.stats.bytes[k] += h->g_stats.bytes[k];
+        }
+        h->ss.flops_up = h->g_fl_up;
+        h->ss.flops_down = h->g_fl_down;
+        h->solve_kind = 3;
+        h->pending = true;
+        if (h->own_stream) finish_pending(*h);
+        return HPS_OK;
+      }
+      if (h->g_last == key && !h->g_bad) {
+        if (capture_solve(*h, nrhs, reinterpret_cast<const zt*>(s), reinterpret_cast<const zt*>(t),
+                          reinterpret_cast<zt*>(u))) {
+          h->g_key = key;
+          h->launches[1] = h->g_launches;
+          h->solve_kind = 3;
+          h->pending = true;
+          if (h->own_stream) finish_pending(*h);
+          return HPS_OK;
+        }
+        h->g_bad = true;  // eager from now on for this key
+        h->launches[1] = 0;
+      } else if (!(h->g_last == key)) {
+        h->g_bad = false;
+      }
+      h->g_last = key;
+    }
     for (int r0 = 0; r0 < nrhs; r0 += chunk) {
       const int nr = std::min(chunk, nrhs - r0);
       DevBuf sd, td, tc, ud;

@@ -58,6 +58,7 @@ enum HpsKnob {
   KN_MERGE_SMALL,      // 1: levels with n3 <= 28 merged by one CTA per merge (merge_small.cu)
   KN_GEMM_3M,          // 1: tiled ZGEMM by three real products per complex MAC (3M form, DESIGN 3.14)
   KN_NAT_LOOKAHEAD,    // 1: block-step W^{-1} with lookahead (next block's D^{-1} beside the update)
+  KN_SOLVE_GRAPH,      // 1: repeated identical solves replay a CUDA graph (hps_solve)
   KN_COUNT
 };
 int knob(HpsKnob k);

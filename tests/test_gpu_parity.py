@@ -136,6 +136,68 @@ def test_natural_blocked_lookahead():
     assert rel(res[1][0], O.R(1)) < TOL and rel(res[1][1], O.solve(s, t)) < TOL
 
 
+@pytest.mark.parametrize("use_stream", [False, True])
+def test_solve_graph_replay(use_stream):
+    """Repeated solves with the same device buffers run as one CUDA graph launch from the third call
+    on (knob solve_graph): new contents of s and t between the calls, a switch to
+    other buffers and back, s = NULL, on the library's own stream and on a caller's torch stream; every
+    result bitwise equal to the eager path (solve_graph = 0) and to the oracle at the suite's
+    tolerance; the launch count of a replayed solve equals the eager one."""
+    import torch
+    nx, ny, p, kappa, eta = 8, 4, 8, 9.0, 9.0 - 1j
+    g, c, s, t = problem(nx, ny, p, kappa, eta, nrhs=3)
+    O = oracle.Oracle(0.0, 1.0, 0.0, 1.0, nx, ny, p, kappa, eta, c)
+    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    st = torch.cuda.Stream() if use_stream else None
+    rng = np.random.default_rng(5)
+    seq = []
+    for k in range(6):
+        sk = s * (1 + 0.5 * k) + rng.standard_normal(s.shape)
+        tk = t * (1 - 0.3 * k) + 1j * rng.standard_normal(t.shape)
+        seq.append((sk, tk))
+    res = {}
+    for graph in (0, 1):
+        with hps.debug_knobs(solve_graph=graph):
+            S = hps.Solver(g, p, kappa, eta, d(c), stream=st)
+            sd, td = d(s), d(t)
+            ud = torch.empty((3, nx * ny, p * p - 4), dtype=torch.complex128, device="cuda")
+            s2, t2, u2 = d(s), d(t), torch.empty_like(ud)
+            out, launches = [], []
+            for k, (sk, tk) in enumerate(seq):
+                if k == 4:  # other buffers once (a new key: eager), then back to the captured key (replay)
+                    s2.copy_(d(sk))
+                    t2.copy_(d(tk))
+                    torch.cuda.synchronize()
+                    S.solve(s2, t2, u2)
+                    S.sync()
+                    torch.cuda.synchronize()
+                    out.append(u2.cpu().numpy())
+                    launches.append(S.launches(1))
+                    continue
+                sd.copy_(d(sk))
+                td.copy_(d(tk))
+                torch.cuda.synchronize()
+                S.solve(sd, td, ud)
+                S.sync()
+                torch.cuda.synchronize()
+                out.append(ud.cpu().numpy())
+                launches.append(S.launches(1))
+            for _ in range(3):  # s = NULL, repeated (its own key)
+                S.solve(None, td, ud)
+                S.sync()
+                torch.cuda.synchronize()
+            out.append(ud.cpu().numpy())
+            launches.append(S.launches(1))
+            S.close()
+        res[graph] = (out, launches)
+    for k, (sk, tk) in enumerate(seq):
+        assert rel(res[1][0][k], O.solve(sk, tk)) < TOL
+    assert rel(res[1][0][-1], O.solve(np.zeros_like(s), seq[-1][1])) < TOL
+    for a, b in zip(res[0][0], res[1][0]):
+        assert np.array_equal(a, b)
+    assert res[0][1] == res[1][1]
+
+
 def test_leaf_schur_natural_and_pivoted_paths():
     """The complex interior Schur inverse (leaf_mode 0 with complex c) runs in natural order
     (DESIGN.md 3.12); the seq_pivot knob forces the pivoted path; leaf_panel switches the natural-order
