@@ -59,6 +59,8 @@ enum HpsKnob {
   KN_GEMM_3M,          // 1: tiled ZGEMM by three real products per complex MAC (3M form, DESIGN 3.14)
   KN_NAT_LOOKAHEAD,    // 1: block-step W^{-1} with lookahead (next block's D^{-1} beside the update)
   KN_SOLVE_GRAPH,      // 1: repeated identical solves replay a CUDA graph (hps_solve)
+  KN_GEMM_SLICES,      // s > 0: big products as s 7-bit integer slices on the INT8 tensor path (zgemm_slices.cu)
+  KN_GEMM_SLICES_MIN,  // smallest M, N and K of a product that takes the integer-slice form
   KN_COUNT
 };
 int knob(HpsKnob k);
@@ -135,6 +137,8 @@ struct ZGemm {
 };
 
 void zgemm(const ZGemm& g, cudaStream_t st);
+// integer-slice form of one product (zgemm_slices.cu); false: not eligible / unavailable, nothing written
+bool zgemm_slices(const ZGemm& g, cudaStream_t st);
 
 // Planned tile configurations of batched products (zgemm.cu, representative-action planner of the
 // solve's matrix products): lookup (-1: none), set (cfg -1 removes), clear, candidates for N,

@@ -765,6 +765,8 @@ void zgemm_impl(const ZGemm& g0, cudaStream_t st) {
   const bool gemv = (force < 0 && g.N <= 4) || force == 9;
   ProfScope ps(gemv ? K_ZGEMV : K_ZGEMM, 8.0 * mn * g.K * bt,
                16.0 * bt * ((double)g.M * g.K + (double)g.K * g.N + mn * (g.Cin.ptr ? 2.0 : 1.0)), st);
+  // opt-in: the big products as integer-slice products on the INT8 tensor path (off by default)
+  if (!gemv && g_zgemm_force == -1 && knob(KN_GEMM_SLICES) > 0 && zgemm_slices(g, st)) return;
   if (force >= 0 && launch_cfg(force, g, st)) return;
   if (g.N <= 4 && force != -2) {
     if (g.N == 1)

@@ -703,6 +703,45 @@ def test_zgemm_3m_error_bound(cfg):
         assert errs[1] < 8 * errs[0] + 1e-17, errs
 
 
+@pytest.mark.parametrize("ns,tol", [(6, 2e-10), (7, 2e-12), (8, 2e-14)])
+@pytest.mark.parametrize("M,N,K,batch", [(130, 200, 671, 1), (96, 80, 3584, 2), (70, 12, 33, 3)])
+def test_zgemm_integer_slices(M, N, K, batch, ns, tol):
+    """Opt-in integer-slice form of the big products (knob gemm_slices = s, zgemm_slices.cu, DESIGN.md
+    11): s 7-bit slices per real operand, slice products exact in int32 on the INT8 tensor path, folded
+    in FP64 -- vs the oracle's triple-loop product with alpha, beta, operands whose rows span six
+    decades; normwise error per slice count as tools/ozaki_probe.py measures it.  Off by default."""
+    rng = np.random.default_rng(M + 3 * N + K)
+    A = rng.standard_normal((batch, M, K)) + 1j * rng.standard_normal((batch, M, K))
+    B = rng.standard_normal((batch, K, N)) + 1j * rng.standard_normal((batch, K, N))
+    B = B * 10.0 ** rng.uniform(-6, 0, (batch, K, 1))
+    Cin = rng.standard_normal((batch, M, N)) + 1j * rng.standard_normal((batch, M, N))
+    with hps.debug_knobs(gemm_slices=ns, gemm_slices_min=12):
+        for alpha, beta in [(1.0, 1.0), (-1.0, 0.5 - 2j), (0.5j, 0.0)]:
+            C, _ = hps.zgemm_batched(A, B, Cin if beta != 0 else None, alpha, beta)
+            for b in range(batch):
+                P = oracle.matmul(A[b], B[b])
+                ref = alpha * P + beta * Cin[b]
+                scale = np.max(np.abs(A[b]), axis=1)[:, None] * np.max(np.abs(B[b]), axis=0)[None, :] * np.sqrt(K)
+                assert np.max(np.abs(C[b] - ref) / scale) < tol
+
+
+def test_config2_integer_slices():
+    """C2 whole problem with every product of n >= 100 in the integer-slice form (s = 8): root R and u
+    vs the oracle at the suite's tolerance and within 1e-11 of the default DMMA path."""
+    cfg, g, c, s, t = _bench_inputs(2)
+    with hps.debug_knobs(gemm_slices=8, gemm_slices_min=100):
+        S = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
+        u = S.solve(s, t)
+        R = S.R(1)
+    S2 = hps.Solver(g, cfg.p, cfg.kappa, cfg.eta, c)
+    u2 = S2.solve(s, t)
+    O = oracle.Oracle(cfg.x0, cfg.x1, cfg.y0, cfg.y1, cfg.nx, cfg.ny, cfg.p, cfg.kappa, cfg.eta, c)
+    assert rel(R, O.R(1)) < TOL
+    assert rel(u, O.solve(s, t)) < TOL
+    assert rel(u, u2) < 1e-11
+    assert rel(R, S2.R(1)) < 1e-11
+
+
 # ---------------------------------------------------------------------------
 # BASELINE configurations at full size, in the bench's launch configuration
 # ---------------------------------------------------------------------------
