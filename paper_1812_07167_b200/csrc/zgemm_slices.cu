@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -84,7 +85,7 @@ Lt* lt() {
   return ok ? &L : nullptr;
 }
 
-// One s8 x s8 -> s32 product shape: D^T (N x M, column-major, ld N) = Y8 (Kp x N, ld Kp)^T X8 (Kp x M, ld Kp)
+// One s8 x s8 -> s32 product shape: D^T (N x M, column-major, ld N) = Y8 (Kk x N, ld)^T X8 (Kk x M, ld)
 struct LtPlan {
   cublasLtMatmulDesc_t op = nullptr;
   cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
@@ -93,13 +94,13 @@ struct LtPlan {
   bool ok = false;
 };
 constexpr size_t kLtWs = 64u << 20;
-std::map<std::tuple<int, int, int, int>, LtPlan> g_plans;
+std::map<std::tuple<int, int, int, int, int>, LtPlan> g_plans;
 
-LtPlan* lt_plan(Lt& L, int M, int N, int Kp) {
+LtPlan* lt_plan(Lt& L, int M, int N, int Kp, int ld) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_lt_mu);
-  auto key = std::make_tuple(dev, M, N, Kp);
+  auto key = std::make_tuple(dev, M, N, Kp, ld);
   auto it = g_plans.find(key);
   if (it != g_plans.end()) return it->second.ok ? &it->second : nullptr;
   LtPlan& P = g_plans[key];
@@ -107,8 +108,8 @@ LtPlan* lt_plan(Lt& L, int M, int N, int Kp) {
   bool ok = L.desc_create(&P.op, CUBLAS_COMPUTE_32I, CUDA_R_32I) == CUBLAS_STATUS_SUCCESS &&
             L.desc_set(P.op, CUBLASLT_MATMUL_DESC_TRANSA, &tr, sizeof(tr)) == CUBLAS_STATUS_SUCCESS &&
             L.desc_set(P.op, CUBLASLT_MATMUL_DESC_TRANSB, &nt, sizeof(nt)) == CUBLAS_STATUS_SUCCESS &&
-            L.lay_create(&P.a, CUDA_R_8I, Kp, N, Kp) == CUBLAS_STATUS_SUCCESS &&
-            L.lay_create(&P.b, CUDA_R_8I, Kp, M, Kp) == CUBLAS_STATUS_SUCCESS &&
+            L.lay_create(&P.a, CUDA_R_8I, Kp, N, ld) == CUBLAS_STATUS_SUCCESS &&
+            L.lay_create(&P.b, CUDA_R_8I, Kp, M, ld) == CUBLAS_STATUS_SUCCESS &&
             L.lay_create(&P.c, CUDA_R_32I, N, M, N) == CUBLAS_STATUS_SUCCESS;
   if (ok) {
     cublasLtMatmulPreference_t pref = nullptr;
@@ -133,7 +134,11 @@ LtPlan* lt_plan(Lt& L, int M, int N, int Kp) {
 
 // ---------------------------------------------------------------------------------------------
 // Slicing: one CTA per kept index r (row i of A, or column j of B); the reduced index is k.
-//   planes [3][s][R][Kp] int8 (k fastest: the "TN" operand layout of the s8 GEMM), exps [3][R].
+//   planes [3][R][s][Kp] int8 (k fastest: the "TN" operand layout of the s8 GEMM), exps [3][R].  Row r
+//   holds its slices side by side -- A: X_0 .. X_{s-1}, B: Y_{s-1} .. Y_0 -- so that the equal-weight
+//   sum  sum_{i+j=w} X_i Y_j^T  is ONE product over the concatenated index: the first (w + 1) Kp entries
+//   of an A row against the last (w + 1) Kp entries of a B row (s products per real product, each
+//   written once, instead of s (s + 1) / 2 accumulated ones).
 // ---------------------------------------------------------------------------------------------
 template <bool IS_B>
 __device__ __forceinline__ zt slice_elem(const ZGemm& g, const zt* base, const int* rm, int r, int k) {
@@ -218,7 +223,8 @@ __global__ void __launch_bounds__(256) zslice_kernel(const ZGemm g, int b, int R
             cp[q] = (signed char)(int)rq;
             y[t][q] = z - rq;  // exact: |z| <= 64, the remainder keeps every remaining bit
           }
-          *reinterpret_cast<char4*>(planes + (((int64_t)t * s + i) * R + r) * Kp + k4) = c;
+          const int slot = IS_B ? s - 1 - i : i;
+          *reinterpret_cast<char4*>(planes + (((int64_t)t * R + r) * s + slot) * Kp + k4) = c;
         }
       }
     }
@@ -276,15 +282,20 @@ bool zgemm_slices(const ZGemm& g, cudaStream_t st) {
   if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return false;
   Lt* L = lt();
   if (!L) return false;
-  LtPlan* P = lt_plan(*L, g.M, g.N, Kp);
-  if (!P) return false;
+  LtPlan* P[9];
+  size_t lws = 1;
+  for (int w = 0; w < s; ++w) {
+    P[w] = lt_plan(*L, g.M, g.N, (w + 1) * Kp, s * Kp);
+    if (!P[w]) return false;
+    lws = std::max(lws, P[w]->ws);
+  }
 
   const size_t a8 = (size_t)3 * s * g.M * Kp, b8 = (size_t)3 * s * g.N * Kp;
   const size_t accb = sizeof(int) * (size_t)3 * s * g.M * g.N;
   const size_t eb = sizeof(int) * (size_t)3 * (g.M + g.N);
   auto up = [](size_t v) { return (v + 255) / 256 * 256; };
   char* ws = nullptr;
-  const size_t total = up(a8) + up(b8) + up(accb) + up(eb) + up(P->ws ? P->ws : 1);
+  const size_t total = up(a8) + up(b8) + up(accb) + up(eb) + up(lws);
   if (cudaMallocAsync(reinterpret_cast<void**>(&ws), total, st) != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -303,15 +314,13 @@ bool zgemm_slices(const ZGemm& g, cudaStream_t st) {
     zslice_kernel<false><<<g.M, 256, 0, st>>>(g, b, g.M, Kp, s, A8, eA);
     zslice_kernel<true><<<g.N, 256, 0, st>>>(g, b, g.N, Kp, s, B8, eB);
     for (int t = 0; t < 3 && ok; ++t)
-      for (int w = 0; w < s && ok; ++w)
-        for (int i = 0; i <= w && ok; ++i) {
-          const int j = w - i;
-          const int8_t* X = A8 + ((size_t)t * s + i) * g.M * Kp;  // [M][Kp]
-          const int8_t* Y = B8 + ((size_t)t * s + j) * g.N * Kp;  // [N][Kp]
-          int* D = acc + ((size_t)t * s + w) * g.M * g.N;         // [M][N] = column-major N x M
-          ok = L->matmul(L->h, P->op, &one, Y, P->a, X, P->b, i == 0 ? &zero : &one, D, P->c, D, P->c, &P->algo, ltws,
-                         P->ws, st) == CUBLAS_STATUS_SUCCESS;
-        }
+      for (int w = 0; w < s && ok; ++w) {
+        const int8_t* X = A8 + (size_t)t * g.M * s * Kp;                           // rows [X_0 .. X_w | ...]
+        const int8_t* Y = B8 + (size_t)t * g.N * s * Kp + (size_t)(s - 1 - w) * Kp;  // rows [... | Y_w .. Y_0]
+        int* D = acc + ((size_t)t * s + w) * g.M * g.N;                            // [M][N] = column-major N x M
+        ok = L->matmul(L->h, P[w]->op, &one, Y, P[w]->a, X, P[w]->b, &zero, D, P[w]->c, D, P[w]->c, &P[w]->algo, ltws,
+                       P[w]->ws, st) == CUBLAS_STATUS_SUCCESS;
+      }
     if (ok) {
       zfold_kernel<<<fold_grid, 256, 0, st>>>(g, b, s, acc, eA, eB);
       ++folded;

@@ -2,7 +2,7 @@
 # integer-slice products (knob gemm_slices, zgemm_slices.cu): parity tests, product timings, C3/C4 sweeps,
 # polynomial errors with the knob on
 cd "$(dirname "$0")/.."
-O=gpurun_out/ax
+O=gpurun_out/${OUT:-ax}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/build.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "integer_slices" > $O/pytest_slices.txt 2>&1
