@@ -206,6 +206,11 @@ def run_hps(args, rank, world, dist):
     cfg = inputs.CONFIGS[args.config]
     nrhs = args.nrhs or cfg.nrhs
     root_R = args.keep_root_R
+    if args.gemm_slices > 0:   # process-wide knobs, set once and kept (not the default path)
+        kn = {"gemm_slices": args.gemm_slices}
+        if args.gemm_slices_min > 0:
+            kn["gemm_slices_min"] = args.gemm_slices_min
+        hps.debug_knobs(**kn).__enter__()
     g, c, s, t = setup(cfg, hps)
     s, t = s[:nrhs], t[:nrhs]
     comm, g_plan, nleaf = None, g, cfg.nleaf
@@ -430,6 +435,11 @@ def run_hps(args, rank, world, dist):
     out["fp64_tensor_peak_tflops"] = {"live": round(_LIVE_PEAK, 3) if _LIVE_PEAK else None,
                                       "builder": load_json(os.path.join(ROOT, "bench", "peaks_fp64.json"), {}).get(
                                           "dmma_m8n8k4_tflops")}
+    if args.gemm_slices > 0:
+        out["gemm_slices"] = {"s": args.gemm_slices, "min": hps.debug_get("gemm_slices_min"),
+                              "note": "opt-in: products with M, N, K >= min run as integer-slice products on the INT8 "
+                                      "tensor path (cuBLASLt s8 GEMM between this repo's slicing and folding kernels); "
+                                      "the roofline object's DMMA peak does not bound them"}
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, c, s, t, args)
     return out
@@ -549,6 +559,10 @@ def main():
     ap.add_argument("--impl", default="hps", choices=["hps", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-plan", action="store_true", help="skip the representative-action planner (default rules)")
+    ap.add_argument("--gemm-slices", type=int, default=0,
+                    help="opt-in: big merge products as S 7-bit integer slices on the INT8 tensor path "
+                         "(library knob gemm_slices, DESIGN.md 3.17; 0 = off, the default and the headline)")
+    ap.add_argument("--gemm-slices-min", type=int, default=0, help="smallest M, N, K of a sliced product (0: library default)")
     ap.add_argument("--keep-root-R", type=int, default=None, choices=[0, 1],
                     help="form the root operator R^1 (default: configs 1-3 yes, 4-5 no; SURVEY hard part 8)")
     args = ap.parse_args()
