@@ -49,7 +49,7 @@ const KnobDef g_knob_defs[KN_COUNT] = {
     {"natb", 1},        {"nat_pivot_rel", 25}, {"nat_bb_min", 512}, {"leaf_panel", 0}, {"gemm_bcol", 1},
     {"gemm_group", 8}, {"leaf_inplace", 1}, {"seq_force_bad", 0}, {"rhs_chunk", 0},
     {"dgj_nt", 256}, {"merge_small", 0}, {"gemm_3m", 1}, {"nat_lookahead", 1}, {"solve_graph", 1},
-    {"gemm_slices", 0}, {"gemm_slices_min", 896}};
+    {"gemm_slices", 0}, {"gemm_slices_min", 1100}};
 std::atomic<int> g_knobs[KN_COUNT];
 std::once_flag g_knob_once;
 void knob_init() {
