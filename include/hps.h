@@ -380,7 +380,7 @@ int hps_release_cache(void);
 /* Debug and tuning knobs (process-wide; the library reads no environment variables).  `name` is
  * one of: debug_alloc, big_cache, side, side_solve, nat_min, nat_max, nat_force_fail, dgj_pivot,
  * dgj_force_bad, dgj_rpt, lr_trace, gemv_short, gemv_k16, trace, gemm_smallk, gj, seq_pivot,
- * nat_w, nat_lpr, natc, natb, nat_pivot_rel, nat_bb_min, leaf_panel, gemm_bcol, gemm_group, leaf_inplace, seq_force_bad, rhs_chunk, dgj_nt, merge_small, gemm_3m, nat_lookahead, solve_graph (meanings in csrc/hps_internal.cuh).  The *_force_*
+ * nat_w, nat_lpr, natc, natb, nat_pivot_rel, nat_bb_min, leaf_panel, gemm_bcol, gemm_group, leaf_inplace, seq_force_bad, rhs_chunk, dgj_nt, merge_small, gemm_3m, nat_lookahead, solve_graph, gemm_slices, gemm_slices_min (meanings in csrc/hps_internal.cuh).  The *_force_*
  * and *_pivot knobs are FAULT INJECTION for the tests of the pivoted fallback paths: never set
  * them in production.  value -1 restores the default.  Returns 0 or HPS_EINVAL (unknown name). */
 int hps_debug_set(const char* name, int value);
